@@ -1,0 +1,29 @@
+# Builds the B200 engine (product) and the CPU oracle (test infrastructure).
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-ffp-contract=off,-Wall -Xptxas -v \
+           --expt-relaxed-constexpr -Iinclude
+PKG := paper_2504_15302_b200
+SRC := $(wildcard $(PKG)/csrc/*.cu)
+HDR := $(wildcard $(PKG)/csrc/*.cuh) include/rd.h
+OBJ := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRC))
+LIB := $(PKG)/lib/librd_b200.so
+
+all: $(LIB) oracle
+
+build/%.o: $(PKG)/csrc/%.cu $(HDR)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
+
+$(LIB): $(OBJ)
+	@mkdir -p $(PKG)/lib
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ)
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf build $(LIB)
+	$(MAKE) -C oracle clean
+
+.PHONY: all oracle clean

@@ -1,0 +1,330 @@
+"""bench.py — RAGDoll retrieval stage on B200: IVF-Flat top-k queries/sec.
+
+Workload (BASELINE.json configs[1], the metric's config): 10M x 768 fp32
+synthetic vectors, nlist 4096, nprobe 64, k 10, query batch 1024, fully
+HBM-resident. One step = one search of one batch of synthetic queries.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c2|c1|c3|c5] [--batch B]
+
+value       : whole-job queries/s with queries already in HBM (device timing,
+              CUDA events on the search stream, max over ranks).
+e2e         : same metric through the public C-ABI rd_search with host
+              buffers: H2D of the queries and D2H of ids+distances every step.
+roofline    : the dominant kernel (N4 list scan): algorithmic bytes of the
+              probed lists' vectors per launch / its CUDA-event duration.
+cpu_baseline: the CPU oracle (oracle/librd_cpu.so — the only CPU IVF path;
+              the reference has none) on a bounded query sample, rank 0, N=1.
+--impl reference: that same CPU path as the timed arm.
+Inputs are larger than L2 (30.7 GB index), so no explicit flush is needed.
+N>1 (torchrun): each rank holds a row stripe of every list of an N x 10M
+knowledge base (weak scaling), searches the same batch, and rank 0 merges
+the NCCL-gathered per-shard top-k on the device.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (n per GPU, d, nlist, nprobe, k, batch, offload_fraction, workload label)
+    "c1": dict(n=1_000_000, d=768, nlist=1024, nprobe=32, k=10, batch=32, offload=0.0,
+               workload="ivf-flat 1M x 768 fp32, nlist 1024, nprobe 32, k 10, batch 32, HBM-resident"),
+    "c2": dict(n=10_000_000, d=768, nlist=4096, nprobe=64, k=10, batch=1024, offload=0.0,
+               workload="ivf-flat 10M x 768 fp32, nlist 4096, nprobe 64, k 10, batch 1024, HBM-resident"),
+    "c3": dict(n=10_000_000, d=768, nlist=4096, nprobe=64, k=10, batch=1024, offload=0.5,
+               workload="ivf-flat 10M x 768 fp32, nlist 4096, nprobe 64, k 10, batch 1024, 50% lists in pinned host DRAM"),
+    "c5": dict(n=10_000_000, d=768, nlist=4096, nprobe=128, k=20, batch=64, offload=None,
+               workload="ivf-flat 10M x 768 fp32, nlist 4096, nprobe 128, k 20, batch 64, under a 70B LLM-decode HBM reservation"),
+}
+METRIC = "IVF top-k queries/sec at 10M×768 nprobe=64 k=10; achieved HBM GB/s vs peak"
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def c5_reservation(lib):
+    """RAGDoll placement for C5: ref_70b model (configs/ref_70b.json:11-19) fully on the GPU
+    in decode at gen batch 64; reservation = w_gpu*W + c_gpu*C(B) + H(B)*0.25
+    (memory_planner.cpp:20, prefetch_timeline.cpp:85-86)."""
+    GiB, MiB = 1 << 30, 1 << 20
+    return lib.llm_reservation_bytes(weight_total=140 * GiB, kv_bytes_per_request=256 * MiB,
+                                     workspace_bytes_per_request=128 * MiB, w_gpu=1.0, c_gpu=1.0,
+                                     gen_batch_size=64, decode_phase=1, workspace_fraction=0.25)
+
+
+def cpu_baseline(cfg, desc_args, sample, steps=1):
+    """Times the CPU oracle on `sample` queries of the same workload (rank 0, N=1)."""
+    from paper_2504_15302_b200.retriever import Library
+    subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "oracle")])
+    oracle = Library(os.path.join(ROOT, "oracle", "librd_cpu.so"))
+    desc = oracle.desc(**desc_args)
+    t0 = time.time()
+    idx = oracle.synthetic_index(desc)
+    build_s = time.time() - t0
+    cores = len(os.sched_getaffinity(0))
+    vals = []
+    for s in range(steps):
+        q, _ = oracle.synth_queries(desc, 10_000_000 + s * sample, sample)
+        t0 = time.perf_counter()
+        idx.search(q, cfg["nprobe"], cfg["k"])
+        vals.append(sample / (time.perf_counter() - t0))
+    idx.close()
+    return {"value": statistics.median(vals), "unit": "queries/s", "cores": cores, "kind": "port",
+            "sample": f"{sample} queries of the same workload per step, exact IVF-Flat, {cores} threads "
+                      f"(index build {build_s:.1f}s untimed)", "per_step": vals}
+
+
+def run_reference(args, cfg):
+    world, rank, _ = dist_env()
+    line = {"metric": METRIC, "impl": "reference", "unit": "queries/s", "higher_is_better": True,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "dtype": "f32 (f64 exact distances)", "data": "synthetic (splitmix64 spec, SURVEY §8d)",
+            "config": {"workload": cfg["workload"], "global_batch": cfg["batch"], "nprobe": cfg["nprobe"],
+                       "k": cfg["k"], "n": cfg["n"], "nlist": cfg["nlist"], "d": cfg["d"]}}
+    if rank != 0:
+        return
+    sample = args.cpu_sample
+    desc_args = dict(n=cfg["n"], d=cfg["d"], nlist=cfg["nlist"])
+    res = cpu_baseline(cfg, desc_args, sample, steps=args.warmup + args.steps)
+    vals = res["per_step"][args.warmup:]
+    v = statistics.median(vals)
+    line.update({"value": v, "ms_per_step": 1000.0 * sample / v, "scaling": "replicas only",
+                 "vs_baseline": None,
+                 "cpu_baseline": {"value": v, "unit": "queries/s", "cores": res["cores"], "kind": "port",
+                                  "sample": res["sample"]},
+                 "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+    from paper_2504_15302_b200.retriever import engine
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    lib = engine()
+    B, k, nprobe, d = cfg["batch"], cfg["k"], cfg["nprobe"], cfg["d"]
+    n_total = cfg["n"] * world
+    desc = lib.desc(n_total, d, cfg["nlist"], shard=rank, num_shards=world)
+    t0 = time.time()
+    idx = lib.synthetic_index(desc, device=local)
+    build_s = time.time() - t0
+    reservation = None
+    if cfg["offload"] is None:  # C5: budget = device memory - LLM reservation - engine workspace
+        free, total = torch.cuda.mem_get_info()
+        reservation = c5_reservation(lib)
+        budget = int(total - reservation - (4 << 30))
+        idx.place(hbm_budget_bytes=budget)
+    elif cfg["offload"] > 0:
+        idx.place(offload_fraction=cfg["offload"])
+    info = idx.info()
+    hold = None
+    if reservation is not None:  # actually hold the LLM's bytes while searching
+        free, _ = torch.cuda.mem_get_info()
+        hold = torch.empty(int(min(reservation, free - (6 << 30))), dtype=torch.uint8, device="cuda")
+
+    nb = args.warmup + args.steps
+    qs = [lib.synth_queries(desc, i * B, B)[0] for i in range(nb)]
+    dq = [torch.from_numpy(q).cuda() for q in qs]
+    di = torch.empty((B, k), dtype=torch.int64, device="cuda")
+    dd = torch.empty((B, k), dtype=torch.float32, device="cuda")
+    gi = [torch.empty((B, k), dtype=torch.int64, device="cuda") for _ in range(world)]
+    gd = [torch.empty((B, k), dtype=torch.float32, device="cuda") for _ in range(world)]
+    mi = torch.empty((B, k), dtype=torch.int64, device="cuda")
+    md = torch.empty((B, k), dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+
+    def step(i):
+        idx.search_device(dq[i].data_ptr(), B, nprobe, k, di.data_ptr(), dd.data_ptr(), stream=sptr)
+        if world > 1:
+            dist.all_gather(gi, di)
+            dist.all_gather(gd, dd)
+            if rank == 0:
+                ti, td = torch.stack(gi), torch.stack(gd)
+                lib.check(lib.lib.rd_merge_topk_device(world, B, k, ti.data_ptr(), td.data_ptr(), mi.data_ptr(),
+                                                       md.data_ptr(), sptr), "merge")
+
+    # correctness / certification on one synced search
+    st = idx.search_device(dq[0].data_ptr(), B, nprobe, k, di.data_ptr(), dd.data_ptr(), stream=sptr, sync=True)
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    idx.timing_reset()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ev0.record(stream)
+        for i in range(args.warmup, nb):
+            step(i)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    tm = idx.timing_read()
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = B * args.steps / (ms / 1000.0)
+
+    # e2e: public C-ABI with host buffers (H2D queries + D2H ids/dists each step)
+    e2e = None
+    if world == 1:
+        for i in range(min(args.warmup, 2)):
+            idx.search(qs[i], nprobe, k)
+        t0 = time.perf_counter()
+        for i in range(args.warmup, nb):
+            idx.search(qs[i], nprobe, k)
+        e2e_s = time.perf_counter() - t0
+        e2e = {"value": B * args.steps / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": B * d * 4,
+               "d2h_bytes_per_step": B * k * 12}
+
+    # roofline of the dominant kernel (N4 resident list scan), measured over the timed region
+    peaks = measured_peaks()
+    peak = peaks["hbm_gbs"] if peaks else 6650.0
+    scan_ms = tm["scan_ms"] / max(1, tm["searches"])
+    scan_bytes = st["bytes_lists_resident"]
+    achieved = scan_bytes / (scan_ms * 1e-3) / 1e9 if scan_ms > 0 else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "scan_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(args.config)
+    launches_per_search = st["kernel_launches"]
+
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (splitmix64 spec, SURVEY §8d), generated on device",
+        "config": {"workload": cfg["workload"], "global_batch": B, "nprobe": nprobe, "k": k, "n_per_gpu": info["n"],
+                   "n_total": n_total, "nlist": cfg["nlist"], "d": d, "parallelism": f"shard{world}",
+                   "l2": "inputs larger than L2 (index %.1f GB)" % (info["n"] * d * 4 / 1e9)},
+        "e2e": e2e,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "ivf_scan_kernel (N4)", "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
+                     "bytes_per_launch": scan_bytes, "avg_launch_ms": scan_ms},
+        "step_breakdown_ms": {k2: tm[k2] / max(1, tm["searches"]) for k2 in ("coarse_ms", "scan_ms", "tail_ms", "total_ms")},
+        "step_gbps_algorithmic": st["bytes_algorithmic"] / (ms_step * 1e-3) / 1e9,
+        "gpu_launches": launches_per_search * args.steps + (args.steps if world > 1 else 0),
+        "clocks": clk.summary(),
+        "certified": {"margin_failures": st["margin_failures"], "probe_failures": st["probe_failures"]},
+        "index": {"build_s": build_s, "lists_resident": info["lists_resident"], "hbm_bytes": info["hbm_bytes"],
+                  "host_pinned_bytes": info["host_pinned_bytes"], "h2d_list_bytes_per_step": st["h2d_list_bytes"],
+                  "llm_reservation_bytes": reservation},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        idx.close()
+        del dq, hold
+        torch.cuda.empty_cache()
+        cb = cpu_baseline(cfg, dict(n=cfg["n"], d=d, nlist=cfg["nlist"]), args.cpu_sample)
+        cb.pop("per_step", None)
+        line["cpu_baseline"] = cb
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--cpu-sample", type=int, default=128)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    cfg = dict(CONFIGS[args.config])
+    if args.batch:
+        cfg["batch"] = args.batch
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

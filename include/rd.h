@@ -1,0 +1,208 @@
+/*
+ * rd.h — C-ABI of the RAGDoll retrieval stage: batched IVF-Flat search over an
+ * inverted-list index that is partly resident in GPU memory (HBM) and partly
+ * offloaded to pinned host DRAM.
+ *
+ * Two libraries implement this header:
+ *   paper_2504_15302_b200/lib/librd_b200.so  — the B200 engine (product; sm_100a CUDA)
+ *   oracle/librd_cpu.so                      — the CPU oracle (test infrastructure only)
+ * so the engine is a literal drop-in for a CPU retrieval stage.
+ *
+ * What this replaces in the reference (/root/reference/proj):
+ *   The reference (ragsim) has no search implementation; its retrieval stage is
+ *   the closed-form cost `retrieval_time(P, db)` (core/src/cost_model.cpp:15-21,
+ *   decl core/include/ragsim/cost_model.hpp:27-29), called by the retrieval
+ *   worker (core/src/simulator.cpp:359, serial mode :560) and the profiler
+ *   (core/src/scheduler.cpp:126). `rd_search` is the real computation whose
+ *   measured wall time replaces that number. The reference's "index" is
+ *   `DatabaseProfile` (core/include/ragsim/domain.hpp:57-68) and its placement
+ *   knob is `PlacementConfig::resident_partitions` (domain.hpp:78): here a
+ *   partition is an inverted list and residency is per list (rd_index_place).
+ *
+ * Conventions follow the reference:
+ *   - status codes are the ragsim CLI exit codes (tools/main.cpp:30, 424-440;
+ *     SPEC.md:540): 0 ok, 2 invalid argument / parse, 3 infeasible placement
+ *     (ragsim::InfeasibleError, core/include/ragsim/errors.hpp:16-19),
+ *     4 runtime (CUDA) failure. No exception crosses the ABI; the message of
+ *     the last failure on the calling thread is in rd_last_error().
+ *   - one in-flight search per handle (the single retrieval worker,
+ *     SPEC.md:432); residency changes only between searches.
+ *   - synthetic data derives from one master seed through ragsim's splitmix64
+ *     Rng / derive_seed (core/include/ragsim/rng.hpp:12-56).
+ *
+ * Output ordering: per query ascending (distance, id); id = -1 and
+ * distance = +inf pad when fewer than k candidates exist. Distances are squared
+ * L2, the canonical exact value (see rd_exact_l2).
+ */
+#ifndef RD_H_
+#define RD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RD_ABI_VERSION 1
+
+/* Status codes (ragsim CLI exit codes, tools/main.cpp:30). */
+#define RD_OK 0
+#define RD_ERR_INVALID 2
+#define RD_ERR_INFEASIBLE 3
+#define RD_ERR_RUNTIME 4
+
+/* Synthetic-data stream ids under the master seed. They avoid
+ * the reference's own streams 1, 2 (tools/main.cpp:101,316) and
+ * 0x100000000|n (core/src/simulator.cpp:204). */
+#define RD_STREAM_CENTROIDS 0x1001u
+#define RD_STREAM_ASSIGN 0x1002u
+#define RD_STREAM_VECTOR_NOISE 0x1003u
+#define RD_STREAM_QUERY_PICK 0x1004u
+#define RD_STREAM_QUERY_NOISE 0x1005u
+#define RD_DEFAULT_SEED 250415302ull
+
+typedef struct rd_index rd_index; /* opaque, library-owned */
+
+/* Counter-based synthetic knowledge base. Vector i belongs to list
+ * a(i) = u(s_a, i) mod nlist and x_i[t] = c_{a(i)}[t] + sigma * f(s_x, i*d + t).
+ * shard/num_shards row-stripe every list: shard g keeps rows
+ * [g*len/G, (g+1)*len/G) of each list. */
+typedef struct {
+  int64_t n;          /* vectors in the whole (unsharded) knowledge base */
+  int32_t d;          /* dimension */
+  int32_t nlist;      /* inverted lists ("partitions") */
+  uint64_t seed;      /* master seed */
+  float sigma;        /* vector noise scale around its centroid (0.25) */
+  int32_t shard;      /* this handle's stripe, 0 <= shard < num_shards */
+  int32_t num_shards; /* 1 = unsharded */
+} rd_synth_desc;
+
+/* Placement between searches (reference analogue: PlacementConfig, domain.hpp:75-82).
+ * Lists not resident live in pinned host memory and are streamed per search. */
+typedef struct {
+  uint64_t hbm_budget_bytes;     /* 0 = no byte budget */
+  double offload_fraction;       /* fraction of lists (by count) to offload; 0 = none */
+  const uint8_t* resident_mask;  /* nullable; nlist bytes, 1 = HBM-resident. Overrides the two above */
+  const uint32_t* list_heat;     /* nullable; nlist probe counts: hottest lists stay resident */
+  int32_t staging_slots;         /* depth of the H2D staging ring; 0 = derive (queue_capacity rule) */
+  int32_t reserved;
+} rd_placement;
+
+typedef struct {
+  double seconds;               /* wall time of the call */
+  uint64_t bytes_algorithmic;   /* unique probed lists' vectors + centroids + queries + results */
+  uint64_t bytes_lists_resident;/* vector bytes of probed resident lists */
+  uint64_t h2d_list_bytes;      /* vector bytes of probed offloaded lists streamed from host */
+  uint64_t lists_probed;        /* unique lists probed by the batch */
+  uint64_t tiles;               /* scan work items */
+  uint64_t kernel_launches;     /* device kernels launched by this call */
+  double scan_ms;               /* device time of the resident list-scan kernel (CUDA events) */
+  double coarse_ms;             /* device time of coarse quantization + probe selection */
+  double offload_ms;            /* device time from first H2D to last offloaded scan */
+  uint32_t margin_failures;     /* queries whose candidate margin could not be certified */
+  uint32_t probe_failures;      /* queries whose probe set could not be certified */
+} rd_search_stats;
+
+typedef struct {
+  int64_t n;            /* vectors held by this handle (its shard) */
+  int32_t d, nlist;
+  int64_t n_resident;   /* vectors resident in HBM */
+  uint64_t hbm_bytes;   /* device bytes held by the index */
+  uint64_t host_pinned_bytes;
+  int32_t lists_resident;
+  int32_t staging_slots;
+  float max_norm;       /* max ||x|| over the index (used by the margin bound) */
+  int32_t device;
+} rd_index_info;
+
+/* LLM-side memory reservation for the retrieval GPU (C5). Mirrors
+ * ragsim::ModelProfile (domain.hpp:37-55) and the PlacementConfig weight/KV
+ * shares. Reservation = w_gpu*W + c_gpu*C(B) + H(B)*workspace_fraction
+ * (core/src/memory_planner.cpp:20, decode workspace core/src/prefetch_timeline.cpp:85-86). */
+typedef struct {
+  uint64_t weight_total;
+  uint64_t kv_bytes_per_request;
+  uint64_t workspace_bytes_per_request;
+  double w_gpu;
+  double c_gpu;
+  int32_t gen_batch_size;
+  int32_t decode_phase;          /* 1: H(B) scaled by workspace_fraction (decode) */
+  double workspace_fraction;     /* cost.decode_workspace_fraction (0.25) */
+} rd_llm_reservation;
+
+/* ---- library ---- */
+const char* rd_last_error(void);
+int rd_abi_version(void);
+const char* rd_backend(void); /* "b200-sm100a" or "cpu-oracle" */
+
+/* ---- index lifecycle (reference: DatabaseProfile, domain.hpp:57-68) ---- */
+int rd_index_create_synthetic(const rd_synth_desc* desc, int32_t device, rd_index** out);
+/* vectors: n x d row-major in list order; list_offsets: nlist+1 prefix offsets;
+ * ids: nullable (default: row index). All host pointers, copied in. */
+int rd_index_create_from_host(int64_t n, int32_t d, int32_t nlist, const float* vectors,
+                              const int64_t* list_offsets, const float* centroids,
+                              const int64_t* ids, int32_t device, rd_index** out);
+int rd_index_place(rd_index* h, const rd_placement* placement);
+int rd_index_info_get(const rd_index* h, rd_index_info* out);
+/* Copies list_offsets (nlist+1) and optionally ids (n) / resident mask (nlist) to host. */
+int rd_index_layout(const rd_index* h, int64_t* list_offsets, int64_t* ids, uint8_t* resident_mask);
+void rd_index_destroy(rd_index* h);
+
+/* ---- search (reference seam: retrieval_time, cost_model.cpp:15-21) ---- */
+/* Host buffers: queries B x d row-major; out_ids / out_dists B x k. */
+int rd_search(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32_t k,
+              int64_t* out_ids, float* out_dists, rd_search_stats* stats);
+/* Device buffers on the index's device, stream = cudaStream_t (NULL = legacy
+ * default). Asynchronous: returns after enqueueing; stats device times are
+ * filled only when sync != 0. CPU oracle: returns RD_ERR_INVALID. */
+int rd_search_device(rd_index* h, const float* d_queries, int64_t B, int32_t nprobe, int32_t k,
+                     int64_t* d_ids, float* d_dists, void* stream, int32_t sync,
+                     rd_search_stats* stats);
+/* Probe sets only (coarse quantization + selection): out_lists B x nprobe,
+ * ascending (exact centroid distance, list id). */
+int rd_probe(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32_t* out_lists);
+
+/* ---- device-time accounting (CUDA events on each search's stream) ---- */
+typedef struct {
+  int64_t searches; /* searches accounted since the last reset */
+  double scan_ms;   /* summed device time of the resident list scan (N4) */
+  double coarse_ms; /* summed device time of qnorm + N1 coarse + N2 select + N3 plan */
+  double tail_ms;   /* summed device time after the resident scan: offload wait, N6/N7 merge */
+  double total_ms;  /* summed device time of whole searches */
+} rd_timing;
+int rd_timing_reset(rd_index* h);
+int rd_timing_read(rd_index* h, rd_timing* out); /* synchronizes the recorded searches */
+
+/* ---- shard merge (multi-GPU) ----
+ * G shard results, each B x k ascending, laid out [G][B][k]; writes the merged
+ * per-query top-k ascending (distance, id). Host-side; used by rank 0. */
+int rd_merge_topk(int32_t G, int64_t B, int32_t k, const int64_t* shard_ids,
+                  const float* shard_dists, int64_t* out_ids, float* out_dists);
+/* Device-side merge of [G][B][k] device buffers. CPU oracle: RD_ERR_INVALID. */
+int rd_merge_topk_device(int32_t G, int64_t B, int32_t k, const int64_t* d_shard_ids,
+                         const float* d_shard_dists, int64_t* d_out_ids, float* d_out_dists,
+                         void* stream);
+
+/* ---- synthetic data and canonical arithmetic (shared spec) ---- */
+uint64_t rd_derive_seed(uint64_t master, uint64_t stream); /* rng.hpp:52-56 */
+uint64_t rd_splitmix_at(uint64_t seed, uint64_t i);       /* (i+1)-th Rng(seed).next_u64(), rng.hpp:16-21 */
+/* Queries b0..b0+B-1: q_b = x_{r(b)} + qsigma * f(s_qn, b*d+t), r(b) = u(s_q, b) mod n
+ * (r over the unsharded knowledge base). src_ids nullable (B). */
+int rd_synth_queries(const rd_synth_desc* desc, int64_t b0, int64_t B, float qsigma,
+                     float* out_queries, int64_t* out_src_ids);
+/* Vector x_id of the synthetic knowledge base (d floats). */
+int rd_synth_vector(const rd_synth_desc* desc, int64_t id, float* out);
+/* Canonical exact squared L2: eight fp64 residue-class sums over t mod 8, no
+ * FMA contraction, combined ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7)), rounded to f32. */
+float rd_exact_l2(const float* a, const float* b, int32_t d);
+
+/* ---- placement arithmetic (reference: memory_planner.cpp:12-35, prefetch_timeline.cpp:79-90) ---- */
+int rd_llm_reservation_bytes(const rd_llm_reservation* r, double* out_bytes);
+/* Staging-ring depth: max(1, floor(free_bytes / item_bytes)) (queue_capacity rule). */
+int32_t rd_staging_depth(double free_bytes, double item_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RD_H_ */

@@ -1,0 +1,594 @@
+/*
+ * rd_oracle.c — CPU ORACLE for the RAGDoll retrieval stage. TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+ * reference legs may load this library, and only as the checker or the timed
+ * CPU baseline. The product path (paper_2504_15302_b200/lib/librd_b200.so)
+ * never links, loads or falls back to it.
+ *
+ * It implements include/rd.h with plain, exact IVF-Flat semantics restated
+ * from first principles, because the reference has no search implementation
+ * (its retrieval stage is retrieval_time(), /root/reference/proj/core/src/cost_model.cpp:15-21;
+ * real vector search is out of the reference's scope).
+ * IVF result parity is therefore UNPINNED by the reference itself; what IS
+ * pinned against the compiled reference (oracle/_ref, tests/golden/) is:
+ *   - the splitmix64 Rng / derive_seed streams every synthetic input derives
+ *     from (/root/reference/proj/core/include/ragsim/rng.hpp:12-56), and
+ *   - the placement arithmetic (memory_planner.cpp:12-35, prefetch_timeline.cpp:79-90).
+ *
+ * Algorithm (exact IVF-Flat, squared L2):
+ *   1. coarse: exact distance from the query to every centroid;
+ *   2. probes: the nprobe smallest by (distance, list id);
+ *   3. scan: exact distance to every vector of the probed lists;
+ *   4. top-k: the k smallest by (distance, id), ascending; pad (-1, +inf).
+ * "Exact distance" is the canonical rd_exact_l2 (see below), identical
+ * bit-for-bit between this file and the CUDA engine's rerank.
+ *
+ * Build: gcc -O3 -march=x86-64-v3 -ffp-contract=off (see oracle/Makefile).
+ */
+#define _GNU_SOURCE
+#include <math.h>
+#include <pthread.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <unistd.h>
+
+#include "../include/rd.h"
+
+/* ------------------------------------------------------------------ errors */
+static __thread char g_err[512];
+
+static int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+const char* rd_last_error(void) { return g_err; }
+int rd_abi_version(void) { return RD_ABI_VERSION; }
+const char* rd_backend(void) { return "cpu-oracle"; }
+
+/* ------------------------------------------------------------------ rng
+ * ragsim::Rng::next_u64 (rng.hpp:16-21): state += golden gamma, two
+ * xorshift-multiply rounds. Counter form: the (i+1)-th output of Rng(seed). */
+static inline uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+uint64_t rd_splitmix_at(uint64_t seed, uint64_t i) {
+  return mix64(seed + (i + 1) * 0x9e3779b97f4a7c15ull);
+}
+
+/* ragsim::derive_seed (rng.hpp:52-56): Rng(master ^ stream*C), discard one, take one. */
+uint64_t rd_derive_seed(uint64_t master, uint64_t stream) {
+  uint64_t s = master ^ (stream * 0xd1b54a32d192ed03ull);
+  return rd_splitmix_at(s, 1);
+}
+
+/* uniform on [-1, 1), 24-bit, exact in fp32. */
+static inline float unif(uint64_t seed, uint64_t i) {
+  uint64_t u = rd_splitmix_at(seed, i);
+  int32_t m = (int32_t)((u >> 40) & 0xFFFFFFu) - (1 << 23);
+  return (float)m * 0x1p-23f;
+}
+
+/* ------------------------------------------------------------------ canonical exact L2 */
+typedef double v4d __attribute__((vector_size(32)));
+typedef float v4f __attribute__((vector_size(16)));
+
+float rd_exact_l2(const float* a, const float* b, int32_t d) {
+  v4d s0 = {0, 0, 0, 0}, s1 = {0, 0, 0, 0};
+  int32_t t = 0;
+  for (; t + 8 <= d; t += 8) {
+    v4f a0, a1, b0, b1;
+    memcpy(&a0, a + t, 16);
+    memcpy(&a1, a + t + 4, 16);
+    memcpy(&b0, b + t, 16);
+    memcpy(&b1, b + t + 4, 16);
+    v4d d0 = __builtin_convertvector(a0, v4d) - __builtin_convertvector(b0, v4d);
+    v4d d1 = __builtin_convertvector(a1, v4d) - __builtin_convertvector(b1, v4d);
+    s0 = s0 + d0 * d0;
+    s1 = s1 + d1 * d1;
+  }
+  double s[8] = {s0[0], s0[1], s0[2], s0[3], s1[0], s1[1], s1[2], s1[3]};
+  for (; t < d; ++t) {
+    double df = (double)a[t] - (double)b[t];
+    s[t & 7] = s[t & 7] + df * df;
+  }
+  double tot = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+  return (float)tot;
+}
+
+/* ------------------------------------------------------------------ threads */
+static int n_threads(void) {
+  const char* e = getenv("RD_CPU_THREADS");
+  if (e && atoi(e) > 0) return atoi(e);
+  long n = sysconf(_SC_NPROCESSORS_ONLN);
+  return n > 0 ? (int)n : 1;
+}
+
+typedef void (*work_fn)(void* ctx, int64_t begin, int64_t end);
+typedef struct {
+  work_fn fn;
+  void* ctx;
+  int64_t n, chunk;
+  int64_t next;
+  pthread_mutex_t mu;
+} pool_job;
+
+static void* pool_worker(void* p) {
+  pool_job* j = (pool_job*)p;
+  for (;;) {
+    pthread_mutex_lock(&j->mu);
+    int64_t b = j->next;
+    j->next += j->chunk;
+    pthread_mutex_unlock(&j->mu);
+    if (b >= j->n) break;
+    int64_t e = b + j->chunk < j->n ? b + j->chunk : j->n;
+    j->fn(j->ctx, b, e);
+  }
+  return NULL;
+}
+
+static void parallel_for(int64_t n, int64_t chunk, work_fn fn, void* ctx) {
+  if (n <= 0) return;
+  int T = n_threads();
+  if (chunk < 1) chunk = 1;
+  pool_job job = {fn, ctx, n, chunk, 0, PTHREAD_MUTEX_INITIALIZER};
+  if (T == 1 || n <= chunk) {
+    fn(ctx, 0, n);
+    return;
+  }
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)T);
+  for (int i = 0; i < T; ++i) pthread_create(&th[i], NULL, pool_worker, &job);
+  for (int i = 0; i < T; ++i) pthread_join(th[i], NULL);
+  free(th);
+}
+
+/* ------------------------------------------------------------------ index */
+struct rd_index {
+  int64_t n;
+  int32_t d, nlist;
+  float* vectors;   /* n x d, list order */
+  int64_t* offsets; /* nlist + 1 */
+  int64_t* ids;     /* n */
+  float* centroids; /* nlist x d */
+  uint8_t* resident;
+  float max_norm;
+};
+
+static int check_desc(const rd_synth_desc* s) {
+  if (!s) return fail(RD_ERR_INVALID, "null synth descriptor");
+  if (s->n < 1 || s->d < 1 || s->nlist < 1)
+    return fail(RD_ERR_INVALID, "synth: n, d, nlist must be >= 1");
+  if (s->num_shards < 1 || s->shard < 0 || s->shard >= s->num_shards)
+    return fail(RD_ERR_INVALID, "synth: shard %d of %d out of range", s->shard, s->num_shards);
+  return RD_OK;
+}
+
+typedef struct {
+  const rd_synth_desc* s;
+  uint64_t sc, sx;
+  const int64_t* ids;
+  const int32_t* lists_of_rows;
+  float* out;
+  const float* centroids;
+} gen_ctx;
+
+static void gen_centroids(void* p, int64_t b, int64_t e) {
+  gen_ctx* g = (gen_ctx*)p;
+  int32_t d = g->s->d;
+  for (int64_t j = b; j < e; ++j)
+    for (int32_t t = 0; t < d; ++t) g->out[j * d + t] = unif(g->sc, (uint64_t)(j * d + t));
+}
+
+static void gen_rows(void* p, int64_t b, int64_t e) {
+  gen_ctx* g = (gen_ctx*)p;
+  int32_t d = g->s->d;
+  float sigma = g->s->sigma;
+  for (int64_t r = b; r < e; ++r) {
+    int64_t id = g->ids[r];
+    const float* c = g->centroids + (int64_t)g->lists_of_rows[r] * d;
+    float* x = g->out + r * d;
+    for (int32_t t = 0; t < d; ++t) {
+      float noise = sigma * unif(g->sx, (uint64_t)(id * d + t));
+      x[t] = c[t] + noise;
+    }
+  }
+}
+
+static void compute_norm_max(rd_index* h) {
+  double mx = 0;
+  for (int64_t r = 0; r < h->n; ++r) {
+    double s = 0;
+    const float* x = h->vectors + r * h->d;
+    for (int32_t t = 0; t < h->d; ++t) s += (double)x[t] * x[t];
+    if (s > mx) mx = s;
+  }
+  h->max_norm = (float)sqrt(mx);
+}
+
+int rd_index_create_synthetic(const rd_synth_desc* s, int32_t device, rd_index** out) {
+  (void)device;
+  int rc = check_desc(s);
+  if (rc) return rc;
+  if (!out) return fail(RD_ERR_INVALID, "null out");
+  const int64_t n = s->n;
+  const int32_t d = s->d, nl = s->nlist, G = s->num_shards, g = s->shard;
+  const uint64_t sa = rd_derive_seed(s->seed, RD_STREAM_ASSIGN);
+  rd_index* h = (rd_index*)calloc(1, sizeof *h);
+  h->d = d;
+  h->nlist = nl;
+  h->centroids = (float*)malloc(sizeof(float) * (size_t)nl * d);
+  gen_ctx gc = {s, rd_derive_seed(s->seed, RD_STREAM_CENTROIDS),
+                rd_derive_seed(s->seed, RD_STREAM_VECTOR_NOISE), NULL, NULL, h->centroids, NULL};
+  parallel_for(nl, 16, gen_centroids, &gc);
+
+  /* list membership: a(i) = u(s_a, i) mod nlist, members ascending by id */
+  int32_t* assign = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
+  int64_t* full_len = (int64_t*)calloc((size_t)nl, sizeof(int64_t));
+  for (int64_t i = 0; i < n; ++i) {
+    assign[i] = (int32_t)(rd_splitmix_at(sa, (uint64_t)i) % (uint64_t)nl);
+    full_len[assign[i]]++;
+  }
+  /* row stripe of this shard: [g*len/G, (g+1)*len/G) */
+  h->offsets = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nl + 1));
+  h->offsets[0] = 0;
+  for (int32_t l = 0; l < nl; ++l) {
+    int64_t lo = g * full_len[l] / G, hi = (int64_t)(g + 1) * full_len[l] / G;
+    h->offsets[l + 1] = h->offsets[l] + (hi - lo);
+  }
+  h->n = h->offsets[nl];
+  h->ids = (int64_t*)malloc(sizeof(int64_t) * (size_t)(h->n > 0 ? h->n : 1));
+  int32_t* row_list = (int32_t*)malloc(sizeof(int32_t) * (size_t)(h->n > 0 ? h->n : 1));
+  int64_t* cursor = (int64_t*)calloc((size_t)nl, sizeof(int64_t));
+  for (int64_t i = 0; i < n; ++i) {
+    int32_t l = assign[i];
+    int64_t pos = cursor[l]++;
+    int64_t lo = g * full_len[l] / G, hi = (int64_t)(g + 1) * full_len[l] / G;
+    if (pos >= lo && pos < hi) {
+      int64_t r = h->offsets[l] + (pos - lo);
+      h->ids[r] = i;
+      row_list[r] = l;
+    }
+  }
+  free(cursor);
+  free(full_len);
+  free(assign);
+  h->vectors = (float*)malloc(sizeof(float) * (size_t)(h->n > 0 ? h->n : 1) * d);
+  if (!h->vectors) {
+    free(row_list);
+    rd_index_destroy(h);
+    return fail(RD_ERR_RUNTIME, "oracle: out of host memory for %lld vectors", (long long)h->n);
+  }
+  gc.ids = h->ids;
+  gc.lists_of_rows = row_list;
+  gc.out = h->vectors;
+  gc.centroids = h->centroids;
+  parallel_for(h->n, 4096, gen_rows, &gc);
+  free(row_list);
+  h->resident = (uint8_t*)malloc((size_t)nl);
+  memset(h->resident, 1, (size_t)nl);
+  compute_norm_max(h);
+  *out = h;
+  return RD_OK;
+}
+
+int rd_index_create_from_host(int64_t n, int32_t d, int32_t nlist, const float* vectors,
+                              const int64_t* list_offsets, const float* centroids,
+                              const int64_t* ids, int32_t device, rd_index** out) {
+  (void)device;
+  if (n < 0 || d < 1 || nlist < 1 || !list_offsets || !centroids || !out || (n > 0 && !vectors))
+    return fail(RD_ERR_INVALID, "create_from_host: invalid arguments");
+  if (list_offsets[0] != 0 || list_offsets[nlist] != n)
+    return fail(RD_ERR_INVALID, "create_from_host: list_offsets must run 0..n");
+  for (int32_t l = 0; l < nlist; ++l)
+    if (list_offsets[l + 1] < list_offsets[l])
+      return fail(RD_ERR_INVALID, "create_from_host: list_offsets not monotone at %d", l);
+  rd_index* h = (rd_index*)calloc(1, sizeof *h);
+  h->n = n;
+  h->d = d;
+  h->nlist = nlist;
+  h->vectors = (float*)malloc(sizeof(float) * (size_t)(n > 0 ? n : 1) * d);
+  if (n) memcpy(h->vectors, vectors, sizeof(float) * (size_t)n * d);
+  h->offsets = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nlist + 1));
+  memcpy(h->offsets, list_offsets, sizeof(int64_t) * (size_t)(nlist + 1));
+  h->centroids = (float*)malloc(sizeof(float) * (size_t)nlist * d);
+  memcpy(h->centroids, centroids, sizeof(float) * (size_t)nlist * d);
+  h->ids = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+  for (int64_t i = 0; i < n; ++i) h->ids[i] = ids ? ids[i] : i;
+  h->resident = (uint8_t*)malloc((size_t)nlist);
+  memset(h->resident, 1, (size_t)nlist);
+  compute_norm_max(h);
+  *out = h;
+  return RD_OK;
+}
+
+void rd_index_destroy(rd_index* h) {
+  if (!h) return;
+  free(h->vectors);
+  free(h->offsets);
+  free(h->ids);
+  free(h->centroids);
+  free(h->resident);
+  free(h);
+}
+
+/* Residency does not change results; the oracle records it so the placement
+ * rule (shared with the engine) can be tested on CPU. */
+static int choose_resident(const rd_index* h, const rd_placement* p, uint8_t* mask) {
+  const int32_t nl = h->nlist;
+  const uint64_t row_bytes = (uint64_t)h->d * sizeof(float);
+  if (p->resident_mask) {
+    uint64_t bytes = 0;
+    for (int32_t l = 0; l < nl; ++l) {
+      mask[l] = p->resident_mask[l] ? 1 : 0;
+      if (mask[l]) bytes += (uint64_t)(h->offsets[l + 1] - h->offsets[l]) * row_bytes;
+    }
+    if (p->hbm_budget_bytes && bytes > p->hbm_budget_bytes)
+      return fail(RD_ERR_INFEASIBLE, "placement infeasible: resident lists need %llu bytes > budget %llu",
+                  (unsigned long long)bytes, (unsigned long long)p->hbm_budget_bytes);
+    return RD_OK;
+  }
+  if (p->offload_fraction < 0 || p->offload_fraction > 1)
+    return fail(RD_ERR_INVALID, "offload_fraction must be in [0, 1]");
+  /* order: heat descending, then list id ascending */
+  int32_t* order = (int32_t*)malloc(sizeof(int32_t) * (size_t)nl);
+  for (int32_t l = 0; l < nl; ++l) order[l] = l;
+  if (p->list_heat) {
+    for (int32_t i = 1; i < nl; ++i) { /* stable insertion sort by heat desc */
+      int32_t v = order[i], j = i - 1;
+      while (j >= 0 && p->list_heat[order[j]] < p->list_heat[v]) {
+        order[j + 1] = order[j];
+        --j;
+      }
+      order[j + 1] = v;
+    }
+  }
+  int64_t target = nl - (int64_t)floor(p->offload_fraction * nl + 0.5);
+  uint64_t bytes = 0;
+  memset(mask, 0, (size_t)nl);
+  for (int64_t i = 0; i < target; ++i) {
+    int32_t l = order[i];
+    uint64_t lb = (uint64_t)(h->offsets[l + 1] - h->offsets[l]) * row_bytes;
+    if (p->hbm_budget_bytes && bytes + lb > p->hbm_budget_bytes) break;
+    bytes += lb;
+    mask[l] = 1;
+  }
+  free(order);
+  return RD_OK;
+}
+
+int rd_index_place(rd_index* h, const rd_placement* p) {
+  if (!h || !p) return fail(RD_ERR_INVALID, "null argument");
+  uint8_t* mask = (uint8_t*)malloc((size_t)h->nlist);
+  int rc = choose_resident(h, p, mask);
+  if (rc == RD_OK) memcpy(h->resident, mask, (size_t)h->nlist);
+  free(mask);
+  return rc;
+}
+
+int rd_index_info_get(const rd_index* h, rd_index_info* o) {
+  if (!h || !o) return fail(RD_ERR_INVALID, "null argument");
+  memset(o, 0, sizeof *o);
+  o->n = h->n;
+  o->d = h->d;
+  o->nlist = h->nlist;
+  for (int32_t l = 0; l < h->nlist; ++l)
+    if (h->resident[l]) {
+      o->lists_resident++;
+      o->n_resident += h->offsets[l + 1] - h->offsets[l];
+    }
+  o->max_norm = h->max_norm;
+  o->device = -1;
+  return RD_OK;
+}
+
+int rd_index_layout(const rd_index* h, int64_t* offs, int64_t* ids, uint8_t* mask) {
+  if (!h) return fail(RD_ERR_INVALID, "null index");
+  if (offs) memcpy(offs, h->offsets, sizeof(int64_t) * (size_t)(h->nlist + 1));
+  if (ids) memcpy(ids, h->ids, sizeof(int64_t) * (size_t)h->n);
+  if (mask) memcpy(mask, h->resident, (size_t)h->nlist);
+  return RD_OK;
+}
+
+/* ------------------------------------------------------------------ search */
+typedef struct {
+  float dist;
+  int64_t id;
+} cand;
+
+static inline int cand_less(float da, int64_t ia, float db, int64_t ib) {
+  return da < db || (da == db && ia < ib);
+}
+
+/* keep the k smallest (dist, id) ascending in top[0..*cnt) */
+static inline void topk_push(cand* top, int32_t* cnt, int32_t k, float dist, int64_t id) {
+  int32_t c = *cnt;
+  if (c == k && !cand_less(dist, id, top[k - 1].dist, top[k - 1].id)) return;
+  int32_t pos = c < k ? c : k - 1;
+  while (pos > 0 && cand_less(dist, id, top[pos - 1].dist, top[pos - 1].id)) {
+    top[pos] = top[pos - 1];
+    --pos;
+  }
+  top[pos].dist = dist;
+  top[pos].id = id;
+  if (c < k) *cnt = c + 1;
+}
+
+typedef struct {
+  const rd_index* h;
+  const float* q;
+  int32_t nprobe, k;
+  int64_t* out_ids;
+  float* out_dists;
+  int32_t* out_lists;
+} search_ctx;
+
+static void probe_one(const rd_index* h, const float* q, int32_t nprobe, int32_t* lists) {
+  cand* top = (cand*)malloc(sizeof(cand) * (size_t)nprobe);
+  int32_t cnt = 0;
+  for (int32_t j = 0; j < h->nlist; ++j)
+    topk_push(top, &cnt, nprobe, rd_exact_l2(q, h->centroids + (int64_t)j * h->d, h->d), j);
+  for (int32_t i = 0; i < nprobe; ++i) lists[i] = i < cnt ? (int32_t)top[i].id : -1;
+  free(top);
+}
+
+static void search_range(void* p, int64_t b, int64_t e) {
+  search_ctx* c = (search_ctx*)p;
+  const rd_index* h = c->h;
+  int32_t np = c->nprobe < h->nlist ? c->nprobe : h->nlist;
+  int32_t* lists = (int32_t*)malloc(sizeof(int32_t) * (size_t)np);
+  cand* top = (cand*)malloc(sizeof(cand) * (size_t)c->k);
+  for (int64_t qi = b; qi < e; ++qi) {
+    const float* q = c->q + qi * h->d;
+    probe_one(h, q, np, lists);
+    if (c->out_lists) {
+      for (int32_t i = 0; i < c->nprobe; ++i) c->out_lists[qi * c->nprobe + i] = i < np ? lists[i] : -1;
+      continue;
+    }
+    int32_t cnt = 0;
+    for (int32_t pi = 0; pi < np; ++pi) {
+      int32_t l = lists[pi];
+      for (int64_t r = h->offsets[l]; r < h->offsets[l + 1]; ++r)
+        topk_push(top, &cnt, c->k, rd_exact_l2(q, h->vectors + r * h->d, h->d), h->ids[r]);
+    }
+    for (int32_t i = 0; i < c->k; ++i) {
+      c->out_ids[qi * c->k + i] = i < cnt ? top[i].id : -1;
+      c->out_dists[qi * c->k + i] = i < cnt ? top[i].dist : INFINITY;
+    }
+  }
+  free(top);
+  free(lists);
+}
+
+int rd_search(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32_t k,
+              int64_t* out_ids, float* out_dists, rd_search_stats* stats) {
+  if (!h || (B > 0 && (!queries || !out_ids || !out_dists)))
+    return fail(RD_ERR_INVALID, "search: null argument");
+  if (B < 0 || nprobe < 1 || k < 1) return fail(RD_ERR_INVALID, "search: B >= 0, nprobe >= 1, k >= 1 required");
+  search_ctx c = {h, queries, nprobe, k, out_ids, out_dists, NULL};
+  parallel_for(B, 1, search_range, &c);
+  if (stats) memset(stats, 0, sizeof *stats);
+  return RD_OK;
+}
+
+int rd_probe(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32_t* out_lists) {
+  if (!h || (B > 0 && (!queries || !out_lists))) return fail(RD_ERR_INVALID, "probe: null argument");
+  if (B < 0 || nprobe < 1) return fail(RD_ERR_INVALID, "probe: nprobe >= 1 required");
+  search_ctx c = {h, queries, nprobe, 1, NULL, NULL, out_lists};
+  parallel_for(B, 1, search_range, &c);
+  return RD_OK;
+}
+
+int rd_search_device(rd_index* h, const float* dq, int64_t B, int32_t nprobe, int32_t k, int64_t* di,
+                     float* dd, void* stream, int32_t sync, rd_search_stats* st) {
+  (void)h; (void)dq; (void)B; (void)nprobe; (void)k; (void)di; (void)dd; (void)stream; (void)sync; (void)st;
+  return fail(RD_ERR_INVALID, "cpu oracle has no device search");
+}
+
+int rd_merge_topk_device(int32_t G, int64_t B, int32_t k, const int64_t* a, const float* b, int64_t* c,
+                         float* d, void* s) {
+  (void)G; (void)B; (void)k; (void)a; (void)b; (void)c; (void)d; (void)s;
+  return fail(RD_ERR_INVALID, "cpu oracle has no device merge");
+}
+
+int rd_timing_reset(rd_index* h) {
+  if (!h) return fail(RD_ERR_INVALID, "null index");
+  return RD_OK;
+}
+
+int rd_timing_read(rd_index* h, rd_timing* out) {
+  if (!h || !out) return fail(RD_ERR_INVALID, "null argument");
+  memset(out, 0, sizeof *out);
+  return RD_OK;
+}
+
+int rd_merge_topk(int32_t G, int64_t B, int32_t k, const int64_t* sid, const float* sd, int64_t* oid,
+                  float* od) {
+  if (G < 1 || B < 0 || k < 1 || (B > 0 && (!sid || !sd || !oid || !od)))
+    return fail(RD_ERR_INVALID, "merge: invalid arguments");
+  cand* top = (cand*)malloc(sizeof(cand) * (size_t)k);
+  for (int64_t q = 0; q < B; ++q) {
+    int32_t cnt = 0;
+    for (int32_t g = 0; g < G; ++g)
+      for (int32_t i = 0; i < k; ++i) {
+        int64_t id = sid[((int64_t)g * B + q) * k + i];
+        if (id < 0) continue;
+        topk_push(top, &cnt, k, sd[((int64_t)g * B + q) * k + i], id);
+      }
+    for (int32_t i = 0; i < k; ++i) {
+      oid[q * k + i] = i < cnt ? top[i].id : -1;
+      od[q * k + i] = i < cnt ? top[i].dist : INFINITY;
+    }
+  }
+  free(top);
+  return RD_OK;
+}
+
+/* ------------------------------------------------------------------ synthetic queries */
+static void synth_vec(const rd_synth_desc* s, uint64_t sc, uint64_t sa, uint64_t sx, int64_t id, float* out) {
+  int32_t a = (int32_t)(rd_splitmix_at(sa, (uint64_t)id) % (uint64_t)s->nlist);
+  for (int32_t t = 0; t < s->d; ++t) {
+    float c = unif(sc, (uint64_t)a * s->d + t);
+    float noise = s->sigma * unif(sx, (uint64_t)(id * s->d + t));
+    out[t] = c + noise;
+  }
+}
+
+int rd_synth_vector(const rd_synth_desc* s, int64_t id, float* out) {
+  int rc = check_desc(s);
+  if (rc) return rc;
+  if (id < 0 || id >= s->n || !out) return fail(RD_ERR_INVALID, "synth_vector: id out of range");
+  synth_vec(s, rd_derive_seed(s->seed, RD_STREAM_CENTROIDS), rd_derive_seed(s->seed, RD_STREAM_ASSIGN),
+            rd_derive_seed(s->seed, RD_STREAM_VECTOR_NOISE), id, out);
+  return RD_OK;
+}
+
+int rd_synth_queries(const rd_synth_desc* s, int64_t b0, int64_t B, float qsigma, float* out, int64_t* src) {
+  int rc = check_desc(s);
+  if (rc) return rc;
+  if (b0 < 0 || B < 0 || (B > 0 && !out)) return fail(RD_ERR_INVALID, "synth_queries: invalid arguments");
+  uint64_t sc = rd_derive_seed(s->seed, RD_STREAM_CENTROIDS), sa = rd_derive_seed(s->seed, RD_STREAM_ASSIGN),
+           sx = rd_derive_seed(s->seed, RD_STREAM_VECTOR_NOISE), sq = rd_derive_seed(s->seed, RD_STREAM_QUERY_PICK),
+           sn = rd_derive_seed(s->seed, RD_STREAM_QUERY_NOISE);
+  for (int64_t i = 0; i < B; ++i) {
+    int64_t b = b0 + i;
+    int64_t r = (int64_t)(rd_splitmix_at(sq, (uint64_t)b) % (uint64_t)s->n);
+    float* q = out + i * s->d;
+    synth_vec(s, sc, sa, sx, r, q);
+    for (int32_t t = 0; t < s->d; ++t) q[t] = q[t] + qsigma * unif(sn, (uint64_t)(b * s->d + t));
+    if (src) src[i] = r;
+  }
+  return RD_OK;
+}
+
+/* ------------------------------------------------------------------ placement arithmetic */
+/* gpu_used of ragsim::check_feasible (memory_planner.cpp:17-20) with the decode
+ * workspace share of queue_capacity (prefetch_timeline.cpp:84-86). */
+int rd_llm_reservation_bytes(const rd_llm_reservation* r, double* out) {
+  if (!r || !out) return fail(RD_ERR_INVALID, "null argument");
+  if (r->gen_batch_size < 0 || r->w_gpu < 0 || r->w_gpu > 1 || r->c_gpu < 0 || r->c_gpu > 1)
+    return fail(RD_ERR_INVALID, "reservation: fractions in [0,1] and batch >= 0 required");
+  double W = (double)r->weight_total;
+  double C = (double)r->kv_bytes_per_request * r->gen_batch_size;
+  double H = (double)r->workspace_bytes_per_request * r->gen_batch_size;
+  if (r->decode_phase) H *= r->workspace_fraction;
+  *out = r->w_gpu * W + r->c_gpu * C + H;
+  return RD_OK;
+}
+
+/* queue_capacity's rule (prefetch_timeline.cpp:87-89): max(1, floor(free / item)). */
+int32_t rd_staging_depth(double free_bytes, double item_bytes) {
+  if (item_bytes <= 0) return 1;
+  double q = floor(free_bytes / item_bytes);
+  if (q < 1) return 1;
+  if (q > 1 << 20) return 1 << 20;
+  return (int32_t)q;
+}

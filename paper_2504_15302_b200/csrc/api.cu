@@ -1,0 +1,1006 @@
+// api.cu — host side of the B200 retrieval engine behind include/rd.h.
+//
+// Owns the index in HBM (list-order arena, norms, ids, centroids), the pinned
+// host arena of offloaded lists, the H2D staging ring, per-search workspaces,
+// streams and events, and orchestrates one search:
+//
+//   qnorm -> N1 coarse GEMM -> N2 select+exact refine -> N3 plan
+//     -> N4 resident scan (persistent, main stream)
+//     || N9 offloaded lists: cudaMemcpyAsync pinned->staging on a copy stream,
+//        event-gated scans of staged slots on a side stream
+//   -> N6/N7 merge + exact rerank -> results
+//
+// Reference seam: retrieval_time(P, db) (cost_model.cpp:15-21), called by the
+// retrieval worker (simulator.cpp:359,560). Error model: ragsim exit codes
+// (tools/main.cpp:30) with the message in rd_last_error().
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <functional>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/rd.h"
+#include "ivf_kernels.cuh"
+#include "rd_device.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct RdError : std::runtime_error {
+  int code;
+  RdError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void throw_rd(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  throw RdError(code, buf);
+}
+
+#define CK(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess)                                                                      \
+      throw_rd(RD_ERR_RUNTIME, "%s failed: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, \
+               __LINE__);                                                                       \
+  } while (0)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return RD_OK;
+  } catch (const RdError& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return RD_ERR_RUNTIME;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return RD_ERR_RUNTIME;
+  }
+}
+
+// ------------------------------------------------------------------ device buffers
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    reset();
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) {
+      p = nullptr;
+      throw_rd(RD_ERR_RUNTIME, "cudaMalloc(%zu bytes) failed: %s", count * sizeof(T), cudaGetErrorString(e));
+    }
+    n = count;
+  }
+  void ensure(size_t count) {
+    if (count > n) alloc(std::max(count, n + n / 2));
+  }
+};
+
+template <class T>
+struct HBuf {  // pinned, mapped host memory
+  T* p = nullptr;
+  size_t n = 0;
+  HBuf() = default;
+  HBuf(const HBuf&) = delete;
+  HBuf& operator=(const HBuf&) = delete;
+  ~HBuf() { reset(); }
+  void reset() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    reset();
+    if (count == 0) count = 1;
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&p), count * sizeof(T),
+                                  cudaHostAllocPortable | cudaHostAllocMapped);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      throw_rd(RD_ERR_RUNTIME, "cudaHostAlloc(%zu bytes) failed: %s", count * sizeof(T), cudaGetErrorString(e));
+    }
+    n = count;
+  }
+  void ensure(size_t count) {
+    if (count > n) alloc(std::max(count, n + n / 2));
+  }
+};
+
+// ------------------------------------------------------------------ tensor maps
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !ptr) throw_rd(RD_ERR_RUNTIME, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+// 2D fp32 map over rows x d, box [32 dims x box_rows], 128B swizzle.
+CUtensorMap make_row_map(const float* base, long long rows, int d, int box_rows) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof m);
+  if (rows < 1) rows = 1;
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)d * sizeof(float)};
+  cuuint32_t box[2] = {(cuuint32_t)rd::kScanKSlice, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw_rd(RD_ERR_RUNTIME, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return m;
+}
+
+// ------------------------------------------------------------------ host arithmetic
+inline uint64_t derive_seed(uint64_t master, uint64_t stream) {
+  return rd::splitmix_at(master ^ (stream * 0xd1b54a32d192ed03ull), 1);
+}
+
+void parallel_for(long long n, const std::function<void(long long, long long)>& fn) {
+  unsigned T = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  if (n < 65536 || T == 1) {
+    fn(0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const long long chunk = (n + T - 1) / T;
+  for (unsigned i = 0; i < T; ++i) {
+    const long long b = i * chunk, e = std::min(n, b + chunk);
+    if (b < e) th.emplace_back(fn, b, e);
+  }
+  for (auto& t : th) t.join();
+}
+
+}  // namespace
+
+// ====================================================================== the index
+struct rd_index {
+  int device = 0;
+  int num_sms = 148;
+  long long n = 0;
+  int d = 0, nlist = 0;
+  std::vector<long long> list_off;  // host copy, nlist + 1
+  long long max_len = 0;
+  float cmax = 0.f, xmax = 0.f;
+
+  DBuf<float> centroids, cnorm, xnorm, arena;
+  DBuf<long long> d_list_off, d_ids, d_res_row0;
+  DBuf<const float*> d_list_base;
+  std::vector<uint8_t> resident;      // host mask
+  std::vector<long long> res_row0;    // host: row in arena or -1
+  std::vector<long long> host_row0;   // host: row in host arena or -1
+  long long n_resident = 0;
+  HBuf<float> host_arena;
+  CUtensorMap map256{}, map32{};
+
+  // staging ring for offloaded lists
+  int slots = 0;
+  long long slot_rows = 0;
+  DBuf<float> staging;
+  CUtensorMap smap256{}, smap32{};
+
+  // per-search workspace
+  struct Ws {
+    DBuf<float> qnorm, Dc, q, dists;
+    DBuf<int> probes, list_nq, list_qoff, list_ntile, list_toff, list_q, part_count, part_row, meta, off_meta;
+    DBuf<unsigned> bitmap, fails;
+    DBuf<rd::ScanTile> tiles, off_tiles;
+    DBuf<unsigned long long> counters;
+    DBuf<float> part_dist;
+    DBuf<long long> ids;
+    HBuf<float> hq, hd;
+    HBuf<long long> hi;
+    HBuf<int> h_nq, h_qoff, h_meta;
+    HBuf<rd::ScanTile> h_tiles;
+    HBuf<unsigned long long> h_counters;
+    HBuf<unsigned> h_fails;
+  } ws;
+
+  cudaStream_t copy_stream = nullptr, off_stream = nullptr;
+  cudaEvent_t ev[8] = {};
+  // device-time accounting: 4 events per search (start, plan done, resident scan done, end)
+  static constexpr int kRing = 64;
+  cudaEvent_t tev[kRing][4] = {};
+  long long t_recorded = 0, t_accounted = 0;
+  rd_timing t_acc{};
+
+  void account(long long i) {  // fold search i's events into t_acc (synchronizes on them)
+    cudaEvent_t* e = tev[i % kRing];
+    CK(cudaEventSynchronize(e[3]));
+    float a = 0, b = 0, c = 0, t = 0;
+    CK(cudaEventElapsedTime(&a, e[0], e[1]));
+    CK(cudaEventElapsedTime(&b, e[1], e[2]));
+    CK(cudaEventElapsedTime(&c, e[2], e[3]));
+    CK(cudaEventElapsedTime(&t, e[0], e[3]));
+    t_acc.searches += 1;
+    t_acc.coarse_ms += a;
+    t_acc.scan_ms += b;
+    t_acc.tail_ms += c;
+    t_acc.total_ms += t;
+  }
+  cudaEvent_t* next_timing_slot() {
+    if (t_recorded - t_accounted >= kRing) account(t_accounted++);
+    return tev[t_recorded++ % kRing];
+  }
+  std::vector<cudaEvent_t> slot_ready, slot_done;
+
+  ~rd_index() {
+    cudaSetDevice(device);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (off_stream) cudaStreamDestroy(off_stream);
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto e : slot_ready) cudaEventDestroy(e);
+    for (auto e : slot_done) cudaEventDestroy(e);
+    for (auto& r : tev)
+      for (auto e : r)
+        if (e) cudaEventDestroy(e);
+  }
+
+  void init_runtime() {
+    CK(cudaSetDevice(device));
+    CK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device));
+    int major = 0;
+    CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    if (major != 10) throw_rd(RD_ERR_RUNTIME, "librd_b200 requires an sm_100 (B200) device, found sm_%d.x", major);
+    CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&off_stream, cudaStreamNonBlocking));
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    for (auto& r : tev)
+      for (auto& e : r) CK(cudaEventCreate(&e));
+  }
+
+  void finish_layout() {
+    max_len = 0;
+    for (int l = 0; l < nlist; ++l) max_len = std::max(max_len, list_off[l + 1] - list_off[l]);
+    d_list_off.alloc(nlist + 1);
+    CK(cudaMemcpy(d_list_off.p, list_off.data(), sizeof(long long) * (nlist + 1), cudaMemcpyHostToDevice));
+    // all lists resident in list order
+    resident.assign(nlist, 1);
+    res_row0.resize(nlist);
+    host_row0.assign(nlist, -1);
+    for (int l = 0; l < nlist; ++l) res_row0[l] = list_off[l];
+    n_resident = n;
+    upload_residency();
+    DBuf<float> tmp;
+    tmp.alloc(1);
+    CK(launch_row_norms_wrap(centroids.p, nlist, cnorm.p));
+    CK(rd::launch_max_f32(cnorm.p, nlist, tmp.p, 0));
+    float m2 = 0;
+    CK(cudaMemcpy(&m2, tmp.p, sizeof(float), cudaMemcpyDeviceToHost));
+    cmax = std::sqrt(m2) * (1.f + 1e-6f);
+    CK(rd::launch_max_f32(xnorm.p, n, tmp.p, 0));
+    CK(cudaMemcpy(&m2, tmp.p, sizeof(float), cudaMemcpyDeviceToHost));
+    xmax = std::sqrt(m2) * (1.f + 1e-6f);
+    CK(cudaDeviceSynchronize());
+  }
+
+  cudaError_t launch_row_norms_wrap(const float* X, long long rows, float* out) {
+    return rd::launch_row_norms(X, rows, d, out, 0);
+  }
+
+  void upload_residency() {
+    d_res_row0.alloc(nlist);
+    CK(cudaMemcpy(d_res_row0.p, res_row0.data(), sizeof(long long) * nlist, cudaMemcpyHostToDevice));
+    std::vector<const float*> base(nlist);
+    for (int l = 0; l < nlist; ++l)
+      base[l] = resident[l] ? arena.p + (size_t)res_row0[l] * d : host_arena.p + (size_t)host_row0[l] * d;
+    d_list_base.alloc(nlist);
+    CK(cudaMemcpy(d_list_base.p, base.data(), sizeof(const float*) * nlist, cudaMemcpyHostToDevice));
+    map256 = make_row_map(arena.p, std::max(1LL, n_resident), d, rd::kScanRows);
+    map32 = make_row_map(arena.p, std::max(1LL, n_resident), d, 32);
+  }
+};
+
+namespace {
+
+void check_dims(int d) {
+  if (d < 32 || d % 32 != 0 || d > 1024)
+    throw_rd(RD_ERR_INVALID, "d must be a multiple of 32 in [32, 1024], got %d", d);
+}
+
+std::unique_ptr<rd_index> new_index(int device) {
+  auto h = std::make_unique<rd_index>();
+  h->device = device;
+  h->init_runtime();
+  return h;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rd_last_error(void) { return g_err.c_str(); }
+int rd_abi_version(void) { return RD_ABI_VERSION; }
+const char* rd_backend(void) { return "b200-sm100a"; }
+
+uint64_t rd_splitmix_at(uint64_t seed, uint64_t i) { return rd::splitmix_at(seed, i); }
+uint64_t rd_derive_seed(uint64_t master, uint64_t stream) { return derive_seed(master, stream); }
+
+float rd_exact_l2(const float* a, const float* b, int32_t d) {
+  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int32_t t = 0; t < d; ++t) {
+    volatile double df = (double)a[t] - (double)b[t];  // volatile: no contraction into an FMA
+    volatile double sq = df * df;
+    s[t & 7] = s[t & 7] + sq;
+  }
+  return (float)(((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7])));
+}
+
+static void validate_desc(const rd_synth_desc* s) {
+  if (!s) throw_rd(RD_ERR_INVALID, "null synth descriptor");
+  if (s->n < 1 || s->d < 1 || s->nlist < 1) throw_rd(RD_ERR_INVALID, "synth: n, d, nlist must be >= 1");
+  if (s->num_shards < 1 || s->shard < 0 || s->shard >= s->num_shards)
+    throw_rd(RD_ERR_INVALID, "synth: shard %d of %d out of range", s->shard, s->num_shards);
+}
+
+static void synth_vec_host(const rd_synth_desc* s, uint64_t sc, uint64_t sa, uint64_t sx, int64_t id, float* out) {
+  const int a = (int)(rd::splitmix_at(sa, (uint64_t)id) % (uint64_t)s->nlist);
+  for (int t = 0; t < s->d; ++t) {
+    volatile float noise = s->sigma * rd::unif(sx, (uint64_t)id * s->d + t);
+    out[t] = rd::unif(sc, (uint64_t)a * s->d + t) + noise;
+  }
+}
+
+int rd_synth_vector(const rd_synth_desc* s, int64_t id, float* out) {
+  return guarded([&] {
+    validate_desc(s);
+    if (id < 0 || id >= s->n || !out) throw_rd(RD_ERR_INVALID, "synth_vector: id out of range");
+    synth_vec_host(s, derive_seed(s->seed, RD_STREAM_CENTROIDS), derive_seed(s->seed, RD_STREAM_ASSIGN),
+                   derive_seed(s->seed, RD_STREAM_VECTOR_NOISE), id, out);
+  });
+}
+
+int rd_synth_queries(const rd_synth_desc* s, int64_t b0, int64_t B, float qsigma, float* out, int64_t* src) {
+  return guarded([&] {
+    validate_desc(s);
+    if (b0 < 0 || B < 0 || (B > 0 && !out)) throw_rd(RD_ERR_INVALID, "synth_queries: invalid arguments");
+    const uint64_t sc = derive_seed(s->seed, RD_STREAM_CENTROIDS), sa = derive_seed(s->seed, RD_STREAM_ASSIGN),
+                   sx = derive_seed(s->seed, RD_STREAM_VECTOR_NOISE),
+                   sq = derive_seed(s->seed, RD_STREAM_QUERY_PICK), sn = derive_seed(s->seed, RD_STREAM_QUERY_NOISE);
+    parallel_for(B * 64, [&](long long lo, long long hi) {
+      for (long long i = (lo + 63) / 64; i < (hi + 63) / 64 && i < B; ++i) {
+        const int64_t b = b0 + i;
+        const int64_t r = (int64_t)(rd::splitmix_at(sq, (uint64_t)b) % (uint64_t)s->n);
+        float* q = out + i * s->d;
+        synth_vec_host(s, sc, sa, sx, r, q);
+        for (int t = 0; t < s->d; ++t) {
+          volatile float noise = qsigma * rd::unif(sn, (uint64_t)b * s->d + t);
+          q[t] = q[t] + noise;
+        }
+        if (src) src[i] = r;
+      }
+    });
+  });
+}
+
+int rd_index_create_synthetic(const rd_synth_desc* s, int32_t device, rd_index** out) {
+  return guarded([&] {
+    validate_desc(s);
+    check_dims(s->d);
+    if (!out) throw_rd(RD_ERR_INVALID, "null out");
+    auto h = new_index(device);
+    h->d = s->d;
+    h->nlist = s->nlist;
+    const long long n = s->n;
+    const int nl = s->nlist, G = s->num_shards, g = s->shard;
+    const uint64_t sa = derive_seed(s->seed, RD_STREAM_ASSIGN);
+    // list membership on the host (counting sort, ids ascending within a list)
+    std::vector<int32_t> assign(n);
+    parallel_for(n, [&](long long lo, long long hi) {
+      for (long long i = lo; i < hi; ++i) assign[i] = (int32_t)(rd::splitmix_at(sa, (uint64_t)i) % (uint64_t)nl);
+    });
+    std::vector<long long> full_len(nl, 0);
+    for (long long i = 0; i < n; ++i) full_len[assign[i]]++;
+    h->list_off.assign(nl + 1, 0);
+    for (int l = 0; l < nl; ++l) {
+      const long long lo = g * full_len[l] / G, hi = (long long)(g + 1) * full_len[l] / G;
+      h->list_off[l + 1] = h->list_off[l] + (hi - lo);
+    }
+    h->n = h->list_off[nl];
+    std::vector<long long> ids(std::max(1LL, h->n));
+    {
+      std::vector<long long> cursor(nl, 0);
+      for (long long i = 0; i < n; ++i) {
+        const int l = assign[i];
+        const long long pos = cursor[l]++;
+        const long long lo = g * full_len[l] / G, hi = (long long)(g + 1) * full_len[l] / G;
+        if (pos >= lo && pos < hi) ids[h->list_off[l] + (pos - lo)] = i;
+      }
+    }
+    std::vector<int32_t>().swap(assign);
+    h->centroids.alloc((size_t)nl * h->d);
+    h->cnorm.alloc(nl);
+    CK(rd::launch_gen_centroids(h->centroids.p, nl, h->d, derive_seed(s->seed, RD_STREAM_CENTROIDS), 0));
+    h->d_ids.alloc(h->n);
+    CK(cudaMemcpy(h->d_ids.p, ids.data(), sizeof(long long) * h->n, cudaMemcpyHostToDevice));
+    h->arena.alloc((size_t)h->n * h->d);
+    CK(rd::launch_gen_vectors(h->arena.p, h->d_ids.p, h->n, h->d, nl, h->centroids.p, sa,
+                              derive_seed(s->seed, RD_STREAM_VECTOR_NOISE), s->sigma, 0));
+    h->xnorm.alloc(h->n);
+    CK(rd::launch_row_norms(h->arena.p, h->n, h->d, h->xnorm.p, 0));
+    h->finish_layout();
+    *out = h.release();
+  });
+}
+
+int rd_index_create_from_host(int64_t n, int32_t d, int32_t nlist, const float* vectors, const int64_t* list_offsets,
+                              const float* centroids, const int64_t* ids, int32_t device, rd_index** out) {
+  return guarded([&] {
+    if (n < 0 || nlist < 1 || !list_offsets || !centroids || !out || (n > 0 && !vectors))
+      throw_rd(RD_ERR_INVALID, "create_from_host: invalid arguments");
+    check_dims(d);
+    if (list_offsets[0] != 0 || list_offsets[nlist] != n)
+      throw_rd(RD_ERR_INVALID, "create_from_host: list_offsets must run 0..n");
+    for (int l = 0; l < nlist; ++l)
+      if (list_offsets[l + 1] < list_offsets[l])
+        throw_rd(RD_ERR_INVALID, "create_from_host: list_offsets not monotone at %d", l);
+    if (n >= (1LL << 31)) throw_rd(RD_ERR_INVALID, "create_from_host: at most 2^31-1 vectors per handle");
+    auto h = new_index(device);
+    h->n = n;
+    h->d = d;
+    h->nlist = nlist;
+    h->list_off.assign(list_offsets, list_offsets + nlist + 1);
+    h->centroids.alloc((size_t)nlist * d);
+    h->cnorm.alloc(nlist);
+    CK(cudaMemcpy(h->centroids.p, centroids, sizeof(float) * (size_t)nlist * d, cudaMemcpyHostToDevice));
+    h->arena.alloc((size_t)n * d);
+    if (n) CK(cudaMemcpy(h->arena.p, vectors, sizeof(float) * (size_t)n * d, cudaMemcpyHostToDevice));
+    h->d_ids.alloc(n);
+    std::vector<long long> idv(std::max<int64_t>(1, n));
+    for (long long i = 0; i < n; ++i) idv[i] = ids ? ids[i] : i;
+    CK(cudaMemcpy(h->d_ids.p, idv.data(), sizeof(long long) * n, cudaMemcpyHostToDevice));
+    h->xnorm.alloc(n);
+    CK(rd::launch_row_norms(h->arena.p, n, d, h->xnorm.p, 0));
+    h->finish_layout();
+    *out = h.release();
+  });
+}
+
+void rd_index_destroy(rd_index* h) { delete h; }
+
+int rd_index_info_get(const rd_index* h, rd_index_info* o) {
+  return guarded([&] {
+    if (!h || !o) throw_rd(RD_ERR_INVALID, "null argument");
+    std::memset(o, 0, sizeof *o);
+    o->n = h->n;
+    o->d = h->d;
+    o->nlist = h->nlist;
+    o->n_resident = h->n_resident;
+    for (int l = 0; l < h->nlist; ++l) o->lists_resident += h->resident[l];
+    o->hbm_bytes = (uint64_t)h->n_resident * h->d * 4 + (uint64_t)h->n * 12 + (uint64_t)h->nlist * (h->d + 1) * 4 +
+                   (uint64_t)h->slots * h->slot_rows * h->d * 4;
+    o->host_pinned_bytes = (uint64_t)h->host_arena.n * 4;
+    o->staging_slots = h->slots;
+    o->max_norm = h->xmax;
+    o->device = h->device;
+  });
+}
+
+int rd_index_layout(const rd_index* h, int64_t* offs, int64_t* ids, uint8_t* mask) {
+  return guarded([&] {
+    if (!h) throw_rd(RD_ERR_INVALID, "null index");
+    CK(cudaSetDevice(h->device));
+    if (offs) std::memcpy(offs, h->list_off.data(), sizeof(int64_t) * (h->nlist + 1));
+    if (ids && h->n) CK(cudaMemcpy(ids, h->d_ids.p, sizeof(int64_t) * h->n, cudaMemcpyDeviceToHost));
+    if (mask) std::memcpy(mask, h->resident.data(), h->nlist);
+  });
+}
+
+// ---------------------------------------------------------------- placement (N8)
+int rd_index_place(rd_index* h, const rd_placement* p) {
+  return guarded([&] {
+    if (!h || !p) throw_rd(RD_ERR_INVALID, "null argument");
+    CK(cudaSetDevice(h->device));
+    const int nl = h->nlist;
+    const uint64_t row_bytes = (uint64_t)h->d * sizeof(float);
+    std::vector<uint8_t> mask(nl, 0);
+    uint64_t res_bytes = 0;
+    if (p->resident_mask) {
+      for (int l = 0; l < nl; ++l) {
+        mask[l] = p->resident_mask[l] ? 1 : 0;
+        if (mask[l]) res_bytes += (uint64_t)(h->list_off[l + 1] - h->list_off[l]) * row_bytes;
+      }
+      if (p->hbm_budget_bytes && res_bytes > p->hbm_budget_bytes)
+        throw_rd(RD_ERR_INFEASIBLE, "placement infeasible: resident lists need %llu bytes > budget %llu",
+                 (unsigned long long)res_bytes, (unsigned long long)p->hbm_budget_bytes);
+    } else {
+      if (p->offload_fraction < 0 || p->offload_fraction > 1)
+        throw_rd(RD_ERR_INVALID, "offload_fraction must be in [0, 1]");
+      std::vector<int> order(nl);
+      for (int l = 0; l < nl; ++l) order[l] = l;
+      if (p->list_heat)
+        std::stable_sort(order.begin(), order.end(),
+                         [&](int a, int b) { return p->list_heat[a] > p->list_heat[b]; });
+      const long long target = nl - (long long)std::floor(p->offload_fraction * nl + 0.5);
+      for (long long i = 0; i < target; ++i) {
+        const int l = order[i];
+        const uint64_t lb = (uint64_t)(h->list_off[l + 1] - h->list_off[l]) * row_bytes;
+        if (p->hbm_budget_bytes && res_bytes + lb > p->hbm_budget_bytes) break;
+        res_bytes += lb;
+        mask[l] = 1;
+      }
+    }
+    // relayout: resident lists compact into a new arena, the rest to pinned host memory
+    long long n_res = 0, n_off = 0, max_off = 0;
+    for (int l = 0; l < nl; ++l) {
+      const long long len = h->list_off[l + 1] - h->list_off[l];
+      if (mask[l])
+        n_res += len;
+      else {
+        n_off += len;
+        max_off = std::max(max_off, len);
+      }
+    }
+    // staging ring: slots of >= the largest offloaded list; depth by the queue_capacity rule
+    long long slot_rows = 0;
+    int slots = 0;
+    if (n_off > 0) {
+      slot_rows = std::max<long long>(max_off, 16384);
+      slot_rows = (slot_rows + 255) / 256 * 256;
+      const double slot_bytes = (double)slot_rows * row_bytes;
+      double free_bytes;
+      if (p->hbm_budget_bytes) {
+        free_bytes = (double)p->hbm_budget_bytes - (double)res_bytes;
+      } else {
+        size_t fr = 0, tot = 0;
+        CK(cudaMemGetInfo(&fr, &tot));
+        free_bytes = (double)fr - (double)(1ull << 30);
+      }
+      slots = p->staging_slots > 0 ? p->staging_slots : std::min(8, rd_staging_depth(free_bytes, slot_bytes));
+      if (p->hbm_budget_bytes && res_bytes + slots * slot_bytes > (double)p->hbm_budget_bytes)
+        throw_rd(RD_ERR_INFEASIBLE, "placement infeasible: no room for one %.0f-byte staging slot in the budget",
+                 slot_bytes);
+    }
+    HBuf<float> new_host;
+    std::vector<long long> new_res(nl, -1), new_host_row(nl, -1);
+    if (n_off) new_host.alloc((size_t)n_off * h->d);
+    DBuf<float> new_arena;
+    new_arena.alloc((size_t)std::max(1LL, n_res) * h->d);
+    long long rr = 0, hr = 0;
+    for (int l = 0; l < nl; ++l) {
+      const long long len = h->list_off[l + 1] - h->list_off[l];
+      const float* src = h->resident[l] ? h->arena.p + (size_t)h->res_row0[l] * h->d
+                                        : h->host_arena.p + (size_t)h->host_row0[l] * h->d;
+      if (mask[l]) {
+        new_res[l] = rr;
+        if (len) CK(cudaMemcpy(new_arena.p + (size_t)rr * h->d, src, len * row_bytes, cudaMemcpyDefault));
+        rr += len;
+      } else {
+        new_host_row[l] = hr;
+        if (len) CK(cudaMemcpy(new_host.p + (size_t)hr * h->d, src, len * row_bytes, cudaMemcpyDefault));
+        hr += len;
+      }
+    }
+    CK(cudaDeviceSynchronize());
+    std::swap(h->arena.p, new_arena.p);
+    std::swap(h->arena.n, new_arena.n);
+    std::swap(h->host_arena.p, new_host.p);
+    std::swap(h->host_arena.n, new_host.n);
+    h->resident = mask;
+    h->res_row0 = new_res;
+    h->host_row0 = new_host_row;
+    h->n_resident = n_res;
+    h->upload_residency();
+    // staging ring
+    for (auto e : h->slot_ready) cudaEventDestroy(e);
+    for (auto e : h->slot_done) cudaEventDestroy(e);
+    h->slot_ready.clear();
+    h->slot_done.clear();
+    h->staging.reset();
+    h->slots = slots;
+    h->slot_rows = slot_rows;
+    if (slots) {
+      h->staging.alloc((size_t)slots * slot_rows * h->d);
+      h->smap256 = make_row_map(h->staging.p, (long long)slots * slot_rows, h->d, rd::kScanRows);
+      h->smap32 = make_row_map(h->staging.p, (long long)slots * slot_rows, h->d, 32);
+      h->slot_ready.resize(slots);
+      h->slot_done.resize(slots);
+      for (int s = 0; s < slots; ++s) {
+        CK(cudaEventCreateWithFlags(&h->slot_ready[s], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h->slot_done[s], cudaEventDisableTiming));
+      }
+    }
+  });
+}
+
+// ---------------------------------------------------------------- search
+namespace {
+
+struct Plan {
+  int R;
+  int max_chunks;
+  int cap;
+  long long max_tiles;
+};
+
+Plan make_plan(const rd_index* h, long long B, int nprobe) {
+  Plan pl;
+  const int np = std::min(nprobe, h->nlist);
+  const double avg = h->nlist ? (double)h->n / h->nlist : 0.0;
+  const double est_rows = std::min((double)h->n, (double)B * np * avg);
+  long long R = (long long)std::ceil(est_rows / (h->num_sms * 8.0));
+  R = std::max<long long>(rd::kScanRows, std::min<long long>(4096, (R + rd::kScanRows - 1) / rd::kScanRows * rd::kScanRows));
+  pl.R = (int)R;
+  pl.max_chunks = (int)std::max<long long>(1, (h->max_len + R - 1) / R);
+  pl.cap = np * pl.max_chunks;
+  pl.max_tiles = std::min<long long>(B * np, B * np / rd::kScanG + h->nlist) * pl.max_chunks + 1;
+  return pl;
+}
+
+void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, long long* d_ids, float* d_dists,
+               cudaStream_t s, bool sync, rd_search_stats* st) {
+  if (nprobe < 1 || k < 1) throw_rd(RD_ERR_INVALID, "search: nprobe >= 1 and k >= 1 required");
+  if (k > rd::kTopK) throw_rd(RD_ERR_INVALID, "search: k <= %d supported, got %d", rd::kTopK, k);
+  if (std::min(nprobe, h->nlist) + rd::kCoarseExtra > 512) throw_rd(RD_ERR_INVALID, "search: nprobe <= 480 supported");
+  if (B >= (1LL << 24)) throw_rd(RD_ERR_INVALID, "search: batch too large (max 2^24-1 per call)");
+  CK(cudaSetDevice(h->device));
+  auto& w = h->ws;
+  const int nl = h->nlist, d = h->d;
+  const Plan pl = make_plan(h, B, nprobe);
+  const int W = (int)((B + 31) / 32);
+  w.qnorm.ensure(B);
+  w.Dc.ensure((size_t)B * nl);
+  w.probes.ensure((size_t)B * nprobe);
+  w.bitmap.ensure((size_t)nl * W);
+  w.list_nq.ensure(nl);
+  w.list_qoff.ensure(nl);
+  w.list_ntile.ensure(nl);
+  w.list_toff.ensure(nl);
+  w.list_q.ensure((size_t)B * nprobe);
+  w.tiles.ensure(pl.max_tiles);
+  w.meta.ensure(2);
+  w.counters.ensure(3);
+  w.fails.ensure(2);
+  w.part_count.ensure(B);
+  w.part_dist.ensure((size_t)B * pl.cap * rd::kTopK);
+  w.part_row.ensure((size_t)B * pl.cap * rd::kTopK);
+  w.h_fails.ensure(2);
+  w.h_counters.ensure(3);
+
+  cudaEvent_t* te = h->next_timing_slot();
+  cudaEvent_t e0 = te[0], e1 = te[1], e2 = te[2], e3 = h->ev[3], e_plan = h->ev[4], e_off = h->ev[5];
+  unsigned long long launches = 0;
+  CK(cudaEventRecord(e0, s));
+  CK(cudaMemsetAsync(w.fails.p, 0, 2 * sizeof(unsigned), s));
+  CK(rd::launch_row_norms(d_q, B, d, w.qnorm.p, s));
+  CK(rd::launch_coarse(d_q, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, s));
+  rd::SelectParams sp{w.Dc.p, d_q, w.qnorm.p, h->centroids.p, w.probes.p, w.fails.p, (int)B, nl, nprobe, d, h->cmax};
+  CK(rd::launch_select(sp, s));
+  launches += 3;
+  rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
+                    w.list_ntile.p, w.list_toff.p, w.list_q.p, w.tiles.p, w.meta.p, w.counters.p,
+                    (int)B, nl, nprobe, pl.R};
+  CK(rd::launch_plan(pp, s));
+  launches += 4;
+  CK(cudaEventRecord(e1, s));
+  CK(cudaMemsetAsync(w.part_count.p, 0, sizeof(int) * B, s));
+  CK(cudaMemsetAsync(w.meta.p + 1, 0, sizeof(int), s));
+  CK(cudaEventRecord(e_plan, s));
+  const bool has_off = h->slots > 0;
+  if (has_off) {  // fetch the probe histogram for host-side staging decisions
+    w.h_nq.ensure(nl);
+    w.h_qoff.ensure(nl);
+    CK(cudaMemcpyAsync(w.h_nq.p, w.list_nq.p, sizeof(int) * nl, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(w.h_qoff.p, w.list_qoff.p, sizeof(int) * nl, cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(e_plan, s));
+  }
+  rd::ScanParams sc{w.tiles.p, w.meta.p, w.meta.p + 1, d_q, w.qnorm.p, w.list_q.p, h->xnorm.p,
+                    w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d};
+  CK(rd::launch_scan(h->map256, h->map32, sc, h->num_sms, s));
+  launches += 1;
+  CK(cudaEventRecord(e2, s));
+
+  unsigned long long h2d = 0;
+  if (has_off) {
+    CK(cudaEventSynchronize(e_plan));
+    // offloaded, probed lists in ascending id, packed into staging slots
+    std::vector<std::vector<int>> batches;
+    long long fill = 0;
+    for (int l = 0; l < nl; ++l) {
+      if (h->resident[l] || w.h_nq.p[l] == 0) continue;
+      const long long len = h->list_off[l + 1] - h->list_off[l];
+      if (len == 0) continue;
+      if (batches.empty() || fill + len > h->slot_rows) {
+        batches.emplace_back();
+        fill = 0;
+      }
+      batches.back().push_back(l);
+      fill += len;
+    }
+    // host-planned tiles for every batch, uploaded once
+    std::vector<rd::ScanTile> tv;
+    std::vector<int> tstart(batches.size() + 1, 0);
+    for (size_t bi = 0; bi < batches.size(); ++bi) {
+      tstart[bi] = (int)tv.size();
+      const int slot = (int)(bi % h->slots);
+      long long srow = (long long)slot * h->slot_rows;
+      for (int l : batches[bi]) {
+        const long long len = h->list_off[l + 1] - h->list_off[l];
+        const int nq = w.h_nq.p[l];
+        const int ngr = (nq + rd::kScanG - 1) / rd::kScanG;
+        for (long long c = 0; c * pl.R < len; ++c)
+          for (int g = 0; g < ngr; ++g) {
+            rd::ScanTile T;
+            T.src_row = srow + c * pl.R;
+            T.grow0 = h->list_off[l] + c * pl.R;
+            T.list = l;
+            T.nrows = (int)std::min<long long>(pl.R, len - c * pl.R);
+            T.qoff = w.h_qoff.p[l] + g * rd::kScanG;
+            T.nq = std::min(rd::kScanG, nq - g * rd::kScanG);
+            tv.push_back(T);
+          }
+        srow += len;
+      }
+    }
+    tstart[batches.size()] = (int)tv.size();
+    const size_t nb = batches.size();
+    if (nb) {
+      w.h_tiles.ensure(tv.size());
+      std::memcpy(w.h_tiles.p, tv.data(), sizeof(rd::ScanTile) * tv.size());
+      w.off_tiles.ensure(tv.size());
+      w.h_meta.ensure(2 * nb);
+      for (size_t bi = 0; bi < nb; ++bi) {
+        w.h_meta.p[2 * bi] = tstart[bi + 1] - tstart[bi];
+        w.h_meta.p[2 * bi + 1] = 0;
+      }
+      DBuf<int>& dmeta = w.off_meta;
+      dmeta.ensure(2 * nb);
+      CK(cudaStreamWaitEvent(h->off_stream, e_plan, 0));
+      CK(cudaMemcpyAsync(w.off_tiles.p, w.h_tiles.p, sizeof(rd::ScanTile) * tv.size(), cudaMemcpyHostToDevice,
+                         h->off_stream));
+      CK(cudaMemcpyAsync(dmeta.p, w.h_meta.p, sizeof(int) * 2 * nb, cudaMemcpyHostToDevice, h->off_stream));
+      CK(cudaEventRecord(e3, h->off_stream));
+      CK(cudaEventRecord(h->ev[6], h->copy_stream));
+      for (size_t bi = 0; bi < nb; ++bi) {
+        const int slot = (int)(bi % h->slots);
+        if (bi >= (size_t)h->slots) CK(cudaStreamWaitEvent(h->copy_stream, h->slot_done[slot], 0));
+        long long srow = (long long)slot * h->slot_rows;
+        for (int l : batches[bi]) {
+          const long long len = h->list_off[l + 1] - h->list_off[l];
+          const size_t bytes = (size_t)len * d * sizeof(float);
+          CK(cudaMemcpyAsync(h->staging.p + (size_t)srow * d, h->host_arena.p + (size_t)h->host_row0[l] * d, bytes,
+                             cudaMemcpyHostToDevice, h->copy_stream));
+          h2d += bytes;
+          srow += len;
+        }
+        CK(cudaEventRecord(h->slot_ready[slot], h->copy_stream));
+        CK(cudaStreamWaitEvent(h->off_stream, h->slot_ready[slot], 0));
+        rd::ScanParams so = sc;
+        so.tiles = w.off_tiles.p + tstart[bi];
+        so.ntiles = dmeta.p + 2 * bi;
+        so.tile_counter = dmeta.p + 2 * bi + 1;
+        const int grid = std::max(1, std::min(h->num_sms, tstart[bi + 1] - tstart[bi]));
+        CK(rd::launch_scan(h->smap256, h->smap32, so, grid, h->off_stream));
+        launches += 1;
+        CK(cudaEventRecord(h->slot_done[slot], h->off_stream));
+      }
+    }
+    CK(cudaEventRecord(e_off, h->off_stream));
+    CK(cudaStreamWaitEvent(s, e_off, 0));
+  }
+
+  rd::MergeParams mp{w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d_q, w.qnorm.p, h->d_list_off.p,
+                     h->d_list_base.p, h->d_ids.p, nl, d, k, h->xmax, d_ids, d_dists, w.fails.p + 1, (int)B};
+  CK(rd::launch_merge(mp, s));
+  launches += 1;
+  CK(cudaEventRecord(te[3], s));
+  if (st) {
+    std::memset(st, 0, sizeof *st);
+    st->kernel_launches = launches;
+  }
+  if (sync) {
+    CK(cudaMemcpyAsync(w.h_counters.p, w.counters.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(w.h_fails.p, w.fails.p, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    int ntiles = 0;
+    CK(cudaMemcpyAsync(&ntiles, w.meta.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (st) {
+      float ms = 0;
+      const unsigned long long row_bytes = (unsigned long long)d * 4;
+      st->lists_probed = w.h_counters.p[0];
+      st->bytes_lists_resident = w.h_counters.p[1] * row_bytes;
+      st->h2d_list_bytes = h2d;
+      st->bytes_algorithmic = (w.h_counters.p[1] + w.h_counters.p[2]) * row_bytes +
+                              (unsigned long long)nl * row_bytes + (unsigned long long)B * row_bytes +
+                              (unsigned long long)B * k * 12ull;
+      st->tiles = (uint64_t)ntiles;
+      CK(cudaEventElapsedTime(&ms, e1, e2));
+      st->scan_ms = ms;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      st->coarse_ms = ms;
+      if (has_off) {
+        CK(cudaEventElapsedTime(&ms, e_plan, e_off));
+        st->offload_ms = ms;
+      }
+      st->probe_failures = w.h_fails.p[0];
+      st->margin_failures = w.h_fails.p[1];
+    }
+  }
+}
+
+}  // namespace
+
+int rd_search_device(rd_index* h, const float* d_q, int64_t B, int32_t nprobe, int32_t k, int64_t* d_ids,
+                     float* d_dists, void* stream, int32_t sync, rd_search_stats* st) {
+  return guarded([&] {
+    if (!h || B < 0 || (B > 0 && (!d_q || !d_ids || !d_dists))) throw_rd(RD_ERR_INVALID, "search: invalid arguments");
+    if (B == 0) {
+      if (st) std::memset(st, 0, sizeof *st);
+      return;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    do_search(h, d_q, B, nprobe, k, reinterpret_cast<long long*>(d_ids), d_dists, (cudaStream_t)stream, sync != 0, st);
+    if (st) st->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+int rd_search(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32_t k, int64_t* out_ids,
+              float* out_dists, rd_search_stats* st) {
+  return guarded([&] {
+    if (!h || B < 0 || (B > 0 && (!queries || !out_ids || !out_dists)))
+      throw_rd(RD_ERR_INVALID, "search: invalid arguments");
+    if (nprobe < 1 || k < 1) throw_rd(RD_ERR_INVALID, "search: nprobe >= 1 and k >= 1 required");
+    const auto t0 = std::chrono::steady_clock::now();
+    if (B == 0) {
+      if (st) std::memset(st, 0, sizeof *st);
+      return;
+    }
+    CK(cudaSetDevice(h->device));
+    auto& w = h->ws;
+    const size_t qn = (size_t)B * h->d, rn = (size_t)B * k;
+    w.hq.ensure(qn);
+    w.hi.ensure(rn);
+    w.hd.ensure(rn);
+    w.q.ensure(qn);
+    w.ids.ensure(rn);
+    w.dists.ensure(rn);
+    std::memcpy(w.hq.p, queries, qn * sizeof(float));
+    cudaStream_t s = 0;
+    CK(cudaMemcpyAsync(w.q.p, w.hq.p, qn * sizeof(float), cudaMemcpyHostToDevice, s));
+    do_search(h, w.q.p, B, nprobe, k, w.ids.p, w.dists.p, s, true, st);
+    CK(cudaMemcpyAsync(w.hi.p, w.ids.p, rn * sizeof(long long), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(w.hd.p, w.dists.p, rn * sizeof(float), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::memcpy(out_ids, w.hi.p, rn * sizeof(long long));
+    std::memcpy(out_dists, w.hd.p, rn * sizeof(float));
+    if (st) st->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+int rd_probe(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32_t* out_lists) {
+  return guarded([&] {
+    if (!h || B < 0 || (B > 0 && (!queries || !out_lists))) throw_rd(RD_ERR_INVALID, "probe: invalid arguments");
+    if (nprobe < 1 || std::min(nprobe, h->nlist) + rd::kCoarseExtra > 512)
+      throw_rd(RD_ERR_INVALID, "probe: 1 <= nprobe <= 480 required");
+    if (B == 0) return;
+    CK(cudaSetDevice(h->device));
+    auto& w = h->ws;
+    const int nl = h->nlist, d = h->d;
+    w.q.ensure((size_t)B * d);
+    w.qnorm.ensure(B);
+    w.Dc.ensure((size_t)B * nl);
+    w.probes.ensure((size_t)B * nprobe);
+    w.fails.ensure(2);
+    CK(cudaMemcpy(w.q.p, queries, sizeof(float) * B * d, cudaMemcpyHostToDevice));
+    CK(cudaMemset(w.fails.p, 0, 2 * sizeof(unsigned)));
+    CK(rd::launch_row_norms(w.q.p, B, d, w.qnorm.p, 0));
+    CK(rd::launch_coarse(w.q.p, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, 0));
+    rd::SelectParams sp{w.Dc.p, w.q.p, w.qnorm.p, h->centroids.p, w.probes.p, w.fails.p, (int)B, nl, nprobe, d, h->cmax};
+    CK(rd::launch_select(sp, 0));
+    CK(cudaMemcpy(out_lists, w.probes.p, sizeof(int) * B * nprobe, cudaMemcpyDeviceToHost));
+  });
+}
+
+int rd_timing_reset(rd_index* h) {
+  return guarded([&] {
+    if (!h) throw_rd(RD_ERR_INVALID, "null index");
+    CK(cudaSetDevice(h->device));
+    while (h->t_accounted < h->t_recorded) {  // drain so the ring's events are free again
+      CK(cudaEventSynchronize(h->tev[h->t_accounted % rd_index::kRing][3]));
+      ++h->t_accounted;
+    }
+    h->t_acc = rd_timing{};
+  });
+}
+
+int rd_timing_read(rd_index* h, rd_timing* out) {
+  return guarded([&] {
+    if (!h || !out) throw_rd(RD_ERR_INVALID, "null argument");
+    CK(cudaSetDevice(h->device));
+    while (h->t_accounted < h->t_recorded) h->account(h->t_accounted++);
+    *out = h->t_acc;
+  });
+}
+
+// ---------------------------------------------------------------- shard merge
+int rd_merge_topk(int32_t G, int64_t B, int32_t k, const int64_t* sid, const float* sd, int64_t* oid, float* od) {
+  return guarded([&] {
+    if (G < 1 || B < 0 || k < 1 || (B > 0 && (!sid || !sd || !oid || !od)))
+      throw_rd(RD_ERR_INVALID, "merge: invalid arguments");
+    std::vector<std::pair<float, int64_t>> c;
+    for (int64_t q = 0; q < B; ++q) {
+      c.clear();
+      for (int g = 0; g < G; ++g)
+        for (int i = 0; i < k; ++i) {
+          const size_t o = ((size_t)g * B + q) * k + i;
+          if (sid[o] >= 0) c.emplace_back(sd[o], sid[o]);
+        }
+      const size_t m = std::min<size_t>(k, c.size());
+      std::partial_sort(c.begin(), c.begin() + m, c.end());
+      for (int i = 0; i < k; ++i) {
+        oid[q * k + i] = (size_t)i < m ? c[i].second : -1;
+        od[q * k + i] = (size_t)i < m ? c[i].first : INFINITY;
+      }
+    }
+  });
+}
+
+int rd_merge_topk_device(int32_t G, int64_t B, int32_t k, const int64_t* ids, const float* dists, int64_t* oid,
+                         float* od, void* stream) {
+  return guarded([&] {
+    if (G < 1 || B < 0 || k < 1 || k > 32) throw_rd(RD_ERR_INVALID, "merge_device: invalid arguments (k <= 32)");
+    CK(rd::launch_shard_merge(G, B, k, reinterpret_cast<const long long*>(ids), dists,
+                              reinterpret_cast<long long*>(oid), od, (cudaStream_t)stream));
+  });
+}
+
+// ---------------------------------------------------------------- placement arithmetic
+int rd_llm_reservation_bytes(const rd_llm_reservation* r, double* out) {
+  return guarded([&] {
+    if (!r || !out) throw_rd(RD_ERR_INVALID, "null argument");
+    if (r->gen_batch_size < 0 || r->w_gpu < 0 || r->w_gpu > 1 || r->c_gpu < 0 || r->c_gpu > 1)
+      throw_rd(RD_ERR_INVALID, "reservation: fractions in [0,1] and batch >= 0 required");
+    const double W = (double)r->weight_total;
+    const double C = (double)r->kv_bytes_per_request * r->gen_batch_size;
+    double H = (double)r->workspace_bytes_per_request * r->gen_batch_size;
+    if (r->decode_phase) H *= r->workspace_fraction;
+    *out = r->w_gpu * W + r->c_gpu * C + H;
+  });
+}
+
+int32_t rd_staging_depth(double free_bytes, double item_bytes) {
+  if (item_bytes <= 0) return 1;
+  const double q = std::floor(free_bytes / item_bytes);
+  if (q < 1) return 1;
+  if (q > (double)(1 << 20)) return 1 << 20;
+  return (int32_t)q;
+}
+
+}  // extern "C"

@@ -1,0 +1,271 @@
+// coarse.cu — N1 coarse quantization and N2 per-query nprobe selection (sm_100a).
+//
+// N1: Dc[b][j] = ||c_j||^2 - 2 q_b.c_j with a register-tiled FFMA GEMM
+//     (64 queries x 128 centroids per CTA, 4x8 per thread, k-major smem tiles).
+// N2: one CTA per query: radix-select the C = nprobe + 32 smallest approximate
+//     distances, recompute those exactly (canonical fp64 sum, identical to the
+//     oracle), order by (exact distance, list id) and keep nprobe. The probe set
+//     is certified when every non-candidate's approximate distance, less the
+//     GEMM's error bound, exceeds the nprobe-th exact distance.
+#include <float.h>
+
+#include "ivf_kernels.cuh"
+#include "rd_device.cuh"
+
+namespace rd {
+
+namespace {
+
+constexpr int kBM = 64, kBN = 128, kBK = 16;
+
+__global__ void __launch_bounds__(256) coarse_gemm_kernel(const float* __restrict__ Q,
+                                                          const float* __restrict__ C,
+                                                          const float* __restrict__ cnorm,
+                                                          float* __restrict__ Dc, int B, int nlist,
+                                                          int d) {
+  __shared__ __align__(16) float As[kBK][kBM + 4];
+  __shared__ __align__(16) float Bs[kBK][kBN + 4];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;  // 16 x 16 threads: 4 queries x 8 centroids each
+  const int qb = blockIdx.y * kBM, cb = blockIdx.x * kBN;
+  float acc[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+  for (int k0 = 0; k0 < d; k0 += kBK) {
+    {  // A: 64 rows x 16 k = 256 float4
+      const int r = tid >> 2, kq = (tid & 3) * 4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (qb + r < B && k0 + kq < d) v = *reinterpret_cast<const float4*>(Q + (size_t)(qb + r) * d + k0 + kq);
+      As[kq + 0][r] = v.x;
+      As[kq + 1][r] = v.y;
+      As[kq + 2][r] = v.z;
+      As[kq + 3][r] = v.w;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // B: 128 rows x 16 k = 512 float4
+      const int idx = tid + h * 256;
+      const int r = idx >> 2, kq = (idx & 3) * 4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (cb + r < nlist && k0 + kq < d) v = *reinterpret_cast<const float4*>(C + (size_t)(cb + r) * d + k0 + kq);
+      Bs[kq + 0][r] = v.x;
+      Bs[kq + 1][r] = v.y;
+      Bs[kq + 2][r] = v.z;
+      Bs[kq + 3][r] = v.w;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kBK; ++k) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[k][ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[k][tx * 8]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[k][tx * 8 + 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w};
+      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int q = qb + ty * 4 + i;
+    if (q >= B) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = cb + tx * 8 + j;
+      if (c < nlist) Dc[(size_t)q * nlist + c] = __ldg(cnorm + c) - 2.f * acc[i][j];
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t f2key(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(uint32_t k) {
+  uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+  return __uint_as_float(u);
+}
+
+// block-wide exclusive scan of one int per thread (256 threads); returns total via *total
+__device__ int block_excl_scan(int v, int* sh, int* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int s = lane < 8 ? sh[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < 8) sh[lane] = s;
+  }
+  __syncthreads();
+  const int base = w ? sh[w - 1] : 0;
+  *total = sh[7];
+  __syncthreads();
+  return base + x - v;
+}
+
+constexpr int kSelThreads = 256;
+constexpr int kSelMaxCand = 512;
+
+// dynamic smem: keys[nlist] (u32)
+__global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const SelectParams p) {
+  extern __shared__ uint32_t keys[];
+  __shared__ int hist[2048];
+  __shared__ int scan_sh[8];
+  __shared__ int cand[kSelMaxCand];
+  __shared__ float cdist[kSelMaxCand];
+  __shared__ uint32_t sel_prefix, sel_k;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int nlist = p.nlist;
+  const float* drow = p.Dc + (size_t)b * nlist;
+  for (int j = tid; j < nlist; j += kSelThreads) keys[j] = f2key(drow[j]);
+  const int C = min(nlist, p.nprobe + kCoarseExtra);
+  __syncthreads();
+
+  // radix select of the C-th smallest key: 11 + 11 + 10 bits
+  uint32_t prefix = 0, mask = 0, kk = (uint32_t)C;
+  const int shifts[3] = {21, 10, 0};
+  const int widths[3] = {11, 11, 10};
+  for (int pass = 0; pass < 3; ++pass) {
+    const int sh = shifts[pass], nb = 1 << widths[pass];
+    for (int i = tid; i < nb; i += kSelThreads) hist[i] = 0;
+    __syncthreads();
+    for (int j = tid; j < nlist; j += kSelThreads) {
+      const uint32_t kv = keys[j];
+      if ((kv & mask) == prefix) atomicAdd(&hist[(kv >> sh) & (nb - 1)], 1);
+    }
+    __syncthreads();
+    // each thread owns nb/256 consecutive bins
+    const int per = nb / kSelThreads;
+    int local = 0;
+    for (int i = 0; i < per; ++i) local += hist[tid * per + i];
+    int tot;
+    const int before = block_excl_scan(local, scan_sh, &tot);
+    if (before < (int)kk && before + local >= (int)kk) {
+      int run = before;
+      for (int i = 0; i < per; ++i) {
+        const int h = hist[tid * per + i];
+        if (run + h >= (int)kk) {
+          sel_prefix = prefix | ((uint32_t)(tid * per + i) << sh);
+          sel_k = kk - run;
+          break;
+        }
+        run += h;
+      }
+    }
+    __syncthreads();
+    prefix = sel_prefix;
+    kk = sel_k;
+    mask |= (uint32_t)(nb - 1) << sh;
+    __syncthreads();
+  }
+  const uint32_t T = prefix;  // the C-th smallest key; kk = how many equal-to-T to take
+
+  // ordered compaction: all keys < T, then the first kk keys == T by list id
+  const int per = (nlist + kSelThreads - 1) / kSelThreads;
+  const int j0 = tid * per, j1 = min(nlist, j0 + per);
+  int nlt = 0, neq = 0;
+  for (int j = j0; j < j1; ++j) {
+    nlt += keys[j] < T;
+    neq += keys[j] == T;
+  }
+  int tot_lt, tot_eq;
+  int olt = block_excl_scan(nlt, scan_sh, &tot_lt);
+  int oeq = block_excl_scan(neq, scan_sh, &tot_eq);
+  for (int j = j0; j < j1; ++j) {
+    if (keys[j] < T) {
+      cand[olt++] = j;
+    } else if (keys[j] == T) {
+      if (oeq < (int)kk) cand[tot_lt + oeq] = j;
+      ++oeq;
+    }
+  }
+  __syncthreads();
+  const int ncand = tot_lt + (int)kk;  // == C
+
+  // exact rerank of candidates: 8 lanes per candidate
+  const float* q = p.queries + (size_t)b * p.d;
+  const int grp = tid >> 3, j8 = tid & 7;
+  for (int c0 = 0; c0 < ncand; c0 += kSelThreads / 8) {
+    const int c = c0 + grp;
+    const int cc = c < ncand ? c : ncand - 1;
+    const float e = exact_l2_group8(q, p.centroids + (size_t)cand[cc] * p.d, p.d, j8);
+    if (c < ncand && j8 == 0) cdist[c] = e;
+  }
+  // pad to power of two and bitonic sort by (dist, list id)
+  int P2 = 1;
+  while (P2 < ncand) P2 <<= 1;
+  for (int c = ncand + tid; c < P2; c += kSelThreads) {
+    cdist[c] = __builtin_huge_valf();
+    cand[c] = 0x7fffffff;
+  }
+  __syncthreads();
+  for (int size = 2; size <= P2; size <<= 1) {
+    for (int jj = size >> 1; jj > 0; jj >>= 1) {
+      for (int i = tid; i < P2; i += kSelThreads) {
+        const int l = i ^ jj;
+        if (l > i) {
+          const bool up = (i & size) == 0;
+          const float di = cdist[i], dl = cdist[l];
+          const int ii = cand[i], il = cand[l];
+          const bool l_less = dl < di || (dl == di && il < ii);
+          if (l_less == up) {
+            cdist[i] = dl;
+            cdist[l] = di;
+            cand[i] = il;
+            cand[l] = ii;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  const int np = min(p.nprobe, nlist);
+  for (int i = tid; i < p.nprobe; i += kSelThreads) p.probes[(size_t)b * p.nprobe + i] = i < np ? cand[i] : -1;
+  if (tid == 0 && C < nlist) {
+    // error bound of the approximate distance: sequential fp32 FFMA over d terms
+    const float qn = p.qnorm[b];
+    const float u = 5.9604645e-8f;
+    const float eps = 2.f * ((p.d + 4) * u * 2.f * sqrtf(qn) * p.cmax + 8.f * u * (qn + p.cmax * p.cmax)) + 1e-30f;
+    const float lower = key2f(T) + qn - eps;  // lower bound on any excluded exact distance
+    if (!(lower > cdist[np - 1])) atomicAdd(p.probe_fail, 1u);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_coarse(const float* Q, const float* C, const float* cnorm, float* Dc, int B,
+                          int nlist, int d, cudaStream_t s) {
+  dim3 grid((nlist + kBN - 1) / kBN, (B + kBM - 1) / kBM);
+  coarse_gemm_kernel<<<grid, 256, 0, s>>>(Q, C, cnorm, Dc, B, nlist, d);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select(const SelectParams& p, cudaStream_t s) {
+  if (p.nprobe + kCoarseExtra > kSelMaxCand) return cudaErrorInvalidValue;
+  const size_t smem = sizeof(uint32_t) * (size_t)p.nlist;
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(coarse_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  coarse_select_kernel<<<p.B, kSelThreads, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace rd

@@ -1,0 +1,112 @@
+// ivf_kernels.cuh — launch interface of the IVF-Flat search kernels (sm_100a).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rd {
+
+// Scan geometry (see DESIGN.md §Kernels / N4):
+constexpr int kScanRows = 256;      // rows of one row tile (one TMA box)
+constexpr int kScanKSlice = 32;     // fp32 dims per stage: 128 B rows, SWIZZLE_128B
+constexpr int kScanStages = 4;      // smem ring depth (32 KiB per stage)
+constexpr int kScanG = 16;          // max queries per tile
+constexpr int kScanThreads = 288;   // 8 consumer warps + 1 TMA producer warp
+constexpr int kScanStageBytes = kScanRows * 128;
+constexpr int kCoarseExtra = 32;    // approximate coarse candidates beyond nprobe
+
+// One unit of scan work: rows [row0, row0+nrows) of one list against <= 16 queries.
+struct __align__(16) ScanTile {
+  long long src_row;  // TMA row coordinate of the first row in the source arena
+  long long grow0;    // global (list-order) row index of the first row
+  int list;
+  int nrows;
+  int qoff;           // offset into list_q (query ids probing `list`)
+  int nq;
+};
+
+struct ScanParams {
+  const ScanTile* tiles;
+  const int* ntiles;       // device scalar
+  int* tile_counter;       // device scalar, zeroed before launch
+  const float* queries;    // B x d
+  const float* qnorm;      // B
+  const int* list_q;       // query ids grouped by list
+  const float* xnorm;      // n (global row order)
+  float* part_dist;        // B x cap x 32
+  int* part_row;           // B x cap x 32
+  int* part_count;         // B
+  int part_cap;
+  int d;
+};
+
+size_t scan_smem_bytes(int d);
+cudaError_t launch_scan(const CUtensorMap& map256, const CUtensorMap& map32, const ScanParams& p,
+                        int grid, cudaStream_t s);
+
+// Coarse quantization: Dc[b][j] = ||c_j||^2 - 2 q_b . c_j (the query norm is
+// constant per query and added where an absolute distance is needed).
+cudaError_t launch_coarse(const float* Q, const float* C, const float* cnorm, float* Dc, int B,
+                          int nlist, int d, cudaStream_t s);
+
+struct SelectParams {
+  const float* Dc;         // B x nlist
+  const float* queries;    // B x d
+  const float* qnorm;      // B
+  const float* centroids;  // nlist x d
+  int* probes;             // B x nprobe
+  unsigned* probe_fail;    // device scalar
+  int B, nlist, nprobe, d;
+  float cmax;              // max ||c||
+};
+cudaError_t launch_select(const SelectParams& p, cudaStream_t s);
+
+struct PlanParams {
+  const int* probes;          // B x nprobe
+  unsigned* bitmap;           // nlist x W
+  int W;                      // words per list = ceil(B / 32)
+  const long long* list_off;  // nlist + 1 (global rows)
+  const long long* res_row0;  // nlist: row in the resident arena, -1 = offloaded
+  int* list_nq;               // nlist
+  int* list_qoff;             // nlist
+  int* list_ntile;            // nlist (resident tiles)
+  int* list_toff;             // nlist
+  int* list_q;                // B x nprobe
+  ScanTile* tiles;
+  int* ntiles;                // device scalar
+  unsigned long long* counters;  // [0] unique lists, [1] resident rows probed, [2] offloaded rows probed
+  int B, nlist, nprobe, R;
+};
+cudaError_t launch_plan(const PlanParams& p, cudaStream_t s);
+
+struct MergeParams {
+  const float* part_dist;
+  const int* part_row;
+  const int* part_count;
+  int part_cap;
+  const float* queries;
+  const float* qnorm;
+  const long long* list_off;       // nlist + 1
+  const float* const* list_base;   // nlist: device-visible pointer to the list's first row
+  const long long* ids;            // n (global row order)
+  int nlist, d, k;
+  float xmax;
+  long long* out_ids;              // B x k
+  float* out_dists;                // B x k
+  unsigned* margin_fail;
+  int B;
+};
+cudaError_t launch_merge(const MergeParams& p, cudaStream_t s);
+
+// [G][B][k] shard results -> [B][k] (device)
+cudaError_t launch_shard_merge(int G, long long B, int k, const long long* ids, const float* dists,
+                               long long* out_ids, float* out_dists, cudaStream_t s);
+
+// Index build helpers
+cudaError_t launch_gen_centroids(float* C, int nlist, int d, uint64_t sc, cudaStream_t s);
+cudaError_t launch_gen_vectors(float* X, const long long* ids, long long n, int d, int nlist,
+                               const float* C, uint64_t sa, uint64_t sx, float sigma, cudaStream_t s);
+cudaError_t launch_row_norms(const float* X, long long n, int d, float* out, cudaStream_t s);
+cudaError_t launch_max_f32(const float* v, long long n, float* out, cudaStream_t s);
+
+}  // namespace rd

@@ -1,0 +1,172 @@
+// merge.cu — N6 per-query top-k merge and N7 exact fp32 rerank (sm_100a).
+//
+// One CTA per query: its warps merge the per-tile top-32 partial lists with
+// warp bitonic merges, the block keeps the 32 best approximate candidates and
+// recomputes their distances with the canonical exact sum (8 lanes per
+// candidate), orders them by (exact distance, id) and writes the top-k. The
+// result is certified when the 32nd approximate distance, less the scan's
+// error bound, still exceeds the k-th exact distance: then no vector dropped
+// anywhere upstream can belong to the exact top-k (SURVEY §7 "Hard parts").
+#include "ivf_kernels.cuh"
+#include "rd_device.cuh"
+
+namespace rd {
+
+namespace {
+
+constexpr float kInf = __builtin_huge_valf();
+constexpr long long kNoKey = 0x7fffffffffffffffll;
+
+__device__ __forceinline__ int list_of_row(const long long* off, int nlist, long long row) {
+  int lo = 0, hi = nlist;  // off[lo] <= row < off[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(off + mid) <= row)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) merge_rerank_kernel(const MergeParams p) {
+  __shared__ float sd[8][kTopK];
+  __shared__ long long sk[8][kTopK];
+  __shared__ float ex_d[kTopK];
+  __shared__ long long ex_id[kTopK];
+  __shared__ float tau_s;
+  const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int cnt = min(p.part_count[b], p.part_cap);
+
+  float ld = kInf;
+  long long lk = kNoKey;
+  for (int i = warp; i < cnt; i += 8) {
+    // partials are ascending; read reversed to get a descending batch
+    const size_t o = ((size_t)b * p.part_cap + i) * kTopK + (kTopK - 1 - lane);
+    const float bd = p.part_dist[o];
+    const int br = p.part_row[o];
+    const float v = br < 0 ? kInf : bd;
+    const long long key = br < 0 ? kNoKey : (long long)br;
+    if (pair_less(v, key, ld, lk)) {
+      ld = v;
+      lk = key;
+    }
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) bitonic_step(ld, lk, lane, j, true);
+  }
+  sd[warp][lane] = ld;
+  sk[warp][lane] = lk;
+  __syncthreads();
+  if (warp == 0) {
+    for (int w = 1; w < 8; ++w) {
+      const float v = sd[w][kTopK - 1 - lane];
+      const long long key = sk[w][kTopK - 1 - lane];
+      if (pair_less(v, key, ld, lk)) {
+        ld = v;
+        lk = key;
+      }
+#pragma unroll
+      for (int j = 16; j > 0; j >>= 1) bitonic_step(ld, lk, lane, j, true);
+    }
+    sd[0][lane] = ld;
+    sk[0][lane] = lk;
+    if (lane == 31) tau_s = ld;
+  }
+  __syncthreads();
+
+  // exact rerank: thread (c = tid/8, j = tid%8)
+  const int c = tid >> 3, j8 = tid & 7;
+  const long long row = sk[0][c];
+  const float* q = p.queries + (size_t)b * p.d;
+  long long id = kNoKey;
+  const float* x = q;
+  int dd = 0;  // a padded slot runs zero terms so the warp stays converged for the shuffles
+  if (row != kNoKey) {
+    const int l = list_of_row(p.list_off, p.nlist, row);
+    x = p.list_base[l] + (size_t)(row - p.list_off[l]) * p.d;
+    dd = p.d;
+    id = p.ids[row];
+  }
+  float e = exact_l2_group8_any(q, x, dd, j8);
+  if (row == kNoKey) e = kInf;
+  if (j8 == 0) {
+    ex_d[c] = e;
+    ex_id[c] = id;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    float dd = ex_d[lane];
+    long long kk = ex_id[lane];
+    warp_sort32(dd, kk, lane, true);
+    if (lane < p.k) {
+      p.out_ids[(size_t)b * p.k + lane] = kk == kNoKey ? -1 : kk;
+      p.out_dists[(size_t)b * p.k + lane] = kk == kNoKey ? kInf : dd;
+    }
+    for (int i = kTopK + lane; i < p.k; i += 32) {  // k > 32 is rejected by the host; pad defensively
+      p.out_ids[(size_t)b * p.k + i] = -1;
+      p.out_dists[(size_t)b * p.k + i] = kInf;
+    }
+    const float ek = __shfl_sync(0xffffffffu, dd, min(p.k, kTopK) - 1);
+    if (lane == 0) {
+      const float tau = tau_s;
+      if (tau != kInf) {
+        const float qn = p.qnorm[b];
+        const float u = 5.9604645e-8f;
+        const float xm = p.xmax;
+        const float eps =
+            2.f * ((p.d / 2 + 8) * u * 2.f * sqrtf(qn) * xm + 8.f * u * (qn + xm * xm)) + 1e-30f;
+        if (!(tau - eps > ek)) atomicAdd(p.margin_fail, 1u);
+      }
+    }
+  }
+}
+
+__global__ void shard_merge_kernel(int G, long long B, int k, const long long* __restrict__ ids,
+                                   const float* __restrict__ dists, long long* __restrict__ oid,
+                                   float* __restrict__ od) {
+  // one warp per query; k <= 32; candidates G*k absorbed in batches of 32
+  const long long q = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (q >= B) return;
+  float ld = kInf;
+  long long lk = kNoKey;
+  const long long tot = (long long)G * k;
+  for (long long c0 = 0; c0 < tot; c0 += 32) {
+    const long long c = c0 + lane;
+    float v = kInf;
+    long long key = kNoKey;
+    if (c < tot) {
+      const int g = (int)(c / k), i = (int)(c - (long long)g * k);
+      const long long id = ids[((long long)g * B + q) * k + i];
+      if (id >= 0) {
+        v = dists[((long long)g * B + q) * k + i];
+        key = id;
+      }
+    }
+    warp_merge32(ld, lk, v, key, lane);
+  }
+  if (lane < k) {
+    oid[q * k + lane] = lk == kNoKey ? -1 : lk;
+    od[q * k + lane] = lk == kNoKey ? kInf : ld;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_merge(const MergeParams& p, cudaStream_t s) {
+  if (p.B == 0) return cudaSuccess;
+  merge_rerank_kernel<<<p.B, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_merge(int G, long long B, int k, const long long* ids, const float* dists,
+                               long long* out_ids, float* out_dists, cudaStream_t s) {
+  if (B == 0) return cudaSuccess;
+  if (k > 32) return cudaErrorInvalidValue;
+  const long long threads = B * 32;
+  shard_merge_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(G, B, k, ids, dists, out_ids,
+                                                                       out_dists);
+  return cudaGetLastError();
+}
+
+}  // namespace rd

@@ -1,0 +1,129 @@
+"""GPU parity: the B200 engine (librd_b200.so, called through the C-ABI)
+against the CPU oracle on the same seeded inputs. The bar is bit-exact: the
+engine reranks its candidates with the canonical exact distance, so ids and
+distances must be identical to the oracle's, and every query's candidate
+margin and probe set must be certified (SURVEY §8c parity rule, tolerance
+1e-5 relative for distances is implied by bit equality)."""
+import os
+
+import numpy as np
+import pytest
+
+import numpy_ref as R
+from make_golden import CASES
+
+pytestmark = pytest.mark.gpu
+GOLD = np.load(os.path.join(os.path.dirname(__file__), "golden", "ivf_small.npz"))
+
+
+def _check(res, want_ids, want_d):
+    np.testing.assert_array_equal(res.ids, want_ids)
+    np.testing.assert_array_equal(res.dists, want_d)
+    assert res.stats["margin_failures"] == 0
+    assert res.stats["probe_failures"] == 0
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_engine_matches_golden(engine, name):
+    c = CASES[name]
+    desc = engine.desc(c["n"], c["d"], c["nlist"], shard=c.get("shard", 0), num_shards=c.get("num_shards", 1))
+    idx = engine.synthetic_index(desc)
+    offs, ids, _ = idx.layout()
+    np.testing.assert_array_equal(offs, GOLD[f"{name}/offs"])
+    q = GOLD[f"{name}/queries"]
+    np.testing.assert_array_equal(idx.probe(q, c["nprobe"]), GOLD[f"{name}/probes"])
+    _check(idx.search(q, c["nprobe"], c["k"]), GOLD[f"{name}/out_ids"], GOLD[f"{name}/out_dists"])
+
+
+@pytest.mark.parametrize("B,nprobe,k", [(1, 8, 10), (7, 1, 1), (32, 16, 10), (100, 64, 20), (33, 5, 32)])
+def test_engine_vs_oracle_synthetic(engine, oracle, B, nprobe, k):
+    n, d, nlist = 40000, 768, 64
+    desc = engine.desc(n, d, nlist)
+    q, _ = engine.synth_queries(desc, 1000, B)
+    e = engine.synthetic_index(desc).search(q, nprobe, k)
+    o = oracle.synthetic_index(desc).search(q, nprobe, k)
+    _check(e, o.ids, o.dists)
+
+
+def test_engine_generator_bit_exact(engine, oracle):
+    desc = engine.desc(5000, 96, 17)
+    ei = engine.synthetic_index(desc)
+    oi = oracle.synthetic_index(desc)
+    eo, eids, _ = ei.layout()
+    oo, oids, _ = oi.layout()
+    np.testing.assert_array_equal(eo, oo)
+    np.testing.assert_array_equal(eids, oids)
+    # vectors: search with nprobe = nlist and k = n returns exact distances to every vector
+    q, _ = engine.synth_queries(desc, 0, 3)
+    want = R.vectors_of(oids[:50], 96, 17)
+    np.testing.assert_array_equal(want, np.stack([engine.synth_vector(desc, int(i)) for i in oids[:50]]))
+    _check(ei.search(q, 17, 32), *[getattr(oi.search(q, 17, 32), a) for a in ("ids", "dists")])
+
+
+def test_from_host_ties_duplicates_empty_lists(engine, oracle):
+    rng = np.random.default_rng(3)
+    d, nlist = 64, 12
+    lens = np.array([0, 5, 0, 700, 3, 0, 400, 1, 9, 0, 260, 33])
+    n = int(lens.sum())
+    X = rng.integers(-2, 3, size=(n, d)).astype(np.float32)
+    X[5:40] = X[0]  # exact duplicates -> equal distances, id order decides
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    C = rng.integers(-2, 3, size=(nlist, d)).astype(np.float32)
+    ids = (rng.permutation(n).astype(np.int64) * 7 + 5)
+    Q = np.concatenate([X[:3], rng.integers(-2, 3, size=(9, d)).astype(np.float32)])
+    for nprobe, k in [(nlist, 32), (3, 10), (1, 32)]:
+        e = engine.index_from_host(X, offs, C, ids).search(Q, nprobe, k)
+        o = oracle.index_from_host(X, offs, C, ids).search(Q, nprobe, k)
+        np.testing.assert_array_equal(e.ids, o.ids)
+        np.testing.assert_array_equal(e.dists, o.dists)
+
+
+@pytest.mark.parametrize("frac", [0.5, 1.0])
+def test_offloaded_lists_same_results(engine, oracle, frac):
+    n, d, nlist, B, nprobe, k = 60000, 768, 64, 48, 16, 10
+    desc = engine.desc(n, d, nlist)
+    q, _ = engine.synth_queries(desc, 77, B)
+    idx = engine.synthetic_index(desc)
+    idx.place(offload_fraction=frac, staging_slots=2)
+    info = idx.info()
+    assert info["lists_resident"] == nlist - int(np.floor(frac * nlist + 0.5))
+    e = idx.search(q, nprobe, k)
+    assert e.stats["h2d_list_bytes"] > 0
+    o = oracle.synthetic_index(desc).search(q, nprobe, k)
+    _check(e, o.ids, o.dists)
+    idx.place(offload_fraction=0.0)  # back to fully resident between searches
+    _check(idx.search(q, nprobe, k), o.ids, o.dists)
+
+
+def test_device_shard_merge(engine):
+    import torch
+    rng = np.random.default_rng(5)
+    G, B, k = 4, 50, 10
+    d = np.sort(rng.random((G, B, k)).astype(np.float32), axis=2)
+    ids = rng.integers(0, 1 << 40, size=(G, B, k)).astype(np.int64)
+    ids[1, :, 5:] = -1
+    want_i, want_d = engine.merge_topk(ids, d)
+    ti, td = torch.from_numpy(ids).cuda(), torch.from_numpy(d).cuda()
+    oi = torch.empty((B, k), dtype=torch.int64, device="cuda")
+    od = torch.empty((B, k), dtype=torch.float32, device="cuda")
+    engine.check(engine.lib.rd_merge_topk_device(G, B, k, ti.data_ptr(), td.data_ptr(), oi.data_ptr(),
+                                                 od.data_ptr(), None))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(oi.cpu().numpy(), want_i)
+    np.testing.assert_array_equal(od.cpu().numpy(), want_d)
+
+
+def test_search_device_matches_host_path(engine):
+    import torch
+    desc = engine.desc(30000, 768, 64)
+    idx = engine.synthetic_index(desc)
+    q, _ = engine.synth_queries(desc, 5, 64)
+    h = idx.search(q, 8, 10)
+    dq = torch.from_numpy(q).cuda()
+    di = torch.empty((64, 10), dtype=torch.int64, device="cuda")
+    dd = torch.empty((64, 10), dtype=torch.float32, device="cuda")
+    st = idx.search_device(dq.data_ptr(), 64, 8, 10, di.data_ptr(), dd.data_ptr(),
+                           stream=torch.cuda.current_stream().cuda_stream, sync=True)
+    assert st["margin_failures"] == 0
+    np.testing.assert_array_equal(di.cpu().numpy(), h.ids)
+    np.testing.assert_array_equal(dd.cpu().numpy(), h.dists)

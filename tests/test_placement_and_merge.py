@@ -1,0 +1,68 @@
+"""Host-side logic on CPU: the placement rule, the shard-merge algebra (the
+multi-GPU exchange step), and the exported C-ABI surface."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_engine_exports_every_header_symbol(engine_lib, oracle):
+    from paper_2504_15302_b200.retriever import EXPORTED_SYMBOLS
+    hdr = open(os.path.join(ROOT, "include", "rd.h")).read()
+    declared = set(re.findall(r"\b(rd_[a-z0-9_]+)\s*\(", hdr))
+    assert declared == set(EXPORTED_SYMBOLS)
+    for lib in (engine_lib, oracle):
+        for sym in declared:
+            assert hasattr(lib.lib, sym), (lib.path, sym)
+    assert engine_lib.backend == "b200-sm100a" and oracle.backend == "cpu-oracle"
+
+
+def _shard_results(oracle, G, n=3000, d=64, nlist=24, B=10, nprobe=6, k=10):
+    desc = oracle.desc(n, d, nlist)
+    Q, _ = oracle.synth_queries(desc, 0, B)
+    full = oracle.synthetic_index(desc).search(Q, nprobe, k)
+    parts = [oracle.synthetic_index(oracle.desc(n, d, nlist, shard=g, num_shards=G)).search(Q, nprobe, k)
+             for g in range(G)]
+    return full, np.stack([p.ids for p in parts]), np.stack([p.dists for p in parts])
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 8])
+def test_row_striped_shards_merge_to_unsharded(oracle, engine_lib, G):
+    full, sid, sd = _shard_results(oracle, G)
+    for lib in (engine_lib, oracle):
+        mi, md = lib.merge_topk(sid, sd)
+        np.testing.assert_array_equal(mi, full.ids)
+        np.testing.assert_array_equal(md, full.dists)
+
+
+def test_shards_partition_the_lists(oracle):
+    n, d, nlist, G = 2000, 16, 12, 3
+    offs, ids, _ = oracle.synthetic_index(oracle.desc(n, d, nlist)).layout()
+    parts = [oracle.synthetic_index(oracle.desc(n, d, nlist, shard=g, num_shards=G)).layout() for g in range(G)]
+    for l in range(nlist):
+        cat = np.concatenate([p[1][p[0][l]:p[0][l + 1]] for p in parts])
+        np.testing.assert_array_equal(cat, ids[offs[l]:offs[l + 1]])
+
+
+def test_placement_rule(oracle):
+    from paper_2504_15302_b200.retriever import InfeasibleError
+    desc = oracle.desc(4000, 32, 20)
+    idx = oracle.synthetic_index(desc)
+    offs, _, _ = idx.layout(with_ids=False)
+    lens = np.diff(offs)
+    idx.place(offload_fraction=0.5)
+    _, _, mask = idx.layout(with_ids=False)
+    assert mask.sum() == 10 and mask[:10].all()
+    heat = np.arange(20)[::-1].copy()[::-1]  # list 19 hottest
+    idx.place(offload_fraction=0.25, list_heat=heat)
+    _, _, mask = idx.layout(with_ids=False)
+    assert mask.sum() == 15 and mask[5:].all()
+    budget = int(lens[:3].sum() * 32 * 4)
+    idx.place(hbm_budget_bytes=budget)
+    _, _, mask = idx.layout(with_ids=False)
+    assert mask[:3].all() and not mask[3:].any()
+    with pytest.raises(InfeasibleError):
+        idx.place(hbm_budget_bytes=budget, resident_mask=np.ones(20, np.uint8))
