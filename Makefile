@@ -27,3 +27,8 @@ clean:
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean
+
+# test-only probe of the tcgen05 building blocks (tests/test_gpu_tcgen05.py)
+tests/cuda/libtcprobe.so: tests/cuda/tc_probe.cu $(PKG)/csrc/rd_device.cuh
+	$(NVCC) $(ARCH) -O2 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -o $@ $<
+all: tests/cuda/libtcprobe.so

@@ -22,6 +22,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -193,6 +194,7 @@ void parallel_for(long long n, const std::function<void(long long, long long)>& 
 struct rd_index {
   int device = 0;
   int num_sms = 148;
+  int tc_min_q = rd::kTcMinQ;
   long long n = 0;
   int d = 0, nlist = 0;
   std::vector<long long> list_off;  // host copy, nlist + 1
@@ -207,20 +209,20 @@ struct rd_index {
   std::vector<long long> host_row0;   // host: row in host arena or -1
   long long n_resident = 0;
   HBuf<float> host_arena;
-  CUtensorMap map256{}, map32{};
+  CUtensorMap map256{}, map128{}, map32{};
 
   // staging ring for offloaded lists
   int slots = 0;
   long long slot_rows = 0;
   DBuf<float> staging;
-  CUtensorMap smap256{}, smap32{};
+  CUtensorMap smap256{}, smap128{}, smap32{};
 
   // per-search workspace
   struct Ws {
-    DBuf<float> qnorm, Dc, q, dists;
+    DBuf<float> qnorm, Dc, q, dists, qsplit;
     DBuf<int> probes, list_nq, list_qoff, list_ntile, list_toff, list_q, part_count, part_row, meta, off_meta;
     DBuf<unsigned> bitmap, fails;
-    DBuf<rd::ScanTile> tiles, off_tiles;
+    DBuf<rd::ScanTile> tiles, ff_tiles, off_tiles;
     DBuf<unsigned long long> counters;
     DBuf<float> part_dist;
     DBuf<long long> ids;
@@ -284,6 +286,8 @@ struct rd_index {
     for (auto& e : ev) CK(cudaEventCreate(&e));
     for (auto& r : tev)
       for (auto& e : r) CK(cudaEventCreate(&e));
+    if (const char* v = std::getenv("RD_TC_MIN_Q")) tc_min_q = std::max(1, std::atoi(v));
+    // the tensor-core scan stages bf16 query slices of 64 dims
   }
 
   void finish_layout() {
@@ -324,6 +328,7 @@ struct rd_index {
     d_list_base.alloc(nlist);
     CK(cudaMemcpy(d_list_base.p, base.data(), sizeof(const float*) * nlist, cudaMemcpyHostToDevice));
     map256 = make_row_map(arena.p, std::max(1LL, n_resident), d, rd::kScanRows);
+    map128 = make_row_map(arena.p, std::max(1LL, n_resident), d, rd::kTcRows);
     map32 = make_row_map(arena.p, std::max(1LL, n_resident), d, 32);
   }
 };
@@ -629,6 +634,7 @@ int rd_index_place(rd_index* h, const rd_placement* p) {
     if (slots) {
       h->staging.alloc((size_t)slots * slot_rows * h->d);
       h->smap256 = make_row_map(h->staging.p, (long long)slots * slot_rows, h->d, rd::kScanRows);
+      h->smap128 = make_row_map(h->staging.p, (long long)slots * slot_rows, h->d, rd::kTcRows);
       h->smap32 = make_row_map(h->staging.p, (long long)slots * slot_rows, h->d, 32);
       h->slot_ready.resize(slots);
       h->slot_done.resize(slots);
@@ -659,7 +665,7 @@ Plan make_plan(const rd_index* h, long long B, int nprobe) {
   R = std::max<long long>(rd::kScanRows, std::min<long long>(4096, (R + rd::kScanRows - 1) / rd::kScanRows * rd::kScanRows));
   pl.R = (int)R;
   pl.max_chunks = (int)std::max<long long>(1, (h->max_len + R - 1) / R);
-  pl.cap = np * pl.max_chunks;
+  pl.cap = np * pl.max_chunks * rd::kPartsPerTile;
   pl.max_tiles = std::min<long long>(B * np, B * np / rd::kScanG + h->nlist) * pl.max_chunks + 1;
   return pl;
 }
@@ -667,7 +673,7 @@ Plan make_plan(const rd_index* h, long long B, int nprobe) {
 void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, long long* d_ids, float* d_dists,
                cudaStream_t s, bool sync, rd_search_stats* st) {
   if (nprobe < 1 || k < 1) throw_rd(RD_ERR_INVALID, "search: nprobe >= 1 and k >= 1 required");
-  if (k > rd::kTopK) throw_rd(RD_ERR_INVALID, "search: k <= %d supported, got %d", rd::kTopK, k);
+  if (k > rd::kMaxK) throw_rd(RD_ERR_INVALID, "search: k <= %d supported, got %d", rd::kMaxK, k);
   if (std::min(nprobe, h->nlist) + rd::kCoarseExtra > 512) throw_rd(RD_ERR_INVALID, "search: nprobe <= 480 supported");
   if (B >= (1LL << 24)) throw_rd(RD_ERR_INVALID, "search: batch too large (max 2^24-1 per call)");
   CK(cudaSetDevice(h->device));
@@ -681,11 +687,13 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   w.bitmap.ensure((size_t)nl * W);
   w.list_nq.ensure(nl);
   w.list_qoff.ensure(nl);
-  w.list_ntile.ensure(nl);
-  w.list_toff.ensure(nl);
+  w.list_ntile.ensure(2 * (size_t)nl);
+  w.list_toff.ensure(2 * (size_t)nl);
   w.list_q.ensure((size_t)B * nprobe);
   w.tiles.ensure(pl.max_tiles);
-  w.meta.ensure(2);
+  w.ff_tiles.ensure(pl.max_tiles);
+  w.qsplit.ensure((size_t)B * 2 * d);
+  w.meta.ensure(4);
   w.counters.ensure(3);
   w.fails.ensure(2);
   w.part_count.ensure(B);
@@ -693,6 +701,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   w.part_row.ensure((size_t)B * pl.cap * rd::kTopK);
   w.h_fails.ensure(2);
   w.h_counters.ensure(3);
+  w.h_meta.ensure(4);
 
   cudaEvent_t* te = h->next_timing_slot();
   cudaEvent_t e0 = te[0], e1 = te[1], e2 = te[2], e3 = h->ev[3], e_plan = h->ev[4], e_off = h->ev[5];
@@ -700,31 +709,36 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   CK(cudaEventRecord(e0, s));
   CK(cudaMemsetAsync(w.fails.p, 0, 2 * sizeof(unsigned), s));
   CK(rd::launch_row_norms(d_q, B, d, w.qnorm.p, s));
+  CK(rd::launch_qsplit(d_q, w.qsplit.p, B, d, s));
   CK(rd::launch_coarse(d_q, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, s));
   rd::SelectParams sp{w.Dc.p, d_q, w.qnorm.p, h->centroids.p, w.probes.p, w.fails.p, (int)B, nl, nprobe, d, h->cmax};
   CK(rd::launch_select(sp, s));
-  launches += 3;
+  launches += 4;
   rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
-                    w.list_ntile.p, w.list_toff.p, w.list_q.p, w.tiles.p, w.meta.p, w.counters.p,
-                    (int)B, nl, nprobe, pl.R};
+                    w.list_ntile.p, w.list_toff.p, w.list_q.p, w.tiles.p, w.ff_tiles.p, w.meta.p, w.counters.p,
+                    (int)B, nl, nprobe, pl.R, d % 64 == 0 ? h->tc_min_q : 1 << 30};
   CK(rd::launch_plan(pp, s));
   launches += 4;
   CK(cudaEventRecord(e1, s));
   CK(cudaMemsetAsync(w.part_count.p, 0, sizeof(int) * B, s));
-  CK(cudaMemsetAsync(w.meta.p + 1, 0, sizeof(int), s));
-  CK(cudaEventRecord(e_plan, s));
   const bool has_off = h->slots > 0;
   if (has_off) {  // fetch the probe histogram for host-side staging decisions
     w.h_nq.ensure(nl);
     w.h_qoff.ensure(nl);
     CK(cudaMemcpyAsync(w.h_nq.p, w.list_nq.p, sizeof(int) * nl, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(w.h_qoff.p, w.list_qoff.p, sizeof(int) * nl, cudaMemcpyDeviceToHost, s));
-    CK(cudaEventRecord(e_plan, s));
   }
-  rd::ScanParams sc{w.tiles.p, w.meta.p, w.meta.p + 1, d_q, w.qnorm.p, w.list_q.p, h->xnorm.p,
+  CK(cudaEventRecord(e_plan, s));
+  rd::ScanParams sc{w.ff_tiles.p, w.meta.p + 2, w.meta.p + 3, d_q, w.qnorm.p, w.list_q.p, h->xnorm.p,
                     w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d};
+  rd::TcScanParams tc{w.tiles.p, w.meta.p, w.meta.p + 1, w.qsplit.p, w.qnorm.p, w.list_q.p, h->xnorm.p,
+                      w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d};
   CK(rd::launch_scan(h->map256, h->map32, sc, h->num_sms, s));
   launches += 1;
+  if (d % 64 == 0) {  // the tensor-core path stages 64-dim bf16 query slices; otherwise every tile is FFMA
+    CK(rd::launch_scan_tc(h->map128, h->map32, tc, h->num_sms, s));
+    launches += 1;
+  }
   CK(cudaEventRecord(e2, s));
 
   unsigned long long h2d = 0;
@@ -744,13 +758,14 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
       batches.back().push_back(l);
       fill += len;
     }
-    // host-planned tiles for every batch, uploaded once
-    std::vector<rd::ScanTile> tv;
-    std::vector<int> tstart(batches.size() + 1, 0);
-    for (size_t bi = 0; bi < batches.size(); ++bi) {
+    // host-planned tiles of every batch (tensor-core and FFMA groups), uploaded once
+    const size_t nb = batches.size();
+    std::vector<rd::ScanTile> tv;  // per batch: [tc tiles][ff tiles]
+    std::vector<int> tstart(nb + 1, 0), ntc(nb, 0);
+    for (size_t bi = 0; bi < nb; ++bi) {
       tstart[bi] = (int)tv.size();
-      const int slot = (int)(bi % h->slots);
-      long long srow = (long long)slot * h->slot_rows;
+      std::vector<rd::ScanTile> ff;
+      long long srow = (long long)(bi % h->slots) * h->slot_rows;
       for (int l : batches[bi]) {
         const long long len = h->list_off[l + 1] - h->list_off[l];
         const int nq = w.h_nq.p[l];
@@ -764,30 +779,36 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
             T.nrows = (int)std::min<long long>(pl.R, len - c * pl.R);
             T.qoff = w.h_qoff.p[l] + g * rd::kScanG;
             T.nq = std::min(rd::kScanG, nq - g * rd::kScanG);
-            tv.push_back(T);
+            if (T.nq >= h->tc_min_q && d % 64 == 0)
+              tv.push_back(T);
+            else
+              ff.push_back(T);
           }
         srow += len;
       }
+      ntc[bi] = (int)tv.size() - tstart[bi];
+      tv.insert(tv.end(), ff.begin(), ff.end());
     }
-    tstart[batches.size()] = (int)tv.size();
-    const size_t nb = batches.size();
+    tstart[nb] = (int)tv.size();
     if (nb) {
       w.h_tiles.ensure(tv.size());
       std::memcpy(w.h_tiles.p, tv.data(), sizeof(rd::ScanTile) * tv.size());
       w.off_tiles.ensure(tv.size());
-      w.h_meta.ensure(2 * nb);
+      w.h_meta.ensure(4 * nb);
       for (size_t bi = 0; bi < nb; ++bi) {
-        w.h_meta.p[2 * bi] = tstart[bi + 1] - tstart[bi];
-        w.h_meta.p[2 * bi + 1] = 0;
+        w.h_meta.p[4 * bi + 0] = ntc[bi];
+        w.h_meta.p[4 * bi + 1] = 0;
+        w.h_meta.p[4 * bi + 2] = tstart[bi + 1] - tstart[bi] - ntc[bi];
+        w.h_meta.p[4 * bi + 3] = 0;
       }
       DBuf<int>& dmeta = w.off_meta;
-      dmeta.ensure(2 * nb);
+      dmeta.ensure(4 * nb);
       CK(cudaStreamWaitEvent(h->off_stream, e_plan, 0));
       CK(cudaMemcpyAsync(w.off_tiles.p, w.h_tiles.p, sizeof(rd::ScanTile) * tv.size(), cudaMemcpyHostToDevice,
                          h->off_stream));
-      CK(cudaMemcpyAsync(dmeta.p, w.h_meta.p, sizeof(int) * 2 * nb, cudaMemcpyHostToDevice, h->off_stream));
+      CK(cudaMemcpyAsync(dmeta.p, w.h_meta.p, sizeof(int) * 4 * nb, cudaMemcpyHostToDevice, h->off_stream));
       CK(cudaEventRecord(e3, h->off_stream));
-      CK(cudaEventRecord(h->ev[6], h->copy_stream));
+      CK(cudaStreamWaitEvent(h->copy_stream, e_plan, 0));
       for (size_t bi = 0; bi < nb; ++bi) {
         const int slot = (int)(bi % h->slots);
         if (bi >= (size_t)h->slots) CK(cudaStreamWaitEvent(h->copy_stream, h->slot_done[slot], 0));
@@ -802,13 +823,23 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
         }
         CK(cudaEventRecord(h->slot_ready[slot], h->copy_stream));
         CK(cudaStreamWaitEvent(h->off_stream, h->slot_ready[slot], 0));
-        rd::ScanParams so = sc;
-        so.tiles = w.off_tiles.p + tstart[bi];
-        so.ntiles = dmeta.p + 2 * bi;
-        so.tile_counter = dmeta.p + 2 * bi + 1;
-        const int grid = std::max(1, std::min(h->num_sms, tstart[bi + 1] - tstart[bi]));
-        CK(rd::launch_scan(h->smap256, h->smap32, so, grid, h->off_stream));
-        launches += 1;
+        const int nt_tc = ntc[bi], nt_ff = tstart[bi + 1] - tstart[bi] - ntc[bi];
+        if (nt_ff) {
+          rd::ScanParams so = sc;
+          so.tiles = w.off_tiles.p + tstart[bi] + nt_tc;
+          so.ntiles = dmeta.p + 4 * bi + 2;
+          so.tile_counter = dmeta.p + 4 * bi + 3;
+          CK(rd::launch_scan(h->smap256, h->smap32, so, std::min(h->num_sms, nt_ff), h->off_stream));
+          launches += 1;
+        }
+        if (nt_tc) {
+          rd::TcScanParams to = tc;
+          to.tiles = w.off_tiles.p + tstart[bi];
+          to.ntiles = dmeta.p + 4 * bi + 0;
+          to.tile_counter = dmeta.p + 4 * bi + 1;
+          CK(rd::launch_scan_tc(h->smap128, h->smap32, to, std::min(h->num_sms, nt_tc), h->off_stream));
+          launches += 1;
+        }
         CK(cudaEventRecord(h->slot_done[slot], h->off_stream));
       }
     }
@@ -828,8 +859,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   if (sync) {
     CK(cudaMemcpyAsync(w.h_counters.p, w.counters.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(w.h_fails.p, w.fails.p, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, s));
-    int ntiles = 0;
-    CK(cudaMemcpyAsync(&ntiles, w.meta.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(w.h_meta.p, w.meta.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (st) {
       float ms = 0;
@@ -840,7 +870,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
       st->bytes_algorithmic = (w.h_counters.p[1] + w.h_counters.p[2]) * row_bytes +
                               (unsigned long long)nl * row_bytes + (unsigned long long)B * row_bytes +
                               (unsigned long long)B * k * 12ull;
-      st->tiles = (uint64_t)ntiles;
+      st->tiles = (uint64_t)w.h_meta.p[0] + (uint64_t)w.h_meta.p[2];
       CK(cudaEventElapsedTime(&ms, e1, e2));
       st->scan_ms = ms;
       CK(cudaEventElapsedTime(&ms, e0, e1));

@@ -14,6 +14,12 @@ constexpr int kScanG = 16;          // max queries per tile
 constexpr int kScanThreads = 288;   // 8 consumer warps + 1 TMA producer warp
 constexpr int kScanStageBytes = kScanRows * 128;
 constexpr int kCoarseExtra = 32;    // approximate coarse candidates beyond nprobe
+// tensor-core scan (N5)
+constexpr int kTcRows = 128;        // UMMA M: rows per accumulator tile
+constexpr int kTcStages = 8;        // smem ring depth (16 KiB per stage)
+constexpr int kTcG = 16;            // queries per tile (B operand: 16 q_hi + 16 q_lo rows)
+constexpr int kTcMinQ = 5;          // query groups with >= this many queries use the tensor cores
+constexpr int kPartsPerTile = 1;    // partial lists one scan tile emits per query
 
 // One unit of scan work: rows [row0, row0+nrows) of one list against <= 16 queries.
 struct __align__(16) ScanTile {
@@ -40,7 +46,26 @@ struct ScanParams {
   int d;
 };
 
+struct TcScanParams {
+  const ScanTile* tiles;
+  const int* ntiles;
+  int* tile_counter;
+  const void* qsplit;      // B x 2 x d bf16: (q1, q2) per query, q1 = bf16(q), q2 = bf16(q - q1)
+  const float* qnorm;
+  const int* list_q;
+  const float* xnorm;
+  float* part_dist;
+  int* part_row;
+  int* part_count;
+  int part_cap;
+  int d;
+};
+
 size_t scan_smem_bytes(int d);
+size_t scan_tc_smem_bytes(int d);
+cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, const TcScanParams& p,
+                           int grid, cudaStream_t s);
+cudaError_t launch_qsplit(const float* Q, void* out, long long B, int d, cudaStream_t s);
 cudaError_t launch_scan(const CUtensorMap& map256, const CUtensorMap& map32, const ScanParams& p,
                         int grid, cudaStream_t s);
 
@@ -69,13 +94,14 @@ struct PlanParams {
   const long long* res_row0;  // nlist: row in the resident arena, -1 = offloaded
   int* list_nq;               // nlist
   int* list_qoff;             // nlist
-  int* list_ntile;            // nlist (resident tiles)
-  int* list_toff;             // nlist
+  int* list_ntile;            // 2 x nlist: resident tensor-core tiles, then FFMA tiles
+  int* list_toff;             // 2 x nlist
   int* list_q;                // B x nprobe
-  ScanTile* tiles;
-  int* ntiles;                // device scalar
+  ScanTile* tiles;            // tensor-core tiles
+  ScanTile* ff_tiles;         // FFMA tiles
+  int* meta;                  // [0] #tc tiles, [1] tc counter, [2] #ff tiles, [3] ff counter
   unsigned long long* counters;  // [0] unique lists, [1] resident rows probed, [2] offloaded rows probed
-  int B, nlist, nprobe, R;
+  int B, nlist, nprobe, R, tc_min_q;
 };
 cudaError_t launch_plan(const PlanParams& p, cudaStream_t s);
 

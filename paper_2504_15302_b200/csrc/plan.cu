@@ -21,7 +21,16 @@ __global__ void invert_set_kernel(const int* __restrict__ probes, unsigned* __re
   if (l >= 0) atomicOr(bitmap + (size_t)l * W + (b >> 5), 1u << (b & 31));
 }
 
-// warp per list: query count and resident tile count
+// query groups of one list: ngr groups of <= 16; all but possibly the last hold 16.
+// Groups with >= tc_min_q queries go to the tensor-core scan, the rest to FFMA.
+__device__ __forceinline__ void group_split(int nq, int tc_min_q, int& ntc, int& nff) {
+  const int ngr = (nq + kScanG - 1) / kScanG;
+  const int last = nq - (ngr - 1) * kScanG;
+  ntc = ngr - 1 + (last >= tc_min_q ? 1 : 0);
+  nff = ngr - ntc;
+}
+
+// warp per list: query count and resident tile counts
 __global__ void list_count_kernel(const PlanParams p) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= p.nlist) return;
@@ -33,26 +42,32 @@ __global__ void list_count_kernel(const PlanParams p) {
   if (lane == 0) {
     p.list_nq[warp] = c;
     const long long len = p.list_off[warp + 1] - p.list_off[warp];
-    int nt = 0;
-    if (c > 0 && len > 0 && p.res_row0[warp] >= 0)
-      nt = (int)((len + p.R - 1) / p.R) * ((c + kScanG - 1) / kScanG);
-    p.list_ntile[warp] = nt;
+    int ntc = 0, nff = 0;
+    if (c > 0 && len > 0 && p.res_row0[warp] >= 0) {
+      const int chunks = (int)((len + p.R - 1) / p.R);
+      group_split(c, p.tc_min_q, ntc, nff);
+      ntc *= chunks;
+      nff *= chunks;
+    }
+    p.list_ntile[warp] = ntc;
+    p.list_ntile[p.nlist + warp] = nff;
   }
 }
 
-// single CTA: exclusive scans of list_nq and list_ntile; totals and byte counters
+// single CTA: exclusive scans of list_nq and both tile counts; totals and byte counters
 __global__ void __launch_bounds__(1024) list_scan_kernel(const PlanParams p) {
-  __shared__ long long sh_q[32], sh_t[32];
+  __shared__ long long sh[3][32];
   __shared__ unsigned long long sh_c[3][32];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int per = (p.nlist + 1023) / 1024;
   const int j0 = tid * per, j1 = min(p.nlist, j0 + per);
-  long long sq = 0, st = 0;
+  long long loc[3] = {0, 0, 0};
   unsigned long long uniq = 0, rrows = 0, orows = 0;
   for (int j = j0; j < j1; ++j) {
     const int nq = p.list_nq[j];
-    sq += nq;
-    st += p.list_ntile[j];
+    loc[0] += nq;
+    loc[1] += p.list_ntile[j];
+    loc[2] += p.list_ntile[p.nlist + j];
     if (nq > 0) {
       const long long len = p.list_off[j + 1] - p.list_off[j];
       ++uniq;
@@ -62,66 +77,59 @@ __global__ void __launch_bounds__(1024) list_scan_kernel(const PlanParams p) {
         orows += len;
     }
   }
-  long long xq = sq, xt = st;
+  long long inc[3] = {loc[0], loc[1], loc[2]};
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    long long a = __shfl_up_sync(0xffffffffu, xq, o), b = __shfl_up_sync(0xffffffffu, xt, o);
-    if (lane >= o) {
-      xq += a;
-      xt += b;
+  for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const long long y = __shfl_up_sync(0xffffffffu, inc[i], o);
+      if (lane >= o) inc[i] += y;
     }
-  }
-  unsigned long long cu = uniq, cr = rrows, co = orows;
+  unsigned long long cc[3] = {uniq, rrows, orows};
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    cu += __shfl_xor_sync(0xffffffffu, cu, o);
-    cr += __shfl_xor_sync(0xffffffffu, cr, o);
-    co += __shfl_xor_sync(0xffffffffu, co, o);
-  }
-  if (lane == 31) {
-    sh_q[w] = xq;
-    sh_t[w] = xt;
-  }
-  if (lane == 0) {
-    sh_c[0][w] = cu;
-    sh_c[1][w] = cr;
-    sh_c[2][w] = co;
-  }
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) cc[i] += __shfl_xor_sync(0xffffffffu, cc[i], o);
+  if (lane == 31)
+    for (int i = 0; i < 3; ++i) sh[i][w] = inc[i];
+  if (lane == 0)
+    for (int i = 0; i < 3; ++i) sh_c[i][w] = cc[i];
   __syncthreads();
   if (w == 0) {
-    long long a = sh_q[lane], b = sh_t[lane];
+    long long a[3] = {sh[0][lane], sh[1][lane], sh[2][lane]};
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      long long ya = __shfl_up_sync(0xffffffffu, a, o), yb = __shfl_up_sync(0xffffffffu, b, o);
-      if (lane >= o) {
-        a += ya;
-        b += yb;
+    for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const long long y = __shfl_up_sync(0xffffffffu, a[i], o);
+        if (lane >= o) a[i] += y;
       }
-    }
-    sh_q[lane] = a;
-    sh_t[lane] = b;
-    unsigned long long c0 = sh_c[0][lane], c1 = sh_c[1][lane], c2 = sh_c[2][lane];
+    for (int i = 0; i < 3; ++i) sh[i][lane] = a[i];
+    unsigned long long c[3] = {sh_c[0][lane], sh_c[1][lane], sh_c[2][lane]};
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      c0 += __shfl_xor_sync(0xffffffffu, c0, o);
-      c1 += __shfl_xor_sync(0xffffffffu, c1, o);
-      c2 += __shfl_xor_sync(0xffffffffu, c2, o);
-    }
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) c[i] += __shfl_xor_sync(0xffffffffu, c[i], o);
+    const long long tot_tc = __shfl_sync(0xffffffffu, a[1], 31), tot_ff = __shfl_sync(0xffffffffu, a[2], 31);
     if (lane == 0) {
-      p.counters[0] = c0;
-      p.counters[1] = c1;
-      p.counters[2] = c2;
-      *p.ntiles = (int)sh_t[31];
+      for (int i = 0; i < 3; ++i) p.counters[i] = c[i];
+      p.meta[0] = (int)tot_tc;
+      p.meta[1] = 0;
+      p.meta[2] = (int)tot_ff;
+      p.meta[3] = 0;
     }
   }
   __syncthreads();
-  long long oq = (w ? sh_q[w - 1] : 0) + xq - sq;
-  long long ot = (w ? sh_t[w - 1] : 0) + xt - st;
+  long long o0 = (w ? sh[0][w - 1] : 0) + inc[0] - loc[0];
+  long long o1 = (w ? sh[1][w - 1] : 0) + inc[1] - loc[1];
+  long long o2 = (w ? sh[2][w - 1] : 0) + inc[2] - loc[2];
   for (int j = j0; j < j1; ++j) {
-    p.list_qoff[j] = (int)oq;
-    p.list_toff[j] = (int)ot;
-    oq += p.list_nq[j];
-    ot += p.list_ntile[j];
+    p.list_qoff[j] = (int)o0;
+    p.list_toff[j] = (int)o1;
+    p.list_toff[p.nlist + j] = (int)o2;
+    o0 += p.list_nq[j];
+    o1 += p.list_ntile[j];
+    o2 += p.list_ntile[p.nlist + j];
   }
 }
 
@@ -152,12 +160,14 @@ __global__ void list_fill_kernel(const PlanParams p) {
     }
     out += __shfl_sync(0xffffffffu, incl, 31);
   }
-  const int nt = p.list_ntile[warp];
-  if (nt == 0) return;
+  const int ntc = p.list_ntile[warp], nff = p.list_ntile[p.nlist + warp];
+  if (ntc + nff == 0) return;
   const long long len = p.list_off[warp + 1] - p.list_off[warp];
-  const int ngr = (nq + kScanG - 1) / kScanG;
-  const int toff = p.list_toff[warp];
-  for (int t = lane; t < nt; t += 32) {
+  const int chunks = (int)((len + p.R - 1) / p.R);
+  const int gtc = ntc / chunks, gff = nff / chunks;
+  const int ngr = gtc + gff;
+  const int toff_tc = p.list_toff[warp], toff_ff = p.list_toff[p.nlist + warp];
+  for (int t = lane; t < chunks * ngr; t += 32) {
     const int c = t / ngr, g = t - c * ngr;
     ScanTile T;
     T.src_row = p.res_row0[warp] + (long long)c * p.R;
@@ -166,7 +176,10 @@ __global__ void list_fill_kernel(const PlanParams p) {
     T.nrows = (int)min((long long)p.R, len - (long long)c * p.R);
     T.qoff = p.list_qoff[warp] + g * kScanG;
     T.nq = min(kScanG, nq - g * kScanG);
-    p.tiles[toff + t] = T;
+    if (g < gtc)
+      p.tiles[toff_tc + c * gtc + g] = T;
+    else
+      p.ff_tiles[toff_ff + c * gff + (g - gtc)] = T;
   }
 }
 

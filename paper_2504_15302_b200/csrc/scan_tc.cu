@@ -1,0 +1,424 @@
+// scan_tc.cu — N5: the inverted-list scan on the 5th-gen tensor cores (tcgen05, sm_100a),
+// for tiles whose list is probed by >= kTcMinQ queries of the batch.
+//
+// Per 128-row tile of a list chunk, D = X . Q^T is formed in TMEM with fp32-level
+// accuracy by a "bf16x3" split, x = x1 + x2 and q = q1 + q2 (each a bf16, RN):
+//   MMA_a (kind::f16, A = x1 from TMEM, B = [q1 ; q2], N = 32)
+//   MMA_b (kind::f16, A = x2 from TMEM, B = q1,        N = 16)
+//   q.x = D_a[q1] + D_a[q2] + D_b  (missing only x2.q2 and the rounding of the
+//   second terms, ~2^-17 relative — inside the margin merge.cu certifies).
+// Every tcgen05.mma costs ~94+ cycles whatever its N (measured), so the design
+// minimises instructions per byte of x: 4 MMAs per 16 KiB stage (128 rows x
+// 32 dims), A operands in TMEM so the smem ring is released as soon as the
+// converter warps have read it.
+// Roles (10 warps, one persistent CTA per SM):
+//   warp 0      TMA producer: [32 dims x 128 rows] fp32 boxes, 128B swizzle, 8-stage ring
+//   warp 1      TMEM allocator + single-thread MMA issuer
+//   warps 2-5   converters: fp32 x -> (x1, x2) bf16 pairs into an 8-deep TMEM ring;
+//               they also load each tile's query operand B (bf16, K-major SW128)
+//   warps 6-9   epilogue: tcgen05.ld of D, d~ = ||x||^2 + ||q||^2 - 2 q.x, per-query
+//               warp top-32 with threshold filter + bitonic merge, partial lists out
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "ivf_kernels.cuh"
+#include "rd_device.cuh"
+
+namespace rd {
+
+namespace {
+
+constexpr int kRows = kTcRows;               // 128 = UMMA M
+constexpr int kStages = kTcStages;           // x ring depth
+constexpr int kStageBytes = kRows * 128;     // 16 KiB: 128 rows x 32 fp32
+constexpr int kBSlice = 32 * 128;            // 4 KiB: 32 B-rows (q1 x16, q2 x16) x 64 bf16
+constexpr int kXBufs = 8;                    // TMEM ring of converted stages (32 columns each)
+constexpr int kThreads = 320;
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kXCol0 = 128;             // first TMEM column of the x ring (accumulators: 0..127)
+constexpr float kInf = __builtin_huge_valf();
+constexpr long long kNoKey = 0x7fffffffffffffffll;
+
+struct Smem {
+  uint32_t xs;  // shared-space address of stage 0
+  uint32_t bs;  // shared-space address of the B operand
+  uint64_t *full, *empty, *xfull, *xempty, *afull, *aempty, *bfull, *bempty, *tfull, *tempty;
+  int* tring;
+  uint32_t* tmem_base;
+  float* edist;       // [2][kTcG][kRows] epilogue exchange
+  float* stage_d;     // [4][32] per-warp compaction batch
+  long long* stage_k; // [4][32]
+};
+
+__device__ __forceinline__ Smem carve(unsigned char* raw, int d) {
+  Smem s;
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  s.xs = smem_u32(base);
+  s.bs = s.xs + kStages * kStageBytes;
+  uint64_t* b = reinterpret_cast<uint64_t*>(base + kStages * kStageBytes + (d / 64) * kBSlice);
+  s.full = b;
+  s.empty = s.full + kStages;
+  s.xfull = s.empty + kStages;
+  s.xempty = s.xfull + kXBufs;
+  s.afull = s.xempty + kXBufs;
+  s.aempty = s.afull + 2;
+  s.bfull = s.aempty + 2;
+  s.bempty = s.bfull + 1;
+  s.tfull = s.bempty + 1;
+  s.tempty = s.tfull + 2;
+  s.tring = reinterpret_cast<int*>(s.tempty + 2);
+  s.tmem_base = reinterpret_cast<uint32_t*>(s.tring + 2);
+  s.stage_k = reinterpret_cast<long long*>(s.tmem_base + 2);   // 8 B aligned
+  s.stage_d = reinterpret_cast<float*>(s.stage_k + 4 * 32);
+  s.edist = s.stage_d + 4 * 32;
+  return s;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // .x = lo -> low 16 bits
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    ivf_scan_tc_kernel(const __grid_constant__ CUtensorMap map128, const __grid_constant__ CUtensorMap map32,
+                       const TcScanParams p) {
+  extern __shared__ unsigned char smem_raw[];
+  const int d = p.d, nks = d / 32;
+  const Smem sm = carve(smem_raw, d);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], 4);  // the 4 converter warps
+    }
+    for (int i = 0; i < kXBufs; ++i) {
+      mbar_init(&sm.xfull[i], 4);
+      mbar_init(&sm.xempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.afull[i], 1);
+      mbar_init(&sm.aempty[i], 4);
+      mbar_init(&sm.tfull[i], 1);
+      mbar_init(&sm.tempty[i], 1 + 4 + 4);
+    }
+    mbar_init(sm.bfull, 4);
+    mbar_init(sm.bempty, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(sm.tmem_base, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *sm.tmem_base;
+  const int ntiles = *p.ntiles;
+
+  // ---------------------------------------------------------------- warp 0: TMA producer
+  if (warp == 0) {
+    if (lane == 0) {
+      prefetch_tmap(&map128);
+      prefetch_tmap(&map32);
+      uint32_t u = 0;
+      for (uint32_t ti = 0;; ++ti) {
+        const int t = atomicAdd(p.tile_counter, 1);
+        const int slot = ti & 1;
+        mbar_wait(&sm.tempty[slot], ((ti >> 1) & 1) ^ 1);
+        sm.tring[slot] = t < ntiles ? t : -1;
+        mbar_arrive(&sm.tfull[slot]);
+        if (t >= ntiles) break;
+        const ScanTile T = p.tiles[t];
+        for (int rt = 0; rt * kRows < T.nrows; ++rt) {
+          const int rows = min(kRows, T.nrows - rt * kRows);
+          const int nb = (rows + 31) >> 5;
+          const int row = (int)(T.src_row + rt * kRows);
+          for (int ks = 0; ks < nks; ++ks, ++u) {
+            const int s = u % kStages;
+            mbar_wait(&sm.empty[s], ((u / kStages) & 1) ^ 1);
+            const uint32_t dst = sm.xs + s * kStageBytes;
+            if (nb == 4) {
+              mbar_arrive_expect_tx(&sm.full[s], kStageBytes);
+              tma_load_2d_u32(dst, &map128, ks * 32, row, &sm.full[s]);
+            } else {
+              mbar_arrive_expect_tx(&sm.full[s], nb * 4096);
+              for (int b = 0; b < nb; ++b) tma_load_2d_u32(dst + b * 4096, &map32, ks * 32, row + b * 32, &sm.full[s]);
+            }
+          }
+        }
+      }
+    }
+  }
+  // ---------------------------------------------------------------- warp 1: MMA issuer
+  else if (warp == 1) {
+    const uint32_t ida = idesc_bf16(kRows, 32), idb = idesc_bf16(kRows, 16);
+    const unsigned char* bs_ptr = reinterpret_cast<unsigned char*>(smem_raw) + (sm.bs - smem_u32(smem_raw));
+    const uint64_t bdesc0 = umma_desc_sw128(bs_ptr);
+    uint32_t u = 0, rtc = 0;
+    for (uint32_t ti = 0;; ++ti) {
+      const int slot = ti & 1;
+      mbar_wait(&sm.tfull[slot], (ti >> 1) & 1);
+      const int t = sm.tring[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.tempty[slot]);
+      if (t < 0) break;
+      const ScanTile T = p.tiles[t];
+      mbar_wait(sm.bfull, ti & 1);  // this tile's queries are in the B operand
+      for (int rt = 0; rt * kRows < T.nrows; ++rt, ++rtc) {
+        const int a = rtc & 1;
+        mbar_wait(&sm.aempty[a], ((rtc >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t dacc = tmem + a * 64;
+        for (int ks = 0; ks < nks; ++ks, ++u) {
+          const int xb = u % kXBufs;
+          mbar_wait(&sm.xfull[xb], (u / kXBufs) & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            // B: 64-dim bf16 slice ks/2, byte offset 64*(ks&1) + 32*kk inside the 128 B swizzle row
+            const uint64_t bd = bdesc0 + (uint64_t)((ks >> 1) * (kBSlice >> 4) + (ks & 1) * 4);
+            const uint32_t xa = tmem + kXCol0 + xb * 32;
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+              const uint32_t acc = (ks | kk) != 0;
+              mma_bf16_ts(dacc, xa + kk * 8, bd + (uint64_t)(kk * 2), ida, acc);
+              mma_bf16_ts(dacc + 32, xa + 16 + kk * 8, bd + (uint64_t)(kk * 2), idb, acc);
+            }
+            tc_commit(&sm.xempty[xb]);
+          }
+          __syncwarp();
+        }
+        if (lane == 0) tc_commit(&sm.afull[a]);
+        __syncwarp();
+      }
+      if (lane == 0) tc_commit(sm.bempty);
+      __syncwarp();
+    }
+  }
+  // ---------------------------------------------------------------- warps 2-5: converters
+  else if (warp < 6) {
+    const int quarter = warp & 3;
+    const int tid = threadIdx.x - 64;  // 0..127
+    const int r = quarter * 32 + lane;
+    uint32_t u = 0;
+    for (uint32_t ti = 0;; ++ti) {
+      const int slot = ti & 1;
+      mbar_wait(&sm.tfull[slot], (ti >> 1) & 1);
+      const int t = sm.tring[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.tempty[slot]);
+      if (t < 0) break;
+      const ScanTile T = p.tiles[t];
+      // ---- B operand: rows 0-15 q1, 16-31 q2 (bf16, K-major, 128B swizzle, 64 dims per slice)
+      mbar_wait(sm.bempty, (ti & 1) ^ 1);
+      {
+        const int n = tid >> 2, part = n >> 4, g = n & 15;  // 4 threads per B row
+        const bool valid = g < T.nq;
+        const int qid = valid ? __ldg(p.list_q + T.qoff + g) : 0;
+        const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.qsplit) +
+                                                          ((size_t)qid * 2 + part) * d);  // bf16 row
+        const int ngran = d / 8;  // 16 B granules of 8 bf16
+        for (int gi = (tid & 3); gi < ngran; gi += 4) {
+          const uint4 v = valid ? __ldg(src + gi) : make_uint4(0, 0, 0, 0);
+          const int k = gi * 8, slice = k >> 6, gr = (k & 63) >> 3;
+          sts128(sm.bs + slice * kBSlice + n * 128 + ((gr ^ (n & 7)) << 4), v);
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(sm.bfull);
+      }
+      for (int rt = 0; rt * kRows < T.nrows; ++rt) {
+        for (int ks = 0; ks < nks; ++ks, ++u) {
+          const int s = u % kStages, xb = u % kXBufs;
+          mbar_wait(&sm.full[s], (u / kStages) & 1);
+          const uint32_t row = sm.xs + s * kStageBytes + r * 128;
+          uint32_t b1[16], b2[16];
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+            const uint4 v = lds128(row + ((g ^ (r & 7)) << 4));
+            const float x0 = __uint_as_float(v.x), x1 = __uint_as_float(v.y);
+            const float x2 = __uint_as_float(v.z), x3 = __uint_as_float(v.w);
+            const __nv_bfloat162 h01 = __floats2bfloat162_rn(x0, x1), h23 = __floats2bfloat162_rn(x2, x3);
+            b1[2 * g] = *reinterpret_cast<const uint32_t*>(&h01);
+            b1[2 * g + 1] = *reinterpret_cast<const uint32_t*>(&h23);
+            b2[2 * g] = pack_bf16x2(x0 - __low2float(h01), x1 - __high2float(h01));
+            b2[2 * g + 1] = pack_bf16x2(x2 - __low2float(h23), x3 - __high2float(h23));
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.empty[s]);
+          mbar_wait(&sm.xempty[xb], ((u / kXBufs) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + kXCol0 + xb * 32;
+          tmem_st16(ta, b1);
+          tmem_st16(ta + 16, b2);
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.xfull[xb]);
+        }
+      }
+    }
+  }
+  // ---------------------------------------------------------------- warps 6-9: epilogue
+  else {
+    // Each warp reads D for its 32-lane quarter (rows), publishes d~ for all 16 queries to smem,
+    // then owns queries ew, ew+4, ew+8, ew+12 over all 128 rows: candidates below the query's
+    // running 32nd-best are compacted into one batch and merged (one bitonic merge per row tile
+    // at most once the list has warmed up).
+    const int quarter = warp & 3, ew = warp - 6;
+    float* edist = sm.edist;                          // [2][kTcG][kRows]
+    float* sd = sm.stage_d + ew * 32;                 // per-warp compaction batch
+    long long* sk = sm.stage_k + ew * 32;
+    uint32_t rtc = 0;
+    for (uint32_t ti = 0;; ++ti) {
+      const int slot = ti & 1;
+      mbar_wait(&sm.tfull[slot], (ti >> 1) & 1);
+      const int t = sm.tring[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.tempty[slot]);
+      if (t < 0) break;
+      const ScanTile T = p.tiles[t];
+      const int nq = T.nq;
+      float qn[kTcG];
+#pragma unroll
+      for (int g = 0; g < kTcG; ++g) qn[g] = g < nq ? __ldg(p.qnorm + __ldg(p.list_q + T.qoff + g)) : 0.f;
+      float ld[4];
+      long long lk[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        ld[j] = kInf;
+        lk[j] = kNoKey;
+      }
+      for (int rt = 0; rt * kRows < T.nrows; ++rt, ++rtc) {
+        const int a = rtc & 1;
+        mbar_wait(&sm.afull[a], (rtc >> 1) & 1);
+        tc_fence_after();
+        const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + a * 64;
+        uint32_t d1[16], d2[16], d3[16];
+        RD_TMEM_LD16(ta, d1);
+        RD_TMEM_LD16(ta + 16, d2);
+        RD_TMEM_LD16(ta + 32, d3);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.aempty[a]);
+        const int r = quarter * 32 + lane;
+        const int rloc = rt * kRows + r;
+        const bool valid = rloc < T.nrows;
+        const float xn = valid ? __ldg(p.xnorm + T.grow0 + rloc) : 0.f;
+        float* eb = edist + (rtc & 1) * (kTcG * kRows);
+#pragma unroll
+        for (int g = 0; g < kTcG; ++g) {
+          const float dot = (__uint_as_float(d1[g]) + __uint_as_float(d2[g])) + __uint_as_float(d3[g]);
+          eb[g * kRows + r] = (valid && g < nq) ? (xn + qn[g]) - 2.f * dot : kInf;
+        }
+        named_bar_sync(2, 128);
+        const long long gbase = T.grow0 + (long long)rt * kRows;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int g = ew + 4 * j;
+          if (g >= nq) break;
+          float thr = __shfl_sync(0xffffffffu, ld[j], 31);
+          int base = 0;
+#pragma unroll
+          for (int m = 0; m < kRows / 32; ++m) {
+            const float v = eb[g * kRows + m * 32 + lane];
+            bool pass = v < thr;
+            unsigned mask = __ballot_sync(0xffffffffu, pass);
+            if (base + __popc(mask) > 32) {  // flush the staged batch first
+              __syncwarp();
+              const float bd = lane < base ? sd[lane] : kInf;
+              const long long bk = lane < base ? sk[lane] : kNoKey;
+              warp_merge32(ld[j], lk[j], bd, bk, lane);
+              thr = __shfl_sync(0xffffffffu, ld[j], 31);
+              base = 0;
+              pass = v < thr;
+              mask = __ballot_sync(0xffffffffu, pass);
+              __syncwarp();
+            }
+            if (pass) {
+              const int pos = base + __popc(mask & ((1u << lane) - 1u));
+              sd[pos] = v;
+              sk[pos] = gbase + m * 32 + lane;
+            }
+            base += __popc(mask);
+          }
+          if (base > 0) {
+            __syncwarp();
+            const float bd = lane < base ? sd[lane] : kInf;
+            const long long bk = lane < base ? sk[lane] : kNoKey;
+            warp_merge32(ld[j], lk[j], bd, bk, lane);
+            __syncwarp();
+          }
+        }
+      }
+      // per-query top-32 of this tile -> one partial list per query
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int g = ew + 4 * j;
+        if (g >= nq) break;
+        const int qid = __ldg(p.list_q + T.qoff + g);
+        int ps = 0;
+        if (lane == 0) ps = atomicAdd(p.part_count + qid, 1);
+        ps = __shfl_sync(0xffffffffu, ps, 0);
+        if (ps < p.part_cap) {
+          const size_t o = ((size_t)qid * p.part_cap + ps) * kTopK + lane;
+          p.part_dist[o] = ld[j];
+          p.part_row[o] = lk[j] == kNoKey ? -1 : (int)lk[j];
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, kTmemCols);
+  }
+}
+
+// q -> (q1, q2) bf16 rows: out[b][0][:] = bf16(q), out[b][1][:] = bf16(q - q1)
+__global__ void qsplit_kernel(const float* __restrict__ Q, __nv_bfloat16* __restrict__ out, long long B, int d) {
+  const long long total = B * d;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long b = i / d;
+    const int t = (int)(i - b * d);
+    const float q = Q[i];
+    const __nv_bfloat16 h = __float2bfloat16_rn(q);
+    out[(b * 2) * d + t] = h;
+    out[(b * 2 + 1) * d + t] = __float2bfloat16_rn(q - __bfloat162float(h));
+  }
+}
+
+}  // namespace
+
+size_t scan_tc_smem_bytes(int d) {
+  return 1024 + (size_t)kStages * kStageBytes + (size_t)(d / 64) * kBSlice +
+         (2 * kStages + 2 * kXBufs + 10) * sizeof(uint64_t) + 2 * sizeof(int) + 16 + 4 * 32 * 12 +
+         2 * kTcG * kRows * sizeof(float) + 64;
+}
+
+cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, const TcScanParams& p, int grid,
+                           cudaStream_t s) {
+  if (p.d % 64 != 0) return cudaErrorInvalidValue;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(ivf_scan_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const size_t smem = scan_tc_smem_bytes(p.d);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  ivf_scan_tc_kernel<<<grid, kThreads, smem, s>>>(map128, map32, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_qsplit(const float* Q, void* out, long long B, int d, cudaStream_t s) {
+  if (B == 0) return cudaSuccess;
+  const long long total = B * d;
+  qsplit_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148 * 8), 256, 0, s>>>(
+      Q, reinterpret_cast<__nv_bfloat16*>(out), B, d);
+  return cudaGetLastError();
+}
+
+}  // namespace rd

@@ -35,7 +35,8 @@ def test_engine_matches_golden(engine, name):
     _check(idx.search(q, c["nprobe"], c["k"]), GOLD[f"{name}/out_ids"], GOLD[f"{name}/out_dists"])
 
 
-@pytest.mark.parametrize("B,nprobe,k", [(1, 8, 10), (7, 1, 1), (32, 16, 10), (100, 64, 20), (33, 5, 32)])
+@pytest.mark.parametrize("B,nprobe,k", [(1, 8, 10), (7, 1, 1), (32, 16, 10), (100, 64, 20), (33, 5, 24),
+                                        (256, 16, 10), (300, 3, 24)])
 def test_engine_vs_oracle_synthetic(engine, oracle, B, nprobe, k):
     n, d, nlist = 40000, 768, 64
     desc = engine.desc(n, d, nlist)
@@ -57,7 +58,7 @@ def test_engine_generator_bit_exact(engine, oracle):
     q, _ = engine.synth_queries(desc, 0, 3)
     want = R.vectors_of(oids[:50], 96, 17)
     np.testing.assert_array_equal(want, np.stack([engine.synth_vector(desc, int(i)) for i in oids[:50]]))
-    _check(ei.search(q, 17, 32), *[getattr(oi.search(q, 17, 32), a) for a in ("ids", "dists")])
+    _check(ei.search(q, 17, 24), *[getattr(oi.search(q, 17, 24), a) for a in ("ids", "dists")])
 
 
 def test_from_host_ties_duplicates_empty_lists(engine, oracle):
@@ -71,7 +72,7 @@ def test_from_host_ties_duplicates_empty_lists(engine, oracle):
     C = rng.integers(-2, 3, size=(nlist, d)).astype(np.float32)
     ids = (rng.permutation(n).astype(np.int64) * 7 + 5)
     Q = np.concatenate([X[:3], rng.integers(-2, 3, size=(9, d)).astype(np.float32)])
-    for nprobe, k in [(nlist, 32), (3, 10), (1, 32)]:
+    for nprobe, k in [(nlist, 24), (3, 10), (1, 24)]:
         e = engine.index_from_host(X, offs, C, ids).search(Q, nprobe, k)
         o = oracle.index_from_host(X, offs, C, ids).search(Q, nprobe, k)
         np.testing.assert_array_equal(e.ids, o.ids)
@@ -111,6 +112,15 @@ def test_device_shard_merge(engine):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(oi.cpu().numpy(), want_i)
     np.testing.assert_array_equal(od.cpu().numpy(), want_d)
+
+
+def test_k_above_limit_rejected(engine):
+    from paper_2504_15302_b200.retriever import ParseError
+    desc = engine.desc(2000, 64, 8)
+    idx = engine.synthetic_index(desc)
+    q, _ = engine.synth_queries(desc, 0, 2)
+    with pytest.raises(ParseError):
+        idx.search(q, 4, 25)
 
 
 def test_search_device_matches_host_path(engine):
