@@ -225,7 +225,9 @@ struct rd_index {
     DBuf<rd::ScanTile> tiles, ff_tiles, off_tiles;
     DBuf<unsigned long long> counters;
     DBuf<float> part_dist;
-    DBuf<long long> ids;
+    DBuf<long long> ids, fb_id;
+    DBuf<int> fail_list;
+    DBuf<float> fb_dist;
     HBuf<float> hq, hd;
     HBuf<long long> hi;
     HBuf<int> h_nq, h_qoff, h_meta;
@@ -847,10 +849,17 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     CK(cudaStreamWaitEvent(s, e_off, 0));
   }
 
+  w.fail_list.ensure(B);
+  w.fb_dist.ensure((size_t)B * nprobe * rd::kTopK);
+  w.fb_id.ensure((size_t)B * nprobe * rd::kTopK);
   rd::MergeParams mp{w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d_q, w.qnorm.p, h->d_list_off.p,
-                     h->d_list_base.p, h->d_ids.p, nl, d, k, h->xmax, d_ids, d_dists, w.fails.p + 1, (int)B};
+                     h->d_list_base.p, h->d_ids.p, nl, d, k, h->xmax, d_ids, d_dists, w.fails.p + 1,
+                     w.fail_list.p, (int)B};
   CK(rd::launch_merge(mp, s));
-  launches += 1;
+  rd::FallbackParams fp{w.fail_list.p, w.fails.p + 1, w.probes.p, nprobe, d_q, h->d_list_off.p, h->d_list_base.p,
+                        h->d_ids.p, nl, d, k, w.fb_dist.p, w.fb_id.p, d_ids, d_dists};
+  CK(rd::launch_fallback(fp, h->num_sms, s));
+  launches += 3;
   CK(cudaEventRecord(te[3], s));
   if (st) {
     std::memset(st, 0, sizeof *st);

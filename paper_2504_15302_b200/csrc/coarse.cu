@@ -121,22 +121,11 @@ __device__ int block_excl_scan(int v, int* sh, int* total) {
 constexpr int kSelThreads = 256;
 constexpr int kSelMaxCand = 512;
 
-// dynamic smem: keys[nlist] (u32)
-__global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const SelectParams p) {
-  extern __shared__ uint32_t keys[];
-  __shared__ int hist[2048];
-  __shared__ int scan_sh[8];
-  __shared__ int cand[kSelMaxCand];
-  __shared__ float cdist[kSelMaxCand];
-  __shared__ uint32_t sel_prefix, sel_k;
-  const int b = blockIdx.x, tid = threadIdx.x;
-  const int nlist = p.nlist;
-  const float* drow = p.Dc + (size_t)b * nlist;
-  for (int j = tid; j < nlist; j += kSelThreads) keys[j] = f2key(drow[j]);
-  const int C = min(nlist, p.nprobe + kCoarseExtra);
-  __syncthreads();
-
-  // radix select of the C-th smallest key: 11 + 11 + 10 bits
+// Selects the C smallest of keys[0..nlist) into cand[0..C): all keys < T plus the
+// first keys == T by index (radix select, 11+11+10 bits, then an ordered compaction).
+__device__ uint32_t select_smallest(const uint32_t* keys, int nlist, int C, int* hist, int* scan_sh, int* cand,
+                                    uint32_t* sel_prefix, uint32_t* sel_k) {
+  const int tid = threadIdx.x;
   uint32_t prefix = 0, mask = 0, kk = (uint32_t)C;
   const int shifts[3] = {21, 10, 0};
   const int widths[3] = {11, 11, 10};
@@ -149,7 +138,6 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
       if ((kv & mask) == prefix) atomicAdd(&hist[(kv >> sh) & (nb - 1)], 1);
     }
     __syncthreads();
-    // each thread owns nb/256 consecutive bins
     const int per = nb / kSelThreads;
     int local = 0;
     for (int i = 0; i < per; ++i) local += hist[tid * per + i];
@@ -160,22 +148,20 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
       for (int i = 0; i < per; ++i) {
         const int h = hist[tid * per + i];
         if (run + h >= (int)kk) {
-          sel_prefix = prefix | ((uint32_t)(tid * per + i) << sh);
-          sel_k = kk - run;
+          *sel_prefix = prefix | ((uint32_t)(tid * per + i) << sh);
+          *sel_k = kk - run;
           break;
         }
         run += h;
       }
     }
     __syncthreads();
-    prefix = sel_prefix;
-    kk = sel_k;
+    prefix = *sel_prefix;
+    kk = *sel_k;
     mask |= (uint32_t)(nb - 1) << sh;
     __syncthreads();
   }
-  const uint32_t T = prefix;  // the C-th smallest key; kk = how many equal-to-T to take
-
-  // ordered compaction: all keys < T, then the first kk keys == T by list id
+  const uint32_t T = prefix;
   const int per = (nlist + kSelThreads - 1) / kSelThreads;
   const int j0 = tid * per, j1 = min(nlist, j0 + per);
   int nlt = 0, neq = 0;
@@ -195,55 +181,90 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
     }
   }
   __syncthreads();
-  const int ncand = tot_lt + (int)kk;  // == C
+  return T;
+}
 
-  // exact rerank of candidates: 8 lanes per candidate
+// dynamic smem: keys[nlist] (u32)
+__global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const SelectParams p) {
+  extern __shared__ uint32_t keys[];
+  __shared__ int hist[2048];
+  __shared__ int scan_sh[8];
+  __shared__ int cand[kSelMaxCand];
+  __shared__ float cdist[kSelMaxCand];
+  __shared__ uint32_t sel_prefix, sel_k;
+  __shared__ int certified;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int nlist = p.nlist;
   const float* q = p.queries + (size_t)b * p.d;
   const int grp = tid >> 3, j8 = tid & 7;
-  for (int c0 = 0; c0 < ncand; c0 += kSelThreads / 8) {
-    const int c = c0 + grp;
-    const int cc = c < ncand ? c : ncand - 1;
-    const float e = exact_l2_group8(q, p.centroids + (size_t)cand[cc] * p.d, p.d, j8);
-    if (c < ncand && j8 == 0) cdist[c] = e;
-  }
-  // pad to power of two and bitonic sort by (dist, list id)
-  int P2 = 1;
-  while (P2 < ncand) P2 <<= 1;
-  for (int c = ncand + tid; c < P2; c += kSelThreads) {
-    cdist[c] = __builtin_huge_valf();
-    cand[c] = 0x7fffffff;
-  }
+  const int np = min(p.nprobe, nlist);
+  const float* drow = p.Dc + (size_t)b * nlist;
+  for (int j = tid; j < nlist; j += kSelThreads) keys[j] = f2key(drow[j]);
   __syncthreads();
-  for (int size = 2; size <= P2; size <<= 1) {
-    for (int jj = size >> 1; jj > 0; jj >>= 1) {
-      for (int i = tid; i < P2; i += kSelThreads) {
-        const int l = i ^ jj;
-        if (l > i) {
-          const bool up = (i & size) == 0;
-          const float di = cdist[i], dl = cdist[l];
-          const int ii = cand[i], il = cand[l];
-          const bool l_less = dl < di || (dl == di && il < ii);
-          if (l_less == up) {
-            cdist[i] = dl;
-            cdist[l] = di;
-            cand[i] = il;
-            cand[l] = ii;
+
+  // attempt 0: C = nprobe + 32 approximate candidates, refined exactly and certified;
+  // attempt 1 (only if uncertified): exact distances to every centroid, C = nprobe.
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const int C = attempt == 0 ? min(nlist, p.nprobe + kCoarseExtra) : np;
+    const uint32_t T = select_smallest(keys, nlist, C, hist, scan_sh, cand, &sel_prefix, &sel_k);
+    for (int c0 = 0; c0 < C; c0 += kSelThreads / 8) {
+      const int c = c0 + grp;
+      const int cc = c < C ? c : C - 1;
+      const float e = exact_l2_group8(q, p.centroids + (size_t)cand[cc] * p.d, p.d, j8);
+      if (c < C && j8 == 0) cdist[c] = e;
+    }
+    int P2 = 1;
+    while (P2 < C) P2 <<= 1;
+    for (int c = C + tid; c < P2; c += kSelThreads) {
+      cdist[c] = __builtin_huge_valf();
+      cand[c] = 0x7fffffff;
+    }
+    __syncthreads();
+    for (int size = 2; size <= P2; size <<= 1) {
+      for (int jj = size >> 1; jj > 0; jj >>= 1) {
+        for (int i = tid; i < P2; i += kSelThreads) {
+          const int l = i ^ jj;
+          if (l > i) {
+            const bool up = (i & size) == 0;
+            const float di = cdist[i], dl = cdist[l];
+            const int ii = cand[i], il = cand[l];
+            const bool l_less = dl < di || (dl == di && il < ii);
+            if (l_less == up) {
+              cdist[i] = dl;
+              cdist[l] = di;
+              cand[i] = il;
+              cand[l] = ii;
+            }
           }
         }
+        __syncthreads();
       }
-      __syncthreads();
     }
+    if (tid == 0) {
+      int ok = 1;
+      if (attempt == 0 && C < nlist) {
+        // error bound of the approximate distance: sequential fp32 FFMA over d terms
+        const float qn = p.qnorm[b];
+        const float u = 5.9604645e-8f;
+        const float eps = 2.f * ((p.d + 4) * u * 2.f * sqrtf(qn) * p.cmax + 8.f * u * (qn + p.cmax * p.cmax)) + 1e-30f;
+        const float lower = key2f(T) + qn - eps;  // lower bound on any excluded exact distance
+        ok = lower > cdist[np - 1];
+      }
+      certified = ok;
+      if (!ok) atomicAdd(p.probe_fail, 1u);
+    }
+    __syncthreads();
+    if (certified) break;
+    // exact keys for every centroid, then select again
+    for (int c0 = 0; c0 < nlist; c0 += kSelThreads / 8) {
+      const int c = c0 + grp;
+      const int cc = c < nlist ? c : nlist - 1;
+      const float e = exact_l2_group8(q, p.centroids + (size_t)cc * p.d, p.d, j8);
+      if (c < nlist && j8 == 0) keys[c] = f2key(e);
+    }
+    __syncthreads();
   }
-  const int np = min(p.nprobe, nlist);
   for (int i = tid; i < p.nprobe; i += kSelThreads) p.probes[(size_t)b * p.nprobe + i] = i < np ? cand[i] : -1;
-  if (tid == 0 && C < nlist) {
-    // error bound of the approximate distance: sequential fp32 FFMA over d terms
-    const float qn = p.qnorm[b];
-    const float u = 5.9604645e-8f;
-    const float eps = 2.f * ((p.d + 4) * u * 2.f * sqrtf(qn) * p.cmax + 8.f * u * (qn + p.cmax * p.cmax)) + 1e-30f;
-    const float lower = key2f(T) + qn - eps;  // lower bound on any excluded exact distance
-    if (!(lower > cdist[np - 1])) atomicAdd(p.probe_fail, 1u);
-  }
 }
 
 }  // namespace

@@ -119,10 +119,30 @@ struct MergeParams {
   float xmax;
   long long* out_ids;              // B x k
   float* out_dists;                // B x k
-  unsigned* margin_fail;
+  unsigned* margin_fail;            // device scalar: number of uncertified queries
+  int* fail_list;                  // B: ids of uncertified queries (exact fallback work list)
   int B;
 };
 cudaError_t launch_merge(const MergeParams& p, cudaStream_t s);
+
+// Exact fallback for uncertified queries: every row of every probed list is compared
+// with the canonical exact distance and ordered by (distance, id).
+struct FallbackParams {
+  const int* fail_list;
+  const unsigned* fail_count;
+  const int* probes;               // B x nprobe
+  int nprobe;
+  const float* queries;
+  const long long* list_off;
+  const float* const* list_base;
+  const long long* ids;
+  int nlist, d, k;
+  float* fb_dist;                  // B x nprobe x 32
+  long long* fb_id;
+  long long* out_ids;
+  float* out_dists;
+};
+cudaError_t launch_fallback(const FallbackParams& p, int num_sms, cudaStream_t s);
 
 // [G][B][k] shard results -> [B][k] (device)
 cudaError_t launch_shard_merge(int G, long long B, int k, const long long* ids, const float* dists,

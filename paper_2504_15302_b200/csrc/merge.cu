@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(256) merge_rerank_kernel(const MergeParams p) 
         const float xm = p.xmax;
         const float eps =
             2.f * ((p.d / 2 + 8) * u * 2.f * sqrtf(qn) * xm + 8.f * u * (qn + xm * xm)) + 1e-30f;
-        if (!(tau - eps > ek)) atomicAdd(p.margin_fail, 1u);
+        if (!(tau - eps > ek)) p.fail_list[atomicAdd(p.margin_fail, 1u)] = b;
       }
     }
   }
@@ -151,7 +151,78 @@ __global__ void shard_merge_kernel(int G, long long B, int k, const long long* _
   }
 }
 
+// persistent: work item w -> (failed query w / nprobe, probe w % nprobe); exact top-32 of the list
+__global__ void __launch_bounds__(256) fallback_scan_kernel(const FallbackParams p) {
+  __shared__ float wd[8][kTopK];
+  __shared__ long long wk[8][kTopK];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long work = (long long)(*p.fail_count) * p.nprobe;
+  for (long long w = blockIdx.x; w < work; w += gridDim.x) {
+    const int q = p.fail_list[w / p.nprobe];
+    const int l = p.probes[(size_t)q * p.nprobe + (w % p.nprobe)];
+    float ld = kInf;
+    long long lk = kNoKey;
+    if (l >= 0) {
+      const long long r0 = p.list_off[l], r1 = p.list_off[l + 1];
+      const float* base = p.list_base[l];
+      const float* qv = p.queries + (size_t)q * p.d;
+      for (long long c = r0 + 32LL * warp; c < r1; c += 32LL * 8) {
+        float mine = kInf;
+        long long myid = kNoKey;
+        for (int pass = 0; pass < 8; ++pass) {
+          const long long row = c + pass * 4 + (lane >> 3);
+          const bool ok = row < r1;
+          const float e = exact_l2_group8_any(qv, ok ? base + (size_t)(row - r0) * p.d : qv, ok ? p.d : 0, lane & 7);
+          const float v = __shfl_sync(0xffffffffu, e, (lane & 3) * 8);
+          if ((lane >> 2) == pass && c + lane < r1) {
+            mine = v;
+            myid = p.ids[c + lane];
+          }
+        }
+        const float thr = __shfl_sync(0xffffffffu, ld, 31);
+        const long long thk = __shfl_sync(0xffffffffu, lk, 31);
+        const bool pass = pair_less(mine, myid, thr, thk);
+        if (__any_sync(0xffffffffu, pass)) warp_merge32(ld, lk, pass ? mine : kInf, pass ? myid : kNoKey, lane);
+      }
+    }
+    wd[warp][lane] = ld;
+    wk[warp][lane] = lk;
+    __syncthreads();
+    if (warp == 0) {
+      for (int o = 1; o < 8; ++o) warp_merge32(ld, lk, wd[o][lane], wk[o][lane], lane);
+      p.fb_dist[w * kTopK + lane] = ld;
+      p.fb_id[w * kTopK + lane] = lk;
+    }
+    __syncthreads();
+  }
+}
+
+// one warp per failed query: merge its nprobe exact partials, overwrite its result row
+__global__ void fallback_merge_kernel(const FallbackParams p) {
+  const int lane = threadIdx.x & 31;
+  const int nf = (int)*p.fail_count;
+  for (int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; f < nf; f += (gridDim.x * blockDim.x) >> 5) {
+    float ld = kInf;
+    long long lk = kNoKey;
+    for (int i = 0; i < p.nprobe; ++i) {
+      const long long w = (long long)f * p.nprobe + i;
+      warp_merge32(ld, lk, p.fb_dist[w * kTopK + lane], p.fb_id[w * kTopK + lane], lane);
+    }
+    const int q = p.fail_list[f];
+    if (lane < p.k) {
+      p.out_ids[(size_t)q * p.k + lane] = lk == kNoKey ? -1 : lk;
+      p.out_dists[(size_t)q * p.k + lane] = lk == kNoKey ? kInf : ld;
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_fallback(const FallbackParams& p, int num_sms, cudaStream_t s) {
+  fallback_scan_kernel<<<num_sms, 256, 0, s>>>(p);
+  fallback_merge_kernel<<<8, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_merge(const MergeParams& p, cudaStream_t s) {
   if (p.B == 0) return cudaSuccess;
