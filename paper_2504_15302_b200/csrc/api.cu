@@ -226,7 +226,7 @@ struct rd_index {
     DBuf<unsigned long long> counters;
     DBuf<float> part_dist;
     DBuf<long long> ids, fb_id;
-    DBuf<int> fail_list;
+    DBuf<int> fail_list, qthr;
     DBuf<float> fb_dist;
     HBuf<float> hq, hd;
     HBuf<long long> hi;
@@ -723,6 +723,8 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   launches += 4;
   CK(cudaEventRecord(e1, s));
   CK(cudaMemsetAsync(w.part_count.p, 0, sizeof(int) * B, s));
+  w.qthr.ensure(B);
+  CK(cudaMemsetAsync(w.qthr.p, 0x7f, sizeof(int) * B, s));  // 0x7f7f7f7f: a huge positive float
   const bool has_off = h->slots > 0;
   if (has_off) {  // fetch the probe histogram for host-side staging decisions
     w.h_nq.ensure(nl);
@@ -732,9 +734,9 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   }
   CK(cudaEventRecord(e_plan, s));
   rd::ScanParams sc{w.ff_tiles.p, w.meta.p + 2, w.meta.p + 3, d_q, w.qnorm.p, w.list_q.p, h->xnorm.p,
-                    w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d};
+                    w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p};
   rd::TcScanParams tc{w.tiles.p, w.meta.p, w.meta.p + 1, w.qsplit.p, w.qnorm.p, w.list_q.p, h->xnorm.p,
-                      w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d};
+                      w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p};
   CK(rd::launch_scan(h->map256, h->map32, sc, h->num_sms, s));
   launches += 1;
   if (d % 64 == 0) {  // the tensor-core path stages 64-dim bf16 query slices; otherwise every tile is FFMA
@@ -771,7 +773,8 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
       for (int l : batches[bi]) {
         const long long len = h->list_off[l + 1] - h->list_off[l];
         const int nq = w.h_nq.p[l];
-        const int ngr = (nq + rd::kScanG - 1) / rd::kScanG;
+        const bool tcl = nq >= h->tc_min_q && d % 64 == 0;
+        const int ngr = tcl ? (nq + rd::kTcG - 1) / rd::kTcG : (nq + rd::kScanG - 1) / rd::kScanG;
         for (long long c = 0; c * pl.R < len; ++c)
           for (int g = 0; g < ngr; ++g) {
             rd::ScanTile T;
@@ -779,12 +782,16 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
             T.grow0 = h->list_off[l] + c * pl.R;
             T.list = l;
             T.nrows = (int)std::min<long long>(pl.R, len - c * pl.R);
-            T.qoff = w.h_qoff.p[l] + g * rd::kScanG;
-            T.nq = std::min(rd::kScanG, nq - g * rd::kScanG);
-            if (T.nq >= h->tc_min_q && d % 64 == 0)
+            if (tcl) {
+              const int q0 = (int)((long long)g * nq / ngr), q1 = (int)((long long)(g + 1) * nq / ngr);
+              T.qoff = w.h_qoff.p[l] + q0;
+              T.nq = q1 - q0;
               tv.push_back(T);
-            else
+            } else {
+              T.qoff = w.h_qoff.p[l] + g * rd::kScanG;
+              T.nq = std::min(rd::kScanG, nq - g * rd::kScanG);
               ff.push_back(T);
+            }
           }
         srow += len;
       }

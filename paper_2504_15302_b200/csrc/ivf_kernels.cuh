@@ -16,8 +16,8 @@ constexpr int kScanStageBytes = kScanRows * 128;
 constexpr int kCoarseExtra = 32;    // approximate coarse candidates beyond nprobe
 // tensor-core scan (N5)
 constexpr int kTcRows = 128;        // UMMA M: rows per accumulator tile
-constexpr int kTcStages = 8;        // smem ring depth (16 KiB per stage)
-constexpr int kTcG = 16;            // queries per tile (B operand: 16 q_hi + 16 q_lo rows)
+constexpr int kTcStages = 6;        // smem ring depth (16 KiB per stage)
+constexpr int kTcG = 32;            // queries per tensor-core tile (B operand: 32 q1 + 32 q2 rows)
 constexpr int kTcMinQ = 5;          // query groups with >= this many queries use the tensor cores
 constexpr int kPartsPerTile = 1;    // partial lists one scan tile emits per query
 
@@ -44,6 +44,7 @@ struct ScanParams {
   int* part_count;         // B
   int part_cap;
   int d;
+  int* qthr;               // B: per-query pruning threshold (f2ord), min over completed tiles' 32nd
 };
 
 struct TcScanParams {
@@ -59,6 +60,7 @@ struct TcScanParams {
   int* part_count;
   int part_cap;
   int d;
+  int* qthr;               // B: per-query pruning threshold (f2ord), min over completed tiles' 32nd
 };
 
 size_t scan_smem_bytes(int d);

@@ -21,13 +21,17 @@ __global__ void invert_set_kernel(const int* __restrict__ probes, unsigned* __re
   if (l >= 0) atomicOr(bitmap + (size_t)l * W + (b >> 5), 1u << (b & 31));
 }
 
-// query groups of one list: ngr groups of <= 16; all but possibly the last hold 16.
-// Groups with >= tc_min_q queries go to the tensor-core scan, the rest to FFMA.
+// Query groups of one list. A list probed by >= tc_min_q queries is scanned once per
+// balanced group of <= kTcG queries on the tensor cores (almost always a single group, so the
+// list's bytes are read once); sparser lists form one FFMA group (<= tc_min_q - 1 <= kScanG).
 __device__ __forceinline__ void group_split(int nq, int tc_min_q, int& ntc, int& nff) {
-  const int ngr = (nq + kScanG - 1) / kScanG;
-  const int last = nq - (ngr - 1) * kScanG;
-  ntc = ngr - 1 + (last >= tc_min_q ? 1 : 0);
-  nff = ngr - ntc;
+  if (nq >= tc_min_q) {
+    ntc = (nq + kTcG - 1) / kTcG;
+    nff = 0;
+  } else {
+    ntc = 0;
+    nff = (nq + kScanG - 1) / kScanG;
+  }
 }
 
 // warp per list: query count and resident tile counts
@@ -174,12 +178,17 @@ __global__ void list_fill_kernel(const PlanParams p) {
     T.grow0 = p.list_off[warp] + (long long)c * p.R;
     T.list = warp;
     T.nrows = (int)min((long long)p.R, len - (long long)c * p.R);
-    T.qoff = p.list_qoff[warp] + g * kScanG;
-    T.nq = min(kScanG, nq - g * kScanG);
-    if (g < gtc)
+    if (g < gtc) {  // balanced tensor-core groups
+      const int q0 = (int)((long long)g * nq / gtc), q1 = (int)((long long)(g + 1) * nq / gtc);
+      T.qoff = p.list_qoff[warp] + q0;
+      T.nq = q1 - q0;
       p.tiles[toff_tc + c * gtc + g] = T;
-    else
-      p.ff_tiles[toff_ff + c * gff + (g - gtc)] = T;
+    } else {
+      const int gg = g - gtc;
+      T.qoff = p.list_qoff[warp] + gg * kScanG;
+      T.nq = min(kScanG, nq - gg * kScanG);
+      p.ff_tiles[toff_ff + c * gff + gg] = T;
+    }
   }
 }
 

@@ -250,6 +250,27 @@ __device__ __forceinline__ void warp_sort32(float& d, long long& k, int lane, bo
     }
   }
 }
+// Insert one candidate (broadcast in all lanes) into the ascending list L.
+__device__ __forceinline__ void warp_insert1(float& ld, long long& lk, float cd, long long ck, int lane) {
+  const unsigned lt = __ballot_sync(0xffffffffu, pair_less(ld, lk, cd, ck));
+  const int pos = __popc(lt);
+  const float ud = __shfl_up_sync(0xffffffffu, ld, 1);
+  const long long uk = __shfl_up_sync(0xffffffffu, lk, 1);
+  if (lane == pos) {
+    ld = cd;
+    lk = ck;
+  } else if (lane > pos) {
+    ld = ud;
+    lk = uk;
+  }
+}
+// orderable int for an atomicMin over non-negative-or-negative floats
+__device__ __forceinline__ int f2ord(float f) {
+  const int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
+
 // L ascending (one per lane) absorbs batch B (one per lane, any order): L becomes
 // the 32 smallest of L ∪ B, ascending.
 __device__ __forceinline__ void warp_merge32(float& ld, long long& lk, float bd, long long bk,

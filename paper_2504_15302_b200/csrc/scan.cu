@@ -175,9 +175,12 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     }
     named_bar_sync(1, 256);
 
-    // running top-32 of the two queries this warp owns (g = warp, warp + 8)
+    // running top-32 of the two queries this warp owns (g = warp, warp + 8), and their
+    // global pruning thresholds (min over completed tiles' 32nd best)
     float ld0 = kInf, ld1 = kInf;
     long long lk0 = kNoKey, lk1 = kNoKey;
+    const float qt0 = warp < nq ? ord2f(*(volatile int*)(p.qthr + __ldg(p.list_q + T.qoff + warp))) : kInf;
+    const float qt1 = warp + 8 < nq ? ord2f(*(volatile int*)(p.qthr + __ldg(p.list_q + T.qoff + warp + 8))) : kInf;
 
     for (int rt = 0; rt * kScanRows < T.nrows; ++rt, it += nks) {
       float acc[2][kScanG];
@@ -223,7 +226,8 @@ __global__ void __launch_bounds__(kScanThreads, 1)
         if (g >= nq) break;
         float& ld = h ? ld1 : ld0;
         long long& lk = h ? lk1 : lk0;
-        float thr = __shfl_sync(0xffffffffu, ld, 31);
+        const float qt = h ? qt1 : qt0;
+        float thr = fminf(__shfl_sync(0xffffffffu, ld, 31), qt);
         const long long gbase = T.grow0 + (long long)rt * kScanRows;
 #pragma unroll 1
         for (int m = 0; m < kScanRows / 32; ++m) {
@@ -231,7 +235,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
           const bool pass = v < thr;
           if (__any_sync(0xffffffffu, pass)) {
             warp_merge32(ld, lk, pass ? v : kInf, pass ? gbase + m * 32 + lane : kNoKey, lane);
-            thr = __shfl_sync(0xffffffffu, ld, 31);
+            thr = fminf(__shfl_sync(0xffffffffu, ld, 31), qt);
           }
         }
       }
@@ -243,13 +247,18 @@ __global__ void __launch_bounds__(kScanThreads, 1)
       const int g = warp + 8 * h;
       if (g >= nq) break;
       const int qid = __ldg(p.list_q + T.qoff + g);
+      const float ld = h ? ld1 : ld0;
+      const long long lk = h ? lk1 : lk0;
+      if (__shfl_sync(0xffffffffu, ld, 0) == kInf) continue;  // nothing survived: no partial
+      const float l31 = __shfl_sync(0xffffffffu, ld, 31);
       int pslot = 0;
-      if (lane == 0) pslot = atomicAdd(p.part_count + qid, 1);
+      if (lane == 0) {
+        pslot = atomicAdd(p.part_count + qid, 1);
+        if (l31 != kInf) atomicMin(p.qthr + qid, f2ord(l31));
+      }
       pslot = __shfl_sync(0xffffffffu, pslot, 0);
       if (pslot < p.part_cap) {
         const size_t o = ((size_t)qid * p.part_cap + pslot) * kTopK + lane;
-        const float ld = h ? ld1 : ld0;
-        const long long lk = h ? lk1 : lk0;
         p.part_dist[o] = ld;
         p.part_row[o] = lk == kNoKey ? -1 : (int)lk;
       }

@@ -3,8 +3,8 @@
 //
 // Per 128-row tile of a list chunk, D = X . Q^T is formed in TMEM with fp32-level
 // accuracy by a "bf16x3" split, x = x1 + x2 and q = q1 + q2 (each a bf16, RN):
-//   MMA_a (kind::f16, A = x1 from TMEM, B = [q1 ; q2], N = 32)
-//   MMA_b (kind::f16, A = x2 from TMEM, B = q1,        N = 16)
+//   MMA_a (kind::f16, A = x1 from TMEM, B = [q1 ; q2], N = 64)
+//   MMA_b (kind::f16, A = x2 from TMEM, B = q1,        N = 32)
 //   q.x = D_a[q1] + D_a[q2] + D_b  (missing only x2.q2 and the rounding of the
 //   second terms, ~2^-17 relative — inside the margin merge.cu certifies).
 // Every tcgen05.mma costs ~94+ cycles whatever its N (measured), so the design
@@ -12,12 +12,13 @@
 // 32 dims), A operands in TMEM so the smem ring is released as soon as the
 // converter warps have read it.
 // Roles (10 warps, one persistent CTA per SM):
-//   warp 0      TMA producer: [32 dims x 128 rows] fp32 boxes, 128B swizzle, 8-stage ring
-//   warp 1      TMEM allocator + single-thread MMA issuer
-//   warps 2-5   converters: fp32 x -> (x1, x2) bf16 pairs into an 8-deep TMEM ring;
-//               they also load each tile's query operand B (bf16, K-major SW128)
-//   warps 6-9   epilogue: tcgen05.ld of D, d~ = ||x||^2 + ||q||^2 - 2 q.x, per-query
-//               warp top-32 with threshold filter + bitonic merge, partial lists out
+//   warp 0        TMA producer: [32 dims x 128 rows] fp32 boxes, 128B swizzle, 6-stage ring
+//   warp 1        TMEM allocator + single-thread MMA issuer
+//   warps 2-5     converter group 0 (even stages): fp32 x -> (x1, x2) bf16 pairs into an
+//                 8-deep TMEM ring; also loads each tile's query operand B (bf16, K-major SW128)
+//   warps 10-13   converter group 1 (odd stages)
+//   warps 6-9     epilogue: tcgen05.ld of D, d~ = ||x||^2 + ||q||^2 - 2 q.x, per-query
+//                 warp top-32 with threshold filter + bitonic merge, partial lists out
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -32,11 +33,13 @@ namespace {
 constexpr int kRows = kTcRows;               // 128 = UMMA M
 constexpr int kStages = kTcStages;           // x ring depth
 constexpr int kStageBytes = kRows * 128;     // 16 KiB: 128 rows x 32 fp32
-constexpr int kBSlice = 32 * 128;            // 4 KiB: 32 B-rows (q1 x16, q2 x16) x 64 bf16
+constexpr int kBRows = 2 * kTcG;             // B operand rows: q1 (32), q2 (32)
+constexpr int kBSlice = kBRows * 128;        // 8 KiB per 64-dim bf16 slice
 constexpr int kXBufs = 8;                    // TMEM ring of converted stages (32 columns each)
-constexpr int kThreads = 320;
+constexpr int kThreads = 448;                // 14 warps
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kXCol0 = 128;             // first TMEM column of the x ring (accumulators: 0..127)
+constexpr uint32_t kAccCols = 128;           // per accumulator buffer: D_a (64) + D_b (32)
+constexpr uint32_t kXCol0 = 2 * kAccCols;    // first TMEM column of the x ring
 constexpr float kInf = __builtin_huge_valf();
 constexpr long long kNoKey = 0x7fffffffffffffffll;
 
@@ -101,7 +104,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.afull[i], 1);
       mbar_init(&sm.aempty[i], 4);
       mbar_init(&sm.tfull[i], 1);
-      mbar_init(&sm.tempty[i], 1 + 4 + 4);
+      mbar_init(&sm.tempty[i], 1 + 4 + 4 + 4);
     }
     mbar_init(sm.bfull, 4);
     mbar_init(sm.bempty, 1);
@@ -150,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   // ---------------------------------------------------------------- warp 1: MMA issuer
   else if (warp == 1) {
-    const uint32_t ida = idesc_bf16(kRows, 32), idb = idesc_bf16(kRows, 16);
+    const uint32_t ida = idesc_bf16(kRows, kBRows), idb = idesc_bf16(kRows, kTcG);
     const unsigned char* bs_ptr = reinterpret_cast<unsigned char*>(smem_raw) + (sm.bs - smem_u32(smem_raw));
     const uint64_t bdesc0 = umma_desc_sw128(bs_ptr);
     uint32_t u = 0, rtc = 0;
@@ -167,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int a = rtc & 1;
         mbar_wait(&sm.aempty[a], ((rtc >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t dacc = tmem + a * 64;
+        const uint32_t dacc = tmem + a * kAccCols;
         for (int ks = 0; ks < nks; ++ks, ++u) {
           const int xb = u % kXBufs;
           mbar_wait(&sm.xfull[xb], (u / kXBufs) & 1);
@@ -180,7 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int kk = 0; kk < 2; ++kk) {
               const uint32_t acc = (ks | kk) != 0;
               mma_bf16_ts(dacc, xa + kk * 8, bd + (uint64_t)(kk * 2), ida, acc);
-              mma_bf16_ts(dacc + 32, xa + 16 + kk * 8, bd + (uint64_t)(kk * 2), idb, acc);
+              mma_bf16_ts(dacc + kBRows, xa + 16 + kk * 8, bd + (uint64_t)(kk * 2), idb, acc);
             }
             tc_commit(&sm.xempty[xb]);
           }
@@ -193,10 +196,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
     }
   }
-  // ---------------------------------------------------------------- warps 2-5: converters
-  else if (warp < 6) {
+  // ------------------------------------------------- warps 2-5 / 10-13: converter groups 0 / 1
+  else if (warp < 6 || warp >= 10) {
     const int quarter = warp & 3;
-    const int tid = threadIdx.x - 64;  // 0..127
+    const int grp = warp >= 10;
+    const int tid = threadIdx.x - 64;  // 0..127 (group 0 only loads B)
     const int r = quarter * 32 + lane;
     uint32_t u = 0;
     for (uint32_t ti = 0;; ++ti) {
@@ -207,19 +211,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(&sm.tempty[slot]);
       if (t < 0) break;
       const ScanTile T = p.tiles[t];
-      // ---- B operand: rows 0-15 q1, 16-31 q2 (bf16, K-major, 128B swizzle, 64 dims per slice)
-      mbar_wait(sm.bempty, (ti & 1) ^ 1);
-      {
-        const int n = tid >> 2, part = n >> 4, g = n & 15;  // 4 threads per B row
-        const bool valid = g < T.nq;
-        const int qid = valid ? __ldg(p.list_q + T.qoff + g) : 0;
-        const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.qsplit) +
-                                                          ((size_t)qid * 2 + part) * d);  // bf16 row
+      // ---- B operand: rows 0-31 q1, 32-63 q2 (bf16, K-major, 128B swizzle, 64 dims per slice)
+      if (grp == 0) {
+        mbar_wait(sm.bempty, (ti & 1) ^ 1);
         const int ngran = d / 8;  // 16 B granules of 8 bf16
-        for (int gi = (tid & 3); gi < ngran; gi += 4) {
-          const uint4 v = valid ? __ldg(src + gi) : make_uint4(0, 0, 0, 0);
-          const int k = gi * 8, slice = k >> 6, gr = (k & 63) >> 3;
-          sts128(sm.bs + slice * kBSlice + n * 128 + ((gr ^ (n & 7)) << 4), v);
+        for (int n = tid >> 1; n < kBRows; n += 64) {  // 2 threads per B row
+          const int part = n / kTcG, g = n % kTcG;
+          const bool valid = g < T.nq;
+          const int qid = valid ? __ldg(p.list_q + T.qoff + g) : 0;
+          const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.qsplit) +
+                                                            ((size_t)qid * 2 + part) * d);  // bf16 row
+          for (int gi = (tid & 1); gi < ngran; gi += 2) {
+            const uint4 v = valid ? __ldg(src + gi) : make_uint4(0, 0, 0, 0);
+            const int k = gi * 8, slice = k >> 6, gr = (k & 63) >> 3;
+            sts128(sm.bs + slice * kBSlice + n * 128 + ((gr ^ (n & 7)) << 4), v);
+          }
         }
         fence_proxy_async();
         __syncwarp();
@@ -227,6 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       for (int rt = 0; rt * kRows < T.nrows; ++rt) {
         for (int ks = 0; ks < nks; ++ks, ++u) {
+          if ((int)(u & 1) != grp) continue;
           const int s = u % kStages, xb = u % kXBufs;
           mbar_wait(&sm.full[s], (u / kStages) & 1);
           const uint32_t row = sm.xs + s * kStageBytes + r * 128;
@@ -259,12 +266,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   // ---------------------------------------------------------------- warps 6-9: epilogue
   else {
+    constexpr int kOwn = kTcG / 4;  // queries owned per epilogue warp
     // Each warp reads D for its 32-lane quarter (rows), publishes d~ for all 16 queries to smem,
     // then owns queries ew, ew+4, ew+8, ew+12 over all 128 rows: candidates below the query's
     // running 32nd-best are compacted into one batch and merged (one bitonic merge per row tile
     // at most once the list has warmed up).
     const int quarter = warp & 3, ew = warp - 6;
-    float* edist = sm.edist;                          // [2][kTcG][kRows]
+    float* edist = sm.edist;                          // [kTcG][kRows]
     float* sd = sm.stage_d + ew * 32;                 // per-warp compaction batch
     long long* sk = sm.stage_k + ew * 32;
     uint32_t rtc = 0;
@@ -277,25 +285,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (t < 0) break;
       const ScanTile T = p.tiles[t];
       const int nq = T.nq;
-      float qn[kTcG];
+      float qn[kOwn];  // ||q||^2 of the owned queries (added by the owner, not per row)
 #pragma unroll
-      for (int g = 0; g < kTcG; ++g) qn[g] = g < nq ? __ldg(p.qnorm + __ldg(p.list_q + T.qoff + g)) : 0.f;
-      float ld[4];
-      long long lk[4];
+      for (int j = 0; j < kOwn; ++j) {
+        const int g = ew + 4 * j;
+        qn[j] = g < nq ? __ldg(p.qnorm + __ldg(p.list_q + T.qoff + g)) : 0.f;
+      }
+      float ld[kOwn], qt[kOwn];
+      long long lk[kOwn];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < kOwn; ++j) {
+        const int g = ew + 4 * j;
         ld[j] = kInf;
         lk[j] = kNoKey;
+        qt[j] = g < nq ? ord2f(*(volatile int*)(p.qthr + __ldg(p.list_q + T.qoff + g))) : kInf;
       }
       for (int rt = 0; rt * kRows < T.nrows; ++rt, ++rtc) {
         const int a = rtc & 1;
         mbar_wait(&sm.afull[a], (rtc >> 1) & 1);
         tc_fence_after();
-        const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + a * 64;
-        uint32_t d1[16], d2[16], d3[16];
+        const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + a * kAccCols;
+        uint32_t d1[32], d2[32], d3[32];
         RD_TMEM_LD16(ta, d1);
-        RD_TMEM_LD16(ta + 16, d2);
-        RD_TMEM_LD16(ta + 32, d3);
+        RD_TMEM_LD16(ta + 16, (d1 + 16));
+        RD_TMEM_LD16(ta + 32, d2);
+        RD_TMEM_LD16(ta + 48, (d2 + 16));
+        RD_TMEM_LD16(ta + 64, d3);
+        RD_TMEM_LD16(ta + 80, (d3 + 16));
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
@@ -304,23 +320,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int rloc = rt * kRows + r;
         const bool valid = rloc < T.nrows;
         const float xn = valid ? __ldg(p.xnorm + T.grow0 + rloc) : 0.f;
-        float* eb = edist + (rtc & 1) * (kTcG * kRows);
+        float* eb = edist;
+        named_bar_sync(2, 128);  // every owner finished reading the previous row tile
 #pragma unroll
         for (int g = 0; g < kTcG; ++g) {
           const float dot = (__uint_as_float(d1[g]) + __uint_as_float(d2[g])) + __uint_as_float(d3[g]);
-          eb[g * kRows + r] = (valid && g < nq) ? (xn + qn[g]) - 2.f * dot : kInf;
+          eb[g * kRows + r] = (valid && g < nq) ? xn - 2.f * dot : kInf;
         }
         named_bar_sync(2, 128);
         const long long gbase = T.grow0 + (long long)rt * kRows;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < kOwn; ++j) {
           const int g = ew + 4 * j;
           if (g >= nq) break;
-          float thr = __shfl_sync(0xffffffffu, ld[j], 31);
+          // prune with the tighter of this list's 32nd and the query's global threshold
+          float thr = fminf(__shfl_sync(0xffffffffu, ld[j], 31), qt[j]);
           int base = 0;
 #pragma unroll
           for (int m = 0; m < kRows / 32; ++m) {
-            const float v = eb[g * kRows + m * 32 + lane];
+            const float v = eb[g * kRows + m * 32 + lane] + qn[j];
             bool pass = v < thr;
             unsigned mask = __ballot_sync(0xffffffffu, pass);
             if (base + __popc(mask) > 32) {  // flush the staged batch first
@@ -328,7 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float bd = lane < base ? sd[lane] : kInf;
               const long long bk = lane < base ? sk[lane] : kNoKey;
               warp_merge32(ld[j], lk[j], bd, bk, lane);
-              thr = __shfl_sync(0xffffffffu, ld[j], 31);
+              thr = fminf(__shfl_sync(0xffffffffu, ld[j], 31), qt[j]);
               base = 0;
               pass = v < thr;
               mask = __ballot_sync(0xffffffffu, pass);
@@ -343,21 +361,30 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (base > 0) {
             __syncwarp();
-            const float bd = lane < base ? sd[lane] : kInf;
-            const long long bk = lane < base ? sk[lane] : kNoKey;
-            warp_merge32(ld[j], lk[j], bd, bk, lane);
+            if (base <= 3) {
+              for (int i = 0; i < base; ++i) warp_insert1(ld[j], lk[j], sd[i], sk[i], lane);
+            } else {
+              const float bd = lane < base ? sd[lane] : kInf;
+              const long long bk = lane < base ? sk[lane] : kNoKey;
+              warp_merge32(ld[j], lk[j], bd, bk, lane);
+            }
             __syncwarp();
           }
         }
       }
       // per-query top-32 of this tile -> one partial list per query
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < kOwn; ++j) {
         const int g = ew + 4 * j;
         if (g >= nq) break;
         const int qid = __ldg(p.list_q + T.qoff + g);
+        const float l31 = __shfl_sync(0xffffffffu, ld[j], 31);
+        if (__shfl_sync(0xffffffffu, ld[j], 0) == kInf) continue;  // nothing survived: no partial
         int ps = 0;
-        if (lane == 0) ps = atomicAdd(p.part_count + qid, 1);
+        if (lane == 0) {
+          ps = atomicAdd(p.part_count + qid, 1);
+          if (l31 != kInf) atomicMin(p.qthr + qid, f2ord(l31));
+        }
         ps = __shfl_sync(0xffffffffu, ps, 0);
         if (ps < p.part_cap) {
           const size_t o = ((size_t)qid * p.part_cap + ps) * kTopK + lane;
@@ -395,7 +422,7 @@ __global__ void qsplit_kernel(const float* __restrict__ Q, __nv_bfloat16* __rest
 size_t scan_tc_smem_bytes(int d) {
   return 1024 + (size_t)kStages * kStageBytes + (size_t)(d / 64) * kBSlice +
          (2 * kStages + 2 * kXBufs + 10) * sizeof(uint64_t) + 2 * sizeof(int) + 16 + 4 * 32 * 12 +
-         2 * kTcG * kRows * sizeof(float) + 64;
+         (size_t)kTcG * kRows * sizeof(float) + 64;
 }
 
 cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, const TcScanParams& p, int grid,

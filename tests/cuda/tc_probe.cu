@@ -124,7 +124,22 @@ __global__ void __launch_bounds__(128, 1) tc_timing_kernel(int mode, int n, long
     const uint64_t ad = umma_desc_sw128(base), bd = umma_desc_sw128(base + 128 * 128);
     const uint32_t id32 = idesc_tf32(128, 32), id16 = idesc_tf32(128, 16), id256 = idesc_tf32(128, 256);
     long long t0 = clock64();
-    if (mode >= 10) {  // straight-line issue: 8 unrolled MMAs per iteration, constant descriptors
+    if (mode >= 16) {  // bf16 TS patterns of the scan kernel: (N=64, N=32) pairs, commit every 4 MMAs?
+      __shared__ uint64_t bar2;
+      mbar_init(&bar2, 1);
+      fence_mbar_init();
+      const uint32_t ia = idesc_bf16(128, 64), ib = idesc_bf16(128, 32);
+      for (int i = 0; i < n; i += 4) {
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          mma_bf16_ts(tm, tm + 256 + kk * 8, bd + kk * 2, mode == 19 ? ib : ia, 1);
+          mma_bf16_ts(tm + 64, tm + 256 + 16 + kk * 8, bd + kk * 2, ib, 1);
+        }
+        if (mode == 17) tc_commit(&bar2);
+      }
+      n = 0;
+    }
+    if (mode >= 10 && mode < 16) {  // straight-line issue: 8 unrolled MMAs per iteration, constant descriptors
       const uint32_t idm = mode == 10 ? id32 : (mode == 11 ? id256 : mode == 13 ? idesc_tf32(64, 256) : mode == 14 ? idesc_tf32(64, 192) : mode == 15 ? idesc_tf32(64, 128) : id16);
       for (int i = 0; i < n; i += 8) {
 #pragma unroll

@@ -2,7 +2,7 @@ import ctypes as C, os, torch
 torch.cuda.init()
 lib = C.CDLL(os.path.join(os.path.dirname(__file__), "..", "tests", "cuda", "libtcprobe.so"))
 lib.tc_timing.restype = C.c_longlong
-for mode, name in [(0, "SS M128 N=32"), (1, "TS M128 N=16"), (2, "SS N=32 2acc"), (3, "SS M128 N=256"), (4, "SS M64 N256"), (5, "SS M64 N128"), (6, "SS M128 N128"), (7, "SS M64 N64"), (8, "SS M128 N64"), (9, "SS M64 N32"), (10, "UNROLLED SS M128 N32"), (11, "UNROLLED SS M128 N256"), (12, "UNROLLED TS M128 N16"), (13, "UNROLLED SS M64 N256"), (14, "UNROLLED SS M64 N192"), (15, "UNROLLED SS M64 N128")]:
+for mode, name in [(0, "SS M128 N=32"), (1, "TS M128 N=16"), (2, "SS N=32 2acc"), (3, "SS M128 N=256"), (4, "SS M64 N256"), (5, "SS M64 N128"), (6, "SS M128 N128"), (7, "SS M64 N64"), (8, "SS M128 N64"), (9, "SS M64 N32"), (10, "UNROLLED SS M128 N32"), (11, "UNROLLED SS M128 N256"), (12, "UNROLLED TS M128 N16"), (13, "UNROLLED SS M64 N256"), (14, "UNROLLED SS M64 N192"), (15, "UNROLLED SS M64 N128"), (16, "BF16 TS N64+N32 no commit"), (17, "BF16 TS N64+N32 commit/4"), (19, "BF16 TS N32+N32 no commit")]:
     res = []
     for n in (1, 8, 128, 512):
         lib.tc_timing(mode, n)
