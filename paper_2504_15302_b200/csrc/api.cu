@@ -724,7 +724,12 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   CK(cudaEventRecord(e1, s));
   CK(cudaMemsetAsync(w.part_count.p, 0, sizeof(int) * B, s));
   w.qthr.ensure(B);
-  CK(cudaMemsetAsync(w.qthr.p, 0x7f, sizeof(int) * B, s));  // 0x7f7f7f7f: a huge positive float
+  {
+    rd::SeedParams sd{w.probes.p, nprobe, d_q, w.qnorm.p, h->d_list_off.p, h->d_res_row0.p, h->arena.p, d, h->xmax,
+                      w.qthr.p, (int)B};
+    CK(rd::launch_seed(sd, s));
+    launches += 1;
+  }
   const bool has_off = h->slots > 0;
   if (has_off) {  // fetch the probe histogram for host-side staging decisions
     w.h_nq.ensure(nl);

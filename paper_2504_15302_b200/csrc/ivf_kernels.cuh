@@ -18,7 +18,7 @@ constexpr int kCoarseExtra = 32;    // approximate coarse candidates beyond npro
 constexpr int kTcRows = 128;        // UMMA M: rows per accumulator tile
 constexpr int kTcStages = 6;        // smem ring depth (16 KiB per stage)
 constexpr int kTcG = 32;            // queries per tensor-core tile (B operand: 32 q1 + 32 q2 rows)
-constexpr int kTcMinQ = 5;          // query groups with >= this many queries use the tensor cores
+constexpr int kTcMinQ = 1;          // lists probed by >= this many queries use the tensor cores
 constexpr int kPartsPerTile = 1;    // partial lists one scan tile emits per query
 
 // One unit of scan work: rows [row0, row0+nrows) of one list against <= 16 queries.
@@ -126,6 +126,24 @@ struct MergeParams {
   int B;
 };
 cudaError_t launch_merge(const MergeParams& p, cudaStream_t s);
+
+// Seeds each query's pruning threshold before the scan: 32 rows of its nearest resident
+// probed list, exact distances, threshold = max + 2*eps (a valid upper bound on the final
+// 32nd-best approximate distance, so certification is preserved).
+struct SeedParams {
+  const int* probes;             // B x nprobe, ascending by centroid distance
+  int nprobe;
+  const float* queries;
+  const float* qnorm;
+  const long long* list_off;
+  const long long* res_row0;     // -1 = offloaded (not used for seeding)
+  const float* arena;            // resident arena
+  int d;
+  float xmax;
+  int* qthr;                     // out: f2ord(threshold) or "none"
+  int B;
+};
+cudaError_t launch_seed(const SeedParams& p, cudaStream_t s);
 
 // Exact fallback for uncertified queries: every row of every probed list is compared
 // with the canonical exact distance and ordered by (distance, id).

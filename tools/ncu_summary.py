@@ -27,7 +27,7 @@ if kfilter:
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(src)))
     hh = rows[1]
-    data = rows[2:]
+    data = [x for x in rows[2:] if len(x) == len(hh) and x[0] != hh[0]]
     si = hh.index("Warp Stall Sampling (All Samples)")
     ii = hh.index("Instructions Executed")
     sc = hh.index("Source")
