@@ -152,6 +152,38 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
+// 3D bf16 map over a [rows][2][d] (hi, lo) split buffer, box {64 dims, 1 part, 128 rows}, 128B swizzle.
+CUtensorMap make_split_map(const void* base, long long rows, int d) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof m);
+  if (rows < 1) rows = 1;
+  cuuint64_t dims[3] = {(cuuint64_t)d, 2, (cuuint64_t)rows};
+  cuuint64_t strides[2] = {(cuuint64_t)d * 2, (cuuint64_t)d * 4};
+  cuuint32_t box[3] = {64, 1, 128};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw_rd(RD_ERR_RUNTIME, "cuTensorMapEncodeTiled (split) failed (%d)", (int)r);
+  return m;
+}
+
+// 2D bf16 map over the [rows][2][d] split buffer viewed as [2*rows x d], box {64, 1} (gather4 source).
+CUtensorMap make_gather_map(const void* base, long long rows, int d) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof m);
+  if (rows < 1) rows = 1;
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)(2 * rows)};
+  cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+  cuuint32_t box[2] = {64, 1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw_rd(RD_ERR_RUNTIME, "cuTensorMapEncodeTiled (gather) failed (%d)", (int)r);
+  return m;
+}
+
 // 2D fp32 map over rows x d, box [32 dims x box_rows], 128B swizzle.
 CUtensorMap make_row_map(const float* base, long long rows, int d, int box_rows) {
   CUtensorMap m;
@@ -202,6 +234,8 @@ struct rd_index {
   float cmax = 0.f, xmax = 0.f;
 
   DBuf<float> centroids, cnorm, xnorm, arena;
+  DBuf<float> csplit;  // nlist x 2 x d bf16 (c1, c2) for the tensor-core coarse GEMM
+  CUtensorMap cmap{};
   DBuf<long long> d_list_off, d_ids, d_res_row0;
   DBuf<const float*> d_list_base;
   std::vector<uint8_t> resident;      // host mask
@@ -307,6 +341,11 @@ struct rd_index {
     DBuf<float> tmp;
     tmp.alloc(1);
     CK(launch_row_norms_wrap(centroids.p, nlist, cnorm.p));
+    if (d % 64 == 0) {
+      csplit.alloc((size_t)nlist * d);  // 2 x bf16 per element = one float
+      CK(rd::launch_qsplit(centroids.p, csplit.p, nlist, d, 0));
+      cmap = make_split_map(csplit.p, nlist, d);
+    }
     CK(rd::launch_max_f32(cnorm.p, nlist, tmp.p, 0));
     float m2 = 0;
     CK(cudaMemcpy(&m2, tmp.p, sizeof(float), cudaMemcpyDeviceToHost));
@@ -712,7 +751,12 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   CK(cudaMemsetAsync(w.fails.p, 0, 2 * sizeof(unsigned), s));
   CK(rd::launch_row_norms(d_q, B, d, w.qnorm.p, s));
   CK(rd::launch_qsplit(d_q, w.qsplit.p, B, d, s));
-  CK(rd::launch_coarse(d_q, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, s));
+  if (d % 64 == 0) {
+    const CUtensorMap qmap = make_split_map(w.qsplit.p, B, d);
+    CK(rd::launch_coarse_tc(qmap, h->cmap, h->cnorm.p, w.Dc.p, (int)B, nl, d, s));
+  } else {
+    CK(rd::launch_coarse(d_q, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, s));
+  }
   rd::SelectParams sp{w.Dc.p, d_q, w.qnorm.p, h->centroids.p, w.probes.p, w.fails.p, (int)B, nl, nprobe, d, h->cmax};
   CK(rd::launch_select(sp, s));
   launches += 4;
@@ -738,6 +782,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     CK(cudaMemcpyAsync(w.h_qoff.p, w.list_qoff.p, sizeof(int) * nl, cudaMemcpyDeviceToHost, s));
   }
   CK(cudaEventRecord(e_plan, s));
+  const CUtensorMap gmap = make_gather_map(w.qsplit.p, B, d);
   rd::ScanParams sc{w.ff_tiles.p, w.meta.p + 2, w.meta.p + 3, d_q, w.qnorm.p, w.list_q.p, h->xnorm.p,
                     w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p};
   rd::TcScanParams tc{w.tiles.p, w.meta.p, w.meta.p + 1, w.qsplit.p, w.qnorm.p, w.list_q.p, h->xnorm.p,
@@ -745,7 +790,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   CK(rd::launch_scan(h->map256, h->map32, sc, h->num_sms, s));
   launches += 1;
   if (d % 64 == 0) {  // the tensor-core path stages 64-dim bf16 query slices; otherwise every tile is FFMA
-    CK(rd::launch_scan_tc(h->map128, h->map32, tc, h->num_sms, s));
+    CK(rd::launch_scan_tc(h->map128, h->map32, gmap, tc, h->num_sms, s));
     launches += 1;
   }
   CK(cudaEventRecord(e2, s));
@@ -851,7 +896,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
           to.tiles = w.off_tiles.p + tstart[bi];
           to.ntiles = dmeta.p + 4 * bi + 0;
           to.tile_counter = dmeta.p + 4 * bi + 1;
-          CK(rd::launch_scan_tc(h->smap128, h->smap32, to, std::min(h->num_sms, nt_tc), h->off_stream));
+          CK(rd::launch_scan_tc(h->smap128, h->smap32, gmap, to, std::min(h->num_sms, nt_tc), h->off_stream));
           launches += 1;
         }
         CK(cudaEventRecord(h->slot_done[slot], h->off_stream));
@@ -972,7 +1017,14 @@ int rd_probe(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32
     CK(cudaMemcpy(w.q.p, queries, sizeof(float) * B * d, cudaMemcpyHostToDevice));
     CK(cudaMemset(w.fails.p, 0, 2 * sizeof(unsigned)));
     CK(rd::launch_row_norms(w.q.p, B, d, w.qnorm.p, 0));
-    CK(rd::launch_coarse(w.q.p, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, 0));
+    if (d % 64 == 0) {
+      w.qsplit.ensure((size_t)B * d);
+      CK(rd::launch_qsplit(w.q.p, w.qsplit.p, B, d, 0));
+      const CUtensorMap qmap = make_split_map(w.qsplit.p, B, d);
+      CK(rd::launch_coarse_tc(qmap, h->cmap, h->cnorm.p, w.Dc.p, (int)B, nl, d, 0));
+    } else {
+      CK(rd::launch_coarse(w.q.p, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, 0));
+    }
     rd::SelectParams sp{w.Dc.p, w.q.p, w.qnorm.p, h->centroids.p, w.probes.p, w.fails.p, (int)B, nl, nprobe, d, h->cmax};
     CK(rd::launch_select(sp, 0));
     CK(cudaMemcpy(out_lists, w.probes.p, sizeof(int) * B * nprobe, cudaMemcpyDeviceToHost));

@@ -184,29 +184,142 @@ __device__ uint32_t select_smallest(const uint32_t* keys, int nlist, int C, int*
   return T;
 }
 
-// dynamic smem: keys[nlist] (u32)
+__device__ __forceinline__ float block_reduce_min(float v, float* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  float r = sh[0];
+  for (int i = 1; i < kSelThreads / 32; ++i) r = fminf(r, sh[i]);
+  return r;
+}
+__device__ __forceinline__ float block_reduce_max(float v, float* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  float r = sh[0];
+  for (int i = 1; i < kSelThreads / 32; ++i) r = fmaxf(r, sh[i]);
+  return r;
+}
+
+// dynamic smem: keys[nlist] (u32; approximate distances as floats, then exact keys in the fallback)
 __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const SelectParams p) {
   extern __shared__ uint32_t keys[];
   __shared__ int hist[2048];
   __shared__ int scan_sh[8];
+  __shared__ float fsh[8];
   __shared__ int cand[kSelMaxCand];
   __shared__ float cdist[kSelMaxCand];
   __shared__ uint32_t sel_prefix, sel_k;
-  __shared__ int certified;
+  __shared__ int certified, ncand_s, found_bin;
   const int b = blockIdx.x, tid = threadIdx.x;
   const int nlist = p.nlist;
   const float* q = p.queries + (size_t)b * p.d;
   const int grp = tid >> 3, j8 = tid & 7;
   const int np = min(p.nprobe, nlist);
   const float* drow = p.Dc + (size_t)b * nlist;
-  for (int j = tid; j < nlist; j += kSelThreads) keys[j] = f2key(drow[j]);
-  __syncthreads();
+  float* vals = reinterpret_cast<float*>(keys);
+  float vmin = __builtin_huge_valf(), vmax = -__builtin_huge_valf();
+  for (int j = tid; j < nlist; j += kSelThreads) {
+    const float v = drow[j];
+    vals[j] = v;
+    vmin = fminf(vmin, v);
+    vmax = fmaxf(vmax, v);
+  }
+  vmin = block_reduce_min(vmin, fsh);
+  vmax = block_reduce_max(vmax, fsh);
+  const int Cwant = min(nlist, p.nprobe + kCoarseExtra);
 
-  // attempt 0: C = nprobe + 32 approximate candidates, refined exactly and certified;
-  // attempt 1 (only if uncertified): exact distances to every centroid, C = nprobe.
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    const int C = attempt == 0 ? min(nlist, p.nprobe + kCoarseExtra) : np;
-    const uint32_t T = select_smallest(keys, nlist, C, hist, scan_sh, cand, &sel_prefix, &sel_k);
+  // attempt 0: a candidate set {approx < hi} of size in [C, kSelMaxCand], found with value-linear
+  // 2048-bin histograms (refined inside the crossing bin when it is too dense); exact refine;
+  // certification with hi as the lower bound of every excluded approximate distance.
+  // attempt 1 (uncertified or no usable threshold): exact distances to every centroid.
+  int ncand = -1;
+  float hi_edge = __builtin_huge_valf();
+  if (Cwant == nlist && nlist <= kSelMaxCand) {
+    ncand = nlist;  // every centroid is a candidate: nothing excluded
+  } else if (Cwant < nlist && vmax > vmin) {
+    float lo = vmin, hi = vmax;
+    int below = 0;
+    for (int round = 0; round < 3 && ncand < 0; ++round) {
+      const float width = (hi - lo) / 2048.f;
+      if (!(width > 0.f)) break;
+      for (int i = tid; i < 2048; i += kSelThreads) hist[i] = 0;
+      __syncthreads();
+      for (int j = tid; j < nlist; j += kSelThreads) {
+        const float v = vals[j];
+        if (v >= lo && v < hi) atomicAdd(&hist[min(2047, (int)((v - lo) / width))], 1);
+      }
+      __syncthreads();
+      int local = 0;
+      for (int i = 0; i < 8; ++i) local += hist[tid * 8 + i];
+      int tot;
+      const int before = block_excl_scan(local, scan_sh, &tot);
+      if (tid == 0) found_bin = 2047;
+      __syncthreads();
+      if (below + before < Cwant && below + before + local >= Cwant) {
+        int run = below + before;
+        for (int i = 0; i < 8; ++i) {
+          run += hist[tid * 8 + i];
+          if (run >= Cwant) {
+            found_bin = tid * 8 + i;
+            break;
+          }
+        }
+      }
+      __syncthreads();
+      const int fb = found_bin;
+      const float edge_hi = (fb == 2047) ? hi : lo + (fb + 1) * width;
+      const float edge_lo = lo + fb * width;
+      // exact recount of {v < edge_hi}
+      int c = 0;
+      for (int j = tid; j < nlist; j += kSelThreads) c += vals[j] < edge_hi;
+      int total;
+      block_excl_scan(c, scan_sh, &total);
+      if (total >= Cwant && total <= kSelMaxCand) {
+        ncand = total;
+        hi_edge = edge_hi;
+      } else {
+        int cb = 0;
+        for (int j = tid; j < nlist; j += kSelThreads) cb += vals[j] < edge_lo;
+        int tb;
+        block_excl_scan(cb, scan_sh, &tb);
+        below = tb;
+        lo = edge_lo;
+        hi = edge_hi;
+      }
+    }
+  }
+  if (ncand >= 0) {
+    if (tid == 0) ncand_s = 0;
+    __syncthreads();
+    for (int j = tid; j < nlist; j += kSelThreads)
+      if (vals[j] < hi_edge) cand[atomicAdd(&ncand_s, 1)] = j;
+    __syncthreads();
+  }
+
+  for (int attempt = (ncand >= 0 ? 0 : 1); attempt < 2; ++attempt) {
+    int C;
+    if (attempt == 0) {
+      C = ncand;
+    } else {
+      // exact keys for every centroid, then the np smallest by (exact distance, list id)
+      for (int c0 = 0; c0 < nlist; c0 += kSelThreads / 8) {
+        const int c = c0 + grp;
+        const int cc = c < nlist ? c : nlist - 1;
+        const float e = exact_l2_group8(q, p.centroids + (size_t)cc * p.d, p.d, j8);
+        __syncthreads();
+        if (c < nlist && j8 == 0) keys[c] = f2key(e);
+      }
+      __syncthreads();
+      C = np;
+      select_smallest(keys, nlist, C, hist, scan_sh, cand, &sel_prefix, &sel_k);
+    }
     for (int c0 = 0; c0 < C; c0 += kSelThreads / 8) {
       const int c = c0 + grp;
       const int cc = c < C ? c : C - 1;
@@ -242,12 +355,13 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
     }
     if (tid == 0) {
       int ok = 1;
-      if (attempt == 0 && C < nlist) {
-        // error bound of the approximate distance: sequential fp32 FFMA over d terms
+      if (attempt == 0) {
+        // every excluded centroid has approx >= hi_edge; the GEMM's error bound turns that into
+        // a lower bound on its exact distance
         const float qn = p.qnorm[b];
         const float u = 5.9604645e-8f;
         const float eps = 2.f * ((p.d + 4) * u * 2.f * sqrtf(qn) * p.cmax + 8.f * u * (qn + p.cmax * p.cmax)) + 1e-30f;
-        const float lower = key2f(T) + qn - eps;  // lower bound on any excluded exact distance
+        const float lower = hi_edge + qn - eps;
         ok = lower > cdist[np - 1];
       }
       certified = ok;
@@ -255,14 +369,6 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
     }
     __syncthreads();
     if (certified) break;
-    // exact keys for every centroid, then select again
-    for (int c0 = 0; c0 < nlist; c0 += kSelThreads / 8) {
-      const int c = c0 + grp;
-      const int cc = c < nlist ? c : nlist - 1;
-      const float e = exact_l2_group8(q, p.centroids + (size_t)cc * p.d, p.d, j8);
-      if (c < nlist && j8 == 0) keys[c] = f2key(e);
-    }
-    __syncthreads();
   }
   for (int i = tid; i < p.nprobe; i += kSelThreads) p.probes[(size_t)b * p.nprobe + i] = i < np ? cand[i] : -1;
 }

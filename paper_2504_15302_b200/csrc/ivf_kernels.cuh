@@ -65,8 +65,9 @@ struct TcScanParams {
 
 size_t scan_smem_bytes(int d);
 size_t scan_tc_smem_bytes(int d);
-cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, const TcScanParams& p,
-                           int grid, cudaStream_t s);
+// qmap: 2D bf16 map over the qsplit buffer as [2B rows x d], box {64, 1} (gather4 source)
+cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, const CUtensorMap& qmap,
+                           const TcScanParams& p, int grid, cudaStream_t s);
 cudaError_t launch_qsplit(const float* Q, void* out, long long B, int d, cudaStream_t s);
 cudaError_t launch_scan(const CUtensorMap& map256, const CUtensorMap& map32, const ScanParams& p,
                         int grid, cudaStream_t s);
@@ -75,6 +76,11 @@ cudaError_t launch_scan(const CUtensorMap& map256, const CUtensorMap& map32, con
 // constant per query and added where an absolute distance is needed).
 cudaError_t launch_coarse(const float* Q, const float* C, const float* cnorm, float* Dc, int B,
                           int nlist, int d, cudaStream_t s);
+// tensor-core variant (d % 64 == 0): qmap / cmap are 3D bf16 maps over the (hi, lo) splits,
+// dims {d, 2, rows}, box {64, 1, 128}, 128 B swizzle
+size_t coarse_tc_smem_bytes();
+cudaError_t launch_coarse_tc(const CUtensorMap& qmap, const CUtensorMap& cmap, const float* cnorm, float* Dc, int B,
+                             int nlist, int d, cudaStream_t s);
 
 struct SelectParams {
   const float* Dc;         // B x nlist

@@ -34,11 +34,27 @@ __host__ __device__ __forceinline__ float unif(uint64_t seed, uint64_t i) {
 // Eight lanes j = lane & 7 of an aligned group each sum residue class t = j (mod 8)
 // sequentially in fp64 (no contraction), then the fixed tree
 // ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7)); every lane of the group returns the f32 value.
-__device__ __forceinline__ float exact_l2_group8(const float* __restrict__ q,
-                                                 const float* __restrict__ x, int d, int j) {
+template <bool kLdg>
+__device__ __forceinline__ float exact_l2_group8_impl(const float* __restrict__ q, const float* x, int d, int j) {
+  // loads are batched 8 deep ahead of the strictly sequential fp64 accumulation, which keeps
+  // the summation order (and so the result) canonical while hiding memory latency
   double s = 0.0;
-  for (int t = j; t < d; t += 8) {
-    double df = __dsub_rn((double)__ldg(q + t), (double)__ldg(x + t));
+  int t = j;
+  for (; t + 56 < d; t += 64) {
+    float qv[8], xv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      qv[i] = kLdg ? __ldg(q + t + 8 * i) : q[t + 8 * i];
+      xv[i] = kLdg ? __ldg(x + t + 8 * i) : x[t + 8 * i];
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const double df = __dsub_rn((double)qv[i], (double)xv[i]);
+      s = __dadd_rn(s, __dmul_rn(df, df));
+    }
+  }
+  for (; t < d; t += 8) {
+    const double df = __dsub_rn((double)(kLdg ? __ldg(q + t) : q[t]), (double)(kLdg ? __ldg(x + t) : x[t]));
     s = __dadd_rn(s, __dmul_rn(df, df));
   }
   s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
@@ -46,18 +62,13 @@ __device__ __forceinline__ float exact_l2_group8(const float* __restrict__ q,
   s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
   return __double2float_rn(s);
 }
+__device__ __forceinline__ float exact_l2_group8(const float* __restrict__ q, const float* __restrict__ x, int d,
+                                                 int j) {
+  return exact_l2_group8_impl<true>(q, x, d, j);
+}
 // same value, x possibly in mapped host memory (no __ldg on the non-coherent path)
-__device__ __forceinline__ float exact_l2_group8_any(const float* __restrict__ q, const float* x,
-                                                     int d, int j) {
-  double s = 0.0;
-  for (int t = j; t < d; t += 8) {
-    double df = __dsub_rn((double)q[t], (double)x[t]);
-    s = __dadd_rn(s, __dmul_rn(df, df));
-  }
-  s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
-  s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
-  s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
-  return __double2float_rn(s);
+__device__ __forceinline__ float exact_l2_group8_any(const float* __restrict__ q, const float* x, int d, int j) {
+  return exact_l2_group8_impl<false>(q, x, d, j);
 }
 
 // ---------------------------------------------------------------- PTX: smem, mbarrier, TMA
@@ -104,6 +115,23 @@ __device__ __forceinline__ void tma_load_2d_u32(uint32_t dst, const CUtensorMap*
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
       "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_u32(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+// 4 arbitrary rows x box-width columns of a 2D map (box {cols, 1}) into 4 consecutive smem rows
+__device__ __forceinline__ void tma_gather4_u32(uint32_t dst, const CUtensorMap* map, int col, int r0, int r1, int r2,
+                                                int r3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
@@ -164,6 +192,16 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(const void* smem_ptr) {
   desc |= (uint64_t)1 << 46;                        // version (sm100)
   desc |= (uint64_t)2 << 61;                        // SWIZZLE_128B
   return desc;
+}
+// D[tmem] (+)= A[smem desc] * B[smem desc]^T, kind::f16 (BF16 inputs, F32 accumulate)
+__device__ __forceinline__ void mma_bf16_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
 }
 // D[tmem] (+)= A[tmem] * B[smem desc]^T, kind::f16 (BF16 inputs, F32 accumulate)
 __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,

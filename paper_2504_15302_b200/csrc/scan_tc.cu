@@ -85,7 +85,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 
 __global__ void __launch_bounds__(kThreads, 1)
     ivf_scan_tc_kernel(const __grid_constant__ CUtensorMap map128, const __grid_constant__ CUtensorMap map32,
-                       const TcScanParams p) {
+                       const __grid_constant__ CUtensorMap qmap, const TcScanParams p) {
   extern __shared__ unsigned char smem_raw[];
   const int d = p.d, nks = d / 32;
   const Smem sm = carve(smem_raw, d);
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.tfull[i], 1);
       mbar_init(&sm.tempty[i], 1 + 4 + 4 + 4);
     }
-    mbar_init(sm.bfull, 4);
+    mbar_init(sm.bfull, 1);
     mbar_init(sm.bempty, 1);
     fence_mbar_init();
   }
@@ -122,15 +122,44 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       prefetch_tmap(&map128);
       prefetch_tmap(&map32);
-      uint32_t u = 0;
-      for (uint32_t ti = 0;; ++ti) {
-        const int t = atomicAdd(p.tile_counter, 1);
-        const int slot = ti & 1;
+      prefetch_tmap(&qmap);
+    }
+    uint32_t u = 0;
+    const int nslices = d / 64;
+    for (uint32_t ti = 0;; ++ti) {
+      int t = 0;
+      const int slot = ti & 1;
+      if (lane == 0) {
+        t = atomicAdd(p.tile_counter, 1);
         mbar_wait(&sm.tempty[slot], ((ti >> 1) & 1) ^ 1);
         sm.tring[slot] = t < ntiles ? t : -1;
         mbar_arrive(&sm.tfull[slot]);
-        if (t >= ntiles) break;
-        const ScanTile T = p.tiles[t];
+      }
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= ntiles) break;
+      const ScanTile T = p.tiles[t];
+      // ---- B operand by TMA gather4: rows 0-31 q1, 32-63 q2 of the tile's queries (qsplit row
+      // 2*qid + part); padding rows repeat the last query (their D columns are ignored)
+      mbar_wait(sm.bempty, (ti & 1) ^ 1);
+      // only the quads holding real queries are loaded; the others keep stale rows whose D
+      // columns the epilogue never reads
+      const int qq = (T.nq + 3) >> 2;  // quads per part
+      if (lane == 0) mbar_arrive_expect_tx(sm.bfull, (uint32_t)(nslices * 2 * qq * 512));
+      __syncwarp();
+      for (int gi = lane; gi < nslices * 2 * qq; gi += 32) {
+        const int slice = gi / (2 * qq), qi = gi % (2 * qq);
+        const int part = qi >= qq ? 1 : 0;
+        const int g0 = (qi - part * qq) * 4;
+        const int quad = part * (kTcG / 4) + g0 / 4;
+        int r[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int g = min(g0 + i, T.nq - 1);
+          r[i] = 2 * __ldg(p.list_q + T.qoff + g) + part;
+        }
+        tma_gather4_u32(sm.bs + slice * kBSlice + quad * 512, &qmap, slice * 64, r[0], r[1], r[2], r[3], sm.bfull);
+      }
+      if (lane == 0) {
         for (int rt = 0; rt * kRows < T.nrows; ++rt) {
           const int rows = min(kRows, T.nrows - rt * kRows);
           const int nb = (rows + 31) >> 5;
@@ -149,6 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      __syncwarp();
     }
   }
   // ---------------------------------------------------------------- warp 1: MMA issuer
@@ -211,26 +241,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(&sm.tempty[slot]);
       if (t < 0) break;
       const ScanTile T = p.tiles[t];
-      // ---- B operand: rows 0-31 q1, 32-63 q2 (bf16, K-major, 128B swizzle, 64 dims per slice)
-      if (grp == 0) {
-        mbar_wait(sm.bempty, (ti & 1) ^ 1);
-        const int ngran = d / 8;  // 16 B granules of 8 bf16
-        for (int n = tid >> 1; n < kBRows; n += 64) {  // 2 threads per B row
-          const int part = n / kTcG, g = n % kTcG;
-          const bool valid = g < T.nq;
-          const int qid = valid ? __ldg(p.list_q + T.qoff + g) : 0;
-          const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.qsplit) +
-                                                            ((size_t)qid * 2 + part) * d);  // bf16 row
-          for (int gi = (tid & 1); gi < ngran; gi += 2) {
-            const uint4 v = valid ? __ldg(src + gi) : make_uint4(0, 0, 0, 0);
-            const int k = gi * 8, slice = k >> 6, gr = (k & 63) >> 3;
-            sts128(sm.bs + slice * kBSlice + n * 128 + ((gr ^ (n & 7)) << 4), v);
-          }
-        }
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(sm.bfull);
-      }
       for (int rt = 0; rt * kRows < T.nrows; ++rt) {
         for (int ks = 0; ks < nks; ++ks, ++u) {
           if ((int)(u & 1) != grp) continue;
@@ -425,8 +435,8 @@ size_t scan_tc_smem_bytes(int d) {
          (size_t)kTcG * kRows * sizeof(float) + 64;
 }
 
-cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, const TcScanParams& p, int grid,
-                           cudaStream_t s) {
+cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, const CUtensorMap& qmap,
+                           const TcScanParams& p, int grid, cudaStream_t s) {
   if (p.d % 64 != 0) return cudaErrorInvalidValue;
   static bool attr_set = false;
   if (!attr_set) {
@@ -436,7 +446,7 @@ cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, 
   }
   const size_t smem = scan_tc_smem_bytes(p.d);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  ivf_scan_tc_kernel<<<grid, kThreads, smem, s>>>(map128, map32, p);
+  ivf_scan_tc_kernel<<<grid, kThreads, smem, s>>>(map128, map32, qmap, p);
   return cudaGetLastError();
 }
 
