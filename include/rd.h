@@ -81,7 +81,9 @@ typedef struct {
 /* Placement between searches (reference analogue: PlacementConfig, domain.hpp:75-82).
  * Lists not resident live in pinned host memory and are streamed per search. */
 typedef struct {
-  uint64_t hbm_budget_bytes;     /* 0 = no byte budget */
+  uint64_t hbm_budget_bytes;     /* 0 = no byte budget; else covers resident lists plus (once any list
+                                    is offloaded) a staging ring of >= 2 slots of
+                                    max(largest list, 16384 rows), rows rounded up to 256 */
   double offload_fraction;       /* fraction of lists (by count) to offload; 0 = none */
   const uint8_t* resident_mask;  /* nullable; nlist bytes, 1 = HBM-resident. Overrides the two above */
   const uint32_t* list_heat;     /* nullable; nlist probe counts: hottest lists stay resident */

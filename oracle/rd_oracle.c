@@ -354,10 +354,31 @@ static int choose_resident(const rd_index* h, const rd_placement* p, uint8_t* ma
   int64_t target = nl - (int64_t)floor(p->offload_fraction * nl + 0.5);
   uint64_t bytes = 0;
   memset(mask, 0, (size_t)nl);
+  /* the budget covers resident lists plus, once anything is offloaded, a staging ring of at
+   * least two slots of max(largest list, 16384 rows) rounded up to 256 rows (include/rd.h) */
+  uint64_t budget = p->hbm_budget_bytes;
+  if (budget) {
+    uint64_t all = 0;
+    int64_t maxlen = 0;
+    for (int32_t l = 0; l < nl; ++l)
+      if (h->offsets[l + 1] - h->offsets[l] > maxlen) maxlen = h->offsets[l + 1] - h->offsets[l];
+    for (int64_t i = 0; i < target; ++i) all += (uint64_t)(h->offsets[order[i] + 1] - h->offsets[order[i]]) * row_bytes;
+    if (target < nl || all > budget) {
+      int64_t rows = maxlen > 16384 ? maxlen : 16384;
+      uint64_t slot = (uint64_t)((rows + 255) / 256 * 256) * row_bytes;
+      uint64_t reserve = (uint64_t)(p->staging_slots > 2 ? p->staging_slots : 2) * slot;
+      if (reserve > budget) {
+        free(order);
+        return fail(RD_ERR_INFEASIBLE, "placement infeasible: budget %llu below the %llu-byte staging ring",
+                    (unsigned long long)budget, (unsigned long long)reserve);
+      }
+      budget -= reserve;
+    }
+  }
   for (int64_t i = 0; i < target; ++i) {
     int32_t l = order[i];
     uint64_t lb = (uint64_t)(h->offsets[l + 1] - h->offsets[l]) * row_bytes;
-    if (p->hbm_budget_bytes && bytes + lb > p->hbm_budget_bytes) break;
+    if (budget && bytes + lb > budget) break;
     bytes += lb;
     mask[l] = 1;
   }

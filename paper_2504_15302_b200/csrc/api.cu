@@ -595,10 +595,26 @@ int rd_index_place(rd_index* h, const rd_placement* p) {
         std::stable_sort(order.begin(), order.end(),
                          [&](int a, int b) { return p->list_heat[a] > p->list_heat[b]; });
       const long long target = nl - (long long)std::floor(p->offload_fraction * nl + 0.5);
+      // the budget covers the resident lists and, once anything is offloaded, a staging ring of
+      // at least two slots of max(largest list, 16384 rows) (include/rd.h, rd_placement)
+      uint64_t budget = p->hbm_budget_bytes;
+      if (budget) {
+        uint64_t all = 0;
+        for (long long i = 0; i < target; ++i)
+          all += (uint64_t)(h->list_off[order[i] + 1] - h->list_off[order[i]]) * row_bytes;
+        if (target < nl || all > budget) {
+          const uint64_t slot = (uint64_t)((std::max<long long>(h->max_len, 16384) + 255) / 256 * 256) * row_bytes;
+          const uint64_t reserve = (uint64_t)std::max(2, p->staging_slots) * slot;
+          if (reserve > budget)
+            throw_rd(RD_ERR_INFEASIBLE, "placement infeasible: budget %llu below the %llu-byte staging ring",
+                     (unsigned long long)budget, (unsigned long long)reserve);
+          budget -= reserve;
+        }
+      }
       for (long long i = 0; i < target; ++i) {
         const int l = order[i];
         const uint64_t lb = (uint64_t)(h->list_off[l + 1] - h->list_off[l]) * row_bytes;
-        if (p->hbm_budget_bytes && res_bytes + lb > p->hbm_budget_bytes) break;
+        if (budget && res_bytes + lb > budget) break;
         res_bytes += lb;
         mask[l] = 1;
       }

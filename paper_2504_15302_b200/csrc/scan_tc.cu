@@ -32,10 +32,14 @@ namespace {
 
 constexpr int kRows = kTcRows;               // 128 = UMMA M
 constexpr int kStages = kTcStages;           // x ring depth
+// converter group g owns stages / TMEM buffers with u % 2 == g; an odd ring depth would let one
+// group wait on a phase two ahead of the other group's and alias its mbarrier parity
+static_assert(kTcStages % 2 == 0, "x ring depth must be even");
 constexpr int kStageBytes = kRows * 128;     // 16 KiB: 128 rows x 32 fp32
 constexpr int kBRows = 2 * kTcG;             // B operand rows: q1 (32), q2 (32)
 constexpr int kBSlice = kBRows * 128;        // 8 KiB per 64-dim bf16 slice
 constexpr int kXBufs = 8;                    // TMEM ring of converted stages (32 columns each)
+static_assert(kXBufs % 2 == 0, "TMEM ring depth must be even");
 constexpr int kThreads = 448;                // 14 warps
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kAccCols = 128;           // per accumulator buffer: D_a (64) + D_b (32)

@@ -60,9 +60,18 @@ def test_placement_rule(oracle):
     idx.place(offload_fraction=0.25, list_heat=heat)
     _, _, mask = idx.layout(with_ids=False)
     assert mask.sum() == 15 and mask[5:].all()
-    budget = int(lens[:3].sum() * 32 * 4)
-    idx.place(hbm_budget_bytes=budget)
-    _, _, mask = idx.layout(with_ids=False)
-    assert mask[:3].all() and not mask[3:].any()
+    total = int(lens.sum() * 32 * 4)
+    idx.place(hbm_budget_bytes=total)  # everything fits: no staging ring needed
+    assert idx.layout(with_ids=False)[2].all()
+    with pytest.raises(InfeasibleError):  # one byte short: the 2-slot ring (4 MiB) does not fit
+        idx.place(hbm_budget_bytes=total - 1)
     with pytest.raises(InfeasibleError):
-        idx.place(hbm_budget_bytes=budget, resident_mask=np.ones(20, np.uint8))
+        idx.place(hbm_budget_bytes=total - 1, resident_mask=np.ones(20, np.uint8))
+    # a larger index: the budget covers the staging ring plus the first three lists
+    big = oracle.synthetic_index(oracle.desc(200000, 32, 20))
+    blens = np.diff(big.layout(with_ids=False)[0])
+    ring = 2 * 16384 * 32 * 4  # two slots of max(largest list, 16384) rows
+    assert blens.max() <= 16384
+    big.place(hbm_budget_bytes=int(blens[:3].sum() * 32 * 4) + ring)
+    bmask = big.layout(with_ids=False)[2]
+    assert bmask[:3].all() and not bmask[3:].any()
