@@ -183,13 +183,20 @@ def run_ours(args, cfg):
     idx = lib.synthetic_index(desc, device=local)
     build_s = time.time() - t0
     reservation = None
+    heat = None
+    if cfg["offload"] is None or cfg["offload"] > 0:
+        # joint placement pins the hot lists: probe frequency from a calibration batch of queries
+        # disjoint from the timed ones (north_star item 4)
+        cal, _ = lib.synth_queries(desc, 50_000_000, 4096)
+        pr = idx.probe(cal, nprobe)
+        heat = np.bincount(pr[pr >= 0].ravel(), minlength=cfg["nlist"]).astype(np.uint32)
     if cfg["offload"] is None:  # C5: budget = device memory - LLM reservation - engine workspace
         free, total = torch.cuda.mem_get_info()
         reservation = c5_reservation(lib)
         budget = int(total - reservation - (4 << 30))
-        idx.place(hbm_budget_bytes=budget)
+        idx.place(hbm_budget_bytes=budget, list_heat=heat)
     elif cfg["offload"] > 0:
-        idx.place(offload_fraction=cfg["offload"])
+        idx.place(offload_fraction=cfg["offload"], list_heat=heat)
     info = idx.info()
     hold = None
     if reservation is not None:  # actually hold the LLM's bytes while searching
