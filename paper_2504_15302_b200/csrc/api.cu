@@ -153,13 +153,13 @@ EncodeTiledFn encode_fn() {
 }
 
 // 3D bf16 map over a [rows][2][d] (hi, lo) split buffer, box {64 dims, 1 part, 128 rows}, 128B swizzle.
-CUtensorMap make_split_map(const void* base, long long rows, int d) {
+CUtensorMap make_split_map(const void* base, long long rows, int d, int box_rows = 128) {
   CUtensorMap m;
   std::memset(&m, 0, sizeof m);
   if (rows < 1) rows = 1;
   cuuint64_t dims[3] = {(cuuint64_t)d, 2, (cuuint64_t)rows};
   cuuint64_t strides[2] = {(cuuint64_t)d * 2, (cuuint64_t)d * 4};
-  cuuint32_t box[3] = {64, 1, 128};
+  cuuint32_t box[3] = {64, 1, (cuuint32_t)box_rows};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -227,6 +227,7 @@ struct rd_index {
   int device = 0;
   int num_sms = 148;
   int tc_min_q = rd::kTcMinQ;
+  int debug_skip = 0;  // profiling only
   long long n = 0;
   int d = 0, nlist = 0;
   std::vector<long long> list_off;  // host copy, nlist + 1
@@ -236,6 +237,11 @@ struct rd_index {
   DBuf<float> centroids, cnorm, xnorm, arena;
   DBuf<float> csplit;  // nlist x 2 x d bf16 (c1, c2) for the tensor-core coarse GEMM
   CUtensorMap cmap{};
+  // pre-split bf16 (x1, x2) copy of the resident arena for the conversion-free tensor-core scan;
+  // kept only while every list is resident and device memory allows (RD_PRESPLIT=0 disables)
+  DBuf<float> xsplit;
+  CUtensorMap xmap128{}, xmap32{};
+  bool presplit = false;
   DBuf<long long> d_list_off, d_ids, d_res_row0;
   DBuf<const float*> d_list_base;
   std::vector<uint8_t> resident;      // host mask
@@ -323,6 +329,7 @@ struct rd_index {
     for (auto& r : tev)
       for (auto& e : r) CK(cudaEventCreate(&e));
     if (const char* v = std::getenv("RD_TC_MIN_Q")) tc_min_q = std::max(1, std::atoi(v));
+    if (const char* v = std::getenv("RD_DEBUG_SKIP")) debug_skip = std::atoi(v);
     // the tensor-core scan stages bf16 query slices of 64 dims
   }
 
@@ -354,6 +361,24 @@ struct rd_index {
     CK(cudaMemcpy(&m2, tmp.p, sizeof(float), cudaMemcpyDeviceToHost));
     xmax = std::sqrt(m2) * (1.f + 1e-6f);
     CK(cudaDeviceSynchronize());
+    build_presplit();
+  }
+
+  void build_presplit() {
+    presplit = false;
+    xsplit.reset();
+    const char* env = std::getenv("RD_PRESPLIT");
+    if (d % 64 != 0 || (env && std::atoi(env) == 0) || n_resident != n || n == 0) return;
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    const size_t need = (size_t)n * d * 4;
+    if (need + (size_t(4) << 30) > fr) return;  // not enough room: the converter path stays
+    xsplit.alloc((size_t)n * d);
+    CK(rd::launch_qsplit(arena.p, xsplit.p, n, d, 0));
+    CK(cudaDeviceSynchronize());
+    xmap128 = make_split_map(xsplit.p, n, d, rd::kTcRows);
+    xmap32 = make_split_map(xsplit.p, n, d, 32);
+    presplit = true;
   }
 
   cudaError_t launch_row_norms_wrap(const float* X, long long rows, float* out) {
@@ -363,6 +388,8 @@ struct rd_index {
   void upload_residency() {
     d_res_row0.alloc(nlist);
     CK(cudaMemcpy(d_res_row0.p, res_row0.data(), sizeof(long long) * nlist, cudaMemcpyHostToDevice));
+    xsplit.reset();  // any relayout invalidates the pre-split copy (rebuilt by build_presplit)
+    presplit = false;
     std::vector<const float*> base(nlist);
     for (int l = 0; l < nlist; ++l)
       base[l] = resident[l] ? arena.p + (size_t)res_row0[l] * d : host_arena.p + (size_t)host_row0[l] * d;
@@ -551,7 +578,7 @@ int rd_index_info_get(const rd_index* h, rd_index_info* o) {
     o->n_resident = h->n_resident;
     for (int l = 0; l < h->nlist; ++l) o->lists_resident += h->resident[l];
     o->hbm_bytes = (uint64_t)h->n_resident * h->d * 4 + (uint64_t)h->n * 12 + (uint64_t)h->nlist * (h->d + 1) * 4 +
-                   (uint64_t)h->slots * h->slot_rows * h->d * 4;
+                   (uint64_t)h->slots * h->slot_rows * h->d * 4 + (uint64_t)h->xsplit.n * 4;
     o->host_pinned_bytes = (uint64_t)h->host_arena.n * 4;
     o->staging_slots = h->slots;
     o->max_norm = h->xmax;
@@ -680,6 +707,7 @@ int rd_index_place(rd_index* h, const rd_placement* p) {
     h->host_row0 = new_host_row;
     h->n_resident = n_res;
     h->upload_residency();
+    h->build_presplit();
     // staging ring
     for (auto e : h->slot_ready) cudaEventDestroy(e);
     for (auto e : h->slot_done) cudaEventDestroy(e);
@@ -802,11 +830,12 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   rd::ScanParams sc{w.ff_tiles.p, w.meta.p + 2, w.meta.p + 3, d_q, w.qnorm.p, w.list_q.p, h->xnorm.p,
                     w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p};
   rd::TcScanParams tc{w.tiles.p, w.meta.p, w.meta.p + 1, w.qsplit.p, w.qnorm.p, w.list_q.p, h->xnorm.p,
-                      w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p};
+                      w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p, h->debug_skip};
   CK(rd::launch_scan(h->map256, h->map32, sc, h->num_sms, s));
   launches += 1;
   if (d % 64 == 0) {  // the tensor-core path stages 64-dim bf16 query slices; otherwise every tile is FFMA
-    CK(rd::launch_scan_tc(h->map128, h->map32, gmap, tc, h->num_sms, s));
+    CK(rd::launch_scan_tc(h->presplit ? h->xmap128 : h->map128, h->presplit ? h->xmap32 : h->map32, gmap, tc,
+                          h->num_sms, s, h->presplit));
     launches += 1;
   }
   CK(cudaEventRecord(e2, s));
@@ -912,7 +941,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
           to.tiles = w.off_tiles.p + tstart[bi];
           to.ntiles = dmeta.p + 4 * bi + 0;
           to.tile_counter = dmeta.p + 4 * bi + 1;
-          CK(rd::launch_scan_tc(h->smap128, h->smap32, gmap, to, std::min(h->num_sms, nt_tc), h->off_stream));
+          CK(rd::launch_scan_tc(h->smap128, h->smap32, gmap, to, std::min(h->num_sms, nt_tc), h->off_stream, false));
           launches += 1;
         }
         CK(cudaEventRecord(h->slot_done[slot], h->off_stream));

@@ -61,13 +61,15 @@ struct TcScanParams {
   int part_cap;
   int d;
   int* qthr;               // B: per-query pruning threshold (f2ord), min over completed tiles' 32nd
+  int debug_skip;          // profiling only (RD_DEBUG_SKIP): 1 = no epilogue selection, 2 = no conversion, 4 = no MMA
 };
 
 size_t scan_smem_bytes(int d);
 size_t scan_tc_smem_bytes(int d);
 // qmap: 2D bf16 map over the qsplit buffer as [2B rows x d], box {64, 1} (gather4 source)
+// presplit: map128 / map32 are 3D bf16 maps over the pre-split [rows][2][d] arena, box {64, 1, 128|32}
 cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, const CUtensorMap& qmap,
-                           const TcScanParams& p, int grid, cudaStream_t s);
+                           const TcScanParams& p, int grid, cudaStream_t s, bool presplit);
 cudaError_t launch_qsplit(const float* Q, void* out, long long B, int d, cudaStream_t s);
 cudaError_t launch_scan(const CUtensorMap& map256, const CUtensorMap& map32, const ScanParams& p,
                         int grid, cudaStream_t s);

@@ -87,18 +87,26 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<const uint32_t*>(&v);
 }
 
+// kPre = false: fp32 arena; converter warps split x into (x1, x2) in TMEM; TS MMAs, 32-dim stages.
+// kPre = true : pre-split bf16 (x1, x2) arena ([rows][2][d], built with the index); the producer TMA-loads
+//               both 64-dim tiles of a stage straight into 128B-swizzled smem and the MMAs read A from
+//               smem (SS) — no conversion on the scan path; converter warps are idle.
+template <bool kPre>
 __global__ void __launch_bounds__(kThreads, 1)
     ivf_scan_tc_kernel(const __grid_constant__ CUtensorMap map128, const __grid_constant__ CUtensorMap map32,
                        const __grid_constant__ CUtensorMap qmap, const TcScanParams p) {
   extern __shared__ unsigned char smem_raw[];
-  const int d = p.d, nks = d / 32;
+  const int d = p.d, nks = kPre ? d / 64 : d / 32;
   const Smem sm = carve(smem_raw, d);
+  // ring geometry: the same 96 KiB hold 6 x 16 KiB fp32 stages or 3 x 32 KiB pre-split stages
+  constexpr int RS = kPre ? kStages / 2 : kStages;
+  constexpr int RB = kPre ? 2 * kStageBytes : kStageBytes;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], 4);  // the 4 converter warps
+      mbar_init(&sm.empty[s], kPre ? 1 : 4);  // MMA commit (pre-split) or the 4 converter warps
     }
     for (int i = 0; i < kXBufs; ++i) {
       mbar_init(&sm.xfull[i], 4);
@@ -108,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.afull[i], 1);
       mbar_init(&sm.aempty[i], 4);
       mbar_init(&sm.tfull[i], 1);
-      mbar_init(&sm.tempty[i], 1 + 4 + 4 + 4);
+      mbar_init(&sm.tempty[i], kPre ? 1 + 4 : 1 + 4 + 4 + 4);
     }
     mbar_init(sm.bfull, 1);
     mbar_init(sm.bempty, 1);
@@ -169,15 +177,29 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int nb = (rows + 31) >> 5;
           const int row = (int)(T.src_row + rt * kRows);
           for (int ks = 0; ks < nks; ++ks, ++u) {
-            const int s = u % kStages;
-            mbar_wait(&sm.empty[s], ((u / kStages) & 1) ^ 1);
-            const uint32_t dst = sm.xs + s * kStageBytes;
-            if (nb == 4) {
-              mbar_arrive_expect_tx(&sm.full[s], kStageBytes);
-              tma_load_2d_u32(dst, &map128, ks * 32, row, &sm.full[s]);
+            const int s = u % RS;
+            mbar_wait(&sm.empty[s], ((u / RS) & 1) ^ 1);
+            const uint32_t dst = sm.xs + s * RB;
+            if constexpr (kPre) {  // x1 and x2 tiles of a 64-dim slice: 2 x 16 KiB
+              if (nb == 4) {
+                mbar_arrive_expect_tx(&sm.full[s], 2 * kRows * 128);
+                tma_load_3d_u32(dst, &map128, ks * 64, 0, row, &sm.full[s]);
+                tma_load_3d_u32(dst + kRows * 128, &map128, ks * 64, 1, row, &sm.full[s]);
+              } else {
+                mbar_arrive_expect_tx(&sm.full[s], 2 * nb * 4096);
+                for (int b = 0; b < nb; ++b) {
+                  tma_load_3d_u32(dst + b * 4096, &map32, ks * 64, 0, row + b * 32, &sm.full[s]);
+                  tma_load_3d_u32(dst + kRows * 128 + b * 4096, &map32, ks * 64, 1, row + b * 32, &sm.full[s]);
+                }
+              }
             } else {
-              mbar_arrive_expect_tx(&sm.full[s], nb * 4096);
-              for (int b = 0; b < nb; ++b) tma_load_2d_u32(dst + b * 4096, &map32, ks * 32, row + b * 32, &sm.full[s]);
+              if (nb == 4) {
+                mbar_arrive_expect_tx(&sm.full[s], kStageBytes);
+                tma_load_2d_u32(dst, &map128, ks * 32, row, &sm.full[s]);
+              } else {
+                mbar_arrive_expect_tx(&sm.full[s], nb * 4096);
+                for (int b = 0; b < nb; ++b) tma_load_2d_u32(dst + b * 4096, &map32, ks * 32, row + b * 32, &sm.full[s]);
+              }
             }
           }
         }
@@ -206,6 +228,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t dacc = tmem + a * kAccCols;
         for (int ks = 0; ks < nks; ++ks, ++u) {
+          if constexpr (kPre) {
+            const int s = u % RS;
+            mbar_wait(&sm.full[s], (u / RS) & 1);
+            tc_fence_after();
+            if (lane == 0) {
+              const unsigned char* st = reinterpret_cast<unsigned char*>(smem_raw) + (sm.xs - smem_u32(smem_raw)) +
+                                        s * RB;
+              const uint64_t a1 = umma_desc_sw128(st), a2 = umma_desc_sw128(st + kRows * 128);
+              const uint64_t bd = bdesc0 + (uint64_t)(ks * (kBSlice >> 4));
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) {
+                const uint32_t acc = (ks | kk) != 0;
+                mma_bf16_ss(dacc, a1 + kk * 2, bd + (uint64_t)(kk * 2), ida, acc);
+                mma_bf16_ss(dacc + kBRows, a2 + kk * 2, bd + (uint64_t)(kk * 2), idb, acc);
+              }
+              tc_commit(&sm.empty[s]);
+            }
+            __syncwarp();
+            continue;
+          }
           const int xb = u % kXBufs;
           mbar_wait(&sm.xfull[xb], (u / kXBufs) & 1);
           tc_fence_after();
@@ -216,6 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int kk = 0; kk < 2; ++kk) {
               const uint32_t acc = (ks | kk) != 0;
+              if (p.debug_skip & 4) continue;
               mma_bf16_ts(dacc, xa + kk * 8, bd + (uint64_t)(kk * 2), ida, acc);
               mma_bf16_ts(dacc + kBRows, xa + 16 + kk * 8, bd + (uint64_t)(kk * 2), idb, acc);
             }
@@ -232,13 +275,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   // ------------------------------------------------- warps 2-5 / 10-13: converter groups 0 / 1
   else if (warp < 6 || warp >= 10) {
+    if constexpr (kPre) goto done;  // no conversion on the pre-split path
     const int quarter = warp & 3;
     const int grp = warp >= 10;
     const int tid = threadIdx.x - 64;  // 0..127 (group 0 only loads B)
     const int r = quarter * 32 + lane;
     uint32_t u = 0;
+    // Software-pipelined: the TMEM stores of stage u complete (wait::st) while stage u+2 is being
+    // converted; xfull[u] is published one iteration late (the 8-deep TMEM ring absorbs it) and
+    // always before this warp blocks on the next tile.
+    int pend = -1;  // TMEM buffer whose stores are in flight
+    auto flush = [&]() {
+      if (pend >= 0) {
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.xfull[pend]);
+        pend = -1;
+      }
+    };
     for (uint32_t ti = 0;; ++ti) {
       const int slot = ti & 1;
+      flush();
       mbar_wait(&sm.tfull[slot], (ti >> 1) & 1);
       const int t = sm.tring[slot];
       __syncwarp();
@@ -254,6 +312,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t b1[16], b2[16];
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
+            if (p.debug_skip & 2) {
+              b1[2 * g] = b1[2 * g + 1] = b2[2 * g] = b2[2 * g + 1] = 0u;
+              continue;
+            }
             const uint4 v = lds128(row + ((g ^ (r & 7)) << 4));
             const float x0 = __uint_as_float(v.x), x1 = __uint_as_float(v.y);
             const float x2 = __uint_as_float(v.z), x3 = __uint_as_float(v.w);
@@ -265,15 +327,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.empty[s]);
+          flush();  // previous stage's stores have had a whole conversion to land
           mbar_wait(&sm.xempty[xb], ((u / kXBufs) & 1) ^ 1);
           tc_fence_after();
           const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + kXCol0 + xb * 32;
           tmem_st16(ta, b1);
           tmem_st16(ta + 16, b2);
-          tmem_st_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.xfull[xb]);
+          pend = xb;
+          if (p.debug_skip & 8) flush();  // A/B switch: unpipelined stores
         }
       }
     }
@@ -343,6 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         named_bar_sync(2, 128);
         const long long gbase = T.grow0 + (long long)rt * kRows;
+        if (p.debug_skip & 1) continue;
 #pragma unroll
         for (int j = 0; j < kOwn; ++j) {
           const int g = ew + 4 * j;
@@ -409,6 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
+done:
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -440,17 +503,22 @@ size_t scan_tc_smem_bytes(int d) {
 }
 
 cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, const CUtensorMap& qmap,
-                           const TcScanParams& p, int grid, cudaStream_t s) {
+                           const TcScanParams& p, int grid, cudaStream_t s, bool presplit) {
   if (p.d % 64 != 0) return cudaErrorInvalidValue;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(ivf_scan_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(ivf_scan_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(ivf_scan_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   const size_t smem = scan_tc_smem_bytes(p.d);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  ivf_scan_tc_kernel<<<grid, kThreads, smem, s>>>(map128, map32, qmap, p);
+  if (presplit)
+    ivf_scan_tc_kernel<true><<<grid, kThreads, smem, s>>>(map128, map32, qmap, p);
+  else
+    ivf_scan_tc_kernel<false><<<grid, kThreads, smem, s>>>(map128, map32, qmap, p);
   return cudaGetLastError();
 }
 

@@ -35,9 +35,12 @@ def test_engine_matches_golden(engine, name):
     _check(idx.search(q, c["nprobe"], c["k"]), GOLD[f"{name}/out_ids"], GOLD[f"{name}/out_dists"])
 
 
+@pytest.mark.parametrize("presplit", ["1", "0"])
 @pytest.mark.parametrize("B,nprobe,k", [(1, 8, 10), (7, 1, 1), (32, 16, 10), (100, 64, 20), (33, 5, 24),
                                         (256, 16, 10), (300, 3, 24)])
-def test_engine_vs_oracle_synthetic(engine, oracle, B, nprobe, k):
+def test_engine_vs_oracle_synthetic(engine, oracle, B, nprobe, k, presplit, monkeypatch):
+    # presplit=1: conversion-free scan over the bf16 (x1, x2) copy; 0: converter-warp scan over fp32
+    monkeypatch.setenv("RD_PRESPLIT", presplit)
     n, d, nlist = 40000, 768, 64
     desc = engine.desc(n, d, nlist)
     q, _ = engine.synth_queries(desc, 1000, B)
