@@ -266,6 +266,25 @@ def run_ours(args, cfg):
         e2e = {"value": B * args.steps / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": B * d * 4,
                "d2h_bytes_per_step": B * k * 12}
 
+    # batch sweep of BASELINE configs[1] (same index, queries in HBM): q/s per batch size
+    sweep = {}
+    if world == 1 and not args.no_sweep and args.config == "c2":
+        for Bs in (1, 8, 32, 64, 128, 256, 512, 1024):
+            qs_s = torch.from_numpy(lib.synth_queries(desc, 70_000_000 + Bs, Bs)[0]).cuda()
+            oi = torch.empty((Bs, k), dtype=torch.int64, device="cuda")
+            od = torch.empty((Bs, k), dtype=torch.float32, device="cuda")
+            for _ in range(3):
+                idx.search_device(qs_s.data_ptr(), Bs, nprobe, k, oi.data_ptr(), od.data_ptr(), stream=sptr)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 10
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(reps):
+                idx.search_device(qs_s.data_ptr(), Bs, nprobe, k, oi.data_ptr(), od.data_ptr(), stream=sptr)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            sweep[str(Bs)] = Bs * reps / (e0.elapsed_time(e1) / 1000.0)
+
     # roofline of the dominant kernel (N4 resident list scan), measured over the timed region
     peaks = measured_peaks()
     peak = peaks["hbm_gbs"] if peaks else 6650.0
@@ -295,6 +314,7 @@ def run_ours(args, cfg):
         "step_breakdown_ms": {k2: tm[k2] / max(1, tm["searches"]) for k2 in ("coarse_ms", "scan_ms", "tail_ms", "total_ms")},
         "step_gbps_algorithmic": st["bytes_algorithmic"] / (ms_step * 1e-3) / 1e9,
         "gpu_launches": launches_per_search * args.steps + (args.steps if world > 1 else 0),
+        "batch_sweep_qps": sweep,
         "clocks": clk.summary(),
         "certified": {"margin_failures": st["margin_failures"], "probe_failures": st["probe_failures"]},
         "index": {"build_s": build_s, "lists_resident": info["lists_resident"], "hbm_bytes": info["hbm_bytes"],
@@ -323,6 +343,7 @@ def main():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--cpu-sample", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = dict(CONFIGS[args.config])

@@ -242,6 +242,7 @@ struct rd_index {
   DBuf<float> xsplit;
   CUtensorMap xmap128{}, xmap32{};
   bool presplit = false;
+  bool budgeted = false;  // last placement had an HBM byte budget
   DBuf<long long> d_list_off, d_ids, d_res_row0;
   DBuf<const float*> d_list_base;
   std::vector<uint8_t> resident;      // host mask
@@ -368,16 +369,17 @@ struct rd_index {
     presplit = false;
     xsplit.reset();
     const char* env = std::getenv("RD_PRESPLIT");
-    if (d % 64 != 0 || (env && std::atoi(env) == 0) || n_resident != n || n == 0) return;
+    // a byte budget (e.g. the LLM reservation, C5) must not be exceeded by a second copy
+    if (d % 64 != 0 || (env && std::atoi(env) == 0) || n_resident == 0 || budgeted) return;
     size_t fr = 0, tot = 0;
     CK(cudaMemGetInfo(&fr, &tot));
-    const size_t need = (size_t)n * d * 4;
+    const size_t need = (size_t)n_resident * d * 4;
     if (need + (size_t(4) << 30) > fr) return;  // not enough room: the converter path stays
-    xsplit.alloc((size_t)n * d);
-    CK(rd::launch_qsplit(arena.p, xsplit.p, n, d, 0));
+    xsplit.alloc((size_t)n_resident * d);
+    CK(rd::launch_qsplit(arena.p, xsplit.p, n_resident, d, 0));
     CK(cudaDeviceSynchronize());
-    xmap128 = make_split_map(xsplit.p, n, d, rd::kTcRows);
-    xmap32 = make_split_map(xsplit.p, n, d, 32);
+    xmap128 = make_split_map(xsplit.p, n_resident, d, rd::kTcRows);
+    xmap32 = make_split_map(xsplit.p, n_resident, d, 32);
     presplit = true;
   }
 
@@ -706,6 +708,7 @@ int rd_index_place(rd_index* h, const rd_placement* p) {
     h->res_row0 = new_res;
     h->host_row0 = new_host_row;
     h->n_resident = n_res;
+    h->budgeted = p->hbm_budget_bytes != 0;
     h->upload_residency();
     h->build_presplit();
     // staging ring
