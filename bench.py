@@ -254,17 +254,39 @@ def run_ours(args, cfg):
     ms_step = ms / args.steps
     value = B * args.steps / (ms / 1000.0)
 
-    # e2e: public C-ABI with host buffers (H2D queries + D2H ids/dists each step)
-    e2e = None
-    if world == 1:
-        for i in range(min(args.warmup, 2)):
-            idx.search(qs[i], nprobe, k)
-        t0 = time.perf_counter()
-        for i in range(args.warmup, nb):
-            idx.search(qs[i], nprobe, k)
-        e2e_s = time.perf_counter() - t0
-        e2e = {"value": B * args.steps / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": B * d * 4,
-               "d2h_bytes_per_step": B * k * 12}
+    # e2e: public C-ABI rd_search with pinned host buffers (H2D queries + D2H ids/dists every
+    # step, inside the timed region); at N > 1 every rank searches its shard and rank 0 merges
+    # the gathered per-shard results with rd_merge_topk (host)
+    hq = [torch.from_numpy(q).pin_memory().numpy() for q in qs]
+    hi = torch.empty((B, k), dtype=torch.int64).pin_memory().numpy()
+    hd = torch.empty((B, k), dtype=torch.float32).pin_memory().numpy()
+
+    def e2e_step(i):
+        idx.search_into(hq[i], nprobe, k, hi, hd)
+        if world > 1:
+            ti = torch.from_numpy(hi).cuda()
+            td = torch.from_numpy(hd).cuda()
+            dist.all_gather(gi, ti)
+            dist.all_gather(gd, td)
+            if rank == 0:
+                lib.merge_topk(torch.stack(gi).cpu().numpy(), torch.stack(gd).cpu().numpy())
+
+    for i in range(min(args.warmup, 2)):
+        e2e_step(i)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for i in range(args.warmup, nb):
+        e2e_step(i)
+    if world > 1:
+        dist.barrier()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": B * args.steps / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": B * d * 4,
+           "d2h_bytes_per_step": B * k * 12}
 
     # batch sweep of BASELINE configs[1] (same index, queries in HBM): q/s per batch size
     sweep = {}

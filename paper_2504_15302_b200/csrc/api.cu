@@ -759,7 +759,7 @@ Plan make_plan(const rd_index* h, long long B, int nprobe) {
 }
 
 void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, long long* d_ids, float* d_dists,
-               cudaStream_t s, bool sync, rd_search_stats* st) {
+               cudaStream_t s, bool sync, rd_search_stats* st, const std::function<void()>& before_sync = {}) {
   if (nprobe < 1 || k < 1) throw_rd(RD_ERR_INVALID, "search: nprobe >= 1 and k >= 1 required");
   if (k > rd::kMaxK) throw_rd(RD_ERR_INVALID, "search: k <= %d supported, got %d", rd::kMaxK, k);
   if (std::min(nprobe, h->nlist) + rd::kCoarseExtra > 512) throw_rd(RD_ERR_INVALID, "search: nprobe <= 480 supported");
@@ -970,6 +970,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     std::memset(st, 0, sizeof *st);
     st->kernel_launches = launches;
   }
+  if (before_sync) before_sync();  // e.g. the host path's result copies, ordered before the one sync
   if (sync) {
     CK(cudaMemcpyAsync(w.h_counters.p, w.counters.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(w.h_fails.p, w.fails.p, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, s));
@@ -1029,21 +1030,36 @@ int rd_search(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int3
     CK(cudaSetDevice(h->device));
     auto& w = h->ws;
     const size_t qn = (size_t)B * h->d, rn = (size_t)B * k;
-    w.hq.ensure(qn);
-    w.hi.ensure(rn);
-    w.hd.ensure(rn);
     w.q.ensure(qn);
     w.ids.ensure(rn);
     w.dists.ensure(rn);
-    std::memcpy(w.hq.p, queries, qn * sizeof(float));
+    // caller buffers that are already page-locked are copied directly; others go through the
+    // handle's pinned staging buffers
+    auto pinned = [](const void* ptr) {
+      cudaPointerAttributes a;
+      if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+      return a.type == cudaMemoryTypeHost;
+    };
+    const bool pq = pinned(queries), pi = pinned(out_ids), pd = pinned(out_dists);
+    const float* qsrc = queries;
+    if (!pq) {
+      w.hq.ensure(qn);
+      std::memcpy(w.hq.p, queries, qn * sizeof(float));
+      qsrc = w.hq.p;
+    }
+    long long* idst = pi ? reinterpret_cast<long long*>(out_ids) : (w.hi.ensure(rn), w.hi.p);
+    float* ddst = pd ? out_dists : (w.hd.ensure(rn), w.hd.p);
     cudaStream_t s = 0;
-    CK(cudaMemcpyAsync(w.q.p, w.hq.p, qn * sizeof(float), cudaMemcpyHostToDevice, s));
-    do_search(h, w.q.p, B, nprobe, k, w.ids.p, w.dists.p, s, true, st);
-    CK(cudaMemcpyAsync(w.hi.p, w.ids.p, rn * sizeof(long long), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(w.hd.p, w.dists.p, rn * sizeof(float), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    std::memcpy(out_ids, w.hi.p, rn * sizeof(long long));
-    std::memcpy(out_dists, w.hd.p, rn * sizeof(float));
+    CK(cudaMemcpyAsync(w.q.p, qsrc, qn * sizeof(float), cudaMemcpyHostToDevice, s));
+    do_search(h, w.q.p, B, nprobe, k, w.ids.p, w.dists.p, s, true, st, [&] {
+      CK(cudaMemcpyAsync(idst, w.ids.p, rn * sizeof(long long), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(ddst, w.dists.p, rn * sizeof(float), cudaMemcpyDeviceToHost, s));
+    });
+    if (!pi) std::memcpy(out_ids, w.hi.p, rn * sizeof(long long));
+    if (!pd) std::memcpy(out_dists, w.hd.p, rn * sizeof(float));
     if (st) st->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   });
 }

@@ -301,6 +301,14 @@ class Index:
                                                 C.byref(st)), "search")
         return SearchResult(ids, dists, st.as_dict())
 
+    def search_into(self, queries: np.ndarray, nprobe: int, k: int, out_ids: np.ndarray,
+                    out_dists: np.ndarray) -> dict:
+        """rd_search into caller-owned host buffers (page-locked buffers are copied directly)."""
+        st = SearchStats()
+        self._lib.check(self._lib.lib.rd_search(self._h, _fp(queries), queries.shape[0], nprobe, k, _i64p(out_ids),
+                                                _fp(out_dists), C.byref(st)), "search")
+        return st.as_dict()
+
     def search_device(self, q_ptr: int, B: int, nprobe: int, k: int, ids_ptr: int, dists_ptr: int,
                       stream: int = 0, sync: bool = False) -> dict:
         """Device-pointer search (inputs resident in HBM); enqueues on `stream`."""

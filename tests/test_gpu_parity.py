@@ -140,3 +140,17 @@ def test_search_device_matches_host_path(engine):
     assert st["margin_failures"] == 0
     np.testing.assert_array_equal(di.cpu().numpy(), h.ids)
     np.testing.assert_array_equal(dd.cpu().numpy(), h.dists)
+
+
+def test_search_into_pinned_buffers(engine):
+    import torch
+    desc = engine.desc(30000, 768, 64)
+    idx = engine.synthetic_index(desc)
+    q, _ = engine.synth_queries(desc, 9, 40)
+    want = idx.search(q, 8, 10)
+    hq = torch.from_numpy(q).pin_memory().numpy()
+    hi = torch.empty((40, 10), dtype=torch.int64).pin_memory().numpy()
+    hd = torch.empty((40, 10), dtype=torch.float32).pin_memory().numpy()
+    idx.search_into(hq, 8, 10, hi, hd)
+    np.testing.assert_array_equal(hi, want.ids)
+    np.testing.assert_array_equal(hd, want.dists)
