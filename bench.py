@@ -172,8 +172,15 @@ def run_ours(args, cfg):
     from paper_2504_15302_b200.retriever import engine
 
     world, rank, local = dist_env()
+    # one process per GPU; RD_DIST_BACKEND=gloo (with ranks sharing a device) only exercises the
+    # multi-rank code path on a single-GPU box
+    backend = os.environ.get("RD_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
-        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend, rank=rank, world_size=world)
     torch.cuda.set_device(local)
     lib = engine()
     B, k, nprobe, d = cfg["batch"], cfg["k"], cfg["nprobe"], cfg["d"]
