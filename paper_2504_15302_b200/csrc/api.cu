@@ -804,7 +804,9 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   } else {
     CK(rd::launch_coarse(d_q, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, s));
   }
-  rd::SelectParams sp{w.Dc.p, d_q, w.qnorm.p, h->centroids.p, w.probes.p, w.fails.p, (int)B, nl, nprobe, d, h->cmax};
+  w.qthr.ensure(B);
+  rd::SelectParams sp{w.Dc.p, d_q, w.qnorm.p, h->centroids.p, w.probes.p, w.fails.p, (int)B, nl, nprobe, d, h->cmax,
+                      h->d_list_off.p, h->d_res_row0.p, h->arena.p, h->xmax, w.qthr.p};
   CK(rd::launch_select(sp, s));
   launches += 4;
   rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
@@ -814,13 +816,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   launches += 4;
   CK(cudaEventRecord(e1, s));
   CK(cudaMemsetAsync(w.part_count.p, 0, sizeof(int) * B, s));
-  w.qthr.ensure(B);
-  {
-    rd::SeedParams sd{w.probes.p, nprobe, d_q, w.qnorm.p, h->d_list_off.p, h->d_res_row0.p, h->arena.p, d, h->xmax,
-                      w.qthr.p, (int)B};
-    CK(rd::launch_seed(sd, s));
-    launches += 1;
-  }
+
   const bool has_off = h->slots > 0;
   if (has_off) {  // fetch the probe histogram for host-side staging decisions
     w.h_nq.ensure(nl);
@@ -834,8 +830,10 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
                     w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p};
   rd::TcScanParams tc{w.tiles.p, w.meta.p, w.meta.p + 1, w.qsplit.p, w.qnorm.p, w.list_q.p, h->xnorm.p,
                       w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p, h->debug_skip};
-  CK(rd::launch_scan(h->map256, h->map32, sc, h->num_sms, s));
-  launches += 1;
+  if (d % 64 != 0 || h->tc_min_q > 1) {  // FFMA tiles exist only in these cases
+    CK(rd::launch_scan(h->map256, h->map32, sc, h->num_sms, s));
+    launches += 1;
+  }
   if (d % 64 == 0) {  // the tensor-core path stages 64-dim bf16 query slices; otherwise every tile is FFMA
     CK(rd::launch_scan_tc(h->presplit ? h->xmap128 : h->map128, h->presplit ? h->xmap32 : h->map32, gmap, tc,
                           h->num_sms, s, h->presplit));
@@ -1089,7 +1087,8 @@ int rd_probe(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32
     } else {
       CK(rd::launch_coarse(w.q.p, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, 0));
     }
-    rd::SelectParams sp{w.Dc.p, w.q.p, w.qnorm.p, h->centroids.p, w.probes.p, w.fails.p, (int)B, nl, nprobe, d, h->cmax};
+    rd::SelectParams sp{w.Dc.p, w.q.p, w.qnorm.p, h->centroids.p, w.probes.p, w.fails.p, (int)B, nl, nprobe, d, h->cmax,
+                        h->d_list_off.p, h->d_res_row0.p, h->arena.p, h->xmax, nullptr};
     CK(rd::launch_select(sp, 0));
     CK(cudaMemcpy(out_lists, w.probes.p, sizeof(int) * B * nprobe, cudaMemcpyDeviceToHost));
   });

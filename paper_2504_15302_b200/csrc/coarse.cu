@@ -371,6 +371,47 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
     if (certified) break;
   }
   for (int i = tid; i < p.nprobe; i += kSelThreads) p.probes[(size_t)b * p.nprobe + i] = i < np ? cand[i] : -1;
+
+  // fused seed: exact distances to the first 32 rows of the nearest resident probed list with
+  // >= 32 rows; threshold = max + 2*eps_scan (valid upper bound on the final 32nd-best approximate
+  // distance, so the scan's certification holds; see merge.cu seed_kernel)
+  if (p.qthr) {
+    __shared__ int lsel;
+    __shared__ float red[kSelThreads / 32];
+    if (tid == 0) {
+      lsel = -1;
+      for (int i = 0; i < np; ++i) {
+        const int l = cand[i];
+        if (p.res_row0[l] >= 0 && p.list_off[l + 1] - p.list_off[l] >= 32) {
+          lsel = l;
+          break;
+        }
+      }
+    }
+    __syncthreads();
+    const int l = lsel;
+    if (l < 0) {
+      if (tid == 0) p.qthr[b] = 0x7f7f7f7f;
+    } else {
+      const float e = exact_l2_group8(q, p.arena + (size_t)(p.res_row0[l] + grp) * p.d, p.d, j8);
+      float m = e;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if ((tid & 31) == 0) red[tid >> 5] = m;
+      __syncthreads();
+      if (tid == 0) {
+        float mx = red[0];
+        for (int i = 1; i < kSelThreads / 32; ++i) mx = fmaxf(mx, red[i]);
+        const float qn = p.qnorm[b];
+        const float u = 5.9604645e-8f;
+        const float eps =
+            2.f * ((p.d / 2 + 8) * u * 2.f * sqrtf(qn) * p.xmax + 8.f * u * (qn + p.xmax * p.xmax)) + 1e-30f;
+        const float thr = mx + 2.f * eps;
+        const int ti = __float_as_int(thr);
+        p.qthr[b] = ti >= 0 ? ti : ti ^ 0x7fffffff;
+      }
+    }
+  }
 }
 
 }  // namespace

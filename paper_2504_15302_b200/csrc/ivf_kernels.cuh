@@ -93,6 +93,12 @@ struct SelectParams {
   unsigned* probe_fail;    // device scalar
   int B, nlist, nprobe, d;
   float cmax;              // max ||c||
+  // fused seeding of the scan's pruning threshold (see SeedParams); qthr == nullptr skips it
+  const long long* list_off;
+  const long long* res_row0;
+  const float* arena;
+  float xmax;
+  int* qthr;
 };
 cudaError_t launch_select(const SelectParams& p, cudaStream_t s);
 
