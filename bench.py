@@ -43,6 +43,11 @@ CONFIGS = {
                workload="ivf-flat 10M x 768 fp32, nlist 4096, nprobe 64, k 10, batch 1024, HBM-resident"),
     "c3": dict(n=10_000_000, d=768, nlist=4096, nprobe=64, k=10, batch=1024, offload=0.5,
                workload="ivf-flat 10M x 768 fp32, nlist 4096, nprobe 64, k 10, batch 1024, 50% lists in pinned host DRAM"),
+    # C4: 100M x 768 sharded over the GPUs of one box (nlist 16384, nprobe 64 — BASELINE leaves them
+    # open; SURVEY §7 recommends these). With one GPU, one shard of 8 (12.5M rows) is run: the work
+    # of one rank of the 8-GPU job.
+    "c4": dict(n=100_000_000, d=768, nlist=16384, nprobe=64, k=10, batch=1024, offload=0.0, total=True,
+               workload="ivf-flat 100M x 768 fp32 sharded over the box's GPUs, nlist 16384, nprobe 64, k 10, batch 1024"),
     "c5": dict(n=10_000_000, d=768, nlist=4096, nprobe=128, k=20, batch=64, offload=None,
                workload="ivf-flat 10M x 768 fp32, nlist 4096, nprobe 128, k 20, batch 64, under a 70B LLM-decode HBM reservation"),
 }
@@ -184,8 +189,13 @@ def run_ours(args, cfg):
     torch.cuda.set_device(local)
     lib = engine()
     B, k, nprobe, d = cfg["batch"], cfg["k"], cfg["nprobe"], cfg["d"]
-    n_total = cfg["n"] * world
-    desc = lib.desc(n_total, d, cfg["nlist"], shard=rank, num_shards=world)
+    if cfg.get("total"):  # fixed total knowledge base (C4): rank r holds stripe r of max(world, 8)
+        n_total = cfg["n"]
+        shards = world if world > 1 else 8
+    else:  # weak scaling: cfg["n"] rows per GPU
+        n_total = cfg["n"] * world
+        shards = world
+    desc = lib.desc(n_total, d, cfg["nlist"], shard=rank, num_shards=shards)
     t0 = time.time()
     idx = lib.synthetic_index(desc, device=local)
     build_s = time.time() - t0
@@ -330,15 +340,17 @@ def run_ours(args, cfg):
         return
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (splitmix64 spec, SURVEY §8d), generated on device",
+        "scaling": "strong" if cfg.get("total") else "weak",
         "config": {"workload": cfg["workload"], "global_batch": B, "nprobe": nprobe, "k": k, "n_per_gpu": info["n"],
-                   "n_total": n_total, "nlist": cfg["nlist"], "d": d, "parallelism": f"shard{world}",
+                   "n_total": n_total, "nlist": cfg["nlist"], "d": d,
+                   "parallelism": f"shard{world}" if shards == world else f"one shard of {shards} on 1 GPU",
                    "l2": "inputs larger than L2 (index %.1f GB)" % (info["n"] * d * 4 / 1e9)},
         "e2e": e2e,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "ivf_scan_kernel (N4)", "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
+                     "kernel": "ivf_scan_tc_kernel (N5; FFMA ivf_scan_kernel N4 when d % 64 != 0)", "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
                      "bytes_per_launch": scan_bytes, "avg_launch_ms": scan_ms},
         "step_breakdown_ms": {k2: tm[k2] / max(1, tm["searches"]) for k2 in ("coarse_ms", "scan_ms", "tail_ms", "total_ms")},
         "step_gbps_algorithmic": st["bytes_algorithmic"] / (ms_step * 1e-3) / 1e9,
