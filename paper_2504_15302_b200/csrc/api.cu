@@ -228,6 +228,9 @@ struct rd_index {
   int num_sms = 148;
   int tc_min_q = rd::kTcMinQ;
   int debug_skip = 0;  // profiling only
+  bool dbg_ts = std::getenv("RD_DEBUG_TS") != nullptr;  // profiling only: select checkpoints to stderr
+  int stage_max_b = -1;  // batches up to this size stage exact-distance rows in smem (-1: 2 x SMs)
+  bool stage_rows(long long B) const { return B <= (stage_max_b >= 0 ? stage_max_b : 2LL * num_sms); }
   long long n = 0;
   int d = 0, nlist = 0;
   std::vector<long long> list_off;  // host copy, nlist + 1
@@ -244,6 +247,7 @@ struct rd_index {
   bool presplit = false;
   bool budgeted = false;  // last placement had an HBM byte budget
   DBuf<long long> d_list_off, d_ids, d_res_row0;
+  DBuf<int> d_row_list;  // list of each global row (merge: row -> list without a search)
   DBuf<const float*> d_list_base;
   std::vector<uint8_t> resident;      // host mask
   std::vector<long long> res_row0;    // host: row in arena or -1
@@ -331,6 +335,7 @@ struct rd_index {
       for (auto& e : r) CK(cudaEventCreate(&e));
     if (const char* v = std::getenv("RD_TC_MIN_Q")) tc_min_q = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("RD_DEBUG_SKIP")) debug_skip = std::atoi(v);
+    if (const char* v = std::getenv("RD_STAGE_MAX_B")) stage_max_b = std::atoi(v);
     // the tensor-core scan stages bf16 query slices of 64 dims
   }
 
@@ -339,6 +344,8 @@ struct rd_index {
     for (int l = 0; l < nlist; ++l) max_len = std::max(max_len, list_off[l + 1] - list_off[l]);
     d_list_off.alloc(nlist + 1);
     CK(cudaMemcpy(d_list_off.p, list_off.data(), sizeof(long long) * (nlist + 1), cudaMemcpyHostToDevice));
+    d_row_list.alloc(n);
+    CK(rd::launch_row_list(d_list_off.p, nlist, d_row_list.p, 0));
     // all lists resident in list order
     resident.assign(nlist, 1);
     res_row0.resize(nlist);
@@ -579,7 +586,7 @@ int rd_index_info_get(const rd_index* h, rd_index_info* o) {
     o->nlist = h->nlist;
     o->n_resident = h->n_resident;
     for (int l = 0; l < h->nlist; ++l) o->lists_resident += h->resident[l];
-    o->hbm_bytes = (uint64_t)h->n_resident * h->d * 4 + (uint64_t)h->n * 12 + (uint64_t)h->nlist * (h->d + 1) * 4 +
+    o->hbm_bytes = (uint64_t)h->n_resident * h->d * 4 + (uint64_t)h->n * 16 + (uint64_t)h->nlist * (h->d + 1) * 4 +
                    (uint64_t)h->slots * h->slot_rows * h->d * 4 + (uint64_t)h->xsplit.n * 4;
     o->host_pinned_bytes = (uint64_t)h->host_arena.n * 4;
     o->staging_slots = h->slots;
@@ -806,8 +813,23 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   }
   w.qthr.ensure(B);
   rd::SelectParams sp{w.Dc.p, d_q, w.qnorm.p, h->centroids.p, w.probes.p, w.fails.p, (int)B, nl, nprobe, d, h->cmax,
-                      h->d_list_off.p, h->d_res_row0.p, h->arena.p, h->xmax, w.qthr.p};
-  CK(rd::launch_select(sp, s));
+                      h->d_list_off.p, h->d_res_row0.p, h->arena.p, h->xmax, w.qthr.p, 0};
+  if (h->dbg_ts) {
+    static unsigned long long* dbg = nullptr;
+    if (!dbg) CK(cudaMalloc(&dbg, 32 * sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(dbg, 0, 32 * sizeof(unsigned long long), s));
+    sp.dbg = dbg;
+    CK(rd::launch_select(sp, h->stage_rows(B), s));
+    if (std::getenv("RD_DEBUG_TWICE")) CK(rd::launch_select(sp, h->stage_rows(B), s));
+    unsigned long long t[32];
+    CK(cudaMemcpyAsync(t, dbg, sizeof t, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    fprintf(stderr, "select ncand=%lld namb=%lld cycles:", (long long)t[15], (long long)t[14]);
+    for (int i = 1; i < 14; ++i) fprintf(stderr, " %d:%lld", i, t[16 + i] ? (long long)(t[16 + i] - t[16]) : -1LL);
+    fprintf(stderr, "\n");
+  } else {
+    CK(rd::launch_select(sp, h->stage_rows(B), s));
+  }
   launches += 4;
   rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
                     w.list_ntile.p, w.list_toff.p, w.list_q.p, w.tiles.p, w.ff_tiles.p, w.meta.p, w.counters.p,
@@ -956,9 +978,9 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   w.fb_dist.ensure((size_t)B * nprobe * rd::kTopK);
   w.fb_id.ensure((size_t)B * nprobe * rd::kTopK);
   rd::MergeParams mp{w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d_q, w.qnorm.p, h->d_list_off.p,
-                     h->d_list_base.p, h->d_ids.p, nl, d, k, h->xmax, d_ids, d_dists, w.fails.p + 1,
-                     w.fail_list.p, (int)B};
-  CK(rd::launch_merge(mp, s));
+                     h->d_list_base.p, h->d_ids.p, h->d_row_list.p, nl, d, k, h->xmax, d_ids, d_dists,
+                     w.fails.p + 1, w.fail_list.p, (int)B};
+  CK(rd::launch_merge(mp, h->stage_rows(B), s));
   rd::FallbackParams fp{w.fail_list.p, w.fails.p + 1, w.probes.p, nprobe, d_q, h->d_list_off.p, h->d_list_base.p,
                         h->d_ids.p, nl, d, k, w.fb_dist.p, w.fb_id.p, d_ids, d_dists};
   CK(rd::launch_fallback(fp, h->num_sms, s));
@@ -1088,8 +1110,8 @@ int rd_probe(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32
       CK(rd::launch_coarse(w.q.p, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, 0));
     }
     rd::SelectParams sp{w.Dc.p, w.q.p, w.qnorm.p, h->centroids.p, w.probes.p, w.fails.p, (int)B, nl, nprobe, d, h->cmax,
-                        h->d_list_off.p, h->d_res_row0.p, h->arena.p, h->xmax, nullptr};
-    CK(rd::launch_select(sp, 0));
+                        h->d_list_off.p, h->d_res_row0.p, h->arena.p, h->xmax, nullptr, 1};
+    CK(rd::launch_select(sp, h->stage_rows(B), 0));
     CK(cudaMemcpy(out_lists, w.probes.p, sizeof(int) * B * nprobe, cudaMemcpyDeviceToHost));
   });
 }

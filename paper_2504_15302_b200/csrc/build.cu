@@ -58,7 +58,20 @@ __global__ void max_f32_kernel(const float* __restrict__ v, long long n, float* 
   if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(out), __float_as_int(m));  // m >= 0
 }
 
+// one CTA per list: row_list[off[l] .. off[l+1]) = l
+__global__ void row_list_kernel(const long long* __restrict__ off, int* __restrict__ row_list) {
+  const int l = blockIdx.x;
+  const long long r0 = off[l], r1 = off[l + 1];
+  for (long long r = r0 + threadIdx.x; r < r1; r += blockDim.x) row_list[r] = l;
+}
+
 }  // namespace
+
+cudaError_t launch_row_list(const long long* off, int nlist, int* row_list, cudaStream_t s) {
+  if (nlist == 0) return cudaSuccess;
+  row_list_kernel<<<nlist, 256, 0, s>>>(off, row_list);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_gen_centroids(float* C, int nlist, int d, uint64_t sc, cudaStream_t s) {
   const long long total = (long long)nlist * d;

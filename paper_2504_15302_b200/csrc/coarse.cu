@@ -207,38 +207,130 @@ __device__ __forceinline__ float block_reduce_max(float v, float* sh) {
   return r;
 }
 
-// dynamic smem: keys[nlist] (u32; approximate distances as floats, then exact keys in the fallback)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// profiling only (RD_DEBUG_TS): globaltimer / clock64 checkpoints of CTA 0
+#define RD_TS(i)                                                 \
+  do {                                                           \
+    if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0) {          \
+      p.dbg[i] = gtimer();                                       \
+      p.dbg[16 + i] = clock64();                                 \
+    }                                                            \
+  } while (0)
+
+// dynamic smem: keys[nlist] (u32; approximate distances as floats, then exact keys in the fallback),
+// q widened to fp64 [d]; kStage (small batches: one CTA per query is latency-bound) adds q as fp32
+// [d] and a 32-row staging area [32][d + kStagePad] filled by bulk (TMA) row copies.
+//
+// Search mode (p.exact_order == 0) needs the probe SET only (the scan, the plan and the exact
+// fallback are order-independent; the order only picks the seeding list). With the coarse GEMM's
+// error bound eps (|approx + ||q||^2 - exact| <= eps), a candidate is
+//   sure-in   if at most nprobe candidates (itself included) have approx <= its approx + 2 eps and
+//             its approx + 2 eps is below every excluded centroid's approx (hi_edge),
+//   sure-out  if nprobe candidates have approx < its approx - 2 eps,
+//   ambiguous otherwise,
+// and the excluded centroids are sure-out when nprobe candidates lie below hi_edge - 2 eps. The
+// exact top-nprobe set is then the sure-in candidates plus the best ambiguous ones by (canonical
+// exact distance, list id) — only those few need the fp64 sum. Exact-order mode (rd_probe) and
+// uncertified queries recompute every candidate (or every centroid) exactly.
+template <bool kStage>
 __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const SelectParams p) {
-  extern __shared__ uint32_t keys[];
+  extern __shared__ __align__(16) uint32_t keys[];
   __shared__ int hist[2048];
   __shared__ int scan_sh[8];
   __shared__ float fsh[8];
   __shared__ int cand[kSelMaxCand];
   __shared__ float cdist[kSelMaxCand];
   __shared__ uint32_t sel_prefix, sel_k;
-  __shared__ int certified, ncand_s, found_bin;
-  const int b = blockIdx.x, tid = threadIdx.x;
-  const int nlist = p.nlist;
-  const float* q = p.queries + (size_t)b * p.d;
+  __shared__ int certified, ncand_s, found_bin, below_s, nin_s, na_s, lsel;
+  __shared__ unsigned char lok[kSelMaxCand];  // candidate list can seed (resident, >= 32 rows)
+  __shared__ unsigned long long amin;
+  __shared__ __align__(8) uint64_t bar;
+  RD_TS(0);
+  const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nlist = p.nlist, d = p.d;
+  const float* q = p.queries + (size_t)b * d;
   const int grp = tid >> 3, j8 = tid & 7;
   const int np = min(p.nprobe, nlist);
   const float* drow = p.Dc + (size_t)b * nlist;
   float* vals = reinterpret_cast<float*>(keys);
+  double* qd = reinterpret_cast<double*>(vals + ((nlist + 3) & ~3));
+  float* qf = reinterpret_cast<float*>(qd + d);  // kStage
+  float* st = qf + d;                            // kStage: [32][d + kStagePad]
+  const int ds = d + kStagePad;
+  uint32_t bphase = 0;
+  if (tid == 0) {
+    amin = ~0ull;
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  float qv[1024 / kSelThreads];  // d <= 1024; stored after the distance row's loads are in flight
+#pragma unroll
+  for (int k = 0; k < 1024 / kSelThreads; ++k) qv[k] = tid + k * kSelThreads < d ? q[tid + k * kSelThreads] : 0.f;
+  const float qn = p.qnorm[b];
+  // bulk-copies rows r < nrows (row_ptr(r), device memory) into st; every thread waits
+  auto stage_bulk = [&](int nrows, auto row_ptr) {
+    if (warp == 0) {
+      if (lane == 0) mbar_arrive_expect_tx(&bar, (uint32_t)(nrows * d * 4));
+      __syncwarp();
+      if (lane < nrows) bulk_g2s(st + lane * ds, row_ptr(lane), (uint32_t)(d * 4), &bar);
+    }
+    mbar_wait(&bar, bphase);
+    bphase ^= 1;
+  };
+
   float vmin = __builtin_huge_valf(), vmax = -__builtin_huge_valf();
-  for (int j = tid; j < nlist; j += kSelThreads) {
-    const float v = drow[j];
-    vals[j] = v;
-    vmin = fminf(vmin, v);
-    vmax = fmaxf(vmax, v);
+  int jmin = 0;
+  constexpr int kVB = 16;  // row loads in flight per thread
+  for (int j0 = tid; j0 < nlist; j0 += kVB * kSelThreads) {
+    float v[kVB];
+#pragma unroll
+    for (int k = 0; k < kVB; ++k) {
+      const int j = j0 + k * kSelThreads;
+      v[k] = j < nlist ? drow[j] : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < kVB; ++k) {
+      const int j = j0 + k * kSelThreads;
+      if (j < nlist) {
+        vals[j] = v[k];
+        if (v[k] < vmin) jmin = j;
+        vmin = fminf(vmin, v[k]);
+        vmax = fmaxf(vmax, v[k]);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 1024 / kSelThreads; ++k)
+    if (tid + k * kSelThreads < d) {
+      qd[tid + k * kSelThreads] = (double)qv[k];
+      if constexpr (kStage) qf[tid + k * kSelThreads] = qv[k];
+    }
+  if constexpr (kStage) {  // approximate nearest centroid: warm L2 with its list's first 32 rows (the likely seed)
+    __syncthreads();
+    if (vmin < __builtin_huge_valf()) atomicMin(&amin, ((unsigned long long)f2key(vmin) << 32) | (unsigned)jmin);
   }
   vmin = block_reduce_min(vmin, fsh);
   vmax = block_reduce_max(vmax, fsh);
+  if constexpr (kStage) {
+    if (p.qthr && amin != ~0ull) {
+      const int l = (int)(amin & 0xffffffffu);
+      const long long r0 = p.res_row0[l];
+      if (r0 >= 0 && p.list_off[l + 1] - p.list_off[l] >= 32) {
+        const int lines = d / 32;  // 128 B lines per row
+        for (int i = tid; i < 32 * lines; i += kSelThreads)
+          prefetch_l2(p.arena + (size_t)(r0 + i / lines) * d + (i % lines) * 32);
+      }
+    }
+  }
+  RD_TS(1);
   const int Cwant = min(nlist, p.nprobe + kCoarseExtra);
 
-  // attempt 0: a candidate set {approx < hi} of size in [C, kSelMaxCand], found with value-linear
-  // 2048-bin histograms (refined inside the crossing bin when it is too dense); exact refine;
-  // certification with hi as the lower bound of every excluded approximate distance.
-  // attempt 1 (uncertified or no usable threshold): exact distances to every centroid.
+  // candidate set {approx < hi_edge} of size in [C, kSelMaxCand], found with value-linear 2048-bin
+  // histograms (refined inside the crossing bin when it is too dense)
   int ncand = -1;
   float hi_edge = __builtin_huge_valf();
   if (Cwant == nlist && nlist <= kSelMaxCand) {
@@ -295,6 +387,7 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
       }
     }
   }
+  RD_TS(2);
   if (ncand >= 0) {
     if (tid == 0) ncand_s = 0;
     __syncthreads();
@@ -302,83 +395,200 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
       if (vals[j] < hi_edge) cand[atomicAdd(&ncand_s, 1)] = j;
     __syncthreads();
   }
+  RD_TS(3);
+  if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0) p.dbg[15] = (unsigned long long)ncand;
 
-  for (int attempt = (ncand >= 0 ? 0 : 1); attempt < 2; ++attempt) {
-    int C;
-    if (attempt == 0) {
-      C = ncand;
-    } else {
-      // exact keys for every centroid, then the np smallest by (exact distance, list id)
-      for (int c0 = 0; c0 < nlist; c0 += kSelThreads / 8) {
-        const int c = c0 + grp;
-        const int cc = c < nlist ? c : nlist - 1;
-        const float e = exact_l2_group8(q, p.centroids + (size_t)cc * p.d, p.d, j8);
-        __syncthreads();
-        if (c < nlist && j8 == 0) keys[c] = f2key(e);
+  const float u = 5.9604645e-8f;
+  const float eps = 2.f * ((d + 4) * u * 2.f * sqrtf(qn) * p.cmax + 8.f * u * (qn + p.cmax * p.cmax)) + 1e-30f;
+  bool done = false;
+
+  // ------------------------------------------------------------ search mode: the probe set
+  if (!p.exact_order && ncand >= 0) {
+    const int C = ncand;
+    const float e2 = 2.f * eps;
+    int* state = hist;           // [512] 0 out, 1 in (sure or chosen), 2 ambiguous
+    int* byrank = hist + 512;    // [512] candidate index by approximate rank
+    int* ambl = hist + 1024;     // [512] ambiguous candidates in approximate-rank order
+    float* adist = reinterpret_cast<float*>(hist + 1536);  // [512] their exact distances
+    for (int i = tid; i < C; i += kSelThreads) {
+      const int l = cand[i];
+      cdist[i] = vals[l];
+      // seeding eligibility, resolved here so the rank-order walk below needs no global loads
+      if (p.qthr) lok[i] = p.res_row0[l] >= 0 && p.list_off[l + 1] - p.list_off[l] >= 32;
+    }
+    if (tid == 0) below_s = 0;
+    __syncthreads();
+    // rank and window counts: one group of 8 lanes per candidate, lane j8 scans k = j8 (mod 8)
+    int below = 0;
+    for (int i0 = 0; i0 < C; i0 += kSelThreads / 8) {
+      const int i = i0 + grp;
+      const float vi = i < C ? cdist[i] : 0.f;
+      const int ci = i < C ? cand[i] : 0;
+      int r = 0, lt = 0, lo = 0;
+      if (i < C)
+#pragma unroll 4
+        for (int k = j8; k < C; k += 8) {
+          const float vk = cdist[k];
+          r += vk < vi || (vk == vi && cand[k] < ci);
+          lt += vk <= vi + e2;
+          lo += vk < vi - e2;
+        }
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        r += __shfl_xor_sync(0xffffffffu, r, o);
+        lt += __shfl_xor_sync(0xffffffffu, lt, o);
+        lo += __shfl_xor_sync(0xffffffffu, lo, o);
       }
-      __syncthreads();
-      C = np;
-      select_smallest(keys, nlist, C, hist, scan_sh, cand, &sel_prefix, &sel_k);
+      if (i < C && j8 == 0) {
+        byrank[r] = i;
+        state[i] = lo >= np ? 0 : (lt <= np && vi + e2 < hi_edge) ? 1 : 2;
+        below += vi < hi_edge - e2;
+      }
     }
-    for (int c0 = 0; c0 < C; c0 += kSelThreads / 8) {
-      const int c = c0 + grp;
-      const int cc = c < C ? c : C - 1;
-      const float e = exact_l2_group8(q, p.centroids + (size_t)cand[cc] * p.d, p.d, j8);
-      if (c < C && j8 == 0) cdist[c] = e;
-    }
-    int P2 = 1;
-    while (P2 < C) P2 <<= 1;
-    for (int c = C + tid; c < P2; c += kSelThreads) {
-      cdist[c] = __builtin_huge_valf();
-      cand[c] = 0x7fffffff;
+    if (below) atomicAdd(&below_s, below);
+    __syncthreads();
+    RD_TS(7);
+    if (warp == 0) {  // ambiguous list in rank order; sure-in count
+      int nin = 0, na = 0;
+      for (int r0 = 0; r0 < C; r0 += 32) {
+        const int r = r0 + lane;
+        const int stt = r < C ? state[byrank[r]] : 0;
+        const unsigned mi = __ballot_sync(0xffffffffu, stt == 1), ma = __ballot_sync(0xffffffffu, stt == 2);
+        if (stt == 2) ambl[na + __popc(ma & ((1u << lane) - 1u))] = byrank[r];
+        nin += __popc(mi);
+        na += __popc(ma);
+      }
+      if (lane == 0) {
+        nin_s = nin;
+        na_s = na;
+      }
     }
     __syncthreads();
-    for (int size = 2; size <= P2; size <<= 1) {
-      for (int jj = size >> 1; jj > 0; jj >>= 1) {
-        for (int i = tid; i < P2; i += kSelThreads) {
-          const int l = i ^ jj;
-          if (l > i) {
-            const bool up = (i & size) == 0;
-            const float di = cdist[i], dl = cdist[l];
-            const int ii = cand[i], il = cand[l];
-            const bool l_less = dl < di || (dl == di && il < ii);
-            if (l_less == up) {
-              cdist[i] = dl;
-              cdist[l] = di;
-              cand[i] = il;
-              cand[l] = ii;
+    RD_TS(8);
+    const int nin = nin_s, na = na_s, need = np - nin;
+    if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0) p.dbg[14] = (unsigned long long)na;
+    if (below_s >= np && need >= 0 && need <= na) {
+      if (need > 0 && need < na) {  // the best `need` ambiguous candidates by exact (distance, list id)
+        for (int a0 = 0; a0 < na; a0 += kSelThreads / 8) {
+          const int rows = min(kSelThreads / 8, na - a0);
+          const int a = a0 + grp;
+          float e;
+          if constexpr (kStage) {
+            stage_bulk(rows, [&](int r) { return p.centroids + (size_t)cand[ambl[a0 + r]] * d; });
+            e = exact_l2_group8_qd(qd, st + grp * ds, a < na ? d : 0, j8);
+            __syncthreads();  // the staging area is reused by the next chunk
+          } else {
+            e = exact_l2_group8_qd(qd, p.centroids + (size_t)cand[ambl[a < na ? a : na - 1]] * d, d, j8);
+          }
+          if (a < na && j8 == 0) adist[a] = e;
+        }
+        __syncthreads();
+        for (int a = tid; a < na; a += kSelThreads) {
+          const float da = adist[a];
+          const int ia = cand[ambl[a]];
+          int r = 0;
+          for (int k = 0; k < na; ++k) {
+            const float dk = adist[k];
+            r += dk < da || (dk == da && cand[ambl[k]] < ia);
+          }
+          state[ambl[a]] = r < need ? 1 : 0;
+        }
+      } else {
+        for (int a = tid; a < na; a += kSelThreads) state[ambl[a]] = need == na ? 1 : 0;
+      }
+      __syncthreads();
+      RD_TS(9);
+      if (warp == 0) {  // probes in approximate-rank order; seeding list = first resident one with >= 32 rows
+        int n = 0, ls = -1;
+        for (int r0 = 0; r0 < C; r0 += 32) {
+          const int r = r0 + lane;
+          const int i = r < C ? byrank[r] : 0;
+          const bool in = r < C && state[i] == 1;
+          const unsigned m = __ballot_sync(0xffffffffu, in);
+          if (in) {
+            const int l = cand[i];
+            p.probes[(size_t)b * p.nprobe + n + __popc(m & ((1u << lane) - 1u))] = l;
+            if (p.qthr) {
+              const unsigned mo = __ballot_sync(m, lok[i] != 0);
+              if (ls < 0 && mo) ls = __shfl_sync(m, l, __ffs(mo) - 1);
             }
           }
+          ls = __shfl_sync(0xffffffffu, ls, __ffs(m ? m : 1u) - 1);
+          n += __popc(m);
+        }
+        for (int i = np + lane; i < p.nprobe; i += 32) p.probes[(size_t)b * p.nprobe + i] = -1;
+        if (lane == 0) lsel = ls;
+      }
+      done = true;
+    } else if (tid == 0) {
+      atomicAdd(p.probe_fail, 1u);
+    }
+    __syncthreads();
+  }
+
+  // ------------------------------------------------------------ exact order (rd_probe) / fallback
+  if (!done) {
+    for (int attempt = (ncand >= 0 && p.exact_order ? 0 : 1); attempt < 2; ++attempt) {
+      int C;
+      if (attempt == 0) {
+        C = ncand;
+      } else {
+        // exact keys for every centroid, then the np smallest by (exact distance, list id)
+        for (int c0 = 0; c0 < nlist; c0 += kSelThreads / 8) {
+          const int c = c0 + grp;
+          const int cc = c < nlist ? c : nlist - 1;
+          const float e = exact_l2_group8_qd(qd, p.centroids + (size_t)cc * d, d, j8);
+          __syncthreads();
+          if (c < nlist && j8 == 0) keys[c] = f2key(e);
+        }
+        __syncthreads();
+        C = np;
+        select_smallest(keys, nlist, C, hist, scan_sh, cand, &sel_prefix, &sel_k);
+      }
+      for (int c0 = 0; c0 < C; c0 += kSelThreads / 8) {
+        const int c = c0 + grp;
+        const int cc = c < C ? c : C - 1;
+        const float e = exact_l2_group8_qd(qd, p.centroids + (size_t)cand[cc] * d, d, j8);
+        if (c < C && j8 == 0) cdist[c] = e;
+      }
+      // rank sort by (exact distance, list id): keys are distinct (list ids)
+      __syncthreads();
+      {
+        float* rd_ = reinterpret_cast<float*>(hist);  // hist is free here: [0, 512) dists, [512, 1024) ids
+        int* rc_ = hist + kSelMaxCand;
+        for (int i = tid; i < C; i += kSelThreads) {
+          const float di = cdist[i];
+          const int ii = cand[i];
+          int r = 0;
+          for (int jx = 0; jx < C; ++jx) {
+            const float dj = cdist[jx];
+            r += dj < di || (dj == di && cand[jx] < ii);
+          }
+          rd_[r] = di;
+          rc_[r] = ii;
+        }
+        __syncthreads();
+        for (int i = tid; i < C; i += kSelThreads) {
+          cdist[i] = rd_[i];
+          cand[i] = rc_[i];
         }
         __syncthreads();
       }
-    }
-    if (tid == 0) {
-      int ok = 1;
-      if (attempt == 0) {
-        // every excluded centroid has approx >= hi_edge; the GEMM's error bound turns that into
-        // a lower bound on its exact distance
-        const float qn = p.qnorm[b];
-        const float u = 5.9604645e-8f;
-        const float eps = 2.f * ((p.d + 4) * u * 2.f * sqrtf(qn) * p.cmax + 8.f * u * (qn + p.cmax * p.cmax)) + 1e-30f;
-        const float lower = hi_edge + qn - eps;
-        ok = lower > cdist[np - 1];
+      if (tid == 0) {
+        int ok = 1;
+        if (attempt == 0) {
+          // every excluded centroid has approx >= hi_edge; the GEMM's error bound turns that into
+          // a lower bound on its exact distance
+          ok = hi_edge + qn - eps > cdist[np - 1];
+        }
+        certified = ok;
+        if (!ok) atomicAdd(p.probe_fail, 1u);
       }
-      certified = ok;
-      if (!ok) atomicAdd(p.probe_fail, 1u);
+      __syncthreads();
+      if (certified) break;
     }
-    __syncthreads();
-    if (certified) break;
-  }
-  for (int i = tid; i < p.nprobe; i += kSelThreads) p.probes[(size_t)b * p.nprobe + i] = i < np ? cand[i] : -1;
-
-  // fused seed: exact distances to the first 32 rows of the nearest resident probed list with
-  // >= 32 rows; threshold = max + 2*eps_scan (valid upper bound on the final 32nd-best approximate
-  // distance, so the scan's certification holds; see merge.cu seed_kernel)
-  if (p.qthr) {
-    __shared__ int lsel;
-    __shared__ float red[kSelThreads / 32];
-    if (tid == 0) {
+    for (int i = tid; i < p.nprobe; i += kSelThreads) p.probes[(size_t)b * p.nprobe + i] = i < np ? cand[i] : -1;
+    if (p.qthr && tid == 0) {
       lsel = -1;
       for (int i = 0; i < np; ++i) {
         const int l = cand[i];
@@ -389,29 +599,42 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
       }
     }
     __syncthreads();
+  }
+  RD_TS(5);
+
+  // fused seed: fp32 distances to the first 32 rows of the seeding list; threshold = max * (1 + rel
+  // bound) + 2 eps_scan, a valid upper bound on the final 32nd-best approximate distance, so the
+  // scan's certification holds (merge.cu)
+  if (p.qthr) {
+    __shared__ float red[kSelThreads / 32];
     const int l = lsel;
     if (l < 0) {
       if (tid == 0) p.qthr[b] = 0x7f7f7f7f;
     } else {
-      const float e = exact_l2_group8(q, p.arena + (size_t)(p.res_row0[l] + grp) * p.d, p.d, j8);
+      const float* r0 = p.arena + (size_t)p.res_row0[l] * d;
+      float e;
+      if constexpr (kStage) {
+        stage_bulk(32, [&](int r) { return r0 + (size_t)r * d; });
+        e = l2_group8_f32(qf, st + grp * ds, d, j8);
+      } else {
+        e = l2_group8_f32(q, r0 + (size_t)grp * d, d, j8);
+      }
       float m = e;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-      if ((tid & 31) == 0) red[tid >> 5] = m;
+      if (lane == 0) red[warp] = m;
       __syncthreads();
       if (tid == 0) {
         float mx = red[0];
         for (int i = 1; i < kSelThreads / 32; ++i) mx = fmaxf(mx, red[i]);
-        const float qn = p.qnorm[b];
-        const float u = 5.9604645e-8f;
-        const float eps =
-            2.f * ((p.d / 2 + 8) * u * 2.f * sqrtf(qn) * p.xmax + 8.f * u * (qn + p.xmax * p.xmax)) + 1e-30f;
-        const float thr = mx + 2.f * eps;
-        const int ti = __float_as_int(thr);
-        p.qthr[b] = ti >= 0 ? ti : ti ^ 0x7fffffff;
+        const float eps_s =
+            2.f * ((d / 2 + 8) * u * 2.f * sqrtf(qn) * p.xmax + 8.f * u * (qn + p.xmax * p.xmax)) + 1e-30f;
+        const float thr = mx * (1.f + 2.f * l2_f32_rel_bound(d)) + 2.f * eps_s;
+        p.qthr[b] = f2ord(thr);
       }
     }
   }
+  RD_TS(6);
 }
 
 }  // namespace
@@ -423,16 +646,24 @@ cudaError_t launch_coarse(const float* Q, const float* C, const float* cnorm, fl
   return cudaGetLastError();
 }
 
-cudaError_t launch_select(const SelectParams& p, cudaStream_t s) {
+cudaError_t launch_select(const SelectParams& p, bool stage, cudaStream_t s) {
   if (p.nprobe + kCoarseExtra > kSelMaxCand) return cudaErrorInvalidValue;
-  const size_t smem = sizeof(uint32_t) * (size_t)p.nlist;
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(coarse_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t keys = sizeof(uint32_t) * (size_t)((p.nlist + 3) & ~3);
+  const size_t qd = sizeof(double) * (size_t)p.d;
+  const size_t smem =
+      stage ? keys + qd + sizeof(float) * ((size_t)p.d + 32 * (size_t)(p.d + kStagePad)) : keys + qd;
+  if (stage && smem > 200 * 1024) stage = false;  // very large nlist: the direct-load variant
+  static size_t attr[2] = {0, 0};
+  if (smem > 48 * 1024 && smem > attr[stage]) {
+    cudaError_t e = cudaFuncSetAttribute(stage ? coarse_select_kernel<true> : coarse_select_kernel<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = smem;
+    attr[stage] = smem;
   }
-  coarse_select_kernel<<<p.B, kSelThreads, smem, s>>>(p);
+  if (stage)
+    coarse_select_kernel<true><<<p.B, kSelThreads, smem, s>>>(p);
+  else
+    coarse_select_kernel<false><<<p.B, kSelThreads, smem, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -99,8 +99,11 @@ struct SelectParams {
   const float* arena;
   float xmax;
   int* qthr;
+  int exact_order;         // 1: probes in exact (distance, list id) order (rd_probe); 0: the set (search)
+  unsigned long long* dbg = nullptr;  // RD_DEBUG_TS: globaltimer checkpoints of CTA 0
 };
-cudaError_t launch_select(const SelectParams& p, cudaStream_t s);
+// stage: q and candidate rows go through shared memory (latency-bound small batches)
+cudaError_t launch_select(const SelectParams& p, bool stage, cudaStream_t s);
 
 struct PlanParams {
   const int* probes;          // B x nprobe
@@ -131,6 +134,7 @@ struct MergeParams {
   const long long* list_off;       // nlist + 1
   const float* const* list_base;   // nlist: device-visible pointer to the list's first row
   const long long* ids;            // n (global row order)
+  const int* row_list;             // n: list of each global row
   int nlist, d, k;
   float xmax;
   long long* out_ids;              // B x k
@@ -139,7 +143,8 @@ struct MergeParams {
   int* fail_list;                  // B: ids of uncertified queries (exact fallback work list)
   int B;
 };
-cudaError_t launch_merge(const MergeParams& p, cudaStream_t s);
+// stage: the 32 rerank rows go through shared memory (latency-bound small batches)
+cudaError_t launch_merge(const MergeParams& p, bool stage, cudaStream_t s);
 
 // Seeds each query's pruning threshold before the scan: 32 rows of its nearest resident
 // probed list, exact distances, threshold = max + 2*eps (a valid upper bound on the final
@@ -188,5 +193,7 @@ cudaError_t launch_gen_vectors(float* X, const long long* ids, long long n, int 
                                const float* C, uint64_t sa, uint64_t sx, float sigma, cudaStream_t s);
 cudaError_t launch_row_norms(const float* X, long long n, int d, float* out, cudaStream_t s);
 cudaError_t launch_max_f32(const float* v, long long n, float* out, cudaStream_t s);
+// row_list[r] = l for off[l] <= r < off[l + 1]
+cudaError_t launch_row_list(const long long* off, int nlist, int* row_list, cudaStream_t s);
 
 }  // namespace rd

@@ -17,42 +17,54 @@ namespace {
 constexpr float kInf = __builtin_huge_valf();
 constexpr long long kNoKey = 0x7fffffffffffffffll;
 
-__device__ __forceinline__ int list_of_row(const long long* off, int nlist, long long row) {
-  int lo = 0, hi = nlist;  // off[lo] <= row < off[hi]
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (__ldg(off + mid) <= row)
-      lo = mid;
-    else
-      hi = mid;
-  }
-  return lo;
-}
-
+// One CTA per query. kStage (small batches): the 32 candidate rows are staged in shared memory with
+// every load in flight before the canonical sums run; otherwise each group of 8 lanes streams its
+// row from global memory (enough CTAs are resident to hide the latency).
+template <bool kStage>
 __global__ void __launch_bounds__(256) merge_rerank_kernel(const MergeParams p) {
+  extern __shared__ __align__(16) float dyn[];  // kStage: q[d], rows[32][d + kStagePad]
   __shared__ float sd[8][kTopK];
   __shared__ long long sk[8][kTopK];
   __shared__ float ex_d[kTopK];
   __shared__ long long ex_id[kTopK];
+  __shared__ const float* rowp[kTopK];
   __shared__ float tau_s;
   const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cnt = min(p.part_count[b], p.part_cap);
+  const float* q = p.queries + (size_t)b * p.d;
+  if constexpr (kStage) {
+    for (int i = tid; i < (p.d >> 2); i += 256) reinterpret_cast<float4*>(dyn)[i] = reinterpret_cast<const float4*>(q)[i];
+  }
 
+  // partial lists are ascending; read reversed to get a descending batch. Four partials per warp
+  // are loaded before any is merged so their latencies overlap.
   float ld = kInf;
   long long lk = kNoKey;
-  for (int i = warp; i < cnt; i += 8) {
-    // partials are ascending; read reversed to get a descending batch
-    const size_t o = ((size_t)b * p.part_cap + i) * kTopK + (kTopK - 1 - lane);
-    const float bd = p.part_dist[o];
-    const int br = p.part_row[o];
-    const float v = br < 0 ? kInf : bd;
-    const long long key = br < 0 ? kNoKey : (long long)br;
-    if (pair_less(v, key, ld, lk)) {
-      ld = v;
-      lk = key;
+  for (int i0 = warp; i0 < cnt; i0 += 32) {
+    float bd[4];
+    int br[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + 8 * u;
+      br[u] = -1;
+      if (i < cnt) {
+        const size_t o = ((size_t)b * p.part_cap + i) * kTopK + (kTopK - 1 - lane);
+        bd[u] = p.part_dist[o];
+        br[u] = p.part_row[o];
+      }
     }
 #pragma unroll
-    for (int j = 16; j > 0; j >>= 1) bitonic_step(ld, lk, lane, j, true);
+    for (int u = 0; u < 4; ++u) {
+      if (i0 + 8 * u >= cnt) break;
+      const float v = br[u] < 0 ? kInf : bd[u];
+      const long long key = br[u] < 0 ? kNoKey : (long long)br[u];
+      if (pair_less(v, key, ld, lk)) {
+        ld = v;
+        lk = key;
+      }
+#pragma unroll
+      for (int j = 16; j > 0; j >>= 1) bitonic_step(ld, lk, lane, j, true);
+    }
   }
   sd[warp][lane] = ld;
   sk[warp][lane] = lk;
@@ -68,31 +80,37 @@ __global__ void __launch_bounds__(256) merge_rerank_kernel(const MergeParams p) 
 #pragma unroll
       for (int j = 16; j > 0; j >>= 1) bitonic_step(ld, lk, lane, j, true);
     }
-    sd[0][lane] = ld;
-    sk[0][lane] = lk;
+    // candidate rows: list of the row (row_list), its device-visible address and user id
+    const float* xp = nullptr;
+    long long id = kNoKey;
+    if (lk != kNoKey) {
+      const int l = __ldg(p.row_list + lk);
+      xp = p.list_base[l] + (size_t)(lk - __ldg(p.list_off + l)) * p.d;
+      id = __ldg(p.ids + lk);
+    }
+    rowp[lane] = xp;
+    ex_id[lane] = id;
     if (lane == 31) tau_s = ld;
   }
   __syncthreads();
 
   // exact rerank: thread (c = tid/8, j = tid%8)
   const int c = tid >> 3, j8 = tid & 7;
-  const long long row = sk[0][c];
-  const float* q = p.queries + (size_t)b * p.d;
-  long long id = kNoKey;
-  const float* x = q;
-  int dd = 0;  // a padded slot runs zero terms so the warp stays converged for the shuffles
-  if (row != kNoKey) {
-    const int l = list_of_row(p.list_off, p.nlist, row);
-    x = p.list_base[l] + (size_t)(row - p.list_off[l]) * p.d;
-    dd = p.d;
-    id = p.ids[row];
+  const float* xp = rowp[c];
+  float e;
+  if constexpr (kStage) {
+    float* st = dyn + p.d;
+    int nrows = 0;  // candidates are ascending, so the valid ones are a prefix
+    while (nrows < kTopK && rowp[nrows]) ++nrows;
+    stage_rows_ld<256>(st, nrows, p.d, [&](int r) { return rowp[r]; });
+    __syncthreads();
+    e = exact_l2_group8_impl<false>(dyn, st + c * (p.d + kStagePad), xp ? p.d : 0, j8);
+  } else {
+    // a padded slot runs zero terms so the warp stays converged for the shuffles
+    e = exact_l2_group8_any(q, xp ? xp : q, xp ? p.d : 0, j8);
   }
-  float e = exact_l2_group8_any(q, x, dd, j8);
-  if (row == kNoKey) e = kInf;
-  if (j8 == 0) {
-    ex_d[c] = e;
-    ex_id[c] = id;
-  }
+  if (!xp) e = kInf;
+  if (j8 == 0) ex_d[c] = e;
   __syncthreads();
   if (warp == 0) {
     float dd = ex_d[lane];
@@ -270,9 +288,21 @@ cudaError_t launch_fallback(const FallbackParams& p, int num_sms, cudaStream_t s
   return cudaGetLastError();
 }
 
-cudaError_t launch_merge(const MergeParams& p, cudaStream_t s) {
+cudaError_t launch_merge(const MergeParams& p, bool stage, cudaStream_t s) {
   if (p.B == 0) return cudaSuccess;
-  merge_rerank_kernel<<<p.B, 256, 0, s>>>(p);
+  if (stage) {
+    const size_t smem = sizeof(float) * ((size_t)p.d + kTopK * (size_t)(p.d + kStagePad));
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+      cudaError_t e = cudaFuncSetAttribute(merge_rerank_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+      attr = smem;
+    }
+    merge_rerank_kernel<true><<<p.B, 256, smem, s>>>(p);
+  } else {
+    merge_rerank_kernel<false><<<p.B, 256, 0, s>>>(p);
+  }
   return cudaGetLastError();
 }
 

@@ -62,6 +62,29 @@ __device__ __forceinline__ float exact_l2_group8_impl(const float* __restrict__ 
   s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
   return __double2float_rn(s);
 }
+// same value with q already widened to fp64 (shared memory): half the conversions
+__device__ __forceinline__ float exact_l2_group8_qd(const double* qd, const float* x, int d, int j) {
+  double s = 0.0;
+  int t = j;
+  for (; t + 56 < d; t += 64) {
+    float xv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) xv[i] = x[t + 8 * i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const double df = __dsub_rn(qd[t + 8 * i], (double)xv[i]);
+      s = __dadd_rn(s, __dmul_rn(df, df));
+    }
+  }
+  for (; t < d; t += 8) {
+    const double df = __dsub_rn(qd[t], (double)x[t]);
+    s = __dadd_rn(s, __dmul_rn(df, df));
+  }
+  s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
+  s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+  s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
+  return __double2float_rn(s);
+}
 __device__ __forceinline__ float exact_l2_group8(const float* __restrict__ q, const float* __restrict__ x, int d,
                                                  int j) {
   return exact_l2_group8_impl<true>(q, x, d, j);
@@ -74,6 +97,79 @@ __device__ __forceinline__ float exact_l2_group8_any(const float* __restrict__ q
 // ---------------------------------------------------------------- PTX: smem, mbarrier, TMA
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ---------------------------------------------------------------- row staging for exact distances
+// The canonical sum is a chain of d/8 dependent fp64 adds per lane; reading x from global memory
+// inside that chain costs one memory round trip per 8-element batch (12 at d = 768). At low
+// occupancy (small batches) that latency is the whole cost, so the rows are first staged into
+// shared memory with every load in flight at once, then summed from smem.
+constexpr int kStagePad = 8;  // floats of padding per staged row: 4 groups of a warp hit distinct banks
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+// 1D bulk (TMA) copy global -> shared, completion counted on an mbarrier's tx-count
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// fp32 squared distance by groups of 8 lanes (same lane/class layout as the canonical sum);
+// |result - ||q - x||^2| <= l2_f32_rel_bound(d) * ||q - x||^2
+__device__ __forceinline__ float l2_group8_f32(const float* q, const float* x, int d, int j) {
+  float s = 0.f;
+  for (int t = j; t < d; t += 8) {
+    const float df = q[t] - x[t];
+    s = fmaf(df, df, s);
+  }
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  s += __shfl_xor_sync(0xffffffffu, s, 4);
+  return s;
+}
+__host__ __device__ __forceinline__ float l2_f32_rel_bound(int d) { return 2.f * (d / 8 + 8) * 5.9604645e-8f; }
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// rows r < nrows of row_ptr(r) (device memory, 16 B aligned, d % 4 == 0) -> dst[r * (d + kStagePad)],
+// cp.async, all in flight; the caller waits (cp_async_wait_all) and syncs
+template <int NT, class RowPtr>
+__device__ __forceinline__ void stage_rows_async(float* dst, int nrows, int d, RowPtr row_ptr) {
+  const int v4 = d >> 2, ds = d + kStagePad;
+  for (int i = threadIdx.x; i < nrows * v4; i += NT) {
+    const int r = i / v4, c = i - r * v4;
+    cp_async16(dst + r * ds + 4 * c, row_ptr(r) + 4 * c);
+  }
+}
+// same with ordinary loads (rows possibly in mapped host memory), 8 loads in flight per thread
+template <int NT, class RowPtr>
+__device__ __forceinline__ void stage_rows_ld(float* dst, int nrows, int d, RowPtr row_ptr) {
+  const int v4 = d >> 2, ds = d + kStagePad, tot = nrows * v4;
+  for (int i0 = threadIdx.x; i0 < tot; i0 += 8 * NT) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * NT;
+      if (i < tot) {
+        const int r = i / v4, c = i - r * v4;
+        v[u] = *reinterpret_cast<const float4*>(row_ptr(r) + 4 * c);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * NT;
+      if (i < tot) {
+        const int r = i / v4, c = i - r * v4;
+        *reinterpret_cast<float4*>(dst + r * ds + 4 * c) = v[u];
+      }
+    }
+  }
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
