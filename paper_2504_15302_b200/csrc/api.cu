@@ -266,7 +266,7 @@ struct rd_index {
   struct Ws {
     DBuf<float> qnorm, Dc, q, dists, qsplit;
     DBuf<int> probes, list_nq, list_qoff, list_ntile, list_toff, list_q, part_count, part_row, meta, off_meta;
-    DBuf<unsigned> bitmap, fails;
+    DBuf<unsigned> bitmap, fails, fb_ctr;
     DBuf<rd::ScanTile> tiles, ff_tiles, off_tiles;
     DBuf<unsigned long long> counters;
     DBuf<float> part_dist;
@@ -802,10 +802,11 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   cudaEvent_t e0 = te[0], e1 = te[1], e2 = te[2], e3 = h->ev[3], e_plan = h->ev[4], e_off = h->ev[5];
   unsigned long long launches = 0;
   CK(cudaEventRecord(e0, s));
-  CK(cudaMemsetAsync(w.fails.p, 0, 2 * sizeof(unsigned), s));
-  CK(rd::launch_row_norms(d_q, B, d, w.qnorm.p, s));
-  CK(rd::launch_qsplit(d_q, w.qsplit.p, B, d, s));
-  if (d % 64 == 0) {
+  // ||q||^2 and the query split (the tensor-core scan's operand) in one pass
+  CK(rd::launch_qprep(d_q, B, d, w.qnorm.p, d % 64 == 0 ? w.qsplit.p : nullptr, w.fails.p, w.part_count.p, s));
+  if (rd::coarse_small((int)B)) {
+    CK(rd::launch_coarse_small(d_q, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, h->num_sms, s));
+  } else if (d % 64 == 0) {
     const CUtensorMap qmap = make_split_map(w.qsplit.p, B, d);
     CK(rd::launch_coarse_tc(qmap, h->cmap, h->cnorm.p, w.Dc.p, (int)B, nl, d, s));
   } else {
@@ -830,14 +831,13 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   } else {
     CK(rd::launch_select(sp, h->stage_rows(B), s));
   }
-  launches += 4;
+  launches += 3;
   rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
                     w.list_ntile.p, w.list_toff.p, w.list_q.p, w.tiles.p, w.ff_tiles.p, w.meta.p, w.counters.p,
                     (int)B, nl, nprobe, pl.R, d % 64 == 0 ? h->tc_min_q : 1 << 30};
   CK(rd::launch_plan(pp, s));
-  launches += 4;
+  launches += rd::plan_fused_ok((int)B, nl) ? 1 : 4;
   CK(cudaEventRecord(e1, s));
-  CK(cudaMemsetAsync(w.part_count.p, 0, sizeof(int) * B, s));
 
   const bool has_off = h->slots > 0;
   if (has_off) {  // fetch the probe histogram for host-side staging decisions
@@ -974,6 +974,10 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     CK(cudaStreamWaitEvent(s, e_off, 0));
   }
 
+  if (!w.fb_ctr.p) {  // the fallback kernel's completion counter: zeroed once, re-armed by the kernel
+    w.fb_ctr.alloc(1);
+    CK(cudaMemset(w.fb_ctr.p, 0, sizeof(unsigned)));
+  }
   w.fail_list.ensure(B);
   w.fb_dist.ensure((size_t)B * nprobe * rd::kTopK);
   w.fb_id.ensure((size_t)B * nprobe * rd::kTopK);
@@ -982,9 +986,9 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
                      w.fails.p + 1, w.fail_list.p, (int)B};
   CK(rd::launch_merge(mp, h->stage_rows(B), s));
   rd::FallbackParams fp{w.fail_list.p, w.fails.p + 1, w.probes.p, nprobe, d_q, h->d_list_off.p, h->d_list_base.p,
-                        h->d_ids.p, nl, d, k, w.fb_dist.p, w.fb_id.p, d_ids, d_dists};
+                        h->d_ids.p, nl, d, k, w.fb_dist.p, w.fb_id.p, d_ids, d_dists, w.fb_ctr.p};
   CK(rd::launch_fallback(fp, h->num_sms, s));
-  launches += 3;
+  launches += 2;
   CK(cudaEventRecord(te[3], s));
   if (st) {
     std::memset(st, 0, sizeof *st);
@@ -1100,10 +1104,11 @@ int rd_probe(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32
     w.fails.ensure(2);
     CK(cudaMemcpy(w.q.p, queries, sizeof(float) * B * d, cudaMemcpyHostToDevice));
     CK(cudaMemset(w.fails.p, 0, 2 * sizeof(unsigned)));
-    CK(rd::launch_row_norms(w.q.p, B, d, w.qnorm.p, 0));
-    if (d % 64 == 0) {
-      w.qsplit.ensure((size_t)B * d);
-      CK(rd::launch_qsplit(w.q.p, w.qsplit.p, B, d, 0));
+    w.qsplit.ensure((size_t)B * d);
+    CK(rd::launch_qprep(w.q.p, B, d, w.qnorm.p, d % 64 == 0 ? w.qsplit.p : nullptr, nullptr, nullptr, 0));
+    if (rd::coarse_small((int)B)) {
+      CK(rd::launch_coarse_small(w.q.p, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, h->num_sms, 0));
+    } else if (d % 64 == 0) {
       const CUtensorMap qmap = make_split_map(w.qsplit.p, B, d);
       CK(rd::launch_coarse_tc(qmap, h->cmap, h->cnorm.p, w.Dc.p, (int)B, nl, d, 0));
     } else {

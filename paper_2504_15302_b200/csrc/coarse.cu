@@ -7,6 +7,7 @@
 //     oracle), order by (exact distance, list id) and keep nprobe. The probe set
 //     is certified when every non-candidate's approximate distance, less the
 //     GEMM's error bound, exceeds the nprobe-th exact distance.
+#include <cuda_bf16.h>
 #include <float.h>
 
 #include "ivf_kernels.cuh"
@@ -23,6 +24,7 @@ __global__ void __launch_bounds__(256) coarse_gemm_kernel(const float* __restric
                                                           const float* __restrict__ cnorm,
                                                           float* __restrict__ Dc, int B, int nlist,
                                                           int d) {
+  RD_PDL_PROLOGUE();
   __shared__ __align__(16) float As[kBK][kBM + 4];
   __shared__ __align__(16) float Bs[kBK][kBN + 4];
   const int tid = threadIdx.x;
@@ -79,6 +81,79 @@ __global__ void __launch_bounds__(256) coarse_gemm_kernel(const float* __restric
       const int c = cb + tx * 8 + j;
       if (c < nlist) Dc[(size_t)q * nlist + c] = __ldg(cnorm + c) - 2.f * acc[i][j];
     }
+  }
+}
+
+// Small batches (B <= kSmallB): Dc is a memory-bound GEMV over the centroids, so one warp per
+// centroid streams its row once (float4, coalesced) against every query of the batch held in smem,
+// across >= one CTA per SM — instead of the tensor-core tile kernel's 32-CTA, latency-bound K loop.
+// Any summation order is covered by the select kernel's error bound ((d + 4) u 2 |q| |c|).
+constexpr int kSmallB = 16;
+constexpr int kGemvThreads = 256;
+constexpr int kGemvMaxV = 8;  // float4 per lane per row: d <= 1024
+// one warp per centroid (grid = nlist / 8 CTAs): the row's float4 loads are all issued before any
+// use; queries come through L1 (B x d x 4 <= 64 KB)
+__global__ void __launch_bounds__(kGemvThreads) coarse_gemv_kernel(const float* __restrict__ Q,
+                                                                   const float* __restrict__ C,
+                                                                   const float* __restrict__ cnorm,
+                                                                   float* __restrict__ Dc, int B, int nlist,
+                                                                   int d) {
+  RD_PDL_PROLOGUE();
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (kGemvThreads / 32) + (threadIdx.x >> 5);
+  if (c >= nlist) return;
+  const int d4 = d / 4;
+  const float4* crow = reinterpret_cast<const float4*>(C + (size_t)c * d);
+  float4 cv[kGemvMaxV];
+#pragma unroll
+  for (int k = 0; k < kGemvMaxV; ++k) {
+    const int i = lane + 32 * k;
+    cv[k] = i < d4 ? __ldg(crow + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const float cn = __ldg(cnorm + c);
+  for (int b = 0; b < B; ++b) {
+    const float4* qrow = reinterpret_cast<const float4*>(Q + (size_t)b * d);
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < kGemvMaxV; ++k) {
+      const int i = lane + 32 * k;
+      if (i < d4) {
+        const float4 qv = __ldg(qrow + i);
+        acc = fmaf(qv.x, cv[k].x, fmaf(qv.y, cv[k].y, fmaf(qv.z, cv[k].z, fmaf(qv.w, cv[k].w, acc))));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) Dc[(size_t)b * nlist + c] = cn - 2.f * acc;
+  }
+}
+
+// query preparation in one pass, one warp per query: ||q||^2 (the same fp64 lane-strided sum and
+// shuffle tree as row_norms) and the bf16 (hi, lo) split rows the tensor-core kernels gather
+// It also zeroes the per-search counters (zero2: 2 words, zeroB: B words) so they need no memset.
+__global__ void qprep_kernel(const float* __restrict__ Q, long long B, int d, float* __restrict__ qnorm,
+                             __nv_bfloat16* __restrict__ qsplit, unsigned* zero2, int* zeroB) {
+  RD_PDL_PROLOGUE();
+  const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (zero2 && blockIdx.x == 0 && threadIdx.x < 2) zero2[threadIdx.x] = 0u;
+  for (long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; r < B; r += warps) {
+    if (zeroB && lane == 0) zeroB[r] = 0;
+    const float* x = Q + (size_t)r * d;
+    double s = 0.0;
+    for (int t = lane; t < d; t += 32) {
+      const float q = x[t];
+      const double v = q;
+      s += v * v;
+      if (qsplit) {
+        const __nv_bfloat16 h = __float2bfloat16_rn(q);
+        qsplit[(r * 2) * d + t] = h;
+        qsplit[(r * 2 + 1) * d + t] = __float2bfloat16_rn(q - __bfloat162float(h));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) qnorm[r] = (float)s;
   }
 }
 
@@ -238,6 +313,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // uncertified queries recompute every candidate (or every centroid) exactly.
 template <bool kStage>
 __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const SelectParams p) {
+  RD_PDL_PROLOGUE();
   extern __shared__ __align__(16) uint32_t keys[];
   __shared__ int hist[2048];
   __shared__ int scan_sh[8];
@@ -642,7 +718,35 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
 cudaError_t launch_coarse(const float* Q, const float* C, const float* cnorm, float* Dc, int B,
                           int nlist, int d, cudaStream_t s) {
   dim3 grid((nlist + kBN - 1) / kBN, (B + kBM - 1) / kBM);
-  coarse_gemm_kernel<<<grid, 256, 0, s>>>(Q, C, cnorm, Dc, B, nlist, d);
+  return launch_k(coarse_gemm_kernel, grid, dim3(256), 0, s, Q, C, cnorm, Dc, B, nlist, d);
+  return cudaGetLastError();
+}
+
+bool coarse_small(int B) { return B <= kSmallB; }
+
+cudaError_t launch_coarse_small(const float* Q, const float* C, const float* cnorm, float* Dc, int B, int nlist,
+                                int d, int num_sms, cudaStream_t s) {
+  (void)num_sms;
+  if (B == 0) return cudaSuccess;
+  if (d > 4 * 32 * kGemvMaxV) return cudaErrorInvalidValue;
+  return launch_k(coarse_gemv_kernel, dim3((nlist + 7) / 8), dim3(kGemvThreads), 0, s, Q, C, cnorm, Dc, B, nlist, d);
+  return cudaGetLastError();
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("RD_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+cudaError_t launch_qprep(const float* Q, long long B, int d, float* qnorm, void* qsplit, unsigned* zero2, int* zeroB,
+                         cudaStream_t s) {
+  if (B == 0) return cudaSuccess;
+  const long long blocks = (B * 32 + 255) / 256;
+  return launch_k(qprep_kernel, dim3((unsigned)(blocks < 148 * 8 ? blocks : 148 * 8)), dim3(256), 0, s, Q, B, d, qnorm,
+                  reinterpret_cast<__nv_bfloat16*>(qsplit), zero2, zeroB);
   return cudaGetLastError();
 }
 
@@ -654,16 +758,16 @@ cudaError_t launch_select(const SelectParams& p, bool stage, cudaStream_t s) {
       stage ? keys + qd + sizeof(float) * ((size_t)p.d + 32 * (size_t)(p.d + kStagePad)) : keys + qd;
   if (stage && smem > 200 * 1024) stage = false;  // very large nlist: the direct-load variant
   static size_t attr[2] = {0, 0};
-  if (smem > 48 * 1024 && smem > attr[stage]) {
+  if (smem > attr[stage]) {  // dynamic + static may exceed the 48 KiB default even below it
     cudaError_t e = cudaFuncSetAttribute(stage ? coarse_select_kernel<true> : coarse_select_kernel<false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr[stage] = smem;
   }
   if (stage)
-    coarse_select_kernel<true><<<p.B, kSelThreads, smem, s>>>(p);
+    return launch_k(coarse_select_kernel<true>, dim3(p.B), dim3(kSelThreads), smem, s, p);
   else
-    coarse_select_kernel<false><<<p.B, kSelThreads, smem, s>>>(p);
+    return launch_k(coarse_select_kernel<false>, dim3(p.B), dim3(kSelThreads), smem, s, p);
   return cudaGetLastError();
 }
 

@@ -27,6 +27,7 @@ constexpr int kThreadsC = 192;
 __global__ void __launch_bounds__(kThreadsC, 1)
     coarse_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap cmap,
                      const float* __restrict__ cnorm, float* __restrict__ Dc, int B, int nlist, int d) {
+  RD_PDL_PROLOGUE();
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -145,7 +146,7 @@ cudaError_t launch_coarse_tc(const CUtensorMap& qmap, const CUtensorMap& cmap, c
     attr = true;
   }
   dim3 grid((nlist + kNC - 1) / kNC, (B + kM - 1) / kM);
-  coarse_tc_kernel<<<grid, kThreadsC, coarse_tc_smem_bytes(), s>>>(qmap, cmap, cnorm, Dc, B, nlist, d);
+  return launch_k(coarse_tc_kernel, grid, dim3(kThreadsC), coarse_tc_smem_bytes(), s, qmap, cmap, cnorm, Dc, B, nlist, d);
   return cudaGetLastError();
 }
 

@@ -4,7 +4,28 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 namespace rd {
+
+// Kernel launch with programmatic stream serialization (PDL): the kernel may be scheduled while
+// its predecessor in the stream drains; the kernel's RD_PDL_PROLOGUE waits for the predecessor's
+// results. RD_PDL=0 in the environment launches them plainly (A/B).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 // Scan geometry (see DESIGN.md §Kernels / N4):
 constexpr int kScanRows = 256;      // rows of one row tile (one TMA box)
@@ -78,6 +99,14 @@ cudaError_t launch_scan(const CUtensorMap& map256, const CUtensorMap& map32, con
 // constant per query and added where an absolute distance is needed).
 cudaError_t launch_coarse(const float* Q, const float* C, const float* cnorm, float* Dc, int B,
                           int nlist, int d, cudaStream_t s);
+// small batches: FFMA GEMV over the centroids (memory-bound; see coarse_small for the cut-over)
+bool coarse_small(int B);
+cudaError_t launch_coarse_small(const float* Q, const float* C, const float* cnorm, float* Dc, int B, int nlist,
+                                int d, int num_sms, cudaStream_t s);
+// ||q||^2 and (when qsplit != nullptr) the bf16 (hi, lo) split rows of a query batch, one pass;
+// zero2 (2 words) and zeroB (B words) are zeroed on the way when non-null
+cudaError_t launch_qprep(const float* Q, long long B, int d, float* qnorm, void* qsplit, unsigned* zero2, int* zeroB,
+                         cudaStream_t s);
 // tensor-core variant (d % 64 == 0): qmap / cmap are 3D bf16 maps over the (hi, lo) splits,
 // dims {d, 2, rows}, box {64, 1, 128}, 128 B swizzle
 size_t coarse_tc_smem_bytes();
@@ -123,6 +152,7 @@ struct PlanParams {
   int B, nlist, nprobe, R, tc_min_q;
 };
 cudaError_t launch_plan(const PlanParams& p, cudaStream_t s);
+bool plan_fused_ok(int B, int nlist);  // the single-CTA plan applies
 
 struct MergeParams {
   const float* part_dist;
@@ -180,6 +210,7 @@ struct FallbackParams {
   long long* fb_id;
   long long* out_ids;
   float* out_dists;
+  unsigned* done_ctr;              // device scalar, 0 between launches (the kernel re-arms it)
 };
 cudaError_t launch_fallback(const FallbackParams& p, int num_sms, cudaStream_t s);
 

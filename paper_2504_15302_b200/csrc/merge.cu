@@ -22,6 +22,7 @@ constexpr long long kNoKey = 0x7fffffffffffffffll;
 // row from global memory (enough CTAs are resident to hide the latency).
 template <bool kStage>
 __global__ void __launch_bounds__(256) merge_rerank_kernel(const MergeParams p) {
+  RD_PDL_PROLOGUE();
   extern __shared__ __align__(16) float dyn[];  // kStage: q[d], rows[32][d + kStagePad]
   __shared__ float sd[8][kTopK];
   __shared__ long long sk[8][kTopK];
@@ -209,12 +210,19 @@ __global__ void __launch_bounds__(256) seed_kernel(const SeedParams p) {
   }
 }
 
-// persistent: work item w -> (failed query w / nprobe, probe w % nprobe); exact top-32 of the list
-__global__ void __launch_bounds__(256) fallback_scan_kernel(const FallbackParams p) {
+// Exact fallback in one launch. Persistent: work item w -> (failed query w / nprobe, probe
+// w % nprobe), the exact top-32 of that list; the last CTA to finish merges each failed query's
+// nprobe partials and overwrites its result row, then re-arms the completion counter. With no
+// failures (the normal case) every CTA returns at once.
+__global__ void __launch_bounds__(256) fallback_kernel(const FallbackParams p) {
+  RD_PDL_PROLOGUE();
   __shared__ float wd[8][kTopK];
   __shared__ long long wk[8][kTopK];
+  __shared__ bool last;
+  const int nf = (int)*p.fail_count;
+  if (nf == 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long work = (long long)(*p.fail_count) * p.nprobe;
+  const long long work = (long long)nf * p.nprobe;
   for (long long w = blockIdx.x; w < work; w += gridDim.x) {
     const int q = p.fail_list[w / p.nprobe];
     const int l = p.probes[(size_t)q * p.nprobe + (w % p.nprobe)];
@@ -253,18 +261,18 @@ __global__ void __launch_bounds__(256) fallback_scan_kernel(const FallbackParams
     }
     __syncthreads();
   }
-}
-
-// one warp per failed query: merge its nprobe exact partials, overwrite its result row
-__global__ void fallback_merge_kernel(const FallbackParams p) {
-  const int lane = threadIdx.x & 31;
-  const int nf = (int)*p.fail_count;
-  for (int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; f < nf; f += (gridDim.x * blockDim.x) >> 5) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(p.done_ctr, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int f = warp; f < nf; f += 8) {  // one warp per failed query
     float ld = kInf;
     long long lk = kNoKey;
     for (int i = 0; i < p.nprobe; ++i) {
       const long long w = (long long)f * p.nprobe + i;
-      warp_merge32(ld, lk, p.fb_dist[w * kTopK + lane], p.fb_id[w * kTopK + lane], lane);
+      warp_merge32(ld, lk, __ldcg(p.fb_dist + w * kTopK + lane), __ldcg(p.fb_id + w * kTopK + lane), lane);
     }
     const int q = p.fail_list[f];
     if (lane < p.k) {
@@ -272,6 +280,7 @@ __global__ void fallback_merge_kernel(const FallbackParams p) {
       p.out_dists[(size_t)q * p.k + lane] = lk == kNoKey ? kInf : ld;
     }
   }
+  if (threadIdx.x == 0) *p.done_ctr = 0u;
 }
 
 }  // namespace
@@ -283,8 +292,7 @@ cudaError_t launch_seed(const SeedParams& p, cudaStream_t s) {
 }
 
 cudaError_t launch_fallback(const FallbackParams& p, int num_sms, cudaStream_t s) {
-  fallback_scan_kernel<<<num_sms, 256, 0, s>>>(p);
-  fallback_merge_kernel<<<8, 256, 0, s>>>(p);
+  return launch_k(fallback_kernel, dim3(num_sms), dim3(256), 0, s, p);
   return cudaGetLastError();
 }
 
@@ -293,15 +301,15 @@ cudaError_t launch_merge(const MergeParams& p, bool stage, cudaStream_t s) {
   if (stage) {
     const size_t smem = sizeof(float) * ((size_t)p.d + kTopK * (size_t)(p.d + kStagePad));
     static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
+    if (smem > attr) {  // dynamic + static may exceed the 48 KiB default even below it
       cudaError_t e = cudaFuncSetAttribute(merge_rerank_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem);
       if (e != cudaSuccess) return e;
       attr = smem;
     }
-    merge_rerank_kernel<true><<<p.B, 256, smem, s>>>(p);
+    return launch_k(merge_rerank_kernel<true>, dim3(p.B), dim3(256), smem, s, p);
   } else {
-    merge_rerank_kernel<false><<<p.B, 256, 0, s>>>(p);
+    return launch_k(merge_rerank_kernel<false>, dim3(p.B), dim3(256), 0, s, p);
   }
   return cudaGetLastError();
 }

@@ -94,6 +94,17 @@ __device__ __forceinline__ float exact_l2_group8_any(const float* __restrict__ q
   return exact_l2_group8_impl<false>(q, x, d, j);
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every kernel of the search chain starts with RD_PDL_PROLOGUE: it lets the next kernel in the
+// stream begin launching (griddepcontrol.launch_dependents), then waits until every kernel it
+// depends on has completed and its writes are visible (griddepcontrol.wait). Without the launch
+// attribute (see launch_k) both are no-ops, so correctness never depends on PDL.
+#define RD_PDL_PROLOGUE()                                              \
+  do {                                                                 \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");    \
+    asm volatile("griddepcontrol.wait;" ::: "memory");                 \
+  } while (0)
+
 // ---------------------------------------------------------------- PTX: smem, mbarrier, TMA
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

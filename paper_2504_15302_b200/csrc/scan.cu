@@ -89,6 +89,7 @@ __device__ __forceinline__ void rowtile_dots(const ScanSmem& sm, int d, int kh, 
 __global__ void __launch_bounds__(kScanThreads, 1)
     ivf_scan_kernel(const __grid_constant__ CUtensorMap map256,
                     const __grid_constant__ CUtensorMap map32, const ScanParams p) {
+  RD_PDL_PROLOGUE();
   extern __shared__ unsigned char smem_raw[];
   const ScanSmem sm = carve(smem_raw, p.d);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -284,7 +285,7 @@ cudaError_t launch_scan(const CUtensorMap& map256, const CUtensorMap& map32, con
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  ivf_scan_kernel<<<grid, kScanThreads, smem, s>>>(map256, map32, p);
+  return launch_k(ivf_scan_kernel, dim3(grid), dim3(kScanThreads), smem, s, map256, map32, p);
   return cudaGetLastError();
 }
 

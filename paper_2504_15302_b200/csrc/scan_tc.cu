@@ -95,6 +95,7 @@ template <bool kPre>
 __global__ void __launch_bounds__(kThreads, 1)
     ivf_scan_tc_kernel(const __grid_constant__ CUtensorMap map128, const __grid_constant__ CUtensorMap map32,
                        const __grid_constant__ CUtensorMap qmap, const TcScanParams p) {
+  RD_PDL_PROLOGUE();
   extern __shared__ unsigned char smem_raw[];
   const int d = p.d, nks = kPre ? d / 64 : d / 32;
   const Smem sm = carve(smem_raw, d);
@@ -516,9 +517,9 @@ cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, 
   const size_t smem = scan_tc_smem_bytes(p.d);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   if (presplit)
-    ivf_scan_tc_kernel<true><<<grid, kThreads, smem, s>>>(map128, map32, qmap, p);
+    return launch_k(ivf_scan_tc_kernel<true>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
   else
-    ivf_scan_tc_kernel<false><<<grid, kThreads, smem, s>>>(map128, map32, qmap, p);
+    return launch_k(ivf_scan_tc_kernel<false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
   return cudaGetLastError();
 }
 

@@ -49,6 +49,19 @@ def test_engine_vs_oracle_synthetic(engine, oracle, B, nprobe, k, presplit, monk
     _check(e, o.ids, o.dists)
 
 
+@pytest.mark.parametrize("B", [1, 16, 17, 64, 128, 200])
+def test_engine_vs_oracle_many_lists(engine, oracle, B):
+    # nlist 4096 (the C2 coarse size): small-batch GEMV coarse (B <= 16), tensor-core coarse, the
+    # single-CTA plan (B <= 128, bitmap of up to 4 words per list in smem), the multi-kernel plan,
+    # smem-staged select / rerank (B <= 2 x SMs)
+    n, d, nlist = 200000, 768, 4096
+    desc = engine.desc(n, d, nlist)
+    q, _ = engine.synth_queries(desc, 7, B)
+    e = engine.synthetic_index(desc).search(q, 64, 10)
+    o = oracle.synthetic_index(desc).search(q, 64, 10)
+    _check(e, o.ids, o.dists)
+
+
 def test_engine_generator_bit_exact(engine, oracle):
     desc = engine.desc(5000, 96, 17)
     ei = engine.synthetic_index(desc)
