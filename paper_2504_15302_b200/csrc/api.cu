@@ -835,7 +835,21 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
                     w.list_ntile.p, w.list_toff.p, w.list_q.p, w.tiles.p, w.ff_tiles.p, w.meta.p, w.counters.p,
                     (int)B, nl, nprobe, pl.R, d % 64 == 0 ? h->tc_min_q : 1 << 30};
-  CK(rd::launch_plan(pp, s));
+  if (h->dbg_ts) {
+    static unsigned long long* dbg = nullptr;
+    if (!dbg) CK(cudaMalloc(&dbg, 32 * sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(dbg, 0, 32 * sizeof(unsigned long long), s));
+    pp.dbg = dbg;
+    CK(rd::launch_plan(pp, s));
+    unsigned long long t[32];
+    CK(cudaMemcpyAsync(t, dbg, sizeof t, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    fprintf(stderr, "plan cycles:");
+    for (int i = 1; i < 8; ++i) fprintf(stderr, " %d:%lld", i, t[16 + i] ? (long long)(t[16 + i] - t[16]) : -1LL);
+    fprintf(stderr, "\n");
+  } else {
+    CK(rd::launch_plan(pp, s));
+  }
   launches += rd::plan_fused_ok((int)B, nl) ? 1 : 4;
   CK(cudaEventRecord(e1, s));
 

@@ -282,20 +282,6 @@ __device__ __forceinline__ float block_reduce_max(float v, float* sh) {
   return r;
 }
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-// profiling only (RD_DEBUG_TS): globaltimer / clock64 checkpoints of CTA 0
-#define RD_TS(i)                                                 \
-  do {                                                           \
-    if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0) {          \
-      p.dbg[i] = gtimer();                                       \
-      p.dbg[16 + i] = clock64();                                 \
-    }                                                            \
-  } while (0)
-
 // dynamic smem: keys[nlist] (u32; approximate distances as floats, then exact keys in the fallback),
 // q widened to fp64 [d]; kStage (small batches: one CTA per query is latency-bound) adds q as fp32
 // [d] and a 32-row staging area [32][d + kStagePad] filled by bulk (TMA) row copies.

@@ -150,6 +150,7 @@ struct PlanParams {
   int* meta;                  // [0] #tc tiles, [1] tc counter, [2] #ff tiles, [3] ff counter
   unsigned long long* counters;  // [0] unique lists, [1] resident rows probed, [2] offloaded rows probed
   int B, nlist, nprobe, R, tc_min_q;
+  unsigned long long* dbg = nullptr;  // RD_DEBUG_TS: globaltimer checkpoints of CTA 0
 };
 cudaError_t launch_plan(const PlanParams& p, cudaStream_t s);
 bool plan_fused_ok(int B, int nlist);  // the single-CTA plan applies

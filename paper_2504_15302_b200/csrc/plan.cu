@@ -95,82 +95,85 @@ __global__ void list_count_kernel(const PlanParams p) {
   }
 }
 
-// single CTA: exclusive scans of list_nq and both tile counts; totals and byte counters
+// single CTA: exclusive scans of list_nq and both tile counts; totals and byte counters. Lists are
+// visited in rounds of 1024 (thread t <-> list round * 1024 + t) so every global access coalesces.
 __global__ void __launch_bounds__(1024) list_scan_kernel(const PlanParams p) {
-  __shared__ long long sh[3][32];
-  __shared__ unsigned long long sh_c[3][32];
+  __shared__ int wsum[3][32];
+  __shared__ int carry[3];
+  __shared__ unsigned long long wcnt[3][32];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int per = (p.nlist + 1023) / 1024;
-  const int j0 = tid * per, j1 = min(p.nlist, j0 + per);
-  long long loc[3] = {0, 0, 0};
-  unsigned long long uniq = 0, rrows = 0, orows = 0;
-  for (int j = j0; j < j1; ++j) {
-    const int nq = p.list_nq[j];
-    loc[0] += nq;
-    loc[1] += p.list_ntile[j];
-    loc[2] += p.list_ntile[p.nlist + j];
-    if (nq > 0) {
-      const long long len = p.list_off[j + 1] - p.list_off[j];
-      ++uniq;
-      if (p.res_row0[j] >= 0)
-        rrows += len;
-      else
-        orows += len;
-    }
-  }
-  long long inc[3] = {loc[0], loc[1], loc[2]};
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1)
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const long long y = __shfl_up_sync(0xffffffffu, inc[i], o);
-      if (lane >= o) inc[i] += y;
-    }
-  unsigned long long cc[3] = {uniq, rrows, orows};
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int i = 0; i < 3; ++i) cc[i] += __shfl_xor_sync(0xffffffffu, cc[i], o);
-  if (lane == 31)
-    for (int i = 0; i < 3; ++i) sh[i][w] = inc[i];
-  if (lane == 0)
-    for (int i = 0; i < 3; ++i) sh_c[i][w] = cc[i];
+  const int nl = p.nlist;
+  if (tid < 3) carry[tid] = 0;
+  unsigned long long cc[3] = {0, 0, 0};
   __syncthreads();
-  if (w == 0) {
-    long long a[3] = {sh[0][lane], sh[1][lane], sh[2][lane]};
+  for (int j0 = 0; j0 < nl; j0 += 1024) {
+    const int j = j0 + tid;
+    int v[3] = {0, 0, 0};
+    if (j < nl) {
+      v[0] = p.list_nq[j];
+      v[1] = p.list_ntile[j];
+      v[2] = p.list_ntile[nl + j];
+      if (v[0] > 0) {
+        ++cc[0];
+        cc[p.res_row0[j] >= 0 ? 1 : 2] += p.list_off[j + 1] - p.list_off[j];
+      }
+    }
+    int inc[3] = {v[0], v[1], v[2]};
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1)
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
-        const long long y = __shfl_up_sync(0xffffffffu, a[i], o);
-        if (lane >= o) a[i] += y;
+        const int y = __shfl_up_sync(0xffffffffu, inc[i], o);
+        if (lane >= o) inc[i] += y;
       }
-    for (int i = 0; i < 3; ++i) sh[i][lane] = a[i];
-    unsigned long long c[3] = {sh_c[0][lane], sh_c[1][lane], sh_c[2][lane]};
+    if (lane == 31)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) wsum[i][w] = inc[i];
+    __syncthreads();
+    if (w == 0) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        int a = wsum[i][lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, a, o);
+          if (lane >= o) a += y;
+        }
+        wsum[i][lane] = a;
+      }
+    }
+    __syncthreads();
+    if (j < nl) {
+      p.list_qoff[j] = carry[0] + (w ? wsum[0][w - 1] : 0) + inc[0] - v[0];
+      p.list_toff[j] = carry[1] + (w ? wsum[1][w - 1] : 0) + inc[1] - v[1];
+      p.list_toff[nl + j] = carry[2] + (w ? wsum[2][w - 1] : 0) + inc[2] - v[2];
+    }
+    __syncthreads();
+    if (tid == 0)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) carry[i] += wsum[i][31];
+    __syncthreads();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) cc[i] += __shfl_xor_sync(0xffffffffu, cc[i], o);
+  if (lane == 0)
+    for (int i = 0; i < 3; ++i) wcnt[i][w] = cc[i];
+  __syncthreads();
+  if (w == 0) {
+    unsigned long long c[3] = {wcnt[0][lane], wcnt[1][lane], wcnt[2][lane]};
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
       for (int i = 0; i < 3; ++i) c[i] += __shfl_xor_sync(0xffffffffu, c[i], o);
-    const long long tot_tc = __shfl_sync(0xffffffffu, a[1], 31), tot_ff = __shfl_sync(0xffffffffu, a[2], 31);
     if (lane == 0) {
       for (int i = 0; i < 3; ++i) p.counters[i] = c[i];
-      p.meta[0] = (int)tot_tc;
+      p.meta[0] = carry[1];
       p.meta[1] = 0;
-      p.meta[2] = (int)tot_ff;
+      p.meta[2] = carry[2];
       p.meta[3] = 0;
     }
-  }
-  __syncthreads();
-  long long o0 = (w ? sh[0][w - 1] : 0) + inc[0] - loc[0];
-  long long o1 = (w ? sh[1][w - 1] : 0) + inc[1] - loc[1];
-  long long o2 = (w ? sh[2][w - 1] : 0) + inc[2] - loc[2];
-  for (int j = j0; j < j1; ++j) {
-    p.list_qoff[j] = (int)o0;
-    p.list_toff[j] = (int)o1;
-    p.list_toff[p.nlist + j] = (int)o2;
-    o0 += p.list_nq[j];
-    o1 += p.list_ntile[j];
-    o2 += p.list_ntile[p.nlist + j];
   }
 }
 
@@ -212,161 +215,163 @@ __global__ void list_fill_kernel(const PlanParams p) {
 
 // Small batches: the whole plan in one CTA with the list x query bitmap in shared memory (one
 // launch instead of a memset and four dependent launches; same outputs as the multi-kernel path).
+// Lists are visited in rounds of 1024 (thread t <-> list round * 1024 + t) so every per-list global
+// access is coalesced, and each warp writes its probed lists' query ids and tiles cooperatively
+// (lane = tile), since scattered per-thread stores from one SM are what bounds this kernel.
 constexpr int kPlanThreads = 1024;
-constexpr int kPlanMaxPer = 16;  // lists per thread (nlist <= 16384)
 __global__ void __launch_bounds__(kPlanThreads) plan_fused_kernel(const PlanParams p) {
   RD_PDL_PROLOGUE();
   extern __shared__ unsigned bm[];  // nlist x W bitmap, then slen[nlist] (list length, ~len if offloaded)
-  __shared__ long long sh[3][32];
-  __shared__ unsigned long long sh_c[3][32];
+  __shared__ int wsum[3][32];
+  __shared__ int carry[3];
+  __shared__ unsigned long long wcnt[3][32];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  RD_TS(0);
   const int W = p.W, nl = p.nlist;
   int* slen = reinterpret_cast<int*>(bm + nl * W);
-  const int per = (nl + kPlanThreads - 1) / kPlanThreads;
-  const int j0 = min(nl, tid * per), j1 = min(nl, j0 + per);
-  {  // every global load of the count phase in flight at once: list bounds, residency, probes
-    long long off[kPlanMaxPer + 1], rr[kPlanMaxPer];
+  constexpr int kPB = 8;  // probes in flight per thread
+  int pr[kPB];
 #pragma unroll
-    for (int u = 0; u <= kPlanMaxPer; ++u) off[u] = j0 + u <= j1 ? p.list_off[j0 + u] : 0;
-#pragma unroll
-    for (int u = 0; u < kPlanMaxPer; ++u) rr[u] = j0 + u < j1 ? p.res_row0[j0 + u] : 0;
-    constexpr int kPB = 8;
-    int pr[kPB];
-#pragma unroll
-    for (int u = 0; u < kPB; ++u) {
-      const int i = tid + u * kPlanThreads;
-      pr[u] = i < p.B * p.nprobe ? p.probes[i] : -1;
-    }
-    for (int i = tid; i < nl * W; i += kPlanThreads) bm[i] = 0u;
-#pragma unroll
-    for (int u = 0; u < kPlanMaxPer; ++u)
-      if (j0 + u < j1) {
-        const int len = (int)(off[u + 1] - off[u]);
-        slen[j0 + u] = rr[u] >= 0 ? len : ~len;
-      }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < kPB; ++u) {
-      const int i = tid + u * kPlanThreads;
-      if (pr[u] >= 0) atomicOr(&bm[pr[u] * W + ((i / p.nprobe) >> 5)], 1u << ((i / p.nprobe) & 31));
-    }
-    for (int i = tid + kPB * kPlanThreads; i < p.B * p.nprobe; i += kPlanThreads) {
-      const int b = i / p.nprobe, l = p.probes[i];
-      if (l >= 0) atomicOr(&bm[l * W + (b >> 5)], 1u << (b & 31));
-    }
-    __syncthreads();
+  for (int u = 0; u < kPB; ++u) {
+    const int i = tid + u * kPlanThreads;
+    pr[u] = i < p.B * p.nprobe ? p.probes[i] : -1;
   }
-  // per list: query count, resident tile counts (recomputed in the fill pass instead of kept in registers)
-  auto counts = [&](int j, int& nq, int& ntc, int& nff, long long& len) {
-    nq = 0;
-    for (int x = 0; x < W; ++x) nq += __popc(bm[j * W + x]);
-    const int sl = slen[j];
-    len = sl >= 0 ? sl : ~sl;
-    ntc = nff = 0;
-    if (nq > 0 && len > 0 && sl >= 0) {
-      const int chunks = ((int)len + p.R - 1) / p.R;  // 32-bit: rows per list < 2^31
-      group_split(nq, p.tc_min_q, ntc, nff);
-      ntc *= chunks;
-      nff *= chunks;
-    }
-  };
-  long long loc[3] = {0, 0, 0};
-  unsigned long long cc[3] = {0, 0, 0};
-  for (int j = j0; j < j1; ++j) {
-    int nq, ntc, nff;
-    long long len;
-    counts(j, nq, ntc, nff, len);
-    if (nq > 0) {
-      ++cc[0];
-      cc[slen[j] >= 0 ? 1 : 2] += len;
-    }
-    loc[0] += nq;
-    loc[1] += ntc;
-    loc[2] += nff;
+#pragma unroll 4
+  for (int j = tid; j < nl; j += kPlanThreads) {
+    const int len = (int)(p.list_off[j + 1] - p.list_off[j]);
+    slen[j] = p.res_row0[j] >= 0 ? len : ~len;
   }
-  long long inc[3] = {loc[0], loc[1], loc[2]};
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1)
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const long long y = __shfl_up_sync(0xffffffffu, inc[i], o);
-      if (lane >= o) inc[i] += y;
-    }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int i = 0; i < 3; ++i) cc[i] += __shfl_xor_sync(0xffffffffu, cc[i], o);
-  if (lane == 31)
-    for (int i = 0; i < 3; ++i) sh[i][w] = inc[i];
-  if (lane == 0)
-    for (int i = 0; i < 3; ++i) sh_c[i][w] = cc[i];
+  for (int i = tid; i < nl * W; i += kPlanThreads) bm[i] = 0u;
+  if (tid < 3) carry[tid] = 0;
   __syncthreads();
-  if (w == 0) {
-    long long a[3] = {sh[0][lane], sh[1][lane], sh[2][lane]};
+  RD_TS(1);
+#pragma unroll
+  for (int u = 0; u < kPB; ++u) {
+    const int i = tid + u * kPlanThreads;
+    if (pr[u] >= 0) atomicOr(&bm[pr[u] * W + ((i / p.nprobe) >> 5)], 1u << ((i / p.nprobe) & 31));
+  }
+  for (int i = tid + kPB * kPlanThreads; i < p.B * p.nprobe; i += kPlanThreads) {
+    const int b = i / p.nprobe, l = p.probes[i];
+    if (l >= 0) atomicOr(&bm[l * W + (b >> 5)], 1u << (b & 31));
+  }
+  __syncthreads();
+  RD_TS(2);
+  unsigned long long cc[3] = {0, 0, 0};  // unique probed lists, resident rows, offloaded rows
+  for (int j0 = 0; j0 < nl; j0 += kPlanThreads) {
+    const int j = j0 + tid;
+    int v[3] = {0, 0, 0};  // queries, tensor-core tiles, FFMA tiles of list j
+    int len = 0, chunks = 0;
+    long long src0 = 0, g0 = 0;
+    if (j < nl) {
+      for (int x = 0; x < W; ++x) v[0] += __popc(bm[j * W + x]);
+      const int sl = slen[j];
+      len = sl >= 0 ? sl : ~sl;
+      if (v[0] > 0) {
+        ++cc[0];
+        cc[sl >= 0 ? 1 : 2] += len;
+        if (sl >= 0 && len > 0) {
+          chunks = (len + p.R - 1) / p.R;
+          group_split(v[0], p.tc_min_q, v[1], v[2]);
+          src0 = p.res_row0[j];
+          g0 = p.list_off[j];
+        }
+      }
+    }
+    // block exclusive scan of v[] over this round, offset by the running carry
+    int inc[3] = {v[0], v[1] * chunks, v[2] * chunks};
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1)
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
-        const long long y = __shfl_up_sync(0xffffffffu, a[i], o);
-        if (lane >= o) a[i] += y;
+        const int y = __shfl_up_sync(0xffffffffu, inc[i], o);
+        if (lane >= o) inc[i] += y;
       }
-    for (int i = 0; i < 3; ++i) sh[i][lane] = a[i];
-    unsigned long long c[3] = {sh_c[0][lane], sh_c[1][lane], sh_c[2][lane]};
+    if (lane == 31)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) wsum[i][w] = inc[i];
+    __syncthreads();
+    if (w == 0) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        int a = wsum[i][lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, a, o);
+          if (lane >= o) a += y;
+        }
+        wsum[i][lane] = a;  // inclusive over warps
+      }
+    }
+    __syncthreads();
+    const int o0 = carry[0] + (w ? wsum[0][w - 1] : 0) + inc[0] - v[0];
+    const int o1 = carry[1] + (w ? wsum[1][w - 1] : 0) + inc[1] - v[1] * chunks;
+    const int o2 = carry[2] + (w ? wsum[2][w - 1] : 0) + inc[2] - v[2] * chunks;
+    if (j < nl) {
+      p.list_nq[j] = v[0];
+      p.list_qoff[j] = o0;
+    }
+    // warp-cooperative emission for the warp's probed lists
+    unsigned m = __ballot_sync(0xffffffffu, v[0] > 0);
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      const int lj = __shfl_sync(0xffffffffu, j, src), nq = __shfl_sync(0xffffffffu, v[0], src);
+      const int qo = __shfl_sync(0xffffffffu, o0, src);
+      // query ids ascending: lane x < W owns bitmap word x
+      const unsigned bits = lane < W ? bm[lj * W + lane] : 0u;
+      int pos = __popc(bits);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, pos, o);
+        if (lane >= o) pos += y;
+      }
+      pos = qo + pos - __popc(bits);
+      for (unsigned bb = bits; bb; bb &= bb - 1) p.list_q[pos++] = lane * 32 + (__ffs(bb) - 1);
+      const int gtc = __shfl_sync(0xffffffffu, v[1], src), gff = __shfl_sync(0xffffffffu, v[2], src);
+      if (gtc + gff > 0) {
+        emit_tiles(p, lj, nq, qo, __shfl_sync(0xffffffffu, len, src), __shfl_sync(0xffffffffu, src0, src),
+                   __shfl_sync(0xffffffffu, g0, src), __shfl_sync(0xffffffffu, o1, src),
+                   __shfl_sync(0xffffffffu, o2, src), gtc, gff, __shfl_sync(0xffffffffu, chunks, src), lane, 32);
+      }
+    }
+    __syncthreads();  // everyone has read carry
+    if (tid == 0)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) carry[i] += wsum[i][31];
+    __syncthreads();
+  }
+  RD_TS(3);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) cc[i] += __shfl_xor_sync(0xffffffffu, cc[i], o);
+  if (lane == 0)
+    for (int i = 0; i < 3; ++i) wcnt[i][w] = cc[i];
+  __syncthreads();
+  if (w == 0) {
+    unsigned long long c[3] = {wcnt[0][lane], wcnt[1][lane], wcnt[2][lane]};
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
       for (int i = 0; i < 3; ++i) c[i] += __shfl_xor_sync(0xffffffffu, c[i], o);
-    const long long t1 = __shfl_sync(0xffffffffu, a[1], 31), t2 = __shfl_sync(0xffffffffu, a[2], 31);
     if (lane == 0) {
       for (int i = 0; i < 3; ++i) p.counters[i] = c[i];
-      p.meta[0] = (int)t1;
+      p.meta[0] = carry[1];
       p.meta[1] = 0;
-      p.meta[2] = (int)t2;
+      p.meta[2] = carry[2];
       p.meta[3] = 0;
     }
   }
-  __syncthreads();
-  long long o0 = (w ? sh[0][w - 1] : 0) + inc[0] - loc[0];
-  long long o1 = (w ? sh[1][w - 1] : 0) + inc[1] - loc[1];
-  long long o2 = (w ? sh[2][w - 1] : 0) + inc[2] - loc[2];
-  for (int j = j0; j < j1; ++j) {
-    int nq, ntc, nff;
-    long long len;
-    counts(j, nq, ntc, nff, len);
-    p.list_nq[j] = nq;
-    p.list_qoff[j] = (int)o0;
-    p.list_ntile[j] = ntc;
-    p.list_ntile[nl + j] = nff;
-    p.list_toff[j] = (int)o1;
-    p.list_toff[nl + j] = (int)o2;
-    if (nq > 0) {
-      int out = (int)o0;
-      for (int x = 0; x < W; ++x) {
-        unsigned bb = bm[j * W + x];
-        while (bb) {
-          const int bit = __ffs(bb) - 1;
-          bb &= bb - 1;
-          p.list_q[out++] = x * 32 + bit;
-        }
-      }
-      if (ntc + nff > 0) {
-        const int chunks = ((int)len + p.R - 1) / p.R;  // 32-bit: rows per list < 2^31
-        const int gtc = ntc / chunks, gff = nff / chunks;
-        emit_tiles(p, j, nq, (int)o0, (int)len, p.res_row0[j], p.list_off[j], (int)o1, (int)o2, gtc, gff, chunks, 0,
-                   1);
-      }
-    }
-    o0 += nq;
-    o1 += ntc;
-    o2 += nff;
-  }
+  RD_TS(4);
 }
 
 }  // namespace
 
 bool plan_fused_ok(int B, int nlist) {
   const long long W = (B + 31) / 32;
-  return B <= 128 && nlist <= kPlanThreads * kPlanMaxPer && (long long)nlist * (W + 1) * 4 <= 96 * 1024;
+  // one SM's issue rate bounds the fused kernel (~150 instructions per probed list): beyond a few
+  // hundred probed lists the grid-wide multi-kernel plan is faster
+  return B <= 8 && (long long)nlist * (W + 1) * 4 <= 96 * 1024;
 }
 
 cudaError_t launch_plan(const PlanParams& p, cudaStream_t s) {

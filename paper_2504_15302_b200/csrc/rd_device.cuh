@@ -105,6 +105,20 @@ __device__ __forceinline__ float exact_l2_group8_any(const float* __restrict__ q
     asm volatile("griddepcontrol.wait;" ::: "memory");                 \
   } while (0)
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// profiling only (RD_DEBUG_TS): globaltimer / clock64 checkpoints of CTA 0
+#define RD_TS(i)                                                 \
+  do {                                                           \
+    if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0) {          \
+      p.dbg[i] = gtimer();                                       \
+      p.dbg[16 + i] = clock64();                                 \
+    }                                                            \
+  } while (0)
+
 // ---------------------------------------------------------------- PTX: smem, mbarrier, TMA
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
