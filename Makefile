@@ -5,7 +5,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-ffp-contract=off,-
            --expt-relaxed-constexpr -Iinclude
 PKG := paper_2504_15302_b200
 SRC := $(wildcard $(PKG)/csrc/*.cu)
-HDR := $(wildcard $(PKG)/csrc/*.cuh) include/rd.h
+HDR := $(wildcard $(PKG)/csrc/*.cuh) include/rd.h include/rd_format.h
 OBJ := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRC))
 LIB := $(PKG)/lib/librd_b200.so
 

@@ -151,6 +151,14 @@ int rd_index_info_get(const rd_index* h, rd_index_info* out);
 int rd_index_layout(const rd_index* h, int64_t* list_offsets, int64_t* ids, uint8_t* resident_mask);
 void rd_index_destroy(rd_index* h);
 
+/* ---- on-disk index (format in include/rd_format.h, shared by both libraries) ----
+ * save: every list in list order (resident lists from HBM, offloaded ones from pinned host memory).
+ * load: header, offsets, ids and centroids, then the vectors streamed file -> pinned bounce
+ * buffers -> HBM with the reads overlapped with the copies; the loaded index is fully resident.
+ * Errors: RD_ERR_INVALID for a missing / malformed file, RD_ERR_RUNTIME for I/O or device failure. */
+int rd_index_save(const rd_index* h, const char* path);
+int rd_index_load(const char* path, int32_t device, rd_index** out);
+
 /* ---- search (reference seam: retrieval_time, cost_model.cpp:15-21) ---- */
 /* Host buffers: queries B x d row-major; out_ids / out_dists B x k. */
 int rd_search(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32_t k,

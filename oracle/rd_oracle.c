@@ -36,6 +36,7 @@
 #include <unistd.h>
 
 #include "../include/rd.h"
+#include "../include/rd_format.h"
 
 /* ------------------------------------------------------------------ errors */
 static __thread char g_err[512];
@@ -305,6 +306,80 @@ int rd_index_create_from_host(int64_t n, int32_t d, int32_t nlist, const float* 
   for (int64_t i = 0; i < n; ++i) h->ids[i] = ids ? ids[i] : i;
   h->resident = (uint8_t*)malloc((size_t)nlist);
   memset(h->resident, 1, (size_t)nlist);
+  compute_norm_max(h);
+  *out = h;
+  return RD_OK;
+}
+
+/* ------------------------------------------------------------------ on-disk index (rd_format.h) */
+static int write_at(FILE* f, uint64_t off, const void* p, uint64_t bytes) {
+  if (fseeko(f, (off_t)off, SEEK_SET) != 0) return -1;
+  return bytes == 0 || fwrite(p, 1, bytes, f) == bytes ? 0 : -1;
+}
+static int read_at(FILE* f, uint64_t off, void* p, uint64_t bytes) {
+  if (fseeko(f, (off_t)off, SEEK_SET) != 0) return -1;
+  return bytes == 0 || fread(p, 1, bytes, f) == bytes ? 0 : -1;
+}
+
+int rd_index_save(const rd_index* h, const char* path) {
+  if (!h || !path) return fail(RD_ERR_INVALID, "save: null argument");
+  rd_file_header hd;
+  rd_fmt_layout(&hd, h->n, h->d, h->nlist);
+  hd.check = rd_fmt_check(&hd, h->offsets);
+  FILE* f = fopen(path, "wb");
+  if (!f) return fail(RD_ERR_RUNTIME, "save: cannot open %s for writing", path);
+  char pad[RD_FILE_ALIGN];
+  memset(pad, 0, sizeof pad);
+  memcpy(pad, &hd, sizeof hd);
+  int bad = write_at(f, 0, pad, sizeof pad) ||
+            write_at(f, hd.off_list_offsets, h->offsets, 8ull * (uint64_t)(h->nlist + 1)) ||
+            write_at(f, hd.off_ids, h->ids, 8ull * (uint64_t)h->n) ||
+            write_at(f, hd.off_centroids, h->centroids, 4ull * (uint64_t)h->nlist * h->d) ||
+            write_at(f, hd.off_vectors, h->vectors, 4ull * (uint64_t)h->n * h->d);
+  if (fclose(f) != 0) bad = 1;
+  return bad ? fail(RD_ERR_RUNTIME, "save: write to %s failed", path) : RD_OK;
+}
+
+int rd_index_load(const char* path, int32_t device, rd_index** out) {
+  (void)device;
+  if (!path || !out) return fail(RD_ERR_INVALID, "load: null argument");
+  FILE* f = fopen(path, "rb");
+  if (!f) return fail(RD_ERR_INVALID, "load: cannot open %s", path);
+  rd_file_header hd;
+  const char* why = NULL;
+  int64_t* offs = NULL;
+  if (fseeko(f, 0, SEEK_END) != 0) why = "load: cannot size file";
+  const uint64_t size = why ? 0 : (uint64_t)ftello(f);
+  if (!why && read_at(f, 0, &hd, sizeof hd)) why = "truncated rd index file";
+  if (!why) why = rd_fmt_validate(&hd, size, NULL);
+  if (!why) {
+    offs = (int64_t*)malloc(8ull * (uint64_t)(hd.nlist + 1));
+    if (read_at(f, hd.off_list_offsets, offs, 8ull * (uint64_t)(hd.nlist + 1))) why = "truncated rd index file";
+  }
+  if (!why) why = rd_fmt_validate(&hd, size, offs);
+  if (why) {
+    free(offs);
+    fclose(f);
+    return fail(RD_ERR_INVALID, "load %s: %s", path, why);
+  }
+  rd_index* h = (rd_index*)calloc(1, sizeof *h);
+  h->n = hd.n;
+  h->d = hd.d;
+  h->nlist = hd.nlist;
+  h->offsets = offs;
+  h->ids = (int64_t*)malloc(8ull * (uint64_t)(hd.n > 0 ? hd.n : 1));
+  h->centroids = (float*)malloc(4ull * (uint64_t)hd.nlist * hd.d);
+  h->vectors = (float*)malloc(4ull * (uint64_t)(hd.n > 0 ? hd.n : 1) * hd.d);
+  h->resident = (uint8_t*)malloc((size_t)hd.nlist);
+  memset(h->resident, 1, (size_t)hd.nlist);
+  const int bad = read_at(f, hd.off_ids, h->ids, 8ull * (uint64_t)hd.n) ||
+                  read_at(f, hd.off_centroids, h->centroids, 4ull * (uint64_t)hd.nlist * hd.d) ||
+                  read_at(f, hd.off_vectors, h->vectors, 4ull * (uint64_t)hd.n * hd.d);
+  fclose(f);
+  if (bad) {
+    rd_index_destroy(h);
+    return fail(RD_ERR_RUNTIME, "load %s: read failed", path);
+  }
   compute_norm_max(h);
   *out = h;
   return RD_OK;

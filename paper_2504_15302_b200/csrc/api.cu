@@ -15,6 +15,9 @@
 // (tools/main.cpp:30) with the message in rd_last_error().
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <functional>
@@ -31,6 +34,7 @@
 #include <vector>
 
 #include "../../include/rd.h"
+#include "../../include/rd_format.h"
 #include "ivf_kernels.cuh"
 #include "rd_device.cuh"
 
@@ -576,6 +580,159 @@ int rd_index_create_from_host(int64_t n, int32_t d, int32_t nlist, const float* 
 }
 
 void rd_index_destroy(rd_index* h) { delete h; }
+
+// ---------------------------------------------------------------- on-disk index (include/rd_format.h)
+namespace {
+
+void pwrite_all(int fd, const void* p, size_t bytes, uint64_t off, const char* path) {
+  const char* b = static_cast<const char*>(p);
+  while (bytes) {
+    const ssize_t w = ::pwrite(fd, b, bytes, (off_t)off);
+    if (w <= 0) throw_rd(RD_ERR_RUNTIME, "save: write to %s failed", path);
+    b += w;
+    off += (uint64_t)w;
+    bytes -= (size_t)w;
+  }
+}
+void pread_all(int fd, void* p, size_t bytes, uint64_t off, const char* path) {
+  char* b = static_cast<char*>(p);
+  while (bytes) {
+    const ssize_t r = ::pread(fd, b, bytes, (off_t)off);
+    if (r <= 0) throw_rd(RD_ERR_RUNTIME, "load: read from %s failed", path);
+    b += r;
+    off += (uint64_t)r;
+    bytes -= (size_t)r;
+  }
+}
+struct Fd {
+  int fd = -1;
+  ~Fd() {
+    if (fd >= 0) ::close(fd);
+  }
+};
+constexpr size_t kIoChunk = size_t(64) << 20;  // pinned bounce buffer (bytes)
+
+}  // namespace
+
+int rd_index_save(const rd_index* h, const char* path) {
+  return guarded([&] {
+    if (!h || !path) throw_rd(RD_ERR_INVALID, "save: null argument");
+    CK(cudaSetDevice(h->device));
+    rd_file_header hd;
+    rd_fmt_layout(&hd, h->n, h->d, h->nlist);
+    hd.check = rd_fmt_check(&hd, reinterpret_cast<const int64_t*>(h->list_off.data()));
+    Fd f;
+    f.fd = ::open(path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
+    if (f.fd < 0) throw_rd(RD_ERR_RUNTIME, "save: cannot open %s for writing", path);
+    std::vector<char> head(RD_FILE_ALIGN, 0);
+    std::memcpy(head.data(), &hd, sizeof hd);
+    pwrite_all(f.fd, head.data(), head.size(), 0, path);
+    pwrite_all(f.fd, h->list_off.data(), 8 * (size_t)(h->nlist + 1), hd.off_list_offsets, path);
+    {
+      std::vector<long long> ids(std::max<long long>(1, h->n));
+      if (h->n) CK(cudaMemcpy(ids.data(), h->d_ids.p, 8 * (size_t)h->n, cudaMemcpyDeviceToHost));
+      pwrite_all(f.fd, ids.data(), 8 * (size_t)h->n, hd.off_ids, path);
+      std::vector<float> c((size_t)h->nlist * h->d);
+      CK(cudaMemcpy(c.data(), h->centroids.p, 4 * c.size(), cudaMemcpyDeviceToHost));
+      pwrite_all(f.fd, c.data(), 4 * c.size(), hd.off_centroids, path);
+    }
+    // vectors in list order, gathered from HBM (resident lists) or pinned host memory (offloaded)
+    HBuf<float> bounce;
+    const size_t row_bytes = 4 * (size_t)h->d;
+    const long long chunk_rows = std::max<long long>(1, (long long)(kIoChunk / row_bytes));
+    bounce.alloc((size_t)chunk_rows * h->d);
+    long long fill = 0, row = 0;  // rows in the bounce buffer; global row of its first row
+    auto flush = [&] {
+      if (!fill) return;
+      pwrite_all(f.fd, bounce.p, (size_t)fill * row_bytes, hd.off_vectors + (uint64_t)row * row_bytes, path);
+      row += fill;
+      fill = 0;
+    };
+    for (int l = 0; l < h->nlist; ++l) {
+      const long long len = h->list_off[l + 1] - h->list_off[l];
+      const float* src = h->resident[l] ? h->arena.p + (size_t)h->res_row0[l] * h->d
+                                        : h->host_arena.p + (size_t)h->host_row0[l] * h->d;
+      for (long long r = 0; r < len;) {
+        const long long take = std::min(len - r, chunk_rows - fill);
+        CK(cudaMemcpy(bounce.p + (size_t)fill * h->d, src + (size_t)r * h->d, (size_t)take * row_bytes,
+                      cudaMemcpyDefault));
+        fill += take;
+        r += take;
+        if (fill == chunk_rows) flush();
+      }
+    }
+    flush();
+    if (::fsync(f.fd) != 0) throw_rd(RD_ERR_RUNTIME, "save: fsync of %s failed", path);
+  });
+}
+
+int rd_index_load(const char* path, int32_t device, rd_index** out) {
+  return guarded([&] {
+    if (!path || !out) throw_rd(RD_ERR_INVALID, "load: null argument");
+    Fd f;
+    f.fd = ::open(path, O_RDONLY);
+    if (f.fd < 0) throw_rd(RD_ERR_INVALID, "load: cannot open %s", path);
+    struct stat stt;
+    if (::fstat(f.fd, &stt) != 0) throw_rd(RD_ERR_RUNTIME, "load: cannot stat %s", path);
+    const uint64_t size = (uint64_t)stt.st_size;
+    rd_file_header hd;
+    if (size < sizeof hd) throw_rd(RD_ERR_INVALID, "load %s: truncated rd index file", path);
+    pread_all(f.fd, &hd, sizeof hd, 0, path);
+    if (const char* why = rd_fmt_validate(&hd, size, nullptr)) throw_rd(RD_ERR_INVALID, "load %s: %s", path, why);
+    std::vector<long long> offs((size_t)hd.nlist + 1);
+    pread_all(f.fd, offs.data(), 8 * offs.size(), hd.off_list_offsets, path);
+    if (const char* why = rd_fmt_validate(&hd, size, reinterpret_cast<const int64_t*>(offs.data())))
+      throw_rd(RD_ERR_INVALID, "load %s: %s", path, why);
+    check_dims(hd.d);
+    if (hd.n >= (1LL << 31)) throw_rd(RD_ERR_INVALID, "load: at most 2^31-1 vectors per handle");
+    auto h = new_index(device);
+    h->n = hd.n;
+    h->d = hd.d;
+    h->nlist = hd.nlist;
+    h->list_off = offs;
+    const int d = hd.d;
+    {
+      std::vector<float> c((size_t)hd.nlist * d);
+      pread_all(f.fd, c.data(), 4 * c.size(), hd.off_centroids, path);
+      h->centroids.alloc(c.size());
+      h->cnorm.alloc(hd.nlist);
+      CK(cudaMemcpy(h->centroids.p, c.data(), 4 * c.size(), cudaMemcpyHostToDevice));
+      std::vector<long long> ids(std::max<long long>(1, hd.n));
+      pread_all(f.fd, ids.data(), 8 * (size_t)hd.n, hd.off_ids, path);
+      h->d_ids.alloc(hd.n);
+      if (hd.n) CK(cudaMemcpy(h->d_ids.p, ids.data(), 8 * (size_t)hd.n, cudaMemcpyHostToDevice));
+    }
+    // vectors: file -> two pinned bounce buffers -> HBM; the read of chunk i+1 overlaps the copy of chunk i
+    h->arena.alloc((size_t)hd.n * d);
+    const uint64_t total = 4ull * (uint64_t)hd.n * d;
+    HBuf<char> buf[2];
+    cudaEvent_t done[2];
+    for (int i = 0; i < 2; ++i) {
+      buf[i].alloc(kIoChunk);
+      CK(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+    }
+    try {
+      for (uint64_t o = 0, i = 0; o < total; o += kIoChunk, ++i) {
+        const size_t bytes = (size_t)std::min<uint64_t>(kIoChunk, total - o);
+        if (i >= 2) CK(cudaEventSynchronize(done[i & 1]));
+        pread_all(f.fd, buf[i & 1].p, bytes, hd.off_vectors + o, path);
+        CK(cudaMemcpyAsync(reinterpret_cast<char*>(h->arena.p) + o, buf[i & 1].p, bytes, cudaMemcpyHostToDevice,
+                           h->copy_stream));
+        CK(cudaEventRecord(done[i & 1], h->copy_stream));
+      }
+      CK(cudaStreamSynchronize(h->copy_stream));
+    } catch (...) {
+      cudaStreamSynchronize(h->copy_stream);
+      for (auto e : done) cudaEventDestroy(e);
+      throw;
+    }
+    for (auto e : done) cudaEventDestroy(e);
+    h->xnorm.alloc(hd.n);
+    CK(rd::launch_row_norms(h->arena.p, hd.n, d, h->xnorm.p, 0));
+    h->finish_layout();
+    *out = h.release();
+  });
+}
 
 int rd_index_info_get(const rd_index* h, rd_index_info* o) {
   return guarded([&] {

@@ -100,6 +100,8 @@ _SIGS = {
     "rd_index_info_get": (C.c_int, [_P, C.POINTER(IndexInfo)]),
     "rd_index_layout": (C.c_int, [_P, _I64P, _I64P, C.POINTER(C.c_uint8)]),
     "rd_index_destroy": (None, [_P]),
+    "rd_index_save": (C.c_int, [_P, C.c_char_p]),
+    "rd_index_load": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(_P)]),
     "rd_search": (C.c_int, [_P, _FP, C.c_int64, C.c_int32, C.c_int32, _I64P, _FP, C.POINTER(SearchStats)]),
     "rd_search_device": (C.c_int, [_P, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.c_int32, C.POINTER(SearchStats)]),
@@ -201,6 +203,12 @@ class Library:
         h = C.c_void_p()
         self.check(self.lib.rd_index_create_from_host(n, d, nlist, _fp(vectors), _i64p(list_offsets),
                                                       _fp(centroids), idp, device, C.byref(h)), "create_from_host")
+        return Index(self, h)
+
+    def load_index(self, path: str, device: int = 0) -> "Index":
+        """An index from the on-disk format (include/rd_format.h), fully resident."""
+        h = C.c_void_p()
+        self.check(self.lib.rd_index_load(os.fsencode(path), device, C.byref(h)), "load")
         return Index(self, h)
 
     # -- merges and arithmetic
@@ -318,6 +326,10 @@ class Index:
                                                        C.c_void_p(stream), 1 if sync else 0, C.byref(st)),
                         "search_device")
         return st.as_dict()
+
+    def save(self, path: str) -> None:
+        """Writes the index in the on-disk format (include/rd_format.h)."""
+        self._lib.check(self._lib.lib.rd_index_save(self._h, os.fsencode(path)), "save")
 
     def timing_reset(self) -> None:
         self._lib.check(self._lib.lib.rd_timing_reset(self._h), "timing_reset")
