@@ -151,6 +151,31 @@ int rd_index_info_get(const rd_index* h, rd_index_info* out);
 int rd_index_layout(const rd_index* h, int64_t* list_offsets, int64_t* ids, uint8_t* resident_mask);
 void rd_index_destroy(rd_index* h);
 
+/* ---- between-batch list migration ----
+ * Reference analogue: the retrieval worker's partition reconfiguration between batches
+ * (core/src/simulator.cpp:331-352), costed |dP| * M_p / bw by plan_transfer
+ * (core/src/memory_planner.cpp:137-142), with loads gated behind weight shrinks
+ * ("shrink before grow", core/src/simulator.cpp:323-326). Here a partition is an inverted list:
+ * `demote` lists leave HBM first (copied to pinned host memory unless a host copy already exists:
+ * host copies are write-once and kept), the remaining resident lists are compacted in place, then
+ * `promote` lists are copied host -> HBM into the freed space, so the HBM footprint never exceeds
+ * max(before, after). hbm_budget_bytes (0 = none) must cover the resident lists after the move
+ * plus, while any list is offloaded, two staging slots of max(largest offloaded list, 16384 rows)
+ * rounded up to 256 rows; otherwise RD_ERR_INFEASIBLE and nothing changes. Invalid ids, promoting
+ * a resident list, demoting an offloaded one or naming a list twice: RD_ERR_INVALID.
+ * Only between searches (one in-flight call per handle). */
+typedef struct {
+  double seconds;            /* wall time of the migration */
+  uint64_t h2d_bytes;        /* promoted list bytes, pinned host -> HBM */
+  uint64_t d2h_bytes;        /* demoted list bytes without a host copy yet, HBM -> pinned host */
+  uint64_t d2d_bytes;        /* resident bytes moved by the in-place compaction (engine only) */
+  int32_t lists_promoted;
+  int32_t lists_demoted;
+  uint64_t resident_bytes;   /* resident list bytes after the migration */
+} rd_migration_stats;
+int rd_index_migrate(rd_index* h, const int32_t* promote, int32_t n_promote, const int32_t* demote,
+                     int32_t n_demote, uint64_t hbm_budget_bytes, rd_migration_stats* stats);
+
 /* ---- on-disk index (format in include/rd_format.h, shared by both libraries) ----
  * save: every list in list order (resident lists from HBM, offloaded ones from pinned host memory).
  * load: header, offsets, ids and centroids, then the vectors streamed file -> pinned bounce

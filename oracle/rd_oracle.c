@@ -161,6 +161,7 @@ struct rd_index {
   int64_t* ids;     /* n */
   float* centroids; /* nlist x d */
   uint8_t* resident;
+  uint8_t* hostcopy; /* list has a (write-once) pinned host copy: offloaded at some point */
   float max_norm;
 };
 
@@ -275,6 +276,7 @@ int rd_index_create_synthetic(const rd_synth_desc* s, int32_t device, rd_index**
   parallel_for(h->n, 4096, gen_rows, &gc);
   free(row_list);
   h->resident = (uint8_t*)malloc((size_t)nl);
+  h->hostcopy = (uint8_t*)calloc((size_t)nl, 1);
   memset(h->resident, 1, (size_t)nl);
   compute_norm_max(h);
   *out = h;
@@ -306,6 +308,7 @@ int rd_index_create_from_host(int64_t n, int32_t d, int32_t nlist, const float* 
   for (int64_t i = 0; i < n; ++i) h->ids[i] = ids ? ids[i] : i;
   h->resident = (uint8_t*)malloc((size_t)nlist);
   memset(h->resident, 1, (size_t)nlist);
+  h->hostcopy = (uint8_t*)calloc((size_t)nlist, 1);
   compute_norm_max(h);
   *out = h;
   return RD_OK;
@@ -372,6 +375,7 @@ int rd_index_load(const char* path, int32_t device, rd_index** out) {
   h->vectors = (float*)malloc(4ull * (uint64_t)(hd.n > 0 ? hd.n : 1) * hd.d);
   h->resident = (uint8_t*)malloc((size_t)hd.nlist);
   memset(h->resident, 1, (size_t)hd.nlist);
+  h->hostcopy = (uint8_t*)calloc((size_t)hd.nlist, 1);
   const int bad = read_at(f, hd.off_ids, h->ids, 8ull * (uint64_t)hd.n) ||
                   read_at(f, hd.off_centroids, h->centroids, 4ull * (uint64_t)hd.nlist * hd.d) ||
                   read_at(f, hd.off_vectors, h->vectors, 4ull * (uint64_t)hd.n * hd.d);
@@ -392,6 +396,7 @@ void rd_index_destroy(rd_index* h) {
   free(h->ids);
   free(h->centroids);
   free(h->resident);
+  free(h->hostcopy);
   free(h);
 }
 
@@ -465,9 +470,72 @@ int rd_index_place(rd_index* h, const rd_placement* p) {
   if (!h || !p) return fail(RD_ERR_INVALID, "null argument");
   uint8_t* mask = (uint8_t*)malloc((size_t)h->nlist);
   int rc = choose_resident(h, p, mask);
-  if (rc == RD_OK) memcpy(h->resident, mask, (size_t)h->nlist);
+  if (rc == RD_OK) {
+    memcpy(h->resident, mask, (size_t)h->nlist);
+    for (int32_t l = 0; l < h->nlist; ++l) h->hostcopy[l] = !mask[l]; /* the relayout keeps offloaded lists only */
+  }
   free(mask);
   return rc;
+}
+
+int rd_index_migrate(rd_index* h, const int32_t* promote, int32_t n_promote, const int32_t* demote,
+                     int32_t n_demote, uint64_t hbm_budget_bytes, rd_migration_stats* st) {
+  if (!h || n_promote < 0 || n_demote < 0 || (n_promote && !promote) || (n_demote && !demote))
+    return fail(RD_ERR_INVALID, "migrate: invalid arguments");
+  const int32_t nl = h->nlist;
+  const uint64_t row_bytes = (uint64_t)h->d * sizeof(float);
+  uint8_t* seen = (uint8_t*)calloc((size_t)nl, 1);
+  for (int32_t i = 0; i < n_promote + n_demote; ++i) {
+    const int is_p = i < n_promote;
+    const int32_t l = is_p ? promote[i] : demote[i - n_promote];
+    const char* why = NULL;
+    if (l < 0 || l >= nl) why = "list id out of range";
+    else if (seen[l]) why = "list named twice";
+    else if (is_p && h->resident[l]) why = "promoted list is already resident";
+    else if (!is_p && !h->resident[l]) why = "demoted list is not resident";
+    if (why) {
+      free(seen);
+      return fail(RD_ERR_INVALID, "migrate: %s (%d)", why, l);
+    }
+    seen[l] = 1;
+  }
+  uint64_t res_bytes = 0;
+  int64_t max_off = -1;
+  for (int32_t l = 0; l < nl; ++l) {
+    const int after = seen[l] ? !h->resident[l] : h->resident[l];
+    const int64_t len = h->offsets[l + 1] - h->offsets[l];
+    if (after) res_bytes += (uint64_t)len * row_bytes;
+    else if (len > max_off) max_off = len;
+  }
+  free(seen);
+  if (hbm_budget_bytes) {
+    uint64_t need = res_bytes;
+    if (max_off >= 0) {
+      const int64_t rows = max_off > 16384 ? max_off : 16384;
+      need += 2ull * (uint64_t)((rows + 255) / 256 * 256) * row_bytes;
+    }
+    if (need > hbm_budget_bytes)
+      return fail(RD_ERR_INFEASIBLE, "migration infeasible: %llu bytes needed > budget %llu",
+                  (unsigned long long)need, (unsigned long long)hbm_budget_bytes);
+  }
+  rd_migration_stats s;
+  memset(&s, 0, sizeof s);
+  for (int32_t i = 0; i < n_demote; ++i) {
+    const int32_t l = demote[i];
+    if (!h->hostcopy[l]) s.d2h_bytes += (uint64_t)(h->offsets[l + 1] - h->offsets[l]) * row_bytes;
+    h->hostcopy[l] = 1;
+    h->resident[l] = 0;
+  }
+  for (int32_t i = 0; i < n_promote; ++i) {
+    const int32_t l = promote[i];
+    s.h2d_bytes += (uint64_t)(h->offsets[l + 1] - h->offsets[l]) * row_bytes;
+    h->resident[l] = 1;
+  }
+  s.lists_promoted = n_promote;
+  s.lists_demoted = n_demote;
+  s.resident_bytes = res_bytes;
+  if (st) *st = s;
+  return RD_OK;
 }
 
 int rd_index_info_get(const rd_index* h, rd_index_info* o) {

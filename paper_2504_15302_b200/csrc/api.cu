@@ -258,6 +258,7 @@ struct rd_index {
   std::vector<long long> host_row0;   // host: row in host arena or -1
   long long n_resident = 0;
   HBuf<float> host_arena;
+  long long host_used = 0;            // rows of host_arena holding list copies (write-once per list)
   CUtensorMap map256{}, map128{}, map32{};
 
   // staging ring for offloaded lists
@@ -392,6 +393,28 @@ struct rd_index {
     xmap128 = make_split_map(xsplit.p, n_resident, d, rd::kTcRows);
     xmap32 = make_split_map(xsplit.p, n_resident, d, 32);
     presplit = true;
+  }
+
+  // H2D staging ring for offloaded lists: `slots` slots of `slot_rows` rows (0 slots: none)
+  void set_staging(int nslots, long long nrows) {
+    for (auto e : slot_ready) cudaEventDestroy(e);
+    for (auto e : slot_done) cudaEventDestroy(e);
+    slot_ready.clear();
+    slot_done.clear();
+    staging.reset();
+    slots = nslots;
+    slot_rows = nrows;
+    if (!slots) return;
+    staging.alloc((size_t)slots * slot_rows * d);
+    smap256 = make_row_map(staging.p, (long long)slots * slot_rows, d, rd::kScanRows);
+    smap128 = make_row_map(staging.p, (long long)slots * slot_rows, d, rd::kTcRows);
+    smap32 = make_row_map(staging.p, (long long)slots * slot_rows, d, 32);
+    slot_ready.resize(slots);
+    slot_done.resize(slots);
+    for (int s = 0; s < slots; ++s) {
+      CK(cudaEventCreateWithFlags(&slot_ready[s], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&slot_done[s], cudaEventDisableTiming));
+    }
   }
 
   cudaError_t launch_row_norms_wrap(const float* X, long long rows, float* out) {
@@ -872,29 +895,140 @@ int rd_index_place(rd_index* h, const rd_placement* p) {
     h->res_row0 = new_res;
     h->host_row0 = new_host_row;
     h->n_resident = n_res;
+    h->host_used = n_off;
     h->budgeted = p->hbm_budget_bytes != 0;
     h->upload_residency();
     h->build_presplit();
-    // staging ring
-    for (auto e : h->slot_ready) cudaEventDestroy(e);
-    for (auto e : h->slot_done) cudaEventDestroy(e);
-    h->slot_ready.clear();
-    h->slot_done.clear();
-    h->staging.reset();
-    h->slots = slots;
-    h->slot_rows = slot_rows;
-    if (slots) {
-      h->staging.alloc((size_t)slots * slot_rows * h->d);
-      h->smap256 = make_row_map(h->staging.p, (long long)slots * slot_rows, h->d, rd::kScanRows);
-      h->smap128 = make_row_map(h->staging.p, (long long)slots * slot_rows, h->d, rd::kTcRows);
-      h->smap32 = make_row_map(h->staging.p, (long long)slots * slot_rows, h->d, 32);
-      h->slot_ready.resize(slots);
-      h->slot_done.resize(slots);
-      for (int s = 0; s < slots; ++s) {
-        CK(cudaEventCreateWithFlags(&h->slot_ready[s], cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&h->slot_done[s], cudaEventDisableTiming));
-      }
+    h->set_staging(slots, slot_rows);
+  });
+}
+
+// ---------------------------------------------------------------- migration
+int rd_index_migrate(rd_index* h, const int32_t* promote, int32_t n_promote, const int32_t* demote, int32_t n_demote,
+                     uint64_t hbm_budget_bytes, rd_migration_stats* st) {
+  return guarded([&] {
+    if (!h || n_promote < 0 || n_demote < 0 || (n_promote && !promote) || (n_demote && !demote))
+      throw_rd(RD_ERR_INVALID, "migrate: invalid arguments");
+    CK(cudaSetDevice(h->device));
+    const auto t0 = std::chrono::steady_clock::now();
+    const int nl = h->nlist, d = h->d;
+    const size_t row_bytes = (size_t)d * sizeof(float);
+    auto len_of = [&](int l) { return h->list_off[l + 1] - h->list_off[l]; };
+    std::vector<uint8_t> seen(nl, 0);
+    for (int i = 0; i < n_promote + n_demote; ++i) {
+      const bool is_p = i < n_promote;
+      const int l = is_p ? promote[i] : demote[i - n_promote];
+      const char* why = nullptr;
+      if (l < 0 || l >= nl)
+        why = "list id out of range";
+      else if (seen[l])
+        why = "list named twice";
+      else if (is_p && h->resident[l])
+        why = "promoted list is already resident";
+      else if (!is_p && !h->resident[l])
+        why = "demoted list is not resident";
+      if (why) throw_rd(RD_ERR_INVALID, "migrate: %s (%d)", why, l);
+      seen[l] = 1;
     }
+    std::vector<uint8_t> after(h->resident);
+    for (int l = 0; l < nl; ++l)
+      if (seen[l]) after[l] = !after[l];
+    long long res_rows = 0, max_off = -1;
+    for (int l = 0; l < nl; ++l) {
+      if (after[l])
+        res_rows += len_of(l);
+      else
+        max_off = std::max(max_off, len_of(l));
+    }
+    const long long slot_rows = max_off >= 0 ? (std::max<long long>(max_off, 16384) + 255) / 256 * 256 : 0;
+    if (hbm_budget_bytes) {
+      const uint64_t need = (uint64_t)res_rows * row_bytes + (max_off >= 0 ? 2ull * slot_rows * row_bytes : 0);
+      if (need > hbm_budget_bytes)
+        throw_rd(RD_ERR_INFEASIBLE, "migration infeasible: %llu bytes needed > budget %llu",
+                 (unsigned long long)need, (unsigned long long)hbm_budget_bytes);
+    }
+    rd_migration_stats ms;
+    std::memset(&ms, 0, sizeof ms);
+    cudaStream_t cs = h->copy_stream;
+    // 1. demote: lists without a host copy go to pinned host memory (write-once copies)
+    long long need_host = h->host_used;
+    for (int i = 0; i < n_demote; ++i)
+      if (h->host_row0[demote[i]] < 0) need_host += len_of(demote[i]);
+    if ((size_t)need_host * d > h->host_arena.n) {  // grow the host arena, keeping its contents
+      HBuf<float> grown;
+      grown.alloc((size_t)std::max<long long>(need_host, h->host_used + h->host_used / 2) * d);
+      if (h->host_used) std::memcpy(grown.p, h->host_arena.p, (size_t)h->host_used * row_bytes);
+      std::swap(h->host_arena.p, grown.p);
+      std::swap(h->host_arena.n, grown.n);
+    }
+    for (int i = 0; i < n_demote; ++i) {
+      const int l = demote[i];
+      if (h->host_row0[l] >= 0) continue;
+      const size_t bytes = (size_t)len_of(l) * row_bytes;
+      CK(cudaMemcpyAsync(h->host_arena.p + (size_t)h->host_used * d, h->arena.p + (size_t)h->res_row0[l] * d, bytes,
+                         cudaMemcpyDeviceToHost, cs));
+      h->host_row0[l] = h->host_used;
+      h->host_used += len_of(l);
+      ms.d2h_bytes += bytes;
+    }
+    CK(cudaStreamSynchronize(cs));
+    // 2. compact the lists that stay resident, in arena order, toward row 0 (forward chunked copies
+    //    never overlap: a chunk is at most the shift)
+    std::vector<int> keep;
+    for (int l = 0; l < nl; ++l)
+      if (h->resident[l] && after[l]) keep.push_back(l);
+    std::sort(keep.begin(), keep.end(), [&](int a, int b) { return h->res_row0[a] < h->res_row0[b]; });
+    long long tail = 0;
+    for (int l : keep) {
+      const long long old = h->res_row0[l], len = len_of(l);
+      if (old != tail && len > 0) {
+        const long long chunk = std::min(len, old - tail);
+        for (long long r = 0; r < len; r += chunk) {
+          const long long c = std::min(chunk, len - r);
+          CK(cudaMemcpyAsync(h->arena.p + (size_t)(tail + r) * d, h->arena.p + (size_t)(old + r) * d, (size_t)c * row_bytes,
+                             cudaMemcpyDeviceToDevice, cs));
+        }
+        ms.d2d_bytes += (size_t)len * row_bytes;
+      }
+      h->res_row0[l] = tail;
+      tail += len;
+    }
+    for (int i = 0; i < n_demote; ++i) h->res_row0[demote[i]] = -1;
+    // 3. promote into the freed space (the arena grows only if the resident set outgrows it)
+    if ((size_t)res_rows * d > h->arena.n) {
+      DBuf<float> grown;
+      grown.alloc((size_t)res_rows * d);
+      if (tail) CK(cudaMemcpyAsync(grown.p, h->arena.p, (size_t)tail * row_bytes, cudaMemcpyDeviceToDevice, cs));
+      CK(cudaStreamSynchronize(cs));
+      std::swap(h->arena.p, grown.p);
+      std::swap(h->arena.n, grown.n);
+    }
+    for (int i = 0; i < n_promote; ++i) {
+      const int l = promote[i];
+      const size_t bytes = (size_t)len_of(l) * row_bytes;
+      if (bytes)
+        CK(cudaMemcpyAsync(h->arena.p + (size_t)tail * d, h->host_arena.p + (size_t)h->host_row0[l] * d, bytes,
+                           cudaMemcpyHostToDevice, cs));
+      h->res_row0[l] = tail;
+      tail += len_of(l);
+      ms.h2d_bytes += bytes;
+    }
+    CK(cudaStreamSynchronize(cs));
+    h->resident = after;
+    h->n_resident = tail;
+    if (hbm_budget_bytes) h->budgeted = true;
+    // 4. staging ring for the new offloaded set (slot >= its largest list)
+    if (max_off < 0)
+      h->set_staging(0, 0);
+    else if (h->slots == 0 || h->slot_rows < slot_rows)
+      h->set_staging(std::max(2, h->slots), slot_rows);
+    h->upload_residency();
+    h->build_presplit();
+    ms.lists_promoted = n_promote;
+    ms.lists_demoted = n_demote;
+    ms.resident_bytes = (uint64_t)tail * row_bytes;
+    ms.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (st) *st = ms;
   });
 }
 

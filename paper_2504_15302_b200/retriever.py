@@ -55,6 +55,12 @@ class Placement(C.Structure):
                 ("staging_slots", C.c_int32), ("reserved", C.c_int32)]
 
 
+class MigrationStats(C.Structure):
+    _fields_ = [("seconds", C.c_double), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
+                ("d2d_bytes", C.c_uint64), ("lists_promoted", C.c_int32), ("lists_demoted", C.c_int32),
+                ("resident_bytes", C.c_uint64)]
+
+
 class SearchStats(C.Structure):
     _fields_ = [("seconds", C.c_double), ("bytes_algorithmic", C.c_uint64),
                 ("bytes_lists_resident", C.c_uint64), ("h2d_list_bytes", C.c_uint64),
@@ -100,6 +106,7 @@ _SIGS = {
     "rd_index_info_get": (C.c_int, [_P, C.POINTER(IndexInfo)]),
     "rd_index_layout": (C.c_int, [_P, _I64P, _I64P, C.POINTER(C.c_uint8)]),
     "rd_index_destroy": (None, [_P]),
+    "rd_index_migrate": (C.c_int, [_P, _I32P, C.c_int32, _I32P, C.c_int32, C.c_uint64, C.c_void_p]),
     "rd_index_save": (C.c_int, [_P, C.c_char_p]),
     "rd_index_load": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(_P)]),
     "rd_search": (C.c_int, [_P, _FP, C.c_int64, C.c_int32, C.c_int32, _I64P, _FP, C.POINTER(SearchStats)]),
@@ -326,6 +333,16 @@ class Index:
                                                        C.c_void_p(stream), 1 if sync else 0, C.byref(st)),
                         "search_device")
         return st.as_dict()
+
+    def migrate(self, promote=(), demote=(), hbm_budget_bytes: int = 0) -> dict:
+        """Between-batch residency change: demote first, compact, then promote (rd_index_migrate)."""
+        pr = np.ascontiguousarray(np.asarray(promote, dtype=np.int32).reshape(-1))
+        de = np.ascontiguousarray(np.asarray(demote, dtype=np.int32).reshape(-1))
+        st = MigrationStats()
+        self._lib.check(self._lib.lib.rd_index_migrate(self._h, pr.ctypes.data_as(_I32P), pr.size,
+                                                       de.ctypes.data_as(_I32P), de.size, hbm_budget_bytes,
+                                                       C.cast(C.byref(st), C.c_void_p)), "migrate")
+        return {f: getattr(st, f) for f, _ in st._fields_}
 
     def save(self, path: str) -> None:
         """Writes the index in the on-disk format (include/rd_format.h)."""
