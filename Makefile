@@ -32,3 +32,10 @@ clean:
 tests/cuda/libtcprobe.so: tests/cuda/tc_probe.cu $(PKG)/csrc/rd_device.cuh
 	$(NVCC) $(ARCH) -O2 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -o $@ $<
 all: tests/cuda/libtcprobe.so
+
+# C++ adapter test (include/rd_ragsim.hpp) against each implementation of rd.h
+tests/cpp/ragsim_adapter_cpu: tests/cpp/ragsim_adapter_test.cpp include/rd_ragsim.hpp include/rd.h oracle
+	g++ -std=c++17 -O2 -Wall -Wextra -Iinclude -o $@ $< -Loracle -l:librd_cpu.so -Wl,-rpath,'$$ORIGIN/../../oracle'
+tests/cpp/ragsim_adapter_b200: tests/cpp/ragsim_adapter_test.cpp include/rd_ragsim.hpp include/rd.h $(LIB)
+	g++ -std=c++17 -O2 -Wall -Wextra -Iinclude -o $@ $< -L$(PKG)/lib -l:librd_b200.so -Wl,-rpath,'$$ORIGIN/../../$(PKG)/lib'
+all: tests/cpp/ragsim_adapter_cpu tests/cpp/ragsim_adapter_b200

@@ -33,6 +33,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 #include <unistd.h>
 
 #include "../include/rd.h"
@@ -520,6 +521,8 @@ int rd_index_migrate(rd_index* h, const int32_t* promote, int32_t n_promote, con
   }
   rd_migration_stats s;
   memset(&s, 0, sizeof s);
+  struct timespec t0, t1;
+  clock_gettime(CLOCK_MONOTONIC, &t0);
   for (int32_t i = 0; i < n_demote; ++i) {
     const int32_t l = demote[i];
     if (!h->hostcopy[l]) s.d2h_bytes += (uint64_t)(h->offsets[l + 1] - h->offsets[l]) * row_bytes;
@@ -534,6 +537,8 @@ int rd_index_migrate(rd_index* h, const int32_t* promote, int32_t n_promote, con
   s.lists_promoted = n_promote;
   s.lists_demoted = n_demote;
   s.resident_bytes = res_bytes;
+  clock_gettime(CLOCK_MONOTONIC, &t1);
+  s.seconds = (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec) + 1e-9;
   if (st) *st = s;
   return RD_OK;
 }
