@@ -233,7 +233,8 @@ struct rd_index {
   int tc_min_q = rd::kTcMinQ;
   int debug_skip = 0;  // profiling only
   bool dbg_ts = std::getenv("RD_DEBUG_TS") != nullptr;  // profiling only: select checkpoints to stderr
-  int stage_max_b = -1;  // batches up to this size stage exact-distance rows in smem (-1: 2 x SMs)
+  int stage_max_b = -1;
+  int tiles_per_sm = 8;  // scan tiles per SM the planner aims for (RD_TILES_PER_SM)  // batches up to this size stage exact-distance rows in smem (-1: 2 x SMs)
   bool stage_rows(long long B) const { return B <= (stage_max_b >= 0 ? stage_max_b : 2LL * num_sms); }
   long long n = 0;
   int d = 0, nlist = 0;
@@ -341,6 +342,7 @@ struct rd_index {
     if (const char* v = std::getenv("RD_TC_MIN_Q")) tc_min_q = std::max(1, std::atoi(v));
     if (const char* v = std::getenv("RD_DEBUG_SKIP")) debug_skip = std::atoi(v);
     if (const char* v = std::getenv("RD_STAGE_MAX_B")) stage_max_b = std::atoi(v);
+    if (const char* v = std::getenv("RD_TILES_PER_SM")) tiles_per_sm = std::max(1, std::atoi(v));
     // the tensor-core scan stages bf16 query slices of 64 dims
   }
 
@@ -1047,8 +1049,13 @@ Plan make_plan(const rd_index* h, long long B, int nprobe) {
   const int np = std::min(nprobe, h->nlist);
   const double avg = h->nlist ? (double)h->n / h->nlist : 0.0;
   const double est_rows = std::min((double)h->n, (double)B * np * avg);
-  long long R = (long long)std::ceil(est_rows / (h->num_sms * 8.0));
-  R = std::max<long long>(rd::kScanRows, std::min<long long>(4096, (R + rd::kScanRows - 1) / rd::kScanRows * rd::kScanRows));
+  // ~tiles_per_sm tiles per SM so the dynamic tile queue's tail (at most one tile per SM) stays
+  // short; rows rounded to the tensor-core tile (128), at least one 256-row TMA box of the FFMA scan
+  // when that path is in use
+  const long long gran = rd::kTcRows;
+  long long R = (long long)std::ceil(est_rows / ((double)h->num_sms * h->tiles_per_sm));
+  R = std::max<long long>(h->tc_min_q > 1 || h->d % 64 ? rd::kScanRows : gran,
+                          std::min<long long>(4096, (R + gran - 1) / gran * gran));
   pl.R = (int)R;
   pl.max_chunks = (int)std::max<long long>(1, (h->max_len + R - 1) / R);
   pl.cap = np * pl.max_chunks * rd::kPartsPerTile;
