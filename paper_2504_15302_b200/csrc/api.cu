@@ -233,8 +233,8 @@ struct rd_index {
   int tc_min_q = rd::kTcMinQ;
   int debug_skip = 0;  // profiling only
   bool dbg_ts = std::getenv("RD_DEBUG_TS") != nullptr;  // profiling only: select checkpoints to stderr
-  int stage_max_b = -1;
-  int tiles_per_sm = 8;  // scan tiles per SM the planner aims for (RD_TILES_PER_SM)  // batches up to this size stage exact-distance rows in smem (-1: 2 x SMs)
+  int stage_max_b = -1;  // batches up to this size stage exact-distance rows in smem (-1: 2 x SMs)
+  int tiles_per_sm = 8;  // scan tiles per SM the planner aims for (RD_TILES_PER_SM)
   bool stage_rows(long long B) const { return B <= (stage_max_b >= 0 ? stage_max_b : 2LL * num_sms); }
   long long n = 0;
   int d = 0, nlist = 0;
