@@ -227,6 +227,8 @@ void parallel_for(long long n, const std::function<void(long long, long long)>& 
 }  // namespace
 
 // ====================================================================== the index
+constexpr size_t kStatBytes = 64;  // per-search counter block (see rd_index::Ws::blk)
+
 struct rd_index {
   int device = 0;
   int num_sms = 148;
@@ -270,21 +272,25 @@ struct rd_index {
 
   // per-search workspace
   struct Ws {
-    DBuf<float> qnorm, Dc, q, dists, qsplit;
-    DBuf<int> probes, list_nq, list_qoff, list_ntile, list_toff, list_q, part_count, part_row, meta, off_meta;
-    DBuf<unsigned> bitmap, fails, fb_ctr;
+    DBuf<float> qnorm, Dc, q, qsplit;
+    DBuf<int> probes, list_nq, list_qoff, list_ntile, list_toff, list_q, part_count, part_row, off_meta;
+    DBuf<unsigned> bitmap, fb_ctr;
     DBuf<rd::ScanTile> tiles, ff_tiles, off_tiles;
-    DBuf<unsigned long long> counters;
     DBuf<float> part_dist;
-    DBuf<long long> ids, fb_id;
+    DBuf<long long> fb_id;
     DBuf<int> fail_list, qthr;
     DBuf<float> fb_dist;
-    HBuf<float> hq, hd;
-    HBuf<long long> hi;
+    HBuf<float> hq;
     HBuf<int> h_nq, h_qoff, h_meta;
+    // per-search counters in one block so a synced search reads them back with one copy:
+    // [0, 24) counters (u64 x 3), [24, 32) fails (u32 x 2), [32, 48) meta (i32 x 4); the host path
+    // places its result ids / distances right after (kStatBytes) and copies everything at once
+    DBuf<char> blk;
+    HBuf<char> h_blk;
+    unsigned long long* counters() const { return reinterpret_cast<unsigned long long*>(blk.p); }
+    unsigned* fails() const { return reinterpret_cast<unsigned*>(blk.p + 24); }
+    int* meta() const { return reinterpret_cast<int*>(blk.p + 32); }
     HBuf<rd::ScanTile> h_tiles;
-    HBuf<unsigned long long> h_counters;
-    HBuf<unsigned> h_fails;
   } ws;
 
   cudaStream_t copy_stream = nullptr, off_stream = nullptr;
@@ -396,6 +402,30 @@ struct rd_index {
     xmap32 = make_split_map(xsplit.p, n_resident, d, 32);
     presplit = true;
   }
+
+  // Profiling only (RD_DEBUG_TS): runs `launch` with its kernel's CTA-0 checkpoint buffer attached
+  // (globaltimer at [i], clock64 at [16 + i], RD_TS in rd_device.cuh), waits, and prints the clock64
+  // offsets of each checkpoint from the first. Otherwise just launches.
+  template <class F>
+  void traced(const char* name, cudaStream_t s, unsigned long long*& slot, F&& launch) {
+    if (!dbg_ts) {
+      launch();
+      return;
+    }
+    if (!dbg_buf.p) dbg_buf.alloc(32);
+    CK(cudaMemsetAsync(dbg_buf.p, 0, 32 * sizeof(unsigned long long), s));
+    slot = dbg_buf.p;
+    launch();
+    slot = nullptr;
+    unsigned long long t[32];
+    CK(cudaMemcpyAsync(t, dbg_buf.p, sizeof t, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    fprintf(stderr, "%s [14]=%lld [15]=%lld cycles:", name, (long long)t[14], (long long)t[15]);
+    for (int i = 1; i < 14; ++i)
+      if (t[16 + i]) fprintf(stderr, " %d:%lld", i, (long long)(t[16 + i] - t[16]));
+    fprintf(stderr, "\n");
+  }
+  DBuf<unsigned long long> dbg_buf;
 
   // H2D staging ring for offloaded lists: `slots` slots of `slot_rows` rows (0 slots: none)
   void set_staging(int nslots, long long nrows) {
@@ -1063,8 +1093,10 @@ Plan make_plan(const rd_index* h, long long B, int nprobe) {
   return pl;
 }
 
+// result_bytes: bytes after the stat block that the sync copy brings back too (the host path's results)
 void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, long long* d_ids, float* d_dists,
-               cudaStream_t s, bool sync, rd_search_stats* st, const std::function<void()>& before_sync = {}) {
+               cudaStream_t s, bool sync, rd_search_stats* st, size_t result_bytes = 0,
+               const std::function<void()>& before_sync = {}) {
   if (nprobe < 1 || k < 1) throw_rd(RD_ERR_INVALID, "search: nprobe >= 1 and k >= 1 required");
   if (k > rd::kMaxK) throw_rd(RD_ERR_INVALID, "search: k <= %d supported, got %d", rd::kMaxK, k);
   if (std::min(nprobe, h->nlist) + rd::kCoarseExtra > 512) throw_rd(RD_ERR_INVALID, "search: nprobe <= 480 supported");
@@ -1086,22 +1118,19 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   w.tiles.ensure(pl.max_tiles);
   w.ff_tiles.ensure(pl.max_tiles);
   w.qsplit.ensure((size_t)B * 2 * d);
-  w.meta.ensure(4);
-  w.counters.ensure(3);
-  w.fails.ensure(2);
+  w.blk.ensure(kStatBytes + result_bytes);
+  w.h_blk.ensure(kStatBytes + result_bytes);
   w.part_count.ensure(B);
   w.part_dist.ensure((size_t)B * pl.cap * rd::kTopK);
   w.part_row.ensure((size_t)B * pl.cap * rd::kTopK);
-  w.h_fails.ensure(2);
-  w.h_counters.ensure(3);
-  w.h_meta.ensure(4);
+
 
   cudaEvent_t* te = h->next_timing_slot();
   cudaEvent_t e0 = te[0], e1 = te[1], e2 = te[2], e3 = h->ev[3], e_plan = h->ev[4], e_off = h->ev[5];
   unsigned long long launches = 0;
   CK(cudaEventRecord(e0, s));
   // ||q||^2 and the query split (the tensor-core scan's operand) in one pass
-  CK(rd::launch_qprep(d_q, B, d, w.qnorm.p, d % 64 == 0 ? w.qsplit.p : nullptr, w.fails.p, w.part_count.p, s));
+  CK(rd::launch_qprep(d_q, B, d, w.qnorm.p, d % 64 == 0 ? w.qsplit.p : nullptr, w.fails(), w.part_count.p, s));
   if (rd::coarse_small((int)B)) {
     CK(rd::launch_coarse_small(d_q, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, h->num_sms, s));
   } else if (d % 64 == 0) {
@@ -1111,43 +1140,14 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     CK(rd::launch_coarse(d_q, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, s));
   }
   w.qthr.ensure(B);
-  rd::SelectParams sp{w.Dc.p, d_q, w.qnorm.p, h->centroids.p, w.probes.p, w.fails.p, (int)B, nl, nprobe, d, h->cmax,
+  rd::SelectParams sp{w.Dc.p, d_q, w.qnorm.p, h->centroids.p, w.probes.p, w.fails(), (int)B, nl, nprobe, d, h->cmax,
                       h->d_list_off.p, h->d_res_row0.p, h->arena.p, h->xmax, w.qthr.p, 0};
-  if (h->dbg_ts) {
-    static unsigned long long* dbg = nullptr;
-    if (!dbg) CK(cudaMalloc(&dbg, 32 * sizeof(unsigned long long)));
-    CK(cudaMemsetAsync(dbg, 0, 32 * sizeof(unsigned long long), s));
-    sp.dbg = dbg;
-    CK(rd::launch_select(sp, h->stage_rows(B), s));
-    if (std::getenv("RD_DEBUG_TWICE")) CK(rd::launch_select(sp, h->stage_rows(B), s));
-    unsigned long long t[32];
-    CK(cudaMemcpyAsync(t, dbg, sizeof t, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    fprintf(stderr, "select ncand=%lld namb=%lld cycles:", (long long)t[15], (long long)t[14]);
-    for (int i = 1; i < 14; ++i) fprintf(stderr, " %d:%lld", i, t[16 + i] ? (long long)(t[16 + i] - t[16]) : -1LL);
-    fprintf(stderr, "\n");
-  } else {
-    CK(rd::launch_select(sp, h->stage_rows(B), s));
-  }
+  h->traced("select", s, sp.dbg, [&] { CK(rd::launch_select(sp, h->stage_rows(B), s)); });
   launches += 3;
   rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
-                    w.list_ntile.p, w.list_toff.p, w.list_q.p, w.tiles.p, w.ff_tiles.p, w.meta.p, w.counters.p,
+                    w.list_ntile.p, w.list_toff.p, w.list_q.p, w.tiles.p, w.ff_tiles.p, w.meta(), w.counters(),
                     (int)B, nl, nprobe, pl.R, d % 64 == 0 ? h->tc_min_q : 1 << 30};
-  if (h->dbg_ts) {
-    static unsigned long long* dbg = nullptr;
-    if (!dbg) CK(cudaMalloc(&dbg, 32 * sizeof(unsigned long long)));
-    CK(cudaMemsetAsync(dbg, 0, 32 * sizeof(unsigned long long), s));
-    pp.dbg = dbg;
-    CK(rd::launch_plan(pp, s));
-    unsigned long long t[32];
-    CK(cudaMemcpyAsync(t, dbg, sizeof t, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    fprintf(stderr, "plan cycles:");
-    for (int i = 1; i < 8; ++i) fprintf(stderr, " %d:%lld", i, t[16 + i] ? (long long)(t[16 + i] - t[16]) : -1LL);
-    fprintf(stderr, "\n");
-  } else {
-    CK(rd::launch_plan(pp, s));
-  }
+  h->traced("plan", s, pp.dbg, [&] { CK(rd::launch_plan(pp, s)); });
   launches += rd::plan_fused_ok((int)B, nl) ? 1 : 4;
   CK(cudaEventRecord(e1, s));
 
@@ -1160,9 +1160,9 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   }
   CK(cudaEventRecord(e_plan, s));
   const CUtensorMap gmap = make_gather_map(w.qsplit.p, B, d);
-  rd::ScanParams sc{w.ff_tiles.p, w.meta.p + 2, w.meta.p + 3, d_q, w.qnorm.p, w.list_q.p, h->xnorm.p,
+  rd::ScanParams sc{w.ff_tiles.p, w.meta() + 2, w.meta() + 3, d_q, w.qnorm.p, w.list_q.p, h->xnorm.p,
                     w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p};
-  rd::TcScanParams tc{w.tiles.p, w.meta.p, w.meta.p + 1, w.qsplit.p, w.qnorm.p, w.list_q.p, h->xnorm.p,
+  rd::TcScanParams tc{w.tiles.p, w.meta(), w.meta() + 1, w.qsplit.p, w.qnorm.p, w.list_q.p, h->xnorm.p,
                       w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p, h->debug_skip};
   if (d % 64 != 0 || h->tc_min_q > 1) {  // FFMA tiles exist only in these cases
     CK(rd::launch_scan(h->map256, h->map32, sc, h->num_sms, s));
@@ -1295,9 +1295,9 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   w.fb_id.ensure((size_t)B * nprobe * rd::kTopK);
   rd::MergeParams mp{w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d_q, w.qnorm.p, h->d_list_off.p,
                      h->d_list_base.p, h->d_ids.p, h->d_row_list.p, nl, d, k, h->xmax, d_ids, d_dists,
-                     w.fails.p + 1, w.fail_list.p, (int)B};
+                     w.fails() + 1, w.fail_list.p, (int)B};
   CK(rd::launch_merge(mp, h->stage_rows(B), s));
-  rd::FallbackParams fp{w.fail_list.p, w.fails.p + 1, w.probes.p, nprobe, d_q, h->d_list_off.p, h->d_list_base.p,
+  rd::FallbackParams fp{w.fail_list.p, w.fails() + 1, w.probes.p, nprobe, d_q, h->d_list_off.p, h->d_list_base.p,
                         h->d_ids.p, nl, d, k, w.fb_dist.p, w.fb_id.p, d_ids, d_dists, w.fb_ctr.p};
   CK(rd::launch_fallback(fp, h->num_sms, s));
   launches += 2;
@@ -1308,20 +1308,21 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   }
   if (before_sync) before_sync();  // e.g. the host path's result copies, ordered before the one sync
   if (sync) {
-    CK(cudaMemcpyAsync(w.h_counters.p, w.counters.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(w.h_fails.p, w.fails.p, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(w.h_meta.p, w.meta.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    // counters (and, on the host path, the results placed after them) in one copy
+    CK(cudaMemcpyAsync(w.h_blk.p, w.blk.p, kStatBytes + result_bytes, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    const auto* hc = reinterpret_cast<const unsigned long long*>(w.h_blk.p);
+    const auto* hf = reinterpret_cast<const unsigned*>(w.h_blk.p + 24);
+    const auto* hm = reinterpret_cast<const int*>(w.h_blk.p + 32);
     if (st) {
       float ms = 0;
       const unsigned long long row_bytes = (unsigned long long)d * 4;
-      st->lists_probed = w.h_counters.p[0];
-      st->bytes_lists_resident = w.h_counters.p[1] * row_bytes;
+      st->lists_probed = hc[0];
+      st->bytes_lists_resident = hc[1] * row_bytes;
       st->h2d_list_bytes = h2d;
-      st->bytes_algorithmic = (w.h_counters.p[1] + w.h_counters.p[2]) * row_bytes +
-                              (unsigned long long)nl * row_bytes + (unsigned long long)B * row_bytes +
-                              (unsigned long long)B * k * 12ull;
-      st->tiles = (uint64_t)w.h_meta.p[0] + (uint64_t)w.h_meta.p[2];
+      st->bytes_algorithmic = (hc[1] + hc[2]) * row_bytes + (unsigned long long)nl * row_bytes +
+                              (unsigned long long)B * row_bytes + (unsigned long long)B * k * 12ull;
+      st->tiles = (uint64_t)hm[0] + (uint64_t)hm[2];
       CK(cudaEventElapsedTime(&ms, e1, e2));
       st->scan_ms = ms;
       CK(cudaEventElapsedTime(&ms, e0, e1));
@@ -1330,8 +1331,8 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
         CK(cudaEventElapsedTime(&ms, e_plan, e_off));
         st->offload_ms = ms;
       }
-      st->probe_failures = w.h_fails.p[0];
-      st->margin_failures = w.h_fails.p[1];
+      st->probe_failures = hf[0];
+      st->margin_failures = hf[1];
     }
   }
 }
@@ -1367,8 +1368,6 @@ int rd_search(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int3
     auto& w = h->ws;
     const size_t qn = (size_t)B * h->d, rn = (size_t)B * k;
     w.q.ensure(qn);
-    w.ids.ensure(rn);
-    w.dists.ensure(rn);
     // caller buffers that are already page-locked are copied directly; others go through the
     // handle's pinned staging buffers
     auto pinned = [](const void* ptr) {
@@ -1386,16 +1385,24 @@ int rd_search(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int3
       std::memcpy(w.hq.p, queries, qn * sizeof(float));
       qsrc = w.hq.p;
     }
-    long long* idst = pi ? reinterpret_cast<long long*>(out_ids) : (w.hi.ensure(rn), w.hi.p);
-    float* ddst = pd ? out_dists : (w.hd.ensure(rn), w.hd.p);
     cudaStream_t s = 0;
     CK(cudaMemcpyAsync(w.q.p, qsrc, qn * sizeof(float), cudaMemcpyHostToDevice, s));
-    do_search(h, w.q.p, B, nprobe, k, w.ids.p, w.dists.p, s, true, st, [&] {
-      CK(cudaMemcpyAsync(idst, w.ids.p, rn * sizeof(long long), cudaMemcpyDeviceToHost, s));
-      CK(cudaMemcpyAsync(ddst, w.dists.p, rn * sizeof(float), cudaMemcpyDeviceToHost, s));
+    // results live right after the stat block: pinned caller buffers get direct copies, otherwise
+    // stats and results come back in the sync's single copy
+    const bool direct = pi && pd;
+    const size_t res_bytes = rn * (sizeof(long long) + sizeof(float));
+    w.blk.ensure(kStatBytes + res_bytes);
+    long long* d_ids = reinterpret_cast<long long*>(w.blk.p + kStatBytes);
+    float* d_dists = reinterpret_cast<float*>(w.blk.p + kStatBytes + rn * sizeof(long long));
+    do_search(h, w.q.p, B, nprobe, k, d_ids, d_dists, s, true, st, direct ? 0 : res_bytes, [&] {
+      if (!direct) return;
+      CK(cudaMemcpyAsync(out_ids, d_ids, rn * sizeof(long long), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(out_dists, d_dists, rn * sizeof(float), cudaMemcpyDeviceToHost, s));
     });
-    if (!pi) std::memcpy(out_ids, w.hi.p, rn * sizeof(long long));
-    if (!pd) std::memcpy(out_dists, w.hd.p, rn * sizeof(float));
+    if (!direct) {
+      std::memcpy(out_ids, w.h_blk.p + kStatBytes, rn * sizeof(long long));
+      std::memcpy(out_dists, w.h_blk.p + kStatBytes + rn * sizeof(long long), rn * sizeof(float));
+    }
     if (st) st->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   });
 }
@@ -1413,9 +1420,9 @@ int rd_probe(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32
     w.qnorm.ensure(B);
     w.Dc.ensure((size_t)B * nl);
     w.probes.ensure((size_t)B * nprobe);
-    w.fails.ensure(2);
+    w.blk.ensure(kStatBytes);
     CK(cudaMemcpy(w.q.p, queries, sizeof(float) * B * d, cudaMemcpyHostToDevice));
-    CK(cudaMemset(w.fails.p, 0, 2 * sizeof(unsigned)));
+    CK(cudaMemset(w.fails(), 0, 2 * sizeof(unsigned)));
     w.qsplit.ensure((size_t)B * d);
     CK(rd::launch_qprep(w.q.p, B, d, w.qnorm.p, d % 64 == 0 ? w.qsplit.p : nullptr, nullptr, nullptr, 0));
     if (rd::coarse_small((int)B)) {
@@ -1426,7 +1433,7 @@ int rd_probe(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32
     } else {
       CK(rd::launch_coarse(w.q.p, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, 0));
     }
-    rd::SelectParams sp{w.Dc.p, w.q.p, w.qnorm.p, h->centroids.p, w.probes.p, w.fails.p, (int)B, nl, nprobe, d, h->cmax,
+    rd::SelectParams sp{w.Dc.p, w.q.p, w.qnorm.p, h->centroids.p, w.probes.p, w.fails(), (int)B, nl, nprobe, d, h->cmax,
                         h->d_list_off.p, h->d_res_row0.p, h->arena.p, h->xmax, nullptr, 1};
     CK(rd::launch_select(sp, h->stage_rows(B), 0));
     CK(cudaMemcpy(out_lists, w.probes.p, sizeof(int) * B * nprobe, cudaMemcpyDeviceToHost));
