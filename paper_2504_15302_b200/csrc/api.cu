@@ -1148,7 +1148,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
                     w.list_ntile.p, w.list_toff.p, w.list_q.p, w.tiles.p, w.ff_tiles.p, w.meta(), w.counters(),
                     (int)B, nl, nprobe, pl.R, d % 64 == 0 ? h->tc_min_q : 1 << 30};
   h->traced("plan", s, pp.dbg, [&] { CK(rd::launch_plan(pp, s)); });
-  launches += rd::plan_fused_ok((int)B, nl) ? 1 : 4;
+  launches += rd::plan_small_ok((int)B, nprobe) || rd::plan_fused_ok((int)B, nl) ? 1 : 4;
   CK(cudaEventRecord(e1, s));
 
   const bool has_off = h->slots > 0;

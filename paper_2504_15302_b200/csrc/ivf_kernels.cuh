@@ -153,7 +153,8 @@ struct PlanParams {
   unsigned long long* dbg = nullptr;  // RD_DEBUG_TS: globaltimer checkpoints of CTA 0
 };
 cudaError_t launch_plan(const PlanParams& p, cudaStream_t s);
-bool plan_fused_ok(int B, int nlist);  // the single-CTA plan applies
+bool plan_fused_ok(int B, int nlist);  // the single-CTA bitmap plan applies
+bool plan_small_ok(int B, int nprobe);  // the single-CTA sorted-pairs plan applies (B * nprobe <= 512)
 
 struct MergeParams {
   const float* part_dist;

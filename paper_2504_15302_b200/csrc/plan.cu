@@ -365,7 +365,116 @@ __global__ void __launch_bounds__(kPlanThreads) plan_fused_kernel(const PlanPara
   RD_TS(4);
 }
 
+// Tiny batches (B * nprobe <= 1024 pairs): plan from the probe pairs alone. The (list, query) pairs
+// are rank-sorted in one CTA; a list's segment in sorted order IS its query CSR (list_q = the sorted
+// query ids, ascending within a list), so the only passes are O(pairs) plus one coalesced zeroing of
+// list_nq. Same outputs as the bitmap planners for every list.
+constexpr int kSmallPlanThreads = 1024;
+__global__ void __launch_bounds__(kSmallPlanThreads) plan_small_kernel(const PlanParams p) {
+  RD_PDL_PROLOGUE();
+  __shared__ unsigned long long key[kSmallPlanThreads];
+  __shared__ int wsum[3][32];
+  __shared__ unsigned long long wcnt[3][32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int P = p.B * p.nprobe;
+  RD_TS(0);
+  // (list, query) keys; padding / invalid probes sort last
+  unsigned long long kv = ~0ull;
+  if (tid < P) {
+    const int l = p.probes[tid];
+    if (l >= 0) kv = ((unsigned long long)(unsigned)l << 32) | (unsigned)(tid / p.nprobe);
+  }
+  key[tid] = kv;
+  for (int j = tid; j < p.nlist; j += kSmallPlanThreads) p.list_nq[j] = 0;  // coalesced
+  __syncthreads();
+  int r = 0;  // rank of this thread's key (keys are distinct)
+  if (kv != ~0ull)
+    for (int i = 0; i < P; ++i) r += key[i] < kv;
+  __syncthreads();
+  if (kv != ~0ull) key[r] = kv;
+  // number of valid pairs
+  const int valid = __syncthreads_count(kv != ~0ull);
+  RD_TS(1);
+  // segment starts in sorted order: thread t owns sorted position t
+  const unsigned long long mine = tid < valid ? key[tid] : ~0ull;
+  const int l = (int)(mine >> 32);
+  const bool start = tid < valid && (tid == 0 || (key[tid - 1] >> 32) != (mine >> 32));
+  int nq = 0, ntc = 0, nff = 0, chunks = 0, len = 0;
+  long long src0 = -1, g0 = 0;
+  if (start) {
+    int e = tid + 1;
+    while (e < valid && (key[e] >> 32) == (mine >> 32)) ++e;
+    nq = e - tid;
+    g0 = p.list_off[l];
+    len = (int)(p.list_off[l + 1] - g0);
+    src0 = p.res_row0[l];
+    if (src0 >= 0 && len > 0) {
+      chunks = (len + p.R - 1) / p.R;
+      group_split(nq, p.tc_min_q, ntc, nff);
+    }
+  }
+  if (tid < valid) p.list_q[tid] = (int)(mine & 0xffffffffu);
+  // block scan of the segment starts' (1, tc tiles, ff tiles)
+  int v[3] = {start ? 1 : 0, ntc * chunks, nff * chunks};
+  int inc[3] = {v[0], v[1], v[2]};
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int y = __shfl_up_sync(0xffffffffu, inc[i], o);
+      if (lane >= o) inc[i] += y;
+    }
+  if (lane == 31)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) wsum[i][w] = inc[i];
+  unsigned long long cc[3] = {start ? 1ull : 0ull, start && src0 >= 0 ? (unsigned long long)len : 0ull,
+                              start && src0 < 0 ? (unsigned long long)len : 0ull};
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) cc[i] += __shfl_xor_sync(0xffffffffu, cc[i], o);
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) wcnt[i][w] = cc[i];
+  __syncthreads();
+  if (w == 0) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      int a = wsum[i][lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, a, o);
+        if (lane >= o) a += y;
+      }
+      wsum[i][lane] = a;
+      unsigned long long c = wcnt[i][lane];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if (lane == 0) p.counters[i] = c;
+    }
+    if (lane == 0) {
+      p.meta[0] = wsum[1][31];
+      p.meta[1] = 0;
+      p.meta[2] = wsum[2][31];
+      p.meta[3] = 0;
+    }
+  }
+  __syncthreads();
+  RD_TS(2);
+  if (start) {
+    const int o1 = (w ? wsum[1][w - 1] : 0) + inc[1] - v[1];
+    const int o2 = (w ? wsum[2][w - 1] : 0) + inc[2] - v[2];
+    p.list_nq[l] = nq;
+    p.list_qoff[l] = tid;
+    if (ntc + nff > 0) emit_tiles(p, l, nq, tid, len, src0, g0, o1, o2, ntc, nff, chunks, 0, 1);
+  }
+  RD_TS(3);
+}
+
 }  // namespace
+
+// the rank sort is O(pairs) per thread: beyond ~512 pairs the bitmap planners win
+bool plan_small_ok(int B, int nprobe) { return (long long)B * nprobe <= 512; }
 
 bool plan_fused_ok(int B, int nlist) {
   const long long W = (B + 31) / 32;
@@ -375,6 +484,7 @@ bool plan_fused_ok(int B, int nlist) {
 }
 
 cudaError_t launch_plan(const PlanParams& p, cudaStream_t s) {
+  if (plan_small_ok(p.B, p.nprobe)) return launch_k(plan_small_kernel, dim3(1), dim3(kSmallPlanThreads), 0, s, p);
   if (plan_fused_ok(p.B, p.nlist)) {
     const int smem = p.nlist * (p.W + 1) * (int)sizeof(unsigned);
     static int attr = 0;

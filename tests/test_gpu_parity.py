@@ -49,16 +49,17 @@ def test_engine_vs_oracle_synthetic(engine, oracle, B, nprobe, k, presplit, monk
     _check(e, o.ids, o.dists)
 
 
-@pytest.mark.parametrize("B", [1, 16, 17, 64, 128, 200])
-def test_engine_vs_oracle_many_lists(engine, oracle, B):
-    # nlist 4096 (the C2 coarse size): small-batch GEMV coarse (B <= 16), tensor-core coarse, the
-    # single-CTA plan (B <= 128, bitmap of up to 4 words per list in smem), the multi-kernel plan,
-    # smem-staged select / rerank (B <= 2 x SMs)
+@pytest.mark.parametrize("B,nprobe", [(1, 64), (8, 64), (6, 100), (16, 64), (17, 64), (64, 64), (128, 64),
+                                      (200, 64)])
+def test_engine_vs_oracle_many_lists(engine, oracle, B, nprobe):
+    # nlist 4096 (the C2 coarse size): small-batch GEMV coarse (B <= 8), tensor-core coarse, the
+    # sorted-pairs plan (B * nprobe <= 512), the single-CTA bitmap plan (B <= 8, more pairs), the
+    # multi-kernel plan, smem-staged select / rerank (B <= 2 x SMs)
     n, d, nlist = 200000, 768, 4096
     desc = engine.desc(n, d, nlist)
     q, _ = engine.synth_queries(desc, 7, B)
-    e = engine.synthetic_index(desc).search(q, 64, 10)
-    o = oracle.synthetic_index(desc).search(q, 64, 10)
+    e = engine.synthetic_index(desc).search(q, nprobe, 10)
+    o = oracle.synthetic_index(desc).search(q, nprobe, 10)
     _check(e, o.ids, o.dists)
 
 
@@ -95,9 +96,10 @@ def test_from_host_ties_duplicates_empty_lists(engine, oracle):
         np.testing.assert_array_equal(e.dists, o.dists)
 
 
-@pytest.mark.parametrize("frac", [0.5, 1.0])
-def test_offloaded_lists_same_results(engine, oracle, frac):
-    n, d, nlist, B, nprobe, k = 60000, 768, 64, 48, 16, 10
+@pytest.mark.parametrize("frac,B", [(0.5, 48), (1.0, 48), (0.5, 2), (0.5, 8)])
+def test_offloaded_lists_same_results(engine, oracle, frac, B):
+    # B 2 / 8: the sorted-pairs planner with offloaded lists (their pairs get no device tiles)
+    n, d, nlist, nprobe, k = 60000, 768, 64, 16, 10
     desc = engine.desc(n, d, nlist)
     q, _ = engine.synth_queries(desc, 77, B)
     idx = engine.synthetic_index(desc)
