@@ -237,6 +237,7 @@ struct rd_index {
   bool dbg_ts = std::getenv("RD_DEBUG_TS") != nullptr;  // profiling only: select checkpoints to stderr
   int stage_max_b = -1;  // batches up to this size stage exact-distance rows in smem (-1: 2 x SMs)
   int tiles_per_sm = 8;  // scan tiles per SM the planner aims for (RD_TILES_PER_SM)
+  bool no_inner_events = std::getenv("RD_NO_INNER_EVENTS") != nullptr;  // A/B: no per-stage timing events
   bool stage_rows(long long B) const { return B <= (stage_max_b >= 0 ? stage_max_b : 2LL * num_sms); }
   long long n = 0;
   int d = 0, nlist = 0;
@@ -305,9 +306,11 @@ struct rd_index {
     cudaEvent_t* e = tev[i % kRing];
     CK(cudaEventSynchronize(e[3]));
     float a = 0, b = 0, c = 0, t = 0;
-    CK(cudaEventElapsedTime(&a, e[0], e[1]));
-    CK(cudaEventElapsedTime(&b, e[1], e[2]));
-    CK(cudaEventElapsedTime(&c, e[2], e[3]));
+    if (!no_inner_events) {
+      CK(cudaEventElapsedTime(&a, e[0], e[1]));
+      CK(cudaEventElapsedTime(&b, e[1], e[2]));
+      CK(cudaEventElapsedTime(&c, e[2], e[3]));
+    }
     CK(cudaEventElapsedTime(&t, e[0], e[3]));
     t_acc.searches += 1;
     t_acc.coarse_ms += a;
@@ -425,7 +428,7 @@ struct rd_index {
       if (t[16 + i]) fprintf(stderr, " %d:%lld", i, (long long)(t[16 + i] - t[16]));
     fprintf(stderr, "\n");
   }
-  DBuf<unsigned long long> dbg_buf;
+  DBuf<unsigned long long> dbg_buf, dbg_scan;
 
   // H2D staging ring for offloaded lists: `slots` slots of `slot_rows` rows (0 slots: none)
   void set_staging(int nslots, long long nrows) {
@@ -1149,7 +1152,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
                     (int)B, nl, nprobe, pl.R, d % 64 == 0 ? h->tc_min_q : 1 << 30};
   h->traced("plan", s, pp.dbg, [&] { CK(rd::launch_plan(pp, s)); });
   launches += rd::plan_small_ok((int)B, nprobe) || rd::plan_fused_ok((int)B, nl) ? 1 : 4;
-  CK(cudaEventRecord(e1, s));
+  if (!h->no_inner_events) CK(cudaEventRecord(e1, s));
 
   const bool has_off = h->slots > 0;
   if (has_off) {  // fetch the probe histogram for host-side staging decisions
@@ -1169,11 +1172,33 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     launches += 1;
   }
   if (d % 64 == 0) {  // the tensor-core path stages 64-dim bf16 query slices; otherwise every tile is FFMA
+    if (h->dbg_ts) {  // profiling only: per-CTA entry / ready / first tile / end times
+      if (h->dbg_scan.n < 4 * (size_t)h->num_sms) h->dbg_scan.alloc(4 * (size_t)h->num_sms);
+      CK(cudaMemsetAsync(h->dbg_scan.p, 0, 8 * 4 * (size_t)h->num_sms, s));
+      tc.dbg = h->dbg_scan.p;
+    }
     CK(rd::launch_scan_tc(h->presplit ? h->xmap128 : h->map128, h->presplit ? h->xmap32 : h->map32, gmap, tc,
                           h->num_sms, s, h->presplit));
     launches += 1;
+    if (h->dbg_ts) {
+      std::vector<unsigned long long> t(4 * (size_t)h->num_sms);
+      CK(cudaMemcpyAsync(t.data(), h->dbg_scan.p, 8 * t.size(), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      unsigned long long t0 = ~0ull, mx[4] = {0, 0, 0, 0};
+      for (int c = 0; c < h->num_sms; ++c) t0 = std::min(t0, t[4 * c]);
+      double mean[4] = {0, 0, 0, 0};
+      for (int c = 0; c < h->num_sms; ++c)
+        for (int j = 0; j < 4; ++j) {
+          const unsigned long long v = t[4 * c + j] ? t[4 * c + j] - t0 : 0;
+          mx[j] = std::max(mx[j], v);
+          mean[j] += (double)v / h->num_sms;
+        }
+      fprintf(stderr, "scan ns from first CTA entry: entry mean %.0f max %llu | ready mean %.0f max %llu | "
+              "first tile mean %.0f max %llu | end mean %.0f max %llu\n", mean[0], mx[0], mean[1], mx[1], mean[2],
+              mx[2], mean[3], mx[3]);
+    }
   }
-  CK(cudaEventRecord(e2, s));
+  if (!h->no_inner_events) CK(cudaEventRecord(e2, s));
 
   unsigned long long h2d = 0;
   if (has_off) {
@@ -1323,10 +1348,12 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
       st->bytes_algorithmic = (hc[1] + hc[2]) * row_bytes + (unsigned long long)nl * row_bytes +
                               (unsigned long long)B * row_bytes + (unsigned long long)B * k * 12ull;
       st->tiles = (uint64_t)hm[0] + (uint64_t)hm[2];
-      CK(cudaEventElapsedTime(&ms, e1, e2));
-      st->scan_ms = ms;
-      CK(cudaEventElapsedTime(&ms, e0, e1));
-      st->coarse_ms = ms;
+      if (!h->no_inner_events) {
+        CK(cudaEventElapsedTime(&ms, e1, e2));
+        st->scan_ms = ms;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        st->coarse_ms = ms;
+      }
       if (has_off) {
         CK(cudaEventElapsedTime(&ms, e_plan, e_off));
         st->offload_ms = ms;

@@ -83,6 +83,7 @@ struct TcScanParams {
   int d;
   int* qthr;               // B: per-query pruning threshold (f2ord), min over completed tiles' 32nd
   int debug_skip;          // profiling only (RD_DEBUG_SKIP): 1 = no epilogue selection, 2 = no conversion, 4 = no MMA
+  unsigned long long* dbg = nullptr;  // profiling only (RD_DEBUG_TS): per CTA [entry, ready, first tile, end] globaltimer
 };
 
 size_t scan_smem_bytes(int d);

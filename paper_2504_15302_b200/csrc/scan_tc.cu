@@ -96,6 +96,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ivf_scan_tc_kernel(const __grid_constant__ CUtensorMap map128, const __grid_constant__ CUtensorMap map32,
                        const __grid_constant__ CUtensorMap qmap, const TcScanParams p) {
   RD_PDL_PROLOGUE();
+  if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 4 + 0] = gtimer();
   extern __shared__ unsigned char smem_raw[];
   const int d = p.d, nks = kPre ? d / 64 : d / 32;
   const Smem sm = carve(smem_raw, d);
@@ -129,6 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *sm.tmem_base;
   const int ntiles = *p.ntiles;
+  if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 4 + 1] = gtimer();
 
   // ---------------------------------------------------------------- warp 0: TMA producer
   if (warp == 0) {
@@ -223,6 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (t < 0) break;
       const ScanTile T = p.tiles[t];
       mbar_wait(sm.bfull, ti & 1);  // this tile's queries are in the B operand
+      if (p.dbg && ti == 0 && lane == 0) p.dbg[blockIdx.x * 4 + 2] = gtimer();
       for (int rt = 0; rt * kRows < T.nrows; ++rt, ++rtc) {
         const int a = rtc & 1;
         mbar_wait(&sm.aempty[a], ((rtc >> 1) & 1) ^ 1);
@@ -479,6 +482,7 @@ done:
     tc_fence_after();
     tmem_dealloc(tmem, kTmemCols);
   }
+  if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 4 + 3] = gtimer();
 }
 
 // q -> (q1, q2) bf16 rows: out[b][0][:] = bf16(q), out[b][1][:] = bf16(q - q1)
