@@ -238,6 +238,9 @@ struct rd_index {
   int stage_max_b = -1;  // batches up to this size stage exact-distance rows in smem (-1: 2 x SMs)
   int tiles_per_sm = 8;  // scan tiles per SM the planner aims for (RD_TILES_PER_SM)
   bool no_inner_events = std::getenv("RD_NO_INNER_EVENTS") != nullptr;  // A/B: no per-stage timing events
+  // the tensor-core scan stages 64-dim bf16 query slices of up to 32 queries in shared memory:
+  // d % 64 == 0 and d <= 896 (beyond, its B operand does not fit next to the x ring); else FFMA
+  bool tc_scan() const { return d % 64 == 0 && rd::scan_tc_smem_bytes(d) <= 227 * 1024; }
   bool stage_rows(long long B) const { return B <= (stage_max_b >= 0 ? stage_max_b : 2LL * num_sms); }
   long long n = 0;
   int d = 0, nlist = 0;
@@ -393,7 +396,7 @@ struct rd_index {
     xsplit.reset();
     const char* env = std::getenv("RD_PRESPLIT");
     // a byte budget (e.g. the LLM reservation, C5) must not be exceeded by a second copy
-    if (d % 64 != 0 || (env && std::atoi(env) == 0) || n_resident == 0 || budgeted) return;
+    if (!tc_scan() || (env && std::atoi(env) == 0) || n_resident == 0 || budgeted) return;
     size_t fr = 0, tot = 0;
     CK(cudaMemGetInfo(&fr, &tot));
     const size_t need = (size_t)n_resident * d * 4;
@@ -1087,7 +1090,7 @@ Plan make_plan(const rd_index* h, long long B, int nprobe) {
   // when that path is in use
   const long long gran = rd::kTcRows;
   long long R = (long long)std::ceil(est_rows / ((double)h->num_sms * h->tiles_per_sm));
-  R = std::max<long long>(h->tc_min_q > 1 || h->d % 64 ? rd::kScanRows : gran,
+  R = std::max<long long>(h->tc_min_q > 1 || !h->tc_scan() ? rd::kScanRows : gran,
                           std::min<long long>(4096, (R + gran - 1) / gran * gran));
   pl.R = (int)R;
   pl.max_chunks = (int)std::max<long long>(1, (h->max_len + R - 1) / R);
@@ -1149,7 +1152,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   launches += 3;
   rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
                     w.list_ntile.p, w.list_toff.p, w.list_q.p, w.tiles.p, w.ff_tiles.p, w.meta(), w.counters(),
-                    (int)B, nl, nprobe, pl.R, d % 64 == 0 ? h->tc_min_q : 1 << 30};
+                    (int)B, nl, nprobe, pl.R, h->tc_scan() ? h->tc_min_q : 1 << 30};
   h->traced("plan", s, pp.dbg, [&] { CK(rd::launch_plan(pp, s)); });
   launches += rd::plan_small_ok((int)B, nprobe) || rd::plan_fused_ok((int)B, nl) ? 1 : 4;
   if (!h->no_inner_events) CK(cudaEventRecord(e1, s));
@@ -1167,11 +1170,11 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
                     w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p};
   rd::TcScanParams tc{w.tiles.p, w.meta(), w.meta() + 1, w.qsplit.p, w.qnorm.p, w.list_q.p, h->xnorm.p,
                       w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p, h->debug_skip};
-  if (d % 64 != 0 || h->tc_min_q > 1) {  // FFMA tiles exist only in these cases
+  if (!h->tc_scan() || h->tc_min_q > 1) {  // FFMA tiles exist only in these cases
     CK(rd::launch_scan(h->map256, h->map32, sc, h->num_sms, s));
     launches += 1;
   }
-  if (d % 64 == 0) {  // the tensor-core path stages 64-dim bf16 query slices; otherwise every tile is FFMA
+  if (h->tc_scan()) {  // otherwise every tile is FFMA
     if (h->dbg_ts) {  // profiling only: per-CTA entry / ready / first tile / end times
       if (h->dbg_scan.n < 4 * (size_t)h->num_sms) h->dbg_scan.alloc(4 * (size_t)h->num_sms);
       CK(cudaMemsetAsync(h->dbg_scan.p, 0, 8 * 4 * (size_t)h->num_sms, s));
@@ -1228,7 +1231,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
       for (int l : batches[bi]) {
         const long long len = h->list_off[l + 1] - h->list_off[l];
         const int nq = w.h_nq.p[l];
-        const bool tcl = nq >= h->tc_min_q && d % 64 == 0;
+        const bool tcl = nq >= h->tc_min_q && h->tc_scan();
         const int ngr = tcl ? (nq + rd::kTcG - 1) / rd::kTcG : (nq + rd::kScanG - 1) / rd::kScanG;
         for (long long c = 0; c * pl.R < len; ++c)
           for (int g = 0; g < ngr; ++g) {

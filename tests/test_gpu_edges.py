@@ -1,0 +1,74 @@
+"""GPU edge cases against the oracle: dimension limits (FFMA paths at d % 64 != 0, the
+largest d), nprobe beyond nlist, a single list, fewer candidates than k, empty batches,
+scaled data, and the engine's argument validation (ragsim ParseError, exit code 2)."""
+import numpy as np
+import pytest
+
+from paper_2504_15302_b200.retriever import ParseError
+
+pytestmark = pytest.mark.gpu
+
+
+def _same(e, o):
+    np.testing.assert_array_equal(e.ids, o.ids)
+    np.testing.assert_array_equal(e.dists, o.dists)  # exact fallbacks may run; results must not differ
+
+
+@pytest.mark.parametrize("d", [32, 96, 1024])
+def test_dimension_limits(engine, oracle, d):
+    desc = engine.desc(12000, d, 24)
+    q, _ = engine.synth_queries(desc, 3, 20)
+    _same(engine.synthetic_index(desc).search(q, 5, 10), oracle.synthetic_index(desc).search(q, 5, 10))
+
+
+def test_nprobe_beyond_nlist_and_single_list(engine, oracle):
+    desc = engine.desc(3000, 128, 9)
+    q, _ = engine.synth_queries(desc, 0, 7)
+    e, o = engine.synthetic_index(desc), oracle.synthetic_index(desc)
+    _same(e.search(q, 50, 12), o.search(q, 50, 12))  # every list probed
+    pe, po = e.probe(q, 12), o.probe(q, 12)
+    np.testing.assert_array_equal(pe, po)
+    assert (pe[:, 9:] == -1).all()
+    one = engine.desc(2000, 64, 1)
+    q1, _ = engine.synth_queries(one, 0, 5)
+    _same(engine.synthetic_index(one).search(q1, 1, 24), oracle.synthetic_index(one).search(q1, 1, 24))
+
+
+def test_fewer_candidates_than_k(engine, oracle):
+    rng = np.random.default_rng(11)
+    d, nlist = 64, 6
+    lens = np.array([3, 0, 5, 0, 2, 1])
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    X = rng.standard_normal((int(lens.sum()), d)).astype(np.float32)
+    C = rng.standard_normal((nlist, d)).astype(np.float32)
+    Q = rng.standard_normal((4, d)).astype(np.float32)
+    e = engine.index_from_host(X, offs, C).search(Q, 2, 20)
+    o = oracle.index_from_host(X, offs, C).search(Q, 2, 20)
+    _same(e, o)
+    assert (e.ids == -1).any() and np.isinf(e.dists[e.ids == -1]).all()
+
+
+def test_empty_batch_and_scaled_data(engine, oracle):
+    desc = engine.desc(5000, 128, 16)
+    idx = engine.synthetic_index(desc)
+    r = idx.search(np.zeros((0, 128), np.float32), 4, 10)
+    assert r.ids.shape == (0, 10)
+    rng = np.random.default_rng(2)
+    for scale in (1e-3, 1e3):  # the certification bounds scale with ||q|| and max ||x||
+        X = (rng.standard_normal((4000, 128)) * scale).astype(np.float32)
+        offs = np.linspace(0, 4000, 9).astype(np.int64)
+        C = np.stack([X[offs[i]:offs[i + 1]].mean(0) for i in range(8)]).astype(np.float32)
+        Q = (X[:25] + rng.standard_normal((25, 128)).astype(np.float32) * 0.1 * scale).astype(np.float32)
+        _same(engine.index_from_host(X, offs, C).search(Q, 3, 10), oracle.index_from_host(X, offs, C).search(Q, 3, 10))
+
+
+def test_engine_argument_validation(engine):
+    idx = engine.synthetic_index(engine.desc(2000, 64, 8))
+    q = np.zeros((2, 64), np.float32)
+    for nprobe, k in [(0, 10), (4, 0), (4, 25)]:  # k <= 24 keeps >= 8 candidates of certification margin
+        with pytest.raises(ParseError):
+            idx.search(q, nprobe, k)
+    with pytest.raises(ParseError):
+        engine.synthetic_index(engine.desc(100, 48, 4))  # d must be a multiple of 32
+    with pytest.raises(ParseError):
+        idx.migrate(promote=[0])  # already resident
