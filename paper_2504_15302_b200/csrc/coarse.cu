@@ -705,7 +705,6 @@ cudaError_t launch_coarse(const float* Q, const float* C, const float* cnorm, fl
                           int nlist, int d, cudaStream_t s) {
   dim3 grid((nlist + kBN - 1) / kBN, (B + kBM - 1) / kBM);
   return launch_k(coarse_gemm_kernel, grid, dim3(256), 0, s, Q, C, cnorm, Dc, B, nlist, d);
-  return cudaGetLastError();
 }
 
 bool coarse_small(int B) { return B <= 8; }  // measured cut-over vs the tensor-core tile kernel
@@ -716,15 +715,6 @@ cudaError_t launch_coarse_small(const float* Q, const float* C, const float* cno
   if (B == 0) return cudaSuccess;
   if (d > 4 * 32 * kGemvMaxV) return cudaErrorInvalidValue;
   return launch_k(coarse_gemv_kernel, dim3((nlist + 7) / 8), dim3(kGemvThreads), 0, s, Q, C, cnorm, Dc, B, nlist, d);
-  return cudaGetLastError();
-}
-
-bool pdl_enabled() {
-  static const bool on = [] {
-    const char* v = std::getenv("RD_PDL");
-    return !(v && v[0] == '0');
-  }();
-  return on;
 }
 
 cudaError_t launch_qprep(const float* Q, long long B, int d, float* qnorm, void* qsplit, unsigned* zero2, int* zeroB,
@@ -733,28 +723,17 @@ cudaError_t launch_qprep(const float* Q, long long B, int d, float* qnorm, void*
   const long long blocks = (B * 32 + 255) / 256;
   return launch_k(qprep_kernel, dim3((unsigned)(blocks < 148 * 8 ? blocks : 148 * 8)), dim3(256), 0, s, Q, B, d, qnorm,
                   reinterpret_cast<__nv_bfloat16*>(qsplit), zero2, zeroB);
-  return cudaGetLastError();
 }
 
 cudaError_t launch_select(const SelectParams& p, bool stage, cudaStream_t s) {
   if (p.nprobe + kCoarseExtra > kSelMaxCand) return cudaErrorInvalidValue;
   const size_t keys = sizeof(uint32_t) * (size_t)((p.nlist + 3) & ~3);
   const size_t qd = sizeof(double) * (size_t)p.d;
-  const size_t smem =
-      stage ? keys + qd + sizeof(float) * ((size_t)p.d + 32 * (size_t)(p.d + kStagePad)) : keys + qd;
-  if (stage && smem > 200 * 1024) stage = false;  // very large nlist: the direct-load variant
-  static size_t attr[2] = {0, 0};
-  if (smem > attr[stage]) {  // dynamic + static may exceed the 48 KiB default even below it
-    cudaError_t e = cudaFuncSetAttribute(stage ? coarse_select_kernel<true> : coarse_select_kernel<false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr[stage] = smem;
-  }
-  if (stage)
-    return launch_k(coarse_select_kernel<true>, dim3(p.B), dim3(kSelThreads), smem, s, p);
-  else
-    return launch_k(coarse_select_kernel<false>, dim3(p.B), dim3(kSelThreads), smem, s, p);
-  return cudaGetLastError();
+  const size_t staged = keys + qd + sizeof(float) * ((size_t)p.d + 32 * (size_t)(p.d + kStagePad));
+  if (stage && staged <= 200 * 1024)
+    return launch_k(coarse_select_kernel<true>, dim3(p.B), dim3(kSelThreads), staged, s, p);
+  // large batches (enough CTAs to hide latency) or very large nlist: the direct-load variant
+  return launch_k(coarse_select_kernel<false>, dim3(p.B), dim3(kSelThreads), keys + qd, s, p);
 }
 
 }  // namespace rd

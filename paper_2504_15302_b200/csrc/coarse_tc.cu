@@ -138,16 +138,8 @@ cudaError_t launch_coarse_tc(const CUtensorMap& qmap, const CUtensorMap& cmap, c
                              int nlist, int d, cudaStream_t s) {
   if (B == 0) return cudaSuccess;
   if (d % 64 != 0) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(coarse_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)coarse_tc_smem_bytes());
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
   dim3 grid((nlist + kNC - 1) / kNC, (B + kM - 1) / kM);
   return launch_k(coarse_tc_kernel, grid, dim3(kThreadsC), coarse_tc_smem_bytes(), s, qmap, cmap, cnorm, Dc, B, nlist, d);
-  return cudaGetLastError();
 }
 
 }  // namespace rd

@@ -12,8 +12,11 @@ namespace rd {
 // its predecessor in the stream drains; the kernel's RD_PDL_PROLOGUE waits for the predecessor's
 // results. RD_PDL=0 in the environment launches them plainly (A/B).
 bool pdl_enabled();
+cudaError_t ensure_smem(const void* kern, size_t smem);  // per (device, kernel) dynamic smem limit
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  const cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), smem);
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -123,7 +126,7 @@ struct SelectParams {
   unsigned* probe_fail;    // device scalar
   int B, nlist, nprobe, d;
   float cmax;              // max ||c||
-  // fused seeding of the scan's pruning threshold (see SeedParams); qthr == nullptr skips it
+  // fused seeding of the scan's pruning threshold (coarse.cu, seed phase); qthr == nullptr skips it
   const long long* list_off;
   const long long* res_row0;
   const float* arena;
@@ -179,23 +182,6 @@ struct MergeParams {
 // stage: the 32 rerank rows go through shared memory (latency-bound small batches)
 cudaError_t launch_merge(const MergeParams& p, bool stage, cudaStream_t s);
 
-// Seeds each query's pruning threshold before the scan: 32 rows of its nearest resident
-// probed list, exact distances, threshold = max + 2*eps (a valid upper bound on the final
-// 32nd-best approximate distance, so certification is preserved).
-struct SeedParams {
-  const int* probes;             // B x nprobe, ascending by centroid distance
-  int nprobe;
-  const float* queries;
-  const float* qnorm;
-  const long long* list_off;
-  const long long* res_row0;     // -1 = offloaded (not used for seeding)
-  const float* arena;            // resident arena
-  int d;
-  float xmax;
-  int* qthr;                     // out: f2ord(threshold) or "none"
-  int B;
-};
-cudaError_t launch_seed(const SeedParams& p, cudaStream_t s);
 
 // Exact fallback for uncertified queries: every row of every probed list is compared
 // with the canonical exact distance and ordered by (distance, id).

@@ -170,46 +170,6 @@ __global__ void shard_merge_kernel(int G, long long B, int k, const long long* _
   }
 }
 
-// one CTA (256 threads = 32 groups of 8 lanes) per query
-__global__ void __launch_bounds__(256) seed_kernel(const SeedParams p) {
-  __shared__ float red[8];
-  __shared__ int lsel;
-  const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) {
-    lsel = -1;
-    for (int i = 0; i < p.nprobe; ++i) {
-      const int l = p.probes[(size_t)b * p.nprobe + i];
-      if (l < 0) break;
-      if (p.res_row0[l] >= 0 && p.list_off[l + 1] - p.list_off[l] >= 32) {
-        lsel = l;
-        break;
-      }
-    }
-  }
-  __syncthreads();
-  const int l = lsel;
-  if (l < 0) {
-    if (tid == 0) p.qthr[b] = 0x7f7f7f7f;
-    return;
-  }
-  const int g = tid >> 3;  // row 0..31 of the list
-  const float* x = p.arena + (size_t)(p.res_row0[l] + g) * p.d;
-  const float e = exact_l2_group8(p.queries + (size_t)b * p.d, x, p.d, tid & 7);
-  float m = e;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if (lane == 0) red[warp] = m;
-  __syncthreads();
-  if (tid == 0) {
-    float mx = red[0];
-    for (int i = 1; i < 8; ++i) mx = fmaxf(mx, red[i]);
-    const float qn = p.qnorm[b];
-    const float u = 5.9604645e-8f;
-    const float eps = 2.f * ((p.d / 2 + 8) * u * 2.f * sqrtf(qn) * p.xmax + 8.f * u * (qn + p.xmax * p.xmax)) + 1e-30f;
-    p.qthr[b] = f2ord(mx + 2.f * eps);
-  }
-}
-
 // Exact fallback in one launch. Persistent: work item w -> (failed query w / nprobe, probe
 // w % nprobe), the exact top-32 of that list; the last CTA to finish merges each failed query's
 // nprobe partials and overwrites its result row, then re-arms the completion counter. With no
@@ -285,33 +245,17 @@ __global__ void __launch_bounds__(256) fallback_kernel(const FallbackParams p) {
 
 }  // namespace
 
-cudaError_t launch_seed(const SeedParams& p, cudaStream_t s) {
-  if (p.B == 0) return cudaSuccess;
-  seed_kernel<<<p.B, 256, 0, s>>>(p);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_fallback(const FallbackParams& p, int num_sms, cudaStream_t s) {
   return launch_k(fallback_kernel, dim3(num_sms), dim3(256), 0, s, p);
-  return cudaGetLastError();
 }
 
 cudaError_t launch_merge(const MergeParams& p, bool stage, cudaStream_t s) {
   if (p.B == 0) return cudaSuccess;
   if (stage) {
     const size_t smem = sizeof(float) * ((size_t)p.d + kTopK * (size_t)(p.d + kStagePad));
-    static size_t attr = 0;
-    if (smem > attr) {  // dynamic + static may exceed the 48 KiB default even below it
-      cudaError_t e = cudaFuncSetAttribute(merge_rerank_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return e;
-      attr = smem;
-    }
     return launch_k(merge_rerank_kernel<true>, dim3(p.B), dim3(256), smem, s, p);
-  } else {
-    return launch_k(merge_rerank_kernel<false>, dim3(p.B), dim3(256), 0, s, p);
   }
-  return cudaGetLastError();
+  return launch_k(merge_rerank_kernel<false>, dim3(p.B), dim3(256), 0, s, p);
 }
 
 cudaError_t launch_shard_merge(int G, long long B, int k, const long long* ids, const float* dists,

@@ -487,14 +487,7 @@ cudaError_t launch_plan(const PlanParams& p, cudaStream_t s) {
   if (plan_small_ok(p.B, p.nprobe)) return launch_k(plan_small_kernel, dim3(1), dim3(kSmallPlanThreads), 0, s, p);
   if (plan_fused_ok(p.B, p.nlist)) {
     const int smem = p.nlist * (p.W + 1) * (int)sizeof(unsigned);
-    static int attr = 0;
-    if (smem > attr) {  // dynamic + static may exceed the 48 KiB default even below it
-      cudaError_t e = cudaFuncSetAttribute(plan_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e != cudaSuccess) return e;
-      attr = smem;
-    }
     return launch_k(plan_fused_kernel, dim3(1), dim3(kPlanThreads), smem, s, p);
-    return cudaGetLastError();
   }
   cudaError_t e = cudaMemsetAsync(p.bitmap, 0, sizeof(unsigned) * (size_t)p.nlist * p.W, s);
   if (e != cudaSuccess) return e;

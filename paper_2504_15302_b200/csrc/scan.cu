@@ -278,15 +278,7 @@ size_t scan_smem_bytes(int d) {
 cudaError_t launch_scan(const CUtensorMap& map256, const CUtensorMap& map32, const ScanParams& p,
                         int grid, cudaStream_t s) {
   const size_t smem = scan_smem_bytes(p.d);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(ivf_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
   return launch_k(ivf_scan_kernel, dim3(grid), dim3(kScanThreads), smem, s, map256, map32, p);
-  return cudaGetLastError();
 }
 
 }  // namespace rd

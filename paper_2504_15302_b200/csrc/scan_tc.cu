@@ -510,21 +510,11 @@ size_t scan_tc_smem_bytes(int d) {
 cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, const CUtensorMap& qmap,
                            const TcScanParams& p, int grid, cudaStream_t s, bool presplit) {
   if (p.d % 64 != 0) return cudaErrorInvalidValue;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(ivf_scan_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(ivf_scan_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
   const size_t smem = scan_tc_smem_bytes(p.d);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   if (presplit)
     return launch_k(ivf_scan_tc_kernel<true>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
-  else
-    return launch_k(ivf_scan_tc_kernel<false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
-  return cudaGetLastError();
+  return launch_k(ivf_scan_tc_kernel<false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
 }
 
 cudaError_t launch_qsplit(const float* Q, void* out, long long B, int d, cudaStream_t s) {
