@@ -237,6 +237,7 @@ struct rd_index {
   bool dbg_ts = std::getenv("RD_DEBUG_TS") != nullptr;  // profiling only: select checkpoints to stderr
   int stage_max_b = -1;  // batches up to this size stage exact-distance rows in smem (-1: 2 x SMs)
   int tiles_per_sm = 8;  // scan tiles per SM the planner aims for (RD_TILES_PER_SM)
+  long long seed_max_b = 1LL << 40;  // batches up to this size seed the scan's pruning threshold (RD_SEED_MAX_B)
   bool no_inner_events = std::getenv("RD_NO_INNER_EVENTS") != nullptr;  // A/B: no per-stage timing events
   // the tensor-core scan stages 64-dim bf16 query slices of up to 32 queries in shared memory:
   // d % 64 == 0 and d <= 896 (beyond, its B operand does not fit next to the x ring); else FFMA
@@ -355,6 +356,7 @@ struct rd_index {
     if (const char* v = std::getenv("RD_DEBUG_SKIP")) debug_skip = std::atoi(v);
     if (const char* v = std::getenv("RD_STAGE_MAX_B")) stage_max_b = std::atoi(v);
     if (const char* v = std::getenv("RD_TILES_PER_SM")) tiles_per_sm = std::max(1, std::atoi(v));
+    if (const char* v = std::getenv("RD_SEED_MAX_B")) seed_max_b = std::atoll(v);
     // the tensor-core scan stages bf16 query slices of 64 dims
   }
 
@@ -1146,8 +1148,10 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     CK(rd::launch_coarse(d_q, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, s));
   }
   w.qthr.ensure(B);
+  const bool seed = B <= h->seed_max_b;
+  if (!seed) CK(cudaMemsetAsync(w.qthr.p, 0x7f, sizeof(int) * B, s));  // no threshold: huge
   rd::SelectParams sp{w.Dc.p, d_q, w.qnorm.p, h->centroids.p, w.probes.p, w.fails(), (int)B, nl, nprobe, d, h->cmax,
-                      h->d_list_off.p, h->d_res_row0.p, h->arena.p, h->xmax, w.qthr.p, 0};
+                      h->d_list_off.p, h->d_res_row0.p, h->arena.p, h->xmax, seed ? w.qthr.p : nullptr, 0};
   h->traced("select", s, sp.dbg, [&] { CK(rd::launch_select(sp, h->stage_rows(B), s)); });
   launches += 3;
   rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
