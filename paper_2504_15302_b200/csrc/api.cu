@@ -1326,9 +1326,10 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   w.fb_dist.ensure((size_t)B * nprobe * rd::kTopK);
   w.fb_id.ensure((size_t)B * nprobe * rd::kTopK);
   rd::MergeParams mp{w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d_q, w.qnorm.p, h->d_list_off.p,
-                     h->d_list_base.p, h->d_ids.p, h->d_row_list.p, nl, d, k, h->xmax, d_ids, d_dists,
+                     h->d_list_base.p, h->d_ids.p, h->d_row_list.p, h->arena.p,
+                     h->arena.p + (size_t)h->n_resident * d, nl, d, k, h->xmax, d_ids, d_dists,
                      w.fails() + 1, w.fail_list.p, (int)B};
-  CK(rd::launch_merge(mp, h->stage_rows(B), s));
+  h->traced("merge", s, mp.dbg, [&] { CK(rd::launch_merge(mp, h->stage_rows(B), s)); });
   rd::FallbackParams fp{w.fail_list.p, w.fails() + 1, w.probes.p, nprobe, d_q, h->d_list_off.p, h->d_list_base.p,
                         h->d_ids.p, nl, d, k, w.fb_dist.p, w.fb_id.p, d_ids, d_dists, w.fb_ctr.p};
   CK(rd::launch_fallback(fp, h->num_sms, s));

@@ -171,6 +171,8 @@ struct MergeParams {
   const float* const* list_base;   // nlist: device-visible pointer to the list's first row
   const long long* ids;            // n (global row order)
   const int* row_list;             // n: list of each global row
+  const float* arena_lo;           // resident arena [lo, hi): rows there are bulk-copied (TMA), others
+  const float* arena_hi;           // (mapped host memory of offloaded lists) are loaded by the threads
   int nlist, d, k;
   float xmax;
   long long* out_ids;              // B x k
@@ -178,6 +180,7 @@ struct MergeParams {
   unsigned* margin_fail;            // device scalar: number of uncertified queries
   int* fail_list;                  // B: ids of uncertified queries (exact fallback work list)
   int B;
+  unsigned long long* dbg = nullptr;  // RD_DEBUG_TS: globaltimer checkpoints of CTA 0
 };
 // stage: the 32 rerank rows go through shared memory (latency-bound small batches)
 cudaError_t launch_merge(const MergeParams& p, bool stage, cudaStream_t s);

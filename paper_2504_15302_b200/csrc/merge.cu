@@ -30,8 +30,16 @@ __global__ void __launch_bounds__(256) merge_rerank_kernel(const MergeParams p) 
   __shared__ long long ex_id[kTopK];
   __shared__ const float* rowp[kTopK];
   __shared__ float tau_s;
+  __shared__ unsigned host_rows;  // kStage: candidate rows outside the device arena
+  __shared__ __align__(8) uint64_t bar;
+  RD_TS(0);
+  if (kStage && threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
   const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cnt = min(p.part_count[b], p.part_cap);
+  if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0) p.dbg[15] = (unsigned long long)cnt;
   const float* q = p.queries + (size_t)b * p.d;
   if constexpr (kStage) {
     for (int i = tid; i < (p.d >> 2); i += 256) reinterpret_cast<float4*>(dyn)[i] = reinterpret_cast<const float4*>(q)[i];
@@ -70,6 +78,7 @@ __global__ void __launch_bounds__(256) merge_rerank_kernel(const MergeParams p) 
   sd[warp][lane] = ld;
   sk[warp][lane] = lk;
   __syncthreads();
+  RD_TS(1);
   if (warp == 0) {
     for (int w = 1; w < 8; ++w) {
       const float v = sd[w][kTopK - 1 - lane];
@@ -92,19 +101,38 @@ __global__ void __launch_bounds__(256) merge_rerank_kernel(const MergeParams p) 
     rowp[lane] = xp;
     ex_id[lane] = id;
     if (lane == 31) tau_s = ld;
+    if constexpr (kStage) {  // device rows: one bulk (TMA) copy each, all in flight at once
+      float* st = dyn + p.d;
+      const bool dev = xp && xp >= p.arena_lo && xp < p.arena_hi;
+      const unsigned dm = __ballot_sync(0xffffffffu, dev);
+      if (lane == 0) mbar_arrive_expect_tx(&bar, (uint32_t)__popc(dm) * (uint32_t)p.d * 4u);
+      const unsigned hm = __ballot_sync(0xffffffffu, xp && !dev);
+      if (lane == 0) host_rows = hm;
+      __syncwarp();
+      if (dev) bulk_g2s(st + lane * (p.d + kStagePad), xp, (uint32_t)p.d * 4u, &bar);
+    }
   }
   __syncthreads();
 
+  RD_TS(2);
   // exact rerank: thread (c = tid/8, j = tid%8)
   const int c = tid >> 3, j8 = tid & 7;
   const float* xp = rowp[c];
   float e;
   if constexpr (kStage) {
     float* st = dyn + p.d;
-    int nrows = 0;  // candidates are ascending, so the valid ones are a prefix
-    while (nrows < kTopK && rowp[nrows]) ++nrows;
-    stage_rows_ld<256>(st, nrows, p.d, [&](int r) { return rowp[r]; });
+    const unsigned hm = host_rows;
+    if (hm) {  // rows of offloaded lists (mapped host memory): ordinary loads by every thread
+      const int v4 = p.d >> 2, ds = p.d + kStagePad;
+      for (int i = tid; i < kTopK * v4; i += 256) {
+        const int r = i / v4, cc = i - r * v4;
+        if ((hm >> r) & 1u)
+          *reinterpret_cast<float4*>(st + r * ds + 4 * cc) = *reinterpret_cast<const float4*>(rowp[r] + 4 * cc);
+      }
+    }
+    mbar_wait(&bar, 0);
     __syncthreads();
+    RD_TS(3);
     e = exact_l2_group8_impl<false>(dyn, st + c * (p.d + kStagePad), xp ? p.d : 0, j8);
   } else {
     // a padded slot runs zero terms so the warp stays converged for the shuffles
@@ -113,6 +141,7 @@ __global__ void __launch_bounds__(256) merge_rerank_kernel(const MergeParams p) 
   if (!xp) e = kInf;
   if (j8 == 0) ex_d[c] = e;
   __syncthreads();
+  RD_TS(4);
   if (warp == 0) {
     float dd = ex_d[lane];
     long long kk = ex_id[lane];
