@@ -60,6 +60,7 @@ extern "C" {
 #define RD_STREAM_VECTOR_NOISE 0x1003u
 #define RD_STREAM_QUERY_PICK 0x1004u
 #define RD_STREAM_QUERY_NOISE 0x1005u
+#define RD_STREAM_TRAIN_INIT 0x1006u
 #define RD_DEFAULT_SEED 250415302ull
 
 typedef struct rd_index rd_index; /* opaque, library-owned */
@@ -149,6 +150,22 @@ int rd_index_place(rd_index* h, const rd_placement* placement);
 int rd_index_info_get(const rd_index* h, rd_index_info* out);
 /* Copies list_offsets (nlist+1) and optionally ids (n) / resident mask (nlist) to host. */
 int rd_index_layout(const rd_index* h, int64_t* list_offsets, int64_t* ids, uint8_t* resident_mask);
+/* Copies the nlist x d centroids to host. */
+int rd_index_centroids(const rd_index* h, float* out);
+
+/* IVF training from raw vectors (index build): Lloyd's k-means with exact,
+ * deterministic arithmetic, so both libraries produce the same centroids and lists bit for bit:
+ *   init    centroid j = the vector at row r_j, r_0, r_1, ... the first nlist distinct values of
+ *           u(s, i) mod n for i = 0, 1, ... (s = rd_derive_seed(seed, RD_STREAM_TRAIN_INIT));
+ *   assign  every vector to its nearest centroid by (canonical exact distance, centroid id),
+ *           the order rd_probe uses;
+ *   update  centroid = (fp64 sum of its members' components in ascending row order) / count,
+ *           rounded to f32; an empty cluster keeps its centroid;
+ * `iters` rounds of (assign, update), then a final assign; rows are laid out in list order,
+ * ascending row within a list; ids default to the row index. Requires n >= nlist.
+ * The engine assigns with its own coarse path (tensor-core GEMM + certified selection). */
+int rd_index_build(int64_t n, int32_t d, int32_t nlist, const float* vectors, const int64_t* ids,
+                   int32_t iters, uint64_t seed, int32_t device, rd_index** out);
 void rd_index_destroy(rd_index* h);
 
 /* ---- between-batch list migration ----

@@ -284,6 +284,95 @@ int rd_index_create_synthetic(const rd_synth_desc* s, int32_t device, rd_index**
   return RD_OK;
 }
 
+/* ------------------------------------------------------------------ IVF training (rd_index_build) */
+typedef struct {
+  const float* X;
+  const float* C;
+  int32_t d, nlist;
+  int32_t* assign;
+} assign_ctx;
+
+static void assign_rows(void* p, int64_t b, int64_t e) {
+  const assign_ctx* a = (const assign_ctx*)p;
+  for (int64_t r = b; r < e; ++r) {
+    const float* x = a->X + (size_t)r * a->d;
+    float best = INFINITY;
+    int32_t bj = 0;
+    for (int32_t j = 0; j < a->nlist; ++j) {
+      const float dj = rd_exact_l2(x, a->C + (size_t)j * a->d, a->d);
+      if (dj < best) { /* ties keep the lower id */
+        best = dj;
+        bj = j;
+      }
+    }
+    a->assign[r] = bj;
+  }
+}
+
+int rd_index_build(int64_t n, int32_t d, int32_t nlist, const float* vectors, const int64_t* ids, int32_t iters,
+                   uint64_t seed, int32_t device, rd_index** out) {
+  if (n < 1 || d < 1 || nlist < 1 || n < nlist || iters < 0 || !vectors || !out)
+    return fail(RD_ERR_INVALID, "build: need n >= nlist >= 1, d >= 1, iters >= 0 and vectors");
+  float* C = (float*)malloc(sizeof(float) * (size_t)nlist * d);
+  int32_t* assign = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
+  uint8_t* taken = (uint8_t*)calloc((size_t)n, 1);
+  const uint64_t s = rd_derive_seed(seed, RD_STREAM_TRAIN_INIT);
+  uint64_t i = 0;
+  for (int32_t j = 0; j < nlist;) { /* the first nlist distinct rows of u(s, i) mod n */
+    const int64_t r = (int64_t)(rd_splitmix_at(s, i++) % (uint64_t)n);
+    if (taken[r]) continue;
+    taken[r] = 1;
+    memcpy(C + (size_t)j * d, vectors + (size_t)r * d, sizeof(float) * (size_t)d);
+    ++j;
+  }
+  free(taken);
+  assign_ctx ac = {vectors, C, d, nlist, assign};
+  double* sum = (double*)malloc(sizeof(double) * (size_t)nlist * d);
+  int64_t* cnt = (int64_t*)malloc(sizeof(int64_t) * (size_t)nlist);
+  for (int32_t it = 0; it <= iters; ++it) {
+    parallel_for(n, 256, assign_rows, &ac);
+    if (it == iters) break;
+    memset(sum, 0, sizeof(double) * (size_t)nlist * d);
+    memset(cnt, 0, sizeof(int64_t) * (size_t)nlist);
+    for (int64_t r = 0; r < n; ++r) { /* ascending rows: the canonical summation order */
+      double* sl = sum + (size_t)assign[r] * d;
+      const float* x = vectors + (size_t)r * d;
+      for (int32_t t = 0; t < d; ++t) sl[t] = sl[t] + (double)x[t];
+      cnt[assign[r]]++;
+    }
+    for (int32_t j = 0; j < nlist; ++j)
+      if (cnt[j])
+        for (int32_t t = 0; t < d; ++t) C[(size_t)j * d + t] = (float)(sum[(size_t)j * d + t] / (double)cnt[j]);
+  }
+  free(sum);
+  /* list order, ascending row within a list (counting sort) */
+  int64_t* offs = (int64_t*)calloc((size_t)nlist + 1, sizeof(int64_t));
+  for (int64_t r = 0; r < n; ++r) offs[assign[r] + 1]++;
+  for (int32_t j = 0; j < nlist; ++j) offs[j + 1] += offs[j];
+  memcpy(cnt, offs, sizeof(int64_t) * (size_t)nlist);
+  float* Xl = (float*)malloc(sizeof(float) * (size_t)n * d);
+  int64_t* idl = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+  for (int64_t r = 0; r < n; ++r) {
+    const int64_t pos = cnt[assign[r]]++;
+    memcpy(Xl + (size_t)pos * d, vectors + (size_t)r * d, sizeof(float) * (size_t)d);
+    idl[pos] = ids ? ids[r] : r;
+  }
+  const int rc = rd_index_create_from_host(n, d, nlist, Xl, offs, C, idl, device, out);
+  free(Xl);
+  free(idl);
+  free(offs);
+  free(cnt);
+  free(assign);
+  free(C);
+  return rc;
+}
+
+int rd_index_centroids(const rd_index* h, float* out) {
+  if (!h || !out) return fail(RD_ERR_INVALID, "centroids: null argument");
+  memcpy(out, h->centroids, sizeof(float) * (size_t)h->nlist * h->d);
+  return RD_OK;
+}
+
 int rd_index_create_from_host(int64_t n, int32_t d, int32_t nlist, const float* vectors,
                               const int64_t* list_offsets, const float* centroids,
                               const int64_t* ids, int32_t device, rd_index** out) {

@@ -374,23 +374,33 @@ struct rd_index {
     for (int l = 0; l < nlist; ++l) res_row0[l] = list_off[l];
     n_resident = n;
     upload_residency();
+    prepare_centroids();
     DBuf<float> tmp;
     tmp.alloc(1);
-    CK(launch_row_norms_wrap(centroids.p, nlist, cnorm.p));
-    if (d % 64 == 0) {
-      csplit.alloc((size_t)nlist * d);  // 2 x bf16 per element = one float
-      CK(rd::launch_qsplit(centroids.p, csplit.p, nlist, d, 0));
-      cmap = make_split_map(csplit.p, nlist, d);
-    }
-    CK(rd::launch_max_f32(cnorm.p, nlist, tmp.p, 0));
     float m2 = 0;
-    CK(cudaMemcpy(&m2, tmp.p, sizeof(float), cudaMemcpyDeviceToHost));
-    cmax = std::sqrt(m2) * (1.f + 1e-6f);
     CK(rd::launch_max_f32(xnorm.p, n, tmp.p, 0));
     CK(cudaMemcpy(&m2, tmp.p, sizeof(float), cudaMemcpyDeviceToHost));
     xmax = std::sqrt(m2) * (1.f + 1e-6f);
     CK(cudaDeviceSynchronize());
     build_presplit();
+  }
+
+  // coarse-stage state derived from the centroids: ||c||^2, the bf16 (hi, lo) split and its TMA
+  // map for the tensor-core coarse GEMM, and max ||c|| for the selection's error bound
+  void prepare_centroids() {
+    if (cnorm.n < (size_t)nlist) cnorm.alloc(nlist);
+    CK(launch_row_norms_wrap(centroids.p, nlist, cnorm.p));
+    if (d % 64 == 0) {
+      if (csplit.n < (size_t)nlist * d) csplit.alloc((size_t)nlist * d);  // 2 x bf16 per element = one float
+      CK(rd::launch_qsplit(centroids.p, csplit.p, nlist, d, 0));
+      cmap = make_split_map(csplit.p, nlist, d);
+    }
+    DBuf<float> tmp;
+    tmp.alloc(1);
+    CK(rd::launch_max_f32(cnorm.p, nlist, tmp.p, 0));
+    float m2 = 0;
+    CK(cudaMemcpy(&m2, tmp.p, sizeof(float), cudaMemcpyDeviceToHost));
+    cmax = std::sqrt(m2) * (1.f + 1e-6f);
   }
 
   void build_presplit() {
@@ -643,6 +653,128 @@ int rd_index_create_from_host(int64_t n, int32_t d, int32_t nlist, const float* 
 }
 
 void rd_index_destroy(rd_index* h) { delete h; }
+
+int rd_index_centroids(const rd_index* h, float* out) {
+  return guarded([&] {
+    if (!h || !out) throw_rd(RD_ERR_INVALID, "centroids: null argument");
+    CK(cudaSetDevice(h->device));
+    CK(cudaMemcpy(out, h->centroids.p, sizeof(float) * (size_t)h->nlist * h->d, cudaMemcpyDeviceToHost));
+  });
+}
+
+// ---------------------------------------------------------------- IVF training (N10)
+// Lloyd's k-means, exact and deterministic (include/rd.h, rd_index_build): assignment is the
+// search's own coarse path with nprobe = 1 — tensor-core (or FFMA) distances, certified selection,
+// canonical fp64 distances for ambiguous centroids — over batches of the vectors; the update is
+// train.cu's ordered fp64 mean.
+int rd_index_build(int64_t n, int32_t d, int32_t nlist, const float* vectors, const int64_t* ids, int32_t iters,
+                   uint64_t seed, int32_t device, rd_index** out) {
+  return guarded([&] {
+    if (n < 1 || nlist < 1 || n < nlist || iters < 0 || !vectors || !out)
+      throw_rd(RD_ERR_INVALID, "build: need n >= nlist >= 1, iters >= 0 and vectors");
+    check_dims(d);
+    if (n >= (1LL << 31)) throw_rd(RD_ERR_INVALID, "build: at most 2^31-1 vectors per handle");
+    auto h = new_index(device);
+    h->n = n;
+    h->d = d;
+    h->nlist = nlist;
+    cudaStream_t s = 0;
+    DBuf<float> X;  // input order
+    X.alloc((size_t)n * d);
+    CK(cudaMemcpy(X.p, vectors, sizeof(float) * (size_t)n * d, cudaMemcpyHostToDevice));
+    {  // init: the first nlist distinct rows of u(s, i) mod n
+      const uint64_t si = derive_seed(seed, RD_STREAM_TRAIN_INIT);
+      std::vector<uint8_t> taken((size_t)n, 0);
+      std::vector<int> pick;
+      for (uint64_t i = 0; (int)pick.size() < nlist; ++i) {
+        const long long r = (long long)(rd::splitmix_at(si, i) % (uint64_t)n);
+        if (!taken[r]) {
+          taken[r] = 1;
+          pick.push_back((int)r);
+        }
+      }
+      DBuf<int> dpick;
+      dpick.alloc(nlist);
+      CK(cudaMemcpy(dpick.p, pick.data(), sizeof(int) * nlist, cudaMemcpyHostToDevice));
+      h->centroids.alloc((size_t)nlist * d);
+      CK(rd::launch_gather_rows(X.p, dpick.p, nlist, d, h->centroids.p, s));
+    }
+    DBuf<int> assign, keys_sorted, rows, rows_sorted;
+    DBuf<unsigned> counts;
+    DBuf<long long> seg;
+    DBuf<char> temp;
+    assign.alloc(n);
+    keys_sorted.alloc(n);
+    rows.alloc(n);
+    rows_sorted.alloc(n);
+    counts.alloc(nlist);
+    seg.alloc(nlist + 1);
+    int end_bit = 1;
+    while ((1LL << end_bit) < nlist) ++end_bit;
+    size_t temp_bytes = 0;
+    CK(rd::sort_pairs(nullptr, nullptr, nullptr, nullptr, n, end_bit, nullptr, &temp_bytes, s));
+    temp.alloc(temp_bytes);
+    std::vector<unsigned> hcount(nlist);
+    std::vector<long long> hseg(nlist + 1);
+    auto& w = h->ws;
+    const long long chunk = std::max<long long>(1024, std::min<long long>(65536, (1LL << 28) / nlist));
+    auto assign_all = [&] {
+      h->prepare_centroids();
+      w.qnorm.ensure(chunk);
+      w.qsplit.ensure((size_t)chunk * d);
+      w.Dc.ensure((size_t)chunk * nlist);
+      w.blk.ensure(kStatBytes);
+      for (long long b0 = 0; b0 < n; b0 += chunk) {
+        const int B = (int)std::min(chunk, n - b0);
+        const float* q = X.p + (size_t)b0 * d;
+        CK(rd::launch_qprep(q, B, d, w.qnorm.p, d % 64 == 0 ? w.qsplit.p : nullptr, w.fails(), nullptr, s));
+        if (d % 64 == 0) {
+          const CUtensorMap qmap = make_split_map(w.qsplit.p, B, d);
+          CK(rd::launch_coarse_tc(qmap, h->cmap, h->cnorm.p, w.Dc.p, B, nlist, d, s));
+        } else {
+          CK(rd::launch_coarse(q, h->centroids.p, h->cnorm.p, w.Dc.p, B, nlist, d, s));
+        }
+        rd::SelectParams sp{w.Dc.p, q, w.qnorm.p, h->centroids.p, assign.p + b0, w.fails(), B, nlist, 1, d,
+                            h->cmax, nullptr, nullptr, nullptr, 0.f, nullptr, 0};
+        CK(rd::launch_select(sp, false, s));
+      }
+    };
+    auto group = [&] {  // rows stably sorted by cluster; per-cluster segments
+      CK(rd::launch_iota(rows.p, n, s));
+      CK(rd::sort_pairs(assign.p, keys_sorted.p, rows.p, rows_sorted.p, n, end_bit, temp.p, &temp_bytes, s));
+      CK(rd::launch_histogram(assign.p, n, counts.p, nlist, s));
+      CK(cudaMemcpyAsync(hcount.data(), counts.p, sizeof(unsigned) * nlist, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      hseg[0] = 0;
+      for (int l = 0; l < nlist; ++l) hseg[l + 1] = hseg[l] + hcount[l];
+      CK(cudaMemcpy(seg.p, hseg.data(), sizeof(long long) * (nlist + 1), cudaMemcpyHostToDevice));
+    };
+    for (int it = 0; it < iters; ++it) {
+      assign_all();
+      group();
+      CK(rd::launch_centroid_update(X.p, rows_sorted.p, seg.p, nlist, d, h->centroids.p, s));
+    }
+    assign_all();
+    group();
+    // list-order layout
+    h->list_off = hseg;
+    h->arena.alloc((size_t)n * d);
+    CK(rd::launch_gather_rows(X.p, rows_sorted.p, n, d, h->arena.p, s));
+    DBuf<long long> uids;
+    if (ids) {
+      uids.alloc(n);
+      CK(cudaMemcpy(uids.p, ids, sizeof(long long) * (size_t)n, cudaMemcpyHostToDevice));
+    }
+    h->d_ids.alloc(n);
+    CK(rd::launch_gather_ids(ids ? uids.p : nullptr, rows_sorted.p, n, h->d_ids.p, s));
+    CK(cudaStreamSynchronize(s));
+    X.reset();
+    h->xnorm.alloc(n);
+    CK(rd::launch_row_norms(h->arena.p, n, d, h->xnorm.p, 0));
+    h->finish_layout();
+    *out = h.release();
+  });
+}
 
 // ---------------------------------------------------------------- on-disk index (include/rd_format.h)
 namespace {

@@ -216,6 +216,18 @@ cudaError_t launch_gen_vectors(float* X, const long long* ids, long long n, int 
                                const float* C, uint64_t sa, uint64_t sx, float sigma, cudaStream_t s);
 cudaError_t launch_row_norms(const float* X, long long n, int d, float* out, cudaStream_t s);
 cudaError_t launch_max_f32(const float* v, long long n, float* out, cudaStream_t s);
+// IVF training (train.cu)
+cudaError_t launch_iota(int* v, long long n, cudaStream_t s);
+cudaError_t launch_histogram(const int* keys, long long n, unsigned* counts, int nbins, cudaStream_t s);
+// stable radix sort of (key, value) pairs on bits [0, end_bit); temp == nullptr queries *temp_bytes
+cudaError_t sort_pairs(const int* keys_in, int* keys_out, const int* vals_in, int* vals_out, long long n, int end_bit,
+                       void* temp, size_t* temp_bytes, cudaStream_t s);
+// C[l] = fp64 sum of X[rows[seg[l] .. seg[l+1])] in order / count (empty clusters untouched)
+cudaError_t launch_centroid_update(const float* X, const int* rows, const long long* seg, int nlist, int d, float* C,
+                                   cudaStream_t s);
+cudaError_t launch_gather_rows(const float* src, const int* idx, long long count, int d, float* dst, cudaStream_t s);
+// out[i] = ids ? ids[idx[i]] : idx[i]
+cudaError_t launch_gather_ids(const long long* ids, const int* idx, long long count, long long* out, cudaStream_t s);
 // row_list[r] = l for off[l] <= r < off[l + 1]
 cudaError_t launch_row_list(const long long* off, int nlist, int* row_list, cudaStream_t s);
 

@@ -108,6 +108,9 @@ _SIGS = {
     "rd_index_destroy": (None, [_P]),
     "rd_index_migrate": (C.c_int, [_P, _I32P, C.c_int32, _I32P, C.c_int32, C.c_uint64, C.c_void_p]),
     "rd_index_save": (C.c_int, [_P, C.c_char_p]),
+    "rd_index_centroids": (C.c_int, [_P, _FP]),
+    "rd_index_build": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, _FP, _I64P, C.c_int32, C.c_uint64, C.c_int32,
+                                 C.POINTER(_P)]),
     "rd_index_load": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(_P)]),
     "rd_search": (C.c_int, [_P, _FP, C.c_int64, C.c_int32, C.c_int32, _I64P, _FP, C.POINTER(SearchStats)]),
     "rd_search_device": (C.c_int, [_P, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
@@ -210,6 +213,16 @@ class Library:
         h = C.c_void_p()
         self.check(self.lib.rd_index_create_from_host(n, d, nlist, _fp(vectors), _i64p(list_offsets),
                                                       _fp(centroids), idp, device, C.byref(h)), "create_from_host")
+        return Index(self, h)
+
+    def build_index(self, vectors: np.ndarray, nlist: int, iters: int = 10, seed: int = DEFAULT_SEED,
+                    ids: Optional[np.ndarray] = None, device: int = 0) -> "Index":
+        """IVF training (exact, deterministic k-means) + list-order layout (rd_index_build)."""
+        vectors = np.ascontiguousarray(vectors, dtype=np.float32)
+        n, d = vectors.shape
+        idp = _i64p(np.ascontiguousarray(ids, dtype=np.int64)) if ids is not None else None
+        h = C.c_void_p()
+        self.check(self.lib.rd_index_build(n, d, nlist, _fp(vectors), idp, iters, seed, device, C.byref(h)), "build")
         return Index(self, h)
 
     def load_index(self, path: str, device: int = 0) -> "Index":
@@ -343,6 +356,12 @@ class Index:
                                                        de.ctypes.data_as(_I32P), de.size, hbm_budget_bytes,
                                                        C.cast(C.byref(st), C.c_void_p)), "migrate")
         return {f: getattr(st, f) for f, _ in st._fields_}
+
+    def centroids(self) -> np.ndarray:
+        inf = self.info()
+        out = np.empty((inf["nlist"], inf["d"]), dtype=np.float32)
+        self._lib.check(self._lib.lib.rd_index_centroids(self._h, _fp(out)), "centroids")
+        return out
 
     def save(self, path: str) -> None:
         """Writes the index in the on-disk format (include/rd_format.h)."""
