@@ -1240,7 +1240,6 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   if (nprobe < 1 || k < 1) throw_rd(RD_ERR_INVALID, "search: nprobe >= 1 and k >= 1 required");
   if (k > rd::kMaxK) throw_rd(RD_ERR_INVALID, "search: k <= %d supported, got %d", rd::kMaxK, k);
   if (std::min(nprobe, h->nlist) + rd::kCoarseExtra > 512) throw_rd(RD_ERR_INVALID, "search: nprobe <= 480 supported");
-  if (B >= (1LL << 24)) throw_rd(RD_ERR_INVALID, "search: batch too large (max 2^24-1 per call)");
   CK(cudaSetDevice(h->device));
   auto& w = h->ws;
   const int nl = h->nlist, d = h->d;
@@ -1506,22 +1505,63 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
 
 }  // namespace
 
+namespace {
+// Largest batch searched in one pass: bounds the B x nlist coarse-distance workspace (2 GiB).
+long long search_chunk(const rd_index* h) {
+  return std::max<long long>(1024, std::min<long long>(65536, (1LL << 31) / (4LL * h->nlist)));
+}
+void add_stats(rd_search_stats* acc, const rd_search_stats& s) {  // counters summed over chunks
+  acc->bytes_algorithmic += s.bytes_algorithmic;
+  acc->bytes_lists_resident += s.bytes_lists_resident;
+  acc->h2d_list_bytes += s.h2d_list_bytes;
+  acc->lists_probed += s.lists_probed;
+  acc->tiles += s.tiles;
+  acc->kernel_launches += s.kernel_launches;
+  acc->scan_ms += s.scan_ms;
+  acc->coarse_ms += s.coarse_ms;
+  acc->offload_ms += s.offload_ms;
+  acc->margin_failures += s.margin_failures;
+  acc->probe_failures += s.probe_failures;
+}
+}  // namespace
+
 int rd_search_device(rd_index* h, const float* d_q, int64_t B, int32_t nprobe, int32_t k, int64_t* d_ids,
                      float* d_dists, void* stream, int32_t sync, rd_search_stats* st) {
   return guarded([&] {
     if (!h || B < 0 || (B > 0 && (!d_q || !d_ids || !d_dists))) throw_rd(RD_ERR_INVALID, "search: invalid arguments");
-    if (B == 0) {
-      if (st) std::memset(st, 0, sizeof *st);
-      return;
-    }
+    if (st) std::memset(st, 0, sizeof *st);
+    if (B == 0) return;
     const auto t0 = std::chrono::steady_clock::now();
-    do_search(h, d_q, B, nprobe, k, reinterpret_cast<long long*>(d_ids), d_dists, (cudaStream_t)stream, sync != 0, st);
+    const long long chunk = search_chunk(h);
+    for (long long b0 = 0; b0 < B; b0 += chunk) {  // very large batches run as consecutive passes
+      const long long nb = std::min<long long>(chunk, B - b0);
+      rd_search_stats part{};
+      do_search(h, d_q + (size_t)b0 * h->d, nb, nprobe, k, reinterpret_cast<long long*>(d_ids) + (size_t)b0 * k,
+                d_dists + (size_t)b0 * k, (cudaStream_t)stream, sync != 0, st ? &part : nullptr);
+      if (st) add_stats(st, part);
+    }
     if (st) st->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   });
 }
 
 int rd_search(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32_t k, int64_t* out_ids,
               float* out_dists, rd_search_stats* st) {
+  if (h && B > search_chunk(h) && queries && out_ids && out_dists && h->d > 0 && k > 0) {
+    // very large batches: consecutive passes of the one-pass path below
+    const auto t0 = std::chrono::steady_clock::now();
+    rd_search_stats acc{};
+    const long long chunk = search_chunk(h);
+    for (long long b0 = 0; b0 < B; b0 += chunk) {
+      rd_search_stats part{};
+      const int rc = rd_search(h, queries + (size_t)b0 * h->d, std::min<long long>(chunk, B - b0), nprobe, k,
+                               out_ids + (size_t)b0 * k, out_dists + (size_t)b0 * k, &part);
+      if (rc != RD_OK) return rc;
+      add_stats(&acc, part);
+    }
+    acc.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (st) *st = acc;
+    return RD_OK;
+  }
   return guarded([&] {
     if (!h || B < 0 || (B > 0 && (!queries || !out_ids || !out_dists)))
       throw_rd(RD_ERR_INVALID, "search: invalid arguments");

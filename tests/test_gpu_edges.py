@@ -72,3 +72,12 @@ def test_engine_argument_validation(engine):
         engine.synthetic_index(engine.desc(100, 48, 4))  # d must be a multiple of 32
     with pytest.raises(ParseError):
         idx.migrate(promote=[0])  # already resident
+
+
+def test_batch_larger_than_one_pass(engine, oracle):
+    # 70000 queries > the one-pass limit (65536 at this nlist): consecutive passes, same results
+    desc = engine.desc(5000, 32, 64)
+    q, _ = engine.synth_queries(desc, 0, 70000)
+    e = engine.synthetic_index(desc).search(q, 2, 5)
+    o = oracle.synthetic_index(desc).search(q, 2, 5)
+    _same(e, o)
