@@ -81,3 +81,21 @@ def test_batch_larger_than_one_pass(engine, oracle):
     e = engine.synthetic_index(desc).search(q, 2, 5)
     o = oracle.synthetic_index(desc).search(q, 2, 5)
     _same(e, o)
+
+
+@pytest.mark.parametrize("nprobe", [1, 5, 17, 40])
+def test_probe_set_boundary_ties(engine, oracle, nprobe):
+    # binary centroids and queries: whole groups of centroids at exactly the same distance, so the
+    # nprobe boundary cuts through ties that only the list id decides (the set-mode certification
+    # must send them to the exact path)
+    rng = np.random.default_rng(nprobe)
+    d, nlist = 32, 64
+    C = rng.integers(0, 2, size=(nlist, d)).astype(np.float32)
+    lens = rng.integers(0, 40, size=nlist)
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    X = rng.integers(0, 2, size=(int(lens.sum()), d)).astype(np.float32)
+    Q = rng.integers(0, 2, size=(24, d)).astype(np.float32)
+    e = engine.index_from_host(X, offs, C)
+    o = oracle.index_from_host(X, offs, C)
+    np.testing.assert_array_equal(e.probe(Q, nprobe), o.probe(Q, nprobe))
+    _same(e.search(Q, nprobe, 10), o.search(Q, nprobe, 10))
