@@ -1,0 +1,508 @@
+// host.cuh — host-side core of the B200 retrieval engine behind include/rd.h: error model,
+// device / pinned buffers, TMA tensor maps, and the index object (index.cu: lifecycle,
+// placement, migration, files, training; search.cu: the search itself).
+//
+// Owns the index in HBM (list-order arena, norms, ids, centroids), the pinned
+// host arena of offloaded lists, the H2D staging ring, per-search workspaces,
+// streams and events, and orchestrates one search:
+//
+//   qnorm -> N1 coarse GEMM -> N2 select+exact refine -> N3 plan
+//     -> N4 resident scan (persistent, main stream)
+//     || N9 offloaded lists: cudaMemcpyAsync pinned->staging on a copy stream,
+//        event-gated scans of staged slots on a side stream
+//   -> N6/N7 merge + exact rerank -> results
+//
+// Reference seam: retrieval_time(P, db) (cost_model.cpp:15-21), called by the
+// retrieval worker (simulator.cpp:359,560). Error model: ragsim exit codes
+// (tools/main.cpp:30) with the message in rd_last_error().
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <functional>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/rd.h"
+#include "../../include/rd_format.h"
+#include "ivf_kernels.cuh"
+#include "rd_device.cuh"
+
+// message of the last failure on this thread (rd_last_error), defined in index.cu
+extern thread_local std::string g_err;
+
+namespace {
+
+struct RdError : std::runtime_error {
+  int code;
+  RdError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void throw_rd(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  throw RdError(code, buf);
+}
+
+#define CK(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess)                                                                      \
+      throw_rd(RD_ERR_RUNTIME, "%s failed: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, \
+               __LINE__);                                                                       \
+  } while (0)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return RD_OK;
+  } catch (const RdError& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return RD_ERR_RUNTIME;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return RD_ERR_RUNTIME;
+  }
+}
+
+// ------------------------------------------------------------------ device buffers
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    reset();
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) {
+      p = nullptr;
+      throw_rd(RD_ERR_RUNTIME, "cudaMalloc(%zu bytes) failed: %s", count * sizeof(T), cudaGetErrorString(e));
+    }
+    n = count;
+  }
+  void ensure(size_t count) {
+    if (count > n) alloc(std::max(count, n + n / 2));
+  }
+};
+
+template <class T>
+struct HBuf {  // pinned, mapped host memory
+  T* p = nullptr;
+  size_t n = 0;
+  HBuf() = default;
+  HBuf(const HBuf&) = delete;
+  HBuf& operator=(const HBuf&) = delete;
+  ~HBuf() { reset(); }
+  void reset() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    reset();
+    if (count == 0) count = 1;
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&p), count * sizeof(T),
+                                  cudaHostAllocPortable | cudaHostAllocMapped);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      throw_rd(RD_ERR_RUNTIME, "cudaHostAlloc(%zu bytes) failed: %s", count * sizeof(T), cudaGetErrorString(e));
+    }
+    n = count;
+  }
+  void ensure(size_t count) {
+    if (count > n) alloc(std::max(count, n + n / 2));
+  }
+};
+
+// ------------------------------------------------------------------ tensor maps
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !ptr) throw_rd(RD_ERR_RUNTIME, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+// 3D bf16 map over a [rows][2][d] (hi, lo) split buffer, box {64 dims, 1 part, 128 rows}, 128B swizzle.
+CUtensorMap make_split_map(const void* base, long long rows, int d, int box_rows = 128) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof m);
+  if (rows < 1) rows = 1;
+  cuuint64_t dims[3] = {(cuuint64_t)d, 2, (cuuint64_t)rows};
+  cuuint64_t strides[2] = {(cuuint64_t)d * 2, (cuuint64_t)d * 4};
+  cuuint32_t box[3] = {64, 1, (cuuint32_t)box_rows};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw_rd(RD_ERR_RUNTIME, "cuTensorMapEncodeTiled (split) failed (%d)", (int)r);
+  return m;
+}
+
+// 2D bf16 map over the [rows][2][d] split buffer viewed as [2*rows x d], box {64, 1} (gather4 source).
+CUtensorMap make_gather_map(const void* base, long long rows, int d) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof m);
+  if (rows < 1) rows = 1;
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)(2 * rows)};
+  cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+  cuuint32_t box[2] = {64, 1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw_rd(RD_ERR_RUNTIME, "cuTensorMapEncodeTiled (gather) failed (%d)", (int)r);
+  return m;
+}
+
+// 2D fp32 map over rows x d, box [32 dims x box_rows], 128B swizzle.
+CUtensorMap make_row_map(const float* base, long long rows, int d, int box_rows) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof m);
+  if (rows < 1) rows = 1;
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)d * sizeof(float)};
+  cuuint32_t box[2] = {(cuuint32_t)rd::kScanKSlice, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw_rd(RD_ERR_RUNTIME, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return m;
+}
+
+// ------------------------------------------------------------------ host arithmetic
+inline uint64_t derive_seed(uint64_t master, uint64_t stream) {
+  return rd::splitmix_at(master ^ (stream * 0xd1b54a32d192ed03ull), 1);
+}
+
+void parallel_for(long long n, const std::function<void(long long, long long)>& fn) {
+  unsigned T = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  if (n < 65536 || T == 1) {
+    fn(0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const long long chunk = (n + T - 1) / T;
+  for (unsigned i = 0; i < T; ++i) {
+    const long long b = i * chunk, e = std::min(n, b + chunk);
+    if (b < e) th.emplace_back(fn, b, e);
+  }
+  for (auto& t : th) t.join();
+}
+
+}  // namespace
+
+// ====================================================================== the index
+constexpr size_t kStatBytes = 64;  // per-search counter block (see rd_index::Ws::blk)
+
+struct rd_index {
+  int device = 0;
+  int num_sms = 148;
+  int tc_min_q = rd::kTcMinQ;
+  int debug_skip = 0;  // profiling only
+  bool dbg_ts = std::getenv("RD_DEBUG_TS") != nullptr;  // profiling only: select checkpoints to stderr
+  int stage_max_b = -1;  // batches up to this size stage exact-distance rows in smem (-1: 2 x SMs)
+  int tiles_per_sm = 8;  // scan tiles per SM the planner aims for (RD_TILES_PER_SM)
+  long long seed_max_b = 1LL << 40;  // batches up to this size seed the scan's pruning threshold (RD_SEED_MAX_B)
+  bool no_inner_events = std::getenv("RD_NO_INNER_EVENTS") != nullptr;  // A/B: no per-stage timing events
+  // the tensor-core scan stages 64-dim bf16 query slices of up to 32 queries in shared memory:
+  // d % 64 == 0 and d <= 896 (beyond, its B operand does not fit next to the x ring); else FFMA
+  bool tc_scan() const { return d % 64 == 0 && rd::scan_tc_smem_bytes(d) <= 227 * 1024; }
+  bool stage_rows(long long B) const { return B <= (stage_max_b >= 0 ? stage_max_b : 2LL * num_sms); }
+  long long n = 0;
+  int d = 0, nlist = 0;
+  std::vector<long long> list_off;  // host copy, nlist + 1
+  long long max_len = 0;
+  float cmax = 0.f, xmax = 0.f;
+
+  DBuf<float> centroids, cnorm, xnorm, arena;
+  DBuf<float> csplit;  // nlist x 2 x d bf16 (c1, c2) for the tensor-core coarse GEMM
+  CUtensorMap cmap{};
+  // pre-split bf16 (x1, x2) copy of the resident arena for the conversion-free tensor-core scan;
+  // kept only while every list is resident and device memory allows (RD_PRESPLIT=0 disables)
+  DBuf<float> xsplit;
+  CUtensorMap xmap128{}, xmap32{};
+  bool presplit = false;
+  bool budgeted = false;  // last placement had an HBM byte budget
+  DBuf<long long> d_list_off, d_ids, d_res_row0;
+  DBuf<int> d_row_list;  // list of each global row (merge: row -> list without a search)
+  DBuf<const float*> d_list_base;
+  std::vector<uint8_t> resident;      // host mask
+  std::vector<long long> res_row0;    // host: row in arena or -1
+  std::vector<long long> host_row0;   // host: row in host arena or -1
+  long long n_resident = 0;
+  HBuf<float> host_arena;
+  long long host_used = 0;            // rows of host_arena holding list copies (write-once per list)
+  CUtensorMap map256{}, map128{}, map32{};
+
+  // staging ring for offloaded lists
+  int slots = 0;
+  long long slot_rows = 0;
+  DBuf<float> staging;
+  CUtensorMap smap256{}, smap128{}, smap32{};
+
+  // per-search workspace
+  struct Ws {
+    DBuf<float> qnorm, Dc, q, qsplit;
+    DBuf<int> probes, list_nq, list_qoff, list_ntile, list_toff, list_q, part_count, part_row, off_meta;
+    DBuf<unsigned> bitmap, fb_ctr;
+    DBuf<rd::ScanTile> tiles, ff_tiles, off_tiles;
+    DBuf<float> part_dist;
+    DBuf<long long> fb_id;
+    DBuf<int> fail_list, qthr;
+    DBuf<float> fb_dist;
+    HBuf<float> hq;
+    HBuf<int> h_nq, h_qoff, h_meta;
+    // per-search counters in one block so a synced search reads them back with one copy:
+    // [0, 24) counters (u64 x 3), [24, 32) fails (u32 x 2), [32, 48) meta (i32 x 4); the host path
+    // places its result ids / distances right after (kStatBytes) and copies everything at once
+    DBuf<char> blk;
+    HBuf<char> h_blk;
+    unsigned long long* counters() const { return reinterpret_cast<unsigned long long*>(blk.p); }
+    unsigned* fails() const { return reinterpret_cast<unsigned*>(blk.p + 24); }
+    int* meta() const { return reinterpret_cast<int*>(blk.p + 32); }
+    HBuf<rd::ScanTile> h_tiles;
+  } ws;
+
+  cudaStream_t copy_stream = nullptr, off_stream = nullptr;
+  cudaEvent_t ev[8] = {};
+  // device-time accounting: 4 events per search (start, plan done, resident scan done, end)
+  static constexpr int kRing = 64;
+  cudaEvent_t tev[kRing][4] = {};
+  long long t_recorded = 0, t_accounted = 0;
+  rd_timing t_acc{};
+
+  void account(long long i) {  // fold search i's events into t_acc (synchronizes on them)
+    cudaEvent_t* e = tev[i % kRing];
+    CK(cudaEventSynchronize(e[3]));
+    float a = 0, b = 0, c = 0, t = 0;
+    if (!no_inner_events) {
+      CK(cudaEventElapsedTime(&a, e[0], e[1]));
+      CK(cudaEventElapsedTime(&b, e[1], e[2]));
+      CK(cudaEventElapsedTime(&c, e[2], e[3]));
+    }
+    CK(cudaEventElapsedTime(&t, e[0], e[3]));
+    t_acc.searches += 1;
+    t_acc.coarse_ms += a;
+    t_acc.scan_ms += b;
+    t_acc.tail_ms += c;
+    t_acc.total_ms += t;
+  }
+  cudaEvent_t* next_timing_slot() {
+    if (t_recorded - t_accounted >= kRing) account(t_accounted++);
+    return tev[t_recorded++ % kRing];
+  }
+  std::vector<cudaEvent_t> slot_ready, slot_done;
+
+  ~rd_index() {
+    cudaSetDevice(device);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (off_stream) cudaStreamDestroy(off_stream);
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto e : slot_ready) cudaEventDestroy(e);
+    for (auto e : slot_done) cudaEventDestroy(e);
+    for (auto& r : tev)
+      for (auto e : r)
+        if (e) cudaEventDestroy(e);
+  }
+
+  void init_runtime() {
+    CK(cudaSetDevice(device));
+    CK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device));
+    int major = 0;
+    CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    if (major != 10) throw_rd(RD_ERR_RUNTIME, "librd_b200 requires an sm_100 (B200) device, found sm_%d.x", major);
+    CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&off_stream, cudaStreamNonBlocking));
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    for (auto& r : tev)
+      for (auto& e : r) CK(cudaEventCreate(&e));
+    if (const char* v = std::getenv("RD_TC_MIN_Q")) tc_min_q = std::max(1, std::atoi(v));
+    if (const char* v = std::getenv("RD_DEBUG_SKIP")) debug_skip = std::atoi(v);
+    if (const char* v = std::getenv("RD_STAGE_MAX_B")) stage_max_b = std::atoi(v);
+    if (const char* v = std::getenv("RD_TILES_PER_SM")) tiles_per_sm = std::max(1, std::atoi(v));
+    if (const char* v = std::getenv("RD_SEED_MAX_B")) seed_max_b = std::atoll(v);
+    // the tensor-core scan stages bf16 query slices of 64 dims
+  }
+
+  void finish_layout() {
+    max_len = 0;
+    for (int l = 0; l < nlist; ++l) max_len = std::max(max_len, list_off[l + 1] - list_off[l]);
+    d_list_off.alloc(nlist + 1);
+    CK(cudaMemcpy(d_list_off.p, list_off.data(), sizeof(long long) * (nlist + 1), cudaMemcpyHostToDevice));
+    d_row_list.alloc(n);
+    CK(rd::launch_row_list(d_list_off.p, nlist, d_row_list.p, 0));
+    // all lists resident in list order
+    resident.assign(nlist, 1);
+    res_row0.resize(nlist);
+    host_row0.assign(nlist, -1);
+    for (int l = 0; l < nlist; ++l) res_row0[l] = list_off[l];
+    n_resident = n;
+    upload_residency();
+    prepare_centroids();
+    DBuf<float> tmp;
+    tmp.alloc(1);
+    float m2 = 0;
+    CK(rd::launch_max_f32(xnorm.p, n, tmp.p, 0));
+    CK(cudaMemcpy(&m2, tmp.p, sizeof(float), cudaMemcpyDeviceToHost));
+    xmax = std::sqrt(m2) * (1.f + 1e-6f);
+    CK(cudaDeviceSynchronize());
+    build_presplit();
+  }
+
+  // coarse-stage state derived from the centroids: ||c||^2, the bf16 (hi, lo) split and its TMA
+  // map for the tensor-core coarse GEMM, and max ||c|| for the selection's error bound
+  void prepare_centroids() {
+    if (cnorm.n < (size_t)nlist) cnorm.alloc(nlist);
+    CK(launch_row_norms_wrap(centroids.p, nlist, cnorm.p));
+    if (d % 64 == 0) {
+      if (csplit.n < (size_t)nlist * d) csplit.alloc((size_t)nlist * d);  // 2 x bf16 per element = one float
+      CK(rd::launch_qsplit(centroids.p, csplit.p, nlist, d, 0));
+      cmap = make_split_map(csplit.p, nlist, d);
+    }
+    DBuf<float> tmp;
+    tmp.alloc(1);
+    CK(rd::launch_max_f32(cnorm.p, nlist, tmp.p, 0));
+    float m2 = 0;
+    CK(cudaMemcpy(&m2, tmp.p, sizeof(float), cudaMemcpyDeviceToHost));
+    cmax = std::sqrt(m2) * (1.f + 1e-6f);
+  }
+
+  void build_presplit() {
+    presplit = false;
+    xsplit.reset();
+    const char* env = std::getenv("RD_PRESPLIT");
+    // a byte budget (e.g. the LLM reservation, C5) must not be exceeded by a second copy
+    if (!tc_scan() || (env && std::atoi(env) == 0) || n_resident == 0 || budgeted) return;
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    const size_t need = (size_t)n_resident * d * 4;
+    if (need + (size_t(4) << 30) > fr) return;  // not enough room: the converter path stays
+    xsplit.alloc((size_t)n_resident * d);
+    CK(rd::launch_qsplit(arena.p, xsplit.p, n_resident, d, 0));
+    CK(cudaDeviceSynchronize());
+    xmap128 = make_split_map(xsplit.p, n_resident, d, rd::kTcRows);
+    xmap32 = make_split_map(xsplit.p, n_resident, d, 32);
+    presplit = true;
+  }
+
+  // Profiling only (RD_DEBUG_TS): runs `launch` with its kernel's CTA-0 checkpoint buffer attached
+  // (globaltimer at [i], clock64 at [16 + i], RD_TS in rd_device.cuh), waits, and prints the clock64
+  // offsets of each checkpoint from the first. Otherwise just launches.
+  template <class F>
+  void traced(const char* name, cudaStream_t s, unsigned long long*& slot, F&& launch) {
+    if (!dbg_ts) {
+      launch();
+      return;
+    }
+    if (!dbg_buf.p) dbg_buf.alloc(32);
+    CK(cudaMemsetAsync(dbg_buf.p, 0, 32 * sizeof(unsigned long long), s));
+    slot = dbg_buf.p;
+    launch();
+    slot = nullptr;
+    unsigned long long t[32];
+    CK(cudaMemcpyAsync(t, dbg_buf.p, sizeof t, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    fprintf(stderr, "%s [14]=%lld [15]=%lld cycles:", name, (long long)t[14], (long long)t[15]);
+    for (int i = 1; i < 14; ++i)
+      if (t[16 + i]) fprintf(stderr, " %d:%lld", i, (long long)(t[16 + i] - t[16]));
+    fprintf(stderr, "\n");
+  }
+  DBuf<unsigned long long> dbg_buf, dbg_scan;
+
+  // H2D staging ring for offloaded lists: `slots` slots of `slot_rows` rows (0 slots: none)
+  void set_staging(int nslots, long long nrows) {
+    for (auto e : slot_ready) cudaEventDestroy(e);
+    for (auto e : slot_done) cudaEventDestroy(e);
+    slot_ready.clear();
+    slot_done.clear();
+    staging.reset();
+    slots = nslots;
+    slot_rows = nrows;
+    if (!slots) return;
+    staging.alloc((size_t)slots * slot_rows * d);
+    smap256 = make_row_map(staging.p, (long long)slots * slot_rows, d, rd::kScanRows);
+    smap128 = make_row_map(staging.p, (long long)slots * slot_rows, d, rd::kTcRows);
+    smap32 = make_row_map(staging.p, (long long)slots * slot_rows, d, 32);
+    slot_ready.resize(slots);
+    slot_done.resize(slots);
+    for (int s = 0; s < slots; ++s) {
+      CK(cudaEventCreateWithFlags(&slot_ready[s], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&slot_done[s], cudaEventDisableTiming));
+    }
+  }
+
+  cudaError_t launch_row_norms_wrap(const float* X, long long rows, float* out) {
+    return rd::launch_row_norms(X, rows, d, out, 0);
+  }
+
+  void upload_residency() {
+    d_res_row0.alloc(nlist);
+    CK(cudaMemcpy(d_res_row0.p, res_row0.data(), sizeof(long long) * nlist, cudaMemcpyHostToDevice));
+    xsplit.reset();  // any relayout invalidates the pre-split copy (rebuilt by build_presplit)
+    presplit = false;
+    std::vector<const float*> base(nlist);
+    for (int l = 0; l < nlist; ++l)
+      base[l] = resident[l] ? arena.p + (size_t)res_row0[l] * d : host_arena.p + (size_t)host_row0[l] * d;
+    d_list_base.alloc(nlist);
+    CK(cudaMemcpy(d_list_base.p, base.data(), sizeof(const float*) * nlist, cudaMemcpyHostToDevice));
+    map256 = make_row_map(arena.p, std::max(1LL, n_resident), d, rd::kScanRows);
+    map128 = make_row_map(arena.p, std::max(1LL, n_resident), d, rd::kTcRows);
+    map32 = make_row_map(arena.p, std::max(1LL, n_resident), d, 32);
+  }
+};
+
+namespace {
+
+void check_dims(int d) {
+  if (d < 32 || d % 32 != 0 || d > 1024)
+    throw_rd(RD_ERR_INVALID, "d must be a multiple of 32 in [32, 1024], got %d", d);
+}
+
+std::unique_ptr<rd_index> new_index(int device) {
+  auto h = std::make_unique<rd_index>();
+  h->device = device;
+  h->init_runtime();
+  return h;
+}
+
+}  // namespace

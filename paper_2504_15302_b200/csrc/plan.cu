@@ -5,7 +5,7 @@
 // deterministically), then every probed, HBM-resident list is cut into scan
 // tiles of <= R rows x <= 16 queries. Tiles of one list are adjacent so the
 // query groups of a chunk hit L2 for each other. Offloaded lists get no device
-// tiles here; the host plans them as their bytes are staged (api.cu).
+// tiles here; the host plans them as their bytes are staged (search.cu).
 #include "ivf_kernels.cuh"
 #include "rd_device.cuh"
 

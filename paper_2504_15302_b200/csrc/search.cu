@@ -1,0 +1,511 @@
+// search.cu — one search behind include/rd.h (rd_search, rd_search_device, rd_probe):
+//
+//   qprep -> N1 coarse (GEMV / tensor-core GEMM) -> N2 select + seed -> N3 plan
+//     -> N4/N5 resident scan (persistent, main stream)
+//     || N9 offloaded lists: cudaMemcpyAsync pinned->staging on a copy stream,
+//        event-gated scans of staged slots on a side stream
+//   -> N6/N7 merge + exact rerank -> (exact fallback) -> results
+//
+// plus device-time accounting and the shard merges (N11). Reference seam: retrieval_time(P, db)
+// (cost_model.cpp:15-21), called by the retrieval worker (simulator.cpp:359,560).
+#include "host.cuh"
+
+extern "C" {
+
+// ---------------------------------------------------------------- search
+namespace {
+
+struct Plan {
+  int R;
+  int max_chunks;
+  int cap;
+  long long max_tiles;
+};
+
+Plan make_plan(const rd_index* h, long long B, int nprobe) {
+  Plan pl;
+  const int np = std::min(nprobe, h->nlist);
+  const double avg = h->nlist ? (double)h->n / h->nlist : 0.0;
+  const double est_rows = std::min((double)h->n, (double)B * np * avg);
+  // ~tiles_per_sm tiles per SM so the dynamic tile queue's tail (at most one tile per SM) stays
+  // short; rows rounded to the tensor-core tile (128), at least one 256-row TMA box of the FFMA scan
+  // when that path is in use
+  const long long gran = rd::kTcRows;
+  long long R = (long long)std::ceil(est_rows / ((double)h->num_sms * h->tiles_per_sm));
+  R = std::max<long long>(h->tc_min_q > 1 || !h->tc_scan() ? rd::kScanRows : gran,
+                          std::min<long long>(4096, (R + gran - 1) / gran * gran));
+  pl.R = (int)R;
+  pl.max_chunks = (int)std::max<long long>(1, (h->max_len + R - 1) / R);
+  pl.cap = np * pl.max_chunks * rd::kPartsPerTile;
+  pl.max_tiles = std::min<long long>(B * np, B * np / rd::kScanG + h->nlist) * pl.max_chunks + 1;
+  return pl;
+}
+
+// result_bytes: bytes after the stat block that the sync copy brings back too (the host path's results)
+void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, long long* d_ids, float* d_dists,
+               cudaStream_t s, bool sync, rd_search_stats* st, size_t result_bytes = 0,
+               const std::function<void()>& before_sync = {}) {
+  if (nprobe < 1 || k < 1) throw_rd(RD_ERR_INVALID, "search: nprobe >= 1 and k >= 1 required");
+  if (k > rd::kMaxK) throw_rd(RD_ERR_INVALID, "search: k <= %d supported, got %d", rd::kMaxK, k);
+  if (std::min(nprobe, h->nlist) + rd::kCoarseExtra > 512) throw_rd(RD_ERR_INVALID, "search: nprobe <= 480 supported");
+  CK(cudaSetDevice(h->device));
+  auto& w = h->ws;
+  const int nl = h->nlist, d = h->d;
+  const Plan pl = make_plan(h, B, nprobe);
+  const int W = (int)((B + 31) / 32);
+  w.qnorm.ensure(B);
+  w.Dc.ensure((size_t)B * nl);
+  w.probes.ensure((size_t)B * nprobe);
+  w.bitmap.ensure((size_t)nl * W);
+  w.list_nq.ensure(nl);
+  w.list_qoff.ensure(nl);
+  w.list_ntile.ensure(2 * (size_t)nl);
+  w.list_toff.ensure(2 * (size_t)nl);
+  w.list_q.ensure((size_t)B * nprobe);
+  w.tiles.ensure(pl.max_tiles);
+  w.ff_tiles.ensure(pl.max_tiles);
+  w.qsplit.ensure((size_t)B * 2 * d);
+  w.blk.ensure(kStatBytes + result_bytes);
+  w.h_blk.ensure(kStatBytes + result_bytes);
+  w.part_count.ensure(B);
+  w.part_dist.ensure((size_t)B * pl.cap * rd::kTopK);
+  w.part_row.ensure((size_t)B * pl.cap * rd::kTopK);
+
+
+  cudaEvent_t* te = h->next_timing_slot();
+  cudaEvent_t e0 = te[0], e1 = te[1], e2 = te[2], e3 = h->ev[3], e_plan = h->ev[4], e_off = h->ev[5];
+  unsigned long long launches = 0;
+  CK(cudaEventRecord(e0, s));
+  // ||q||^2 and the query split (the tensor-core scan's operand) in one pass
+  CK(rd::launch_qprep(d_q, B, d, w.qnorm.p, d % 64 == 0 ? w.qsplit.p : nullptr, w.fails(), w.part_count.p, s));
+  if (rd::coarse_small((int)B)) {
+    CK(rd::launch_coarse_small(d_q, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, h->num_sms, s));
+  } else if (d % 64 == 0) {
+    const CUtensorMap qmap = make_split_map(w.qsplit.p, B, d);
+    CK(rd::launch_coarse_tc(qmap, h->cmap, h->cnorm.p, w.Dc.p, (int)B, nl, d, s));
+  } else {
+    CK(rd::launch_coarse(d_q, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, s));
+  }
+  w.qthr.ensure(B);
+  const bool seed = B <= h->seed_max_b;
+  if (!seed) CK(cudaMemsetAsync(w.qthr.p, 0x7f, sizeof(int) * B, s));  // no threshold: huge
+  rd::SelectParams sp{w.Dc.p, d_q, w.qnorm.p, h->centroids.p, w.probes.p, w.fails(), (int)B, nl, nprobe, d, h->cmax,
+                      h->d_list_off.p, h->d_res_row0.p, h->arena.p, h->xmax, seed ? w.qthr.p : nullptr, 0};
+  h->traced("select", s, sp.dbg, [&] { CK(rd::launch_select(sp, h->stage_rows(B), s)); });
+  launches += 3;
+  rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
+                    w.list_ntile.p, w.list_toff.p, w.list_q.p, w.tiles.p, w.ff_tiles.p, w.meta(), w.counters(),
+                    (int)B, nl, nprobe, pl.R, h->tc_scan() ? h->tc_min_q : 1 << 30};
+  h->traced("plan", s, pp.dbg, [&] { CK(rd::launch_plan(pp, s)); });
+  launches += rd::plan_small_ok((int)B, nprobe) || rd::plan_fused_ok((int)B, nl) ? 1 : 4;
+  if (!h->no_inner_events) CK(cudaEventRecord(e1, s));
+
+  const bool has_off = h->slots > 0;
+  if (has_off) {  // fetch the probe histogram for host-side staging decisions
+    w.h_nq.ensure(nl);
+    w.h_qoff.ensure(nl);
+    CK(cudaMemcpyAsync(w.h_nq.p, w.list_nq.p, sizeof(int) * nl, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(w.h_qoff.p, w.list_qoff.p, sizeof(int) * nl, cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaEventRecord(e_plan, s));
+  const CUtensorMap gmap = make_gather_map(w.qsplit.p, B, d);
+  rd::ScanParams sc{w.ff_tiles.p, w.meta() + 2, w.meta() + 3, d_q, w.qnorm.p, w.list_q.p, h->xnorm.p,
+                    w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p};
+  rd::TcScanParams tc{w.tiles.p, w.meta(), w.meta() + 1, w.qsplit.p, w.qnorm.p, w.list_q.p, h->xnorm.p,
+                      w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p, h->debug_skip};
+  if (!h->tc_scan() || h->tc_min_q > 1) {  // FFMA tiles exist only in these cases
+    CK(rd::launch_scan(h->map256, h->map32, sc, h->num_sms, s));
+    launches += 1;
+  }
+  if (h->tc_scan()) {  // otherwise every tile is FFMA
+    if (h->dbg_ts) {  // profiling only: per-CTA entry / ready / first tile / end times
+      if (h->dbg_scan.n < 4 * (size_t)h->num_sms) h->dbg_scan.alloc(4 * (size_t)h->num_sms);
+      CK(cudaMemsetAsync(h->dbg_scan.p, 0, 8 * 4 * (size_t)h->num_sms, s));
+      tc.dbg = h->dbg_scan.p;
+    }
+    CK(rd::launch_scan_tc(h->presplit ? h->xmap128 : h->map128, h->presplit ? h->xmap32 : h->map32, gmap, tc,
+                          h->num_sms, s, h->presplit));
+    launches += 1;
+    if (h->dbg_ts) {
+      std::vector<unsigned long long> t(4 * (size_t)h->num_sms);
+      CK(cudaMemcpyAsync(t.data(), h->dbg_scan.p, 8 * t.size(), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      unsigned long long t0 = ~0ull, mx[4] = {0, 0, 0, 0};
+      for (int c = 0; c < h->num_sms; ++c) t0 = std::min(t0, t[4 * c]);
+      double mean[4] = {0, 0, 0, 0};
+      for (int c = 0; c < h->num_sms; ++c)
+        for (int j = 0; j < 4; ++j) {
+          const unsigned long long v = t[4 * c + j] ? t[4 * c + j] - t0 : 0;
+          mx[j] = std::max(mx[j], v);
+          mean[j] += (double)v / h->num_sms;
+        }
+      fprintf(stderr, "scan ns from first CTA entry: entry mean %.0f max %llu | ready mean %.0f max %llu | "
+              "first tile mean %.0f max %llu | end mean %.0f max %llu\n", mean[0], mx[0], mean[1], mx[1], mean[2],
+              mx[2], mean[3], mx[3]);
+    }
+  }
+  if (!h->no_inner_events) CK(cudaEventRecord(e2, s));
+
+  unsigned long long h2d = 0;
+  if (has_off) {
+    CK(cudaEventSynchronize(e_plan));
+    // offloaded, probed lists in ascending id, packed into staging slots
+    std::vector<std::vector<int>> batches;
+    long long fill = 0;
+    for (int l = 0; l < nl; ++l) {
+      if (h->resident[l] || w.h_nq.p[l] == 0) continue;
+      const long long len = h->list_off[l + 1] - h->list_off[l];
+      if (len == 0) continue;
+      if (batches.empty() || fill + len > h->slot_rows) {
+        batches.emplace_back();
+        fill = 0;
+      }
+      batches.back().push_back(l);
+      fill += len;
+    }
+    // host-planned tiles of every batch (tensor-core and FFMA groups), uploaded once
+    const size_t nb = batches.size();
+    std::vector<rd::ScanTile> tv;  // per batch: [tc tiles][ff tiles]
+    std::vector<int> tstart(nb + 1, 0), ntc(nb, 0);
+    for (size_t bi = 0; bi < nb; ++bi) {
+      tstart[bi] = (int)tv.size();
+      std::vector<rd::ScanTile> ff;
+      long long srow = (long long)(bi % h->slots) * h->slot_rows;
+      for (int l : batches[bi]) {
+        const long long len = h->list_off[l + 1] - h->list_off[l];
+        const int nq = w.h_nq.p[l];
+        const bool tcl = nq >= h->tc_min_q && h->tc_scan();
+        const int ngr = tcl ? (nq + rd::kTcG - 1) / rd::kTcG : (nq + rd::kScanG - 1) / rd::kScanG;
+        for (long long c = 0; c * pl.R < len; ++c)
+          for (int g = 0; g < ngr; ++g) {
+            rd::ScanTile T;
+            T.src_row = srow + c * pl.R;
+            T.grow0 = h->list_off[l] + c * pl.R;
+            T.list = l;
+            T.nrows = (int)std::min<long long>(pl.R, len - c * pl.R);
+            if (tcl) {
+              const int q0 = (int)((long long)g * nq / ngr), q1 = (int)((long long)(g + 1) * nq / ngr);
+              T.qoff = w.h_qoff.p[l] + q0;
+              T.nq = q1 - q0;
+              tv.push_back(T);
+            } else {
+              T.qoff = w.h_qoff.p[l] + g * rd::kScanG;
+              T.nq = std::min(rd::kScanG, nq - g * rd::kScanG);
+              ff.push_back(T);
+            }
+          }
+        srow += len;
+      }
+      ntc[bi] = (int)tv.size() - tstart[bi];
+      tv.insert(tv.end(), ff.begin(), ff.end());
+    }
+    tstart[nb] = (int)tv.size();
+    if (nb) {
+      w.h_tiles.ensure(tv.size());
+      std::memcpy(w.h_tiles.p, tv.data(), sizeof(rd::ScanTile) * tv.size());
+      w.off_tiles.ensure(tv.size());
+      w.h_meta.ensure(4 * nb);
+      for (size_t bi = 0; bi < nb; ++bi) {
+        w.h_meta.p[4 * bi + 0] = ntc[bi];
+        w.h_meta.p[4 * bi + 1] = 0;
+        w.h_meta.p[4 * bi + 2] = tstart[bi + 1] - tstart[bi] - ntc[bi];
+        w.h_meta.p[4 * bi + 3] = 0;
+      }
+      DBuf<int>& dmeta = w.off_meta;
+      dmeta.ensure(4 * nb);
+      CK(cudaStreamWaitEvent(h->off_stream, e_plan, 0));
+      CK(cudaMemcpyAsync(w.off_tiles.p, w.h_tiles.p, sizeof(rd::ScanTile) * tv.size(), cudaMemcpyHostToDevice,
+                         h->off_stream));
+      CK(cudaMemcpyAsync(dmeta.p, w.h_meta.p, sizeof(int) * 4 * nb, cudaMemcpyHostToDevice, h->off_stream));
+      CK(cudaEventRecord(e3, h->off_stream));
+      CK(cudaStreamWaitEvent(h->copy_stream, e_plan, 0));
+      for (size_t bi = 0; bi < nb; ++bi) {
+        const int slot = (int)(bi % h->slots);
+        if (bi >= (size_t)h->slots) CK(cudaStreamWaitEvent(h->copy_stream, h->slot_done[slot], 0));
+        long long srow = (long long)slot * h->slot_rows;
+        for (int l : batches[bi]) {
+          const long long len = h->list_off[l + 1] - h->list_off[l];
+          const size_t bytes = (size_t)len * d * sizeof(float);
+          CK(cudaMemcpyAsync(h->staging.p + (size_t)srow * d, h->host_arena.p + (size_t)h->host_row0[l] * d, bytes,
+                             cudaMemcpyHostToDevice, h->copy_stream));
+          h2d += bytes;
+          srow += len;
+        }
+        CK(cudaEventRecord(h->slot_ready[slot], h->copy_stream));
+        CK(cudaStreamWaitEvent(h->off_stream, h->slot_ready[slot], 0));
+        const int nt_tc = ntc[bi], nt_ff = tstart[bi + 1] - tstart[bi] - ntc[bi];
+        if (nt_ff) {
+          rd::ScanParams so = sc;
+          so.tiles = w.off_tiles.p + tstart[bi] + nt_tc;
+          so.ntiles = dmeta.p + 4 * bi + 2;
+          so.tile_counter = dmeta.p + 4 * bi + 3;
+          CK(rd::launch_scan(h->smap256, h->smap32, so, std::min(h->num_sms, nt_ff), h->off_stream));
+          launches += 1;
+        }
+        if (nt_tc) {
+          rd::TcScanParams to = tc;
+          to.tiles = w.off_tiles.p + tstart[bi];
+          to.ntiles = dmeta.p + 4 * bi + 0;
+          to.tile_counter = dmeta.p + 4 * bi + 1;
+          CK(rd::launch_scan_tc(h->smap128, h->smap32, gmap, to, std::min(h->num_sms, nt_tc), h->off_stream, false));
+          launches += 1;
+        }
+        CK(cudaEventRecord(h->slot_done[slot], h->off_stream));
+      }
+    }
+    CK(cudaEventRecord(e_off, h->off_stream));
+    CK(cudaStreamWaitEvent(s, e_off, 0));
+  }
+
+  if (!w.fb_ctr.p) {  // the fallback kernel's completion counter: zeroed once, re-armed by the kernel
+    w.fb_ctr.alloc(1);
+    CK(cudaMemset(w.fb_ctr.p, 0, sizeof(unsigned)));
+  }
+  w.fail_list.ensure(B);
+  w.fb_dist.ensure((size_t)B * nprobe * rd::kTopK);
+  w.fb_id.ensure((size_t)B * nprobe * rd::kTopK);
+  rd::MergeParams mp{w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d_q, w.qnorm.p, h->d_list_off.p,
+                     h->d_list_base.p, h->d_ids.p, h->d_row_list.p, h->arena.p,
+                     h->arena.p + (size_t)h->n_resident * d, nl, d, k, h->xmax, d_ids, d_dists,
+                     w.fails() + 1, w.fail_list.p, (int)B};
+  h->traced("merge", s, mp.dbg, [&] { CK(rd::launch_merge(mp, h->stage_rows(B), s)); });
+  rd::FallbackParams fp{w.fail_list.p, w.fails() + 1, w.probes.p, nprobe, d_q, h->d_list_off.p, h->d_list_base.p,
+                        h->d_ids.p, nl, d, k, w.fb_dist.p, w.fb_id.p, d_ids, d_dists, w.fb_ctr.p};
+  CK(rd::launch_fallback(fp, h->num_sms, s));
+  launches += 2;
+  CK(cudaEventRecord(te[3], s));
+  if (st) {
+    std::memset(st, 0, sizeof *st);
+    st->kernel_launches = launches;
+  }
+  if (before_sync) before_sync();  // e.g. the host path's result copies, ordered before the one sync
+  if (sync) {
+    // counters (and, on the host path, the results placed after them) in one copy
+    CK(cudaMemcpyAsync(w.h_blk.p, w.blk.p, kStatBytes + result_bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const auto* hc = reinterpret_cast<const unsigned long long*>(w.h_blk.p);
+    const auto* hf = reinterpret_cast<const unsigned*>(w.h_blk.p + 24);
+    const auto* hm = reinterpret_cast<const int*>(w.h_blk.p + 32);
+    if (st) {
+      float ms = 0;
+      const unsigned long long row_bytes = (unsigned long long)d * 4;
+      st->lists_probed = hc[0];
+      st->bytes_lists_resident = hc[1] * row_bytes;
+      st->h2d_list_bytes = h2d;
+      st->bytes_algorithmic = (hc[1] + hc[2]) * row_bytes + (unsigned long long)nl * row_bytes +
+                              (unsigned long long)B * row_bytes + (unsigned long long)B * k * 12ull;
+      st->tiles = (uint64_t)hm[0] + (uint64_t)hm[2];
+      if (!h->no_inner_events) {
+        CK(cudaEventElapsedTime(&ms, e1, e2));
+        st->scan_ms = ms;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        st->coarse_ms = ms;
+      }
+      if (has_off) {
+        CK(cudaEventElapsedTime(&ms, e_plan, e_off));
+        st->offload_ms = ms;
+      }
+      st->probe_failures = hf[0];
+      st->margin_failures = hf[1];
+    }
+  }
+}
+
+}  // namespace
+
+namespace {
+// Largest batch searched in one pass: bounds the B x nlist coarse-distance workspace (2 GiB).
+long long search_chunk(const rd_index* h) {
+  return std::max<long long>(1024, std::min<long long>(65536, (1LL << 31) / (4LL * h->nlist)));
+}
+void add_stats(rd_search_stats* acc, const rd_search_stats& s) {  // counters summed over chunks
+  acc->bytes_algorithmic += s.bytes_algorithmic;
+  acc->bytes_lists_resident += s.bytes_lists_resident;
+  acc->h2d_list_bytes += s.h2d_list_bytes;
+  acc->lists_probed += s.lists_probed;
+  acc->tiles += s.tiles;
+  acc->kernel_launches += s.kernel_launches;
+  acc->scan_ms += s.scan_ms;
+  acc->coarse_ms += s.coarse_ms;
+  acc->offload_ms += s.offload_ms;
+  acc->margin_failures += s.margin_failures;
+  acc->probe_failures += s.probe_failures;
+}
+}  // namespace
+
+int rd_search_device(rd_index* h, const float* d_q, int64_t B, int32_t nprobe, int32_t k, int64_t* d_ids,
+                     float* d_dists, void* stream, int32_t sync, rd_search_stats* st) {
+  return guarded([&] {
+    if (!h || B < 0 || (B > 0 && (!d_q || !d_ids || !d_dists))) throw_rd(RD_ERR_INVALID, "search: invalid arguments");
+    if (st) std::memset(st, 0, sizeof *st);
+    if (B == 0) return;
+    const auto t0 = std::chrono::steady_clock::now();
+    const long long chunk = search_chunk(h);
+    for (long long b0 = 0; b0 < B; b0 += chunk) {  // very large batches run as consecutive passes
+      const long long nb = std::min<long long>(chunk, B - b0);
+      rd_search_stats part{};
+      do_search(h, d_q + (size_t)b0 * h->d, nb, nprobe, k, reinterpret_cast<long long*>(d_ids) + (size_t)b0 * k,
+                d_dists + (size_t)b0 * k, (cudaStream_t)stream, sync != 0, st ? &part : nullptr);
+      if (st) add_stats(st, part);
+    }
+    if (st) st->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+int rd_search(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32_t k, int64_t* out_ids,
+              float* out_dists, rd_search_stats* st) {
+  if (h && B > search_chunk(h) && queries && out_ids && out_dists && h->d > 0 && k > 0) {
+    // very large batches: consecutive passes of the one-pass path below
+    const auto t0 = std::chrono::steady_clock::now();
+    rd_search_stats acc{};
+    const long long chunk = search_chunk(h);
+    for (long long b0 = 0; b0 < B; b0 += chunk) {
+      rd_search_stats part{};
+      const int rc = rd_search(h, queries + (size_t)b0 * h->d, std::min<long long>(chunk, B - b0), nprobe, k,
+                               out_ids + (size_t)b0 * k, out_dists + (size_t)b0 * k, &part);
+      if (rc != RD_OK) return rc;
+      add_stats(&acc, part);
+    }
+    acc.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (st) *st = acc;
+    return RD_OK;
+  }
+  return guarded([&] {
+    if (!h || B < 0 || (B > 0 && (!queries || !out_ids || !out_dists)))
+      throw_rd(RD_ERR_INVALID, "search: invalid arguments");
+    if (nprobe < 1 || k < 1) throw_rd(RD_ERR_INVALID, "search: nprobe >= 1 and k >= 1 required");
+    const auto t0 = std::chrono::steady_clock::now();
+    if (B == 0) {
+      if (st) std::memset(st, 0, sizeof *st);
+      return;
+    }
+    CK(cudaSetDevice(h->device));
+    auto& w = h->ws;
+    const size_t qn = (size_t)B * h->d, rn = (size_t)B * k;
+    w.q.ensure(qn);
+    // caller buffers that are already page-locked are copied directly; others go through the
+    // handle's pinned staging buffers
+    auto pinned = [](const void* ptr) {
+      cudaPointerAttributes a;
+      if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+      return a.type == cudaMemoryTypeHost;
+    };
+    const bool pq = pinned(queries), pi = pinned(out_ids), pd = pinned(out_dists);
+    const float* qsrc = queries;
+    if (!pq) {
+      w.hq.ensure(qn);
+      std::memcpy(w.hq.p, queries, qn * sizeof(float));
+      qsrc = w.hq.p;
+    }
+    cudaStream_t s = 0;
+    CK(cudaMemcpyAsync(w.q.p, qsrc, qn * sizeof(float), cudaMemcpyHostToDevice, s));
+    // results live right after the stat block: pinned caller buffers get direct copies, otherwise
+    // stats and results come back in the sync's single copy
+    const bool direct = pi && pd;
+    const size_t res_bytes = rn * (sizeof(long long) + sizeof(float));
+    w.blk.ensure(kStatBytes + res_bytes);
+    long long* d_ids = reinterpret_cast<long long*>(w.blk.p + kStatBytes);
+    float* d_dists = reinterpret_cast<float*>(w.blk.p + kStatBytes + rn * sizeof(long long));
+    do_search(h, w.q.p, B, nprobe, k, d_ids, d_dists, s, true, st, direct ? 0 : res_bytes, [&] {
+      if (!direct) return;
+      CK(cudaMemcpyAsync(out_ids, d_ids, rn * sizeof(long long), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(out_dists, d_dists, rn * sizeof(float), cudaMemcpyDeviceToHost, s));
+    });
+    if (!direct) {
+      std::memcpy(out_ids, w.h_blk.p + kStatBytes, rn * sizeof(long long));
+      std::memcpy(out_dists, w.h_blk.p + kStatBytes + rn * sizeof(long long), rn * sizeof(float));
+    }
+    if (st) st->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+int rd_probe(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32_t* out_lists) {
+  return guarded([&] {
+    if (!h || B < 0 || (B > 0 && (!queries || !out_lists))) throw_rd(RD_ERR_INVALID, "probe: invalid arguments");
+    if (nprobe < 1 || std::min(nprobe, h->nlist) + rd::kCoarseExtra > 512)
+      throw_rd(RD_ERR_INVALID, "probe: 1 <= nprobe <= 480 required");
+    if (B == 0) return;
+    CK(cudaSetDevice(h->device));
+    auto& w = h->ws;
+    const int nl = h->nlist, d = h->d;
+    w.q.ensure((size_t)B * d);
+    w.qnorm.ensure(B);
+    w.Dc.ensure((size_t)B * nl);
+    w.probes.ensure((size_t)B * nprobe);
+    w.blk.ensure(kStatBytes);
+    CK(cudaMemcpy(w.q.p, queries, sizeof(float) * B * d, cudaMemcpyHostToDevice));
+    CK(cudaMemset(w.fails(), 0, 2 * sizeof(unsigned)));
+    w.qsplit.ensure((size_t)B * d);
+    CK(rd::launch_qprep(w.q.p, B, d, w.qnorm.p, d % 64 == 0 ? w.qsplit.p : nullptr, nullptr, nullptr, 0));
+    if (rd::coarse_small((int)B)) {
+      CK(rd::launch_coarse_small(w.q.p, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, h->num_sms, 0));
+    } else if (d % 64 == 0) {
+      const CUtensorMap qmap = make_split_map(w.qsplit.p, B, d);
+      CK(rd::launch_coarse_tc(qmap, h->cmap, h->cnorm.p, w.Dc.p, (int)B, nl, d, 0));
+    } else {
+      CK(rd::launch_coarse(w.q.p, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, 0));
+    }
+    rd::SelectParams sp{w.Dc.p, w.q.p, w.qnorm.p, h->centroids.p, w.probes.p, w.fails(), (int)B, nl, nprobe, d, h->cmax,
+                        h->d_list_off.p, h->d_res_row0.p, h->arena.p, h->xmax, nullptr, 1};
+    CK(rd::launch_select(sp, h->stage_rows(B), 0));
+    CK(cudaMemcpy(out_lists, w.probes.p, sizeof(int) * B * nprobe, cudaMemcpyDeviceToHost));
+  });
+}
+
+int rd_timing_reset(rd_index* h) {
+  return guarded([&] {
+    if (!h) throw_rd(RD_ERR_INVALID, "null index");
+    CK(cudaSetDevice(h->device));
+    while (h->t_accounted < h->t_recorded) {  // drain so the ring's events are free again
+      CK(cudaEventSynchronize(h->tev[h->t_accounted % rd_index::kRing][3]));
+      ++h->t_accounted;
+    }
+    h->t_acc = rd_timing{};
+  });
+}
+
+int rd_timing_read(rd_index* h, rd_timing* out) {
+  return guarded([&] {
+    if (!h || !out) throw_rd(RD_ERR_INVALID, "null argument");
+    CK(cudaSetDevice(h->device));
+    while (h->t_accounted < h->t_recorded) h->account(h->t_accounted++);
+    *out = h->t_acc;
+  });
+}
+
+// ---------------------------------------------------------------- shard merge
+int rd_merge_topk(int32_t G, int64_t B, int32_t k, const int64_t* sid, const float* sd, int64_t* oid, float* od) {
+  return guarded([&] {
+    if (G < 1 || B < 0 || k < 1 || (B > 0 && (!sid || !sd || !oid || !od)))
+      throw_rd(RD_ERR_INVALID, "merge: invalid arguments");
+    std::vector<std::pair<float, int64_t>> c;
+    for (int64_t q = 0; q < B; ++q) {
+      c.clear();
+      for (int g = 0; g < G; ++g)
+        for (int i = 0; i < k; ++i) {
+          const size_t o = ((size_t)g * B + q) * k + i;
+          if (sid[o] >= 0) c.emplace_back(sd[o], sid[o]);
+        }
+      const size_t m = std::min<size_t>(k, c.size());
+      std::partial_sort(c.begin(), c.begin() + m, c.end());
+      for (int i = 0; i < k; ++i) {
+        oid[q * k + i] = (size_t)i < m ? c[i].second : -1;
+        od[q * k + i] = (size_t)i < m ? c[i].first : INFINITY;
+      }
+    }
+  });
+}
+
+int rd_merge_topk_device(int32_t G, int64_t B, int32_t k, const int64_t* ids, const float* dists, int64_t* oid,
+                         float* od, void* stream) {
+  return guarded([&] {
+    if (G < 1 || B < 0 || k < 1 || k > 32) throw_rd(RD_ERR_INVALID, "merge_device: invalid arguments (k <= 32)");
+    CK(rd::launch_shard_merge(G, B, k, reinterpret_cast<const long long*>(ids), dists,
+                              reinterpret_cast<long long*>(oid), od, (cudaStream_t)stream));
+  });
+}
+
+}  // extern "C"

@@ -1,5 +1,5 @@
 // train.cu — IVF training helpers for rd_index_build (sm_100a): the deterministic k-means update
-// and the list-order layout. Assignment reuses the search's coarse path (api.cu).
+// and the list-order layout. Assignment reuses the search's coarse path (index.cu, rd_index_build).
 //
 // Determinism: rows are stably sorted by cluster (CUB radix sort keeps equal keys in input order,
 // i.e. ascending row), and each (cluster, dimension) sum runs sequentially in that order in fp64,
