@@ -289,7 +289,6 @@ struct rd_index {
     DBuf<long long> fb_id;
     DBuf<int> fail_list, qthr;
     DBuf<float> fb_dist;
-    HBuf<float> hq;
     HBuf<int> h_nq, h_qoff, h_meta;
     // per-search counters in one block so a synced search reads them back with one copy:
     // [0, 24) counters (u64 x 3), [24, 32) fails (u32 x 2), [32, 48) meta (i32 x 4); the host path

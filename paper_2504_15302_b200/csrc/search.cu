@@ -383,29 +383,14 @@ int rd_search(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int3
     auto& w = h->ws;
     const size_t qn = (size_t)B * h->d, rn = (size_t)B * k;
     w.q.ensure(qn);
-    // caller buffers that are already page-locked are copied directly; others go through the
-    // handle's pinned staging buffers
-    auto pinned = [](const void* ptr) {
-      cudaPointerAttributes a;
-      if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-      }
-      return a.type == cudaMemoryTypeHost;
-    };
-    const bool pq = pinned(queries), pi = pinned(out_ids), pd = pinned(out_dists);
-    const float* qsrc = queries;
-    if (!pq) {
-      w.hq.ensure(qn);
-      std::memcpy(w.hq.p, queries, qn * sizeof(float));
-      qsrc = w.hq.p;
-    }
+    // cudaMemcpyAsync copies straight from the caller's buffer: DMA when it is page-locked, a staged
+    // copy by the driver otherwise (both correct; no pointer-attribute queries on the hot path)
     cudaStream_t s = 0;
-    CK(cudaMemcpyAsync(w.q.p, qsrc, qn * sizeof(float), cudaMemcpyHostToDevice, s));
-    // results live right after the stat block: pinned caller buffers get direct copies, otherwise
-    // stats and results come back in the sync's single copy
-    const bool direct = pi && pd;
+    CK(cudaMemcpyAsync(w.q.p, queries, qn * sizeof(float), cudaMemcpyHostToDevice, s));
+    // results live right after the stat block: small results come back with the counters in the
+    // sync's single copy; large ones go straight into the caller's buffers
     const size_t res_bytes = rn * (sizeof(long long) + sizeof(float));
+    const bool direct = res_bytes > (size_t(64) << 10);
     w.blk.ensure(kStatBytes + res_bytes);
     long long* d_ids = reinterpret_cast<long long*>(w.blk.p + kStatBytes);
     float* d_dists = reinterpret_cast<float*>(w.blk.p + kStatBytes + rn * sizeof(long long));
