@@ -223,14 +223,28 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
         const int slot = (int)(bi % h->slots);
         if (bi >= (size_t)h->slots) CK(cudaStreamWaitEvent(h->copy_stream, h->slot_done[slot], 0));
         long long srow = (long long)slot * h->slot_rows;
-        for (int l : batches[bi]) {
-          const long long len = h->list_off[l + 1] - h->list_off[l];
-          const size_t bytes = (size_t)len * d * sizeof(float);
-          CK(cudaMemcpyAsync(h->staging.p + (size_t)srow * d, h->host_arena.p + (size_t)h->host_row0[l] * d, bytes,
+        // lists adjacent in the host arena (and so in the slot) go out as one copy: fewer, larger
+        // DMAs keep the host link closer to its peak than one copy per list
+        long long run_src = -1, run_dst = 0, run_rows = 0;
+        auto flush = [&] {
+          if (run_rows == 0) return;
+          const size_t bytes = (size_t)run_rows * d * sizeof(float);
+          CK(cudaMemcpyAsync(h->staging.p + (size_t)run_dst * d, h->host_arena.p + (size_t)run_src * d, bytes,
                              cudaMemcpyHostToDevice, h->copy_stream));
           h2d += bytes;
+          run_rows = 0;
+        };
+        for (int l : batches[bi]) {
+          const long long len = h->list_off[l + 1] - h->list_off[l];
+          if (run_rows && h->host_row0[l] != run_src + run_rows) flush();
+          if (run_rows == 0) {
+            run_src = h->host_row0[l];
+            run_dst = srow;
+          }
+          run_rows += len;
           srow += len;
         }
+        flush();
         CK(cudaEventRecord(h->slot_ready[slot], h->copy_stream));
         CK(cudaStreamWaitEvent(h->off_stream, h->slot_ready[slot], 0));
         const int nt_tc = ntc[bi], nt_ff = tstart[bi + 1] - tstart[bi] - ntc[bi];
