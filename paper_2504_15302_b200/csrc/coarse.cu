@@ -88,6 +88,39 @@ __global__ void __launch_bounds__(256) coarse_gemm_kernel(const float* __restric
 // centroid streams its row once (float4, coalesced) against every query of the batch held in smem,
 // across >= one CTA per SM — instead of the tensor-core tile kernel's 32-CTA, latency-bound K loop.
 // Any summation order is covered by the select kernel's error bound ((d + 4) u 2 |q| |c|).
+// query preparation in one pass, one warp per query: ||q||^2 (the same fp64 lane-strided sum and
+// shuffle tree as row_norms) and the bf16 (hi, lo) split rows the tensor-core kernels gather.
+// It also zeroes the per-search counters (zero2: 2 words, zeroB: B words) so they need no memset.
+__device__ __forceinline__ void qprep_rows(const QprepArgs& a, long long r0, long long rstep, bool zero2_here) {
+  const int lane = threadIdx.x & 31;
+  if (a.zero2 && zero2_here && threadIdx.x < 2) a.zero2[threadIdx.x] = 0u;
+  __nv_bfloat16* qsplit = reinterpret_cast<__nv_bfloat16*>(a.qsplit);
+  for (long long r = r0; r < a.B; r += rstep) {
+    if (a.zeroB && lane == 0) a.zeroB[r] = 0;
+    const float* x = a.Q + (size_t)r * a.d;
+    double s = 0.0;
+    for (int t = lane; t < a.d; t += 32) {
+      const float q = x[t];
+      const double v = q;
+      s += v * v;
+      if (qsplit) {
+        const __nv_bfloat16 h = __float2bfloat16_rn(q);
+        qsplit[(r * 2) * a.d + t] = h;
+        qsplit[(r * 2 + 1) * a.d + t] = __float2bfloat16_rn(q - __bfloat162float(h));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) a.qnorm[r] = (float)s;
+  }
+}
+
+__global__ void qprep_kernel(const QprepArgs a) {
+  RD_PDL_PROLOGUE();
+  const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
+  qprep_rows(a, (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5, warps, blockIdx.x == 0);
+}
+
 constexpr int kSmallB = 16;
 constexpr int kGemvThreads = 256;
 constexpr int kGemvMaxV = 8;  // float4 per lane per row: d <= 1024
@@ -97,9 +130,14 @@ __global__ void __launch_bounds__(kGemvThreads) coarse_gemv_kernel(const float* 
                                                                    const float* __restrict__ C,
                                                                    const float* __restrict__ cnorm,
                                                                    float* __restrict__ Dc, int B, int nlist,
-                                                                   int d) {
+                                                                   int d, const QprepArgs qa) {
   RD_PDL_PROLOGUE();
   const int lane = threadIdx.x & 31;
+  const int nblk = (nlist + kGemvThreads / 32 - 1) / (kGemvThreads / 32);
+  if ((int)blockIdx.x >= nblk) {  // trailing CTA: the query prep (fused to save a launch)
+    qprep_rows(qa, threadIdx.x >> 5, kGemvThreads / 32, true);
+    return;
+  }
   const int c = blockIdx.x * (kGemvThreads / 32) + (threadIdx.x >> 5);
   if (c >= nlist) return;
   const int d4 = d / 4;
@@ -125,35 +163,6 @@ __global__ void __launch_bounds__(kGemvThreads) coarse_gemv_kernel(const float* 
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) Dc[(size_t)b * nlist + c] = cn - 2.f * acc;
-  }
-}
-
-// query preparation in one pass, one warp per query: ||q||^2 (the same fp64 lane-strided sum and
-// shuffle tree as row_norms) and the bf16 (hi, lo) split rows the tensor-core kernels gather
-// It also zeroes the per-search counters (zero2: 2 words, zeroB: B words) so they need no memset.
-__global__ void qprep_kernel(const float* __restrict__ Q, long long B, int d, float* __restrict__ qnorm,
-                             __nv_bfloat16* __restrict__ qsplit, unsigned* zero2, int* zeroB) {
-  RD_PDL_PROLOGUE();
-  const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (zero2 && blockIdx.x == 0 && threadIdx.x < 2) zero2[threadIdx.x] = 0u;
-  for (long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; r < B; r += warps) {
-    if (zeroB && lane == 0) zeroB[r] = 0;
-    const float* x = Q + (size_t)r * d;
-    double s = 0.0;
-    for (int t = lane; t < d; t += 32) {
-      const float q = x[t];
-      const double v = q;
-      s += v * v;
-      if (qsplit) {
-        const __nv_bfloat16 h = __float2bfloat16_rn(q);
-        qsplit[(r * 2) * d + t] = h;
-        qsplit[(r * 2 + 1) * d + t] = __float2bfloat16_rn(q - __bfloat162float(h));
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) qnorm[r] = (float)s;
   }
 }
 
@@ -710,19 +719,17 @@ cudaError_t launch_coarse(const float* Q, const float* C, const float* cnorm, fl
 bool coarse_small(int B) { return B <= 8; }  // measured cut-over vs the tensor-core tile kernel
 
 cudaError_t launch_coarse_small(const float* Q, const float* C, const float* cnorm, float* Dc, int B, int nlist,
-                                int d, int num_sms, cudaStream_t s) {
-  (void)num_sms;
+                                int d, const QprepArgs& qa, cudaStream_t s) {
   if (B == 0) return cudaSuccess;
   if (d > 4 * 32 * kGemvMaxV) return cudaErrorInvalidValue;
-  return launch_k(coarse_gemv_kernel, dim3((nlist + 7) / 8), dim3(kGemvThreads), 0, s, Q, C, cnorm, Dc, B, nlist, d);
+  const int nblk = (nlist + kGemvThreads / 32 - 1) / (kGemvThreads / 32);
+  return launch_k(coarse_gemv_kernel, dim3(nblk + 1), dim3(kGemvThreads), 0, s, Q, C, cnorm, Dc, B, nlist, d, qa);
 }
 
-cudaError_t launch_qprep(const float* Q, long long B, int d, float* qnorm, void* qsplit, unsigned* zero2, int* zeroB,
-                         cudaStream_t s) {
-  if (B == 0) return cudaSuccess;
-  const long long blocks = (B * 32 + 255) / 256;
-  return launch_k(qprep_kernel, dim3((unsigned)(blocks < 148 * 8 ? blocks : 148 * 8)), dim3(256), 0, s, Q, B, d, qnorm,
-                  reinterpret_cast<__nv_bfloat16*>(qsplit), zero2, zeroB);
+cudaError_t launch_qprep(const QprepArgs& a, cudaStream_t s) {
+  if (a.B == 0) return cudaSuccess;
+  const long long blocks = (a.B * 32 + 255) / 256;
+  return launch_k(qprep_kernel, dim3((unsigned)(blocks < 148 * 8 ? blocks : 148 * 8)), dim3(256), 0, s, a);
 }
 
 cudaError_t launch_select(const SelectParams& p, bool stage, cudaStream_t s) {

@@ -229,7 +229,8 @@ int rd_index_build(int64_t n, int32_t d, int32_t nlist, const float* vectors, co
       for (long long b0 = 0; b0 < n; b0 += chunk) {
         const int B = (int)std::min(chunk, n - b0);
         const float* q = X.p + (size_t)b0 * d;
-        CK(rd::launch_qprep(q, B, d, w.qnorm.p, d % 64 == 0 ? w.qsplit.p : nullptr, w.fails(), nullptr, s));
+        CK(rd::launch_qprep(rd::QprepArgs{q, B, d, w.qnorm.p, d % 64 == 0 ? w.qsplit.p : nullptr, w.fails(), nullptr},
+                            s));
         if (d % 64 == 0) {
           const CUtensorMap qmap = make_split_map(w.qsplit.p, B, d);
           CK(rd::launch_coarse_tc(qmap, h->cmap, h->cnorm.p, w.Dc.p, B, nlist, d, s));

@@ -103,14 +103,23 @@ cudaError_t launch_scan(const CUtensorMap& map256, const CUtensorMap& map32, con
 // constant per query and added where an absolute distance is needed).
 cudaError_t launch_coarse(const float* Q, const float* C, const float* cnorm, float* Dc, int B,
                           int nlist, int d, cudaStream_t s);
-// small batches: FFMA GEMV over the centroids (memory-bound; see coarse_small for the cut-over)
+// Query preparation: ||q||^2 and (when qsplit != nullptr) the bf16 (hi, lo) split rows of a query
+// batch in one pass; zero2 (2 words) and zeroB (B words) are zeroed on the way when non-null.
+struct QprepArgs {
+  const float* Q;
+  long long B;
+  int d;
+  float* qnorm;
+  void* qsplit;
+  unsigned* zero2;
+  int* zeroB;
+};
+cudaError_t launch_qprep(const QprepArgs& a, cudaStream_t s);
+// small batches: FFMA GEMV over the centroids (memory-bound; see coarse_small for the cut-over), with
+// the query preparation `qa` fused into one trailing CTA
 bool coarse_small(int B);
 cudaError_t launch_coarse_small(const float* Q, const float* C, const float* cnorm, float* Dc, int B, int nlist,
-                                int d, int num_sms, cudaStream_t s);
-// ||q||^2 and (when qsplit != nullptr) the bf16 (hi, lo) split rows of a query batch, one pass;
-// zero2 (2 words) and zeroB (B words) are zeroed on the way when non-null
-cudaError_t launch_qprep(const float* Q, long long B, int d, float* qnorm, void* qsplit, unsigned* zero2, int* zeroB,
-                         cudaStream_t s);
+                                int d, const QprepArgs& qa, cudaStream_t s);
 // tensor-core variant (d % 64 == 0): qmap / cmap are 3D bf16 maps over the (hi, lo) splits,
 // dims {d, 2, rows}, box {64, 1, 128}, 128 B swizzle
 size_t coarse_tc_smem_bytes();

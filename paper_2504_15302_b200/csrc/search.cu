@@ -76,14 +76,17 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   cudaEvent_t e0 = te[0], e1 = te[1], e2 = te[2], e3 = h->ev[3], e_plan = h->ev[4], e_off = h->ev[5];
   unsigned long long launches = 0;
   CK(cudaEventRecord(e0, s));
-  // ||q||^2 and the query split (the tensor-core scan's operand) in one pass
-  CK(rd::launch_qprep(d_q, B, d, w.qnorm.p, d % 64 == 0 ? w.qsplit.p : nullptr, w.fails(), w.part_count.p, s));
+  // ||q||^2 and the query split (the tensor-core scan's operand) in one pass; at small batches it
+  // rides in a trailing CTA of the GEMV coarse kernel
+  const rd::QprepArgs qa{d_q, B, d, w.qnorm.p, d % 64 == 0 ? w.qsplit.p : nullptr, w.fails(), w.part_count.p};
   if (rd::coarse_small((int)B)) {
-    CK(rd::launch_coarse_small(d_q, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, h->num_sms, s));
+    CK(rd::launch_coarse_small(d_q, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, qa, s));
   } else if (d % 64 == 0) {
+    CK(rd::launch_qprep(qa, s));
     const CUtensorMap qmap = make_split_map(w.qsplit.p, B, d);
     CK(rd::launch_coarse_tc(qmap, h->cmap, h->cnorm.p, w.Dc.p, (int)B, nl, d, s));
   } else {
+    CK(rd::launch_qprep(qa, s));
     CK(rd::launch_coarse(d_q, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, s));
   }
   w.qthr.ensure(B);
@@ -92,7 +95,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   rd::SelectParams sp{w.Dc.p, d_q, w.qnorm.p, h->centroids.p, w.probes.p, w.fails(), (int)B, nl, nprobe, d, h->cmax,
                       h->d_list_off.p, h->d_res_row0.p, h->arena.p, h->xmax, seed ? w.qthr.p : nullptr, 0};
   h->traced("select", s, sp.dbg, [&] { CK(rd::launch_select(sp, h->stage_rows(B), s)); });
-  launches += 3;
+  launches += rd::coarse_small((int)B) ? 2 : 3;  // (query prep +) coarse + select
   rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
                     w.list_ntile.p, w.list_toff.p, w.list_q.p, w.tiles.p, w.ff_tiles.p, w.meta(), w.counters(),
                     (int)B, nl, nprobe, pl.R, h->tc_scan() ? h->tc_min_q : 1 << 30};
@@ -438,13 +441,15 @@ int rd_probe(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32
     CK(cudaMemcpy(w.q.p, queries, sizeof(float) * B * d, cudaMemcpyHostToDevice));
     CK(cudaMemset(w.fails(), 0, 2 * sizeof(unsigned)));
     w.qsplit.ensure((size_t)B * d);
-    CK(rd::launch_qprep(w.q.p, B, d, w.qnorm.p, d % 64 == 0 ? w.qsplit.p : nullptr, nullptr, nullptr, 0));
+    const rd::QprepArgs qa{w.q.p, B, d, w.qnorm.p, d % 64 == 0 ? w.qsplit.p : nullptr, nullptr, nullptr};
     if (rd::coarse_small((int)B)) {
-      CK(rd::launch_coarse_small(w.q.p, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, h->num_sms, 0));
+      CK(rd::launch_coarse_small(w.q.p, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, qa, 0));
     } else if (d % 64 == 0) {
+      CK(rd::launch_qprep(qa, 0));
       const CUtensorMap qmap = make_split_map(w.qsplit.p, B, d);
       CK(rd::launch_coarse_tc(qmap, h->cmap, h->cnorm.p, w.Dc.p, (int)B, nl, d, 0));
     } else {
+      CK(rd::launch_qprep(qa, 0));
       CK(rd::launch_coarse(w.q.p, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, 0));
     }
     rd::SelectParams sp{w.Dc.p, w.q.p, w.qnorm.p, h->centroids.p, w.probes.p, w.fails(), (int)B, nl, nprobe, d, h->cmax,
