@@ -29,7 +29,7 @@ ENGINE_PATH = os.path.join(_HERE, "lib", "librd_b200.so")
 RD_OK, RD_ERR_INVALID, RD_ERR_INFEASIBLE, RD_ERR_RUNTIME = 0, 2, 3, 4
 DEFAULT_SEED = 250415302
 STREAMS = {"centroids": 0x1001, "assign": 0x1002, "vector_noise": 0x1003,
-           "query_pick": 0x1004, "query_noise": 0x1005}
+           "query_pick": 0x1004, "query_noise": 0x1005, "train_init": 0x1006}
 
 
 class Error(RuntimeError):
