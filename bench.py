@@ -239,10 +239,13 @@ def run_ours(args, cfg):
     nb = args.warmup + args.steps
     qs = [lib.synth_queries(desc, i * B, B)[0] for i in range(nb)]
     dq = [torch.from_numpy(q).cuda() for q in qs]
-    di = torch.empty((B, k), dtype=torch.int64, device="cuda")
-    dd = torch.empty((B, k), dtype=torch.float32, device="cuda")
-    gi = [torch.empty((B, k), dtype=torch.int64, device="cuda") for _ in range(world)]
-    gd = [torch.empty((B, k), dtype=torch.float32, device="cuda") for _ in range(world)]
+    # one packed result buffer per rank ([B, k] ids then [B, k] distances) so the exchange is a
+    # single all-gather of B * k * 12 bytes
+    nbi = B * k * 8
+    res8 = torch.empty(B * k * 12, dtype=torch.uint8, device="cuda")
+    di = res8[:nbi].view(torch.int64).view(B, k)
+    dd = res8[nbi:].view(torch.float32).view(B, k)
+    gres = [torch.empty_like(res8) for _ in range(world)]
     mi = torch.empty((B, k), dtype=torch.int64, device="cuda")
     md = torch.empty((B, k), dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
@@ -251,10 +254,10 @@ def run_ours(args, cfg):
     def step(i):
         idx.search_device(dq[i].data_ptr(), B, nprobe, k, di.data_ptr(), dd.data_ptr(), stream=sptr)
         if world > 1:
-            dist.all_gather(gi, di)
-            dist.all_gather(gd, dd)
+            dist.all_gather(gres, res8)
             if rank == 0:
-                ti, td = torch.stack(gi), torch.stack(gd)
+                g = torch.stack(gres)
+                ti, td = g[:, :nbi].contiguous(), g[:, nbi:].contiguous()  # [G][B][k] ids, distances
                 lib.check(lib.lib.rd_merge_topk_device(world, B, k, ti.data_ptr(), td.data_ptr(), mi.data_ptr(),
                                                        md.data_ptr(), sptr), "merge")
 
@@ -297,12 +300,14 @@ def run_ours(args, cfg):
     def e2e_step(i):
         idx.search_into(hq[i], nprobe, k, hi, hd)
         if world > 1:
-            ti = torch.from_numpy(hi).cuda()
-            td = torch.from_numpy(hd).cuda()
-            dist.all_gather(gi, ti)
-            dist.all_gather(gd, td)
+            di.copy_(torch.from_numpy(hi), non_blocking=True)
+            dd.copy_(torch.from_numpy(hd), non_blocking=True)
+            dist.all_gather(gres, res8)
             if rank == 0:
-                lib.merge_topk(torch.stack(gi).cpu().numpy(), torch.stack(gd).cpu().numpy())
+                g = torch.stack(gres).cpu()
+                gi = g[:, :nbi].contiguous().view(torch.int64).view(world, B, k).numpy()
+                gd = g[:, nbi:].contiguous().view(torch.float32).view(world, B, k).numpy()
+                lib.merge_topk(gi, gd)
 
     for i in range(min(args.warmup, 2)):
         e2e_step(i)
