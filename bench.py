@@ -211,6 +211,8 @@ def run_ours(args, cfg):
     # one stripe of 8, the per-rank work of the 8-GPU job.
     n_total = cfg["n"]
     shards = world if (world > 1 or not cfg.get("total")) else 8
+    if args.stripe_of > 1 and world == 1:  # one rank's share of an N-GPU run, on one GPU
+        shards = args.stripe_of
     desc = lib.desc(n_total, d, cfg["nlist"], shard=rank, num_shards=shards)
     t0 = time.time()
     idx = lib.synthetic_index(desc, device=local)
@@ -415,6 +417,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--stripe-of", type=int, default=0,
+                    help="N = 1 only: run one row stripe of an N-way split (the per-rank work of N GPUs)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = dict(CONFIGS[args.config])

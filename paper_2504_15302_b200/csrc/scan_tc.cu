@@ -39,6 +39,7 @@ constexpr int kStageBytes = kRows * 128;     // 16 KiB: 128 rows x 32 fp32
 constexpr int kBRows = 2 * kTcG;             // B operand rows: q1 (32), q2 (32)
 constexpr int kBSlice = kBRows * 128;        // 8 KiB per 64-dim bf16 slice
 constexpr int kXBufs = 8;                    // TMEM ring of converted stages (32 columns each)
+constexpr int kMaxBSlices = 16;              // 64-dim query-operand slices (d <= 1024)
 static_assert(kXBufs % 2 == 0, "TMEM ring depth must be even");
 constexpr int kThreads = 448;                // 14 warps
 constexpr uint32_t kTmemCols = 512;
@@ -70,8 +71,8 @@ __device__ __forceinline__ Smem carve(unsigned char* raw, int d) {
   s.xempty = s.xfull + kXBufs;
   s.afull = s.xempty + kXBufs;
   s.aempty = s.afull + 2;
-  s.bfull = s.aempty + 2;
-  s.bempty = s.bfull + 1;
+  s.bfull = s.aempty + 2;  // one per 64-dim B slice (kMaxBSlices)
+  s.bempty = s.bfull + kMaxBSlices;
   s.tfull = s.bempty + 1;
   s.tempty = s.tfull + 2;
   s.tring = reinterpret_cast<int*>(s.tempty + 2);
@@ -81,6 +82,18 @@ __device__ __forceinline__ Smem carve(unsigned char* raw, int d) {
   s.edist = s.stage_d + 4 * 32;
   return s;
 }
+
+// profiling only (p.stall != nullptr): cycles a role spends blocked on one barrier
+#define RD_TWAIT(bar, parity, slot)                                  \
+  do {                                                               \
+    if (p.stall) {                                                   \
+      const long long t0_ = clock64();                               \
+      mbar_wait(bar, parity);                                        \
+      stall_acc[slot] += clock64() - t0_;                            \
+    } else {                                                         \
+      mbar_wait(bar, parity);                                        \
+    }                                                                \
+  } while (0)
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // .x = lo -> low 16 bits
@@ -120,7 +133,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.tfull[i], 1);
       mbar_init(&sm.tempty[i], kPre ? 1 + 4 : 1 + 4 + 4 + 4);
     }
-    mbar_init(sm.bfull, 1);
+    for (int i = 0; i < d / 64; ++i) mbar_init(&sm.bfull[i], 1);
     mbar_init(sm.bempty, 1);
     fence_mbar_init();
   }
@@ -130,6 +143,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *sm.tmem_base;
   const int ntiles = *p.ntiles;
+  long long stall_acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const long long t_begin = clock64();
   if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 4 + 1] = gtimer();
 
   // ---------------------------------------------------------------- warp 0: TMA producer
@@ -146,20 +161,63 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int slot = ti & 1;
       if (lane == 0) {
         t = atomicAdd(p.tile_counter, 1);
-        mbar_wait(&sm.tempty[slot], ((ti >> 1) & 1) ^ 1);
+        RD_TWAIT(&sm.tempty[slot], ((ti >> 1) & 1) ^ 1, 0);
         sm.tring[slot] = t < ntiles ? t : -1;
         mbar_arrive(&sm.tfull[slot]);
       }
       t = __shfl_sync(0xffffffffu, t, 0);
       if (t >= ntiles) break;
       const ScanTile T = p.tiles[t];
+      // x stage i of this tile: row tile i / nks, 64- (or 32-) dim slice i % nks; lane 0 issues
+      const int nst = ((T.nrows + kRows - 1) / kRows) * nks;
+      auto issue_x = [&](int i) {
+        const int rt = i / nks, ks = i - rt * nks;
+        const int rows = min(kRows, T.nrows - rt * kRows);
+        const int nb = (rows + 31) >> 5;
+        const int row = (int)(T.src_row + rt * kRows);
+        const int s = u % RS;
+        RD_TWAIT(&sm.empty[s], ((u / RS) & 1) ^ 1, 1);
+        const uint32_t dst = sm.xs + s * RB;
+        if constexpr (kPre) {  // x1 and x2 tiles of a 64-dim slice: 2 x 16 KiB
+          if (nb == 4) {
+            mbar_arrive_expect_tx(&sm.full[s], 2 * kRows * 128);
+            tma_load_3d_u32(dst, &map128, ks * 64, 0, row, &sm.full[s]);
+            tma_load_3d_u32(dst + kRows * 128, &map128, ks * 64, 1, row, &sm.full[s]);
+          } else {
+            mbar_arrive_expect_tx(&sm.full[s], 2 * nb * 4096);
+            for (int b = 0; b < nb; ++b) {
+              tma_load_3d_u32(dst + b * 4096, &map32, ks * 64, 0, row + b * 32, &sm.full[s]);
+              tma_load_3d_u32(dst + kRows * 128 + b * 4096, &map32, ks * 64, 1, row + b * 32, &sm.full[s]);
+            }
+          }
+        } else {
+          if (nb == 4) {
+            mbar_arrive_expect_tx(&sm.full[s], kStageBytes);
+            tma_load_2d_u32(dst, &map128, ks * 32, row, &sm.full[s]);
+          } else {
+            mbar_arrive_expect_tx(&sm.full[s], nb * 4096);
+            for (int b = 0; b < nb; ++b) tma_load_2d_u32(dst + b * 4096, &map32, ks * 32, row + b * 32, &sm.full[s]);
+          }
+        }
+        ++u;
+      };
+      // With early_x, the first ring's worth of x stages goes out before waiting for the B operand
+      // to be free: those slots free up as the previous tile's last MMAs retire, so HBM keeps
+      // streaming across the tile boundary (matters when tiles are short).
+      const int pre = p.early_x ? min(RS, nst) : 0;
+      if (lane == 0)
+        for (int i = 0; i < pre; ++i) issue_x(i);
+      __syncwarp();
       // ---- B operand by TMA gather4: rows 0-31 q1, 32-63 q2 of the tile's queries (qsplit row
       // 2*qid + part); padding rows repeat the last query (their D columns are ignored)
-      mbar_wait(sm.bempty, (ti & 1) ^ 1);
+      RD_TWAIT(sm.bempty, (ti & 1) ^ 1, 2);
       // only the quads holding real queries are loaded; the others keep stale rows whose D
       // columns the epilogue never reads
       const int qq = (T.nq + 3) >> 2;  // quads per part
-      if (lane == 0) mbar_arrive_expect_tx(sm.bfull, (uint32_t)(nslices * 2 * qq * 512));
+      // one barrier per 64-dim slice: the MMAs of the tile's first row tile start as soon as
+      // their own slice of the query operand has landed instead of after the whole gather
+      if (lane == 0)
+        for (int sl = 0; sl < nslices; ++sl) mbar_arrive_expect_tx(&sm.bfull[sl], (uint32_t)(2 * qq * 512));
       __syncwarp();
       for (int gi = lane; gi < nslices * 2 * qq; gi += 32) {
         const int slice = gi / (2 * qq), qi = gi % (2 * qq);
@@ -172,41 +230,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int g = min(g0 + i, T.nq - 1);
           r[i] = 2 * __ldg(p.list_q + T.qoff + g) + part;
         }
-        tma_gather4_u32(sm.bs + slice * kBSlice + quad * 512, &qmap, slice * 64, r[0], r[1], r[2], r[3], sm.bfull);
+        tma_gather4_u32(sm.bs + slice * kBSlice + quad * 512, &qmap, slice * 64, r[0], r[1], r[2], r[3],
+                        &sm.bfull[slice]);
       }
-      if (lane == 0) {
-        for (int rt = 0; rt * kRows < T.nrows; ++rt) {
-          const int rows = min(kRows, T.nrows - rt * kRows);
-          const int nb = (rows + 31) >> 5;
-          const int row = (int)(T.src_row + rt * kRows);
-          for (int ks = 0; ks < nks; ++ks, ++u) {
-            const int s = u % RS;
-            mbar_wait(&sm.empty[s], ((u / RS) & 1) ^ 1);
-            const uint32_t dst = sm.xs + s * RB;
-            if constexpr (kPre) {  // x1 and x2 tiles of a 64-dim slice: 2 x 16 KiB
-              if (nb == 4) {
-                mbar_arrive_expect_tx(&sm.full[s], 2 * kRows * 128);
-                tma_load_3d_u32(dst, &map128, ks * 64, 0, row, &sm.full[s]);
-                tma_load_3d_u32(dst + kRows * 128, &map128, ks * 64, 1, row, &sm.full[s]);
-              } else {
-                mbar_arrive_expect_tx(&sm.full[s], 2 * nb * 4096);
-                for (int b = 0; b < nb; ++b) {
-                  tma_load_3d_u32(dst + b * 4096, &map32, ks * 64, 0, row + b * 32, &sm.full[s]);
-                  tma_load_3d_u32(dst + kRows * 128 + b * 4096, &map32, ks * 64, 1, row + b * 32, &sm.full[s]);
-                }
-              }
-            } else {
-              if (nb == 4) {
-                mbar_arrive_expect_tx(&sm.full[s], kStageBytes);
-                tma_load_2d_u32(dst, &map128, ks * 32, row, &sm.full[s]);
-              } else {
-                mbar_arrive_expect_tx(&sm.full[s], nb * 4096);
-                for (int b = 0; b < nb; ++b) tma_load_2d_u32(dst + b * 4096, &map32, ks * 32, row + b * 32, &sm.full[s]);
-              }
-            }
-          }
-        }
-      }
+      if (lane == 0)
+        for (int i = pre; i < nst; ++i) issue_x(i);
       __syncwarp();
     }
   }
@@ -218,23 +246,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t u = 0, rtc = 0;
     for (uint32_t ti = 0;; ++ti) {
       const int slot = ti & 1;
-      mbar_wait(&sm.tfull[slot], (ti >> 1) & 1);
+      RD_TWAIT(&sm.tfull[slot], (ti >> 1) & 1, 3);
       const int t = sm.tring[slot];
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.tempty[slot]);
       if (t < 0) break;
       const ScanTile T = p.tiles[t];
-      mbar_wait(sm.bfull, ti & 1);  // this tile's queries are in the B operand
       if (p.dbg && ti == 0 && lane == 0) p.dbg[blockIdx.x * 4 + 2] = gtimer();
       for (int rt = 0; rt * kRows < T.nrows; ++rt, ++rtc) {
         const int a = rtc & 1;
-        mbar_wait(&sm.aempty[a], ((rtc >> 1) & 1) ^ 1);
+        RD_TWAIT(&sm.aempty[a], ((rtc >> 1) & 1) ^ 1, 5);
         tc_fence_after();
         const uint32_t dacc = tmem + a * kAccCols;
         for (int ks = 0; ks < nks; ++ks, ++u) {
+          if (rt == 0 && (kPre || (ks & 1) == 0))  // this slice of the tile's queries has landed
+            RD_TWAIT(&sm.bfull[kPre ? ks : ks >> 1], ti & 1, 4);
           if constexpr (kPre) {
             const int s = u % RS;
-            mbar_wait(&sm.full[s], (u / RS) & 1);
+            RD_TWAIT(&sm.full[s], (u / RS) & 1, 6);
             tc_fence_after();
             if (lane == 0) {
               const unsigned char* st = reinterpret_cast<unsigned char*>(smem_raw) + (sm.xs - smem_u32(smem_raw)) +
@@ -357,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t rtc = 0;
     for (uint32_t ti = 0;; ++ti) {
       const int slot = ti & 1;
-      mbar_wait(&sm.tfull[slot], (ti >> 1) & 1);
+      RD_TWAIT(&sm.tfull[slot], (ti >> 1) & 1, 7);
       const int t = sm.tring[slot];
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.tempty[slot]);
@@ -381,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       for (int rt = 0; rt * kRows < T.nrows; ++rt, ++rtc) {
         const int a = rtc & 1;
-        mbar_wait(&sm.afull[a], (rtc >> 1) & 1);
+        RD_TWAIT(&sm.afull[a], (rtc >> 1) & 1, 8);
         tc_fence_after();
         const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + a * kAccCols;
         uint32_t d1[32], d2[32], d3[32];
@@ -452,21 +481,34 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      // per-query top-32 of this tile -> one partial list per query
+      // per-query top-32 of this tile -> one partial list per query. The slot reservations
+      // (atomicAdd on the query's partial count) and threshold updates of the warp's queries are
+      // issued together, one lane per query, so a tile end costs one atomic round trip rather than
+      // one per query (short tiles made that the scan's per-tile overhead).
+      int myqid = 0, myps = 0;
+      bool myhas = false;
+      float myl31 = kInf;
 #pragma unroll
       for (int j = 0; j < kOwn; ++j) {
         const int g = ew + 4 * j;
-        if (g >= nq) break;
-        const int qid = __ldg(p.list_q + T.qoff + g);
         const float l31 = __shfl_sync(0xffffffffu, ld[j], 31);
-        if (__shfl_sync(0xffffffffu, ld[j], 0) == kInf) continue;  // nothing survived: no partial
-        int ps = 0;
-        if (lane == 0) {
-          ps = atomicAdd(p.part_count + qid, 1);
-          if (l31 != kInf) atomicMin(p.qthr + qid, f2ord(l31));
+        const bool has = g < nq && __shfl_sync(0xffffffffu, ld[j], 0) != kInf;  // something survived
+        if (lane == j) {
+          myhas = has;
+          myl31 = l31;
+          if (g < nq) myqid = __ldg(p.list_q + T.qoff + g);
         }
-        ps = __shfl_sync(0xffffffffu, ps, 0);
-        if (ps < p.part_cap) {
+      }
+      if (myhas) {
+        myps = atomicAdd(p.part_count + myqid, 1);
+        if (myl31 != kInf) atomicMin(p.qthr + myqid, f2ord(myl31));
+      }
+#pragma unroll
+      for (int j = 0; j < kOwn; ++j) {
+        const int ps = __shfl_sync(0xffffffffu, myps, j);
+        const int qid = __shfl_sync(0xffffffffu, myqid, j);
+        const bool has = __shfl_sync(0xffffffffu, myhas ? 1 : 0, j) != 0;
+        if (has && ps < p.part_cap) {
           const size_t o = ((size_t)qid * p.part_cap + ps) * kTopK + lane;
           p.part_dist[o] = ld[j];
           p.part_row[o] = lk[j] == kNoKey ? -1 : (int)lk[j];
@@ -476,6 +518,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
 done:
+  if (p.stall && (threadIdx.x & 31) == 0) {  // lane 0 of each role's first warp reports its waits
+    const int w = threadIdx.x >> 5;
+    unsigned long long* o = p.stall + (size_t)blockIdx.x * 12;
+    if (w == 0) {
+      o[0] = stall_acc[0];
+      o[1] = stall_acc[1];
+      o[2] = stall_acc[2];
+      o[9] = clock64() - t_begin;
+    } else if (w == 1) {
+      o[3] = stall_acc[3];
+      o[4] = stall_acc[4];
+      o[5] = stall_acc[5];
+      o[6] = stall_acc[6];
+    } else if (w == 6) {
+      o[7] = stall_acc[7];
+      o[8] = stall_acc[8];
+    }
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -503,7 +563,7 @@ __global__ void qsplit_kernel(const float* __restrict__ Q, __nv_bfloat16* __rest
 
 size_t scan_tc_smem_bytes(int d) {
   return 1024 + (size_t)kStages * kStageBytes + (size_t)(d / 64) * kBSlice +
-         (2 * kStages + 2 * kXBufs + 10) * sizeof(uint64_t) + 2 * sizeof(int) + 16 + 4 * 32 * 12 +
+         (2 * kStages + 2 * kXBufs + 9 + kMaxBSlices) * sizeof(uint64_t) + 2 * sizeof(int) + 16 + 4 * 32 * 12 +
          (size_t)kTcG * kRows * sizeof(float) + 64;
 }
 

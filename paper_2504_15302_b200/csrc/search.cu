@@ -115,7 +115,8 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   rd::ScanParams sc{w.ff_tiles.p, w.meta() + 2, w.meta() + 3, d_q, w.qnorm.p, w.list_q.p, h->xnorm.p,
                     w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p};
   rd::TcScanParams tc{w.tiles.p, w.meta(), w.meta() + 1, w.qsplit.p, w.qnorm.p, w.list_q.p, h->xnorm.p,
-                      w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p, h->debug_skip};
+                      w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p, h->debug_skip,
+                      h->early_x};
   if (!h->tc_scan() || h->tc_min_q > 1) {  // FFMA tiles exist only in these cases
     CK(rd::launch_scan(h->map256, h->map32, sc, h->num_sms, s));
     launches += 1;
@@ -126,9 +127,29 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
       CK(cudaMemsetAsync(h->dbg_scan.p, 0, 8 * 4 * (size_t)h->num_sms, s));
       tc.dbg = h->dbg_scan.p;
     }
+    const bool stall = std::getenv("RD_DEBUG_STALL") != nullptr;  // profiling only
+    if (stall) {
+      if (h->dbg_stall.n < 12 * (size_t)h->num_sms) h->dbg_stall.alloc(12 * (size_t)h->num_sms);
+      CK(cudaMemsetAsync(h->dbg_stall.p, 0, 8 * 12 * (size_t)h->num_sms, s));
+      tc.stall = h->dbg_stall.p;
+    }
     CK(rd::launch_scan_tc(h->presplit ? h->xmap128 : h->map128, h->presplit ? h->xmap32 : h->map32, gmap, tc,
                           h->num_sms, s, h->presplit));
     launches += 1;
+    if (stall) {
+      std::vector<unsigned long long> v(12 * (size_t)h->num_sms);
+      CK(cudaMemcpyAsync(v.data(), h->dbg_stall.p, 8 * v.size(), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      static const char* nm[10] = {"P.tempty", "P.empty", "P.bempty", "M.tfull", "M.bfull", "M.aempty", "M.full",
+                                   "E.tfull", "E.afull", "total"};
+      fprintf(stderr, "scan stall cycles (mean over CTAs):");
+      for (int k2 = 0; k2 < 10; ++k2) {
+        double m = 0;
+        for (int c = 0; c < h->num_sms; ++c) m += (double)v[12 * c + k2] / h->num_sms;
+        fprintf(stderr, " %s=%.0f", nm[k2], m);
+      }
+      fprintf(stderr, "\n");
+    }
     if (h->dbg_ts) {
       std::vector<unsigned long long> t(4 * (size_t)h->num_sms);
       CK(cudaMemcpyAsync(t.data(), h->dbg_scan.p, 8 * t.size(), cudaMemcpyDeviceToHost, s));

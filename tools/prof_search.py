@@ -19,10 +19,11 @@ ap.add_argument("--nprobe", type=int, default=64)
 ap.add_argument("--k", type=int, default=10)
 ap.add_argument("--searches", type=int, default=3)
 ap.add_argument("--offload", type=float, default=0.0)
+ap.add_argument("--stripe-of", type=int, default=1)
 args = ap.parse_args()
 torch.cuda.init()
 lib = engine()
-desc = lib.desc(args.n, 768, args.nlist)
+desc = lib.desc(args.n, 768, args.nlist, num_shards=args.stripe_of)
 idx = lib.synthetic_index(desc)
 if args.offload:
     idx.place(offload_fraction=args.offload)
