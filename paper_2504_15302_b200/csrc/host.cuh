@@ -246,7 +246,15 @@ struct rd_index {
   bool no_inner_events = std::getenv("RD_NO_INNER_EVENTS") != nullptr;  // A/B: no per-stage timing events
   // the tensor-core scan stages 64-dim bf16 query slices of up to 32 queries in shared memory:
   // d % 64 == 0 and d <= 896 (beyond, its B operand does not fit next to the x ring); else FFMA
-  bool tc_scan() const { return d % 64 == 0 && rd::scan_tc_smem_bytes(d) <= 227 * 1024; }
+  bool tc_scan() const { return d % 64 == 0 && rd::scan_tc_smem_bytes(d, 32) <= 227 * 1024; }
+  // Tile width of the tensor-core scan for a batch: 16-query tiles (deeper x ring) when lists are
+  // probed by few queries, 32 when the average probed list sees more than 8 (RD_TC_G overrides)
+  int tc_g_for(long long B, int nprobe) const {
+    if (tc_g_force == 16 || tc_g_force == 32) return tc_g_force;
+    const double per_list = (double)B * std::min(nprobe, nlist) / std::max(1, nlist);
+    return per_list <= 8.0 ? 16 : 32;
+  }
+  int tc_g_force = std::getenv("RD_TC_G") ? std::atoi(std::getenv("RD_TC_G")) : 0;
   bool stage_rows(long long B) const { return B <= (stage_max_b >= 0 ? stage_max_b : 2LL * num_sms); }
   long long n = 0;
   int d = 0, nlist = 0;

@@ -40,8 +40,7 @@ constexpr int kScanStageBytes = kScanRows * 128;
 constexpr int kCoarseExtra = 32;    // approximate coarse candidates beyond nprobe
 // tensor-core scan (N5)
 constexpr int kTcRows = 128;        // UMMA M: rows per accumulator tile
-constexpr int kTcStages = 6;        // smem ring depth (16 KiB per stage)
-constexpr int kTcG = 32;            // queries per tensor-core tile (B operand: 32 q1 + 32 q2 rows)
+constexpr int kTcGMax = 32;         // widest tensor-core tile (queries); 16- and 32-wide variants exist
 constexpr int kTcMinQ = 1;          // lists probed by >= this many queries use the tensor cores
 constexpr int kPartsPerTile = 1;    // partial lists one scan tile emits per query
 
@@ -92,11 +91,12 @@ struct TcScanParams {
 };
 
 size_t scan_smem_bytes(int d);
-size_t scan_tc_smem_bytes(int d);
+size_t scan_tc_smem_bytes(int d, int tc_g);
 // qmap: 2D bf16 map over the qsplit buffer as [2B rows x d], box {64, 1} (gather4 source)
 // presplit: map128 / map32 are 3D bf16 maps over the pre-split [rows][2][d] arena, box {64, 1, 128|32}
+// tc_g: queries per tile, 16 or 32 (the planner grouped the tiles with the same width)
 cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, const CUtensorMap& qmap,
-                           const TcScanParams& p, int grid, cudaStream_t s, bool presplit);
+                           const TcScanParams& p, int grid, cudaStream_t s, bool presplit, int tc_g);
 cudaError_t launch_qsplit(const float* Q, void* out, long long B, int d, cudaStream_t s);
 cudaError_t launch_scan(const CUtensorMap& map256, const CUtensorMap& map32, const ScanParams& p,
                         int grid, cudaStream_t s);
@@ -165,6 +165,7 @@ struct PlanParams {
   int* meta;                  // [0] #tc tiles, [1] tc counter, [2] #ff tiles, [3] ff counter
   unsigned long long* counters;  // [0] unique lists, [1] resident rows probed, [2] offloaded rows probed
   int B, nlist, nprobe, R, tc_min_q;
+  int tc_g;                   // queries per tensor-core tile (16 or 32)
   unsigned long long* dbg = nullptr;  // RD_DEBUG_TS: globaltimer checkpoints of CTA 0
 };
 cudaError_t launch_plan(const PlanParams& p, cudaStream_t s);

@@ -23,11 +23,11 @@ __global__ void invert_set_kernel(const int* __restrict__ probes, unsigned* __re
 }
 
 // Query groups of one list. A list probed by >= tc_min_q queries is scanned once per
-// balanced group of <= kTcG queries on the tensor cores (almost always a single group, so the
+// balanced group of <= tc_g queries on the tensor cores (usually a single group, so the
 // list's bytes are read once); sparser lists form one FFMA group (<= tc_min_q - 1 <= kScanG).
-__device__ __forceinline__ void group_split(int nq, int tc_min_q, int& ntc, int& nff) {
+__device__ __forceinline__ void group_split(int nq, int tc_min_q, int tc_g, int& ntc, int& nff) {
   if (nq >= tc_min_q) {
-    ntc = (nq + kTcG - 1) / kTcG;
+    ntc = (nq + tc_g - 1) / tc_g;
     nff = 0;
   } else {
     ntc = 0;
@@ -86,7 +86,7 @@ __global__ void list_count_kernel(const PlanParams p) {
     int ntc = 0, nff = 0;
     if (c > 0 && len > 0 && p.res_row0[warp] >= 0) {
       const int chunks = ((int)len + p.R - 1) / p.R;  // 32-bit: rows per list < 2^31
-      group_split(c, p.tc_min_q, ntc, nff);
+      group_split(c, p.tc_min_q, p.tc_g, ntc, nff);
       ntc *= chunks;
       nff *= chunks;
     }
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_fused_kernel(const PlanPara
         cc[sl >= 0 ? 1 : 2] += len;
         if (sl >= 0 && len > 0) {
           chunks = (len + p.R - 1) / p.R;
-          group_split(v[0], p.tc_min_q, v[1], v[2]);
+          group_split(v[0], p.tc_min_q, p.tc_g, v[1], v[2]);
           src0 = p.res_row0[j];
           g0 = p.list_off[j];
         }
@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(kSmallPlanThreads) plan_small_kernel(const Pla
     src0 = p.res_row0[l];
     if (src0 >= 0 && len > 0) {
       chunks = (len + p.R - 1) / p.R;
-      group_split(nq, p.tc_min_q, ntc, nff);
+      group_split(nq, p.tc_min_q, p.tc_g, ntc, nff);
     }
   }
   if (tid < valid) p.list_q[tid] = (int)(mine & 0xffffffffu);

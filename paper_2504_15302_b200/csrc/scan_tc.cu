@@ -31,13 +31,21 @@ namespace rd {
 namespace {
 
 constexpr int kRows = kTcRows;               // 128 = UMMA M
-constexpr int kStages = kTcStages;           // x ring depth
-// converter group g owns stages / TMEM buffers with u % 2 == g; an odd ring depth would let one
-// group wait on a phase two ahead of the other group's and alias its mbarrier parity
-static_assert(kTcStages % 2 == 0, "x ring depth must be even");
 constexpr int kStageBytes = kRows * 128;     // 16 KiB: 128 rows x 32 fp32
-constexpr int kBRows = 2 * kTcG;             // B operand rows: q1 (32), q2 (32)
-constexpr int kBSlice = kBRows * 128;        // 8 KiB per 64-dim bf16 slice
+// Tile width: kG queries per tile (B operand rows: kG q1 + kG q2, 64 dims per slice). The x ring
+// takes what shared memory the B operand leaves: 16-query tiles get a 5 x 32 KiB pre-split ring,
+// 32-query tiles 3 x 32 KiB (search.cu picks the width from the batch's queries per list).
+template <int kG>
+struct TcGeom {
+  static constexpr int G = kG;
+  static constexpr int Stages = kG == 16 ? 10 : 6;  // 16 KiB stages (pre-split stages pair them)
+  static constexpr int BRows = 2 * kG;
+  static constexpr int BSlice = BRows * 128;
+  // converter group g owns stages / TMEM buffers with u % 2 == g; an odd ring depth would let one
+  // group wait on a phase two ahead of the other group's and alias its mbarrier parity
+  static_assert(Stages % 2 == 0, "x ring depth must be even");
+  static_assert(kG == 16 || kG == 32, "tile width");
+};
 constexpr int kXBufs = 8;                    // TMEM ring of converted stages (32 columns each)
 constexpr int kMaxBSlices = 16;              // 64-dim query-operand slices (d <= 1024)
 static_assert(kXBufs % 2 == 0, "TMEM ring depth must be even");
@@ -59,7 +67,9 @@ struct Smem {
   long long* stage_k; // [4][32]
 };
 
+template <int kG>
 __device__ __forceinline__ Smem carve(unsigned char* raw, int d) {
+  constexpr int kStages = TcGeom<kG>::Stages, kBSlice = TcGeom<kG>::BSlice;
   Smem s;
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
   s.xs = smem_u32(base);
@@ -104,15 +114,17 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 // kPre = true : pre-split bf16 (x1, x2) arena ([rows][2][d], built with the index); the producer TMA-loads
 //               both 64-dim tiles of a stage straight into 128B-swizzled smem and the MMAs read A from
 //               smem (SS) — no conversion on the scan path; converter warps are idle.
-template <bool kPre>
+template <bool kPre, int kG>
 __global__ void __launch_bounds__(kThreads, 1)
     ivf_scan_tc_kernel(const __grid_constant__ CUtensorMap map128, const __grid_constant__ CUtensorMap map32,
                        const __grid_constant__ CUtensorMap qmap, const TcScanParams p) {
+  constexpr int kTcG = kG, kStages = TcGeom<kG>::Stages, kBRows = TcGeom<kG>::BRows,
+                kBSlice = TcGeom<kG>::BSlice;
   RD_PDL_PROLOGUE();
   if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 4 + 0] = gtimer();
   extern __shared__ unsigned char smem_raw[];
   const int d = p.d, nks = kPre ? d / 64 : d / 32;
-  const Smem sm = carve(smem_raw, d);
+  const Smem sm = carve<kG>(smem_raw, d);
   // ring geometry: the same 96 KiB hold 6 x 16 KiB fp32 stages or 3 x 32 KiB pre-split stages
   constexpr int RS = kPre ? kStages / 2 : kStages;
   constexpr int RB = kPre ? 2 * kStageBytes : kStageBytes;
@@ -413,13 +425,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         RD_TWAIT(&sm.afull[a], (rtc >> 1) & 1, 8);
         tc_fence_after();
         const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + a * kAccCols;
-        uint32_t d1[32], d2[32], d3[32];
-        RD_TMEM_LD16(ta, d1);
-        RD_TMEM_LD16(ta + 16, (d1 + 16));
-        RD_TMEM_LD16(ta + 32, d2);
-        RD_TMEM_LD16(ta + 48, (d2 + 16));
-        RD_TMEM_LD16(ta + 64, d3);
-        RD_TMEM_LD16(ta + 80, (d3 + 16));
+        // D_a = [x1.q1 | x1.q2] in columns [0, 2 kTcG), D_b = x2.q1 in [2 kTcG, 3 kTcG)
+        uint32_t d1[kTcG], d2[kTcG], d3[kTcG];
+#pragma unroll
+        for (int c = 0; c < kTcG; c += 16) {
+          RD_TMEM_LD16(ta + c, (d1 + c));
+          RD_TMEM_LD16(ta + kTcG + c, (d2 + c));
+          RD_TMEM_LD16(ta + 2 * kTcG + c, (d3 + c));
+        }
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
@@ -561,20 +574,27 @@ __global__ void qsplit_kernel(const float* __restrict__ Q, __nv_bfloat16* __rest
 
 }  // namespace
 
-size_t scan_tc_smem_bytes(int d) {
-  return 1024 + (size_t)kStages * kStageBytes + (size_t)(d / 64) * kBSlice +
-         (2 * kStages + 2 * kXBufs + 9 + kMaxBSlices) * sizeof(uint64_t) + 2 * sizeof(int) + 16 + 4 * 32 * 12 +
-         (size_t)kTcG * kRows * sizeof(float) + 64;
+size_t scan_tc_smem_bytes(int d, int tc_g) {
+  const size_t stages = tc_g == 16 ? TcGeom<16>::Stages : TcGeom<32>::Stages;
+  const size_t bslice = tc_g == 16 ? TcGeom<16>::BSlice : TcGeom<32>::BSlice;
+  return 1024 + stages * kStageBytes + (size_t)(d / 64) * bslice +
+         (2 * stages + 2 * kXBufs + 9 + kMaxBSlices) * sizeof(uint64_t) + 2 * sizeof(int) + 16 + 4 * 32 * 12 +
+         (size_t)tc_g * kRows * sizeof(float) + 64;
 }
 
 cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, const CUtensorMap& qmap,
-                           const TcScanParams& p, int grid, cudaStream_t s, bool presplit) {
-  if (p.d % 64 != 0) return cudaErrorInvalidValue;
-  const size_t smem = scan_tc_smem_bytes(p.d);
+                           const TcScanParams& p, int grid, cudaStream_t s, bool presplit, int tc_g) {
+  if (p.d % 64 != 0 || (tc_g != 16 && tc_g != 32)) return cudaErrorInvalidValue;
+  const size_t smem = scan_tc_smem_bytes(p.d, tc_g);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  if (tc_g == 16) {
+    if (presplit)
+      return launch_k(ivf_scan_tc_kernel<true, 16>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+    return launch_k(ivf_scan_tc_kernel<false, 16>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+  }
   if (presplit)
-    return launch_k(ivf_scan_tc_kernel<true>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
-  return launch_k(ivf_scan_tc_kernel<false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+    return launch_k(ivf_scan_tc_kernel<true, 32>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+  return launch_k(ivf_scan_tc_kernel<false, 32>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
 }
 
 cudaError_t launch_qsplit(const float* Q, void* out, long long B, int d, cudaStream_t s) {

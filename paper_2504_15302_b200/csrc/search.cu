@@ -52,6 +52,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   auto& w = h->ws;
   const int nl = h->nlist, d = h->d;
   const Plan pl = make_plan(h, B, nprobe);
+  const int tc_g = h->tc_g_for(B, nprobe);  // queries per tensor-core tile
   const int W = (int)((B + 31) / 32);
   w.qnorm.ensure(B);
   w.Dc.ensure((size_t)B * nl);
@@ -98,7 +99,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   launches += rd::coarse_small((int)B) ? 2 : 3;  // (query prep +) coarse + select
   rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
                     w.list_ntile.p, w.list_toff.p, w.list_q.p, w.tiles.p, w.ff_tiles.p, w.meta(), w.counters(),
-                    (int)B, nl, nprobe, pl.R, h->tc_scan() ? h->tc_min_q : 1 << 30};
+                    (int)B, nl, nprobe, pl.R, h->tc_scan() ? h->tc_min_q : 1 << 30, tc_g};
   h->traced("plan", s, pp.dbg, [&] { CK(rd::launch_plan(pp, s)); });
   launches += rd::plan_small_ok((int)B, nprobe) || rd::plan_fused_ok((int)B, nl) ? 1 : 4;
   if (!h->no_inner_events) CK(cudaEventRecord(e1, s));
@@ -134,7 +135,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
       tc.stall = h->dbg_stall.p;
     }
     CK(rd::launch_scan_tc(h->presplit ? h->xmap128 : h->map128, h->presplit ? h->xmap32 : h->map32, gmap, tc,
-                          h->num_sms, s, h->presplit));
+                          h->num_sms, s, h->presplit, tc_g));
     launches += 1;
     if (stall) {
       std::vector<unsigned long long> v(12 * (size_t)h->num_sms);
@@ -199,7 +200,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
         const long long len = h->list_off[l + 1] - h->list_off[l];
         const int nq = w.h_nq.p[l];
         const bool tcl = nq >= h->tc_min_q && h->tc_scan();
-        const int ngr = tcl ? (nq + rd::kTcG - 1) / rd::kTcG : (nq + rd::kScanG - 1) / rd::kScanG;
+        const int ngr = tcl ? (nq + tc_g - 1) / tc_g : (nq + rd::kScanG - 1) / rd::kScanG;
         for (long long c = 0; c * pl.R < len; ++c)
           for (int g = 0; g < ngr; ++g) {
             rd::ScanTile T;
@@ -285,7 +286,8 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
           to.tiles = w.off_tiles.p + tstart[bi];
           to.ntiles = dmeta.p + 4 * bi + 0;
           to.tile_counter = dmeta.p + 4 * bi + 1;
-          CK(rd::launch_scan_tc(h->smap128, h->smap32, gmap, to, std::min(h->num_sms, nt_tc), h->off_stream, false));
+          CK(rd::launch_scan_tc(h->smap128, h->smap32, gmap, to, std::min(h->num_sms, nt_tc), h->off_stream, false,
+                                tc_g));
           launches += 1;
         }
         CK(cudaEventRecord(h->slot_done[slot], h->off_stream));
