@@ -247,10 +247,13 @@ struct rd_index {
   // the tensor-core scan stages 64-dim bf16 query slices of up to 32 queries in shared memory:
   // d % 64 == 0 and d <= 896 (beyond, its B operand does not fit next to the x ring); else FFMA
   bool tc_scan() const { return d % 64 == 0 && rd::scan_tc_smem_bytes(d, 32) <= 227 * 1024; }
-  // Tile width of the tensor-core scan for a batch: 16-query tiles (deeper x ring) when lists are
-  // probed by few queries, 32 when the average probed list sees more than 8 (RD_TC_G overrides)
-  int tc_g_for(long long B, int nprobe) const {
+  // Tensor-core tile width for a batch: 16-query tiles (the 16-wide scan's deeper ring) when the
+  // probed lists see <= 8 queries on average, else 32-query tiles (lists read once). Measured: mixing
+  // both widths in one batch (RD_TC_G=1: lists of <= 16 queries narrow, others wide) does not beat
+  // all-wide at B = 1024 and loses at short lists. RD_TC_G=16|32 forces one width.
+  int tc_mode_for(long long B, int nprobe) const {
     if (tc_g_force == 16 || tc_g_force == 32) return tc_g_force;
+    if (tc_g_force == 1) return 0;
     const double per_list = (double)B * std::min(nprobe, nlist) / std::max(1, nlist);
     return per_list <= 8.0 ? 16 : 32;
   }
@@ -293,14 +296,14 @@ struct rd_index {
     DBuf<float> qnorm, Dc, q, qsplit;
     DBuf<int> probes, list_nq, list_qoff, list_ntile, list_toff, list_q, part_count, part_row, off_meta;
     DBuf<unsigned> bitmap, fb_ctr;
-    DBuf<rd::ScanTile> tiles, ff_tiles, off_tiles;
+    DBuf<rd::ScanTile> tiles, tiles16, ff_tiles, off_tiles;  // wide / narrow tensor-core, FFMA, offloaded
     DBuf<float> part_dist;
     DBuf<long long> fb_id;
     DBuf<int> fail_list, qthr;
     DBuf<float> fb_dist;
     HBuf<int> h_nq, h_qoff, h_meta;
     // per-search counters in one block so a synced search reads them back with one copy:
-    // [0, 24) counters (u64 x 3), [24, 32) fails (u32 x 2), [32, 48) meta (i32 x 4); the host path
+    // [0, 24) counters (u64 x 3), [24, 32) fails (u32 x 2), [32, 56) meta (i32 x 6); the host path
     // places its result ids / distances right after (kStatBytes) and copies everything at once
     DBuf<char> blk;
     HBuf<char> h_blk;

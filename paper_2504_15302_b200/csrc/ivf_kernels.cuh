@@ -149,6 +149,11 @@ struct SelectParams {
 // stage: q and candidate rows go through shared memory (latency-bound small batches)
 cudaError_t launch_select(const SelectParams& p, bool stage, cudaStream_t s);
 
+// Scan tile categories (plan.cu): tensor-core tiles of <= 16 queries (16-wide scan), of <= 32
+// queries (32-wide scan), and FFMA tiles.
+constexpr int kTileCats = 3;
+constexpr int kCatNarrow = 0, kCatWide = 1, kCatFfma = 2;
+
 struct PlanParams {
   const int* probes;          // B x nprobe
   unsigned* bitmap;           // nlist x W
@@ -157,15 +162,14 @@ struct PlanParams {
   const long long* res_row0;  // nlist: row in the resident arena, -1 = offloaded
   int* list_nq;               // nlist
   int* list_qoff;             // nlist
-  int* list_ntile;            // 2 x nlist: resident tensor-core tiles, then FFMA tiles
-  int* list_toff;             // 2 x nlist
+  int* list_ntile;            // kTileCats x nlist: resident tiles per category
+  int* list_toff;             // kTileCats x nlist
   int* list_q;                // B x nprobe
-  ScanTile* tiles;            // tensor-core tiles
-  ScanTile* ff_tiles;         // FFMA tiles
-  int* meta;                  // [0] #tc tiles, [1] tc counter, [2] #ff tiles, [3] ff counter
+  ScanTile* tiles[kTileCats]; // tile arrays per category
+  int* meta;                  // per category c: [2c] #tiles, [2c + 1] the scan's tile counter
   unsigned long long* counters;  // [0] unique lists, [1] resident rows probed, [2] offloaded rows probed
   int B, nlist, nprobe, R, tc_min_q;
-  int tc_g;                   // queries per tensor-core tile (16 or 32)
+  int tc_mode;                // 0: lists of <= 16 queries narrow, others wide; 16 / 32: one width
   unsigned long long* dbg = nullptr;  // RD_DEBUG_TS: globaltimer checkpoints of CTA 0
 };
 cudaError_t launch_plan(const PlanParams& p, cudaStream_t s);

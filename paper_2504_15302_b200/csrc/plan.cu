@@ -1,11 +1,13 @@
 // plan.cu — N3 probe inversion and scan work planning (sm_100a).
 //
-// The B x nprobe probe table is inverted into per-list query groups through a
-// list x query bitmap (so queries within a list come out in ascending id,
-// deterministically), then every probed, HBM-resident list is cut into scan
-// tiles of <= R rows x <= 16 queries. Tiles of one list are adjacent so the
-// query groups of a chunk hit L2 for each other. Offloaded lists get no device
-// tiles here; the host plans them as their bytes are staged (search.cu).
+// The B x nprobe probe table is inverted into per-list query groups (queries within a list in
+// ascending id, deterministically), then every probed, HBM-resident list is cut into scan tiles of
+// <= R rows x one query group. Tiles fall in three categories, each with its own array and kernel:
+//   kCatNarrow  tensor-core tiles of <= 16 queries (the 16-wide scan: deeper x ring)
+//   kCatWide    tensor-core tiles of <= 32 queries (the 32-wide scan)
+//   kCatFfma    FFMA tiles of <= kScanG queries (d % 64 != 0, d > 896, or RD_TC_MIN_Q)
+// Tiles of one list are adjacent so the query groups of a chunk hit L2 for each other. Offloaded
+// lists get no device tiles here; the host plans them as their bytes are staged (search.cu).
 #include "ivf_kernels.cuh"
 #include "rd_device.cuh"
 
@@ -22,56 +24,63 @@ __global__ void invert_set_kernel(const int* __restrict__ probes, unsigned* __re
   if (l >= 0) atomicOr(bitmap + (size_t)l * W + (b >> 5), 1u << (b & 31));
 }
 
-// Query groups of one list. A list probed by >= tc_min_q queries is scanned once per
-// balanced group of <= tc_g queries on the tensor cores (usually a single group, so the
-// list's bytes are read once); sparser lists form one FFMA group (<= tc_min_q - 1 <= kScanG).
-__device__ __forceinline__ void group_split(int nq, int tc_min_q, int tc_g, int& ntc, int& nff) {
-  if (nq >= tc_min_q) {
-    ntc = (nq + tc_g - 1) / tc_g;
-    nff = 0;
+// Query groups per chunk of one list, by category. A list probed by >= tc_min_q queries goes to
+// the tensor cores: in mixed mode (tc_mode 0) a list of <= 16 queries is one narrow group and a
+// larger one balanced wide groups of <= 32 (usually one, so the list's bytes are read once);
+// tc_mode 16 / 32 forces one width. Sparser lists form FFMA groups of <= kScanG.
+struct Groups {
+  int g[kTileCats];
+};
+__device__ __forceinline__ Groups group_split(int nq, const PlanParams& p) {
+  Groups G = {{0, 0, 0}};
+  if (nq >= p.tc_min_q) {
+    if (p.tc_mode == 16 || (p.tc_mode == 0 && nq <= 16))
+      G.g[kCatNarrow] = (nq + 15) / 16;
+    else
+      G.g[kCatWide] = (nq + 31) / 32;
   } else {
-    ntc = 0;
-    nff = (nq + kScanG - 1) / kScanG;
+    G.g[kCatFfma] = (nq + kScanG - 1) / kScanG;
   }
+  return G;
 }
 
-// The tiles of one list (chunk-major, group-minor in the tile arrays): groups outer so each group's
-// query split is computed once; chunks c = c0, c0 + cstep, ... (lanes of a warp, or one thread)
+// The tiles of one list: per category, chunk-major and group-minor in that category's array;
+// groups outer so each group's query split is computed once; chunks c = c0, c0 + cstep, ...
+// (lanes of a warp, or one thread). toff: the list's first tile in each category's array.
 __device__ __forceinline__ void emit_tiles(const PlanParams& p, int j, int nq, int qoff, int len, long long src0,
-                                           long long g0, int toff_tc, int toff_ff, int gtc, int gff, int chunks,
+                                           long long g0, const int (&toff)[kTileCats], const Groups& G, int chunks,
                                            int c0, int cstep) {
-  for (int g = 0; g < gtc + gff; ++g) {
-    int tq0, tnq, stride;
-    ScanTile* dst;
-    if (g < gtc) {  // balanced tensor-core groups
-      const bool s32 = nq < 46341;  // g * nq < 2^31 for g <= nq / 32 + 1
-      const int q0 = s32 ? g * nq / gtc : (int)((long long)g * nq / gtc);
-      const int q1 = s32 ? (g + 1) * nq / gtc : (int)((long long)(g + 1) * nq / gtc);
-      tq0 = qoff + q0;
-      tnq = q1 - q0;
-      dst = p.tiles + toff_tc + g;
-      stride = gtc;
-    } else {
-      const int gg = g - gtc;
-      tq0 = qoff + gg * kScanG;
-      tnq = min(kScanG, nq - gg * kScanG);
-      dst = p.ff_tiles + toff_ff + gg;
-      stride = gff;
-    }
-    for (int c = c0; c < chunks; c += cstep) {
-      ScanTile T;
-      T.src_row = src0 + (long long)c * p.R;
-      T.grow0 = g0 + (long long)c * p.R;
-      T.list = j;
-      T.nrows = min(p.R, len - c * p.R);
-      T.qoff = tq0;
-      T.nq = tnq;
-      dst[c * stride] = T;
+#pragma unroll
+  for (int cat = 0; cat < kTileCats; ++cat) {
+    const int ng = G.g[cat];
+    for (int g = 0; g < ng; ++g) {
+      int tq0, tnq;
+      if (cat != kCatFfma) {  // balanced tensor-core groups
+        const bool s32 = nq < 46341;  // g * nq < 2^31 for g <= nq / 16 + 1
+        const int q0 = s32 ? g * nq / ng : (int)((long long)g * nq / ng);
+        const int q1 = s32 ? (g + 1) * nq / ng : (int)((long long)(g + 1) * nq / ng);
+        tq0 = qoff + q0;
+        tnq = q1 - q0;
+      } else {
+        tq0 = qoff + g * kScanG;
+        tnq = min(kScanG, nq - g * kScanG);
+      }
+      ScanTile* dst = p.tiles[cat] + toff[cat] + g;
+      for (int c = c0; c < chunks; c += cstep) {
+        ScanTile T;
+        T.src_row = src0 + (long long)c * p.R;
+        T.grow0 = g0 + (long long)c * p.R;
+        T.list = j;
+        T.nrows = min(p.R, len - c * p.R);
+        T.qoff = tq0;
+        T.nq = tnq;
+        dst[c * ng] = T;
+      }
     }
   }
 }
 
-// warp per list: query count and resident tile counts
+// warp per list: query count and resident tile counts per category
 __global__ void list_count_kernel(const PlanParams p) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= p.nlist) return;
@@ -83,101 +92,123 @@ __global__ void list_count_kernel(const PlanParams p) {
   if (lane == 0) {
     p.list_nq[warp] = c;
     const long long len = p.list_off[warp + 1] - p.list_off[warp];
-    int ntc = 0, nff = 0;
+    Groups G = {{0, 0, 0}};
+    int chunks = 0;
     if (c > 0 && len > 0 && p.res_row0[warp] >= 0) {
-      const int chunks = ((int)len + p.R - 1) / p.R;  // 32-bit: rows per list < 2^31
-      group_split(c, p.tc_min_q, p.tc_g, ntc, nff);
-      ntc *= chunks;
-      nff *= chunks;
+      chunks = ((int)len + p.R - 1) / p.R;  // 32-bit: rows per list < 2^31
+      G = group_split(c, p);
     }
-    p.list_ntile[warp] = ntc;
-    p.list_ntile[p.nlist + warp] = nff;
+#pragma unroll
+    for (int cat = 0; cat < kTileCats; ++cat) p.list_ntile[cat * p.nlist + warp] = G.g[cat] * chunks;
   }
 }
 
-// single CTA: exclusive scans of list_nq and both tile counts; totals and byte counters. Lists are
-// visited in rounds of 1024 (thread t <-> list round * 1024 + t) so every global access coalesces.
-__global__ void __launch_bounds__(1024) list_scan_kernel(const PlanParams p) {
-  __shared__ int wsum[3][32];
-  __shared__ int carry[3];
-  __shared__ unsigned long long wcnt[3][32];
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int nl = p.nlist;
-  if (tid < 3) carry[tid] = 0;
-  unsigned long long cc[3] = {0, 0, 0};
+// Block exclusive scan of kV ints per thread (kNT threads), offset by carry[] (running totals of
+// earlier rounds, updated here); wsum is [kV][32] scratch.
+template <int kNT, int kV>
+__device__ __forceinline__ void block_scan_round(const int (&v)[kV], int (&ex)[kV], int (*wsum)[32], int* carry) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int inc[kV];
+#pragma unroll
+  for (int i = 0; i < kV; ++i) inc[i] = v[i];
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+    for (int i = 0; i < kV; ++i) {
+      const int y = __shfl_up_sync(0xffffffffu, inc[i], o);
+      if (lane >= o) inc[i] += y;
+    }
+  if (lane == 31)
+#pragma unroll
+    for (int i = 0; i < kV; ++i) wsum[i][w] = inc[i];
   __syncthreads();
-  for (int j0 = 0; j0 < nl; j0 += 1024) {
-    const int j = j0 + tid;
-    int v[3] = {0, 0, 0};
-    if (j < nl) {
-      v[0] = p.list_nq[j];
-      v[1] = p.list_ntile[j];
-      v[2] = p.list_ntile[nl + j];
-      if (v[0] > 0) {
-        ++cc[0];
-        cc[p.res_row0[j] >= 0 ? 1 : 2] += p.list_off[j + 1] - p.list_off[j];
+  if (w == 0) {
+#pragma unroll
+    for (int i = 0; i < kV; ++i) {
+      int a = lane < kNT / 32 ? wsum[i][lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, a, o);
+        if (lane >= o) a += y;
       }
+      wsum[i][lane] = a;
     }
-    int inc[3] = {v[0], v[1], v[2]};
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1)
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const int y = __shfl_up_sync(0xffffffffu, inc[i], o);
-        if (lane >= o) inc[i] += y;
-      }
-    if (lane == 31)
-#pragma unroll
-      for (int i = 0; i < 3; ++i) wsum[i][w] = inc[i];
-    __syncthreads();
-    if (w == 0) {
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        int a = wsum[i][lane];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, a, o);
-          if (lane >= o) a += y;
-        }
-        wsum[i][lane] = a;
-      }
-    }
-    __syncthreads();
-    if (j < nl) {
-      p.list_qoff[j] = carry[0] + (w ? wsum[0][w - 1] : 0) + inc[0] - v[0];
-      p.list_toff[j] = carry[1] + (w ? wsum[1][w - 1] : 0) + inc[1] - v[1];
-      p.list_toff[nl + j] = carry[2] + (w ? wsum[2][w - 1] : 0) + inc[2] - v[2];
-    }
-    __syncthreads();
-    if (tid == 0)
-#pragma unroll
-      for (int i = 0; i < 3; ++i) carry[i] += wsum[i][31];
-    __syncthreads();
   }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < kV; ++i) ex[i] = carry[i] + (w ? wsum[i][w - 1] : 0) + inc[i] - v[i];
+  __syncthreads();  // everyone has read carry
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int i = 0; i < kV; ++i) carry[i] += wsum[i][kNT / 32 - 1];
+  __syncthreads();
+}
+
+// block reduction of the byte counters; cat_total[cat] = tiles of each category -> counters / meta
+template <int kNT>
+__device__ __forceinline__ void finish_counters(const PlanParams& p, unsigned long long (&cc)[3],
+                                                unsigned long long (*wcnt)[32], const int* cat_total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
     for (int i = 0; i < 3; ++i) cc[i] += __shfl_xor_sync(0xffffffffu, cc[i], o);
   if (lane == 0)
+#pragma unroll
     for (int i = 0; i < 3; ++i) wcnt[i][w] = cc[i];
   __syncthreads();
   if (w == 0) {
-    unsigned long long c[3] = {wcnt[0][lane], wcnt[1][lane], wcnt[2][lane]};
+    unsigned long long c[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) c[i] = lane < kNT / 32 ? wcnt[i][lane] : 0ull;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
       for (int i = 0; i < 3; ++i) c[i] += __shfl_xor_sync(0xffffffffu, c[i], o);
     if (lane == 0) {
       for (int i = 0; i < 3; ++i) p.counters[i] = c[i];
-      p.meta[0] = carry[1];
-      p.meta[1] = 0;
-      p.meta[2] = carry[2];
-      p.meta[3] = 0;
+      for (int cat = 0; cat < kTileCats; ++cat) {
+        p.meta[2 * cat] = cat_total[cat];
+        p.meta[2 * cat + 1] = 0;
+      }
     }
   }
 }
 
-// warp per list: ascending query ids, then the list's tiles (chunk-major, group-minor)
+// single CTA: exclusive scans of list_nq and the tile counts; totals and byte counters. Lists are
+// visited in rounds of 1024 (thread t <-> list round * 1024 + t) so every global access coalesces.
+__global__ void __launch_bounds__(1024) list_scan_kernel(const PlanParams p) {
+  __shared__ int wsum[1 + kTileCats][32];
+  __shared__ int carry[1 + kTileCats];
+  __shared__ unsigned long long wcnt[3][32];
+  const int tid = threadIdx.x;
+  const int nl = p.nlist;
+  if (tid <= kTileCats) carry[tid] = 0;
+  unsigned long long cc[3] = {0, 0, 0};
+  __syncthreads();
+  for (int j0 = 0; j0 < nl; j0 += 1024) {
+    const int j = j0 + tid;
+    int v[1 + kTileCats] = {0, 0, 0, 0}, ex[1 + kTileCats];
+    if (j < nl) {
+      v[0] = p.list_nq[j];
+#pragma unroll
+      for (int cat = 0; cat < kTileCats; ++cat) v[1 + cat] = p.list_ntile[cat * nl + j];
+      if (v[0] > 0) {
+        ++cc[0];
+        cc[p.res_row0[j] >= 0 ? 1 : 2] += p.list_off[j + 1] - p.list_off[j];
+      }
+    }
+    block_scan_round<1024, 1 + kTileCats>(v, ex, wsum, carry);
+    if (j < nl) {
+      p.list_qoff[j] = ex[0];
+#pragma unroll
+      for (int cat = 0; cat < kTileCats; ++cat) p.list_toff[cat * nl + j] = ex[1 + cat];
+    }
+  }
+  finish_counters<1024>(p, cc, wcnt, carry + 1);
+}
+
+// warp per list: ascending query ids, then the list's tiles
 __global__ void list_fill_kernel(const PlanParams p) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= p.nlist) return;
@@ -204,13 +235,18 @@ __global__ void list_fill_kernel(const PlanParams p) {
     }
     out += __shfl_sync(0xffffffffu, incl, 31);
   }
-  const int ntc = p.list_ntile[warp], nff = p.list_ntile[p.nlist + warp];
-  if (ntc + nff == 0) return;
+  int total = 0;
+#pragma unroll
+  for (int cat = 0; cat < kTileCats; ++cat) total += p.list_ntile[cat * p.nlist + warp];
+  if (total == 0) return;
   const long long len = p.list_off[warp + 1] - p.list_off[warp];
   const int chunks = ((int)len + p.R - 1) / p.R;  // 32-bit: rows per list < 2^31
-  const int gtc = ntc / chunks, gff = nff / chunks;
-  emit_tiles(p, warp, nq, p.list_qoff[warp], (int)len, p.res_row0[warp], p.list_off[warp], p.list_toff[warp],
-             p.list_toff[p.nlist + warp], gtc, gff, chunks, lane, 32);
+  const Groups G = group_split(nq, p);
+  int toff[kTileCats];
+#pragma unroll
+  for (int cat = 0; cat < kTileCats; ++cat) toff[cat] = p.list_toff[cat * p.nlist + warp];
+  emit_tiles(p, warp, nq, p.list_qoff[warp], (int)len, p.res_row0[warp], p.list_off[warp], toff, G, chunks, lane,
+             32);
 }
 
 // Small batches: the whole plan in one CTA with the list x query bitmap in shared memory (one
@@ -222,10 +258,10 @@ constexpr int kPlanThreads = 1024;
 __global__ void __launch_bounds__(kPlanThreads) plan_fused_kernel(const PlanParams p) {
   RD_PDL_PROLOGUE();
   extern __shared__ unsigned bm[];  // nlist x W bitmap, then slen[nlist] (list length, ~len if offloaded)
-  __shared__ int wsum[3][32];
-  __shared__ int carry[3];
+  __shared__ int wsum[1 + kTileCats][32];
+  __shared__ int carry[1 + kTileCats];
   __shared__ unsigned long long wcnt[3][32];
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
   RD_TS(0);
   const int W = p.W, nl = p.nlist;
   int* slen = reinterpret_cast<int*>(bm + nl * W);
@@ -242,7 +278,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_fused_kernel(const PlanPara
     slen[j] = p.res_row0[j] >= 0 ? len : ~len;
   }
   for (int i = tid; i < nl * W; i += kPlanThreads) bm[i] = 0u;
-  if (tid < 3) carry[tid] = 0;
+  if (tid <= kTileCats) carry[tid] = 0;
   __syncthreads();
   RD_TS(1);
 #pragma unroll
@@ -259,64 +295,40 @@ __global__ void __launch_bounds__(kPlanThreads) plan_fused_kernel(const PlanPara
   unsigned long long cc[3] = {0, 0, 0};  // unique probed lists, resident rows, offloaded rows
   for (int j0 = 0; j0 < nl; j0 += kPlanThreads) {
     const int j = j0 + tid;
-    int v[3] = {0, 0, 0};  // queries, tensor-core tiles, FFMA tiles of list j
-    int len = 0, chunks = 0;
+    int nq = 0, len = 0, chunks = 0;
+    Groups G = {{0, 0, 0}};
     long long src0 = 0, g0 = 0;
     if (j < nl) {
-      for (int x = 0; x < W; ++x) v[0] += __popc(bm[j * W + x]);
+      for (int x = 0; x < W; ++x) nq += __popc(bm[j * W + x]);
       const int sl = slen[j];
       len = sl >= 0 ? sl : ~sl;
-      if (v[0] > 0) {
+      if (nq > 0) {
         ++cc[0];
         cc[sl >= 0 ? 1 : 2] += len;
         if (sl >= 0 && len > 0) {
           chunks = (len + p.R - 1) / p.R;
-          group_split(v[0], p.tc_min_q, p.tc_g, v[1], v[2]);
+          G = group_split(nq, p);
           src0 = p.res_row0[j];
           g0 = p.list_off[j];
         }
       }
     }
-    // block exclusive scan of v[] over this round, offset by the running carry
-    int inc[3] = {v[0], v[1] * chunks, v[2] * chunks};
+    int v[1 + kTileCats], ex[1 + kTileCats];
+    v[0] = nq;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1)
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const int y = __shfl_up_sync(0xffffffffu, inc[i], o);
-        if (lane >= o) inc[i] += y;
-      }
-    if (lane == 31)
-#pragma unroll
-      for (int i = 0; i < 3; ++i) wsum[i][w] = inc[i];
-    __syncthreads();
-    if (w == 0) {
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        int a = wsum[i][lane];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, a, o);
-          if (lane >= o) a += y;
-        }
-        wsum[i][lane] = a;  // inclusive over warps
-      }
-    }
-    __syncthreads();
-    const int o0 = carry[0] + (w ? wsum[0][w - 1] : 0) + inc[0] - v[0];
-    const int o1 = carry[1] + (w ? wsum[1][w - 1] : 0) + inc[1] - v[1] * chunks;
-    const int o2 = carry[2] + (w ? wsum[2][w - 1] : 0) + inc[2] - v[2] * chunks;
+    for (int cat = 0; cat < kTileCats; ++cat) v[1 + cat] = G.g[cat] * chunks;
+    block_scan_round<kPlanThreads, 1 + kTileCats>(v, ex, wsum, carry);
     if (j < nl) {
-      p.list_nq[j] = v[0];
-      p.list_qoff[j] = o0;
+      p.list_nq[j] = nq;
+      p.list_qoff[j] = ex[0];
     }
     // warp-cooperative emission for the warp's probed lists
-    unsigned m = __ballot_sync(0xffffffffu, v[0] > 0);
+    unsigned m = __ballot_sync(0xffffffffu, nq > 0);
     while (m) {
       const int src = __ffs(m) - 1;
       m &= m - 1;
-      const int lj = __shfl_sync(0xffffffffu, j, src), nq = __shfl_sync(0xffffffffu, v[0], src);
-      const int qo = __shfl_sync(0xffffffffu, o0, src);
+      const int lj = __shfl_sync(0xffffffffu, j, src), lnq = __shfl_sync(0xffffffffu, nq, src);
+      const int qo = __shfl_sync(0xffffffffu, ex[0], src);
       // query ids ascending: lane x < W owns bitmap word x
       const unsigned bits = lane < W ? bm[lj * W + lane] : 0u;
       int pos = __popc(bits);
@@ -327,45 +339,25 @@ __global__ void __launch_bounds__(kPlanThreads) plan_fused_kernel(const PlanPara
       }
       pos = qo + pos - __popc(bits);
       for (unsigned bb = bits; bb; bb &= bb - 1) p.list_q[pos++] = lane * 32 + (__ffs(bb) - 1);
-      const int gtc = __shfl_sync(0xffffffffu, v[1], src), gff = __shfl_sync(0xffffffffu, v[2], src);
-      if (gtc + gff > 0) {
-        emit_tiles(p, lj, nq, qo, __shfl_sync(0xffffffffu, len, src), __shfl_sync(0xffffffffu, src0, src),
-                   __shfl_sync(0xffffffffu, g0, src), __shfl_sync(0xffffffffu, o1, src),
-                   __shfl_sync(0xffffffffu, o2, src), gtc, gff, __shfl_sync(0xffffffffu, chunks, src), lane, 32);
-      }
-    }
-    __syncthreads();  // everyone has read carry
-    if (tid == 0)
+      Groups LG;
+      int toff[kTileCats], any = 0;
 #pragma unroll
-      for (int i = 0; i < 3; ++i) carry[i] += wsum[i][31];
-    __syncthreads();
+      for (int cat = 0; cat < kTileCats; ++cat) {
+        LG.g[cat] = __shfl_sync(0xffffffffu, G.g[cat], src);
+        toff[cat] = __shfl_sync(0xffffffffu, ex[1 + cat], src);
+        any += LG.g[cat];
+      }
+      if (any > 0)
+        emit_tiles(p, lj, lnq, qo, __shfl_sync(0xffffffffu, len, src), __shfl_sync(0xffffffffu, src0, src),
+                   __shfl_sync(0xffffffffu, g0, src), toff, LG, __shfl_sync(0xffffffffu, chunks, src), lane, 32);
+    }
   }
   RD_TS(3);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int i = 0; i < 3; ++i) cc[i] += __shfl_xor_sync(0xffffffffu, cc[i], o);
-  if (lane == 0)
-    for (int i = 0; i < 3; ++i) wcnt[i][w] = cc[i];
-  __syncthreads();
-  if (w == 0) {
-    unsigned long long c[3] = {wcnt[0][lane], wcnt[1][lane], wcnt[2][lane]};
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int i = 0; i < 3; ++i) c[i] += __shfl_xor_sync(0xffffffffu, c[i], o);
-    if (lane == 0) {
-      for (int i = 0; i < 3; ++i) p.counters[i] = c[i];
-      p.meta[0] = carry[1];
-      p.meta[1] = 0;
-      p.meta[2] = carry[2];
-      p.meta[3] = 0;
-    }
-  }
+  finish_counters<kPlanThreads>(p, cc, wcnt, carry + 1);
   RD_TS(4);
 }
 
-// Tiny batches (B * nprobe <= 1024 pairs): plan from the probe pairs alone. The (list, query) pairs
+// Tiny batches (B * nprobe <= 512 pairs): plan from the probe pairs alone. The (list, query) pairs
 // are rank-sorted in one CTA; a list's segment in sorted order IS its query CSR (list_q = the sorted
 // query ids, ascending within a list), so the only passes are O(pairs) plus one coalesced zeroing of
 // list_nq. Same outputs as the bitmap planners for every list.
@@ -373,9 +365,10 @@ constexpr int kSmallPlanThreads = 1024;
 __global__ void __launch_bounds__(kSmallPlanThreads) plan_small_kernel(const PlanParams p) {
   RD_PDL_PROLOGUE();
   __shared__ unsigned long long key[kSmallPlanThreads];
-  __shared__ int wsum[3][32];
+  __shared__ int wsum[kTileCats][32];
+  __shared__ int carry[kTileCats];
   __shared__ unsigned long long wcnt[3][32];
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int tid = threadIdx.x;
   const int P = p.B * p.nprobe;
   RD_TS(0);
   // (list, query) keys; padding / invalid probes sort last
@@ -385,6 +378,7 @@ __global__ void __launch_bounds__(kSmallPlanThreads) plan_small_kernel(const Pla
     if (l >= 0) kv = ((unsigned long long)(unsigned)l << 32) | (unsigned)(tid / p.nprobe);
   }
   key[tid] = kv;
+  if (tid < kTileCats) carry[tid] = 0;
   for (int j = tid; j < p.nlist; j += kSmallPlanThreads) p.list_nq[j] = 0;  // coalesced
   __syncthreads();
   int r = 0;  // rank of this thread's key (keys are distinct)
@@ -392,14 +386,14 @@ __global__ void __launch_bounds__(kSmallPlanThreads) plan_small_kernel(const Pla
     for (int i = 0; i < P; ++i) r += key[i] < kv;
   __syncthreads();
   if (kv != ~0ull) key[r] = kv;
-  // number of valid pairs
   const int valid = __syncthreads_count(kv != ~0ull);
   RD_TS(1);
   // segment starts in sorted order: thread t owns sorted position t
   const unsigned long long mine = tid < valid ? key[tid] : ~0ull;
   const int l = (int)(mine >> 32);
   const bool start = tid < valid && (tid == 0 || (key[tid - 1] >> 32) != (mine >> 32));
-  int nq = 0, ntc = 0, nff = 0, chunks = 0, len = 0;
+  int nq = 0, chunks = 0, len = 0;
+  Groups G = {{0, 0, 0}};
   long long src0 = -1, g0 = 0;
   if (start) {
     int e = tid + 1;
@@ -410,64 +404,27 @@ __global__ void __launch_bounds__(kSmallPlanThreads) plan_small_kernel(const Pla
     src0 = p.res_row0[l];
     if (src0 >= 0 && len > 0) {
       chunks = (len + p.R - 1) / p.R;
-      group_split(nq, p.tc_min_q, p.tc_g, ntc, nff);
+      G = group_split(nq, p);
     }
   }
   if (tid < valid) p.list_q[tid] = (int)(mine & 0xffffffffu);
-  // block scan of the segment starts' (1, tc tiles, ff tiles)
-  int v[3] = {start ? 1 : 0, ntc * chunks, nff * chunks};
-  int inc[3] = {v[0], v[1], v[2]};
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1)
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const int y = __shfl_up_sync(0xffffffffu, inc[i], o);
-      if (lane >= o) inc[i] += y;
-    }
-  if (lane == 31)
-#pragma unroll
-    for (int i = 0; i < 3; ++i) wsum[i][w] = inc[i];
   unsigned long long cc[3] = {start ? 1ull : 0ull, start && src0 >= 0 ? (unsigned long long)len : 0ull,
                               start && src0 < 0 ? (unsigned long long)len : 0ull};
+  // block scan of the segment starts' tile counts (the query offset is the sorted position itself)
+  int v[kTileCats], ex[kTileCats];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int i = 0; i < 3; ++i) cc[i] += __shfl_xor_sync(0xffffffffu, cc[i], o);
-  if (lane == 0)
-#pragma unroll
-    for (int i = 0; i < 3; ++i) wcnt[i][w] = cc[i];
-  __syncthreads();
-  if (w == 0) {
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      int a = wsum[i][lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, a, o);
-        if (lane >= o) a += y;
-      }
-      wsum[i][lane] = a;
-      unsigned long long c = wcnt[i][lane];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-      if (lane == 0) p.counters[i] = c;
-    }
-    if (lane == 0) {
-      p.meta[0] = wsum[1][31];
-      p.meta[1] = 0;
-      p.meta[2] = wsum[2][31];
-      p.meta[3] = 0;
-    }
-  }
-  __syncthreads();
+  for (int cat = 0; cat < kTileCats; ++cat) v[cat] = G.g[cat] * chunks;
+  block_scan_round<kSmallPlanThreads, kTileCats>(v, ex, wsum, carry);
   RD_TS(2);
   if (start) {
-    const int o1 = (w ? wsum[1][w - 1] : 0) + inc[1] - v[1];
-    const int o2 = (w ? wsum[2][w - 1] : 0) + inc[2] - v[2];
     p.list_nq[l] = nq;
     p.list_qoff[l] = tid;
-    if (ntc + nff > 0) emit_tiles(p, l, nq, tid, len, src0, g0, o1, o2, ntc, nff, chunks, 0, 1);
+    int any = 0;
+#pragma unroll
+    for (int cat = 0; cat < kTileCats; ++cat) any += G.g[cat];
+    if (any > 0) emit_tiles(p, l, nq, tid, len, src0, g0, ex, G, chunks, 0, 1);
   }
+  finish_counters<kSmallPlanThreads>(p, cc, wcnt, carry);
   RD_TS(3);
 }
 

@@ -52,7 +52,10 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   auto& w = h->ws;
   const int nl = h->nlist, d = h->d;
   const Plan pl = make_plan(h, B, nprobe);
-  const int tc_g = h->tc_g_for(B, nprobe);  // queries per tensor-core tile
+  // tensor-core tile widths: mixed (<= 16-query lists narrow, others wide) or one width; the
+  // offloaded lists' host-planned tiles use one width
+  const int tc_mode = h->tc_mode_for(B, nprobe);
+  const int tc_g = tc_mode == 16 ? 16 : 32;
   const int W = (int)((B + 31) / 32);
   w.qnorm.ensure(B);
   w.Dc.ensure((size_t)B * nl);
@@ -60,10 +63,11 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   w.bitmap.ensure((size_t)nl * W);
   w.list_nq.ensure(nl);
   w.list_qoff.ensure(nl);
-  w.list_ntile.ensure(2 * (size_t)nl);
-  w.list_toff.ensure(2 * (size_t)nl);
+  w.list_ntile.ensure(rd::kTileCats * (size_t)nl);
+  w.list_toff.ensure(rd::kTileCats * (size_t)nl);
   w.list_q.ensure((size_t)B * nprobe);
   w.tiles.ensure(pl.max_tiles);
+  w.tiles16.ensure(pl.max_tiles);
   w.ff_tiles.ensure(pl.max_tiles);
   w.qsplit.ensure((size_t)B * 2 * d);
   w.blk.ensure(kStatBytes + result_bytes);
@@ -98,8 +102,8 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   h->traced("select", s, sp.dbg, [&] { CK(rd::launch_select(sp, h->stage_rows(B), s)); });
   launches += rd::coarse_small((int)B) ? 2 : 3;  // (query prep +) coarse + select
   rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
-                    w.list_ntile.p, w.list_toff.p, w.list_q.p, w.tiles.p, w.ff_tiles.p, w.meta(), w.counters(),
-                    (int)B, nl, nprobe, pl.R, h->tc_scan() ? h->tc_min_q : 1 << 30, tc_g};
+                    w.list_ntile.p, w.list_toff.p, w.list_q.p, {w.tiles16.p, w.tiles.p, w.ff_tiles.p}, w.meta(),
+                    w.counters(), (int)B, nl, nprobe, pl.R, h->tc_scan() ? h->tc_min_q : 1 << 30, tc_mode};
   h->traced("plan", s, pp.dbg, [&] { CK(rd::launch_plan(pp, s)); });
   launches += rd::plan_small_ok((int)B, nprobe) || rd::plan_fused_ok((int)B, nl) ? 1 : 4;
   if (!h->no_inner_events) CK(cudaEventRecord(e1, s));
@@ -113,9 +117,10 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   }
   CK(cudaEventRecord(e_plan, s));
   const CUtensorMap gmap = make_gather_map(w.qsplit.p, B, d);
-  rd::ScanParams sc{w.ff_tiles.p, w.meta() + 2, w.meta() + 3, d_q, w.qnorm.p, w.list_q.p, h->xnorm.p,
-                    w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p};
-  rd::TcScanParams tc{w.tiles.p, w.meta(), w.meta() + 1, w.qsplit.p, w.qnorm.p, w.list_q.p, h->xnorm.p,
+  rd::ScanParams sc{w.ff_tiles.p, w.meta() + 2 * rd::kCatFfma, w.meta() + 2 * rd::kCatFfma + 1, d_q, w.qnorm.p,
+                    w.list_q.p, h->xnorm.p, w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p};
+  rd::TcScanParams tc{w.tiles.p, w.meta() + 2 * rd::kCatWide, w.meta() + 2 * rd::kCatWide + 1, w.qsplit.p, w.qnorm.p,
+                      w.list_q.p, h->xnorm.p,
                       w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p, h->debug_skip,
                       h->early_x};
   if (!h->tc_scan() || h->tc_min_q > 1) {  // FFMA tiles exist only in these cases
@@ -134,9 +139,20 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
       CK(cudaMemsetAsync(h->dbg_stall.p, 0, 8 * 12 * (size_t)h->num_sms, s));
       tc.stall = h->dbg_stall.p;
     }
-    CK(rd::launch_scan_tc(h->presplit ? h->xmap128 : h->map128, h->presplit ? h->xmap32 : h->map32, gmap, tc,
-                          h->num_sms, s, h->presplit, tc_g));
-    launches += 1;
+    const CUtensorMap& xm128 = h->presplit ? h->xmap128 : h->map128;
+    const CUtensorMap& xm32 = h->presplit ? h->xmap32 : h->map32;
+    if (tc_mode != 32) {  // narrow tiles: the 16-wide scan (deeper ring)
+      rd::TcScanParams tn = tc;
+      tn.tiles = w.tiles16.p;
+      tn.ntiles = w.meta() + 2 * rd::kCatNarrow;
+      tn.tile_counter = w.meta() + 2 * rd::kCatNarrow + 1;
+      CK(rd::launch_scan_tc(xm128, xm32, gmap, tn, h->num_sms, s, h->presplit, 16));
+      launches += 1;
+    }
+    if (tc_mode != 16) {  // wide tiles: the 32-wide scan
+      CK(rd::launch_scan_tc(xm128, xm32, gmap, tc, h->num_sms, s, h->presplit, 32));
+      launches += 1;
+    }
     if (stall) {
       std::vector<unsigned long long> v(12 * (size_t)h->num_sms);
       CK(cudaMemcpyAsync(v.data(), h->dbg_stall.p, 8 * v.size(), cudaMemcpyDeviceToHost, s));
@@ -334,7 +350,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
       st->h2d_list_bytes = h2d;
       st->bytes_algorithmic = (hc[1] + hc[2]) * row_bytes + (unsigned long long)nl * row_bytes +
                               (unsigned long long)B * row_bytes + (unsigned long long)B * k * 12ull;
-      st->tiles = (uint64_t)hm[0] + (uint64_t)hm[2];
+      st->tiles = (uint64_t)hm[0] + (uint64_t)hm[2] + (uint64_t)hm[4];
       if (!h->no_inner_events) {
         CK(cudaEventElapsedTime(&ms, e1, e2));
         st->scan_ms = ms;
