@@ -241,7 +241,6 @@ struct rd_index {
   bool dbg_ts = std::getenv("RD_DEBUG_TS") != nullptr;  // profiling only: select checkpoints to stderr
   int stage_max_b = -1;  // batches up to this size stage exact-distance rows in smem (-1: 2 x SMs)
   int tiles_per_sm = 8;  // scan tiles per SM the planner aims for (RD_TILES_PER_SM)
-  int early_x = std::getenv("RD_EARLY_X") ? std::atoi(std::getenv("RD_EARLY_X")) : 0;  // see TcScanParams
   long long seed_max_b = 1LL << 40;  // batches up to this size seed the scan's pruning threshold (RD_SEED_MAX_B)
   bool no_inner_events = std::getenv("RD_NO_INNER_EVENTS") != nullptr;  // A/B: no per-stage timing events
   // the tensor-core scan stages 64-dim bf16 query slices of up to 32 queries in shared memory:

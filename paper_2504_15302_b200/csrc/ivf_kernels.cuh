@@ -85,7 +85,6 @@ struct TcScanParams {
   int d;
   int* qthr;               // B: per-query pruning threshold (f2ord), min over completed tiles' 32nd
   int debug_skip;          // profiling only (RD_DEBUG_SKIP): 1 = no epilogue selection, 2 = no conversion, 4 = no MMA
-  int early_x;             // issue a tile's first x stages before waiting for its B operand slot
   unsigned long long* stall = nullptr;  // profiling only (RD_DEBUG_STALL): per CTA x 12 barrier-wait cycles
   unsigned long long* dbg = nullptr;  // profiling only (RD_DEBUG_TS): per CTA [entry, ready, first tile, end] globaltimer
 };

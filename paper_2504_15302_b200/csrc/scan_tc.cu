@@ -213,13 +213,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ++u;
       };
-      // With early_x, the first ring's worth of x stages goes out before waiting for the B operand
-      // to be free: those slots free up as the previous tile's last MMAs retire, so HBM keeps
-      // streaming across the tile boundary (matters when tiles are short).
-      const int pre = p.early_x ? min(RS, nst) : 0;
-      if (lane == 0)
-        for (int i = 0; i < pre; ++i) issue_x(i);
-      __syncwarp();
       // ---- B operand by TMA gather4: rows 0-31 q1, 32-63 q2 of the tile's queries (qsplit row
       // 2*qid + part); padding rows repeat the last query (their D columns are ignored)
       RD_TWAIT(sm.bempty, (ti & 1) ^ 1, 2);
@@ -246,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         &sm.bfull[slice]);
       }
       if (lane == 0)
-        for (int i = pre; i < nst; ++i) issue_x(i);
+        for (int i = 0; i < nst; ++i) issue_x(i);
       __syncwarp();
     }
   }

@@ -121,8 +121,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
                     w.list_q.p, h->xnorm.p, w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p};
   rd::TcScanParams tc{w.tiles.p, w.meta() + 2 * rd::kCatWide, w.meta() + 2 * rd::kCatWide + 1, w.qsplit.p, w.qnorm.p,
                       w.list_q.p, h->xnorm.p,
-                      w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p, h->debug_skip,
-                      h->early_x};
+                      w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p, h->debug_skip};
   if (!h->tc_scan() || h->tc_min_q > 1) {  // FFMA tiles exist only in these cases
     CK(rd::launch_scan(h->map256, h->map32, sc, h->num_sms, s));
     launches += 1;
