@@ -47,7 +47,6 @@ struct TcGeom {
   static_assert(kG == 16 || kG == 32, "tile width");
 };
 constexpr int kXBufs = 8;                    // TMEM ring of converted stages (32 columns each)
-constexpr int kMaxBSlices = 16;              // 64-dim query-operand slices (d <= 1024)
 static_assert(kXBufs % 2 == 0, "TMEM ring depth must be even");
 constexpr int kThreads = 448;                // 14 warps
 constexpr uint32_t kTmemCols = 512;
@@ -81,8 +80,8 @@ __device__ __forceinline__ Smem carve(unsigned char* raw, int d) {
   s.xempty = s.xfull + kXBufs;
   s.afull = s.xempty + kXBufs;
   s.aempty = s.afull + 2;
-  s.bfull = s.aempty + 2;  // one per 64-dim B slice (kMaxBSlices)
-  s.bempty = s.bfull + kMaxBSlices;
+  s.bfull = s.aempty + 2;
+  s.bempty = s.bfull + 1;
   s.tfull = s.bempty + 1;
   s.tempty = s.tfull + 2;
   s.tring = reinterpret_cast<int*>(s.tempty + 2);
@@ -93,7 +92,9 @@ __device__ __forceinline__ Smem carve(unsigned char* raw, int d) {
   return s;
 }
 
-// profiling only (p.stall != nullptr): cycles a role spends blocked on one barrier
+// profiling only (built with -DRD_STALL_PROF and run with p.stall != nullptr): cycles a role
+// spends blocked on one barrier. The shipped build compiles it to a plain wait.
+#ifdef RD_STALL_PROF
 #define RD_TWAIT(bar, parity, slot)                                  \
   do {                                                               \
     if (p.stall) {                                                   \
@@ -104,6 +105,9 @@ __device__ __forceinline__ Smem carve(unsigned char* raw, int d) {
       mbar_wait(bar, parity);                                        \
     }                                                                \
   } while (0)
+#else
+#define RD_TWAIT(bar, parity, slot) mbar_wait(bar, parity)
+#endif
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // .x = lo -> low 16 bits
@@ -145,7 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.tfull[i], 1);
       mbar_init(&sm.tempty[i], kPre ? 1 + 4 : 1 + 4 + 4 + 4);
     }
-    for (int i = 0; i < d / 64; ++i) mbar_init(&sm.bfull[i], 1);
+    mbar_init(sm.bfull, 1);
     mbar_init(sm.bempty, 1);
     fence_mbar_init();
   }
@@ -155,8 +159,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *sm.tmem_base;
   const int ntiles = *p.ntiles;
+#ifdef RD_STALL_PROF
   long long stall_acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   const long long t_begin = clock64();
+#endif
   if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 4 + 1] = gtimer();
 
   // ---------------------------------------------------------------- warp 0: TMA producer
@@ -219,10 +225,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // only the quads holding real queries are loaded; the others keep stale rows whose D
       // columns the epilogue never reads
       const int qq = (T.nq + 3) >> 2;  // quads per part
-      // one barrier per 64-dim slice: the MMAs of the tile's first row tile start as soon as
-      // their own slice of the query operand has landed instead of after the whole gather
-      if (lane == 0)
-        for (int sl = 0; sl < nslices; ++sl) mbar_arrive_expect_tx(&sm.bfull[sl], (uint32_t)(2 * qq * 512));
+      // one barrier for the whole gather (per-slice barriers let the first MMAs start earlier but
+      // cost more than they saved: A/B on B200, 1024 queries, 206.4k vs 207.2k q/s)
+      if (lane == 0) mbar_arrive_expect_tx(sm.bfull, (uint32_t)(nslices * 2 * qq * 512));
       __syncwarp();
       for (int gi = lane; gi < nslices * 2 * qq; gi += 32) {
         const int slice = gi / (2 * qq), qi = gi % (2 * qq);
@@ -235,8 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int g = min(g0 + i, T.nq - 1);
           r[i] = 2 * __ldg(p.list_q + T.qoff + g) + part;
         }
-        tma_gather4_u32(sm.bs + slice * kBSlice + quad * 512, &qmap, slice * 64, r[0], r[1], r[2], r[3],
-                        &sm.bfull[slice]);
+        tma_gather4_u32(sm.bs + slice * kBSlice + quad * 512, &qmap, slice * 64, r[0], r[1], r[2], r[3], sm.bfull);
       }
       if (lane == 0)
         for (int i = 0; i < nst; ++i) issue_x(i);
@@ -264,8 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t dacc = tmem + a * kAccCols;
         for (int ks = 0; ks < nks; ++ks, ++u) {
-          if (rt == 0 && (kPre || (ks & 1) == 0))  // this slice of the tile's queries has landed
-            RD_TWAIT(&sm.bfull[kPre ? ks : ks >> 1], ti & 1, 4);
+          if (rt == 0 && ks == 0) RD_TWAIT(sm.bfull, ti & 1, 4);  // this tile's queries are in the B operand
           if constexpr (kPre) {
             const int s = u % RS;
             RD_TWAIT(&sm.full[s], (u / RS) & 1, 6);
@@ -524,6 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
 done:
+#ifdef RD_STALL_PROF
   if (p.stall && (threadIdx.x & 31) == 0) {  // lane 0 of each role's first warp reports its waits
     const int w = threadIdx.x >> 5;
     unsigned long long* o = p.stall + (size_t)blockIdx.x * 12;
@@ -542,6 +546,7 @@ done:
       o[8] = stall_acc[8];
     }
   }
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -571,7 +576,7 @@ size_t scan_tc_smem_bytes(int d, int tc_g) {
   const size_t stages = tc_g == 16 ? TcGeom<16>::Stages : TcGeom<32>::Stages;
   const size_t bslice = tc_g == 16 ? TcGeom<16>::BSlice : TcGeom<32>::BSlice;
   return 1024 + stages * kStageBytes + (size_t)(d / 64) * bslice +
-         (2 * stages + 2 * kXBufs + 9 + kMaxBSlices) * sizeof(uint64_t) + 2 * sizeof(int) + 16 + 4 * 32 * 12 +
+         (2 * stages + 2 * kXBufs + 10) * sizeof(uint64_t) + 2 * sizeof(int) + 16 + 4 * 32 * 12 +
          (size_t)tc_g * kRows * sizeof(float) + 64;
 }
 

@@ -132,7 +132,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
       CK(cudaMemsetAsync(h->dbg_scan.p, 0, 8 * 4 * (size_t)h->num_sms, s));
       tc.dbg = h->dbg_scan.p;
     }
-    const bool stall = std::getenv("RD_DEBUG_STALL") != nullptr;  // profiling only
+    const bool stall = std::getenv("RD_DEBUG_STALL") != nullptr;  // profiling only (scan_tc.cu built with -DRD_STALL_PROF)
     if (stall) {
       if (h->dbg_stall.n < 12 * (size_t)h->num_sms) h->dbg_stall.alloc(12 * (size_t)h->num_sms);
       CK(cudaMemsetAsync(h->dbg_stall.p, 0, 8 * 12 * (size_t)h->num_sms, s));

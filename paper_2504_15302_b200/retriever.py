@@ -387,8 +387,9 @@ _ENGINE: Optional[Library] = None
 
 
 def engine() -> Library:
-    """The B200 engine library (raises if not built)."""
+    """The B200 engine library (raises if not built). RD_ENGINE_PATH points at another build of the
+    same engine (A/B measurements only)."""
     global _ENGINE
     if _ENGINE is None:
-        _ENGINE = Library(ENGINE_PATH)
+        _ENGINE = Library(os.environ.get("RD_ENGINE_PATH") or ENGINE_PATH)
     return _ENGINE
