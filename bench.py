@@ -270,6 +270,9 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    # per-stage events inside the timed region: the scan kernel's own duration for the roofline
+    # (they cost the chain its launch overlap, ~12 us per search; e2e and the sweep run without)
+    idx.timing_stages(True)
     idx.timing_reset()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -285,6 +288,7 @@ def run_ours(args, cfg):
             dist.barrier()
     ms = ev0.elapsed_time(ev1)
     tm = idx.timing_read()
+    idx.timing_stages(False)
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -350,7 +354,7 @@ def run_ours(args, cfg):
     # roofline of the dominant kernel (N4 resident list scan), measured over the timed region
     peaks = measured_peaks()
     peak = peaks["hbm_gbs"] if peaks else 6650.0
-    scan_ms = tm["scan_ms"] / max(1, tm["searches"])
+    scan_ms = tm["scan_ms"] / max(1, tm["stage_searches"])
     scan_bytes = st["bytes_lists_resident"]
     achieved = scan_bytes / (scan_ms * 1e-3) / 1e9 if scan_ms > 0 else 0.0
     traffic = None
@@ -383,7 +387,7 @@ def run_ours(args, cfg):
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "ivf_scan_tc_kernel (N5; FFMA ivf_scan_kernel N4 when d % 64 != 0)", "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
                      "bytes_per_launch": scan_bytes, "avg_launch_ms": scan_ms},
-        "step_breakdown_ms": {k2: tm[k2] / max(1, tm["searches"]) for k2 in ("coarse_ms", "scan_ms", "tail_ms", "total_ms")},
+        "step_breakdown_ms": {k2: tm[k2] / max(1, tm["stage_searches"]) for k2 in ("coarse_ms", "scan_ms", "tail_ms", "total_ms")},
         "step_gbps_algorithmic": st["bytes_algorithmic"] / (ms_step * 1e-3) / 1e9,
         "gpu_launches": launches_per_search * args.steps + (args.steps if world > 1 else 0),
         "batch_sweep_qps": sweep,

@@ -100,8 +100,9 @@ typedef struct {
   uint64_t lists_probed;        /* unique lists probed by the batch */
   uint64_t tiles;               /* scan work items */
   uint64_t kernel_launches;     /* device kernels launched by this call */
-  double scan_ms;               /* device time of the resident list-scan kernel (CUDA events) */
-  double coarse_ms;             /* device time of coarse quantization + probe selection */
+  double scan_ms;               /* device time of the resident list-scan kernel (CUDA events; 0 unless
+                                   rd_timing_stages is on) */
+  double coarse_ms;             /* device time of coarse quantization + probe selection (likewise) */
   double offload_ms;            /* device time from first H2D to last offloaded scan */
   uint32_t margin_failures;     /* queries whose candidate margin could not be certified */
   uint32_t probe_failures;      /* queries whose probe set could not be certified */
@@ -215,14 +216,20 @@ int rd_search_device(rd_index* h, const float* d_queries, int64_t B, int32_t npr
  * ascending (exact centroid distance, list id). */
 int rd_probe(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32_t* out_lists);
 
-/* ---- device-time accounting (CUDA events on each search's stream) ---- */
+/* ---- device-time accounting (CUDA events on each search's stream) ----
+ * Every search records events around the whole chain. Per-stage events (the
+ * coarse / scan / tail split) sit between kernels and cost the chain its
+ * programmatic-dependent-launch overlap (~6 us per event at small batches), so
+ * they are recorded only while rd_timing_stages(h, 1) is on (default off). */
 typedef struct {
   int64_t searches; /* searches accounted since the last reset */
   double scan_ms;   /* summed device time of the resident list scan (N4) */
   double coarse_ms; /* summed device time of qnorm + N1 coarse + N2 select + N3 plan */
   double tail_ms;   /* summed device time after the resident scan: offload wait, N6/N7 merge */
   double total_ms;  /* summed device time of whole searches */
+  int64_t stage_searches; /* of those, searches with per-stage events (scan/coarse/tail sums cover these) */
 } rd_timing;
+int rd_timing_stages(rd_index* h, int32_t on);
 int rd_timing_reset(rd_index* h);
 int rd_timing_read(rd_index* h, rd_timing* out); /* synchronizes the recorded searches */
 

@@ -757,6 +757,12 @@ int rd_merge_topk_device(int32_t G, int64_t B, int32_t k, const int64_t* a, cons
   return fail(RD_ERR_INVALID, "cpu oracle has no device merge");
 }
 
+int rd_timing_stages(rd_index* h, int32_t on) {
+  (void)on;
+  if (!h) return fail(RD_ERR_INVALID, "null index");
+  return RD_OK;
+}
+
 int rd_timing_reset(rd_index* h) {
   if (!h) return fail(RD_ERR_INVALID, "null index");
   return RD_OK;

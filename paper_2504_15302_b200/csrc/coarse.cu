@@ -308,6 +308,7 @@ __device__ __forceinline__ float block_reduce_max(float v, float* sh) {
 // uncertified queries recompute every candidate (or every centroid) exactly.
 template <bool kStage>
 __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const SelectParams p) {
+  RD_TS(13);  // entry, before the wait on the previous kernel
   RD_PDL_PROLOGUE();
   extern __shared__ __align__(16) uint32_t keys[];
   __shared__ int hist[2048];
@@ -579,6 +580,7 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
           if (in) {
             const int l = cand[i];
             p.probes[(size_t)b * p.nprobe + n + __popc(m & ((1u << lane) - 1u))] = l;
+            if (p.bitmap) atomicOr(p.bitmap + (size_t)l * p.W + (b >> 5), 1u << (b & 31));
             if (p.qthr) {
               const unsigned mo = __ballot_sync(m, lok[i] != 0);
               if (ls < 0 && mo) ls = __shfl_sync(m, l, __ffs(mo) - 1);
@@ -658,7 +660,10 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
       __syncthreads();
       if (certified) break;
     }
-    for (int i = tid; i < p.nprobe; i += kSelThreads) p.probes[(size_t)b * p.nprobe + i] = i < np ? cand[i] : -1;
+    for (int i = tid; i < p.nprobe; i += kSelThreads) {
+      p.probes[(size_t)b * p.nprobe + i] = i < np ? cand[i] : -1;
+      if (p.bitmap && i < np) atomicOr(p.bitmap + (size_t)cand[i] * p.W + (b >> 5), 1u << (b & 31));
+    }
     if (p.qthr && tid == 0) {
       lsel = -1;
       for (int i = 0; i < np; ++i) {

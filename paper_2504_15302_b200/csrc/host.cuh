@@ -239,10 +239,12 @@ struct rd_index {
   int tc_min_q = rd::kTcMinQ;
   int debug_skip = 0;  // profiling only
   bool dbg_ts = std::getenv("RD_DEBUG_TS") != nullptr;  // profiling only: select checkpoints to stderr
+  // profiling only: checkpoints of every kernel of one search, taken without serialising the chain
+  bool dbg_chain = std::getenv("RD_DEBUG_CHAIN") != nullptr;
   int stage_max_b = -1;  // batches up to this size stage exact-distance rows in smem (-1: 2 x SMs)
   int tiles_per_sm = 8;  // scan tiles per SM the planner aims for (RD_TILES_PER_SM)
   long long seed_max_b = 1LL << 40;  // batches up to this size seed the scan's pruning threshold (RD_SEED_MAX_B)
-  bool no_inner_events = std::getenv("RD_NO_INNER_EVENTS") != nullptr;  // A/B: no per-stage timing events
+  bool stage_events = false;  // rd_timing_stages: per-stage events between the chain's kernels
   // the tensor-core scan stages 64-dim bf16 query slices of up to 32 queries in shared memory:
   // d % 64 == 0 and d <= 896 (beyond, its B operand does not fit next to the x ring); else FFMA
   bool tc_scan() const { return d % 64 == 0 && rd::scan_tc_smem_bytes(d, 32) <= 227 * 1024; }
@@ -295,6 +297,7 @@ struct rd_index {
     DBuf<float> qnorm, Dc, q, qsplit;
     DBuf<int> probes, list_nq, list_qoff, list_ntile, list_toff, list_q, part_count, part_row, off_meta;
     DBuf<unsigned> bitmap, fb_ctr;
+    bool bitmap_clean = false;  // the bitmap is all-zero (the plan's list_fill re-zeroes it)
     DBuf<rd::ScanTile> tiles, tiles16, ff_tiles, off_tiles;  // wide / narrow tensor-core, FFMA, offloaded
     DBuf<float> part_dist;
     DBuf<long long> fb_id;
@@ -317,6 +320,7 @@ struct rd_index {
   // device-time accounting: 4 events per search (start, plan done, resident scan done, end)
   static constexpr int kRing = 64;
   cudaEvent_t tev[kRing][4] = {};
+  bool tev_staged[kRing] = {};
   long long t_recorded = 0, t_accounted = 0;
   rd_timing t_acc{};
 
@@ -324,7 +328,8 @@ struct rd_index {
     cudaEvent_t* e = tev[i % kRing];
     CK(cudaEventSynchronize(e[3]));
     float a = 0, b = 0, c = 0, t = 0;
-    if (!no_inner_events) {
+    if (tev_staged[i % kRing]) {
+      t_acc.stage_searches += 1;
       CK(cudaEventElapsedTime(&a, e[0], e[1]));
       CK(cudaEventElapsedTime(&b, e[1], e[2]));
       CK(cudaEventElapsedTime(&c, e[2], e[3]));
@@ -338,6 +343,7 @@ struct rd_index {
   }
   cudaEvent_t* next_timing_slot() {
     if (t_recorded - t_accounted >= kRing) account(t_accounted++);
+    tev_staged[t_recorded % kRing] = stage_events;
     return tev[t_recorded++ % kRing];
   }
   std::vector<cudaEvent_t> slot_ready, slot_done;
@@ -457,7 +463,7 @@ struct rd_index {
       if (t[16 + i]) fprintf(stderr, " %d:%lld", i, (long long)(t[16 + i] - t[16]));
     fprintf(stderr, "\n");
   }
-  DBuf<unsigned long long> dbg_buf, dbg_scan, dbg_stall;
+  DBuf<unsigned long long> dbg_buf, dbg_scan, dbg_stall, dbg_chain_buf;
 
   // H2D staging ring for offloaded lists: `slots` slots of `slot_rows` rows (0 slots: none)
   void set_staging(int nslots, long long nrows) {

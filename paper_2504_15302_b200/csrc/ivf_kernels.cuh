@@ -144,6 +144,10 @@ struct SelectParams {
   int* qthr;
   int exact_order;         // 1: probes in exact (distance, list id) order (rd_probe); 0: the set (search)
   unsigned long long* dbg = nullptr;  // RD_DEBUG_TS: globaltimer checkpoints of CTA 0
+  // the multi-kernel plan's list x query bitmap (nlist x W words, zero on entry): the selection
+  // sets each probe's bit as it writes the probe, so the plan needs no inversion pass
+  unsigned* bitmap = nullptr;
+  int W = 0;
 };
 // stage: q and candidate rows go through shared memory (latency-bound small batches)
 cudaError_t launch_select(const SelectParams& p, bool stage, cudaStream_t s);
@@ -174,6 +178,9 @@ struct PlanParams {
 cudaError_t launch_plan(const PlanParams& p, cudaStream_t s);
 bool plan_fused_ok(int B, int nlist);  // the single-CTA bitmap plan applies
 bool plan_small_ok(int B, int nprobe);  // the single-CTA sorted-pairs plan applies (B * nprobe <= 512)
+// the multi-kernel plan reads the bitmap the selection filled (SelectParams::bitmap) and leaves it
+// zero again for the next search
+inline bool plan_uses_bitmap(int B, int nprobe, int nlist) { return !plan_small_ok(B, nprobe) && !plan_fused_ok(B, nlist); }
 
 struct MergeParams {
   const float* part_dist;

@@ -22,6 +22,7 @@ constexpr long long kNoKey = 0x7fffffffffffffffll;
 // row from global memory (enough CTAs are resident to hide the latency).
 template <bool kStage>
 __global__ void __launch_bounds__(256) merge_rerank_kernel(const MergeParams p) {
+  RD_TS(13);  // entry, before the wait on the previous kernel
   RD_PDL_PROLOGUE();
   extern __shared__ __align__(16) float dyn[];  // kStage: q[d], rows[32][d + kStagePad]
   __shared__ float sd[8][kTopK];

@@ -15,15 +15,6 @@ namespace rd {
 
 namespace {
 
-__global__ void invert_set_kernel(const int* __restrict__ probes, unsigned* __restrict__ bitmap,
-                                  int W, int B, int nprobe) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= (long long)B * nprobe) return;
-  const int b = (int)(i / nprobe);
-  const int l = probes[i];
-  if (l >= 0) atomicOr(bitmap + (size_t)l * W + (b >> 5), 1u << (b & 31));
-}
-
 // Query groups per chunk of one list, by category. A list probed by >= tc_min_q queries goes to
 // the tensor cores: in mixed mode (tc_mode 0) a list of <= 16 queries is one narrow group and a
 // larger one balanced wide groups of <= 32 (usually one, so the list's bytes are read once);
@@ -80,8 +71,10 @@ __device__ __forceinline__ void emit_tiles(const PlanParams& p, int j, int nq, i
   }
 }
 
-// warp per list: query count and resident tile counts per category
+// warp per list: query count and resident tile counts per category (the bitmap was filled by the
+// selection kernel, coarse.cu)
 __global__ void list_count_kernel(const PlanParams p) {
+  RD_PDL_PROLOGUE();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= p.nlist) return;
   const unsigned* row = p.bitmap + (size_t)warp * p.W;
@@ -178,6 +171,7 @@ __device__ __forceinline__ void finish_counters(const PlanParams& p, unsigned lo
 // single CTA: exclusive scans of list_nq and the tile counts; totals and byte counters. Lists are
 // visited in rounds of 1024 (thread t <-> list round * 1024 + t) so every global access coalesces.
 __global__ void __launch_bounds__(1024) list_scan_kernel(const PlanParams p) {
+  RD_PDL_PROLOGUE();
   __shared__ int wsum[1 + kTileCats][32];
   __shared__ int carry[1 + kTileCats];
   __shared__ unsigned long long wcnt[3][32];
@@ -208,17 +202,20 @@ __global__ void __launch_bounds__(1024) list_scan_kernel(const PlanParams p) {
   finish_counters<1024>(p, cc, wcnt, carry + 1);
 }
 
-// warp per list: ascending query ids, then the list's tiles
+// warp per list: ascending query ids, then the list's tiles. Each bitmap word is zeroed once read,
+// so the bitmap is all-zero again for the next search's selection.
 __global__ void list_fill_kernel(const PlanParams p) {
+  RD_PDL_PROLOGUE();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= p.nlist) return;
   const int nq = p.list_nq[warp];
-  if (nq == 0) return;
-  const unsigned* row = p.bitmap + (size_t)warp * p.W;
+  if (nq == 0) return;  // no bit set: the list's words are zero already
+  unsigned* row = p.bitmap + (size_t)warp * p.W;
   int out = p.list_qoff[warp];
   for (int w0 = 0; w0 < p.W; w0 += 32) {
     const int w = w0 + lane;
     const unsigned bits = w < p.W ? row[w] : 0u;
+    if (bits) row[w] = 0u;
     const int c = __popc(bits);
     int incl = c;
 #pragma unroll
@@ -256,6 +253,7 @@ __global__ void list_fill_kernel(const PlanParams p) {
 // (lane = tile), since scattered per-thread stores from one SM are what bounds this kernel.
 constexpr int kPlanThreads = 1024;
 __global__ void __launch_bounds__(kPlanThreads) plan_fused_kernel(const PlanParams p) {
+  RD_TS(13);  // entry, before the wait on the previous kernel
   RD_PDL_PROLOGUE();
   extern __shared__ unsigned bm[];  // nlist x W bitmap, then slen[nlist] (list length, ~len if offloaded)
   __shared__ int wsum[1 + kTileCats][32];
@@ -363,6 +361,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_fused_kernel(const PlanPara
 // list_nq. Same outputs as the bitmap planners for every list.
 constexpr int kSmallPlanThreads = 1024;
 __global__ void __launch_bounds__(kSmallPlanThreads) plan_small_kernel(const PlanParams p) {
+  RD_TS(13);  // entry, before the wait on the previous kernel
   RD_PDL_PROLOGUE();
   __shared__ unsigned long long key[kSmallPlanThreads];
   __shared__ int wsum[kTileCats][32];
@@ -446,15 +445,12 @@ cudaError_t launch_plan(const PlanParams& p, cudaStream_t s) {
     const int smem = p.nlist * (p.W + 1) * (int)sizeof(unsigned);
     return launch_k(plan_fused_kernel, dim3(1), dim3(kPlanThreads), smem, s, p);
   }
-  cudaError_t e = cudaMemsetAsync(p.bitmap, 0, sizeof(unsigned) * (size_t)p.nlist * p.W, s);
-  if (e != cudaSuccess) return e;
-  const long long np = (long long)p.B * p.nprobe;
-  invert_set_kernel<<<(unsigned)((np + 255) / 256), 256, 0, s>>>(p.probes, p.bitmap, p.W, p.B, p.nprobe);
+  // the selection filled p.bitmap (plan_uses_bitmap); count -> scan -> fill, chained with PDL
   const int blocks = (p.nlist * 32 + 255) / 256;
-  list_count_kernel<<<blocks, 256, 0, s>>>(p);
-  list_scan_kernel<<<1, 1024, 0, s>>>(p);
-  list_fill_kernel<<<blocks, 256, 0, s>>>(p);
-  return cudaGetLastError();
+  cudaError_t e = launch_k(list_count_kernel, dim3(blocks), dim3(256), 0, s, p);
+  if (e == cudaSuccess) e = launch_k(list_scan_kernel, dim3(1), dim3(1024), 0, s, p);
+  if (e == cudaSuccess) e = launch_k(list_fill_kernel, dim3(blocks), dim3(256), 0, s, p);
+  return e;
 }
 
 }  // namespace rd

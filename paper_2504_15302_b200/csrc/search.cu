@@ -60,7 +60,6 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   w.qnorm.ensure(B);
   w.Dc.ensure((size_t)B * nl);
   w.probes.ensure((size_t)B * nprobe);
-  w.bitmap.ensure((size_t)nl * W);
   w.list_nq.ensure(nl);
   w.list_qoff.ensure(nl);
   w.list_ntile.ensure(rd::kTileCats * (size_t)nl);
@@ -99,14 +98,35 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   if (!seed) CK(cudaMemsetAsync(w.qthr.p, 0x7f, sizeof(int) * B, s));  // no threshold: huge
   rd::SelectParams sp{w.Dc.p, d_q, w.qnorm.p, h->centroids.p, w.probes.p, w.fails(), (int)B, nl, nprobe, d, h->cmax,
                       h->d_list_off.p, h->d_res_row0.p, h->arena.p, h->xmax, seed ? w.qthr.p : nullptr, 0};
+  unsigned long long* chain = nullptr;  // profiling only (RD_DEBUG_CHAIN): [select 32][plan 32][merge 32][scan 4/CTA]
+  if (h->dbg_chain) {
+    const size_t n = 96 + 4 * (size_t)h->num_sms;
+    if (h->dbg_chain_buf.n < n) h->dbg_chain_buf.alloc(n);
+    chain = h->dbg_chain_buf.p;
+    CK(cudaMemsetAsync(chain, 0, 8 * n, s));
+    sp.dbg = chain;
+  }
+  const bool use_bm = rd::plan_uses_bitmap((int)B, nprobe, nl);
+  if (use_bm) {  // zeroed on (re)allocation or after a search that stopped before its plan
+    if (w.bitmap.n < (size_t)nl * W || !w.bitmap_clean) {
+      w.bitmap.ensure((size_t)nl * W);
+      CK(cudaMemsetAsync(w.bitmap.p, 0, sizeof(unsigned) * w.bitmap.n, s));
+    }
+    w.bitmap_clean = false;
+    sp.bitmap = w.bitmap.p;
+    sp.W = W;
+  }
   h->traced("select", s, sp.dbg, [&] { CK(rd::launch_select(sp, h->stage_rows(B), s)); });
   launches += rd::coarse_small((int)B) ? 2 : 3;  // (query prep +) coarse + select
   rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
                     w.list_ntile.p, w.list_toff.p, w.list_q.p, {w.tiles16.p, w.tiles.p, w.ff_tiles.p}, w.meta(),
                     w.counters(), (int)B, nl, nprobe, pl.R, h->tc_scan() ? h->tc_min_q : 1 << 30, tc_mode};
+  if (chain) pp.dbg = chain + 32;
   h->traced("plan", s, pp.dbg, [&] { CK(rd::launch_plan(pp, s)); });
-  launches += rd::plan_small_ok((int)B, nprobe) || rd::plan_fused_ok((int)B, nl) ? 1 : 4;
-  if (!h->no_inner_events) CK(cudaEventRecord(e1, s));
+  if (use_bm) w.bitmap_clean = true;  // list_fill, now enqueued, clears every bit the selection sets
+  launches += use_bm ? 3 : 1;
+  const bool staged = h->stage_events;
+  if (staged) CK(cudaEventRecord(e1, s));
 
   const bool has_off = h->slots > 0;
   if (has_off) {  // fetch the probe histogram for host-side staging decisions
@@ -115,7 +135,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     CK(cudaMemcpyAsync(w.h_nq.p, w.list_nq.p, sizeof(int) * nl, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(w.h_qoff.p, w.list_qoff.p, sizeof(int) * nl, cudaMemcpyDeviceToHost, s));
   }
-  CK(cudaEventRecord(e_plan, s));
+  if (has_off) CK(cudaEventRecord(e_plan, s));  // an event between two kernels costs their PDL overlap
   const CUtensorMap gmap = make_gather_map(w.qsplit.p, B, d);
   rd::ScanParams sc{w.ff_tiles.p, w.meta() + 2 * rd::kCatFfma, w.meta() + 2 * rd::kCatFfma + 1, d_q, w.qnorm.p,
                     w.list_q.p, h->xnorm.p, w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p};
@@ -127,6 +147,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     launches += 1;
   }
   if (h->tc_scan()) {  // otherwise every tile is FFMA
+    if (chain) tc.dbg = chain + 96;
     if (h->dbg_ts) {  // profiling only: per-CTA entry / ready / first tile / end times
       if (h->dbg_scan.n < 4 * (size_t)h->num_sms) h->dbg_scan.alloc(4 * (size_t)h->num_sms);
       CK(cudaMemsetAsync(h->dbg_scan.p, 0, 8 * 4 * (size_t)h->num_sms, s));
@@ -184,7 +205,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
               mx[2], mean[3], mx[3]);
     }
   }
-  if (!h->no_inner_events) CK(cudaEventRecord(e2, s));
+  if (staged) CK(cudaEventRecord(e2, s));
 
   unsigned long long h2d = 0;
   if (has_off) {
@@ -323,12 +344,42 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
                      h->d_list_base.p, h->d_ids.p, h->d_row_list.p, h->arena.p,
                      h->arena.p + (size_t)h->n_resident * d, nl, d, k, h->xmax, d_ids, d_dists,
                      w.fails() + 1, w.fail_list.p, (int)B};
+  if (chain) mp.dbg = chain + 64;
   h->traced("merge", s, mp.dbg, [&] { CK(rd::launch_merge(mp, h->stage_rows(B), s)); });
   rd::FallbackParams fp{w.fail_list.p, w.fails() + 1, w.probes.p, nprobe, d_q, h->d_list_off.p, h->d_list_base.p,
                         h->d_ids.p, nl, d, k, w.fb_dist.p, w.fb_id.p, d_ids, d_dists, w.fb_ctr.p};
   CK(rd::launch_fallback(fp, h->num_sms, s));
   launches += 2;
   CK(cudaEventRecord(te[3], s));
+  if (chain) {  // ns from select's entry: [13] = entry (before the PDL wait), [0] = past the wait
+    std::vector<unsigned long long> t(96 + 4 * (size_t)h->num_sms);
+    CK(cudaMemcpyAsync(t.data(), chain, 8 * t.size(), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const long long t0 = (long long)t[13];
+    const char* nm[3] = {"select", "plan", "merge"};
+    for (int kk = 0; kk < 3; ++kk) {
+      fprintf(stderr, "%s:", nm[kk]);
+      if (t[32 * kk + 13]) fprintf(stderr, " entry=%lld", (long long)t[32 * kk + 13] - t0);
+      for (int i = 0; i < 13; ++i)
+        if (t[32 * kk + i]) fprintf(stderr, " %d=%lld", i, (long long)t[32 * kk + i] - t0);
+      fprintf(stderr, "\n");
+    }
+    long long mn[4], mx[4];
+    double mean[4];
+    for (int j = 0; j < 4; ++j) {
+      mn[j] = 1LL << 62, mx[j] = -(1LL << 62), mean[j] = 0;
+      int cnt = 0;
+      for (int c = 0; c < h->num_sms; ++c) {
+        const unsigned long long v = t[96 + 4 * c + j];
+        if (!v) continue;
+        const long long r = (long long)v - t0;
+        mn[j] = std::min(mn[j], r), mx[j] = std::max(mx[j], r), mean[j] += r, ++cnt;
+      }
+      if (cnt) mean[j] /= cnt;
+    }
+    fprintf(stderr, "scan: entry %lld/%.0f/%lld ready %lld/%.0f/%lld first %lld/%.0f/%lld end %lld/%.0f/%lld (min/mean/max)\n",
+            mn[0], mean[0], mx[0], mn[1], mean[1], mx[1], mn[2], mean[2], mx[2], mn[3], mean[3], mx[3]);
+  }
   if (st) {
     std::memset(st, 0, sizeof *st);
     st->kernel_launches = launches;
@@ -350,7 +401,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
       st->bytes_algorithmic = (hc[1] + hc[2]) * row_bytes + (unsigned long long)nl * row_bytes +
                               (unsigned long long)B * row_bytes + (unsigned long long)B * k * 12ull;
       st->tiles = (uint64_t)hm[0] + (uint64_t)hm[2] + (uint64_t)hm[4];
-      if (!h->no_inner_events) {
+      if (staged) {
         CK(cudaEventElapsedTime(&ms, e1, e2));
         st->scan_ms = ms;
         CK(cudaEventElapsedTime(&ms, e0, e1));
@@ -494,6 +545,13 @@ int rd_probe(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32
                         h->d_list_off.p, h->d_res_row0.p, h->arena.p, h->xmax, nullptr, 1};
     CK(rd::launch_select(sp, h->stage_rows(B), 0));
     CK(cudaMemcpy(out_lists, w.probes.p, sizeof(int) * B * nprobe, cudaMemcpyDeviceToHost));
+  });
+}
+
+int rd_timing_stages(rd_index* h, int32_t on) {
+  return guarded([&] {
+    if (!h) throw_rd(RD_ERR_INVALID, "null index");
+    h->stage_events = on != 0;
   });
 }
 

@@ -81,7 +81,7 @@ class IndexInfo(C.Structure):
 
 class Timing(C.Structure):
     _fields_ = [("searches", C.c_int64), ("scan_ms", C.c_double), ("coarse_ms", C.c_double),
-                ("tail_ms", C.c_double), ("total_ms", C.c_double)]
+                ("tail_ms", C.c_double), ("total_ms", C.c_double), ("stage_searches", C.c_int64)]
 
 
 class LlmReservation(C.Structure):
@@ -119,6 +119,7 @@ _SIGS = {
     "rd_merge_topk": (C.c_int, [C.c_int32, C.c_int64, C.c_int32, _I64P, _FP, _I64P, _FP]),
     "rd_merge_topk_device": (C.c_int, [C.c_int32, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                        C.c_void_p, C.c_void_p]),
+    "rd_timing_stages": (C.c_int, [_P, C.c_int32]),
     "rd_timing_reset": (C.c_int, [_P]),
     "rd_timing_read": (C.c_int, [_P, C.POINTER(Timing)]),
     "rd_derive_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
@@ -366,6 +367,10 @@ class Index:
     def save(self, path: str) -> None:
         """Writes the index in the on-disk format (include/rd_format.h)."""
         self._lib.check(self._lib.lib.rd_index_save(self._h, os.fsencode(path)), "save")
+
+    def timing_stages(self, on: bool) -> None:
+        """Per-stage device timing (coarse / scan / tail) for the following searches (rd.h)."""
+        self._lib.check(self._lib.lib.rd_timing_stages(self._h, 1 if on else 0), "timing_stages")
 
     def timing_reset(self) -> None:
         self._lib.check(self._lib.lib.rd_timing_reset(self._h), "timing_reset")

@@ -20,11 +20,13 @@ ap.add_argument("--k", type=int, default=10)
 ap.add_argument("--searches", type=int, default=3)
 ap.add_argument("--offload", type=float, default=0.0)
 ap.add_argument("--stripe-of", type=int, default=1)
+ap.add_argument("--no-stages", action="store_true", help="no per-stage events (as the product runs)")
 args = ap.parse_args()
 torch.cuda.init()
 lib = engine()
 desc = lib.desc(args.n, 768, args.nlist, num_shards=args.stripe_of)
 idx = lib.synthetic_index(desc)
+idx.timing_stages(not args.no_stages)
 if args.offload:
     idx.place(offload_fraction=args.offload)
 for i in range(args.searches):
