@@ -242,7 +242,7 @@ struct rd_index {
   // profiling only: checkpoints of every kernel of one search, taken without serialising the chain
   bool dbg_chain = std::getenv("RD_DEBUG_CHAIN") != nullptr;
   int stage_max_b = -1;  // batches up to this size stage exact-distance rows in smem (-1: 2 x SMs)
-  int tiles_per_sm = 8;  // scan tiles per SM the planner aims for (RD_TILES_PER_SM)
+  int tiles_per_sm = 0;  // scan tiles per SM the planner aims for (RD_TILES_PER_SM; 0 = by batch, make_plan)
   long long seed_max_b = 1LL << 40;  // batches up to this size seed the scan's pruning threshold (RD_SEED_MAX_B)
   bool stage_events = false;  // rd_timing_stages: per-stage events between the chain's kernels
   // the tensor-core scan stages 64-dim bf16 query slices of up to 32 queries in shared memory:

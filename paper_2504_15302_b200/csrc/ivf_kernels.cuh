@@ -157,6 +157,18 @@ cudaError_t launch_select(const SelectParams& p, bool stage, cudaStream_t s);
 constexpr int kTileCats = 3;
 constexpr int kCatNarrow = 0, kCatWide = 1, kCatFfma = 2;
 
+// Rows per scan chunk of a list of `len` rows under the plan's cap R (a multiple of kTcRows): the
+// fewest chunks of <= R rows, balanced and rounded up to the tensor-core tile, so a list is not cut
+// into full chunks plus a short remainder (2441 rows at R = 1152: 896 + 896 + 649, not
+// 1152 + 1152 + 137) — every tile costs the scan a fixed overhead, whatever its length.
+__host__ __device__ __forceinline__ int chunk_rows(long long len, int R) {
+  if (len <= R) return R;
+  const long long n = (len + R - 1) / R;
+  const long long r = (len + n - 1) / n;
+  const long long rr = (r + kTcRows - 1) / kTcRows * kTcRows;
+  return (int)(rr < R ? rr : R);
+}
+
 struct PlanParams {
   const int* probes;          // B x nprobe
   unsigned* bitmap;           // nlist x W

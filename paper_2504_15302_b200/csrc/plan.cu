@@ -40,7 +40,7 @@ __device__ __forceinline__ Groups group_split(int nq, const PlanParams& p) {
 // (lanes of a warp, or one thread). toff: the list's first tile in each category's array.
 __device__ __forceinline__ void emit_tiles(const PlanParams& p, int j, int nq, int qoff, int len, long long src0,
                                            long long g0, const int (&toff)[kTileCats], const Groups& G, int chunks,
-                                           int c0, int cstep) {
+                                           int rl, int c0, int cstep) {
 #pragma unroll
   for (int cat = 0; cat < kTileCats; ++cat) {
     const int ng = G.g[cat];
@@ -59,10 +59,10 @@ __device__ __forceinline__ void emit_tiles(const PlanParams& p, int j, int nq, i
       ScanTile* dst = p.tiles[cat] + toff[cat] + g;
       for (int c = c0; c < chunks; c += cstep) {
         ScanTile T;
-        T.src_row = src0 + (long long)c * p.R;
-        T.grow0 = g0 + (long long)c * p.R;
+        T.src_row = src0 + (long long)c * rl;
+        T.grow0 = g0 + (long long)c * rl;
         T.list = j;
-        T.nrows = min(p.R, len - c * p.R);
+        T.nrows = min(rl, len - c * rl);
         T.qoff = tq0;
         T.nq = tnq;
         dst[c * ng] = T;
@@ -88,7 +88,8 @@ __global__ void list_count_kernel(const PlanParams p) {
     Groups G = {{0, 0, 0}};
     int chunks = 0;
     if (c > 0 && len > 0 && p.res_row0[warp] >= 0) {
-      chunks = ((int)len + p.R - 1) / p.R;  // 32-bit: rows per list < 2^31
+      const int rl = chunk_rows(len, p.R);
+      chunks = ((int)len + rl - 1) / rl;  // 32-bit: rows per list < 2^31
       G = group_split(c, p);
     }
 #pragma unroll
@@ -237,13 +238,14 @@ __global__ void list_fill_kernel(const PlanParams p) {
   for (int cat = 0; cat < kTileCats; ++cat) total += p.list_ntile[cat * p.nlist + warp];
   if (total == 0) return;
   const long long len = p.list_off[warp + 1] - p.list_off[warp];
-  const int chunks = ((int)len + p.R - 1) / p.R;  // 32-bit: rows per list < 2^31
+  const int rl = chunk_rows(len, p.R);
+  const int chunks = ((int)len + rl - 1) / rl;  // 32-bit: rows per list < 2^31
   const Groups G = group_split(nq, p);
   int toff[kTileCats];
 #pragma unroll
   for (int cat = 0; cat < kTileCats; ++cat) toff[cat] = p.list_toff[cat * p.nlist + warp];
-  emit_tiles(p, warp, nq, p.list_qoff[warp], (int)len, p.res_row0[warp], p.list_off[warp], toff, G, chunks, lane,
-             32);
+  emit_tiles(p, warp, nq, p.list_qoff[warp], (int)len, p.res_row0[warp], p.list_off[warp], toff, G, chunks, rl,
+             lane, 32);
 }
 
 // Small batches: the whole plan in one CTA with the list x query bitmap in shared memory (one
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_fused_kernel(const PlanPara
   unsigned long long cc[3] = {0, 0, 0};  // unique probed lists, resident rows, offloaded rows
   for (int j0 = 0; j0 < nl; j0 += kPlanThreads) {
     const int j = j0 + tid;
-    int nq = 0, len = 0, chunks = 0;
+    int nq = 0, len = 0, chunks = 0, rl = p.R;
     Groups G = {{0, 0, 0}};
     long long src0 = 0, g0 = 0;
     if (j < nl) {
@@ -304,7 +306,8 @@ __global__ void __launch_bounds__(kPlanThreads) plan_fused_kernel(const PlanPara
         ++cc[0];
         cc[sl >= 0 ? 1 : 2] += len;
         if (sl >= 0 && len > 0) {
-          chunks = (len + p.R - 1) / p.R;
+          rl = chunk_rows(len, p.R);
+          chunks = (len + rl - 1) / rl;
           G = group_split(nq, p);
           src0 = p.res_row0[j];
           g0 = p.list_off[j];
@@ -347,7 +350,8 @@ __global__ void __launch_bounds__(kPlanThreads) plan_fused_kernel(const PlanPara
       }
       if (any > 0)
         emit_tiles(p, lj, lnq, qo, __shfl_sync(0xffffffffu, len, src), __shfl_sync(0xffffffffu, src0, src),
-                   __shfl_sync(0xffffffffu, g0, src), toff, LG, __shfl_sync(0xffffffffu, chunks, src), lane, 32);
+                   __shfl_sync(0xffffffffu, g0, src), toff, LG, __shfl_sync(0xffffffffu, chunks, src),
+                   __shfl_sync(0xffffffffu, rl, src), lane, 32);
     }
   }
   RD_TS(3);
@@ -391,7 +395,7 @@ __global__ void __launch_bounds__(kSmallPlanThreads) plan_small_kernel(const Pla
   const unsigned long long mine = tid < valid ? key[tid] : ~0ull;
   const int l = (int)(mine >> 32);
   const bool start = tid < valid && (tid == 0 || (key[tid - 1] >> 32) != (mine >> 32));
-  int nq = 0, chunks = 0, len = 0;
+  int nq = 0, chunks = 0, len = 0, rl = p.R;
   Groups G = {{0, 0, 0}};
   long long src0 = -1, g0 = 0;
   if (start) {
@@ -402,7 +406,8 @@ __global__ void __launch_bounds__(kSmallPlanThreads) plan_small_kernel(const Pla
     len = (int)(p.list_off[l + 1] - g0);
     src0 = p.res_row0[l];
     if (src0 >= 0 && len > 0) {
-      chunks = (len + p.R - 1) / p.R;
+      rl = chunk_rows(len, p.R);
+      chunks = (len + rl - 1) / rl;
       G = group_split(nq, p);
     }
   }
@@ -421,7 +426,7 @@ __global__ void __launch_bounds__(kSmallPlanThreads) plan_small_kernel(const Pla
     int any = 0;
 #pragma unroll
     for (int cat = 0; cat < kTileCats; ++cat) any += G.g[cat];
-    if (any > 0) emit_tiles(p, l, nq, tid, len, src0, g0, ex, G, chunks, 0, 1);
+    if (any > 0) emit_tiles(p, l, nq, tid, len, src0, g0, ex, G, chunks, rl, 0, 1);
   }
   finish_counters<kSmallPlanThreads>(p, cc, wcnt, carry);
   RD_TS(3);

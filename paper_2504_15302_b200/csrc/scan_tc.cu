@@ -220,30 +220,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++u;
       };
       // ---- B operand by TMA gather4: rows 0-31 q1, 32-63 q2 of the tile's queries (qsplit row
-      // 2*qid + part); padding rows repeat the last query (their D columns are ignored)
-      RD_TWAIT(sm.bempty, (ti & 1) ^ 1, 2);
-      // only the quads holding real queries are loaded; the others keep stale rows whose D
-      // columns the epilogue never reads
+      // 2*qid + part); padding rows repeat the last query (their D columns are ignored). Only the
+      // quads holding real queries are loaded; the others keep stale rows whose D columns the
+      // epilogue never reads. Lane (grp, qi) owns quad qi of part qi / qq for slices grp, grp + ngrp..
       const int qq = (T.nq + 3) >> 2;  // quads per part
+      const int per = 2 * qq, ngrp = 32 / per, grp = lane / per, qi = lane - grp * per;
+      const int part = qi >= qq ? 1 : 0;
+      const int g0 = (qi - part * qq) * 4;
+      int r[4];
+      if (grp < ngrp)  // the ids load while the ring is refilled below
+#pragma unroll
+        for (int i = 0; i < 4; ++i) r[i] = 2 * __ldg(p.list_q + T.qoff + min(g0 + i, T.nq - 1)) + part;
+      // the first ring's worth of this tile's x stages go out before the wait for the B operand
+      // buffer (free once the previous tile's MMAs are done), so HBM keeps streaming across the
+      // tile boundary and only the gather's latency is exposed
+      const int npre = min(nst, RS);
+      if (lane == 0)
+        for (int i = 0; i < npre; ++i) issue_x(i);
+      __syncwarp();
+      RD_TWAIT(sm.bempty, (ti & 1) ^ 1, 2);
       // one barrier for the whole gather (per-slice barriers let the first MMAs start earlier but
       // cost more than they saved: A/B on B200, 1024 queries, 206.4k vs 207.2k q/s)
       if (lane == 0) mbar_arrive_expect_tx(sm.bfull, (uint32_t)(nslices * 2 * qq * 512));
       __syncwarp();
-      for (int gi = lane; gi < nslices * 2 * qq; gi += 32) {
-        const int slice = gi / (2 * qq), qi = gi % (2 * qq);
-        const int part = qi >= qq ? 1 : 0;
-        const int g0 = (qi - part * qq) * 4;
-        const int quad = part * (kTcG / 4) + g0 / 4;
-        int r[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int g = min(g0 + i, T.nq - 1);
-          r[i] = 2 * __ldg(p.list_q + T.qoff + g) + part;
-        }
-        tma_gather4_u32(sm.bs + slice * kBSlice + quad * 512, &qmap, slice * 64, r[0], r[1], r[2], r[3], sm.bfull);
+      if (grp < ngrp) {
+        const uint32_t dst = sm.bs + (part * (kTcG / 4) + g0 / 4) * 512;
+        for (int slice = grp; slice < nslices; slice += ngrp)
+          tma_gather4_u32(dst + slice * kBSlice, &qmap, slice * 64, r[0], r[1], r[2], r[3], sm.bfull);
       }
       if (lane == 0)
-        for (int i = 0; i < nst; ++i) issue_x(i);
+        for (int i = npre; i < nst; ++i) issue_x(i);
       __syncwarp();
     }
   }

@@ -28,12 +28,15 @@ Plan make_plan(const rd_index* h, long long B, int nprobe) {
   const double avg = h->nlist ? (double)h->n / h->nlist : 0.0;
   const double est_rows = std::min((double)h->n, (double)B * np * avg);
   // ~tiles_per_sm tiles per SM so the dynamic tile queue's tail (at most one tile per SM) stays
-  // short; rows rounded to the tensor-core tile (128), at least one 256-row TMA box of the FFMA scan
-  // when that path is in use
+  // short, against a fixed cost per tile (query-operand gather, partial top-k records). Measured on
+  // B200 (C2): 32 per SM up to a few hundred queries (+0.4-1.5 % over 8), 8 from 512 queries on,
+  // where one chunk per list keeps the partial records few. Rows rounded to the tensor-core tile
+  // (128), at least 256 (shorter tiles lost at one query), and at least one 256-row TMA box of the
+  // FFMA scan when that path is in use; chunk_rows then balances each list's chunks.
   const long long gran = rd::kTcRows;
-  long long R = (long long)std::ceil(est_rows / ((double)h->num_sms * h->tiles_per_sm));
-  R = std::max<long long>(h->tc_min_q > 1 || !h->tc_scan() ? rd::kScanRows : gran,
-                          std::min<long long>(4096, (R + gran - 1) / gran * gran));
+  const int tps = h->tiles_per_sm > 0 ? h->tiles_per_sm : (B >= 512 ? 8 : 32);
+  long long R = (long long)std::ceil(est_rows / ((double)h->num_sms * tps));
+  R = std::max<long long>(rd::kScanRows, std::min<long long>(4096, (R + gran - 1) / gran * gran));
   pl.R = (int)R;
   pl.max_chunks = (int)std::max<long long>(1, (h->max_len + R - 1) / R);
   pl.cap = np * pl.max_chunks * rd::kPartsPerTile;
@@ -237,13 +240,14 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
         const int nq = w.h_nq.p[l];
         const bool tcl = nq >= h->tc_min_q && h->tc_scan();
         const int ngr = tcl ? (nq + tc_g - 1) / tc_g : (nq + rd::kScanG - 1) / rd::kScanG;
-        for (long long c = 0; c * pl.R < len; ++c)
+        const int rl = rd::chunk_rows(len, pl.R);
+        for (long long c = 0; c * rl < len; ++c)
           for (int g = 0; g < ngr; ++g) {
             rd::ScanTile T;
-            T.src_row = srow + c * pl.R;
-            T.grow0 = h->list_off[l] + c * pl.R;
+            T.src_row = srow + c * rl;
+            T.grow0 = h->list_off[l] + c * rl;
             T.list = l;
-            T.nrows = (int)std::min<long long>(pl.R, len - c * pl.R);
+            T.nrows = (int)std::min<long long>(rl, len - c * rl);
             if (tcl) {
               const int q0 = (int)((long long)g * nq / ngr), q1 = (int)((long long)(g + 1) * nq / ngr);
               T.qoff = w.h_qoff.p[l] + q0;
