@@ -94,19 +94,42 @@ __global__ void __launch_bounds__(256) coarse_gemm_kernel(const float* __restric
 __device__ __forceinline__ void qprep_rows(const QprepArgs& a, long long r0, long long rstep, bool zero2_here) {
   const int lane = threadIdx.x & 31;
   if (a.zero2 && zero2_here && threadIdx.x < 2) a.zero2[threadIdx.x] = 0u;
-  __nv_bfloat16* qsplit = reinterpret_cast<__nv_bfloat16*>(a.qsplit);
+  constexpr int kV = 8;  // float4 per lane: d <= 1024
+  const int d4 = a.d / 4;
   for (long long r = r0; r < a.B; r += rstep) {
     if (a.zeroB && lane == 0) a.zeroB[r] = 0;
-    const float* x = a.Q + (size_t)r * a.d;
+    // the whole row is loaded before any use (stores to qsplit could alias it otherwise and keep
+    // the loads serialised, one round trip per 32 elements)
+    const float4* x = reinterpret_cast<const float4*>(a.Q + (size_t)r * a.d);
+    float4 v[kV];
+#pragma unroll
+    for (int k = 0; k < kV; ++k) {
+      const int i = lane + 32 * k;
+      v[k] = i < d4 ? __ldg(x + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     double s = 0.0;
-    for (int t = lane; t < a.d; t += 32) {
-      const float q = x[t];
-      const double v = q;
-      s += v * v;
-      if (qsplit) {
-        const __nv_bfloat16 h = __float2bfloat16_rn(q);
-        qsplit[(r * 2) * a.d + t] = h;
-        qsplit[(r * 2 + 1) * a.d + t] = __float2bfloat16_rn(q - __bfloat162float(h));
+#pragma unroll
+    for (int k = 0; k < kV; ++k) {
+      const int i = lane + 32 * k;
+      if (i >= d4) break;
+      const float q[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+      uint32_t hi[2], lo[2];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) s = fma((double)q[e], (double)q[e], s);  // squares are exact in fp64
+      if (a.qsplit) {
+#pragma unroll
+        for (int e = 0; e < 4; e += 2) {
+          const __nv_bfloat162 h = __floats2bfloat162_rn(q[e], q[e + 1]);
+          const __nv_bfloat162 l =
+              __floats2bfloat162_rn(q[e] - __low2float(h), q[e + 1] - __high2float(h));
+          hi[e / 2] = *reinterpret_cast<const uint32_t*>(&h);
+          lo[e / 2] = *reinterpret_cast<const uint32_t*>(&l);
+        }
+        __nv_bfloat16* qs = reinterpret_cast<__nv_bfloat16*>(a.qsplit);
+        uint2* q1 = reinterpret_cast<uint2*>(qs + (size_t)(r * 2) * a.d);
+        uint2* q2 = reinterpret_cast<uint2*>(qs + (size_t)(r * 2 + 1) * a.d);
+        q1[i] = make_uint2(hi[0], hi[1]);
+        q2[i] = make_uint2(lo[0], lo[1]);
       }
     }
 #pragma unroll
@@ -711,6 +734,7 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
     }
   }
   RD_TS(6);
+  RD_TS_END();
 }
 
 }  // namespace

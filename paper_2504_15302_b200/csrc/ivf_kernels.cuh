@@ -185,6 +185,9 @@ struct PlanParams {
   unsigned long long* counters;  // [0] unique lists, [1] resident rows probed, [2] offloaded rows probed
   int B, nlist, nprobe, R, tc_min_q;
   int tc_mode;                // 0: lists of <= 16 queries narrow, others wide; 16 / 32: one width
+  // lists j >= tail_from are cut at Rt (<= R) rows: the scan's dynamic queue hands out tiles in
+  // list order, so its last tiles are the short ones and the CTAs finish closer together
+  int Rt, tail_from;
   unsigned long long* dbg = nullptr;  // RD_DEBUG_TS: globaltimer checkpoints of CTA 0
 };
 cudaError_t launch_plan(const PlanParams& p, cudaStream_t s);

@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(256) merge_rerank_kernel(const MergeParams p) 
       }
     }
   }
+  RD_TS_END();
 }
 
 __global__ void shard_merge_kernel(int G, long long B, int k, const long long* __restrict__ ids,

@@ -88,7 +88,7 @@ __global__ void list_count_kernel(const PlanParams p) {
     Groups G = {{0, 0, 0}};
     int chunks = 0;
     if (c > 0 && len > 0 && p.res_row0[warp] >= 0) {
-      const int rl = chunk_rows(len, p.R);
+      const int rl = chunk_rows(len, warp >= p.tail_from ? p.Rt : p.R);
       chunks = ((int)len + rl - 1) / rl;  // 32-bit: rows per list < 2^31
       G = group_split(c, p);
     }
@@ -238,7 +238,7 @@ __global__ void list_fill_kernel(const PlanParams p) {
   for (int cat = 0; cat < kTileCats; ++cat) total += p.list_ntile[cat * p.nlist + warp];
   if (total == 0) return;
   const long long len = p.list_off[warp + 1] - p.list_off[warp];
-  const int rl = chunk_rows(len, p.R);
+  const int rl = chunk_rows(len, warp >= p.tail_from ? p.Rt : p.R);
   const int chunks = ((int)len + rl - 1) / rl;  // 32-bit: rows per list < 2^31
   const Groups G = group_split(nq, p);
   int toff[kTileCats];
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_fused_kernel(const PlanPara
         ++cc[0];
         cc[sl >= 0 ? 1 : 2] += len;
         if (sl >= 0 && len > 0) {
-          rl = chunk_rows(len, p.R);
+          rl = chunk_rows(len, j >= p.tail_from ? p.Rt : p.R);
           chunks = (len + rl - 1) / rl;
           G = group_split(nq, p);
           src0 = p.res_row0[j];
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(kSmallPlanThreads) plan_small_kernel(const Pla
     len = (int)(p.list_off[l + 1] - g0);
     src0 = p.res_row0[l];
     if (src0 >= 0 && len > 0) {
-      rl = chunk_rows(len, p.R);
+      rl = chunk_rows(len, l >= p.tail_from ? p.Rt : p.R);
       chunks = (len + rl - 1) / rl;
       G = group_split(nq, p);
     }

@@ -111,6 +111,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 // profiling only (RD_DEBUG_TS): globaltimer / clock64 checkpoints of CTA 0
+// profiling only: the latest end over all CTAs of a kernel at slot 12
+#define RD_TS_END()                                                              \
+  do {                                                                           \
+    if (p.dbg && threadIdx.x == 0) atomicMax(p.dbg + 12, gtimer());              \
+  } while (0)
+
 #define RD_TS(i)                                                 \
   do {                                                           \
     if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0) {          \

@@ -16,7 +16,7 @@ extern "C" {
 namespace {
 
 struct Plan {
-  int R;
+  int R, Rt, tail_from;
   int max_chunks;
   int cap;
   long long max_tiles;
@@ -38,7 +38,12 @@ Plan make_plan(const rd_index* h, long long B, int nprobe) {
   long long R = (long long)std::ceil(est_rows / ((double)h->num_sms * tps));
   R = std::max<long long>(rd::kScanRows, std::min<long long>(4096, (R + gran - 1) / gran * gran));
   pl.R = (int)R;
-  pl.max_chunks = (int)std::max<long long>(1, (h->max_len + R - 1) / R);
+  // the last eighth of the lists (in id order, the order the scan's queue hands tiles out) in
+  // quarter-size chunks: a shorter tail at one more tile per list there
+  pl.Rt = (int)std::max<long long>(rd::kScanRows, (R / 4 + gran - 1) / gran * gran);
+  pl.tail_from = h->nlist - h->nlist / 8;
+  if (const char* v = std::getenv("RD_TAIL_FRAC")) pl.tail_from = h->nlist - (int)(h->nlist * std::atof(v));
+  pl.max_chunks = (int)std::max<long long>(1, (h->max_len + pl.Rt - 1) / pl.Rt);
   pl.cap = np * pl.max_chunks * rd::kPartsPerTile;
   pl.max_tiles = std::min<long long>(B * np, B * np / rd::kScanG + h->nlist) * pl.max_chunks + 1;
   return pl;
@@ -123,7 +128,8 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   launches += rd::coarse_small((int)B) ? 2 : 3;  // (query prep +) coarse + select
   rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
                     w.list_ntile.p, w.list_toff.p, w.list_q.p, {w.tiles16.p, w.tiles.p, w.ff_tiles.p}, w.meta(),
-                    w.counters(), (int)B, nl, nprobe, pl.R, h->tc_scan() ? h->tc_min_q : 1 << 30, tc_mode};
+                    w.counters(), (int)B, nl, nprobe, pl.R, h->tc_scan() ? h->tc_min_q : 1 << 30, tc_mode,
+                    pl.Rt, pl.tail_from};
   if (chain) pp.dbg = chain + 32;
   h->traced("plan", s, pp.dbg, [&] { CK(rd::launch_plan(pp, s)); });
   if (use_bm) w.bitmap_clean = true;  // list_fill, now enqueued, clears every bit the selection sets
