@@ -573,7 +573,7 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
             e = exact_l2_group8_qd(qd, st + grp * ds, a < na ? d : 0, j8);
             __syncthreads();  // the staging area is reused by the next chunk
           } else {
-            e = exact_l2_group8_qd(qd, p.centroids + (size_t)cand[ambl[a < na ? a : na - 1]] * d, d, j8);
+            e = exact_l2_group8_qd<16>(qd, p.centroids + (size_t)cand[ambl[a < na ? a : na - 1]] * d, d, j8);
           }
           if (a < na && j8 == 0) adist[a] = e;
         }
@@ -716,7 +716,7 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
         stage_bulk(32, [&](int r) { return r0 + (size_t)r * d; });
         e = l2_group8_f32(qf, st + grp * ds, d, j8);
       } else {
-        e = l2_group8_f32(q, r0 + (size_t)grp * d, d, j8);
+        e = l2_group8_f32<16>(q, r0 + (size_t)grp * d, d, j8);
       }
       float m = e;
 #pragma unroll

@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(256) merge_rerank_kernel(const MergeParams p) 
     e = exact_l2_group8_impl<false>(dyn, st + c * (p.d + kStagePad), xp ? p.d : 0, j8);
   } else {
     // a padded slot runs zero terms so the warp stays converged for the shuffles
-    e = exact_l2_group8_any(q, xp ? xp : q, xp ? p.d : 0, j8);
+    e = exact_l2_group8_impl<false, 24>(q, xp ? xp : q, xp ? p.d : 0, j8);  // rows from HBM: 24 loads deep
   }
   if (!xp) e = kInf;
   if (j8 == 0) ex_d[c] = e;

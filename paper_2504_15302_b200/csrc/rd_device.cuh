@@ -34,21 +34,22 @@ __host__ __device__ __forceinline__ float unif(uint64_t seed, uint64_t i) {
 // Eight lanes j = lane & 7 of an aligned group each sum residue class t = j (mod 8)
 // sequentially in fp64 (no contraction), then the fixed tree
 // ((s0+s1)+(s2+s3))+((s4+s5)+(s6+s7)); every lane of the group returns the f32 value.
-template <bool kLdg>
+template <bool kLdg, int kDepth = 8>
 __device__ __forceinline__ float exact_l2_group8_impl(const float* __restrict__ q, const float* x, int d, int j) {
-  // loads are batched 8 deep ahead of the strictly sequential fp64 accumulation, which keeps
-  // the summation order (and so the result) canonical while hiding memory latency
+  // loads are batched kDepth deep ahead of the strictly sequential fp64 accumulation, which keeps
+  // the summation order (and so the result) canonical while hiding memory latency (deeper
+  // batches for rows streamed from HBM: fewer round trips per row)
   double s = 0.0;
   int t = j;
-  for (; t + 56 < d; t += 64) {
-    float qv[8], xv[8];
+  for (; t + 8 * (kDepth - 1) < d; t += 8 * kDepth) {
+    float qv[kDepth], xv[kDepth];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < kDepth; ++i) {
       qv[i] = kLdg ? __ldg(q + t + 8 * i) : q[t + 8 * i];
       xv[i] = kLdg ? __ldg(x + t + 8 * i) : x[t + 8 * i];
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < kDepth; ++i) {
       const double df = __dsub_rn((double)qv[i], (double)xv[i]);
       s = __dadd_rn(s, __dmul_rn(df, df));
     }
@@ -63,15 +64,16 @@ __device__ __forceinline__ float exact_l2_group8_impl(const float* __restrict__ 
   return __double2float_rn(s);
 }
 // same value with q already widened to fp64 (shared memory): half the conversions
+template <int kDepth = 8>
 __device__ __forceinline__ float exact_l2_group8_qd(const double* qd, const float* x, int d, int j) {
   double s = 0.0;
   int t = j;
-  for (; t + 56 < d; t += 64) {
-    float xv[8];
+  for (; t + 8 * (kDepth - 1) < d; t += 8 * kDepth) {
+    float xv[kDepth];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) xv[i] = x[t + 8 * i];
+    for (int i = 0; i < kDepth; ++i) xv[i] = x[t + 8 * i];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < kDepth; ++i) {
       const double df = __dsub_rn(qd[t + 8 * i], (double)xv[i]);
       s = __dadd_rn(s, __dmul_rn(df, df));
     }
@@ -152,9 +154,24 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint3
 }
 // fp32 squared distance by groups of 8 lanes (same lane/class layout as the canonical sum);
 // |result - ||q - x||^2| <= l2_f32_rel_bound(d) * ||q - x||^2
+template <int kDepth = 1>
 __device__ __forceinline__ float l2_group8_f32(const float* q, const float* x, int d, int j) {
   float s = 0.f;
-  for (int t = j; t < d; t += 8) {
+  int t = j;
+  for (; t + 8 * (kDepth - 1) < d; t += 8 * kDepth) {  // kDepth loads in flight, same summation order
+    float qv[kDepth], xv[kDepth];
+#pragma unroll
+    for (int i = 0; i < kDepth; ++i) {
+      qv[i] = q[t + 8 * i];
+      xv[i] = x[t + 8 * i];
+    }
+#pragma unroll
+    for (int i = 0; i < kDepth; ++i) {
+      const float df = qv[i] - xv[i];
+      s = fmaf(df, df, s);
+    }
+  }
+  for (; t < d; t += 8) {
     const float df = q[t] - x[t];
     s = fmaf(df, df, s);
   }
