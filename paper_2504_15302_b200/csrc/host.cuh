@@ -247,7 +247,8 @@ struct rd_index {
   bool stage_events = false;  // rd_timing_stages: per-stage events between the chain's kernels
   // the tensor-core scan stages 64-dim bf16 query slices of up to 32 queries in shared memory:
   // d % 64 == 0 and d <= 896 (beyond, its B operand does not fit next to the x ring); else FFMA
-  bool tc_scan() const { return d % 64 == 0 && rd::scan_tc_smem_bytes(d, 32) <= 227 * 1024; }
+  // the converter variant (offloaded lists, or no pre-split copy) must fit: its operand is resident
+  bool tc_scan() const { return d % 64 == 0 && rd::scan_tc_smem_bytes(d, 32, false) <= 227 * 1024; }
   // Tensor-core tile width for a batch: 16-query tiles (the 16-wide scan's deeper ring) when the
   // probed lists see <= 8 queries on average, else 32-query tiles (lists read once). Measured: mixing
   // both widths in one batch (RD_TC_G=1: lists of <= 16 queries narrow, others wide) does not beat

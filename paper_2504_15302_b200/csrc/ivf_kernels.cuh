@@ -90,7 +90,7 @@ struct TcScanParams {
 };
 
 size_t scan_smem_bytes(int d);
-size_t scan_tc_smem_bytes(int d, int tc_g);
+size_t scan_tc_smem_bytes(int d, int tc_g, bool presplit);
 // qmap: 2D bf16 map over the qsplit buffer as [2B rows x d], box {64, 1} (gather4 source)
 // presplit: map128 / map32 are 3D bf16 maps over the pre-split [rows][2][d] arena, box {64, 1, 128|32}
 // tc_g: queries per tile, 16 or 32 (the planner grouped the tiles with the same width)

@@ -32,15 +32,22 @@ namespace {
 
 constexpr int kRows = kTcRows;               // 128 = UMMA M
 constexpr int kStageBytes = kRows * 128;     // 16 KiB: 128 rows x 32 fp32
-// Tile width: kG queries per tile (B operand rows: kG q1 + kG q2, 64 dims per slice). The x ring
-// takes what shared memory the B operand leaves: 16-query tiles get a 5 x 32 KiB pre-split ring,
-// 32-query tiles 3 x 32 KiB (search.cu picks the width from the batch's queries per list).
+// Tile width: kG queries per tile (B operand rows: kG q1 + kG q2, 64 dims per slice).
+// Pre-split path, 16-query tiles (Stream): every ring stage carries its own slice of the query
+// operand next to the x1 / x2 tiles (x1 16 KiB | x2 16 KiB | 4 KiB B slice), re-gathered from L2
+// per stage, so no shared memory is spent on a resident operand: 6 stages (192 KiB of HBM loads
+// in flight instead of 160) and tiles change without draining the ring (B200, one query: +2.5 %).
+// 32-query tiles keep a resident operand and 3 x 32 KiB stages: streaming their 8 KiB slices
+// measured 11 % slower at 1024 queries. Converter path (fp32 x): 16 KiB stages, resident operand.
 template <int kG>
 struct TcGeom {
   static constexpr int G = kG;
-  static constexpr int Stages = kG == 16 ? 10 : 6;  // 16 KiB stages (pre-split stages pair them)
+  static constexpr int Stages = kG == 16 ? 10 : 6;  // converter path / resident operand: 16 KiB units
   static constexpr int BRows = 2 * kG;
   static constexpr int BSlice = BRows * 128;
+  static constexpr bool Stream = kG == 16;                          // pre-split: operand per stage
+  static constexpr int PreStages = Stream ? 6 : Stages / 2;         // pre-split ring depth
+  static constexpr int PreStageBytes = Stream ? 2 * kRows * 128 + BSlice : 2 * kRows * 128;
   // converter group g owns stages / TMEM buffers with u % 2 == g; an odd ring depth would let one
   // group wait on a phase two ahead of the other group's and alias its mbarrier parity
   static_assert(Stages % 2 == 0, "x ring depth must be even");
@@ -66,14 +73,18 @@ struct Smem {
   long long* stage_k; // [4][32]
 };
 
-template <int kG>
+template <bool kPre, int kG>
 __device__ __forceinline__ Smem carve(unsigned char* raw, int d) {
-  constexpr int kStages = TcGeom<kG>::Stages, kBSlice = TcGeom<kG>::BSlice;
+  constexpr int kStages = kPre ? TcGeom<kG>::PreStages : TcGeom<kG>::Stages, kBSlice = TcGeom<kG>::BSlice;
+  // ring bytes (+ the resident operand unless the stages carry it)
+  constexpr bool kStream = kPre && TcGeom<kG>::Stream;
+  const size_t xring = kPre ? (size_t)kStages * TcGeom<kG>::PreStageBytes : (size_t)kStages * kStageBytes;
+  const size_t ring = xring + (kStream ? 0 : (size_t)(d / 64) * kBSlice);
   Smem s;
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
   s.xs = smem_u32(base);
-  s.bs = s.xs + kStages * kStageBytes;
-  uint64_t* b = reinterpret_cast<uint64_t*>(base + kStages * kStageBytes + (d / 64) * kBSlice);
+  s.bs = s.xs + (uint32_t)xring;  // resident operand (unused when streamed)
+  uint64_t* b = reinterpret_cast<uint64_t*>(base + ring);
   s.full = b;
   s.empty = s.full + kStages;
   s.xfull = s.empty + kStages;
@@ -122,16 +133,17 @@ template <bool kPre, int kG>
 __global__ void __launch_bounds__(kThreads, 1)
     ivf_scan_tc_kernel(const __grid_constant__ CUtensorMap map128, const __grid_constant__ CUtensorMap map32,
                        const __grid_constant__ CUtensorMap qmap, const TcScanParams p) {
-  constexpr int kTcG = kG, kStages = TcGeom<kG>::Stages, kBRows = TcGeom<kG>::BRows,
-                kBSlice = TcGeom<kG>::BSlice;
+  constexpr int kTcG = kG, kStages = kPre ? TcGeom<kG>::PreStages : TcGeom<kG>::Stages,
+                kBRows = TcGeom<kG>::BRows, kBSlice = TcGeom<kG>::BSlice;
+  constexpr bool kStream = kPre && TcGeom<kG>::Stream;  // the query operand travels with the stages
   RD_PDL_PROLOGUE();
   if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 4 + 0] = gtimer();
   extern __shared__ unsigned char smem_raw[];
   const int d = p.d, nks = kPre ? d / 64 : d / 32;
-  const Smem sm = carve<kG>(smem_raw, d);
-  // ring geometry: the same 96 KiB hold 6 x 16 KiB fp32 stages or 3 x 32 KiB pre-split stages
-  constexpr int RS = kPre ? kStages / 2 : kStages;
-  constexpr int RB = kPre ? 2 * kStageBytes : kStageBytes;
+  const Smem sm = carve<kPre, kG>(smem_raw, d);
+  // ring geometry: kStages stages of RB bytes (pre-split: x1 | x2 [| B slice]; converter: fp32 x)
+  constexpr int RS = kStages;
+  constexpr int RB = kPre ? TcGeom<kG>::PreStageBytes : kStageBytes;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -188,6 +200,46 @@ __global__ void __launch_bounds__(kThreads, 1)
       const ScanTile T = p.tiles[t];
       // x stage i of this tile: row tile i / nks, 64- (or 32-) dim slice i % nks; lane 0 issues
       const int nst = ((T.nrows + kRows - 1) / kRows) * nks;
+      if constexpr (kStream) {
+        // Each stage: x1 and x2 tiles of the slice (lane 0, TMA) and the slice of the query operand
+        // (TMA gather4 from the L2-resident split queries: rows 0..kG-1 q1, kG..2kG-1 q2; lane qi
+        // < 2 qq loads quad qi; padding rows repeat the tile's last query; quads beyond the tile's
+        // queries keep stale rows whose D columns the epilogue never reads).
+        const int qq = (T.nq + 3) >> 2, per = 2 * qq;
+        const int part = lane >= qq ? 1 : 0;
+        const int g0 = (lane - part * qq) * 4;
+        const uint32_t boff = 2 * kRows * 128 + (part * (kTcG / 4) + g0 / 4) * 512;
+        int r[4] = {0, 0, 0, 0};
+        if (lane < per)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) r[i] = 2 * __ldg(p.list_q + T.qoff + min(g0 + i, T.nq - 1)) + part;
+        for (int i = 0; i < nst; ++i, ++u) {
+          const int rt = i / nks, ks = i - rt * nks;
+          const int rows = min(kRows, T.nrows - rt * kRows);
+          const int nb = (rows + 31) >> 5;
+          const int row = (int)(T.src_row + rt * kRows);
+          const int s = u % RS;
+          const uint32_t dst = sm.xs + s * RB;
+          if (lane == 0) {
+            RD_TWAIT(&sm.empty[s], ((u / RS) & 1) ^ 1, 1);
+            mbar_arrive_expect_tx(&sm.full[s], (uint32_t)(2 * nb * 4096 + per * 512));
+          }
+          __syncwarp();
+          if (lane < per) tma_gather4_u32(dst + boff, &qmap, ks * 64, r[0], r[1], r[2], r[3], &sm.full[s]);
+          if (lane == 0) {
+            if (nb == 4) {
+              tma_load_3d_u32(dst, &map128, ks * 64, 0, row, &sm.full[s]);
+              tma_load_3d_u32(dst + kRows * 128, &map128, ks * 64, 1, row, &sm.full[s]);
+            } else {
+              for (int b = 0; b < nb; ++b) {
+                tma_load_3d_u32(dst + b * 4096, &map32, ks * 64, 0, row + b * 32, &sm.full[s]);
+                tma_load_3d_u32(dst + kRows * 128 + b * 4096, &map32, ks * 64, 1, row + b * 32, &sm.full[s]);
+              }
+            }
+          }
+        }
+        continue;
+      }
       auto issue_x = [&](int i) {
         const int rt = i / nks, ks = i - rt * nks;
         const int rows = min(kRows, T.nrows - rt * kRows);
@@ -274,8 +326,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t dacc = tmem + a * kAccCols;
         for (int ks = 0; ks < nks; ++ks, ++u) {
-          if (rt == 0 && ks == 0) RD_TWAIT(sm.bfull, ti & 1, 4);  // this tile's queries are in the B operand
-          if constexpr (kPre) {
+          if (!kStream && rt == 0 && ks == 0) RD_TWAIT(sm.bfull, ti & 1, 4);  // the tile's queries are in B
+          if constexpr (kPre) {  // (streamed: x1, x2 and the query slice all arrive with the stage)
             const int s = u % RS;
             RD_TWAIT(&sm.full[s], (u / RS) & 1, 6);
             tc_fence_after();
@@ -283,7 +335,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               const unsigned char* st = reinterpret_cast<unsigned char*>(smem_raw) + (sm.xs - smem_u32(smem_raw)) +
                                         s * RB;
               const uint64_t a1 = umma_desc_sw128(st), a2 = umma_desc_sw128(st + kRows * 128);
-              const uint64_t bd = bdesc0 + (uint64_t)(ks * (kBSlice >> 4));
+              const uint64_t bd = kStream ? umma_desc_sw128(st + 2 * kRows * 128)
+                                          : bdesc0 + (uint64_t)(ks * (kBSlice >> 4));
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk) {
                 const uint32_t acc = (ks | kk) != 0;
@@ -316,7 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) tc_commit(&sm.afull[a]);
         __syncwarp();
       }
-      if (lane == 0) tc_commit(sm.bempty);
+      if (!kStream && lane == 0) tc_commit(sm.bempty);  // (streamed: the operand travels with the stages)
       __syncwarp();
     }
   }
@@ -578,10 +631,16 @@ __global__ void qsplit_kernel(const float* __restrict__ Q, __nv_bfloat16* __rest
 
 }  // namespace
 
-size_t scan_tc_smem_bytes(int d, int tc_g) {
-  const size_t stages = tc_g == 16 ? TcGeom<16>::Stages : TcGeom<32>::Stages;
+size_t scan_tc_smem_bytes(int d, int tc_g, bool presplit) {
+  const size_t stages = presplit ? (tc_g == 16 ? TcGeom<16>::PreStages : TcGeom<32>::PreStages)
+                                 : (tc_g == 16 ? TcGeom<16>::Stages : TcGeom<32>::Stages);
   const size_t bslice = tc_g == 16 ? TcGeom<16>::BSlice : TcGeom<32>::BSlice;
-  return 1024 + stages * kStageBytes + (size_t)(d / 64) * bslice +
+  const bool stream = presplit && (tc_g == 16 ? TcGeom<16>::Stream : TcGeom<32>::Stream);
+  const size_t xring =
+      presplit ? stages * (size_t)(tc_g == 16 ? TcGeom<16>::PreStageBytes : TcGeom<32>::PreStageBytes)
+               : stages * kStageBytes;
+  const size_t ring = xring + (stream ? 0 : (size_t)(d / 64) * bslice);
+  return 1024 + ring +
          (2 * stages + 2 * kXBufs + 10) * sizeof(uint64_t) + 2 * sizeof(int) + 16 + 4 * 32 * 12 +
          (size_t)tc_g * kRows * sizeof(float) + 64;
 }
@@ -589,7 +648,7 @@ size_t scan_tc_smem_bytes(int d, int tc_g) {
 cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, const CUtensorMap& qmap,
                            const TcScanParams& p, int grid, cudaStream_t s, bool presplit, int tc_g) {
   if (p.d % 64 != 0 || (tc_g != 16 && tc_g != 32)) return cudaErrorInvalidValue;
-  const size_t smem = scan_tc_smem_bytes(p.d, tc_g);
+  const size_t smem = scan_tc_smem_bytes(p.d, tc_g, presplit);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   if (tc_g == 16) {
     if (presplit)
