@@ -90,12 +90,13 @@ struct TcScanParams {
 };
 
 size_t scan_smem_bytes(int d);
-size_t scan_tc_smem_bytes(int d, int tc_g, bool presplit);
+size_t scan_tc_smem_bytes(int d, int tc_g, bool presplit, bool stream = false);
 // qmap: 2D bf16 map over the qsplit buffer as [2B rows x d], box {64, 1} (gather4 source)
 // presplit: map128 / map32 are 3D bf16 maps over the pre-split [rows][2][d] arena, box {64, 1, 128|32}
 // tc_g: queries per tile, 16 or 32 (the planner grouped the tiles with the same width)
 cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, const CUtensorMap& qmap,
-                           const TcScanParams& p, int grid, cudaStream_t s, bool presplit, int tc_g);
+                           const TcScanParams& p, int grid, cudaStream_t s, bool presplit, int tc_g,
+                           bool stream = false);
 cudaError_t launch_qsplit(const float* Q, void* out, long long B, int d, cudaStream_t s);
 cudaError_t launch_scan(const CUtensorMap& map256, const CUtensorMap& map32, const ScanParams& p,
                         int grid, cudaStream_t s);

@@ -33,24 +33,30 @@ namespace {
 constexpr int kRows = kTcRows;               // 128 = UMMA M
 constexpr int kStageBytes = kRows * 128;     // 16 KiB: 128 rows x 32 fp32
 // Tile width: kG queries per tile (B operand rows: kG q1 + kG q2, 64 dims per slice).
-// Pre-split path, 16-query tiles (Stream): every ring stage carries its own slice of the query
-// operand next to the x1 / x2 tiles (x1 16 KiB | x2 16 KiB | 4 KiB B slice), re-gathered from L2
-// per stage, so no shared memory is spent on a resident operand: 6 stages (192 KiB of HBM loads
-// in flight instead of 160) and tiles change without draining the ring (B200, one query: +2.5 %).
-// 32-query tiles keep a resident operand and 3 x 32 KiB stages: streaming their 8 KiB slices
-// measured 11 % slower at 1024 queries. Converter path (fp32 x): 16 KiB stages, resident operand.
+// Pre-split path, 16-query tiles, streamed operand (kSB, chosen by the host for batches of about
+// one query per probed list or fewer): every ring stage carries its own slice of the query operand
+// next to the x1 / x2 tiles (x1 16 KiB | x2 16 KiB | 4 KiB B slice), re-gathered from L2 per stage,
+// so no shared memory is spent on a resident operand: 6 stages (192 KiB of HBM loads in flight
+// instead of 160) and tiles change without draining the ring (B200: +2 % at 1-2 queries). The
+// per-stage gathers grow with the queries per tile (-4.7 % at 512 queries, ~8 per list), and for
+// 32-query tiles streaming measured 11 % slower at 1024 queries: those keep a resident operand
+// with 5 / 3 x 32 KiB stages. Converter path (fp32 x): 16 KiB stages, resident operand.
 template <int kG>
 struct TcGeom {
   static constexpr int G = kG;
   static constexpr int Stages = kG == 16 ? 10 : 6;  // converter path / resident operand: 16 KiB units
   static constexpr int BRows = 2 * kG;
   static constexpr int BSlice = BRows * 128;
-  static constexpr bool Stream = kG == 16;                          // pre-split: operand per stage
-  static constexpr int PreStages = Stream ? 6 : Stages / 2;         // pre-split ring depth
-  static constexpr int PreStageBytes = Stream ? 2 * kRows * 128 + BSlice : 2 * kRows * 128;
+};
+// ring depth / stage bytes of a (path, width, streamed operand) variant
+template <bool kPre, int kG, bool kSB>
+struct Ring {
+  static_assert(!kSB || (kPre && kG == 16), "streamed operand: pre-split 16-query tiles only");
+  static constexpr int S = kPre ? (kSB ? 6 : TcGeom<kG>::Stages / 2) : TcGeom<kG>::Stages;
+  static constexpr int B = kPre ? 2 * kRows * 128 + (kSB ? TcGeom<kG>::BSlice : 0) : kRows * 128;
   // converter group g owns stages / TMEM buffers with u % 2 == g; an odd ring depth would let one
   // group wait on a phase two ahead of the other group's and alias its mbarrier parity
-  static_assert(Stages % 2 == 0, "x ring depth must be even");
+  static_assert(TcGeom<kG>::Stages % 2 == 0, "x ring depth must be even");
   static_assert(kG == 16 || kG == 32, "tile width");
 };
 constexpr int kXBufs = 8;                    // TMEM ring of converted stages (32 columns each)
@@ -73,13 +79,12 @@ struct Smem {
   long long* stage_k; // [4][32]
 };
 
-template <bool kPre, int kG>
+template <bool kPre, int kG, bool kSB>
 __device__ __forceinline__ Smem carve(unsigned char* raw, int d) {
-  constexpr int kStages = kPre ? TcGeom<kG>::PreStages : TcGeom<kG>::Stages, kBSlice = TcGeom<kG>::BSlice;
+  constexpr int kStages = Ring<kPre, kG, kSB>::S, kBSlice = TcGeom<kG>::BSlice;
   // ring bytes (+ the resident operand unless the stages carry it)
-  constexpr bool kStream = kPre && TcGeom<kG>::Stream;
-  const size_t xring = kPre ? (size_t)kStages * TcGeom<kG>::PreStageBytes : (size_t)kStages * kStageBytes;
-  const size_t ring = xring + (kStream ? 0 : (size_t)(d / 64) * kBSlice);
+  const size_t xring = (size_t)kStages * Ring<kPre, kG, kSB>::B;
+  const size_t ring = xring + (kSB ? 0 : (size_t)(d / 64) * kBSlice);
   Smem s;
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
   s.xs = smem_u32(base);
@@ -129,21 +134,21 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 // kPre = true : pre-split bf16 (x1, x2) arena ([rows][2][d], built with the index); the producer TMA-loads
 //               both 64-dim tiles of a stage straight into 128B-swizzled smem and the MMAs read A from
 //               smem (SS) — no conversion on the scan path; converter warps are idle.
-template <bool kPre, int kG>
+template <bool kPre, int kG, bool kSB>
 __global__ void __launch_bounds__(kThreads, 1)
     ivf_scan_tc_kernel(const __grid_constant__ CUtensorMap map128, const __grid_constant__ CUtensorMap map32,
                        const __grid_constant__ CUtensorMap qmap, const TcScanParams p) {
-  constexpr int kTcG = kG, kStages = kPre ? TcGeom<kG>::PreStages : TcGeom<kG>::Stages,
-                kBRows = TcGeom<kG>::BRows, kBSlice = TcGeom<kG>::BSlice;
-  constexpr bool kStream = kPre && TcGeom<kG>::Stream;  // the query operand travels with the stages
+  constexpr int kTcG = kG, kStages = Ring<kPre, kG, kSB>::S, kBRows = TcGeom<kG>::BRows,
+                kBSlice = TcGeom<kG>::BSlice;
+  constexpr bool kStream = kSB;  // the query operand travels with the stages
   RD_PDL_PROLOGUE();
   if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 4 + 0] = gtimer();
   extern __shared__ unsigned char smem_raw[];
   const int d = p.d, nks = kPre ? d / 64 : d / 32;
-  const Smem sm = carve<kPre, kG>(smem_raw, d);
+  const Smem sm = carve<kPre, kG, kSB>(smem_raw, d);
   // ring geometry: kStages stages of RB bytes (pre-split: x1 | x2 [| B slice]; converter: fp32 x)
   constexpr int RS = kStages;
-  constexpr int RB = kPre ? TcGeom<kG>::PreStageBytes : kStageBytes;
+  constexpr int RB = Ring<kPre, kG, kSB>::B;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -631,14 +636,14 @@ __global__ void qsplit_kernel(const float* __restrict__ Q, __nv_bfloat16* __rest
 
 }  // namespace
 
-size_t scan_tc_smem_bytes(int d, int tc_g, bool presplit) {
-  const size_t stages = presplit ? (tc_g == 16 ? TcGeom<16>::PreStages : TcGeom<32>::PreStages)
-                                 : (tc_g == 16 ? TcGeom<16>::Stages : TcGeom<32>::Stages);
+size_t scan_tc_smem_bytes(int d, int tc_g, bool presplit, bool stream) {
+  stream = stream && presplit && tc_g == 16;
+  const size_t stages = stream ? Ring<true, 16, true>::S
+                        : presplit ? (tc_g == 16 ? Ring<true, 16, false>::S : Ring<true, 32, false>::S)
+                                   : (tc_g == 16 ? Ring<false, 16, false>::S : Ring<false, 32, false>::S);
+  const size_t sbytes = stream ? Ring<true, 16, true>::B : presplit ? Ring<true, 16, false>::B : Ring<false, 16, false>::B;
   const size_t bslice = tc_g == 16 ? TcGeom<16>::BSlice : TcGeom<32>::BSlice;
-  const bool stream = presplit && (tc_g == 16 ? TcGeom<16>::Stream : TcGeom<32>::Stream);
-  const size_t xring =
-      presplit ? stages * (size_t)(tc_g == 16 ? TcGeom<16>::PreStageBytes : TcGeom<32>::PreStageBytes)
-               : stages * kStageBytes;
+  const size_t xring = stages * sbytes;
   const size_t ring = xring + (stream ? 0 : (size_t)(d / 64) * bslice);
   return 1024 + ring +
          (2 * stages + 2 * kXBufs + 10) * sizeof(uint64_t) + 2 * sizeof(int) + 16 + 4 * 32 * 12 +
@@ -646,18 +651,21 @@ size_t scan_tc_smem_bytes(int d, int tc_g, bool presplit) {
 }
 
 cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, const CUtensorMap& qmap,
-                           const TcScanParams& p, int grid, cudaStream_t s, bool presplit, int tc_g) {
+                           const TcScanParams& p, int grid, cudaStream_t s, bool presplit, int tc_g, bool stream) {
   if (p.d % 64 != 0 || (tc_g != 16 && tc_g != 32)) return cudaErrorInvalidValue;
-  const size_t smem = scan_tc_smem_bytes(p.d, tc_g, presplit);
+  stream = stream && presplit && tc_g == 16;
+  const size_t smem = scan_tc_smem_bytes(p.d, tc_g, presplit, stream);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   if (tc_g == 16) {
+    if (stream)
+      return launch_k(ivf_scan_tc_kernel<true, 16, true>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
     if (presplit)
-      return launch_k(ivf_scan_tc_kernel<true, 16>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
-    return launch_k(ivf_scan_tc_kernel<false, 16>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+      return launch_k(ivf_scan_tc_kernel<true, 16, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+    return launch_k(ivf_scan_tc_kernel<false, 16, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
   }
   if (presplit)
-    return launch_k(ivf_scan_tc_kernel<true, 32>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
-  return launch_k(ivf_scan_tc_kernel<false, 32>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+    return launch_k(ivf_scan_tc_kernel<true, 32, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+  return launch_k(ivf_scan_tc_kernel<false, 32, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
 }
 
 cudaError_t launch_qsplit(const float* Q, void* out, long long B, int d, cudaStream_t s) {
