@@ -21,7 +21,7 @@ constexpr long long kNoKey = 0x7fffffffffffffffll;
 // every load in flight before the canonical sums run; otherwise each group of 8 lanes streams its
 // row from global memory (enough CTAs are resident to hide the latency).
 template <bool kStage>
-__global__ void __launch_bounds__(256) merge_rerank_kernel(const MergeParams p) {
+__global__ void __launch_bounds__(256, kStage ? 1 : 8) merge_rerank_kernel(const MergeParams p) {
   RD_TS(13);  // entry, before the wait on the previous kernel
   RD_PDL_PROLOGUE();
   extern __shared__ __align__(16) float dyn[];  // kStage: q[d], rows[32][d + kStagePad]
@@ -91,17 +91,22 @@ __global__ void __launch_bounds__(256) merge_rerank_kernel(const MergeParams p) 
 #pragma unroll
       for (int j = 16; j > 0; j >>= 1) bitonic_step(ld, lk, lane, j, true);
     }
-    // candidate rows: list of the row (row_list), its device-visible address and user id
+    // The best m = k + 8 candidates (of the 32) are reranked: the (m+1)-th approximate distance
+    // bounds every row not reranked (the rest of the 32 and everything the scan dropped), so
+    // certification reads tau = that distance; the 8 spare candidates keep it holding unless the
+    // data has near-ties at rank k (then the exact fallback runs). Fewer rows cut the rerank's HBM
+    // reads (k = 10: 18 of 32).
+    const int m = min(kTopK, p.k + 8);
     const float* xp = nullptr;
     long long id = kNoKey;
-    if (lk != kNoKey) {
+    if (lk != kNoKey && lane < m) {  // candidate rows: list of the row (row_list), address, user id
       const int l = __ldg(p.row_list + lk);
       xp = p.list_base[l] + (size_t)(lk - __ldg(p.list_off + l)) * p.d;
       id = __ldg(p.ids + lk);
     }
     rowp[lane] = xp;
     ex_id[lane] = id;
-    if (lane == 31) tau_s = ld;
+    if (lane == min(m, kTopK - 1)) tau_s = ld;
     if constexpr (kStage) {  // device rows: one bulk (TMA) copy each, all in flight at once
       float* st = dyn + p.d;
       const bool dev = xp && xp >= p.arena_lo && xp < p.arena_hi;
@@ -137,7 +142,7 @@ __global__ void __launch_bounds__(256) merge_rerank_kernel(const MergeParams p) 
     e = exact_l2_group8_impl<false>(dyn, st + c * (p.d + kStagePad), xp ? p.d : 0, j8);
   } else {
     // a padded slot runs zero terms so the warp stays converged for the shuffles
-    e = exact_l2_group8_impl<false, 24>(q, xp ? xp : q, xp ? p.d : 0, j8);  // rows from HBM: 24 loads deep
+    e = exact_l2_group8_impl<false, 16>(q, xp ? xp : q, xp ? p.d : 0, j8);  // rows from HBM: 16 loads deep (32 registers: one wave of 8 CTAs per SM)
   }
   if (!xp) e = kInf;
   if (j8 == 0) ex_d[c] = e;
