@@ -410,14 +410,20 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
   }
   vmin = block_reduce_min(vmin, fsh);
   vmax = block_reduce_max(vmax, fsh);
+  // kStage: the approximately nearest list's first 32 rows (the likely seeding list) are bulk-copied
+  // into the staging area now and consumed after the candidate search, off the critical path
+  int seed_l = -1;  // uniform: every thread reads the same amin and list metadata
   if constexpr (kStage) {
     if (p.qthr && amin != ~0ull) {
       const int l = (int)(amin & 0xffffffffu);
       const long long r0 = p.res_row0[l];
       if (r0 >= 0 && p.list_off[l + 1] - p.list_off[l] >= 32) {
-        const int lines = d / 32;  // 128 B lines per row
-        for (int i = tid; i < 32 * lines; i += kSelThreads)
-          prefetch_l2(p.arena + (size_t)(r0 + i / lines) * d + (i % lines) * 32);
+        seed_l = l;
+        if (warp == 0) {
+          if (lane == 0) mbar_arrive_expect_tx(&bar, (uint32_t)(32 * d * 4));
+          __syncwarp();
+          bulk_g2s(st + lane * ds, p.arena + (size_t)(r0 + lane) * d, (uint32_t)(d * 4), &bar);
+        }
       }
     }
   }
@@ -492,6 +498,15 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
   }
   RD_TS(3);
   if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0) p.dbg[15] = (unsigned long long)ncand;
+  float seed_pre = 0.f;  // max fp32 distance to the early-staged rows (valid when seed_l >= 0)
+  if constexpr (kStage) {
+    if (seed_l >= 0) {
+      mbar_wait(&bar, bphase);
+      bphase ^= 1;
+      seed_pre = block_reduce_max(l2_group8_f32(qf, st + grp * ds, d, j8), fsh);
+      __syncthreads();  // the staging area is free again
+    }
+  }
 
   const float u = 5.9604645e-8f;
   const float eps = 2.f * ((d + 4) * u * 2.f * sqrtf(qn) * p.cmax + 8.f * u * (qn + p.cmax * p.cmax)) + 1e-30f;
@@ -711,12 +726,15 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
       if (tid == 0) p.qthr[b] = 0x7f7f7f7f;
     } else {
       const float* r0 = p.arena + (size_t)p.res_row0[l] * d;
-      float e;
-      if constexpr (kStage) {
-        stage_bulk(32, [&](int r) { return r0 + (size_t)r * d; });
-        e = l2_group8_f32(qf, st + grp * ds, d, j8);
-      } else {
-        e = l2_group8_f32<16>(q, r0 + (size_t)grp * d, d, j8);
+      float e = 0.f;
+      const bool pre = kStage && l == seed_l;  // computed early (uniform branch)
+      if (!pre) {
+        if constexpr (kStage) {
+          stage_bulk(32, [&](int r) { return r0 + (size_t)r * d; });
+          e = l2_group8_f32(qf, st + grp * ds, d, j8);
+        } else {
+          e = l2_group8_f32<16>(q, r0 + (size_t)grp * d, d, j8);
+        }
       }
       float m = e;
 #pragma unroll
@@ -726,6 +744,7 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
       if (tid == 0) {
         float mx = red[0];
         for (int i = 1; i < kSelThreads / 32; ++i) mx = fmaxf(mx, red[i]);
+        if (pre) mx = seed_pre;
         const float eps_s =
             2.f * ((d / 2 + 8) * u * 2.f * sqrtf(qn) * p.xmax + 8.f * u * (qn + p.xmax * p.xmax)) + 1e-30f;
         const float thr = mx * (1.f + 2.f * l2_f32_rel_bound(d)) + 2.f * eps_s;
