@@ -260,6 +260,8 @@ struct rd_index {
     return per_list <= 8.0 ? 16 : 32;
   }
   int tc_g_force = std::getenv("RD_TC_G") ? std::atoi(std::getenv("RD_TC_G")) : 0;
+  // streamed query operand for the 16-query scan (scan_tc.cu): -1 by batch, RD_STREAM_B=0|1 forces
+  int stream_force = std::getenv("RD_STREAM_B") ? std::atoi(std::getenv("RD_STREAM_B")) : -1;
   bool stage_rows(long long B) const { return B <= (stage_max_b >= 0 ? stage_max_b : 2LL * num_sms); }
   long long n = 0;
   int d = 0, nlist = 0;

@@ -176,7 +176,8 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
       tn.ntiles = w.meta() + 2 * rd::kCatNarrow;
       tn.tile_counter = w.meta() + 2 * rd::kCatNarrow + 1;
       // streamed query operand for about one query per probed list or fewer (scan_tc.cu)
-      const bool stream = (long long)B * std::min(nprobe, nl) <= nl;
+      const bool stream =
+          h->stream_force >= 0 ? h->stream_force != 0 : (long long)B * std::min(nprobe, nl) <= nl;
       CK(rd::launch_scan_tc(xm128, xm32, gmap, tn, h->num_sms, s, h->presplit, 16, stream));
       launches += 1;
     }

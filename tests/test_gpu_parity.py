@@ -169,3 +169,21 @@ def test_search_into_pinned_buffers(engine):
     idx.search_into(hq, 8, 10, hi, hd)
     np.testing.assert_array_equal(hi, want.ids)
     np.testing.assert_array_equal(hd, want.dists)
+
+
+@pytest.mark.parametrize("variant", [dict(RD_TC_G="16", RD_STREAM_B="1"), dict(RD_TC_G="16", RD_STREAM_B="0"),
+                                     dict(RD_TC_G="32"), dict(RD_TC_G="1", RD_STREAM_B="1"),
+                                     dict(RD_TC_G="1", RD_STREAM_B="0")])
+def test_every_scan_variant(engine, oracle, variant, monkeypatch):
+    # one dataset through each tensor-core scan variant (16-query tiles with a streamed or resident
+    # query operand, 32-query tiles, mixed widths): lists probed by 1..40 queries, so tiles of one,
+    # a few and more than 16 / 32 queries all occur
+    for kname, v in variant.items():
+        monkeypatch.setenv(kname, v)
+    n, d, nlist = 60000, 768, 96
+    desc = engine.desc(n, d, nlist)
+    q, _ = engine.synth_queries(desc, 321, 150)
+    e = engine.synthetic_index(desc).search(q, 12, 10)
+    o = oracle.synthetic_index(desc).search(q, 12, 10)
+    _check(e, o.ids, o.dists)
+    assert e.stats["margin_failures"] == 0 and e.stats["probe_failures"] == 0
