@@ -169,8 +169,10 @@ __device__ __forceinline__ void finish_counters(const PlanParams& p, unsigned lo
   }
 }
 
-// single CTA: exclusive scans of list_nq and the tile counts; totals and byte counters. Lists are
-// visited in rounds of 1024 (thread t <-> list round * 1024 + t) so every global access coalesces.
+// single CTA: exclusive scans of list_nq and the tile counts; totals and byte counters. Each
+// thread takes kLV consecutive lists per round (every load of the round in flight at once, then
+// one block scan of the per-thread sums): one round covers 4096 lists.
+constexpr int kLV = 4;
 __global__ void __launch_bounds__(1024) list_scan_kernel(const PlanParams p) {
   RD_PDL_PROLOGUE();
   __shared__ int wsum[1 + kTileCats][32];
@@ -181,23 +183,41 @@ __global__ void __launch_bounds__(1024) list_scan_kernel(const PlanParams p) {
   if (tid <= kTileCats) carry[tid] = 0;
   unsigned long long cc[3] = {0, 0, 0};
   __syncthreads();
-  for (int j0 = 0; j0 < nl; j0 += 1024) {
-    const int j = j0 + tid;
-    int v[1 + kTileCats] = {0, 0, 0, 0}, ex[1 + kTileCats];
-    if (j < nl) {
-      v[0] = p.list_nq[j];
+  for (int j0 = 0; j0 < nl; j0 += 1024 * kLV) {
+    const int jb = j0 + tid * kLV;
+    int v[kLV][1 + kTileCats];
+    long long len[kLV], r0[kLV];
 #pragma unroll
-      for (int cat = 0; cat < kTileCats; ++cat) v[1 + cat] = p.list_ntile[cat * nl + j];
-      if (v[0] > 0) {
+    for (int i = 0; i < kLV; ++i) {
+      const int j = jb + i;
+      const bool ok = j < nl;
+      v[i][0] = ok ? p.list_nq[j] : 0;
+#pragma unroll
+      for (int cat = 0; cat < kTileCats; ++cat) v[i][1 + cat] = ok ? p.list_ntile[cat * nl + j] : 0;
+      len[i] = ok ? p.list_off[j + 1] - p.list_off[j] : 0;
+      r0[i] = ok ? p.res_row0[j] : 0;
+    }
+    int tot[1 + kTileCats] = {0, 0, 0, 0}, ex[1 + kTileCats];
+#pragma unroll
+    for (int i = 0; i < kLV; ++i) {
+#pragma unroll
+      for (int c = 0; c <= kTileCats; ++c) tot[c] += v[i][c];
+      if (v[i][0] > 0) {
         ++cc[0];
-        cc[p.res_row0[j] >= 0 ? 1 : 2] += p.list_off[j + 1] - p.list_off[j];
+        cc[r0[i] >= 0 ? 1 : 2] += len[i];
       }
     }
-    block_scan_round<1024, 1 + kTileCats>(v, ex, wsum, carry);
-    if (j < nl) {
-      p.list_qoff[j] = ex[0];
+    block_scan_round<1024, 1 + kTileCats>(tot, ex, wsum, carry);
 #pragma unroll
-      for (int cat = 0; cat < kTileCats; ++cat) p.list_toff[cat * nl + j] = ex[1 + cat];
+    for (int i = 0; i < kLV; ++i) {
+      const int j = jb + i;
+      if (j < nl) {
+        p.list_qoff[j] = ex[0];
+#pragma unroll
+        for (int cat = 0; cat < kTileCats; ++cat) p.list_toff[cat * nl + j] = ex[1 + cat];
+      }
+#pragma unroll
+      for (int c = 0; c <= kTileCats; ++c) ex[c] += v[i][c];
     }
   }
   finish_counters<1024>(p, cc, wcnt, carry + 1);
