@@ -312,6 +312,13 @@ struct rd_index {
     // places its result ids / distances right after (kStatBytes) and copies everything at once
     DBuf<char> blk;
     HBuf<char> h_blk;
+    // (re)allocates the block; its unused padding is zeroed once so every byte the sync copy
+    // brings back has been written
+    void ensure_blk(size_t n) {
+      if (blk.n >= n) return;
+      blk.ensure(n);
+      CK(cudaMemset(blk.p, 0, kStatBytes));
+    }
     unsigned long long* counters() const { return reinterpret_cast<unsigned long long*>(blk.p); }
     unsigned* fails() const { return reinterpret_cast<unsigned*>(blk.p + 24); }
     int* meta() const { return reinterpret_cast<int*>(blk.p + 32); }

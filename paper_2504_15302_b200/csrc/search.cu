@@ -77,7 +77,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   w.tiles16.ensure(pl.max_tiles);
   w.ff_tiles.ensure(pl.max_tiles);
   w.qsplit.ensure((size_t)B * 2 * d);
-  w.blk.ensure(kStatBytes + result_bytes);
+  w.ensure_blk(kStatBytes + result_bytes);
   w.h_blk.ensure(kStatBytes + result_bytes);
   w.part_count.ensure(B);
   w.part_dist.ensure((size_t)B * pl.cap * rd::kTopK);
@@ -510,7 +510,7 @@ int rd_search(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int3
     // sync's single copy; large ones go straight into the caller's buffers
     const size_t res_bytes = rn * (sizeof(long long) + sizeof(float));
     const bool direct = res_bytes > (size_t(64) << 10);
-    w.blk.ensure(kStatBytes + res_bytes);
+    w.ensure_blk(kStatBytes + res_bytes);
     long long* d_ids = reinterpret_cast<long long*>(w.blk.p + kStatBytes);
     float* d_dists = reinterpret_cast<float*>(w.blk.p + kStatBytes + rn * sizeof(long long));
     do_search(h, w.q.p, B, nprobe, k, d_ids, d_dists, s, true, st, direct ? 0 : res_bytes, [&] {
@@ -539,7 +539,7 @@ int rd_probe(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32
     w.qnorm.ensure(B);
     w.Dc.ensure((size_t)B * nl);
     w.probes.ensure((size_t)B * nprobe);
-    w.blk.ensure(kStatBytes);
+    w.ensure_blk(kStatBytes);
     CK(cudaMemcpy(w.q.p, queries, sizeof(float) * B * d, cudaMemcpyHostToDevice));
     CK(cudaMemset(w.fails(), 0, 2 * sizeof(unsigned)));
     w.qsplit.ensure((size_t)B * d);
