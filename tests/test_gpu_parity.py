@@ -187,3 +187,26 @@ def test_every_scan_variant(engine, oracle, variant, monkeypatch):
     o = oracle.synthetic_index(desc).search(q, 12, 10)
     _check(e, o.ids, o.dists)
     assert e.stats["margin_failures"] == 0 and e.stats["probe_failures"] == 0
+
+
+def test_timing_stages(engine):
+    # per-stage device times only while rd_timing_stages is on; whole-search times always; results
+    # identical either way (the events sit between kernels, they do not change the work)
+    desc = engine.desc(30000, 768, 64)
+    idx = engine.synthetic_index(desc)
+    q, _ = engine.synth_queries(desc, 3, 32)
+    idx.timing_reset()
+    off = idx.search(q, 8, 10)
+    t = idx.timing_read()
+    assert off.stats["scan_ms"] == 0.0 and t["searches"] == 1 and t["stage_searches"] == 0
+    assert t["total_ms"] > 0.0 and t["scan_ms"] == 0.0
+    idx.timing_stages(True)
+    idx.timing_reset()
+    on = idx.search(q, 8, 10)
+    idx.search(q, 8, 10)
+    t = idx.timing_read()
+    idx.timing_stages(False)
+    assert on.stats["scan_ms"] > 0.0 and t["searches"] == 2 and t["stage_searches"] == 2
+    assert 0.0 < t["scan_ms"] < t["total_ms"]
+    np.testing.assert_array_equal(on.ids, off.ids)
+    np.testing.assert_array_equal(on.dists, off.dists)
