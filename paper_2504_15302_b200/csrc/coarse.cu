@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
   __shared__ float cdist[kSelMaxCand];
   __shared__ uint32_t sel_prefix, sel_k;
   __shared__ int certified, ncand_s, found_bin, below_s, nin_s, na_s, lsel;
-  __shared__ unsigned char lok[kSelMaxCand];  // candidate list can seed (resident, >= 32 rows)
+  __shared__ unsigned char lok[kSelMaxCand];  // candidate list can seed (resident, >= seed_rows rows)
   __shared__ unsigned long long amin;
   __shared__ __align__(8) uint64_t bar;
   RD_TS(0);
@@ -417,12 +417,12 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
     if (p.qthr && amin != ~0ull) {
       const int l = (int)(amin & 0xffffffffu);
       const long long r0 = p.res_row0[l];
-      if (r0 >= 0 && p.list_off[l + 1] - p.list_off[l] >= 32) {
+      if (r0 >= 0 && p.list_off[l + 1] - p.list_off[l] >= p.seed_rows) {
         seed_l = l;
         if (warp == 0) {
-          if (lane == 0) mbar_arrive_expect_tx(&bar, (uint32_t)(32 * d * 4));
+          if (lane == 0) mbar_arrive_expect_tx(&bar, (uint32_t)(p.seed_rows * d * 4));
           __syncwarp();
-          bulk_g2s(st + lane * ds, p.arena + (size_t)(r0 + lane) * d, (uint32_t)(d * 4), &bar);
+          if (lane < p.seed_rows) bulk_g2s(st + lane * ds, p.arena + (size_t)(r0 + lane) * d, (uint32_t)(d * 4), &bar);
         }
       }
     }
@@ -503,7 +503,8 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
     if (seed_l >= 0) {
       mbar_wait(&bar, bphase);
       bphase ^= 1;
-      seed_pre = block_reduce_max(l2_group8_f32(qf, st + grp * ds, d, j8), fsh);
+      const float e = l2_group8_f32(qf, st + grp * ds, d, j8);  // rows >= seed_rows: stale, masked
+      seed_pre = block_reduce_max(grp < p.seed_rows ? e : 0.f, fsh);
       __syncthreads();  // the staging area is free again
     }
   }
@@ -524,7 +525,7 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
       const int l = cand[i];
       cdist[i] = vals[l];
       // seeding eligibility, resolved here so the rank-order walk below needs no global loads
-      if (p.qthr) lok[i] = p.res_row0[l] >= 0 && p.list_off[l + 1] - p.list_off[l] >= 32;
+      if (p.qthr) lok[i] = p.res_row0[l] >= 0 && p.list_off[l + 1] - p.list_off[l] >= p.seed_rows;
     }
     if (tid == 0) below_s = 0;
     __syncthreads();
@@ -706,7 +707,7 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
       lsel = -1;
       for (int i = 0; i < np; ++i) {
         const int l = cand[i];
-        if (p.res_row0[l] >= 0 && p.list_off[l + 1] - p.list_off[l] >= 32) {
+        if (p.res_row0[l] >= 0 && p.list_off[l + 1] - p.list_off[l] >= p.seed_rows) {
           lsel = l;
           break;
         }
@@ -730,11 +731,12 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
       const bool pre = kStage && l == seed_l;  // computed early (uniform branch)
       if (!pre) {
         if constexpr (kStage) {
-          stage_bulk(32, [&](int r) { return r0 + (size_t)r * d; });
+          stage_bulk(p.seed_rows, [&](int r) { return r0 + (size_t)r * d; });
           e = l2_group8_f32(qf, st + grp * ds, d, j8);
         } else {
-          e = l2_group8_f32<16>(q, r0 + (size_t)grp * d, d, j8);
+          e = l2_group8_f32<16>(q, r0 + (size_t)min(grp, p.seed_rows - 1) * d, d, j8);
         }
+        if (grp >= p.seed_rows) e = 0.f;  // only the first seed_rows rows bound the threshold
       }
       float m = e;
 #pragma unroll

@@ -68,6 +68,9 @@ struct ScanParams {
   int part_cap;
   int d;
   int* qthr;               // B: per-query pruning threshold (f2ord), min over completed tiles' 32nd
+  // 0-based rank whose distance bounds what the merge needs (min(31, k + 8): it reranks k + 8 and
+  // certifies against the next): rows beyond a tile's (thr_rank+1)-th best can be dropped
+  int thr_rank = 31;
 };
 
 struct TcScanParams {
@@ -87,6 +90,7 @@ struct TcScanParams {
   int debug_skip;          // profiling only (RD_DEBUG_SKIP): 1 = no epilogue selection, 2 = no conversion, 4 = no MMA
   unsigned long long* stall = nullptr;  // profiling only (RD_DEBUG_STALL): per CTA x 12 barrier-wait cycles
   unsigned long long* dbg = nullptr;  // profiling only (RD_DEBUG_TS): per CTA [entry, ready, first tile, end] globaltimer
+  int thr_rank = 31;       // as ScanParams::thr_rank
 };
 
 size_t scan_smem_bytes(int d);
@@ -149,6 +153,9 @@ struct SelectParams {
   // sets each probe's bit as it writes the probe, so the plan needs no inversion pass
   unsigned* bitmap = nullptr;
   int W = 0;
+  // seeding rows: the threshold must bound the (seed_rows)-th best distance (= thr_rank + 1 of the
+  // scans), so a list with at least that many rows can seed
+  int seed_rows = 32;
 };
 // stage: q and candidate rows go through shared memory (latency-bound small batches)
 cudaError_t launch_select(const SelectParams& p, bool stage, cudaStream_t s);

@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
         float& ld = h ? ld1 : ld0;
         long long& lk = h ? lk1 : lk0;
         const float qt = h ? qt1 : qt0;
-        float thr = fminf(__shfl_sync(0xffffffffu, ld, 31), qt);
+        float thr = fminf(__shfl_sync(0xffffffffu, ld, p.thr_rank), qt);
         const long long gbase = T.grow0 + (long long)rt * kScanRows;
 #pragma unroll 1
         for (int m = 0; m < kScanRows / 32; ++m) {
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
           const bool pass = v < thr;
           if (__any_sync(0xffffffffu, pass)) {
             warp_merge32(ld, lk, pass ? v : kInf, pass ? gbase + m * 32 + lane : kNoKey, lane);
-            thr = fminf(__shfl_sync(0xffffffffu, ld, 31), qt);
+            thr = fminf(__shfl_sync(0xffffffffu, ld, p.thr_rank), qt);
           }
         }
       }
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
       const float ld = h ? ld1 : ld0;
       const long long lk = h ? lk1 : lk0;
       if (__shfl_sync(0xffffffffu, ld, 0) == kInf) continue;  // nothing survived: no partial
-      const float l31 = __shfl_sync(0xffffffffu, ld, 31);
+      const float l31 = __shfl_sync(0xffffffffu, ld, p.thr_rank);
       int pslot = 0;
       if (lane == 0) {
         pslot = atomicAdd(p.part_count + qid, 1);

@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int g = ew + 4 * j;
           if (g >= nq) break;
           // prune with the tighter of this list's 32nd and the query's global threshold
-          float thr = fminf(__shfl_sync(0xffffffffu, ld[j], 31), qt[j]);
+          float thr = fminf(__shfl_sync(0xffffffffu, ld[j], p.thr_rank), qt[j]);
           int base = 0;
 #pragma unroll
           for (int m = 0; m < kRows / 32; ++m) {
@@ -528,7 +528,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float bd = lane < base ? sd[lane] : kInf;
               const long long bk = lane < base ? sk[lane] : kNoKey;
               warp_merge32(ld[j], lk[j], bd, bk, lane);
-              thr = fminf(__shfl_sync(0xffffffffu, ld[j], 31), qt[j]);
+              thr = fminf(__shfl_sync(0xffffffffu, ld[j], p.thr_rank), qt[j]);
               base = 0;
               pass = v < thr;
               mask = __ballot_sync(0xffffffffu, pass);
@@ -564,7 +564,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int j = 0; j < kOwn; ++j) {
         const int g = ew + 4 * j;
-        const float l31 = __shfl_sync(0xffffffffu, ld[j], 31);
+        const float l31 = __shfl_sync(0xffffffffu, ld[j], p.thr_rank);  // the bound the merge needs
         const bool has = g < nq && __shfl_sync(0xffffffffu, ld[j], 0) != kInf;  // something survived
         if (lane == j) {
           myhas = has;

@@ -124,6 +124,10 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     sp.bitmap = w.bitmap.p;
     sp.W = W;
   }
+  // the merge reranks min(32, k + 8) candidates and certifies against the next: scans prune with,
+  // and the seed bounds, that rank's distance
+  const int thr_rank = std::min(rd::kTopK - 1, k + 8);
+  sp.seed_rows = thr_rank + 1;
   h->traced("select", s, sp.dbg, [&] { CK(rd::launch_select(sp, h->stage_rows(B), s)); });
   launches += rd::coarse_small((int)B) ? 2 : 3;  // (query prep +) coarse + select
   rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
@@ -151,6 +155,8 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   rd::TcScanParams tc{w.tiles.p, w.meta() + 2 * rd::kCatWide, w.meta() + 2 * rd::kCatWide + 1, w.qsplit.p, w.qnorm.p,
                       w.list_q.p, h->xnorm.p,
                       w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p, h->debug_skip};
+  sc.thr_rank = thr_rank;
+  tc.thr_rank = thr_rank;
   if (!h->tc_scan() || h->tc_min_q > 1) {  // FFMA tiles exist only in these cases
     CK(rd::launch_scan(h->map256, h->map32, sc, h->num_sms, s));
     launches += 1;
