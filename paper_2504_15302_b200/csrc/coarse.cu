@@ -84,12 +84,13 @@ __global__ void __launch_bounds__(256) coarse_gemm_kernel(const float* __restric
   }
 }
 
-// Small batches (B <= kSmallB): Dc is a memory-bound GEMV over the centroids, so one warp per
-// centroid streams its row once (float4, coalesced) against every query of the batch held in smem,
-// across >= one CTA per SM — instead of the tensor-core tile kernel's 32-CTA, latency-bound K loop.
-// Any summation order is covered by the select kernel's error bound ((d + 4) u 2 |q| |c|).
-// query preparation in one pass, one warp per query: ||q||^2 (the same fp64 lane-strided sum and
-// shuffle tree as row_norms) and the bf16 (hi, lo) split rows the tensor-core kernels gather.
+// Small batches (B <= 8, coarse_small): Dc is a memory-bound GEMV over the centroids, so one warp
+// per centroid streams its row once (float4, coalesced) against every query of the batch (through
+// L1), across >= one CTA per SM — instead of the tensor-core tile kernel's 32-CTA, latency-bound K
+// loop. Any summation order is covered by the select kernel's error bound ((d + 4) u 2 |q| |c|).
+// Query preparation in one pass, one warp per query: ||q||^2 (fp64 lane sums and a shuffle tree;
+// used only inside error-bounded approximate distances) and the bf16 (hi, lo) split rows the
+// tensor-core kernels gather.
 // It also zeroes the per-search counters (zero2: 2 words, zeroB: B words) so they need no memset.
 __device__ __forceinline__ void qprep_rows(const QprepArgs& a, long long r0, long long rstep, bool zero2_here) {
   const int lane = threadIdx.x & 31;
@@ -144,7 +145,6 @@ __global__ void qprep_kernel(const QprepArgs a) {
   qprep_rows(a, (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5, warps, blockIdx.x == 0);
 }
 
-constexpr int kSmallB = 16;
 constexpr int kGemvThreads = 256;
 constexpr int kGemvMaxV = 8;  // float4 per lane per row: d <= 1024
 // one warp per centroid (grid = nlist / 8 CTAs): the row's float4 loads are all issued before any
@@ -192,10 +192,6 @@ __global__ void __launch_bounds__(kGemvThreads) coarse_gemv_kernel(const float* 
 __device__ __forceinline__ uint32_t f2key(float f) {
   uint32_t u = __float_as_uint(f);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-__device__ __forceinline__ float key2f(uint32_t k) {
-  uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
-  return __uint_as_float(u);
 }
 
 // block-wide exclusive scan of one int per thread (256 threads); returns total via *total

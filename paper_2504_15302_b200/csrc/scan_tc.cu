@@ -43,7 +43,6 @@ constexpr int kStageBytes = kRows * 128;     // 16 KiB: 128 rows x 32 fp32
 // with 5 / 3 x 32 KiB stages. Converter path (fp32 x): 16 KiB stages, resident operand.
 template <int kG>
 struct TcGeom {
-  static constexpr int G = kG;
   static constexpr int Stages = kG == 16 ? 10 : 6;  // converter path / resident operand: 16 KiB units
   static constexpr int BRows = 2 * kG;
   static constexpr int BSlice = BRows * 128;
@@ -383,7 +382,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     if constexpr (kPre) goto done;  // no conversion on the pre-split path
     const int quarter = warp & 3;
     const int grp = warp >= 10;
-    const int tid = threadIdx.x - 64;  // 0..127 (group 0 only loads B)
     const int r = quarter * 32 + lane;
     uint32_t u = 0;
     // Software-pipelined: the TMEM stores of stage u complete (wait::st) while stage u+2 is being
