@@ -39,3 +39,8 @@ tests/cpp/ragsim_adapter_cpu: tests/cpp/ragsim_adapter_test.cpp include/rd_ragsi
 tests/cpp/ragsim_adapter_b200: tests/cpp/ragsim_adapter_test.cpp include/rd_ragsim.hpp include/rd.h $(LIB)
 	g++ -std=c++17 -O2 -Wall -Wextra -Iinclude -o $@ $< -L$(PKG)/lib -l:librd_b200.so -Wl,-rpath,'$$ORIGIN/../../$(PKG)/lib'
 all: tests/cpp/ragsim_adapter_cpu tests/cpp/ragsim_adapter_b200
+
+# C++ end-to-end latency of rd_search through the C ABI (tools/e2e_latency.cpp)
+tools/e2e_latency: tools/e2e_latency.cpp include/rd.h $(LIB)
+	g++ -std=c++17 -O2 -Wall -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG)/lib -l:librd_b200.so \
+	    -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib' -Wl,-rpath,/usr/local/cuda/lib64
