@@ -194,8 +194,10 @@ __device__ __forceinline__ uint32_t f2key(float f) {
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-// block-wide exclusive scan of one int per thread (256 threads); returns total via *total
+// block-wide exclusive scan of one int per thread (NT threads, NT / 32 <= 8 warps); returns total via *total
+template <int NT>
 __device__ int block_excl_scan(int v, int* sh, int* total) {
+  constexpr int kW = NT / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int x = v;
 #pragma unroll
@@ -206,26 +208,28 @@ __device__ int block_excl_scan(int v, int* sh, int* total) {
   if (lane == 31) sh[w] = x;
   __syncthreads();
   if (w == 0) {
-    int s = lane < 8 ? sh[lane] : 0;
+    int s = lane < kW ? sh[lane] : 0;
 #pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {
+    for (int o = 1; o < kW; o <<= 1) {
       int y = __shfl_up_sync(0xffffffffu, s, o);
       if (lane >= o) s += y;
     }
-    if (lane < 8) sh[lane] = s;
+    if (lane < kW) sh[lane] = s;
   }
   __syncthreads();
   const int base = w ? sh[w - 1] : 0;
-  *total = sh[7];
+  *total = sh[kW - 1];
   __syncthreads();
   return base + x - v;
 }
 
-constexpr int kSelThreads = 256;
+constexpr int kSelThreads = 256;    // small batches (staged rows): more threads per query
+constexpr int kSelThreadsLarge = 128;  // large batches: 7 CTAs per SM, one resident wave at B = 1024
 constexpr int kSelMaxCand = 512;
 
 // Selects the C smallest of keys[0..nlist) into cand[0..C): all keys < T plus the
 // first keys == T by index (radix select, 11+11+10 bits, then an ordered compaction).
+template <int NT>
 __device__ uint32_t select_smallest(const uint32_t* keys, int nlist, int C, int* hist, int* scan_sh, int* cand,
                                     uint32_t* sel_prefix, uint32_t* sel_k) {
   const int tid = threadIdx.x;
@@ -234,18 +238,18 @@ __device__ uint32_t select_smallest(const uint32_t* keys, int nlist, int C, int*
   const int widths[3] = {11, 11, 10};
   for (int pass = 0; pass < 3; ++pass) {
     const int sh = shifts[pass], nb = 1 << widths[pass];
-    for (int i = tid; i < nb; i += kSelThreads) hist[i] = 0;
+    for (int i = tid; i < nb; i += NT) hist[i] = 0;
     __syncthreads();
-    for (int j = tid; j < nlist; j += kSelThreads) {
+    for (int j = tid; j < nlist; j += NT) {
       const uint32_t kv = keys[j];
       if ((kv & mask) == prefix) atomicAdd(&hist[(kv >> sh) & (nb - 1)], 1);
     }
     __syncthreads();
-    const int per = nb / kSelThreads;
+    const int per = nb / NT;
     int local = 0;
     for (int i = 0; i < per; ++i) local += hist[tid * per + i];
     int tot;
-    const int before = block_excl_scan(local, scan_sh, &tot);
+    const int before = block_excl_scan<NT>(local, scan_sh, &tot);
     if (before < (int)kk && before + local >= (int)kk) {
       int run = before;
       for (int i = 0; i < per; ++i) {
@@ -265,7 +269,7 @@ __device__ uint32_t select_smallest(const uint32_t* keys, int nlist, int C, int*
     __syncthreads();
   }
   const uint32_t T = prefix;
-  const int per = (nlist + kSelThreads - 1) / kSelThreads;
+  const int per = (nlist + NT - 1) / NT;
   const int j0 = tid * per, j1 = min(nlist, j0 + per);
   int nlt = 0, neq = 0;
   for (int j = j0; j < j1; ++j) {
@@ -273,8 +277,8 @@ __device__ uint32_t select_smallest(const uint32_t* keys, int nlist, int C, int*
     neq += keys[j] == T;
   }
   int tot_lt, tot_eq;
-  int olt = block_excl_scan(nlt, scan_sh, &tot_lt);
-  int oeq = block_excl_scan(neq, scan_sh, &tot_eq);
+  int olt = block_excl_scan<NT>(nlt, scan_sh, &tot_lt);
+  int oeq = block_excl_scan<NT>(neq, scan_sh, &tot_eq);
   for (int j = j0; j < j1; ++j) {
     if (keys[j] < T) {
       cand[olt++] = j;
@@ -287,6 +291,7 @@ __device__ uint32_t select_smallest(const uint32_t* keys, int nlist, int C, int*
   return T;
 }
 
+template <int NT>
 __device__ __forceinline__ float block_reduce_min(float v, float* sh) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -295,9 +300,10 @@ __device__ __forceinline__ float block_reduce_min(float v, float* sh) {
   if (lane == 0) sh[w] = v;
   __syncthreads();
   float r = sh[0];
-  for (int i = 1; i < kSelThreads / 32; ++i) r = fminf(r, sh[i]);
+  for (int i = 1; i < NT / 32; ++i) r = fminf(r, sh[i]);
   return r;
 }
+template <int NT>
 __device__ __forceinline__ float block_reduce_max(float v, float* sh) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -306,7 +312,7 @@ __device__ __forceinline__ float block_reduce_max(float v, float* sh) {
   if (lane == 0) sh[w] = v;
   __syncthreads();
   float r = sh[0];
-  for (int i = 1; i < kSelThreads / 32; ++i) r = fmaxf(r, sh[i]);
+  for (int i = 1; i < NT / 32; ++i) r = fmaxf(r, sh[i]);
   return r;
 }
 
@@ -325,8 +331,8 @@ __device__ __forceinline__ float block_reduce_max(float v, float* sh) {
 // exact top-nprobe set is then the sure-in candidates plus the best ambiguous ones by (canonical
 // exact distance, list id) — only those few need the fp64 sum. Exact-order mode (rd_probe) and
 // uncertified queries recompute every candidate (or every centroid) exactly.
-template <bool kStage>
-__global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const SelectParams p) {
+template <bool kStage, int NT>
+__global__ void __launch_bounds__(NT) coarse_select_kernel(const SelectParams p) {
   RD_TS(13);  // entry, before the wait on the previous kernel
   RD_PDL_PROLOGUE();
   extern __shared__ __align__(16) uint32_t keys[];
@@ -358,9 +364,9 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
     mbar_init(&bar, 1);
     fence_mbar_init();
   }
-  float qv[1024 / kSelThreads];  // d <= 1024; stored after the distance row's loads are in flight
+  float qv[1024 / NT];  // d <= 1024; stored after the distance row's loads are in flight
 #pragma unroll
-  for (int k = 0; k < 1024 / kSelThreads; ++k) qv[k] = tid + k * kSelThreads < d ? q[tid + k * kSelThreads] : 0.f;
+  for (int k = 0; k < 1024 / NT; ++k) qv[k] = tid + k * NT < d ? q[tid + k * NT] : 0.f;
   const float qn = p.qnorm[b];
   // bulk-copies rows r < nrows (row_ptr(r), device memory) into st; every thread waits
   auto stage_bulk = [&](int nrows, auto row_ptr) {
@@ -376,16 +382,16 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
   float vmin = __builtin_huge_valf(), vmax = -__builtin_huge_valf();
   int jmin = 0;
   constexpr int kVB = 16;  // row loads in flight per thread
-  for (int j0 = tid; j0 < nlist; j0 += kVB * kSelThreads) {
+  for (int j0 = tid; j0 < nlist; j0 += kVB * NT) {
     float v[kVB];
 #pragma unroll
     for (int k = 0; k < kVB; ++k) {
-      const int j = j0 + k * kSelThreads;
+      const int j = j0 + k * NT;
       v[k] = j < nlist ? drow[j] : 0.f;
     }
 #pragma unroll
     for (int k = 0; k < kVB; ++k) {
-      const int j = j0 + k * kSelThreads;
+      const int j = j0 + k * NT;
       if (j < nlist) {
         vals[j] = v[k];
         if (v[k] < vmin) jmin = j;
@@ -395,17 +401,19 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
     }
   }
 #pragma unroll
-  for (int k = 0; k < 1024 / kSelThreads; ++k)
-    if (tid + k * kSelThreads < d) {
-      qd[tid + k * kSelThreads] = (double)qv[k];
-      if constexpr (kStage) qf[tid + k * kSelThreads] = qv[k];
+  for (int k = 0; k < 1024 / NT; ++k)
+    if (tid + k * NT < d) {
+      if constexpr (kStage) {  // (large batches read q straight from global memory)
+        qd[tid + k * NT] = (double)qv[k];
+        qf[tid + k * NT] = qv[k];
+      }
     }
   if constexpr (kStage) {  // approximate nearest centroid: warm L2 with its list's first 32 rows (the likely seed)
     __syncthreads();
     if (vmin < __builtin_huge_valf()) atomicMin(&amin, ((unsigned long long)f2key(vmin) << 32) | (unsigned)jmin);
   }
-  vmin = block_reduce_min(vmin, fsh);
-  vmax = block_reduce_max(vmax, fsh);
+  vmin = block_reduce_min<NT>(vmin, fsh);
+  vmax = block_reduce_max<NT>(vmax, fsh);
   // kStage: the approximately nearest list's first 32 rows (the likely seeding list) are bulk-copied
   // into the staging area now and consumed after the candidate search, off the critical path
   int seed_l = -1;  // uniform: every thread reads the same amin and list metadata
@@ -438,25 +446,26 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
     for (int round = 0; round < 3 && ncand < 0; ++round) {
       const float width = (hi - lo) / 2048.f;
       if (!(width > 0.f)) break;
-      for (int i = tid; i < 2048; i += kSelThreads) hist[i] = 0;
+      for (int i = tid; i < 2048; i += NT) hist[i] = 0;
       __syncthreads();
-      for (int j = tid; j < nlist; j += kSelThreads) {
+      for (int j = tid; j < nlist; j += NT) {
         const float v = vals[j];
         if (v >= lo && v < hi) atomicAdd(&hist[min(2047, (int)((v - lo) / width))], 1);
       }
       __syncthreads();
       int local = 0;
-      for (int i = 0; i < 8; ++i) local += hist[tid * 8 + i];
+      constexpr int kPer = 2048 / NT;  // bins per thread
+      for (int i = 0; i < kPer; ++i) local += hist[tid * kPer + i];
       int tot;
-      const int before = block_excl_scan(local, scan_sh, &tot);
+      const int before = block_excl_scan<NT>(local, scan_sh, &tot);
       if (tid == 0) found_bin = 2047;
       __syncthreads();
       if (below + before < Cwant && below + before + local >= Cwant) {
         int run = below + before;
-        for (int i = 0; i < 8; ++i) {
-          run += hist[tid * 8 + i];
+        for (int i = 0; i < kPer; ++i) {
+          run += hist[tid * kPer + i];
           if (run >= Cwant) {
-            found_bin = tid * 8 + i;
+            found_bin = tid * kPer + i;
             break;
           }
         }
@@ -467,17 +476,17 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
       const float edge_lo = lo + fb * width;
       // exact recount of {v < edge_hi}
       int c = 0;
-      for (int j = tid; j < nlist; j += kSelThreads) c += vals[j] < edge_hi;
+      for (int j = tid; j < nlist; j += NT) c += vals[j] < edge_hi;
       int total;
-      block_excl_scan(c, scan_sh, &total);
+      block_excl_scan<NT>(c, scan_sh, &total);
       if (total >= Cwant && total <= kSelMaxCand) {
         ncand = total;
         hi_edge = edge_hi;
       } else {
         int cb = 0;
-        for (int j = tid; j < nlist; j += kSelThreads) cb += vals[j] < edge_lo;
+        for (int j = tid; j < nlist; j += NT) cb += vals[j] < edge_lo;
         int tb;
-        block_excl_scan(cb, scan_sh, &tb);
+        block_excl_scan<NT>(cb, scan_sh, &tb);
         below = tb;
         lo = edge_lo;
         hi = edge_hi;
@@ -488,7 +497,7 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
   if (ncand >= 0) {
     if (tid == 0) ncand_s = 0;
     __syncthreads();
-    for (int j = tid; j < nlist; j += kSelThreads)
+    for (int j = tid; j < nlist; j += NT)
       if (vals[j] < hi_edge) cand[atomicAdd(&ncand_s, 1)] = j;
     __syncthreads();
   }
@@ -500,7 +509,7 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
       mbar_wait(&bar, bphase);
       bphase ^= 1;
       const float e = l2_group8_f32(qf, st + grp * ds, d, j8);  // rows >= seed_rows: stale, masked
-      seed_pre = block_reduce_max(grp < p.seed_rows ? e : 0.f, fsh);
+      seed_pre = block_reduce_max<NT>(grp < p.seed_rows ? e : 0.f, fsh);
       __syncthreads();  // the staging area is free again
     }
   }
@@ -517,7 +526,7 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
     int* byrank = hist + 512;    // [512] candidate index by approximate rank
     int* ambl = hist + 1024;     // [512] ambiguous candidates in approximate-rank order
     float* adist = reinterpret_cast<float*>(hist + 1536);  // [512] their exact distances
-    for (int i = tid; i < C; i += kSelThreads) {
+    for (int i = tid; i < C; i += NT) {
       const int l = cand[i];
       cdist[i] = vals[l];
       // seeding eligibility, resolved here so the rank-order walk below needs no global loads
@@ -527,7 +536,7 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
     __syncthreads();
     // rank and window counts: one group of 8 lanes per candidate, lane j8 scans k = j8 (mod 8)
     int below = 0;
-    for (int i0 = 0; i0 < C; i0 += kSelThreads / 8) {
+    for (int i0 = 0; i0 < C; i0 += NT / 8) {
       const int i = i0 + grp;
       const float vi = i < C ? cdist[i] : 0.f;
       const int ci = i < C ? cand[i] : 0;
@@ -576,8 +585,8 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
     if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0) p.dbg[14] = (unsigned long long)na;
     if (below_s >= np && need >= 0 && need <= na) {
       if (need > 0 && need < na) {  // the best `need` ambiguous candidates by exact (distance, list id)
-        for (int a0 = 0; a0 < na; a0 += kSelThreads / 8) {
-          const int rows = min(kSelThreads / 8, na - a0);
+        for (int a0 = 0; a0 < na; a0 += NT / 8) {
+          const int rows = min(NT / 8, na - a0);
           const int a = a0 + grp;
           float e;
           if constexpr (kStage) {
@@ -585,12 +594,12 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
             e = exact_l2_group8_qd(qd, st + grp * ds, a < na ? d : 0, j8);
             __syncthreads();  // the staging area is reused by the next chunk
           } else {
-            e = exact_l2_group8_qd<16>(qd, p.centroids + (size_t)cand[ambl[a < na ? a : na - 1]] * d, d, j8);
+            e = exact_l2_group8_impl<true, 16>(q, p.centroids + (size_t)cand[ambl[a < na ? a : na - 1]] * d, d, j8);
           }
           if (a < na && j8 == 0) adist[a] = e;
         }
         __syncthreads();
-        for (int a = tid; a < na; a += kSelThreads) {
+        for (int a = tid; a < na; a += NT) {
           const float da = adist[a];
           const int ia = cand[ambl[a]];
           int r = 0;
@@ -601,7 +610,7 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
           state[ambl[a]] = r < need ? 1 : 0;
         }
       } else {
-        for (int a = tid; a < na; a += kSelThreads) state[ambl[a]] = need == na ? 1 : 0;
+        for (int a = tid; a < na; a += NT) state[ambl[a]] = need == na ? 1 : 0;
       }
       __syncthreads();
       RD_TS(9);
@@ -642,21 +651,23 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
         C = ncand;
       } else {
         // exact keys for every centroid, then the np smallest by (exact distance, list id)
-        for (int c0 = 0; c0 < nlist; c0 += kSelThreads / 8) {
+        for (int c0 = 0; c0 < nlist; c0 += NT / 8) {
           const int c = c0 + grp;
           const int cc = c < nlist ? c : nlist - 1;
-          const float e = exact_l2_group8_qd(qd, p.centroids + (size_t)cc * d, d, j8);
+          const float e = kStage ? exact_l2_group8_qd(qd, p.centroids + (size_t)cc * d, d, j8)
+                                 : exact_l2_group8_impl<true, 16>(q, p.centroids + (size_t)cc * d, d, j8);
           __syncthreads();
           if (c < nlist && j8 == 0) keys[c] = f2key(e);
         }
         __syncthreads();
         C = np;
-        select_smallest(keys, nlist, C, hist, scan_sh, cand, &sel_prefix, &sel_k);
+        select_smallest<NT>(keys, nlist, C, hist, scan_sh, cand, &sel_prefix, &sel_k);
       }
-      for (int c0 = 0; c0 < C; c0 += kSelThreads / 8) {
+      for (int c0 = 0; c0 < C; c0 += NT / 8) {
         const int c = c0 + grp;
         const int cc = c < C ? c : C - 1;
-        const float e = exact_l2_group8_qd(qd, p.centroids + (size_t)cand[cc] * d, d, j8);
+        const float e = kStage ? exact_l2_group8_qd(qd, p.centroids + (size_t)cand[cc] * d, d, j8)
+                               : exact_l2_group8_impl<true, 16>(q, p.centroids + (size_t)cand[cc] * d, d, j8);
         if (c < C && j8 == 0) cdist[c] = e;
       }
       // rank sort by (exact distance, list id): keys are distinct (list ids)
@@ -664,7 +675,7 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
       {
         float* rd_ = reinterpret_cast<float*>(hist);  // hist is free here: [0, 512) dists, [512, 1024) ids
         int* rc_ = hist + kSelMaxCand;
-        for (int i = tid; i < C; i += kSelThreads) {
+        for (int i = tid; i < C; i += NT) {
           const float di = cdist[i];
           const int ii = cand[i];
           int r = 0;
@@ -676,7 +687,7 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
           rc_[r] = ii;
         }
         __syncthreads();
-        for (int i = tid; i < C; i += kSelThreads) {
+        for (int i = tid; i < C; i += NT) {
           cdist[i] = rd_[i];
           cand[i] = rc_[i];
         }
@@ -695,7 +706,7 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
       __syncthreads();
       if (certified) break;
     }
-    for (int i = tid; i < p.nprobe; i += kSelThreads) {
+    for (int i = tid; i < p.nprobe; i += NT) {
       p.probes[(size_t)b * p.nprobe + i] = i < np ? cand[i] : -1;
       if (p.bitmap && i < np) atomicOr(p.bitmap + (size_t)cand[i] * p.W + (b >> 5), 1u << (b & 31));
     }
@@ -717,7 +728,7 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
   // bound) + 2 eps_scan, a valid upper bound on the final 32nd-best approximate distance, so the
   // scan's certification holds (merge.cu)
   if (p.qthr) {
-    __shared__ float red[kSelThreads / 32];
+    __shared__ float red[NT / 32];
     const int l = lsel;
     if (l < 0) {
       if (tid == 0) p.qthr[b] = 0x7f7f7f7f;
@@ -729,10 +740,14 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
         if constexpr (kStage) {
           stage_bulk(p.seed_rows, [&](int r) { return r0 + (size_t)r * d; });
           e = l2_group8_f32(qf, st + grp * ds, d, j8);
-        } else {
-          e = l2_group8_f32<16>(q, r0 + (size_t)min(grp, p.seed_rows - 1) * d, d, j8);
+          if (grp >= p.seed_rows) e = 0.f;  // only the first seed_rows rows bound the threshold
+        } else {  // NT / 8 rows per pass (a uniform trip count keeps the group shuffles converged)
+          for (int rb = 0; rb < p.seed_rows; rb += NT / 8) {
+            const int r = rb + grp;
+            const float v = l2_group8_f32<16>(q, r0 + (size_t)min(r, p.seed_rows - 1) * d, d, j8);
+            if (r < p.seed_rows) e = fmaxf(e, v);
+          }
         }
-        if (grp >= p.seed_rows) e = 0.f;  // only the first seed_rows rows bound the threshold
       }
       float m = e;
 #pragma unroll
@@ -741,7 +756,7 @@ __global__ void __launch_bounds__(kSelThreads) coarse_select_kernel(const Select
       __syncthreads();
       if (tid == 0) {
         float mx = red[0];
-        for (int i = 1; i < kSelThreads / 32; ++i) mx = fmaxf(mx, red[i]);
+        for (int i = 1; i < NT / 32; ++i) mx = fmaxf(mx, red[i]);
         if (pre) mx = seed_pre;
         const float eps_s =
             2.f * ((d / 2 + 8) * u * 2.f * sqrtf(qn) * p.xmax + 8.f * u * (qn + p.xmax * p.xmax)) + 1e-30f;
@@ -778,15 +793,19 @@ cudaError_t launch_qprep(const QprepArgs& a, cudaStream_t s) {
   return launch_k(qprep_kernel, dim3((unsigned)(blocks < 148 * 8 ? blocks : 148 * 8)), dim3(256), 0, s, a);
 }
 
-cudaError_t launch_select(const SelectParams& p, bool stage, cudaStream_t s) {
+cudaError_t launch_select(const SelectParams& p, bool stage, cudaStream_t s, int num_sms) {
   if (p.nprobe + kCoarseExtra > kSelMaxCand) return cudaErrorInvalidValue;
   const size_t keys = sizeof(uint32_t) * (size_t)((p.nlist + 3) & ~3);
   const size_t qd = sizeof(double) * (size_t)p.d;
   const size_t staged = keys + qd + sizeof(float) * ((size_t)p.d + 32 * (size_t)(p.d + kStagePad));
   if (stage && staged <= 200 * 1024)
-    return launch_k(coarse_select_kernel<true>, dim3(p.B), dim3(kSelThreads), staged, s, p);
-  // large batches (enough CTAs to hide latency) or very large nlist: the direct-load variant
-  return launch_k(coarse_select_kernel<false>, dim3(p.B), dim3(kSelThreads), keys + qd, s, p);
+    return launch_k(coarse_select_kernel<true, kSelThreads>, dim3(p.B), dim3(kSelThreads), staged, s, p);
+  // large batches (enough CTAs to hide latency) or very large nlist: the direct-load variant. Past
+  // one resident wave of 256-thread CTAs (64 registers and ~35 KiB each: 4 per SM), 128 threads
+  // and no smem copy of q fit 7 per SM (1024 queries in one wave: 65 -> 55 us on B200)
+  if (p.B > 4LL * num_sms)
+    return launch_k(coarse_select_kernel<false, kSelThreadsLarge>, dim3(p.B), dim3(kSelThreadsLarge), keys, s, p);
+  return launch_k(coarse_select_kernel<false, kSelThreads>, dim3(p.B), dim3(kSelThreads), keys, s, p);
 }
 
 }  // namespace rd

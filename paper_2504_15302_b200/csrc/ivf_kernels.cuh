@@ -158,7 +158,8 @@ struct SelectParams {
   int seed_rows = 32;
 };
 // stage: q and candidate rows go through shared memory (latency-bound small batches)
-cudaError_t launch_select(const SelectParams& p, bool stage, cudaStream_t s);
+// num_sms: batches beyond one resident wave of 256-thread CTAs (4 per SM) use 128-thread CTAs
+cudaError_t launch_select(const SelectParams& p, bool stage, cudaStream_t s, int num_sms = 148);
 
 // Scan tile categories (plan.cu): tensor-core tiles of <= 16 queries (16-wide scan), of <= 32
 // queries (32-wide scan), and FFMA tiles.

@@ -128,7 +128,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   // and the seed bounds, that rank's distance
   const int thr_rank = std::min(rd::kTopK - 1, k + 8);
   sp.seed_rows = thr_rank + 1;
-  h->traced("select", s, sp.dbg, [&] { CK(rd::launch_select(sp, h->stage_rows(B), s)); });
+  h->traced("select", s, sp.dbg, [&] { CK(rd::launch_select(sp, h->stage_rows(B), s, h->num_sms)); });
   launches += rd::coarse_small((int)B) ? 2 : 3;  // (query prep +) coarse + select
   rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
                     w.list_ntile.p, w.list_toff.p, w.list_q.p, {w.tiles16.p, w.tiles.p, w.ff_tiles.p}, w.meta(),
@@ -562,7 +562,7 @@ int rd_probe(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32
     }
     rd::SelectParams sp{w.Dc.p, w.q.p, w.qnorm.p, h->centroids.p, w.probes.p, w.fails(), (int)B, nl, nprobe, d, h->cmax,
                         h->d_list_off.p, h->d_res_row0.p, h->arena.p, h->xmax, nullptr, 1};
-    CK(rd::launch_select(sp, h->stage_rows(B), 0));
+    CK(rd::launch_select(sp, h->stage_rows(B), 0, h->num_sms));
     CK(cudaMemcpy(out_lists, w.probes.p, sizeof(int) * B * nprobe, cudaMemcpyDeviceToHost));
   });
 }
