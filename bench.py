@@ -359,7 +359,9 @@ def run_ours(args, cfg):
     achieved = scan_bytes / (scan_ms * 1e-3) / 1e9 if scan_ms > 0 else 0.0
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "scan_traffic.json")
-    if os.path.exists(tpath):
+    # the captured traffic is of one unsharded launch at the config's default batch: only that
+    # workload may quote it
+    if os.path.exists(tpath) and shards == 1 and not args.batch:
         traffic = json.load(open(tpath)).get(args.config)
     launches_per_search = st["kernel_launches"]
     h2d_link = None
