@@ -262,6 +262,12 @@ struct rd_index {
   int tc_g_force = std::getenv("RD_TC_G") ? std::atoi(std::getenv("RD_TC_G")) : 0;
   // streamed query operand for the 16-query scan (scan_tc.cu): -1 by batch, RD_STREAM_B=0|1 forces
   int stream_force = std::getenv("RD_STREAM_B") ? std::atoi(std::getenv("RD_STREAM_B")) : -1;
+  // spare candidates reranked beyond k (RD_RERANK_MARGIN, 8..32): more tolerate more duplicate
+  // vectors around rank k before a query needs the exact fallback, at more rerank reads and a
+  // looser scan pruning rank
+  int rerank_margin = std::getenv("RD_RERANK_MARGIN")
+                          ? std::max(8, std::min(32, std::atoi(std::getenv("RD_RERANK_MARGIN"))))
+                          : 8;
   bool stage_rows(long long B) const { return B <= (stage_max_b >= 0 ? stage_max_b : 2LL * num_sms); }
   long long n = 0;
   int d = 0, nlist = 0;

@@ -226,6 +226,8 @@ struct MergeParams {
   unsigned* margin_fail;            // device scalar: number of uncertified queries
   int* fail_list;                  // B: ids of uncertified queries (exact fallback work list)
   int B;
+  // candidates reranked exactly (min(32, k + margin)); the next one's distance certifies
+  int m_rerank = 32;
   unsigned long long* dbg = nullptr;  // RD_DEBUG_TS: globaltimer checkpoints of CTA 0
 };
 // stage: the 32 rerank rows go through shared memory (latency-bound small batches)

@@ -91,12 +91,12 @@ __global__ void __launch_bounds__(256, kStage ? 1 : 8) merge_rerank_kernel(const
 #pragma unroll
       for (int j = 16; j > 0; j >>= 1) bitonic_step(ld, lk, lane, j, true);
     }
-    // The best m = k + 8 candidates (of the 32) are reranked: the (m+1)-th approximate distance
-    // bounds every row not reranked (the rest of the 32 and everything the scan dropped), so
-    // certification reads tau = that distance; the 8 spare candidates keep it holding unless the
-    // data has near-ties at rank k (then the exact fallback runs). Fewer rows cut the rerank's HBM
-    // reads (k = 10: 18 of 32).
-    const int m = min(kTopK, p.k + 8);
+    // The best m = min(32, k + margin) candidates are reranked: the (m+1)-th approximate distance
+    // bounds every row not reranked (the rest of the list and everything the scan dropped), so
+    // certification reads tau = that distance; the spare candidates keep it holding unless the data
+    // has (near-)ties across ranks k..m (duplicates; then the exact fallback runs). Fewer rows cut
+    // the rerank's HBM reads (k = 10, margin 8: 18 of 32).
+    const int m = p.m_rerank;
     const float* xp = nullptr;
     long long id = kNoKey;
     if (lk != kNoKey && lane < m) {  // candidate rows: list of the row (row_list), address, user id

@@ -124,9 +124,10 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     sp.bitmap = w.bitmap.p;
     sp.W = W;
   }
-  // the merge reranks min(32, k + 8) candidates and certifies against the next: scans prune with,
-  // and the seed bounds, that rank's distance
-  const int thr_rank = std::min(rd::kTopK - 1, k + 8);
+  // the merge reranks m = min(32, k + margin) candidates and certifies against the next: scans
+  // prune with, and the seed bounds, that rank's distance
+  const int m_rerank = std::min(rd::kTopK, k + h->rerank_margin);
+  const int thr_rank = std::min(rd::kTopK - 1, m_rerank);
   sp.seed_rows = thr_rank + 1;
   h->traced("select", s, sp.dbg, [&] { CK(rd::launch_select(sp, h->stage_rows(B), s, h->num_sms)); });
   launches += rd::coarse_small((int)B) ? 2 : 3;  // (query prep +) coarse + select
@@ -363,6 +364,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
                      h->d_list_base.p, h->d_ids.p, h->d_row_list.p, h->arena.p,
                      h->arena.p + (size_t)h->n_resident * d, nl, d, k, h->xmax, d_ids, d_dists,
                      w.fails() + 1, w.fail_list.p, (int)B};
+  mp.m_rerank = m_rerank;
   if (chain) mp.dbg = chain + 64;
   h->traced("merge", s, mp.dbg, [&] { CK(rd::launch_merge(mp, h->stage_rows(B), s)); });
   rd::FallbackParams fp{w.fail_list.p, w.fails() + 1, w.probes.p, nprobe, d_q, h->d_list_off.p, h->d_list_base.p,

@@ -210,3 +210,29 @@ def test_timing_stages(engine):
     assert 0.0 < t["scan_ms"] < t["total_ms"]
     np.testing.assert_array_equal(on.ids, off.ids)
     np.testing.assert_array_equal(on.dists, off.dists)
+
+
+@pytest.mark.parametrize("margin", ["8", "22"])
+def test_duplicate_heavy_data(engine, oracle, margin, monkeypatch):
+    # a corpus where each query's neighbourhood holds many exact duplicates: ties across ranks
+    # k..k+margin defeat the candidate margin and send queries to the exact fallback (a wider
+    # margin needs more duplicates to do so); results are the oracle's either way
+    monkeypatch.setenv("RD_RERANK_MARGIN", margin)
+    rng = np.random.default_rng(5)
+    d, nlist = 128, 16
+    C = rng.standard_normal((nlist, d)).astype(np.float32)
+    base = (C[rng.integers(0, nlist, 600)] + 0.3 * rng.standard_normal((600, d))).astype(np.float32)
+    X = np.repeat(base, 24, axis=0)  # every vector 24 times: ties span ranks 1..24
+    assign = np.argmin(((X[:, None, :] - C[None]) ** 2).sum(-1), axis=1)
+    order = np.argsort(assign, kind="stable")
+    X = X[order]
+    offs = np.concatenate([[0], np.cumsum(np.bincount(assign, minlength=nlist))]).astype(np.int64)
+    Q = (base[:40] + 0.01 * rng.standard_normal((40, d))).astype(np.float32)
+    e = engine.index_from_host(X, offs, C).search(Q, 3, 10)
+    o = oracle.index_from_host(X, offs, C).search(Q, 3, 10)
+    np.testing.assert_array_equal(e.ids, o.ids)
+    np.testing.assert_array_equal(e.dists, o.dists)
+    if margin == "8":  # 18 reranked, the 19th ties the 10th: every query falls back to exact
+        assert e.stats["margin_failures"] == len(Q)
+    else:  # 32 reranked, the 33rd is another vector: certified without the fallback
+        assert e.stats["margin_failures"] == 0
