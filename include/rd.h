@@ -243,6 +243,58 @@ int rd_merge_topk_device(int32_t G, int64_t B, int32_t k, const int64_t* d_shard
                          const float* d_shard_dists, int64_t* d_out_ids, float* d_out_dists,
                          void* stream);
 
+/* ---- multi-GPU shard groups ----
+ * north_star: "the lists shard across the GPUs of one 8xB200 box, each shard returns a local
+ * top-k, and the results are merged with an NCCL gather over NVLink". A group holds G row stripes
+ * of one knowledge base (stripe g = rows [g*len/G, (g+1)*len/G) of every list; rd_synth_desc
+ * shard/num_shards, or any stripe handles the caller built), searches every stripe with the same
+ * batch, gathers the per-stripe top-k to the root stripe's device (NCCL grouped send/recv; stripes
+ * sharing one device gather by device copies, as NCCL admits one rank per device) and merges them
+ * there by (distance, id). One call returns one merged result, which is what the reference's
+ * retrieval worker consumes per batch (core/src/simulator.cpp:359, serial :560).
+ * Two forms:
+ *   - one process driving G devices: rd_group_create / rd_group_create_synthetic;
+ *   - one process per device (e.g. torchrun): rank 0 calls rd_group_unique_id, the caller
+ *     broadcasts the bytes, every rank calls rd_group_create_rank with its own stripe; rank 0 is
+ *     the root and receives the merged result, other ranks receive their own stripe's top-k.
+ * Group searches are collective in the second form: every rank calls with the same batch.
+ * CPU oracle: the single-process forms search the stripes in turn and merge on the host;
+ * rd_group_unique_id / rd_group_create_rank / rd_group_search_device return RD_ERR_INVALID. */
+#define RD_GROUP_ID_BYTES 128
+#define RD_GROUP_TRANSPORT_NONE 0 /* one stripe */
+#define RD_GROUP_TRANSPORT_NCCL 1 /* NCCL send/recv to the root device */
+#define RD_GROUP_TRANSPORT_COPY 2 /* device-to-device copies (stripes sharing a device; RD_GROUP_TRANSPORT=copy) */
+typedef struct rd_group rd_group;
+typedef struct {
+  int32_t num_shards;   /* stripes in the whole group */
+  int32_t local_shards; /* stripes driven by this process */
+  int32_t rank, nranks; /* one process per device: this rank (root = 0); else 0, 1 */
+  int32_t transport;    /* RD_GROUP_TRANSPORT_* */
+  int32_t root_device;
+  int64_t n;            /* vectors held by this process's stripes */
+  int64_t n_resident;
+} rd_group_info;
+/* G stripe handles on any devices; the group owns them from a successful call on (destroying the
+ * group destroys them). */
+int rd_group_create(rd_index* const* shards, int32_t G, rd_group** out);
+/* Stripe g of desc's knowledge base (desc->shard / num_shards ignored) on devices[g]. */
+int rd_group_create_synthetic(const rd_synth_desc* desc, const int32_t* devices, int32_t G, rd_group** out);
+int rd_group_unique_id(uint8_t* out /* RD_GROUP_ID_BYTES */);
+/* This process's stripe (owned by the group from a successful call on) as rank `rank` of `nranks`. */
+int rd_group_create_rank(rd_index* shard, const uint8_t* id, int32_t nranks, int32_t rank, rd_group** out);
+int rd_group_info_get(const rd_group* g, rd_group_info* out);
+/* Borrowed handle of the i-th local stripe (NULL if out of range): info, timing, migration. */
+rd_index* rd_group_shard(rd_group* g, int32_t i);
+/* rd_index_place on every local stripe (an HBM budget applies per device). */
+int rd_group_place(rd_group* g, const rd_placement* placement);
+/* Host buffers; stats sum the stripes' counters (device times: the slowest stripe). */
+int rd_group_search(rd_group* g, const float* queries, int64_t B, int32_t nprobe, int32_t k,
+                    int64_t* out_ids, float* out_dists, rd_search_stats* stats);
+/* Device buffers on the root device (one process) or this rank's device, stream on that device. */
+int rd_group_search_device(rd_group* g, const float* d_queries, int64_t B, int32_t nprobe, int32_t k,
+                           int64_t* d_ids, float* d_dists, void* stream, int32_t sync, rd_search_stats* stats);
+void rd_group_destroy(rd_group* g);
+
 /* ---- synthetic data and canonical arithmetic (shared spec) ---- */
 uint64_t rd_derive_seed(uint64_t master, uint64_t stream); /* rng.hpp:52-56 */
 uint64_t rd_splitmix_at(uint64_t seed, uint64_t i);       /* (i+1)-th Rng(seed).next_u64(), rng.hpp:16-21 */

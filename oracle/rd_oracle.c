@@ -856,3 +856,296 @@ int32_t rd_staging_depth(double free_bytes, double item_bytes) {
   if (q > 1 << 20) return 1 << 20;
   return (int32_t)q;
 }
+
+/* ------------------------------------------------------------------ sampled oracle (oracle-only entry)
+ * rd_oracle_synth_search: exact IVF-Flat (same semantics as rd_search above) over the synthetic
+ * knowledge base `s` restricted to the row stripes g of s->num_shards with bit g set in
+ * shard_mask, WITHOUT materialising the knowledge base: only the probed lists' rows of the selected
+ * stripes are regenerated from (seed, id) ("CPU verification on a sampled query
+ * subset only, with vectors regenerated from (seed, id)"). This is how a 100M x 768 (307 GB) index
+ * is checked on a host that cannot hold it. s->shard is ignored. Not part of rd.h. */
+typedef struct {
+  const rd_synth_desc* s;
+  uint64_t sc, sx;
+  const float* centroids;
+  const float* q;
+  int32_t np, k;
+  int32_t* lists;              /* B x np probes */
+  const int64_t* mem_off;      /* per marked list slot: member range in mem_ids */
+  const int64_t* mem_ids;      /* selected-stripe members, ascending id */
+  const int32_t* mark;         /* list -> slot or -1 */
+  const int32_t* marked;       /* slot -> list */
+  const int64_t* pair_off;     /* slot -> range in pair_q */
+  const int64_t* pair_q;       /* (query * np + probe index) pairs per slot */
+  cand* part;                  /* B x np x k partial top-k */
+  int32_t* part_cnt;           /* B x np */
+} synth_search_ctx;
+
+static void synth_probe_range(void* p, int64_t b, int64_t e) {
+  synth_search_ctx* c = (synth_search_ctx*)p;
+  const int32_t d = c->s->d, nl = c->s->nlist;
+  cand* top = (cand*)malloc(sizeof(cand) * (size_t)c->np);
+  for (int64_t qi = b; qi < e; ++qi) {
+    int32_t cnt = 0;
+    for (int32_t j = 0; j < nl; ++j)
+      topk_push(top, &cnt, c->np, rd_exact_l2(c->q + qi * d, c->centroids + (int64_t)j * d, d), j);
+    for (int32_t i = 0; i < c->np; ++i) c->lists[qi * c->np + i] = (int32_t)top[i].id;
+  }
+  free(top);
+}
+
+static void synth_scan_range(void* p, int64_t b, int64_t e) {
+  synth_search_ctx* c = (synth_search_ctx*)p;
+  const int32_t d = c->s->d;
+  float* x = (float*)malloc(sizeof(float) * (size_t)d);
+  for (int64_t slot = b; slot < e; ++slot) {
+    const float* cen = c->centroids + (int64_t)c->marked[slot] * d;
+    for (int64_t r = c->mem_off[slot]; r < c->mem_off[slot + 1]; ++r) {
+      const int64_t id = c->mem_ids[r];
+      for (int32_t t = 0; t < d; ++t) x[t] = cen[t] + c->s->sigma * unif(c->sx, (uint64_t)(id * d + t));
+      for (int64_t pi = c->pair_off[slot]; pi < c->pair_off[slot + 1]; ++pi) {
+        const int64_t qp = c->pair_q[pi];
+        const int64_t qi = qp / c->np;
+        topk_push(c->part + qp * c->k, c->part_cnt + qp, c->k, rd_exact_l2(c->q + qi * d, x, d), id);
+      }
+    }
+  }
+  free(x);
+}
+
+typedef struct {
+  uint64_t sa;
+  int32_t nl;
+  int32_t* assign;
+} assign_gen_ctx;
+
+static void synth_assign_range(void* p, int64_t b, int64_t e) {
+  assign_gen_ctx* a = (assign_gen_ctx*)p;
+  for (int64_t i = b; i < e; ++i) a->assign[i] = (int32_t)(rd_splitmix_at(a->sa, (uint64_t)i) % (uint64_t)a->nl);
+}
+
+int rd_oracle_synth_search(const rd_synth_desc* s, uint64_t shard_mask, const float* queries, int64_t B,
+                           int32_t nprobe, int32_t k, int64_t* out_ids, float* out_dists) {
+  int rc = check_desc(s);
+  if (rc) return rc;
+  if (B < 0 || nprobe < 1 || k < 1 || (B > 0 && (!queries || !out_ids || !out_dists)))
+    return fail(RD_ERR_INVALID, "synth_search: invalid arguments");
+  if (B == 0) return RD_OK;
+  const int64_t n = s->n;
+  const int32_t d = s->d, nl = s->nlist, G = s->num_shards;
+  const int32_t np = nprobe < nl ? nprobe : nl;
+  synth_search_ctx c;
+  memset(&c, 0, sizeof c);
+  c.s = s;
+  c.sc = rd_derive_seed(s->seed, RD_STREAM_CENTROIDS);
+  c.sx = rd_derive_seed(s->seed, RD_STREAM_VECTOR_NOISE);
+  c.q = queries;
+  c.np = np;
+  c.k = k;
+  float* cen = (float*)malloc(sizeof(float) * (size_t)nl * d);
+  gen_ctx gc = {s, c.sc, c.sx, NULL, NULL, cen, NULL};
+  parallel_for(nl, 16, gen_centroids, &gc);
+  c.centroids = cen;
+  int32_t* lists = (int32_t*)malloc(sizeof(int32_t) * (size_t)B * np);
+  c.lists = lists;
+  parallel_for(B, 1, synth_probe_range, &c);
+  /* marked lists and their (query, probe) pairs */
+  int32_t* mark = (int32_t*)malloc(sizeof(int32_t) * (size_t)nl);
+  for (int32_t l = 0; l < nl; ++l) mark[l] = -1;
+  int32_t nm = 0;
+  for (int64_t i = 0; i < B * np; ++i)
+    if (mark[lists[i]] < 0) mark[lists[i]] = nm++;
+  int32_t* marked = (int32_t*)malloc(sizeof(int32_t) * (size_t)nm);
+  for (int32_t l = 0; l < nl; ++l)
+    if (mark[l] >= 0) marked[mark[l]] = l;
+  int64_t* pair_off = (int64_t*)calloc((size_t)nm + 1, sizeof(int64_t));
+  int64_t* pair_q = (int64_t*)malloc(sizeof(int64_t) * (size_t)B * np);
+  for (int64_t i = 0; i < B * np; ++i) pair_off[mark[lists[i]] + 1]++;
+  for (int32_t m = 0; m < nm; ++m) pair_off[m + 1] += pair_off[m];
+  int64_t* pcur = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nm > 0 ? nm : 1));
+  for (int32_t m = 0; m < nm; ++m) pcur[m] = pair_off[m];
+  for (int64_t i = 0; i < B * np; ++i) pair_q[pcur[mark[lists[i]]]++] = i;
+  free(pcur);
+  /* membership of the marked lists, ascending id, restricted to the selected stripes */
+  int32_t* assign = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
+  if (!assign) return fail(RD_ERR_RUNTIME, "synth_search: out of host memory");
+  assign_gen_ctx ac = {rd_derive_seed(s->seed, RD_STREAM_ASSIGN), nl, assign};
+  parallel_for(n, 1 << 20, synth_assign_range, &ac);
+  int64_t* full_len = (int64_t*)calloc((size_t)nl, sizeof(int64_t));
+  for (int64_t i = 0; i < n; ++i) full_len[assign[i]]++;
+  int64_t* mem_off = (int64_t*)calloc((size_t)nm + 1, sizeof(int64_t));
+  for (int32_t m = 0; m < nm; ++m) {
+    const int64_t len = full_len[marked[m]];
+    int64_t sel = 0;
+    for (int32_t g = 0; g < G; ++g)
+      if ((shard_mask >> (g & 63)) & 1u) sel += (int64_t)(g + 1) * len / G - (int64_t)g * len / G;
+    mem_off[m + 1] = mem_off[m] + sel;
+  }
+  int64_t* mem_ids = (int64_t*)malloc(sizeof(int64_t) * (size_t)(mem_off[nm] > 0 ? mem_off[nm] : 1));
+  int64_t* pos = (int64_t*)calloc((size_t)nl, sizeof(int64_t));
+  int64_t* mcur = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nm > 0 ? nm : 1));
+  for (int32_t m = 0; m < nm; ++m) mcur[m] = mem_off[m];
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t l = assign[i];
+    const int64_t p = pos[l]++;
+    if (mark[l] < 0) continue;
+    const int64_t len = full_len[l];
+    /* stripe of position p: the g with g*len/G <= p < (g+1)*len/G */
+    int32_t g = (int32_t)((p * G) / (len > 0 ? len : 1));
+    while (g + 1 < G && (int64_t)(g + 1) * len / G <= p) ++g;
+    while (g > 0 && (int64_t)g * len / G > p) --g;
+    if ((shard_mask >> (g & 63)) & 1u) mem_ids[mcur[mark[l]]++] = i;
+  }
+  free(mcur);
+  free(pos);
+  free(full_len);
+  free(assign);
+  c.mark = mark;
+  c.marked = marked;
+  c.mem_off = mem_off;
+  c.mem_ids = mem_ids;
+  c.pair_off = pair_off;
+  c.pair_q = pair_q;
+  c.part = (cand*)malloc(sizeof(cand) * (size_t)B * np * k);
+  c.part_cnt = (int32_t*)calloc((size_t)B * np, sizeof(int32_t));
+  parallel_for(nm, 1, synth_scan_range, &c);
+  cand* top = (cand*)malloc(sizeof(cand) * (size_t)k);
+  for (int64_t qi = 0; qi < B; ++qi) {
+    int32_t cnt = 0;
+    for (int32_t pi = 0; pi < np; ++pi) {
+      const int64_t qp = qi * np + pi;
+      for (int32_t i = 0; i < c.part_cnt[qp]; ++i) topk_push(top, &cnt, k, c.part[qp * k + i].dist, c.part[qp * k + i].id);
+    }
+    for (int32_t i = 0; i < k; ++i) {
+      out_ids[qi * k + i] = i < cnt ? top[i].id : -1;
+      out_dists[qi * k + i] = i < cnt ? top[i].dist : INFINITY;
+    }
+  }
+  free(top);
+  free(c.part);
+  free(c.part_cnt);
+  free(mem_ids);
+  free(mem_off);
+  free(pair_q);
+  free(pair_off);
+  free(marked);
+  free(mark);
+  free(lists);
+  free(cen);
+  return RD_OK;
+}
+
+/* ------------------------------------------------------------------ shard groups (rd.h rd_group_*)
+ * Single-process forms only: every stripe is searched in turn and the per-stripe top-k are merged
+ * on the host (rd_merge_topk) — the algebra the engine's NCCL gather + device merge must match. */
+struct rd_group {
+  rd_index** shards;
+  int32_t G;
+};
+
+int rd_group_create(rd_index* const* shards, int32_t G, rd_group** out) {
+  if (!shards || G < 1 || !out) return fail(RD_ERR_INVALID, "group_create: invalid arguments");
+  for (int32_t g = 0; g < G; ++g) {
+    if (!shards[g]) return fail(RD_ERR_INVALID, "group: null stripe %d", g);
+    if (shards[g]->d != shards[0]->d || shards[g]->nlist != shards[0]->nlist)
+      return fail(RD_ERR_INVALID, "group: stripes must share d and nlist");
+    for (int32_t h = 0; h < g; ++h)
+      if (shards[h] == shards[g]) return fail(RD_ERR_INVALID, "group: stripe handle %d given twice", g);
+  }
+  rd_group* grp = (rd_group*)calloc(1, sizeof *grp);
+  grp->shards = (rd_index**)malloc(sizeof(rd_index*) * (size_t)G);
+  memcpy(grp->shards, shards, sizeof(rd_index*) * (size_t)G);
+  grp->G = G;
+  *out = grp;
+  return RD_OK;
+}
+
+int rd_group_create_synthetic(const rd_synth_desc* desc, const int32_t* devices, int32_t G, rd_group** out) {
+  if (!desc || !devices || G < 1 || !out) return fail(RD_ERR_INVALID, "group_create_synthetic: invalid arguments");
+  rd_index** s = (rd_index**)calloc((size_t)G, sizeof(rd_index*));
+  for (int32_t g = 0; g < G; ++g) {
+    rd_synth_desc one = *desc;
+    one.shard = g;
+    one.num_shards = G;
+    int rc = rd_index_create_synthetic(&one, devices[g], &s[g]);
+    if (rc) {
+      for (int32_t h = 0; h < g; ++h) rd_index_destroy(s[h]);
+      free(s);
+      return rc;
+    }
+  }
+  int rc = rd_group_create(s, G, out);
+  if (rc)
+    for (int32_t g = 0; g < G; ++g) rd_index_destroy(s[g]);
+  free(s);
+  return rc;
+}
+
+int rd_group_unique_id(uint8_t* out) {
+  (void)out;
+  return fail(RD_ERR_INVALID, "cpu oracle has no communicator");
+}
+
+int rd_group_create_rank(rd_index* shard, const uint8_t* id, int32_t nranks, int32_t rank, rd_group** out) {
+  (void)shard; (void)id; (void)nranks; (void)rank; (void)out;
+  return fail(RD_ERR_INVALID, "cpu oracle has no communicator");
+}
+
+int rd_group_info_get(const rd_group* g, rd_group_info* o) {
+  if (!g || !o) return fail(RD_ERR_INVALID, "null argument");
+  memset(o, 0, sizeof *o);
+  o->num_shards = g->G;
+  o->local_shards = g->G;
+  o->nranks = 1;
+  o->transport = g->G > 1 ? RD_GROUP_TRANSPORT_COPY : RD_GROUP_TRANSPORT_NONE;
+  for (int32_t i = 0; i < g->G; ++i) {
+    o->n += g->shards[i]->n;
+    for (int32_t l = 0; l < g->shards[i]->nlist; ++l)
+      if (g->shards[i]->resident[l]) o->n_resident += g->shards[i]->offsets[l + 1] - g->shards[i]->offsets[l];
+  }
+  return RD_OK;
+}
+
+rd_index* rd_group_shard(rd_group* g, int32_t i) {
+  if (!g || i < 0 || i >= g->G) return NULL;
+  return g->shards[i];
+}
+
+int rd_group_place(rd_group* g, const rd_placement* p) {
+  if (!g || !p) return fail(RD_ERR_INVALID, "null argument");
+  for (int32_t i = 0; i < g->G; ++i) {
+    int rc = rd_index_place(g->shards[i], p);
+    if (rc) return rc;
+  }
+  return RD_OK;
+}
+
+int rd_group_search(rd_group* g, const float* queries, int64_t B, int32_t nprobe, int32_t k, int64_t* out_ids,
+                    float* out_dists, rd_search_stats* stats) {
+  if (!g || B < 0 || nprobe < 1 || k < 1 || (B > 0 && (!queries || !out_ids || !out_dists)))
+    return fail(RD_ERR_INVALID, "group search: invalid arguments");
+  if (stats) memset(stats, 0, sizeof *stats);
+  if (B == 0) return RD_OK;
+  int64_t* ids = (int64_t*)malloc(sizeof(int64_t) * (size_t)g->G * B * k);
+  float* dists = (float*)malloc(sizeof(float) * (size_t)g->G * B * k);
+  int rc = RD_OK;
+  for (int32_t i = 0; i < g->G && rc == RD_OK; ++i)
+    rc = rd_search(g->shards[i], queries, B, nprobe, k, ids + (size_t)i * B * k, dists + (size_t)i * B * k, NULL);
+  if (rc == RD_OK) rc = rd_merge_topk(g->G, B, k, ids, dists, out_ids, out_dists);
+  free(ids);
+  free(dists);
+  return rc;
+}
+
+int rd_group_search_device(rd_group* g, const float* dq, int64_t B, int32_t nprobe, int32_t k, int64_t* di, float* dd,
+                           void* stream, int32_t sync, rd_search_stats* st) {
+  (void)g; (void)dq; (void)B; (void)nprobe; (void)k; (void)di; (void)dd; (void)stream; (void)sync; (void)st;
+  return fail(RD_ERR_INVALID, "cpu oracle has no device search");
+}
+
+void rd_group_destroy(rd_group* g) {
+  if (!g) return;
+  for (int32_t i = 0; i < g->G; ++i) rd_index_destroy(g->shards[i]);
+  free(g->shards);
+  free(g);
+}

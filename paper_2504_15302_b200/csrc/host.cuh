@@ -331,6 +331,15 @@ struct rd_index {
     HBuf<rd::ScanTile> h_tiles;
   } ws;
 
+  // the search whose stat block copy do_search enqueued last (rdh::finish_stats reads it back)
+  struct Pending {
+    long long B = 0;
+    int k = 0;
+    unsigned long long h2d = 0, launches = 0;
+    bool staged = false, has_off = false;
+    cudaEvent_t e0{}, e1{}, e2{};
+  } pend;
+
   cudaStream_t copy_stream = nullptr, off_stream = nullptr;
   cudaEvent_t ev[8] = {};
   // device-time accounting: 4 events per search (start, plan done, resident scan done, end)
@@ -538,3 +547,17 @@ std::unique_ptr<rd_index> new_index(int device) {
 }
 
 }  // namespace
+
+// One search (search.cu), shared by the single-index entry points and the shard groups (group.cu).
+namespace rdh {
+enum SearchMode { kAsync = 0, kSync = 1, kStatsAsync = 2 };
+void validate_search(const rd_index* h, int nprobe, int k);
+// Enqueues one search of B device queries on stream s. kAsync: nothing is read back; kSync: the
+// counters are copied back and `st` filled before returning; kStatsAsync: the counter copy is
+// enqueued, the caller synchronizes s and then calls finish_stats. result_bytes: bytes after the
+// stat block the counter copy brings along (the host path's results); before_sync runs before it.
+void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, long long* d_ids, float* d_dists,
+               cudaStream_t s, int mode, rd_search_stats* st, size_t result_bytes = 0,
+               const std::function<void()>& before_sync = {});
+void finish_stats(rd_index* h, rd_search_stats* st);
+}  // namespace rdh

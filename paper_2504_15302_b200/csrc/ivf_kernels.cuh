@@ -254,9 +254,14 @@ struct FallbackParams {
 };
 cudaError_t launch_fallback(const FallbackParams& p, int num_sms, cudaStream_t s);
 
-// [G][B][k] shard results -> [B][k] (device)
+// [G][B][k] shard results -> [B][k] (device), any k with G * k <= shard_merge_max_candidates()
 cudaError_t launch_shard_merge(int G, long long B, int k, const long long* ids, const float* dists,
                                long long* out_ids, float* out_dists, cudaStream_t s);
+int shard_merge_max_candidates();
+// the same with shard g's B x k ids at ids + g * ids_stride bytes and distances at dists + g * d_stride
+cudaError_t launch_shard_merge_strided(int G, long long B, int k, const char* ids, size_t ids_stride,
+                                       const char* dists, size_t d_stride, long long* out_ids, float* out_dists,
+                                       cudaStream_t s);
 
 // Index build helpers
 cudaError_t launch_gen_centroids(float* C, int nlist, int d, uint64_t sc, cudaStream_t s);

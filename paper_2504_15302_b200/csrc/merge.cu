@@ -206,6 +206,59 @@ __global__ void shard_merge_kernel(int G, long long B, int k, const long long* _
   }
 }
 
+// Shard merge for any k: one CTA per query sorts its G * k shard candidates by (distance, id) in
+// shared memory (bitonic over the next power of two, padding +inf) and writes the first k. Shard g's
+// ids / distances of query q sit at ids + g * ids_stride (bytes) + q * k, likewise the distances, so
+// both the [G][B][k] arrays of rd_merge_topk_device and the packed per-shard slots of a shard group
+// (group.cu: [ids B x k | dists B x k] per slot) are read in place.
+__global__ void __launch_bounds__(256) shard_merge_sort_kernel(int G, long long B, int k, int P,
+                                                               const char* __restrict__ ids, size_t ids_stride,
+                                                               const char* __restrict__ dists, size_t d_stride,
+                                                               long long* __restrict__ oid, float* __restrict__ od) {
+  RD_PDL_PROLOGUE();
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  long long* sk = reinterpret_cast<long long*>(sm_raw);
+  float* sv = reinterpret_cast<float*>(sk + P);
+  const long long q = blockIdx.x;
+  const int tot = G * k;
+  for (int c = threadIdx.x; c < P; c += blockDim.x) {
+    float v = kInf;
+    long long key = kNoKey;
+    if (c < tot) {
+      const int g = c / k, i = c - g * k;
+      const long long id = reinterpret_cast<const long long*>(ids + (size_t)g * ids_stride)[q * k + i];
+      if (id >= 0) {
+        v = reinterpret_cast<const float*>(dists + (size_t)g * d_stride)[q * k + i];
+        key = id;
+      }
+    }
+    sv[c] = v;
+    sk[c] = key;
+  }
+  __syncthreads();
+  for (int size = 2; size <= P; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int c = threadIdx.x; c < P; c += blockDim.x) {
+        const int o = c ^ stride;
+        if (o > c) {
+          const bool up = (c & size) == 0;
+          const float a = sv[c], b = sv[o];
+          const long long ka = sk[c], kb = sk[o];
+          if (pair_less(b, kb, a, ka) == up) {
+            sv[c] = b, sv[o] = a;
+            sk[c] = kb, sk[o] = ka;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const bool ok = i < P && sk[i] != kNoKey;
+    oid[q * k + i] = ok ? sk[i] : -1;
+    od[q * k + i] = ok ? sv[i] : kInf;
+  }
+}
+
 // Exact fallback in one launch. Persistent: work item w -> (failed query w / nprobe, probe
 // w % nprobe), the exact top-32 of that list; the last CTA to finish merges each failed query's
 // nprobe partials and overwrites its result row, then re-arms the completion counter. With no
@@ -297,11 +350,29 @@ cudaError_t launch_merge(const MergeParams& p, bool stage, cudaStream_t s) {
 cudaError_t launch_shard_merge(int G, long long B, int k, const long long* ids, const float* dists,
                                long long* out_ids, float* out_dists, cudaStream_t s) {
   if (B == 0) return cudaSuccess;
-  if (k > 32) return cudaErrorInvalidValue;
-  const long long threads = B * 32;
-  shard_merge_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(G, B, k, ids, dists, out_ids,
-                                                                       out_dists);
-  return cudaGetLastError();
+  if (k <= 32) {  // one warp per query, merges in registers
+    const long long threads = B * 32;
+    shard_merge_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(G, B, k, ids, dists, out_ids, out_dists);
+    return cudaGetLastError();
+  }
+  return launch_shard_merge_strided(G, B, k, reinterpret_cast<const char*>(ids), (size_t)B * k * sizeof(long long),
+                                    reinterpret_cast<const char*>(dists), (size_t)B * k * sizeof(float), out_ids,
+                                    out_dists, s);
+}
+
+int shard_merge_max_candidates() { return 8192; }
+
+cudaError_t launch_shard_merge_strided(int G, long long B, int k, const char* ids, size_t ids_stride,
+                                       const char* dists, size_t d_stride, long long* out_ids, float* out_dists,
+                                       cudaStream_t s) {
+  if (B == 0) return cudaSuccess;
+  const long long tot = (long long)G * k;
+  if (G < 1 || k < 1 || tot > shard_merge_max_candidates()) return cudaErrorInvalidValue;
+  int P = 1;
+  while (P < tot) P <<= 1;
+  const size_t smem = (size_t)P * (sizeof(long long) + sizeof(float));
+  return launch_k(shard_merge_sort_kernel, dim3((unsigned)B), dim3(256), smem, s, G, B, k, P, ids, ids_stride, dists,
+                  d_stride, out_ids, out_dists);
 }
 
 }  // namespace rd

@@ -10,8 +10,6 @@
 // (cost_model.cpp:15-21), called by the retrieval worker (simulator.cpp:359,560).
 #include "host.cuh"
 
-extern "C" {
-
 // ---------------------------------------------------------------- search
 namespace {
 
@@ -49,13 +47,53 @@ Plan make_plan(const rd_index* h, long long B, int nprobe) {
   return pl;
 }
 
-// result_bytes: bytes after the stat block that the sync copy brings back too (the host path's results)
-void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, long long* d_ids, float* d_dists,
-               cudaStream_t s, bool sync, rd_search_stats* st, size_t result_bytes = 0,
-               const std::function<void()>& before_sync = {}) {
+}  // namespace
+
+namespace rdh {
+
+void validate_search(const rd_index* h, int nprobe, int k) {
   if (nprobe < 1 || k < 1) throw_rd(RD_ERR_INVALID, "search: nprobe >= 1 and k >= 1 required");
   if (k > rd::kMaxK) throw_rd(RD_ERR_INVALID, "search: k <= %d supported, got %d", rd::kMaxK, k);
   if (std::min(nprobe, h->nlist) + rd::kCoarseExtra > 512) throw_rd(RD_ERR_INVALID, "search: nprobe <= 480 supported");
+}
+
+// Counters of the search whose stat block copy do_search enqueued (mode kSync / kStatsAsync), read
+// after its stream synchronized.
+void finish_stats(rd_index* h, rd_search_stats* st) {
+  const auto& pd = h->pend;
+  std::memset(st, 0, sizeof *st);
+  st->kernel_launches = pd.launches;
+  const auto& w = h->ws;
+  const auto* hc = reinterpret_cast<const unsigned long long*>(w.h_blk.p);
+  const auto* hf = reinterpret_cast<const unsigned*>(w.h_blk.p + 24);
+  const auto* hm = reinterpret_cast<const int*>(w.h_blk.p + 32);
+  float ms = 0;
+  const unsigned long long row_bytes = (unsigned long long)h->d * 4;
+  st->lists_probed = hc[0];
+  st->bytes_lists_resident = hc[1] * row_bytes;
+  st->h2d_list_bytes = pd.h2d;
+  st->bytes_algorithmic = (hc[1] + hc[2]) * row_bytes + (unsigned long long)h->nlist * row_bytes +
+                          (unsigned long long)pd.B * row_bytes + (unsigned long long)pd.B * pd.k * 12ull;
+  st->tiles = (uint64_t)hm[0] + (uint64_t)hm[2] + (uint64_t)hm[4];
+  if (pd.staged) {
+    CK(cudaEventElapsedTime(&ms, pd.e1, pd.e2));
+    st->scan_ms = ms;
+    CK(cudaEventElapsedTime(&ms, pd.e0, pd.e1));
+    st->coarse_ms = ms;
+  }
+  if (pd.has_off) {
+    CK(cudaEventElapsedTime(&ms, h->ev[4], h->ev[5]));
+    st->offload_ms = ms;
+  }
+  st->probe_failures = hf[0];
+  st->margin_failures = hf[1];
+}
+
+// result_bytes: bytes after the stat block that the stats copy brings back too (the host path's results)
+void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, long long* d_ids, float* d_dists,
+               cudaStream_t s, int mode, rd_search_stats* st, size_t result_bytes,
+               const std::function<void()>& before_sync) {
+  validate_search(h, nprobe, k);
   CK(cudaSetDevice(h->device));
   auto& w = h->ws;
   const int nl = h->nlist, d = h->d;
@@ -401,44 +439,22 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     fprintf(stderr, "scan: entry %lld/%.0f/%lld ready %lld/%.0f/%lld first %lld/%.0f/%lld end %lld/%.0f/%lld (min/mean/max)\n",
             mn[0], mean[0], mx[0], mn[1], mean[1], mx[1], mn[2], mean[2], mx[2], mn[3], mean[3], mx[3]);
   }
-  if (st) {
+  if (before_sync) before_sync();  // e.g. the host path's result copies, ordered before the one sync
+  if (mode != kAsync) {
+    // counters (and, on the host path, the results placed after them) in one copy
+    CK(cudaMemcpyAsync(w.h_blk.p, w.blk.p, kStatBytes + result_bytes, cudaMemcpyDeviceToHost, s));
+    h->pend = rd_index::Pending{B, k, h2d, launches, staged, has_off, e0, e1, e2};
+    if (mode == kSync) {
+      CK(cudaStreamSynchronize(s));
+      if (st) finish_stats(h, st);
+    }
+  } else if (st) {
     std::memset(st, 0, sizeof *st);
     st->kernel_launches = launches;
   }
-  if (before_sync) before_sync();  // e.g. the host path's result copies, ordered before the one sync
-  if (sync) {
-    // counters (and, on the host path, the results placed after them) in one copy
-    CK(cudaMemcpyAsync(w.h_blk.p, w.blk.p, kStatBytes + result_bytes, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    const auto* hc = reinterpret_cast<const unsigned long long*>(w.h_blk.p);
-    const auto* hf = reinterpret_cast<const unsigned*>(w.h_blk.p + 24);
-    const auto* hm = reinterpret_cast<const int*>(w.h_blk.p + 32);
-    if (st) {
-      float ms = 0;
-      const unsigned long long row_bytes = (unsigned long long)d * 4;
-      st->lists_probed = hc[0];
-      st->bytes_lists_resident = hc[1] * row_bytes;
-      st->h2d_list_bytes = h2d;
-      st->bytes_algorithmic = (hc[1] + hc[2]) * row_bytes + (unsigned long long)nl * row_bytes +
-                              (unsigned long long)B * row_bytes + (unsigned long long)B * k * 12ull;
-      st->tiles = (uint64_t)hm[0] + (uint64_t)hm[2] + (uint64_t)hm[4];
-      if (staged) {
-        CK(cudaEventElapsedTime(&ms, e1, e2));
-        st->scan_ms = ms;
-        CK(cudaEventElapsedTime(&ms, e0, e1));
-        st->coarse_ms = ms;
-      }
-      if (has_off) {
-        CK(cudaEventElapsedTime(&ms, e_plan, e_off));
-        st->offload_ms = ms;
-      }
-      st->probe_failures = hf[0];
-      st->margin_failures = hf[1];
-    }
-  }
 }
 
-}  // namespace
+}  // namespace rdh
 
 namespace {
 // Largest batch searched in one pass: bounds the B x nlist coarse-distance workspace (2 GiB).
@@ -460,6 +476,8 @@ void add_stats(rd_search_stats* acc, const rd_search_stats& s) {  // counters su
 }
 }  // namespace
 
+extern "C" {
+
 int rd_search_device(rd_index* h, const float* d_q, int64_t B, int32_t nprobe, int32_t k, int64_t* d_ids,
                      float* d_dists, void* stream, int32_t sync, rd_search_stats* st) {
   return guarded([&] {
@@ -471,8 +489,8 @@ int rd_search_device(rd_index* h, const float* d_q, int64_t B, int32_t nprobe, i
     for (long long b0 = 0; b0 < B; b0 += chunk) {  // very large batches run as consecutive passes
       const long long nb = std::min<long long>(chunk, B - b0);
       rd_search_stats part{};
-      do_search(h, d_q + (size_t)b0 * h->d, nb, nprobe, k, reinterpret_cast<long long*>(d_ids) + (size_t)b0 * k,
-                d_dists + (size_t)b0 * k, (cudaStream_t)stream, sync != 0, st ? &part : nullptr);
+      rdh::do_search(h, d_q + (size_t)b0 * h->d, nb, nprobe, k, reinterpret_cast<long long*>(d_ids) + (size_t)b0 * k,
+                d_dists + (size_t)b0 * k, (cudaStream_t)stream, sync != 0 ? rdh::kSync : rdh::kAsync, st ? &part : nullptr);
       if (st) add_stats(st, part);
     }
     if (st) st->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -521,7 +539,7 @@ int rd_search(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int3
     w.ensure_blk(kStatBytes + res_bytes);
     long long* d_ids = reinterpret_cast<long long*>(w.blk.p + kStatBytes);
     float* d_dists = reinterpret_cast<float*>(w.blk.p + kStatBytes + rn * sizeof(long long));
-    do_search(h, w.q.p, B, nprobe, k, d_ids, d_dists, s, true, st, direct ? 0 : res_bytes, [&] {
+    rdh::do_search(h, w.q.p, B, nprobe, k, d_ids, d_dists, s, rdh::kSync, st, direct ? 0 : res_bytes, [&] {
       if (!direct) return;
       CK(cudaMemcpyAsync(out_ids, d_ids, rn * sizeof(long long), cudaMemcpyDeviceToHost, s));
       CK(cudaMemcpyAsync(out_dists, d_dists, rn * sizeof(float), cudaMemcpyDeviceToHost, s));
@@ -623,7 +641,8 @@ int rd_merge_topk(int32_t G, int64_t B, int32_t k, const int64_t* sid, const flo
 int rd_merge_topk_device(int32_t G, int64_t B, int32_t k, const int64_t* ids, const float* dists, int64_t* oid,
                          float* od, void* stream) {
   return guarded([&] {
-    if (G < 1 || B < 0 || k < 1 || k > 32) throw_rd(RD_ERR_INVALID, "merge_device: invalid arguments (k <= 32)");
+    if (G < 1 || B < 0 || k < 1 || (long long)G * k > rd::shard_merge_max_candidates())
+      throw_rd(RD_ERR_INVALID, "merge_device: invalid arguments (G * k <= %d)", rd::shard_merge_max_candidates());
     CK(rd::launch_shard_merge(G, B, k, reinterpret_cast<const long long*>(ids), dists,
                               reinterpret_cast<long long*>(oid), od, (cudaStream_t)stream));
   });

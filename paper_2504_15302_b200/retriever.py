@@ -84,6 +84,15 @@ class Timing(C.Structure):
                 ("tail_ms", C.c_double), ("total_ms", C.c_double), ("stage_searches", C.c_int64)]
 
 
+class GroupInfo(C.Structure):
+    _fields_ = [("num_shards", C.c_int32), ("local_shards", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32),
+                ("transport", C.c_int32), ("root_device", C.c_int32), ("n", C.c_int64), ("n_resident", C.c_int64)]
+
+
+GROUP_TRANSPORTS = {0: "none", 1: "nccl", 2: "copy"}
+GROUP_ID_BYTES = 128
+
+
 class LlmReservation(C.Structure):
     _fields_ = [("weight_total", C.c_uint64), ("kv_bytes_per_request", C.c_uint64),
                 ("workspace_bytes_per_request", C.c_uint64), ("w_gpu", C.c_double), ("c_gpu", C.c_double),
@@ -122,6 +131,17 @@ _SIGS = {
     "rd_timing_stages": (C.c_int, [_P, C.c_int32]),
     "rd_timing_reset": (C.c_int, [_P]),
     "rd_timing_read": (C.c_int, [_P, C.POINTER(Timing)]),
+    "rd_group_create": (C.c_int, [C.POINTER(_P), C.c_int32, C.POINTER(_P)]),
+    "rd_group_create_synthetic": (C.c_int, [C.POINTER(SynthDesc), _I32P, C.c_int32, C.POINTER(_P)]),
+    "rd_group_unique_id": (C.c_int, [C.c_char_p]),
+    "rd_group_create_rank": (C.c_int, [_P, C.c_char_p, C.c_int32, C.c_int32, C.POINTER(_P)]),
+    "rd_group_info_get": (C.c_int, [_P, C.POINTER(GroupInfo)]),
+    "rd_group_shard": (_P, [_P, C.c_int32]),
+    "rd_group_place": (C.c_int, [_P, C.POINTER(Placement)]),
+    "rd_group_search": (C.c_int, [_P, _FP, C.c_int64, C.c_int32, C.c_int32, _I64P, _FP, C.POINTER(SearchStats)]),
+    "rd_group_search_device": (C.c_int, [_P, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_int32, C.POINTER(SearchStats)]),
+    "rd_group_destroy": (None, [_P]),
     "rd_derive_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "rd_splitmix_at": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "rd_synth_queries": (C.c_int, [C.POINTER(SynthDesc), C.c_int64, C.c_int64, C.c_float, _FP, _I64P]),
@@ -232,6 +252,39 @@ class Library:
         self.check(self.lib.rd_index_load(os.fsencode(path), device, C.byref(h)), "load")
         return Index(self, h)
 
+    # -- multi-GPU shard groups (rd_group_*)
+    def group(self, shards) -> "Group":
+        """A group over existing stripe handles (one process, any devices); the group takes them over."""
+        shards = list(shards)
+        arr = (_P * len(shards))(*[sh.handle for sh in shards])
+        h = C.c_void_p()
+        self.check(self.lib.rd_group_create(arr, len(shards), C.byref(h)), "group_create")
+        for sh in shards:  # owned by the group now
+            sh._h = None
+        return Group(self, h)
+
+    def synthetic_group(self, desc: SynthDesc, devices) -> "Group":
+        """Stripe g of desc's knowledge base on devices[g] (one process driving every device)."""
+        devs = np.ascontiguousarray(np.asarray(devices, dtype=np.int32).reshape(-1))
+        h = C.c_void_p()
+        self.check(self.lib.rd_group_create_synthetic(C.byref(desc), devs.ctypes.data_as(_I32P), devs.size,
+                                                      C.byref(h)), "group_create_synthetic")
+        return Group(self, h)
+
+    def group_unique_id(self) -> bytes:
+        buf = C.create_string_buffer(GROUP_ID_BYTES)
+        self.check(self.lib.rd_group_unique_id(buf), "group_unique_id")
+        return buf.raw
+
+    def rank_group(self, shard: "Index", uid: bytes, nranks: int, rank: int) -> "Group":
+        """This process's stripe as rank `rank` of `nranks` (one process per device); collective."""
+        if len(uid) != GROUP_ID_BYTES:
+            raise ParseError(f"group id must be {GROUP_ID_BYTES} bytes")
+        h = C.c_void_p()
+        self.check(self.lib.rd_group_create_rank(shard.handle, uid, nranks, rank, C.byref(h)), "group_create_rank")
+        shard._h = None
+        return Group(self, h)
+
     # -- merges and arithmetic
     def merge_topk(self, shard_ids: np.ndarray, shard_dists: np.ndarray):
         shard_ids = np.ascontiguousarray(shard_ids, dtype=np.int64)
@@ -256,6 +309,27 @@ class Library:
         return int(self.lib.rd_staging_depth(free_bytes, item_bytes))
 
 
+def _check_queries(queries: np.ndarray, d: int) -> np.ndarray:
+    q = np.ascontiguousarray(queries, dtype=np.float32)
+    if q.ndim != 2 or q.shape[1] != d:
+        raise ParseError(f"queries must be (B, {d}), got {tuple(np.shape(queries))}")
+    return q
+
+
+def _check_into(queries, d: int, k: int, out_ids, out_dists) -> None:
+    """search_into hands raw pointers to the library: shapes, dtypes and layout must be exact."""
+    for name, a, dt in (("queries", queries, np.float32), ("out_ids", out_ids, np.int64),
+                        ("out_dists", out_dists, np.float32)):
+        if not isinstance(a, np.ndarray) or a.dtype != dt or not a.flags.c_contiguous or a.ndim != 2:
+            raise ParseError(f"{name} must be a C-contiguous 2-D {np.dtype(dt).name} array")
+    if queries.shape[1] != d:
+        raise ParseError(f"queries must be (B, {d}), got {queries.shape}")
+    if out_ids.shape != (queries.shape[0], k) or out_dists.shape != (queries.shape[0], k):
+        raise ParseError(f"out_ids / out_dists must be ({queries.shape[0]}, {k})")
+    if not out_ids.flags.writeable or not out_dists.flags.writeable:
+        raise ParseError("output buffers must be writeable")
+
+
 @dataclass
 class SearchResult:
     ids: np.ndarray
@@ -271,9 +345,9 @@ class Index:
         self._h = handle
 
     def close(self) -> None:
-        if self._h:
+        if self._h and not getattr(self, "_borrowed", False):  # a group's stripe is freed by the group
             self._lib.lib.rd_index_destroy(self._h)
-            self._h = None
+        self._h = None
 
     def __del__(self):
         try:
@@ -320,8 +394,13 @@ class Index:
             p.list_heat = hh.ctypes.data_as(C.POINTER(C.c_uint32))
         self._lib.check(self._lib.lib.rd_index_place(self._h, C.byref(p)), "place")
 
+    def _dim(self) -> int:
+        if getattr(self, "_d", None) is None:
+            self._d = self.info()["d"]
+        return self._d
+
     def search(self, queries: np.ndarray, nprobe: int, k: int) -> SearchResult:
-        q = np.ascontiguousarray(queries, dtype=np.float32)
+        q = _check_queries(queries, self._dim())
         B = q.shape[0]
         ids = np.empty((B, k), dtype=np.int64)
         dists = np.empty((B, k), dtype=np.float32)
@@ -333,6 +412,7 @@ class Index:
     def search_into(self, queries: np.ndarray, nprobe: int, k: int, out_ids: np.ndarray,
                     out_dists: np.ndarray) -> dict:
         """rd_search into caller-owned host buffers (page-locked buffers are copied directly)."""
+        _check_into(queries, self._dim(), k, out_ids, out_dists)
         st = SearchStats()
         self._lib.check(self._lib.lib.rd_search(self._h, _fp(queries), queries.shape[0], nprobe, k, _i64p(out_ids),
                                                 _fp(out_dists), C.byref(st)), "search")
@@ -386,6 +466,90 @@ class Index:
         self._lib.check(self._lib.lib.rd_probe(self._h, _fp(q), q.shape[0], nprobe,
                                                out.ctypes.data_as(_I32P)), "probe")
         return out
+
+
+class Group:
+    """A shard group (rd_group_*): G row stripes searched together, one merged top-k per call."""
+
+    def __init__(self, lib: Library, handle: C.c_void_p):
+        self._lib = lib
+        self._h = handle
+
+    def close(self) -> None:
+        if self._h:
+            self._lib.lib.rd_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def info(self) -> dict:
+        o = GroupInfo()
+        self._lib.check(self._lib.lib.rd_group_info_get(self._h, C.byref(o)), "group_info")
+        d = {f: getattr(o, f) for f, _ in o._fields_}
+        d["transport"] = GROUP_TRANSPORTS.get(d["transport"], str(d["transport"]))
+        return d
+
+    def shard(self, i: int) -> "Index":
+        """Borrowed view of the i-th local stripe (do not close it; the group owns it)."""
+        h = self._lib.lib.rd_group_shard(self._h, i)
+        if not h:
+            raise ParseError(f"no local stripe {i}")
+        ix = Index(self._lib, C.c_void_p(h))
+        ix._borrowed = True
+        return ix
+
+    def place(self, **kw) -> None:
+        p = Placement(kw.get("hbm_budget_bytes", 0), kw.get("offload_fraction", 0.0), None, None,
+                      kw.get("staging_slots", 0), 0)
+        keep = []
+        if kw.get("list_heat") is not None:
+            hh = np.ascontiguousarray(kw["list_heat"], dtype=np.uint32)
+            keep.append(hh)
+            p.list_heat = hh.ctypes.data_as(C.POINTER(C.c_uint32))
+        if kw.get("resident_mask") is not None:
+            m = np.ascontiguousarray(kw["resident_mask"], dtype=np.uint8)
+            keep.append(m)
+            p.resident_mask = m.ctypes.data_as(C.POINTER(C.c_uint8))
+        self._lib.check(self._lib.lib.rd_group_place(self._h, C.byref(p)), "group_place")
+
+    def search(self, queries: np.ndarray, nprobe: int, k: int) -> SearchResult:
+        q = np.ascontiguousarray(queries, dtype=np.float32)
+        if q.ndim != 2:
+            raise ParseError("queries must be 2-D")
+        B = q.shape[0]
+        ids = np.empty((B, k), dtype=np.int64)
+        dists = np.empty((B, k), dtype=np.float32)
+        st = SearchStats()
+        self._lib.check(self._lib.lib.rd_group_search(self._h, _fp(q), B, nprobe, k, _i64p(ids), _fp(dists),
+                                                      C.byref(st)), "group_search")
+        return SearchResult(ids, dists, st.as_dict())
+
+    def search_into(self, queries: np.ndarray, nprobe: int, k: int, out_ids: np.ndarray,
+                    out_dists: np.ndarray) -> dict:
+        _check_into(queries, queries.shape[1] if getattr(queries, "ndim", 0) == 2 else -1, k, out_ids, out_dists)
+        st = SearchStats()
+        self._lib.check(self._lib.lib.rd_group_search(self._h, _fp(queries), queries.shape[0], nprobe, k,
+                                                      _i64p(out_ids), _fp(out_dists), C.byref(st)), "group_search")
+        return st.as_dict()
+
+    def search_device(self, q_ptr: int, B: int, nprobe: int, k: int, ids_ptr: int, dists_ptr: int,
+                      stream: int = 0, sync: bool = False) -> dict:
+        st = SearchStats()
+        self._lib.check(self._lib.lib.rd_group_search_device(self._h, C.c_void_p(q_ptr), B, nprobe, k,
+                                                             C.c_void_p(ids_ptr), C.c_void_p(dists_ptr),
+                                                             C.c_void_p(stream), 1 if sync else 0, C.byref(st)),
+                        "group_search_device")
+        return st.as_dict()
 
 
 _ENGINE: Optional[Library] = None

@@ -79,3 +79,19 @@ def test_invalid_arguments_raise_parse_error(oracle):
     idx = oracle.synthetic_index(oracle.desc(100, 8, 4))
     with pytest.raises(ParseError):
         idx.search(np.zeros((1, 8), np.float32), nprobe=0, k=1)
+
+
+@pytest.mark.parametrize("G,mask", [(1, 1), (4, 0b0101), (8, 0b11), (3, 0b111)])
+def test_sampled_synth_search_matches_materialised_stripes(oracle, G, mask):
+    # rd_oracle_synth_search (vectors regenerated from (seed, id), nothing materialised) equals the
+    # merge of the materialised oracle stripes it selects
+    from oracle_ext import synth_search
+    n, d, nlist, nprobe, k = 30000, 64, 40, 6, 12
+    desc = oracle.desc(n, d, nlist, num_shards=G)
+    q, _ = oracle.synth_queries(desc, 11, 9)
+    got_i, got_d = synth_search(oracle, desc, q, nprobe, k, mask)
+    parts = [oracle.synthetic_index(oracle.desc(n, d, nlist, shard=g, num_shards=G)).search(q, nprobe, k)
+             for g in range(G) if (mask >> g) & 1]
+    want_i, want_d = oracle.merge_topk(np.stack([p.ids for p in parts]), np.stack([p.dists for p in parts]))
+    np.testing.assert_array_equal(got_i, want_i)
+    np.testing.assert_array_equal(got_d, want_d)

@@ -75,3 +75,21 @@ def test_placement_rule(oracle):
     big.place(hbm_budget_bytes=int(blens[:3].sum() * 32 * 4) + ring)
     bmask = big.layout(with_ids=False)[2]
     assert bmask[:3].all() and not bmask[3:].any()
+
+
+@pytest.mark.parametrize("G", [1, 2, 3])
+def test_oracle_group_equals_unsharded(oracle, G):
+    # rd_group_* algebra on the CPU: stripes searched in turn and merged equal the unsharded search
+    n, d, nlist, B, nprobe, k = 8000, 64, 20, 11, 4, 10
+    desc = oracle.desc(n, d, nlist)
+    q, _ = oracle.synth_queries(desc, 2, B)
+    grp = oracle.synthetic_group(desc, [0] * G)
+    assert grp.info()["num_shards"] == G and grp.info()["n"] == n
+    e = grp.search(q, nprobe, k)
+    o = oracle.synthetic_index(desc).search(q, nprobe, k)
+    np.testing.assert_array_equal(e.ids, o.ids)
+    np.testing.assert_array_equal(e.dists, o.dists)
+    from paper_2504_15302_b200.retriever import ParseError
+    with pytest.raises(ParseError):  # no communicator in the CPU oracle
+        oracle.group_unique_id()
+    grp.close()
