@@ -514,8 +514,10 @@ __global__ void __launch_bounds__(NT) coarse_select_kernel(const SelectParams p)
     }
   }
 
-  const float u = 5.9604645e-8f;
-  const float eps = 2.f * ((d + 4) * u * 2.f * sqrtf(qn) * p.cmax + 8.f * u * (qn + p.cmax * p.cmax)) + 1e-30f;
+  const float u = kUnit;
+  // |approx - exact| of a coarse distance: the GEMM's dot bound (doubled: d = ... - 2 q.c) plus the
+  // norms' and the epilogue's roundings
+  const float eps = 2.f * p.gamma_coarse * sqrtf(qn) * p.cmax + 16.f * u * (qn + p.cmax * p.cmax) + 1e-30f;
   bool done = false;
 
   // ------------------------------------------------------------ search mode: the probe set
@@ -758,8 +760,7 @@ __global__ void __launch_bounds__(NT) coarse_select_kernel(const SelectParams p)
         float mx = red[0];
         for (int i = 1; i < NT / 32; ++i) mx = fmaxf(mx, red[i]);
         if (pre) mx = seed_pre;
-        const float eps_s =
-            2.f * ((d / 2 + 8) * u * 2.f * sqrtf(qn) * p.xmax + 8.f * u * (qn + p.xmax * p.xmax)) + 1e-30f;
+        const float eps_s = 2.f * p.gamma_scan * sqrtf(qn) * p.xmax + 16.f * u * (qn + p.xmax * p.xmax) + 1e-30f;
         const float thr = mx * (1.f + 2.f * l2_f32_rel_bound(d)) + 2.f * eps_s;
         p.qthr[b] = f2ord(thr);
       }

@@ -249,6 +249,11 @@ struct rd_index {
   // d % 64 == 0 and d <= 896 (beyond, its B operand does not fit next to the x ring); else FFMA
   // the converter variant (offloaded lists, or no pre-split copy) must fit: its operand is resident
   bool tc_scan() const { return d % 64 == 0 && rd::scan_tc_smem_bytes(d, 32, false) <= 227 * 1024; }
+  // dot-product error bound of the scans whose candidates the merge certifies (ivf_kernels.cuh): the
+  // tensor-core and FFMA scans may both run in one search (offloaded or sparse lists)
+  float scan_gamma() const {
+    return tc_scan() ? std::max(rd::gamma_bf16x3(d), rd::gamma_ffma_scan(d)) : rd::gamma_ffma_scan(d);
+  }
   // Tensor-core tile width for a batch: 16-query tiles (the 16-wide scan's deeper ring) when the
   // probed lists see <= 8 queries on average, else 32-query tiles (lists read once). Measured: mixing
   // both widths in one batch (RD_TC_G=1: lists of <= 16 queries narrow, others wide) does not beat

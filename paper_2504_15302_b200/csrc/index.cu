@@ -239,6 +239,7 @@ int rd_index_build(int64_t n, int32_t d, int32_t nlist, const float* vectors, co
         }
         rd::SelectParams sp{w.Dc.p, q, w.qnorm.p, h->centroids.p, assign.p + b0, w.fails(), B, nlist, 1, d,
                             h->cmax, nullptr, nullptr, nullptr, 0.f, nullptr, 0};
+        sp.gamma_coarse = d % 64 == 0 ? rd::gamma_bf16x3(d) : rd::gamma_ffma_coarse(d);
         CK(rd::launch_select(sp, false, s, h->num_sms));
       }
     };

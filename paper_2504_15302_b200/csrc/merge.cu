@@ -165,10 +165,8 @@ __global__ void __launch_bounds__(256, kStage ? 1 : 8) merge_rerank_kernel(const
       const float tau = tau_s;
       if (tau != kInf) {
         const float qn = p.qnorm[b];
-        const float u = 5.9604645e-8f;
         const float xm = p.xmax;
-        const float eps =
-            2.f * ((p.d / 2 + 8) * u * 2.f * sqrtf(qn) * xm + 8.f * u * (qn + xm * xm)) + 1e-30f;
+        const float eps = 2.f * p.gamma * sqrtf(qn) * xm + 16.f * kUnit * (qn + xm * xm) + 1e-30f;
         if (!(tau - eps > ek)) p.fail_list[atomicAdd(p.margin_fail, 1u)] = b;
       }
     }

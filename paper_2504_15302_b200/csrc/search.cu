@@ -51,6 +51,11 @@ Plan make_plan(const rd_index* h, long long B, int nprobe) {
 
 namespace rdh {
 
+// the coarse path a batch of B queries takes (do_search, rd_probe) and its dot-product bound
+float coarse_gamma(long long B, int d) {
+  return !rd::coarse_small((int)B) && d % 64 == 0 ? rd::gamma_bf16x3(d) : rd::gamma_ffma_coarse(d);
+}
+
 void validate_search(const rd_index* h, int nprobe, int k) {
   if (nprobe < 1 || k < 1) throw_rd(RD_ERR_INVALID, "search: nprobe >= 1 and k >= 1 required");
   if (k > rd::kMaxK) throw_rd(RD_ERR_INVALID, "search: k <= %d supported, got %d", rd::kMaxK, k);
@@ -144,6 +149,8 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   if (!seed) CK(cudaMemsetAsync(w.qthr.p, 0x7f, sizeof(int) * B, s));  // no threshold: huge
   rd::SelectParams sp{w.Dc.p, d_q, w.qnorm.p, h->centroids.p, w.probes.p, w.fails(), (int)B, nl, nprobe, d, h->cmax,
                       h->d_list_off.p, h->d_res_row0.p, h->arena.p, h->xmax, seed ? w.qthr.p : nullptr, 0};
+  sp.gamma_coarse = coarse_gamma(B, d);
+  sp.gamma_scan = h->scan_gamma();
   unsigned long long* chain = nullptr;  // profiling only (RD_DEBUG_CHAIN): [select 32][plan 32][merge 32][scan 4/CTA]
   if (h->dbg_chain) {
     const size_t n = 96 + 4 * (size_t)h->num_sms;
@@ -403,6 +410,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
                      h->arena.p + (size_t)h->n_resident * d, nl, d, k, h->xmax, d_ids, d_dists,
                      w.fails() + 1, w.fail_list.p, (int)B};
   mp.m_rerank = m_rerank;
+  mp.gamma = h->scan_gamma();
   if (chain) mp.dbg = chain + 64;
   h->traced("merge", s, mp.dbg, [&] { CK(rd::launch_merge(mp, h->stage_rows(B), s)); });
   rd::FallbackParams fp{w.fail_list.p, w.fails() + 1, w.probes.p, nprobe, d_q, h->d_list_off.p, h->d_list_base.p,
@@ -582,6 +590,7 @@ int rd_probe(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32
     }
     rd::SelectParams sp{w.Dc.p, w.q.p, w.qnorm.p, h->centroids.p, w.probes.p, w.fails(), (int)B, nl, nprobe, d, h->cmax,
                         h->d_list_off.p, h->d_res_row0.p, h->arena.p, h->xmax, nullptr, 1};
+    sp.gamma_coarse = rdh::coarse_gamma(B, d);
     CK(rd::launch_select(sp, h->stage_rows(B), 0, h->num_sms));
     CK(cudaMemcpy(out_lists, w.probes.p, sizeof(int) * B * nprobe, cudaMemcpyDeviceToHost));
   });

@@ -34,6 +34,8 @@ def oracle():
 def engine_lib():
     """The engine .so loaded for its host-side entry points (no GPU needed)."""
     from paper_2504_15302_b200.retriever import ENGINE_PATH, Library
+    if os.environ.get("RD_ENGINE_PATH"):  # A/B against another build of the engine
+        return Library(os.environ["RD_ENGINE_PATH"])
     if not os.path.exists(ENGINE_PATH):
         subprocess.check_call(["make", "-C", ROOT, os.path.relpath(ENGINE_PATH, ROOT)])
     return Library(ENGINE_PATH)

@@ -314,3 +314,100 @@ extern "C" int tc_gather4(const float* hX, int R, int Ccols, int c0, const int* 
   cudaFree(O);
   return (int)e;
 }
+
+// kind::f16 (bf16 inputs, fp32 accumulate) accumulation probe: D[128 x 32] = C + A . B^T over
+// K (K % 64 == 0, K <= 512), issued as K / 16 SS MMAs into ONE accumulator, exactly the way the
+// scan and the coarse GEMM chain their K steps. A / B are bf16 bit patterns, row-major; C is the
+// initial accumulator (stored to TMEM with tcgen05.st; has_c = 0 starts from the first product).
+// The test uses it to measure the accumulator's rounding error on adversarial operands.
+__global__ void __launch_bounds__(128, 1) tc_bf16_acc_kernel(const uint16_t* A, const uint16_t* B, const float* C,
+                                                             int has_c, int K, float* D) {
+  extern __shared__ unsigned char dyn[];
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(dyn) + 1023) & ~uintptr_t(1023));
+  unsigned char* sa = base;                       // [K/64][128 rows x 128 B]
+  unsigned char* sb = base + (K / 64) * 128 * 128;  // [K/64][32 rows x 128 B]
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  // 16 B chunks (8 bf16): element k of row r -> slab k / 64, chunk (k % 64) / 8 swizzled by r % 8
+  for (int i = tid; i < 128 * K / 8; i += 128) {
+    const int r = i / (K / 8), k = (i % (K / 8)) * 8, ks = k >> 6, g = (k & 63) >> 3;
+    *reinterpret_cast<uint4*>(sa + ks * 128 * 128 + r * 128 + ((g ^ (r & 7)) << 4)) =
+        reinterpret_cast<const uint4*>(A)[i];
+  }
+  for (int i = tid; i < 32 * K / 8; i += 128) {
+    const int r = i / (K / 8), k = (i % (K / 8)) * 8, ks = k >> 6, g = (k & 63) >> 3;
+    *reinterpret_cast<uint4*>(sb + ks * 32 * 128 + r * 128 + ((g ^ (r & 7)) << 4)) =
+        reinterpret_cast<const uint4*>(B)[i];
+  }
+  fence_proxy_async();
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(&tbase, 32);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tbase;
+  const uint32_t ta = tm + ((uint32_t)(warp * 32) << 16);
+  if (has_c) {
+    uint32_t v[16];
+    for (int h = 0; h < 2; ++h) {
+      for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(C[tid * 32 + h * 16 + j]);
+      tmem_st16(ta + h * 16, v);
+    }
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (tid == 0) {
+    const uint32_t id = idesc_bf16(128, 32);
+    for (int ks = 0; ks < K / 64; ++ks) {
+      const uint64_t ad = umma_desc_sw128(sa + ks * 128 * 128), bd = umma_desc_sw128(sb + ks * 32 * 128);
+      for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(tm, ad + kk * 2, bd + kk * 2, id, (has_c | ks | kk) != 0);
+    }
+    tc_commit(&bar);
+  }
+  __syncwarp();
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  uint32_t r0[16], r1[16];
+  RD_TMEM_LD16(ta, r0);
+  RD_TMEM_LD16(ta + 16, r1);
+  tmem_ld_wait();
+  for (int j = 0; j < 16; ++j) {
+    D[tid * 32 + j] = __uint_as_float(r0[j]);
+    D[tid * 32 + 16 + j] = __uint_as_float(r1[j]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tm, 32);
+  }
+}
+
+extern "C" int tc_bf16_acc(const uint16_t* hA, const uint16_t* hB, const float* hC, int has_c, int K, float* hD) {
+  if (K % 64 != 0 || K <= 0 || K > 512) return -1;
+  uint16_t *A, *B;
+  float *C, *D;
+  cudaMalloc(&A, 128 * K * 2);
+  cudaMalloc(&B, 32 * K * 2);
+  cudaMalloc(&C, 128 * 32 * 4);
+  cudaMalloc(&D, 128 * 32 * 4);
+  cudaMemcpy(A, hA, 128 * K * 2, cudaMemcpyHostToDevice);
+  cudaMemcpy(B, hB, 32 * K * 2, cudaMemcpyHostToDevice);
+  if (has_c) cudaMemcpy(C, hC, 128 * 32 * 4, cudaMemcpyHostToDevice);
+  const int smem = 1024 + (K / 64) * (128 + 32) * 128;
+  cudaFuncSetAttribute(tc_bf16_acc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  tc_bf16_acc_kernel<<<1, 128, smem>>>(A, B, C, has_c, K, D);
+  cudaError_t e = cudaDeviceSynchronize();
+  cudaMemcpy(hD, D, 128 * 32 * 4, cudaMemcpyDeviceToHost);
+  cudaFree(A);
+  cudaFree(B);
+  cudaFree(C);
+  cudaFree(D);
+  return (int)e;
+}

@@ -66,3 +66,99 @@ def test_three_tf32_split_is_fp32_accurate(engine):
     exact = x.astype(np.float64) @ q.T.astype(np.float64)
     scale = np.abs(x).astype(np.float64) @ np.abs(q).T.astype(np.float64)
     assert (np.abs(dot - exact) / scale).max() < 4e-6
+
+
+# ---- kind::f16 (bf16 x bf16 -> fp32) accumulator: the error model the certification bound uses ----
+# (paper_2504_15302_b200/csrc/ivf_kernels.cuh gamma_bf16x3; DESIGN.md §2 "Certification")
+U = 2.0 ** -24
+
+
+def test_bf16_accumulator_alignment_window(engine):
+    """Within one K = 16 MMA step every term is aligned to the largest one and kept to 2^-25 of
+    it: products of 2^-25 next to a 1 survive (their sum is then rounded), 2^-26 are dropped."""
+    from tc_acc import run_acc
+    for j, want in ((25, lambda n: (n // 4) * 4), (26, lambda n: 0)):
+        A = np.zeros((128, 64), np.float32)
+        B = np.zeros((32, 64), np.float32)
+        A[:, 0], B[:, 0] = 1.0, 1.0
+        A[:, 1:16] = 2.0 ** -j
+        for c in range(16):
+            B[c, 1:1 + c] = 1.0  # column c: c tiny products beside the 1
+        D = run_acc(A, B)
+        got = [int(round((D[0, c] - 1.0) / 2.0 ** -25)) for c in range(16)]
+        assert got == [want(n) * (1 if j == 25 else 0) for n in range(16)], (j, got)
+
+
+def test_bf16_accumulator_rounds_toward_zero(engine):
+    from tc_acc import run_acc
+    ulp = 2.0 ** -23
+    for frac, want in ((0.75, 0.0), (1.5, 1.0), (-0.25, -0.5), (-0.75, -1.0)):
+        A = np.zeros((128, 64), np.float32)
+        B = np.zeros((32, 64), np.float32)
+        A[:, 0], B[:, 0] = frac * ulp, 1.0
+        D = run_acc(A, B, np.ones((128, 32), np.float32))
+        assert (D[0, 0] - 1.0) / ulp == want, (frac, D[0, 0])
+
+
+def _families(rng, K):
+    yield "one_big", 2.0 ** rng.uniform(-25, -22, (128, K)), 1 + rng.random((32, K)) * 0.99, 0
+    yield "loguniform", 2.0 ** rng.uniform(-30, 0, (128, K)), 2.0 ** rng.uniform(-30, 0, (32, K)), 0
+    yield "mixed_sign", 2.0 ** rng.uniform(-26, 0, (128, K)), 1 + rng.random((32, K)), 1
+    yield "uniform", rng.random((128, K)) + 0.5, rng.random((32, K)) + 0.5, 0
+
+
+@pytest.mark.parametrize("K", [64, 512])
+def test_bf16_accumulator_error_within_model(engine, K):
+    """Adversarial operands (one dominant product then products just below its 2^-25 window,
+    log-uniform magnitudes, mixed signs): the error stays within 10 u of each step's magnitude
+    (|accumulator| + sum |products|), summed over the K / 16 steps — the model gamma_bf16x3 takes
+    as 11 u per step."""
+    from tc_acc import bf16_val, run_acc
+    rng = np.random.default_rng(K)
+    for t in range(6):
+        for name, A, B, signs in _families(rng, K):
+            if name == "one_big":
+                A[:, rng.integers(0, K)] = 1.0
+            if signs:
+                A = A * rng.choice([-1.0, 1.0], A.shape)
+            A, B = bf16_val(A.astype(np.float32)), bf16_val(B.astype(np.float32))
+            D = run_acc(A, B).astype(np.float64)
+            P = A.astype(np.float64)[:, None, :] * B.astype(np.float64)[None, :, :]  # 128 x 32 x K
+            steps = P.reshape(128, 32, K // 16, 16)
+            partial = np.cumsum(steps.sum(3), axis=2)  # exact running sums after each step
+            acc_before = np.concatenate([np.zeros((128, 32, 1)), partial[:, :, :-1]], axis=2)
+            step_mag = np.abs(acc_before) + np.abs(steps).sum(3)
+            model = 10 * U * step_mag.sum(2)
+            err = np.abs(D - partial[:, :, -1])
+            assert (err <= model * 1.0001 + 1e-45).all(), (name, (err / model).max())
+            assert (err <= 11 * U * (K // 16) * np.abs(P).sum(2) * 1.0001 + 1e-45).all(), name
+
+
+@pytest.mark.parametrize("d", [64, 512])
+def test_bf16x3_dot_within_certification_bound(engine, d):
+    """The scan's dot product as it computes it — x1.q1, x1.q2 and x2.q1 in three accumulators,
+    combined (D1 + D2) + D3 in fp32 — against exact q.x, on split-boundary operands: within
+    gamma_bf16x3(d) * sum |x_t q_t|."""
+    from tc_acc import bf16_val, run_acc
+    rng = np.random.default_rng(d)
+    gamma = (524 + 0.7 * d) * U
+    worst = 0.0
+    for t in range(4):
+        x = (2.0 ** rng.uniform(-4, 8, (128, d)) * rng.choice([-1, 1], (128, d))).astype(np.float32)
+        q = (2.0 ** rng.uniform(-4, 8, (32, d))).astype(np.float32)
+        if t % 2:  # split-boundary values: residuals just under half a bf16 ulp, aligned signs
+            x = np.abs(x)
+            x = (bf16_val(x) * (1 + 2.0 ** -9 - 2.0 ** -17)).astype(np.float32)
+            q = (bf16_val(q) * (1 + 2.0 ** -9 - 2.0 ** -17)).astype(np.float32)
+        x1 = bf16_val(x)
+        x2 = bf16_val((x - x1).astype(np.float32))
+        q1 = bf16_val(q)
+        q2 = bf16_val((q - q1).astype(np.float32))
+        D1, D2, D3 = run_acc(x1, q1), run_acc(x1, q2), run_acc(x2, q1)
+        dot = ((D1 + D2) + D3).astype(np.float64)  # fp32 adds, as the kernels do
+        exact = x.astype(np.float64) @ q.T.astype(np.float64)
+        mag = np.abs(x).astype(np.float64) @ np.abs(q).T.astype(np.float64)
+        r = (np.abs(dot - exact) / mag).max()
+        worst = max(worst, r)
+        assert r <= gamma, (d, t, r / U)
+    print(f"d={d}: worst |dot error| / sum|xq| = {worst / U:.1f} u (bound {gamma / U:.0f} u)")
