@@ -17,9 +17,11 @@ cpu_baseline: the CPU oracle (oracle/librd_cpu.so — the only CPU IVF path;
               the reference has none) on a bounded query sample, rank 0, N=1.
 --impl reference: that same CPU path as the timed arm.
 Inputs are larger than L2 (30.7 GB index), so no explicit flush is needed.
-N>1 (torchrun): each rank holds a row stripe of every list of the config's
-knowledge base (strong scaling: 10M rows split N ways), searches the same batch,
-and rank 0 merges the NCCL-gathered per-shard top-k on the device.
+N>1: the config's knowledge base is split into N row stripes of every list
+(strong scaling: 10M rows split N ways), one per GPU, searched as one shard group
+(rd_group_*): under torchrun one process per GPU (NCCL gather of the per-stripe
+top-k to rank 0 and a device merge, inside the library); `--gpus N` without
+torchrun, one process driving N GPUs.
 """
 import argparse
 import json
@@ -144,189 +146,245 @@ def c5_reservation(lib):
                                      gen_batch_size=64, decode_phase=1, workspace_fraction=0.25)
 
 
-def cpu_baseline(cfg, desc_args, sample, steps=1):
-    """Times the CPU oracle on `sample` queries of the same workload (rank 0, N=1)."""
+def oracle_lib():
+    """The CPU oracle (exact IVF-Flat; test infrastructure), built on demand."""
     from paper_2504_15302_b200.retriever import Library
     subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "oracle")])
-    oracle = Library(os.path.join(ROOT, "oracle", "librd_cpu.so"))
+    return Library(os.path.join(ROOT, "oracle", "librd_cpu.so"))
+
+
+def cpu_desc_args(cfg, shards):
+    """The knowledge base the CPU path holds: the whole config, except C4 (307 GB) where it is the
+    row stripe one GPU of the N-GPU job holds (1 of 8 at N = 1)."""
+    if cfg.get("total"):
+        return dict(n=cfg["n"], d=cfg["d"], nlist=cfg["nlist"], shard=0, num_shards=shards)
+    return dict(n=cfg["n"], d=cfg["d"], nlist=cfg["nlist"])
+
+
+def cpu_baseline(cfg, desc_args, sample, steps=1, batch_of=None):
+    """Times the CPU oracle on `sample` queries of the same workload per step (rank 0, N=1).
+    batch_of(s) gives step s's full query batch (the GPU arm's); its first `sample` queries are
+    timed. Returns the per-step rates and the last step's queries and results (the parity check)."""
+    oracle = oracle_lib()
     desc = oracle.desc(**desc_args)
     t0 = time.time()
     idx = oracle.synthetic_index(desc)
     build_s = time.time() - t0
     cores = len(os.sched_getaffinity(0))
     vals = []
+    q = res = None
     for s in range(steps):
-        q, _ = oracle.synth_queries(desc, 10_000_000 + s * sample, sample)
+        q = batch_of(s)[:sample] if batch_of else oracle.synth_queries(desc, 10_000_000 + s * sample, sample)[0]
         t0 = time.perf_counter()
-        idx.search(q, cfg["nprobe"], cfg["k"])
+        res = idx.search(q, cfg["nprobe"], cfg["k"])
         vals.append(sample / (time.perf_counter() - t0))
     idx.close()
+    cpu = cpu_model()
     return {"value": statistics.median(vals), "unit": "queries/s", "cores": cores, "kind": "port",
-            "sample": f"{sample} queries of the same workload per step, exact IVF-Flat, {cores} threads "
-                      f"(index build {build_s:.1f}s untimed)", "per_step": vals}
+            "cpu_model": cpu,
+            "sample": f"first {sample} queries of each step's batch, exact IVF-Flat (fp64 canonical distances, "
+                      f"query-at-a-time), {cores} threads on {cpu} (index build {build_s:.1f}s untimed)",
+            "per_step": vals, "queries": q, "result": res}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def config_block(cfg, B, n_gpus, shards):
+    per = cfg["n"] // shards
+    return {"workload": cfg["workload"], "global_batch": B, "nprobe": cfg["nprobe"], "k": cfg["k"],
+            "n_total": cfg["n"], "n_per_gpu": per, "nlist": cfg["nlist"], "d": cfg["d"],
+            "parallelism": f"shard{n_gpus}" if shards == n_gpus else f"one shard of {shards} on 1 GPU",
+            "l2": "inputs larger than L2 (index %.1f GB per GPU)" % (per * cfg["d"] * 4 / 1e9)}
+
+
+def shards_for(cfg, n_gpus, stripe_of):
+    # The knowledge base is the config's (the metric is quoted "at 10M x 768"): N GPUs split it into
+    # N row stripes of every list (strong scaling). C4 (100M) does not fit one GPU: there N = 1 runs
+    # one stripe of 8, the per-rank work of the 8-GPU job.
+    if n_gpus > 1:
+        return n_gpus
+    if stripe_of > 1:
+        return stripe_of
+    return 8 if cfg.get("total") else 1
 
 
 def run_reference(args, cfg):
+    """The reference's CPU path on the box's host cores: the exact oracle (the reference has no
+    search of its own), all host threads, on this arm's config; each step times the
+    first --cpu-sample queries of the batch the GPU arm searches in that step."""
     world, rank, _ = dist_env()
+    n_gpus = world if world > 1 else args.gpus
+    shards = shards_for(cfg, n_gpus, args.stripe_of)
+    B = cfg["batch"]
     line = {"metric": METRIC, "impl": "reference", "unit": "queries/s", "higher_is_better": True,
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": n_gpus, "steps": args.steps, "warmup": args.warmup,
             "dtype": "f32 (f64 exact distances)", "data": "synthetic (splitmix64 spec, SURVEY §8d)",
-            "config": {"workload": cfg["workload"], "global_batch": cfg["batch"], "nprobe": cfg["nprobe"],
-                       "k": cfg["k"], "n": cfg["n"], "nlist": cfg["nlist"], "d": cfg["d"]}}
+            "config": config_block(cfg, B, n_gpus, shards)}
     if rank != 0:
         return
-    sample = args.cpu_sample
-    desc_args = dict(n=cfg["n"], d=cfg["d"], nlist=cfg["nlist"])
-    res = cpu_baseline(cfg, desc_args, sample, steps=args.warmup + args.steps)
+    oracle = oracle_lib()
+    desc_full = oracle.desc(cfg["n"], cfg["d"], cfg["nlist"])
+    sample = min(args.cpu_sample, B)
+    if args.cpu_sample_auto:  # the whole batch when the run fits ~150 s of CPU time, else a sample
+        probe = cpu_baseline(cfg, cpu_desc_args(cfg, shards), min(32, B), steps=1,
+                             batch_of=lambda s: oracle.synth_queries(desc_full, 0, min(32, B))[0])
+        sample = int(min(B, max(32, 150.0 * probe["value"] / (args.steps + args.warmup))))
+    res = cpu_baseline(cfg, cpu_desc_args(cfg, shards), sample, steps=args.warmup + args.steps,
+                       batch_of=lambda s: oracle.synth_queries(desc_full, s * B, sample)[0])
     vals = res["per_step"][args.warmup:]
     v = statistics.median(vals)
-    line.update({"value": v, "ms_per_step": 1000.0 * sample / v, "scaling": "replicas only",
+    line.update({"value": v, "ms_per_step": 1000.0 * B / v, "scaling": "replicas only",
                  "vs_baseline": None,
                  "cpu_baseline": {"value": v, "unit": "queries/s", "cores": res["cores"], "kind": "port",
-                                  "sample": res["sample"]},
+                                  "cpu_model": res["cpu_model"], "sample": res["sample"]},
                  "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
     print(json.dumps(line), flush=True)
 
 
 def run_ours(args, cfg):
     import torch
-    import torch.distributed as dist
     from paper_2504_15302_b200.retriever import engine
 
     world, rank, local = dist_env()
-    # one process per GPU; RD_DIST_BACKEND=gloo (with ranks sharing a device) only exercises the
-    # multi-rank code path on a single-GPU box
-    backend = os.environ.get("RD_DIST_BACKEND", "nccl")
-    local = local % max(1, torch.cuda.device_count())
-    if world > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend, rank=rank, world_size=world)
-    torch.cuda.set_device(local)
     lib = engine()
     B, k, nprobe, d = cfg["batch"], cfg["k"], cfg["nprobe"], cfg["d"]
-    # The knowledge base is the config's (the metric is quoted "at 10M x 768"): N GPUs split it into N
-    # row stripes of every list (strong scaling). C4 (100M) does not fit one GPU: there N = 1 runs
-    # one stripe of 8, the per-rank work of the 8-GPU job.
     n_total = cfg["n"]
-    shards = world if (world > 1 or not cfg.get("total")) else 8
-    if args.stripe_of > 1 and world == 1:  # one rank's share of an N-GPU run, on one GPU
-        shards = args.stripe_of
-    desc = lib.desc(n_total, d, cfg["nlist"], shard=rank, num_shards=shards)
+    ndev = torch.cuda.device_count()
+    # Multi-GPU through the library's shard groups (rd_group_*): under torchrun one process per GPU
+    # (rd_group_create_rank: NCCL gather of the per-stripe top-k to rank 0 + device merge, inside the
+    # library); `--gpus N` without torchrun, one process driving N GPUs (rd_group_create_synthetic:
+    # ncclCommInitAll). torch.distributed (gloo) only carries the group id, barriers and the max over
+    # ranks of the device-timed step.
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        local = local % max(1, ndev)
+        n_gpus = world
+    else:
+        dist = None
+        n_gpus = args.gpus
+        # RD_BENCH_DEVICES=0,0 maps the stripes onto given devices: exercises the one-process group
+        # path on a one-GPU box (device copies instead of NCCL); not a scaling measurement
+        devices = [int(x) for x in os.environ["RD_BENCH_DEVICES"].split(",")] if os.environ.get(
+            "RD_BENCH_DEVICES") else list(range(n_gpus))
+        if len(devices) != n_gpus or max(devices) >= ndev:
+            raise SystemExit(f"--gpus {n_gpus}: only {ndev} CUDA devices visible")
+    torch.cuda.set_device(local)
+    shards = shards_for(cfg, n_gpus, args.stripe_of)
     t0 = time.time()
-    idx = lib.synthetic_index(desc, device=local)
+    grp = None
+    if world > 1:
+        desc = lib.desc(n_total, d, cfg["nlist"], shard=rank, num_shards=shards)
+        idx0 = lib.synthetic_index(desc, device=local)
+        obj = [lib.group_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        grp = lib.rank_group(idx0, obj[0], world, rank)
+    elif n_gpus > 1:
+        desc = lib.desc(n_total, d, cfg["nlist"], shard=0, num_shards=shards)
+        grp = lib.synthetic_group(lib.desc(n_total, d, cfg["nlist"]), devices)
+    else:
+        desc = lib.desc(n_total, d, cfg["nlist"], shard=0, num_shards=shards)
+        idx0 = lib.synthetic_index(desc, device=local)
     build_s = time.time() - t0
+    searcher = grp if grp is not None else idx0
+    stripe = grp.shard(0) if grp is not None else idx0  # this process's (first) stripe: stats, timing
     reservation = None
     heat = None
     if cfg["offload"] is None or cfg["offload"] > 0:
         # joint placement pins the hot lists: probe frequency from a calibration batch of queries
-        # disjoint from the timed ones (north_star item 4)
+        # disjoint from the timed ones (north_star item 4); probe sets are the same on every stripe
         cal, _ = lib.synth_queries(desc, 50_000_000, 4096)
-        pr = idx.probe(cal, nprobe)
+        pr = stripe.probe(cal, nprobe)
         heat = np.bincount(pr[pr >= 0].ravel(), minlength=cfg["nlist"]).astype(np.uint32)
     if cfg["offload"] is None:  # C5: budget = device memory - LLM reservation - engine workspace
         free, total = torch.cuda.mem_get_info()
         reservation = c5_reservation(lib)
         budget = int(total - reservation - (4 << 30))
-        idx.place(hbm_budget_bytes=budget, list_heat=heat)
+        searcher.place(hbm_budget_bytes=budget, list_heat=heat)
     elif cfg["offload"] > 0:
-        idx.place(offload_fraction=cfg["offload"], list_heat=heat)
-    info = idx.info()
+        searcher.place(offload_fraction=cfg["offload"], list_heat=heat)
+    info = stripe.info()
     hold = None
     if reservation is not None:  # actually hold the LLM's bytes while searching
         free, _ = torch.cuda.mem_get_info()
         hold = torch.empty(int(min(reservation, free - (6 << 30))), dtype=torch.uint8, device="cuda")
 
     nb = args.warmup + args.steps
-    qs = [lib.synth_queries(desc, i * B, B)[0] for i in range(nb)]
+    full = lib.desc(n_total, d, cfg["nlist"])
+    qs = [lib.synth_queries(full, i * B, B)[0] for i in range(nb)]
     dq = [torch.from_numpy(q).cuda() for q in qs]
-    # one packed result buffer per rank ([B, k] ids then [B, k] distances) so the exchange is a
-    # single all-gather of B * k * 12 bytes
-    nbi = B * k * 8
-    res8 = torch.empty(B * k * 12, dtype=torch.uint8, device="cuda")
-    di = res8[:nbi].view(torch.int64).view(B, k)
-    dd = res8[nbi:].view(torch.float32).view(B, k)
-    gres = [torch.empty_like(res8) for _ in range(world)]
-    mi = torch.empty((B, k), dtype=torch.int64, device="cuda")
-    md = torch.empty((B, k), dtype=torch.float32, device="cuda")
+    di = torch.empty((B, k), dtype=torch.int64, device="cuda")
+    dd = torch.empty((B, k), dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
 
-    def step(i):
-        idx.search_device(dq[i].data_ptr(), B, nprobe, k, di.data_ptr(), dd.data_ptr(), stream=sptr)
-        if world > 1:
-            dist.all_gather(gres, res8)
-            if rank == 0:
-                g = torch.stack(gres)
-                ti, td = g[:, :nbi].contiguous(), g[:, nbi:].contiguous()  # [G][B][k] ids, distances
-                lib.check(lib.lib.rd_merge_topk_device(world, B, k, ti.data_ptr(), td.data_ptr(), mi.data_ptr(),
-                                                       md.data_ptr(), sptr), "merge")
+    def step(i):  # one search of one batch; at N > 1 the merged top-k lands on rank 0 / device 0
+        searcher.search_device(dq[i].data_ptr(), B, nprobe, k, di.data_ptr(), dd.data_ptr(), stream=sptr)
 
-    # correctness / certification on one synced search
-    st = idx.search_device(dq[0].data_ptr(), B, nprobe, k, di.data_ptr(), dd.data_ptr(), stream=sptr, sync=True)
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    # correctness / certification and this stripe's scan bytes on one synced search
+    st = searcher.search_device(dq[0].data_ptr(), B, nprobe, k, di.data_ptr(), dd.data_ptr(), stream=sptr, sync=True)
+    # one stripe's counters (the roofline is per GPU): a one-process group's stats sum its stripes
+    st1 = stripe.search_device(dq[0].data_ptr(), B, nprobe, k, di.data_ptr(), dd.data_ptr(), stream=sptr,
+                               sync=True) if grp is not None and world == 1 else st
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    barrier()
     # per-stage events inside the timed region: the scan kernel's own duration for the roofline
     # (they cost the chain its launch overlap, ~12 us per search; e2e and the sweep run without)
-    idx.timing_stages(True)
-    idx.timing_reset()
+    stripes = [grp.shard(g) for g in range(grp.info()["local_shards"])] if grp is not None else [idx0]
+    for sx in stripes:
+        sx.timing_stages(True)
+        sx.timing_reset()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+        barrier()
         ev0.record(stream)
         for i in range(args.warmup, nb):
             step(i)
         ev1.record(stream)
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+        barrier()
     ms = ev0.elapsed_time(ev1)
-    tm = idx.timing_read()
-    idx.timing_stages(False)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
+    tms = [sx.timing_read() for sx in stripes]
+    for sx in stripes:
+        sx.timing_stages(False)
+    tm = max(tms, key=lambda t: t["scan_ms"])  # the slowest stripe bounds the step
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
     value = B * args.steps / (ms / 1000.0)
 
-    # e2e: public C-ABI rd_search with pinned host buffers (H2D queries + D2H ids/dists every
-    # step, inside the timed region); at N > 1 every rank searches its shard and rank 0 merges
-    # the gathered per-shard results with rd_merge_topk (host)
+    # e2e: the public C-ABI (rd_search / rd_group_search) with pinned host buffers (H2D queries +
+    # D2H ids/dists every step, inside the timed region); at N > 1 a collective group call
     hq = [torch.from_numpy(q).pin_memory().numpy() for q in qs]
     hi = torch.empty((B, k), dtype=torch.int64).pin_memory().numpy()
     hd = torch.empty((B, k), dtype=torch.float32).pin_memory().numpy()
-
-    def e2e_step(i):
-        idx.search_into(hq[i], nprobe, k, hi, hd)
-        if world > 1:
-            di.copy_(torch.from_numpy(hi), non_blocking=True)
-            dd.copy_(torch.from_numpy(hd), non_blocking=True)
-            dist.all_gather(gres, res8)
-            if rank == 0:
-                g = torch.stack(gres).cpu()
-                gi = g[:, :nbi].contiguous().view(torch.int64).view(world, B, k).numpy()
-                gd = g[:, nbi:].contiguous().view(torch.float32).view(world, B, k).numpy()
-                lib.merge_topk(gi, gd)
-
     for i in range(min(args.warmup, 2)):
-        e2e_step(i)
-    if world > 1:
-        dist.barrier()
+        searcher.search_into(hq[i], nprobe, k, hi, hd)
+    barrier()
     t0 = time.perf_counter()
     for i in range(args.warmup, nb):
-        e2e_step(i)
-    if world > 1:
-        dist.barrier()
+        searcher.search_into(hq[i], nprobe, k, hi, hd)
+    barrier()
     e2e_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], device="cuda")
+    if dist is not None:
+        t = torch.tensor([e2e_s], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e = {"value": B * args.steps / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": B * d * 4,
@@ -334,28 +392,28 @@ def run_ours(args, cfg):
 
     # batch sweep of BASELINE configs[1] (same index, queries in HBM): q/s per batch size
     sweep = {}
-    if world == 1 and not args.no_sweep and args.config == "c2":
+    if n_gpus == 1 and not args.no_sweep and args.config == "c2":
         for Bs in (1, 8, 32, 64, 128, 256, 512, 1024):
             qs_s = torch.from_numpy(lib.synth_queries(desc, 70_000_000 + Bs, Bs)[0]).cuda()
             oi = torch.empty((Bs, k), dtype=torch.int64, device="cuda")
             od = torch.empty((Bs, k), dtype=torch.float32, device="cuda")
             for _ in range(3):
-                idx.search_device(qs_s.data_ptr(), Bs, nprobe, k, oi.data_ptr(), od.data_ptr(), stream=sptr)
+                idx0.search_device(qs_s.data_ptr(), Bs, nprobe, k, oi.data_ptr(), od.data_ptr(), stream=sptr)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             reps = 10
             torch.cuda.synchronize()
             e0.record(stream)
             for _ in range(reps):
-                idx.search_device(qs_s.data_ptr(), Bs, nprobe, k, oi.data_ptr(), od.data_ptr(), stream=sptr)
+                idx0.search_device(qs_s.data_ptr(), Bs, nprobe, k, oi.data_ptr(), od.data_ptr(), stream=sptr)
             e1.record(stream)
             torch.cuda.synchronize()
             sweep[str(Bs)] = Bs * reps / (e0.elapsed_time(e1) / 1000.0)
 
-    # roofline of the dominant kernel (N4 resident list scan), measured over the timed region
+    # roofline of the dominant kernel (the resident list scan) of this process's slowest stripe
     peaks = measured_peaks()
     peak = peaks["hbm_gbs"] if peaks else 6650.0
     scan_ms = tm["scan_ms"] / max(1, tm["stage_searches"])
-    scan_bytes = st["bytes_lists_resident"]
+    scan_bytes = st1["bytes_lists_resident"]
     achieved = scan_bytes / (scan_ms * 1e-3) / 1e9 if scan_ms > 0 else 0.0
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "scan_traffic.json")
@@ -363,52 +421,71 @@ def run_ours(args, cfg):
     # workload may quote it
     if os.path.exists(tpath) and shards == 1 and not args.batch:
         traffic = json.load(open(tpath)).get(args.config)
-    launches_per_search = st["kernel_launches"]
     h2d_link = None
-    if st["h2d_list_bytes"] > 0:  # offloaded lists: the host link is the roofline of that part
+    if st1["h2d_list_bytes"] > 0:  # offloaded lists: the host link is the roofline of that part
         link = measure_h2d_gbs()
-        ach = st["h2d_list_bytes"] / (ms_step * 1e-3) / 1e9
+        ach = st1["h2d_list_bytes"] / (ms_step * 1e-3) / 1e9
         h2d_link = {"achieved": ach, "peak": link, "unit": "GB/s", "frac": ach / link,
-                    "bytes_per_step": st["h2d_list_bytes"],
+                    "bytes_per_step": st1["h2d_list_bytes"],
                     "peak_source": "measured in this run: pinned 1 GiB host->device cudaMemcpy, best of 5",
                     "note": "achieved over the whole step: the resident scan and merge overlap or follow the stream"}
 
     if rank != 0:
+        if grp is not None:
+            grp.close()
+        dist.destroy_process_group()
         return
+    read_peak = peaks.get("hbm_read_gbs") if peaks else None
     line = {
-        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": n_gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (splitmix64 spec, SURVEY §8d), generated on device",
         "scaling": "strong",
-        "config": {"workload": cfg["workload"], "global_batch": B, "nprobe": nprobe, "k": k, "n_per_gpu": info["n"],
-                   "n_total": n_total, "nlist": cfg["nlist"], "d": d,
-                   "parallelism": f"shard{world}" if shards == world else f"one shard of {shards} on 1 GPU",
-                   "l2": "inputs larger than L2 (index %.1f GB)" % (info["n"] * d * 4 / 1e9)},
+        "config": config_block(cfg, B, n_gpus, shards),
         "e2e": e2e,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "ivf_scan_tc_kernel (N5; FFMA ivf_scan_kernel N4 when d % 64 != 0)", "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
-                     "bytes_per_launch": scan_bytes, "avg_launch_ms": scan_ms},
+                     "kernel": "ivf_scan_tc_kernel (N5; FFMA ivf_scan_kernel N4 when d % 64 != 0)",
+                     "peak_source": ("MEASURED_PEAKS.json hbm_gbs (a torch copy: read + write bytes); a read-only "
+                                     "stream of the scan's TMA pattern reaches ~7.46 TB/s (tools/micro/bw.cu)")
+                     if peaks else "fallback",
+                     "bytes_per_launch": scan_bytes, "avg_launch_ms": scan_ms,
+                     "stripe": "per GPU (this process's slowest stripe)" if n_gpus > 1 else "the index"},
         "step_breakdown_ms": {k2: tm[k2] / max(1, tm["stage_searches"]) for k2 in ("coarse_ms", "scan_ms", "tail_ms", "total_ms")},
         "step_gbps_algorithmic": st["bytes_algorithmic"] / (ms_step * 1e-3) / 1e9,
-        "gpu_launches": launches_per_search * args.steps + (args.steps if world > 1 else 0),
+        "gpu_launches": st["kernel_launches"] * args.steps,
         "batch_sweep_qps": sweep,
         "clocks": clk.summary(),
         "certified": {"margin_failures": st["margin_failures"], "probe_failures": st["probe_failures"]},
         "h2d_link": h2d_link,
         "index": {"build_s": build_s, "lists_resident": info["lists_resident"], "hbm_bytes": info["hbm_bytes"],
-                  "host_pinned_bytes": info["host_pinned_bytes"], "h2d_list_bytes_per_step": st["h2d_list_bytes"],
+                  "host_pinned_bytes": info["host_pinned_bytes"], "h2d_list_bytes_per_step": st1["h2d_list_bytes"],
                   "llm_reservation_bytes": reservation},
     }
-    if world == 1 and not args.no_cpu_baseline:
-        idx.close()
-        del dq, hold
-        torch.cuda.empty_cache()
-        cb = cpu_baseline(cfg, dict(n=cfg["n"], d=d, nlist=cfg["nlist"]), args.cpu_sample)
-        cb.pop("per_step", None)
+    if grp is not None:
+        gi = grp.info()
+        line["group"] = {"transport": gi["transport"], "num_shards": gi["num_shards"], "local_shards": gi["local_shards"]}
+    if read_peak:
+        line["roofline"]["frac_of_read_peak"] = achieved / read_peak
+    if n_gpus == 1 and not args.no_cpu_baseline:
+        # the CPU path on the first queries of the last timed batch, then the engine on those same
+        # queries (outside every timed region): the parity check of this run
+        sample = min(args.cpu_sample, B)
+        cb = cpu_baseline(cfg, cpu_desc_args(cfg, shards), sample, batch_of=lambda s: qs[nb - 1])
+        mine = idx0.search(cb["queries"], nprobe, k)
+        want = cb["result"]
+        line["parity"] = {"checked": int(sample),
+                          "ids_equal": int((mine.ids == want.ids).all(axis=1).sum()),
+                          "dists_equal": int((mine.dists == want.dists).all(axis=1).sum()),
+                          "oracle": "oracle/librd_cpu.so (exact IVF-Flat, canonical fp64 distances)",
+                          "data": "the whole knowledge base" if shards == 1 else f"stripe 0 of {shards}"}
+        for key in ("per_step", "queries", "result"):
+            cb.pop(key, None)
         line["cpu_baseline"] = cb
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if grp is not None:
+        grp.close()
+    if dist is not None:
         dist.destroy_process_group()
 
 
@@ -420,7 +497,11 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--batch", type=int, default=0)
-    ap.add_argument("--cpu-sample", type=int, default=128)
+    ap.add_argument("--cpu-sample", type=int, default=128,
+                    help="CPU-path queries per step (our arm's cpu_baseline; --impl reference: see --cpu-sample-auto)")
+    ap.add_argument("--cpu-sample-fixed", dest="cpu_sample_auto", action="store_false",
+                    help="--impl reference: time exactly --cpu-sample queries per step instead of the whole "
+                         "batch when ~150 s of CPU time allows")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--stripe-of", type=int, default=0,
