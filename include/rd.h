@@ -80,7 +80,12 @@ typedef struct {
 } rd_synth_desc;
 
 /* Placement between searches (reference analogue: PlacementConfig, domain.hpp:75-82).
- * Lists not resident live in pinned host memory and are streamed per search. */
+ * Lists not resident live in pinned host memory and are streamed per search. The engine keeps the
+ * resident rows as RD_STORE_SPLIT3 (6 B per element) when the tensor-core scan applies and the budget
+ * does not cut the resident set at that size, else as fp32 (4 B per element: under a tight budget
+ * residency beats scan speed, since every list left out streams over the host link per search).
+ * Relayouts happen in place: the store grows or shrinks in chunks (<= 64 MiB) and never holds two
+ * copies of a list; a 64 MiB conversion buffer is the only transient. Waits for searches in flight. */
 typedef struct {
   uint64_t hbm_budget_bytes;     /* 0 = no byte budget; else covers resident lists plus (once any list
                                     is offloaded) a staging ring of >= 2 slots of
@@ -118,7 +123,13 @@ typedef struct {
   int32_t staging_slots;
   float max_norm;       /* max ||x|| over the index (used by the margin bound) */
   int32_t device;
+  int32_t store;        /* resident-row format: RD_STORE_* (engine; the CPU oracle reports 0) */
+  int32_t reserved;
 } rd_index_info;
+/* Resident-row formats. */
+#define RD_STORE_F32 0          /* fp32 rows (FFMA scan, or the tensor-core scan converting on the fly) */
+#define RD_STORE_F32_PRESPLIT 1 /* fp32 rows plus a bf16 (x1, x2) copy for the scan: 8 B per element */
+#define RD_STORE_SPLIT3 2       /* the exact bf16 triple x = (x1 + x2) + x3 only: 6 B per element */
 
 /* LLM-side memory reservation for the retrieval GPU (C5). Mirrors
  * ragsim::ModelProfile (domain.hpp:37-55) and the PlacementConfig weight/KV
@@ -181,7 +192,8 @@ void rd_index_destroy(rd_index* h);
  * plus, while any list is offloaded, two staging slots of max(largest offloaded list, 16384 rows)
  * rounded up to 256 rows; otherwise RD_ERR_INFEASIBLE and nothing changes. Invalid ids, promoting
  * a resident list, demoting an offloaded one or naming a list twice: RD_ERR_INVALID.
- * Only between searches (one in-flight call per handle). */
+ * Only between searches: waits for searches enqueued with rd_search_device first. With a budget, the
+ * staging ring keeps as many slots (>= 2) as the budget leaves room for. */
 typedef struct {
   double seconds;            /* wall time of the migration */
   uint64_t h2d_bytes;        /* promoted list bytes, pinned host -> HBM */

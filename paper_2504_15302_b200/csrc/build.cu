@@ -65,6 +65,67 @@ __global__ void row_list_kernel(const long long* __restrict__ off, int* __restri
   for (long long r = r0 + threadIdx.x; r < r1; r += blockDim.x) row_list[r] = l;
 }
 
+// split3 store (host.cuh): x1 = bf16(x), x2 = bf16(x - x1), x3 = bf16(x - x1 - x2), each
+// residual exact in fp32; (x1 + x2) + x3 reproduces x bit for bit for every finite x whose residuals
+// stay inside bf16's range (a zero keeps its sign through x2 = x3 = x). Elements that do not
+// round-trip are counted in *inexact (the index then keeps fp32 rows); x12 == nullptr only counts.
+// 8 elements per thread, 16 B loads and stores.
+__global__ void split3_kernel(const float* __restrict__ X, long long rows, int d, __nv_bfloat16* __restrict__ x12,
+                              __nv_bfloat16* __restrict__ x3, unsigned* __restrict__ inexact) {
+  const int v8 = d >> 3;
+  const long long total = rows * v8;
+  unsigned bad = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / v8;
+    const int t0 = (int)(i - r * v8) * 8;
+    const float4 a = reinterpret_cast<const float4*>(X + (size_t)r * d + t0)[0];
+    const float4 b = reinterpret_cast<const float4*>(X + (size_t)r * d + t0)[1];
+    const float x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    __align__(16) __nv_bfloat16 h1[8], h2[8], h3[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const __nv_bfloat16 p1 = __float2bfloat16_rn(x[e]);
+      const float r1 = __fsub_rn(x[e], __bfloat162float(p1));
+      const __nv_bfloat16 p2 = x[e] == 0.f ? p1 : __float2bfloat16_rn(r1);
+      const float r2 = __fsub_rn(r1, __bfloat162float(p2));
+      const __nv_bfloat16 p3 = x[e] == 0.f ? p1 : __float2bfloat16_rn(r2);
+      const float back = __fadd_rn(__fadd_rn(__bfloat162float(p1), __bfloat162float(p2)), __bfloat162float(p3));
+      bad += __float_as_uint(back) != __float_as_uint(x[e]);
+      h1[e] = p1, h2[e] = p2, h3[e] = p3;
+    }
+    if (!x12) continue;  // exactness check only
+    __nv_bfloat16* o = x12 + (size_t)r * 2 * d + t0;
+    *reinterpret_cast<uint4*>(o) = *reinterpret_cast<const uint4*>(h1);
+    *reinterpret_cast<uint4*>(o + d) = *reinterpret_cast<const uint4*>(h2);
+    *reinterpret_cast<uint4*>(x3 + (size_t)r * d + t0) = *reinterpret_cast<const uint4*>(h3);
+  }
+  if (bad) atomicAdd(inexact, bad);
+}
+
+// fp32 rows back from a split3 store: X[r][t] = (x1 + x2) + x3
+__global__ void join3_kernel(const __nv_bfloat16* __restrict__ x12, const __nv_bfloat16* __restrict__ x3,
+                             long long rows, int d, float* __restrict__ X) {
+  const int v8 = d >> 3;
+  const long long total = rows * v8;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / v8;
+    const int t0 = (int)(i - r * v8) * 8;
+    __align__(16) __nv_bfloat16 h1[8], h2[8], h3[8];
+    *reinterpret_cast<uint4*>(h1) = *reinterpret_cast<const uint4*>(x12 + (size_t)r * 2 * d + t0);
+    *reinterpret_cast<uint4*>(h2) = *reinterpret_cast<const uint4*>(x12 + (size_t)r * 2 * d + d + t0);
+    *reinterpret_cast<uint4*>(h3) = *reinterpret_cast<const uint4*>(x3 + (size_t)r * d + t0);
+    float x[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      x[e] = __fadd_rn(__fadd_rn(__bfloat162float(h1[e]), __bfloat162float(h2[e])), __bfloat162float(h3[e]));
+    float4* o = reinterpret_cast<float4*>(X + (size_t)r * d + t0);
+    o[0] = make_float4(x[0], x[1], x[2], x[3]);
+    o[1] = make_float4(x[4], x[5], x[6], x[7]);
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_row_list(const long long* off, int nlist, int* row_list, cudaStream_t s) {
@@ -93,6 +154,24 @@ cudaError_t launch_max_f32(const float* v, long long n, float* out, cudaStream_t
   cudaError_t e = cudaMemsetAsync(out, 0, sizeof(float), s);
   if (e != cudaSuccess || n == 0) return e;
   max_f32_kernel<<<148 * 4, 256, 0, s>>>(v, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_split3(const float* X, long long rows, int d, void* x12, void* x3, unsigned* inexact,
+                          cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  if (d % 8) return cudaErrorInvalidValue;
+  const long long total = rows * (d / 8);
+  split3_kernel<<<(unsigned)min((total + 255) / 256, 148LL * 16), 256, 0, s>>>(
+      X, rows, d, reinterpret_cast<__nv_bfloat16*>(x12), reinterpret_cast<__nv_bfloat16*>(x3), inexact);
+  return cudaGetLastError();
+}
+cudaError_t launch_join3(const void* x12, const void* x3, long long rows, int d, float* X, cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  if (d % 8) return cudaErrorInvalidValue;
+  const long long total = rows * (d / 8);
+  join3_kernel<<<(unsigned)min((total + 255) / 256, 148LL * 16), 256, 0, s>>>(
+      reinterpret_cast<const __nv_bfloat16*>(x12), reinterpret_cast<const __nv_bfloat16*>(x3), rows, d, X);
   return cudaGetLastError();
 }
 

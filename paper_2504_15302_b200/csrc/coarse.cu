@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(NT) coarse_select_kernel(const SelectParams p)
   double* qd = reinterpret_cast<double*>(vals + ((nlist + 3) & ~3));
   float* qf = reinterpret_cast<float*>(qd + d);  // kStage
   float* st = qf + d;                            // kStage: [32][d + kStagePad]
-  const int ds = d + kStagePad;
+  const int ds = d + (p.x12 ? d / 2 : 0) + kStagePad;  // staged row stride: fp32 row or split3 x12 + x3
   uint32_t bphase = 0;
   if (tid == 0) {
     amin = ~0ull;
@@ -377,6 +377,22 @@ __global__ void __launch_bounds__(NT) coarse_select_kernel(const SelectParams p)
     }
     mbar_wait(&bar, bphase);
     bphase ^= 1;
+  };
+  // resident-store row sr (seeding) into staging slot i: one fp32 row, or a split3 row's x12 and x3
+  auto stage_seed_row = [&](int i, long long sr) {
+    if (p.x12) {
+      bulk_g2s(st + i * ds, p.x12 + (size_t)sr * 2 * d, (uint32_t)(d * 4), &bar);
+      bulk_g2s(st + i * ds + d, p.x3 + (size_t)sr * d, (uint32_t)(d * 2), &bar);
+    } else {
+      bulk_g2s(st + i * ds, p.arena + (size_t)sr * d, (uint32_t)(d * 4), &bar);
+    }
+  };
+  // a staged seeding row as a RowRef
+  auto staged_ref = [&](int i) {
+    const float* slot = st + i * ds;
+    return p.x12 ? RowRef{nullptr, reinterpret_cast<const __nv_bfloat16*>(slot),
+                          reinterpret_cast<const __nv_bfloat16*>(slot + d)}
+                 : row_f32(slot);
   };
 
   float vmin = __builtin_huge_valf(), vmax = -__builtin_huge_valf();
@@ -424,9 +440,9 @@ __global__ void __launch_bounds__(NT) coarse_select_kernel(const SelectParams p)
       if (r0 >= 0 && p.list_off[l + 1] - p.list_off[l] >= p.seed_rows) {
         seed_l = l;
         if (warp == 0) {
-          if (lane == 0) mbar_arrive_expect_tx(&bar, (uint32_t)(p.seed_rows * d * 4));
+          if (lane == 0) mbar_arrive_expect_tx(&bar, (uint32_t)(p.seed_rows * d * (p.x12 ? 6 : 4)));
           __syncwarp();
-          if (lane < p.seed_rows) bulk_g2s(st + lane * ds, p.arena + (size_t)(r0 + lane) * d, (uint32_t)(d * 4), &bar);
+          if (lane < p.seed_rows) stage_seed_row(lane, r0 + lane);
         }
       }
     }
@@ -508,7 +524,7 @@ __global__ void __launch_bounds__(NT) coarse_select_kernel(const SelectParams p)
     if (seed_l >= 0) {
       mbar_wait(&bar, bphase);
       bphase ^= 1;
-      const float e = l2_group8_f32(qf, st + grp * ds, d, j8);  // rows >= seed_rows: stale, masked
+      const float e = l2_group8_f32_row(qf, staged_ref(grp), d, j8);  // rows >= seed_rows: stale, masked
       seed_pre = block_reduce_max<NT>(grp < p.seed_rows ? e : 0.f, fsh);
       __syncthreads();  // the staging area is free again
     }
@@ -735,18 +751,26 @@ __global__ void __launch_bounds__(NT) coarse_select_kernel(const SelectParams p)
     if (l < 0) {
       if (tid == 0) p.qthr[b] = 0x7f7f7f7f;
     } else {
-      const float* r0 = p.arena + (size_t)p.res_row0[l] * d;
+      const long long sr0 = p.res_row0[l];  // the list's first row in the resident store
       float e = 0.f;
       const bool pre = kStage && l == seed_l;  // computed early (uniform branch)
       if (!pre) {
         if constexpr (kStage) {
-          stage_bulk(p.seed_rows, [&](int r) { return r0 + (size_t)r * d; });
-          e = l2_group8_f32(qf, st + grp * ds, d, j8);
+          if (warp == 0) {
+            if (lane == 0) mbar_arrive_expect_tx(&bar, (uint32_t)(p.seed_rows * d * (p.x12 ? 6 : 4)));
+            __syncwarp();
+            if (lane < p.seed_rows) stage_seed_row(lane, sr0 + lane);
+          }
+          mbar_wait(&bar, bphase);
+          bphase ^= 1;
+          e = l2_group8_f32_row(qf, staged_ref(grp), d, j8);
           if (grp >= p.seed_rows) e = 0.f;  // only the first seed_rows rows bound the threshold
         } else {  // NT / 8 rows per pass (a uniform trip count keeps the group shuffles converged)
           for (int rb = 0; rb < p.seed_rows; rb += NT / 8) {
             const int r = rb + grp;
-            const float v = l2_group8_f32<16>(q, r0 + (size_t)min(r, p.seed_rows - 1) * d, d, j8);
+            const long long sr = sr0 + min(r, p.seed_rows - 1);
+            const RowRef x = p.x12 ? row_split3(p.x12, p.x3, sr, d) : row_f32(p.arena + (size_t)sr * d);
+            const float v = l2_group8_f32_row<16>(q, x, d, j8);
             if (r < p.seed_rows) e = fmaxf(e, v);
           }
         }
@@ -798,7 +822,8 @@ cudaError_t launch_select(const SelectParams& p, bool stage, cudaStream_t s, int
   if (p.nprobe + kCoarseExtra > kSelMaxCand) return cudaErrorInvalidValue;
   const size_t keys = sizeof(uint32_t) * (size_t)((p.nlist + 3) & ~3);
   const size_t qd = sizeof(double) * (size_t)p.d;
-  const size_t staged = keys + qd + sizeof(float) * ((size_t)p.d + 32 * (size_t)(p.d + kStagePad));
+  const size_t ds = (size_t)p.d + (p.x12 ? p.d / 2 : 0) + kStagePad;  // the kernel's staged row stride
+  const size_t staged = keys + qd + sizeof(float) * ((size_t)p.d + 32 * ds);
   if (stage && staged <= 200 * 1024)
     return launch_k(coarse_select_kernel<true, kSelThreads>, dim3(p.B), dim3(kSelThreads), staged, s, p);
   // large batches (enough CTAs to hide latency) or very large nlist: the direct-load variant. Past

@@ -143,6 +143,170 @@ struct HBuf {  // pinned, mapped host memory
   }
 };
 
+// ------------------------------------------------------------------ growable device arenas (CUDA VMM)
+// Driver entry points of the virtual memory management API, bound at run time like the tensor-map
+// encoder (no link-time libcuda dependency).
+struct VmmApi {
+  decltype(&cuMemAddressReserve) reserve = nullptr;
+  decltype(&cuMemAddressFree) free_range = nullptr;
+  decltype(&cuMemCreate) create = nullptr;
+  decltype(&cuMemRelease) release = nullptr;
+  decltype(&cuMemMap) map = nullptr;
+  decltype(&cuMemUnmap) unmap = nullptr;
+  decltype(&cuMemSetAccess) set_access = nullptr;
+  decltype(&cuMemGetAllocationGranularity) granularity = nullptr;
+};
+const VmmApi& vmm() {
+  static VmmApi api = [] {
+    VmmApi a;
+    auto get = [](const char* name) {
+      void* ptr = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint(name, &ptr, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+        ptr = nullptr;
+      return ptr;
+    };
+    a.reserve = reinterpret_cast<decltype(a.reserve)>(get("cuMemAddressReserve"));
+    a.free_range = reinterpret_cast<decltype(a.free_range)>(get("cuMemAddressFree"));
+    a.create = reinterpret_cast<decltype(a.create)>(get("cuMemCreate"));
+    a.release = reinterpret_cast<decltype(a.release)>(get("cuMemRelease"));
+    a.map = reinterpret_cast<decltype(a.map)>(get("cuMemMap"));
+    a.unmap = reinterpret_cast<decltype(a.unmap)>(get("cuMemUnmap"));
+    a.set_access = reinterpret_cast<decltype(a.set_access)>(get("cuMemSetAccess"));
+    a.granularity = reinterpret_cast<decltype(a.granularity)>(get("cuMemGetAllocationGranularity"));
+    return a;
+  }();
+  if (!api.reserve || !api.create || !api.map || !api.unmap || !api.set_access || !api.granularity || !api.release ||
+      !api.free_range)
+    throw_rd(RD_ERR_RUNTIME, "CUDA virtual memory management entry points unavailable");
+  return api;
+}
+#define CUK(x)                                                                                  \
+  do {                                                                                          \
+    CUresult r_ = (x);                                                                          \
+    if (r_ != CUDA_SUCCESS) throw_rd(RD_ERR_RUNTIME, "%s failed (%d) (%s:%d)", #x, (int)r_, __FILE__, __LINE__); \
+  } while (0)
+
+// A device arena over one reserved virtual range, backed by physical memory in fixed-size chunks
+// mapped on demand (CUDA VMM): resize() grows or shrinks the usable prefix in place and map_range()
+// backs any window, so a relayout never holds two copies of the rows (format conversions run
+// tail-first: the destination's tail is mapped as the source's tail is released), the base pointer
+// — and every TMA map encoded over it — stays valid, and the HBM held is what is mapped.
+// n = elements usable (the resident store's rows x row elements).
+template <class T>
+struct VArena {
+  T* p = nullptr;
+  size_t n = 0;            // elements usable
+  size_t cap = 0;          // elements the reserved range can hold
+  size_t chunk = 0;        // bytes per physical chunk
+  int device = -1;
+  std::vector<CUmemGenericAllocationHandle> h;  // per chunk of the range
+  std::vector<uint8_t> on;                      // chunk mapped
+  VArena() = default;
+  VArena(const VArena&) = delete;
+  VArena& operator=(const VArena&) = delete;
+  ~VArena() { reset(); }
+  size_t mapped_bytes() const {
+    size_t c = 0;
+    for (uint8_t b : on) c += b;
+    return c * chunk;
+  }
+  void unmap_chunk(size_t i) {
+    const auto& v = vmm();
+    CUK(v.unmap(reinterpret_cast<CUdeviceptr>(p) + i * chunk, chunk));
+    CUK(v.release(h[i]));
+    on[i] = 0;
+  }
+  void reset() {
+    if (!p) return;
+    const auto& v = vmm();
+    for (size_t i = 0; i < on.size(); ++i)
+      if (on[i]) {
+        v.unmap(reinterpret_cast<CUdeviceptr>(p) + i * chunk, chunk);
+        v.release(h[i]);
+      }
+    v.free_range(reinterpret_cast<CUdeviceptr>(p), on.size() * chunk);
+    h.clear();
+    on.clear();
+    p = nullptr;
+    n = cap = 0;
+  }
+  // reserves room for `capacity` elements on the current device (contents dropped)
+  void reserve(size_t capacity) {
+    reset();
+    const auto& v = vmm();
+    CK(cudaGetDevice(&device));
+    CUmemAllocationProp prop{};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = device;
+    size_t gran = 0;
+    CUK(v.granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+    if (!gran) gran = size_t(2) << 20;
+    const size_t bytes = std::max<size_t>(1, capacity) * sizeof(T);
+    // chunks of at most 64 MiB (the most a store holds beyond its rows), at least one granule,
+    // ~1/512 of the range for large arenas
+    chunk = std::min<size_t>(size_t(64) << 20, std::max(gran, (bytes / 512 + gran - 1) / gran * gran));
+    chunk = (chunk + gran - 1) / gran * gran;
+    const size_t nchunks = (bytes + chunk - 1) / chunk;
+    CUdeviceptr base = 0;
+    CUK(v.reserve(&base, nchunks * chunk, 0, 0, 0));  // default alignment (chunk need not be a power of two)
+    p = reinterpret_cast<T*>(base);
+    cap = nchunks * chunk / sizeof(T);
+    h.assign(nchunks, 0);
+    on.assign(nchunks, 0);
+    n = 0;
+  }
+  // backs elements [lo, hi) with physical memory (chunks already mapped are kept)
+  void map_range(size_t lo, size_t hi) {
+    if (hi > cap) throw_rd(RD_ERR_RUNTIME, "arena window beyond its reservation (%zu > %zu)", hi, cap);
+    if (hi <= lo) return;
+    const auto& v = vmm();
+    const CUdeviceptr base = reinterpret_cast<CUdeviceptr>(p);
+    CUmemAllocationProp prop{};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = device;
+    CUmemAccessDesc acc{};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = device;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    const size_t c0 = lo * sizeof(T) / chunk, c1 = (hi * sizeof(T) + chunk - 1) / chunk;
+    for (size_t i = c0; i < c1; ++i) {
+      if (on[i]) continue;
+      const CUresult r = v.create(&h[i], chunk, &prop, 0);
+      if (r != CUDA_SUCCESS)
+        throw_rd(RD_ERR_RUNTIME, "device memory exhausted backing an arena window of %zu bytes (cuMemCreate %d)",
+                 (hi - lo) * sizeof(T), (int)r);
+      const CUresult m = v.map(base + i * chunk, chunk, 0, h[i], 0);
+      if (m != CUDA_SUCCESS) {
+        v.release(h[i]);
+        throw_rd(RD_ERR_RUNTIME, "cuMemMap failed (%d)", (int)m);
+      }
+      on[i] = 1;
+      CUK(v.set_access(base + i * chunk, chunk, &acc, 1));
+    }
+  }
+  // releases every chunk that lies wholly at or beyond element `from`
+  void unmap_from(size_t from) {
+    const size_t c0 = (from * sizeof(T) + chunk - 1) / chunk;
+    for (size_t i = c0; i < on.size(); ++i)
+      if (on[i]) unmap_chunk(i);
+  }
+  // `count` usable elements from the start: contents below min(old, new) kept
+  void resize(size_t count) {
+    if (count > cap) throw_rd(RD_ERR_RUNTIME, "arena resize beyond its reservation (%zu > %zu)", count, cap);
+    unmap_from(count);
+    map_range(0, count);
+    n = count;
+  }
+  // reserve(capacity) + resize(count): a fresh arena of `count` usable elements
+  void alloc(size_t count, size_t capacity = 0) {
+    reserve(std::max(count, capacity));
+    resize(count);
+  }
+};
+
 // ------------------------------------------------------------------ tensor maps
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -280,14 +444,25 @@ struct rd_index {
   long long max_len = 0;
   float cmax = 0.f, xmax = 0.f;
 
-  DBuf<float> centroids, cnorm, xnorm, arena;
+  DBuf<float> centroids, cnorm, xnorm;
   DBuf<float> csplit;  // nlist x 2 x d bf16 (c1, c2) for the tensor-core coarse GEMM
   CUtensorMap cmap{};
-  // pre-split bf16 (x1, x2) copy of the resident arena for the conversion-free tensor-core scan;
-  // kept only while every list is resident and device memory allows (RD_PRESPLIT=0 disables)
-  DBuf<float> xsplit;
+  // Resident store: the rows of the HBM-resident lists (a list's rows contiguous from res_row0), in
+  // one of two formats:
+  //  split3 (whenever the tensor-core scan applies and the split round-trips): the exact bf16 triple
+  //    x = (x1 + x2) + x3 — xsplit [rows][2][d] (x1, x2), the scan's operand, and x3 [rows][d], read
+  //    only by the exact rerank / fallback / seeding, which rebuild x bit for bit: 6 B per element;
+  //  fp32: arena [rows][d] (the FFMA scan's input: d % 64 != 0, RD_SPLIT3=0, data whose split does
+  //    not round-trip), plus, while no byte budget applies and memory allows, a pre-split xsplit copy
+  //    for the conversion-free scan (8 B per element; RD_PRESPLIT=0 disables).
+  // Every store is a VArena: relayouts grow and shrink it in place.
+  bool split3 = false;
+  VArena<float> arena;
+  VArena<float> xsplit;  // 2 bf16 per float slot
+  VArena<uint16_t> x3;
   CUtensorMap xmap128{}, xmap32{};
   bool presplit = false;
+  DBuf<unsigned> inexact_ctr;  // split3_kernel's count of elements that did not round-trip
   bool budgeted = false;  // last placement had an HBM byte budget
   DBuf<long long> d_list_off, d_ids, d_res_row0;
   DBuf<int> d_row_list;  // list of each global row (merge: row -> list without a search)
@@ -410,6 +585,155 @@ struct rd_index {
     // the tensor-core scan stages bf16 query slices of 64 dims
   }
 
+  // ---- the resident store (format-agnostic row operations; rows are resident-store rows)
+  bool split3_eligible() const {
+    const char* env = std::getenv("RD_SPLIT3");
+    return tc_scan() && tc_min_q == 1 && !(env && std::atoi(env) == 0);
+  }
+  size_t res_row_bytes() const { return (size_t)d * (split3 ? 6 : 4); }
+  void store_reserve(long long rows_cap) {  // capacity for rows_cap rows, contents dropped
+    if (split3) {
+      arena.reset();
+      xsplit.reserve((size_t)std::max(1LL, rows_cap) * d);
+      x3.reserve((size_t)std::max(1LL, rows_cap) * d);
+    } else {
+      xsplit.reset();
+      x3.reset();
+      arena.reserve((size_t)std::max(1LL, rows_cap) * d);
+    }
+  }
+  void store_resize(long long rows) {
+    if (split3) {
+      xsplit.resize((size_t)rows * d);
+      x3.resize((size_t)rows * d);
+    } else {
+      arena.resize((size_t)rows * d);
+    }
+  }
+  uint64_t store_bytes() const { return arena.mapped_bytes() + xsplit.mapped_bytes() + x3.mapped_bytes(); }
+  // fp32 device rows -> store rows [row0, row0 + rows)
+  void store_put(long long row0, const float* src, long long rows, cudaStream_t s) {
+    if (!rows) return;
+    if (split3) {
+      if (!inexact_ctr.p) {
+        inexact_ctr.alloc(1);
+        CK(cudaMemset(inexact_ctr.p, 0, sizeof(unsigned)));
+      }
+      CK(rd::launch_split3(src, rows, d, xsplit.p + (size_t)row0 * d, x3.p + (size_t)row0 * d, inexact_ctr.p, s));
+    } else {
+      CK(cudaMemcpyAsync(arena.p + (size_t)row0 * d, src, (size_t)rows * d * 4, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  // store rows [row0, row0 + rows) -> fp32 device rows
+  void store_get(long long row0, long long rows, float* dst, cudaStream_t s) const {
+    if (!rows) return;
+    if (split3)
+      CK(rd::launch_join3(xsplit.p + (size_t)row0 * d, x3.p + (size_t)row0 * d, rows, d, dst, s));
+    else
+      CK(cudaMemcpyAsync(dst, arena.p + (size_t)row0 * d, (size_t)rows * d * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  // store rows [src, src + rows) -> [dst, dst + rows), dst < src (compaction): chunks never overlap
+  void store_move_down(long long dst, long long src, long long rows, cudaStream_t s) {
+    if (!rows || dst == src) return;
+    const long long chunk = std::min(rows, src - dst);
+    for (long long r = 0; r < rows; r += chunk) {
+      const long long c = std::min(chunk, rows - r);
+      if (split3) {
+        CK(cudaMemcpyAsync(xsplit.p + (size_t)(dst + r) * d, xsplit.p + (size_t)(src + r) * d, (size_t)c * d * 4,
+                           cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(x3.p + (size_t)(dst + r) * d, x3.p + (size_t)(src + r) * d, (size_t)c * d * 2,
+                           cudaMemcpyDeviceToDevice, s));
+      } else {
+        CK(cudaMemcpyAsync(arena.p + (size_t)(dst + r) * d, arena.p + (size_t)(src + r) * d, (size_t)c * d * 4,
+                           cudaMemcpyDeviceToDevice, s));
+      }
+    }
+  }
+  // In-place format change of the resident store (placements), tail-first: the destination's window
+  // for rows [lo, hi) is mapped, the rows converted, and the source's chunks above lo released, so
+  // device memory peaks at max(source, destination) plus about a chunk each. To split3 only when
+  // every element round-trips (checked before anything is released); returns whether it converted.
+  bool convert_store(bool to3) {
+    if (to3 == split3) return true;
+    const long long rows = n_resident;
+    const long long cr = conv_rows();
+    if (to3) {
+      if (!inexact_ctr.p) inexact_ctr.alloc(1);
+      CK(cudaMemset(inexact_ctr.p, 0, sizeof(unsigned)));
+      CK(rd::launch_split3(arena.p, rows, d, nullptr, nullptr, inexact_ctr.p, 0));
+      unsigned bad = 0;
+      CK(cudaMemcpy(&bad, inexact_ctr.p, sizeof bad, cudaMemcpyDeviceToHost));
+      if (bad) return false;
+      xsplit.reserve((size_t)std::max(1LL, n) * d);
+      x3.reserve((size_t)std::max(1LL, n) * d);
+      for (long long hi = rows; hi > 0;) {
+        const long long lo = std::max(0LL, hi - cr);
+        xsplit.map_range((size_t)lo * d, (size_t)hi * d);
+        x3.map_range((size_t)lo * d, (size_t)hi * d);
+        CK(rd::launch_split3(arena.p + (size_t)lo * d, hi - lo, d, xsplit.p + (size_t)lo * d, x3.p + (size_t)lo * d,
+                             inexact_ctr.p, 0));
+        CK(cudaStreamSynchronize(0));
+        arena.unmap_from((size_t)lo * d);
+        hi = lo;
+      }
+      arena.reset();
+      xsplit.n = x3.n = (size_t)rows * d;
+    } else {
+      arena.reserve((size_t)std::max(1LL, n) * d);
+      for (long long hi = rows; hi > 0;) {
+        const long long lo = std::max(0LL, hi - cr);
+        arena.map_range((size_t)lo * d, (size_t)hi * d);
+        CK(rd::launch_join3(xsplit.p + (size_t)lo * d, x3.p + (size_t)lo * d, hi - lo, d, arena.p + (size_t)lo * d, 0));
+        CK(cudaStreamSynchronize(0));
+        xsplit.unmap_from((size_t)lo * d);
+        x3.unmap_from((size_t)lo * d);
+        hi = lo;
+      }
+      xsplit.reset();
+      x3.reset();
+      arena.n = (size_t)rows * d;
+    }
+    split3 = to3;
+    return true;
+  }
+
+  // rows that fit one conversion buffer (host <-> split3 transfers, materialize)
+  long long conv_rows() const { return std::max<long long>(1, (long long)((size_t(64) << 20) / ((size_t)d * 4))); }
+
+  // Builds the store of a fully resident index from fp32 rows produced chunk by chunk
+  // (produce(r0, rows, dst): rows [r0, r0 + rows) in list order into the device buffer dst), with the
+  // row norms on the way: split3 when eligible (the fp32 rows never exist in HBM all at once); if any
+  // element does not round-trip, the rows are produced again into an fp32 store.
+  void materialize(const std::function<void(long long, long long, float*)>& produce) {
+    xnorm.alloc(n);
+    DBuf<float> tmp;
+    const long long cr = std::min<long long>(std::max(1LL, n), conv_rows());
+    tmp.alloc((size_t)cr * d);
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      split3 = attempt == 0 && split3_eligible();
+      if (attempt == 1 && !std::getenv("RD_SPLIT3_QUIET"))
+        fprintf(stderr, "rd: split3 store inexact for this data (%s); using fp32 rows\n", "residual out of bf16 range");
+      store_reserve(n);
+      store_resize(n);
+      if (split3) {
+        if (!inexact_ctr.p) inexact_ctr.alloc(1);
+        CK(cudaMemset(inexact_ctr.p, 0, sizeof(unsigned)));
+      }
+      for (long long r0 = 0; r0 < n; r0 += cr) {
+        const long long c = std::min(cr, n - r0);
+        produce(r0, c, tmp.p);
+        CK(rd::launch_row_norms(tmp.p, c, d, xnorm.p + r0, 0));
+        store_put(r0, tmp.p, c, 0);
+      }
+      if (!split3) break;
+      unsigned bad = 0;
+      CK(cudaMemcpy(&bad, inexact_ctr.p, sizeof bad, cudaMemcpyDeviceToHost));
+      if (bad == 0) break;
+    }
+    CK(cudaDeviceSynchronize());
+    finish_layout();
+  }
+
   void finish_layout() {
     max_len = 0;
     for (int l = 0; l < nlist; ++l) max_len = std::max(max_len, list_off[l + 1] - list_off[l]);
@@ -454,6 +778,10 @@ struct rd_index {
   }
 
   void build_presplit() {
+    if (split3) {  // the store is the scan's operand
+      presplit = n_resident > 0;
+      return;
+    }
     presplit = false;
     xsplit.reset();
     const char* env = std::getenv("RD_PRESPLIT");
@@ -521,20 +849,37 @@ struct rd_index {
     return rd::launch_row_norms(X, rows, d, out, 0);
   }
 
+  // Device-side residency tables after any relayout: res_row0, each list's row base (fp32 rows:
+  // the fp32 arena or mapped host memory; nullptr for a list in the split3 store, whose rows the
+  // kernels address through res_row0) and the scans' tensor maps.
   void upload_residency() {
     d_res_row0.alloc(nlist);
     CK(cudaMemcpy(d_res_row0.p, res_row0.data(), sizeof(long long) * nlist, cudaMemcpyHostToDevice));
-    xsplit.reset();  // any relayout invalidates the pre-split copy (rebuilt by build_presplit)
-    presplit = false;
+    if (!split3) {
+      xsplit.reset();  // any relayout invalidates the pre-split copy (rebuilt by build_presplit)
+      presplit = false;
+    }
     std::vector<const float*> base(nlist);
     for (int l = 0; l < nlist; ++l)
-      base[l] = resident[l] ? arena.p + (size_t)res_row0[l] * d : host_arena.p + (size_t)host_row0[l] * d;
+      base[l] = resident[l] ? (split3 ? nullptr : arena.p + (size_t)res_row0[l] * d)
+                            : host_arena.p + (size_t)host_row0[l] * d;
     d_list_base.alloc(nlist);
     CK(cudaMemcpy(d_list_base.p, base.data(), sizeof(const float*) * nlist, cudaMemcpyHostToDevice));
-    map256 = make_row_map(arena.p, std::max(1LL, n_resident), d, rd::kScanRows);
-    map128 = make_row_map(arena.p, std::max(1LL, n_resident), d, rd::kTcRows);
-    map32 = make_row_map(arena.p, std::max(1LL, n_resident), d, 32);
+    if (split3) {
+      if (n_resident > 0) {
+        xmap128 = make_split_map(xsplit.p, n_resident, d, rd::kTcRows);
+        xmap32 = make_split_map(xsplit.p, n_resident, d, 32);
+      }
+      presplit = n_resident > 0;
+    } else if (arena.p) {
+      map256 = make_row_map(arena.p, std::max(1LL, n_resident), d, rd::kScanRows);
+      map128 = make_row_map(arena.p, std::max(1LL, n_resident), d, rd::kTcRows);
+      map32 = make_row_map(arena.p, std::max(1LL, n_resident), d, 32);
+    }
   }
+  // device pointers the kernels take for the split3 store (nullptr in fp32 mode)
+  const __nv_bfloat16* x12_dev() const { return split3 ? reinterpret_cast<const __nv_bfloat16*>(xsplit.p) : nullptr; }
+  const __nv_bfloat16* x3_dev() const { return split3 ? reinterpret_cast<const __nv_bfloat16*>(x3.p) : nullptr; }
 };
 
 namespace {

@@ -111,12 +111,12 @@ int rd_index_create_synthetic(const rd_synth_desc* s, int32_t device, rd_index**
     CK(rd::launch_gen_centroids(h->centroids.p, nl, h->d, derive_seed(s->seed, RD_STREAM_CENTROIDS), 0));
     h->d_ids.alloc(h->n);
     CK(cudaMemcpy(h->d_ids.p, ids.data(), sizeof(long long) * h->n, cudaMemcpyHostToDevice));
-    h->arena.alloc((size_t)h->n * h->d);
-    CK(rd::launch_gen_vectors(h->arena.p, h->d_ids.p, h->n, h->d, nl, h->centroids.p, sa,
-                              derive_seed(s->seed, RD_STREAM_VECTOR_NOISE), s->sigma, 0));
-    h->xnorm.alloc(h->n);
-    CK(rd::launch_row_norms(h->arena.p, h->n, h->d, h->xnorm.p, 0));
-    h->finish_layout();
+    const uint64_t sx = derive_seed(s->seed, RD_STREAM_VECTOR_NOISE);
+    const float sigma = s->sigma;
+    rd_index* hp = h.get();
+    h->materialize([&](long long r0, long long c, float* dst) {
+      CK(rd::launch_gen_vectors(dst, hp->d_ids.p + r0, c, hp->d, nl, hp->centroids.p, sa, sx, sigma, 0));
+    });
     *out = h.release();
   });
 }
@@ -141,15 +141,13 @@ int rd_index_create_from_host(int64_t n, int32_t d, int32_t nlist, const float* 
     h->centroids.alloc((size_t)nlist * d);
     h->cnorm.alloc(nlist);
     CK(cudaMemcpy(h->centroids.p, centroids, sizeof(float) * (size_t)nlist * d, cudaMemcpyHostToDevice));
-    h->arena.alloc((size_t)n * d);
-    if (n) CK(cudaMemcpy(h->arena.p, vectors, sizeof(float) * (size_t)n * d, cudaMemcpyHostToDevice));
     h->d_ids.alloc(n);
     std::vector<long long> idv(std::max<int64_t>(1, n));
     for (long long i = 0; i < n; ++i) idv[i] = ids ? ids[i] : i;
     CK(cudaMemcpy(h->d_ids.p, idv.data(), sizeof(long long) * n, cudaMemcpyHostToDevice));
-    h->xnorm.alloc(n);
-    CK(rd::launch_row_norms(h->arena.p, n, d, h->xnorm.p, 0));
-    h->finish_layout();
+    h->materialize([&](long long r0, long long c, float* dst) {
+      CK(cudaMemcpy(dst, vectors + (size_t)r0 * d, sizeof(float) * (size_t)c * d, cudaMemcpyHostToDevice));
+    });
     *out = h.release();
   });
 }
@@ -262,8 +260,6 @@ int rd_index_build(int64_t n, int32_t d, int32_t nlist, const float* vectors, co
     group();
     // list-order layout
     h->list_off = hseg;
-    h->arena.alloc((size_t)n * d);
-    CK(rd::launch_gather_rows(X.p, rows_sorted.p, n, d, h->arena.p, s));
     DBuf<long long> uids;
     if (ids) {
       uids.alloc(n);
@@ -272,10 +268,10 @@ int rd_index_build(int64_t n, int32_t d, int32_t nlist, const float* vectors, co
     h->d_ids.alloc(n);
     CK(rd::launch_gather_ids(ids ? uids.p : nullptr, rows_sorted.p, n, h->d_ids.p, s));
     CK(cudaStreamSynchronize(s));
+    h->materialize([&](long long r0, long long c, float* dst) {
+      CK(rd::launch_gather_rows(X.p, rows_sorted.p + r0, c, d, dst, s));
+    });
     X.reset();
-    h->xnorm.alloc(n);
-    CK(rd::launch_row_norms(h->arena.p, n, d, h->xnorm.p, 0));
-    h->finish_layout();
     *out = h.release();
   });
 }
@@ -347,14 +343,23 @@ int rd_index_save(const rd_index* h, const char* path) {
       row += fill;
       fill = 0;
     };
+    DBuf<float> conv;  // resident rows in fp32 (the split3 store rebuilt by join3)
+    if (h->split3) conv.alloc((size_t)std::min(chunk_rows, h->conv_rows()) * h->d);
     for (int l = 0; l < h->nlist; ++l) {
       const long long len = h->list_off[l + 1] - h->list_off[l];
-      const float* src = h->resident[l] ? h->arena.p + (size_t)h->res_row0[l] * h->d
-                                        : h->host_arena.p + (size_t)h->host_row0[l] * h->d;
       for (long long r = 0; r < len;) {
-        const long long take = std::min(len - r, chunk_rows - fill);
-        CK(cudaMemcpy(bounce.p + (size_t)fill * h->d, src + (size_t)r * h->d, (size_t)take * row_bytes,
-                      cudaMemcpyDefault));
+        long long take = std::min(len - r, chunk_rows - fill);
+        float* dst = bounce.p + (size_t)fill * h->d;
+        if (!h->resident[l]) {
+          std::memcpy(dst, h->host_arena.p + (size_t)(h->host_row0[l] + r) * h->d, (size_t)take * row_bytes);
+        } else if (!h->split3) {
+          CK(cudaMemcpy(dst, h->arena.p + (size_t)(h->res_row0[l] + r) * h->d, (size_t)take * row_bytes,
+                        cudaMemcpyDeviceToHost));
+        } else {
+          take = std::min<long long>(take, (long long)(conv.n / h->d));
+          h->store_get(h->res_row0[l] + r, take, conv.p, 0);
+          CK(cudaMemcpy(dst, conv.p, (size_t)take * row_bytes, cudaMemcpyDeviceToHost));
+        }
         fill += take;
         r += take;
         if (fill == chunk_rows) flush();
@@ -401,34 +406,36 @@ int rd_index_load(const char* path, int32_t device, rd_index** out) {
       h->d_ids.alloc(hd.n);
       if (hd.n) CK(cudaMemcpy(h->d_ids.p, ids.data(), 8 * (size_t)hd.n, cudaMemcpyHostToDevice));
     }
-    // vectors: file -> two pinned bounce buffers -> HBM; the read of chunk i+1 overlaps the copy of chunk i
-    h->arena.alloc((size_t)hd.n * d);
-    const uint64_t total = 4ull * (uint64_t)hd.n * d;
+    // vectors: file -> two pinned bounce buffers -> the conversion buffer -> the resident store; the
+    // read of bounce chunk i+1 overlaps the copy of chunk i
+    const size_t row_bytes = 4 * (size_t)d;
+    const long long bounce_rows = std::max<long long>(1, (long long)(kIoChunk / row_bytes));
     HBuf<char> buf[2];
     cudaEvent_t done[2];
     for (int i = 0; i < 2; ++i) {
-      buf[i].alloc(kIoChunk);
+      buf[i].alloc((size_t)bounce_rows * row_bytes);
       CK(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
     }
+    long long nchunk = 0;
     try {
-      for (uint64_t o = 0, i = 0; o < total; o += kIoChunk, ++i) {
-        const size_t bytes = (size_t)std::min<uint64_t>(kIoChunk, total - o);
-        if (i >= 2) CK(cudaEventSynchronize(done[i & 1]));
-        pread_all(f.fd, buf[i & 1].p, bytes, hd.off_vectors + o, path);
-        CK(cudaMemcpyAsync(reinterpret_cast<char*>(h->arena.p) + o, buf[i & 1].p, bytes, cudaMemcpyHostToDevice,
-                           h->copy_stream));
-        CK(cudaEventRecord(done[i & 1], h->copy_stream));
-      }
-      CK(cudaStreamSynchronize(h->copy_stream));
+      h->materialize([&](long long r0, long long c, float* dst) {
+        for (long long r = 0; r < c; r += bounce_rows, ++nchunk) {
+          const long long take = std::min(bounce_rows, c - r);
+          const int slot = (int)(nchunk & 1);
+          if (nchunk >= 2) CK(cudaEventSynchronize(done[slot]));
+          pread_all(f.fd, buf[slot].p, (size_t)take * row_bytes, hd.off_vectors + (uint64_t)(r0 + r) * row_bytes, path);
+          CK(cudaMemcpyAsync(dst + (size_t)r * d, buf[slot].p, (size_t)take * row_bytes, cudaMemcpyHostToDevice,
+                             h->copy_stream));
+          CK(cudaEventRecord(done[slot], h->copy_stream));
+        }
+        CK(cudaStreamSynchronize(h->copy_stream));
+      });
     } catch (...) {
       cudaStreamSynchronize(h->copy_stream);
       for (auto e : done) cudaEventDestroy(e);
       throw;
     }
     for (auto e : done) cudaEventDestroy(e);
-    h->xnorm.alloc(hd.n);
-    CK(rd::launch_row_norms(h->arena.p, hd.n, d, h->xnorm.p, 0));
-    h->finish_layout();
     *out = h.release();
   });
 }
@@ -442,12 +449,15 @@ int rd_index_info_get(const rd_index* h, rd_index_info* o) {
     o->nlist = h->nlist;
     o->n_resident = h->n_resident;
     for (int l = 0; l < h->nlist; ++l) o->lists_resident += h->resident[l];
-    o->hbm_bytes = (uint64_t)h->n_resident * h->d * 4 + (uint64_t)h->n * 16 + (uint64_t)h->nlist * (h->d + 1) * 4 +
-                   (uint64_t)h->slots * h->slot_rows * h->d * 4 + (uint64_t)h->xsplit.n * 4;
+    // what the index holds on the device: the resident store as mapped (rows rounded up to its
+    // arena chunks), the staging ring, per-row norms / ids / list map and the coarse-stage state
+    o->hbm_bytes = h->store_bytes() + (uint64_t)h->staging.n * 4 + (uint64_t)h->n * (4 + 8 + 4) +
+                   (uint64_t)h->nlist * ((uint64_t)h->d * 8 + 4 + 8 + 8 + 8);
     o->host_pinned_bytes = (uint64_t)h->host_arena.n * 4;
     o->staging_slots = h->slots;
     o->max_norm = h->xmax;
     o->device = h->device;
+    o->store = h->split3 ? RD_STORE_SPLIT3 : h->presplit ? RD_STORE_F32_PRESPLIT : RD_STORE_F32;
   });
 }
 
@@ -461,42 +471,170 @@ int rd_index_layout(const rd_index* h, int64_t* offs, int64_t* ids, uint8_t* mas
   });
 }
 
+// ---------------------------------------------------------------- relayout (placement and migration)
+namespace {
+
+// Residency change of an index between searches ("shrink before grow",
+// core/src/simulator.cpp:323-326): lists leaving HBM get a pinned host copy unless they have one
+// (copies are write-once and kept), the lists staying resident are compacted in store order toward
+// row 0, the store shrinks (or grows) in place to the new resident rows — its VArenas unmap or map
+// chunks at the tail — and the lists coming in are copied from their host copies into the tail.
+// Device memory never holds more than max(before, after) of the store plus one conversion buffer
+// (split3 stores only: fp32 <-> split rows). A list is resident in the store's current format.
+void relayout(rd_index* h, const std::vector<uint8_t>& after, rd_migration_stats* ms) {
+  const int nl = h->nlist, d = h->d;
+  const size_t row_f32 = (size_t)d * 4;
+  auto len_of = [&](int l) { return h->list_off[l + 1] - h->list_off[l]; };
+  cudaStream_t cs = h->copy_stream;
+  DBuf<float> conv;
+  auto conv_buf = [&] {
+    if (!conv.p) conv.alloc((size_t)std::min<long long>(h->conv_rows(), std::max(1LL, h->max_len)) * d);
+    return (long long)(conv.n / d);
+  };
+  // 1. host copies of lists leaving HBM
+  long long need_host = h->host_used;
+  for (int l = 0; l < nl; ++l)
+    if (h->resident[l] && !after[l] && h->host_row0[l] < 0) need_host += len_of(l);
+  if ((size_t)need_host * d > h->host_arena.n) {  // grow the host arena, keeping its contents
+    HBuf<float> grown;
+    grown.alloc((size_t)std::max<long long>(need_host, h->host_used + h->host_used / 2) * d);
+    if (h->host_used) std::memcpy(grown.p, h->host_arena.p, (size_t)h->host_used * row_f32);
+    std::swap(h->host_arena.p, grown.p);
+    std::swap(h->host_arena.n, grown.n);  // host_row0 are row offsets: unchanged by the move
+  }
+  for (int l = 0; l < nl; ++l) {
+    if (!(h->resident[l] && !after[l]) || h->host_row0[l] >= 0) continue;
+    const long long len = len_of(l);
+    float* dst = h->host_arena.p + (size_t)h->host_used * d;
+    if (!h->split3) {
+      CK(cudaMemcpyAsync(dst, h->arena.p + (size_t)h->res_row0[l] * d, (size_t)len * row_f32,
+                         cudaMemcpyDeviceToHost, cs));
+    } else {
+      const long long cr = conv_buf();
+      for (long long r = 0; r < len; r += cr) {
+        const long long c = std::min(cr, len - r);
+        h->store_get(h->res_row0[l] + r, c, conv.p, cs);
+        CK(cudaMemcpyAsync(dst + (size_t)r * d, conv.p, (size_t)c * row_f32, cudaMemcpyDeviceToHost, cs));
+      }
+    }
+    h->host_row0[l] = h->host_used;
+    h->host_used += len;
+    if (ms) ms->d2h_bytes += (size_t)len * row_f32;
+  }
+  CK(cudaStreamSynchronize(cs));
+  // 2. compact the lists that stay, in store order, toward row 0
+  std::vector<int> keep;
+  for (int l = 0; l < nl; ++l)
+    if (h->resident[l] && after[l]) keep.push_back(l);
+  std::sort(keep.begin(), keep.end(), [&](int a, int b) { return h->res_row0[a] < h->res_row0[b]; });
+  long long tail = 0;
+  for (int l : keep) {
+    const long long old = h->res_row0[l], len = len_of(l);
+    if (old != tail && len > 0) {
+      h->store_move_down(tail, old, len, cs);
+      if (ms) ms->d2d_bytes += (size_t)len * h->res_row_bytes();
+    }
+    h->res_row0[l] = tail;
+    tail += len;
+  }
+  for (int l = 0; l < nl; ++l)
+    if (h->resident[l] && !after[l]) h->res_row0[l] = -1;
+  CK(cudaStreamSynchronize(cs));
+  // 3. the store to the new resident size, in place
+  long long res_rows = tail;
+  for (int l = 0; l < nl; ++l)
+    if (!h->resident[l] && after[l]) res_rows += len_of(l);
+  h->store_resize(res_rows);
+  // 4. lists coming in, from their host copies into the tail
+  for (int l = 0; l < nl; ++l) {
+    if (h->resident[l] || !after[l]) continue;
+    const long long len = len_of(l);
+    const float* src = h->host_arena.p + (size_t)h->host_row0[l] * d;
+    if (!h->split3) {
+      if (len)
+        CK(cudaMemcpyAsync(h->arena.p + (size_t)tail * d, src, (size_t)len * row_f32, cudaMemcpyHostToDevice, cs));
+    } else {
+      const long long cr = conv_buf();
+      for (long long r = 0; r < len; r += cr) {
+        const long long c = std::min(cr, len - r);
+        CK(cudaMemcpyAsync(conv.p, src + (size_t)r * d, (size_t)c * row_f32, cudaMemcpyHostToDevice, cs));
+        h->store_put(tail + r, conv.p, c, cs);
+      }
+    }
+    h->res_row0[l] = tail;
+    tail += len;
+    if (ms) ms->h2d_bytes += (size_t)len * row_f32;
+  }
+  CK(cudaStreamSynchronize(cs));
+  h->resident = after;
+  h->n_resident = tail;
+}
+
+// A placement keeps host copies of the offloaded lists only (the oracle's rule, rd_oracle.c
+// rd_index_place): the pinned host arena is rebuilt with just those, in list order.
+void compact_host(rd_index* h) {
+  const int nl = h->nlist, d = h->d;
+  long long n_off = 0;
+  for (int l = 0; l < nl; ++l)
+    if (!h->resident[l]) n_off += h->list_off[l + 1] - h->list_off[l];
+  HBuf<float> fresh;
+  if (n_off) fresh.alloc((size_t)n_off * d);
+  long long hr = 0;
+  for (int l = 0; l < nl; ++l) {
+    const long long len = h->list_off[l + 1] - h->list_off[l];
+    if (h->resident[l]) {
+      h->host_row0[l] = -1;
+      continue;
+    }
+    if (len) std::memcpy(fresh.p + (size_t)hr * d, h->host_arena.p + (size_t)h->host_row0[l] * d, (size_t)len * d * 4);
+    h->host_row0[l] = hr;
+    hr += len;
+  }
+  std::swap(h->host_arena.p, fresh.p);
+  std::swap(h->host_arena.n, fresh.n);
+  h->host_used = hr;
+}
+
+// staging-ring rows for an offloaded set whose largest list has max_off rows (rd.h, rd_placement)
+long long ring_slot_rows(long long max_off) { return (std::max<long long>(max_off, 16384) + 255) / 256 * 256; }
+
+}  // namespace
+
 // ---------------------------------------------------------------- placement (N8)
 int rd_index_place(rd_index* h, const rd_placement* p) {
   return guarded([&] {
     if (!h || !p) throw_rd(RD_ERR_INVALID, "null argument");
     CK(cudaSetDevice(h->device));
+    CK(cudaDeviceSynchronize());  // searches enqueued with rd_search_device read the store
     const int nl = h->nlist;
-    const uint64_t row_bytes = (uint64_t)h->d * sizeof(float);
-    std::vector<uint8_t> mask(nl, 0);
-    uint64_t res_bytes = 0;
-    if (p->resident_mask) {
-      for (int l = 0; l < nl; ++l) {
-        mask[l] = p->resident_mask[l] ? 1 : 0;
-        if (mask[l]) res_bytes += (uint64_t)(h->list_off[l + 1] - h->list_off[l]) * row_bytes;
+    const uint64_t budget0 = p->hbm_budget_bytes;
+    auto len_of = [&](int l) { return h->list_off[l + 1] - h->list_off[l]; };
+    // The resident set for a store format (bytes per resident row): the mask, or the hottest lists
+    // up to the offload fraction and the budget; `cut` when the budget, not the fraction, stopped it.
+    auto choose = [&](uint64_t row_bytes, std::vector<uint8_t>& mask, uint64_t& res_bytes, bool& cut) {
+      mask.assign(nl, 0);
+      res_bytes = 0;
+      cut = false;
+      if (p->resident_mask) {
+        for (int l = 0; l < nl; ++l) {
+          mask[l] = p->resident_mask[l] ? 1 : 0;
+          if (mask[l]) res_bytes += (uint64_t)len_of(l) * row_bytes;
+        }
+        return;
       }
-      if (p->hbm_budget_bytes && res_bytes > p->hbm_budget_bytes)
-        throw_rd(RD_ERR_INFEASIBLE, "placement infeasible: resident lists need %llu bytes > budget %llu",
-                 (unsigned long long)res_bytes, (unsigned long long)p->hbm_budget_bytes);
-    } else {
-      if (p->offload_fraction < 0 || p->offload_fraction > 1)
-        throw_rd(RD_ERR_INVALID, "offload_fraction must be in [0, 1]");
       std::vector<int> order(nl);
       for (int l = 0; l < nl; ++l) order[l] = l;
       if (p->list_heat)
-        std::stable_sort(order.begin(), order.end(),
-                         [&](int a, int b) { return p->list_heat[a] > p->list_heat[b]; });
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return p->list_heat[a] > p->list_heat[b]; });
       const long long target = nl - (long long)std::floor(p->offload_fraction * nl + 0.5);
-      // the budget covers the resident lists and, once anything is offloaded, a staging ring of
-      // at least two slots of max(largest list, 16384 rows) (include/rd.h, rd_placement)
-      uint64_t budget = p->hbm_budget_bytes;
+      // the budget covers the resident lists and, once anything is offloaded, a staging ring of at
+      // least two slots of max(largest list, 16384 rows) (include/rd.h, rd_placement)
+      uint64_t budget = budget0;
       if (budget) {
         uint64_t all = 0;
-        for (long long i = 0; i < target; ++i)
-          all += (uint64_t)(h->list_off[order[i] + 1] - h->list_off[order[i]]) * row_bytes;
+        for (long long i = 0; i < target; ++i) all += (uint64_t)len_of(order[i]) * row_bytes;
         if (target < nl || all > budget) {
-          const uint64_t slot = (uint64_t)((std::max<long long>(h->max_len, 16384) + 255) / 256 * 256) * row_bytes;
-          const uint64_t reserve = (uint64_t)std::max(2, p->staging_slots) * slot;
+          const uint64_t reserve = (uint64_t)std::max(2, p->staging_slots) * ring_slot_rows(h->max_len) * h->d * 4;
           if (reserve > budget)
             throw_rd(RD_ERR_INFEASIBLE, "placement infeasible: budget %llu below the %llu-byte staging ring",
                      (unsigned long long)budget, (unsigned long long)reserve);
@@ -505,74 +643,77 @@ int rd_index_place(rd_index* h, const rd_placement* p) {
       }
       for (long long i = 0; i < target; ++i) {
         const int l = order[i];
-        const uint64_t lb = (uint64_t)(h->list_off[l + 1] - h->list_off[l]) * row_bytes;
-        if (budget && res_bytes + lb > budget) break;
+        const uint64_t lb = (uint64_t)len_of(l) * row_bytes;
+        if (budget && res_bytes + lb > budget) {
+          cut = true;
+          break;
+        }
         res_bytes += lb;
         mask[l] = 1;
       }
+    };
+    if (!p->resident_mask && (p->offload_fraction < 0 || p->offload_fraction > 1))
+      throw_rd(RD_ERR_INVALID, "offload_fraction must be in [0, 1]");
+    // Store format: split3 (the fast scan) unless a byte budget would then hold fewer lists than
+    // fp32 rows can — under a tight budget (an LLM co-tenant, C5) residency is worth more than scan
+    // speed, since every list left out streams over the host link on every search.
+    std::vector<uint8_t> mask;
+    uint64_t res_bytes = 0;
+    bool cut = false, fmt3 = false;
+    if (h->split3_eligible()) {
+      choose((uint64_t)h->d * 6, mask, res_bytes, cut);
+      fmt3 = !cut && !(p->resident_mask && budget0 && res_bytes > budget0);
     }
-    // relayout: resident lists compact into a new arena, the rest to pinned host memory
-    long long n_res = 0, n_off = 0, max_off = 0;
+    if (!fmt3) choose((uint64_t)h->d * 4, mask, res_bytes, cut);
+    if (p->resident_mask && budget0 && res_bytes > budget0)
+      throw_rd(RD_ERR_INFEASIBLE, "placement infeasible: resident lists need %llu bytes > budget %llu",
+               (unsigned long long)res_bytes, (unsigned long long)budget0);
+    // staging ring: slots of >= the largest offloaded list; depth by the queue_capacity rule
+    long long n_off = 0, max_off = 0, n_res = 0;
     for (int l = 0; l < nl; ++l) {
-      const long long len = h->list_off[l + 1] - h->list_off[l];
       if (mask[l])
-        n_res += len;
+        n_res += len_of(l);
       else {
-        n_off += len;
-        max_off = std::max(max_off, len);
+        n_off += len_of(l);
+        max_off = std::max(max_off, len_of(l));
       }
     }
-    // staging ring: slots of >= the largest offloaded list; depth by the queue_capacity rule
     long long slot_rows = 0;
     int slots = 0;
+    const uint64_t row_bytes = (uint64_t)h->d * (fmt3 ? 6 : 4);
     if (n_off > 0) {
-      slot_rows = std::max<long long>(max_off, 16384);
-      slot_rows = (slot_rows + 255) / 256 * 256;
-      const double slot_bytes = (double)slot_rows * row_bytes;
+      slot_rows = ring_slot_rows(max_off);
+      const double slot_bytes = (double)slot_rows * h->d * 4;
       double free_bytes;
-      if (p->hbm_budget_bytes) {
-        free_bytes = (double)p->hbm_budget_bytes - (double)res_bytes;
+      if (budget0) {
+        free_bytes = (double)budget0 - (double)res_bytes;
       } else {
         size_t fr = 0, tot = 0;
         CK(cudaMemGetInfo(&fr, &tot));
-        free_bytes = (double)fr - (double)(1ull << 30);
+        // free now, plus what the store gives back, minus what it grows by
+        free_bytes = (double)fr + (double)h->store_bytes() - (double)n_res * row_bytes - (double)(1ull << 30);
       }
       slots = p->staging_slots > 0 ? p->staging_slots : std::min(8, rd_staging_depth(free_bytes, slot_bytes));
-      if (p->hbm_budget_bytes && res_bytes + slots * slot_bytes > (double)p->hbm_budget_bytes)
+      if (budget0 && res_bytes + slots * slot_bytes > (double)budget0)
         throw_rd(RD_ERR_INFEASIBLE, "placement infeasible: no room for one %.0f-byte staging slot in the budget",
                  slot_bytes);
     }
-    HBuf<float> new_host;
-    std::vector<long long> new_res(nl, -1), new_host_row(nl, -1);
-    if (n_off) new_host.alloc((size_t)n_off * h->d);
-    DBuf<float> new_arena;
-    new_arena.alloc((size_t)std::max(1LL, n_res) * h->d);
-    long long rr = 0, hr = 0;
-    for (int l = 0; l < nl; ++l) {
-      const long long len = h->list_off[l + 1] - h->list_off[l];
-      const float* src = h->resident[l] ? h->arena.p + (size_t)h->res_row0[l] * h->d
-                                        : h->host_arena.p + (size_t)h->host_row0[l] * h->d;
-      if (mask[l]) {
-        new_res[l] = rr;
-        if (len) CK(cudaMemcpy(new_arena.p + (size_t)rr * h->d, src, len * row_bytes, cudaMemcpyDefault));
-        rr += len;
-      } else {
-        new_host_row[l] = hr;
-        if (len) CK(cudaMemcpy(new_host.p + (size_t)hr * h->d, src, len * row_bytes, cudaMemcpyDefault));
-        hr += len;
-      }
+    {  // the device must hold the new store next to what stays: fail before touching anything
+      size_t fr = 0, tot = 0;
+      CK(cudaMemGetInfo(&fr, &tot));
+      const double grow = (double)n_res * row_bytes + (double)slots * slot_rows * h->d * 4 -
+                          (double)h->store_bytes() - (double)h->staging.n * 4;
+      if (grow > (double)fr)
+        throw_rd(RD_ERR_INFEASIBLE, "placement infeasible: needs %.0f more device bytes, %zu free", grow, fr);
     }
-    CK(cudaDeviceSynchronize());
-    std::swap(h->arena.p, new_arena.p);
-    std::swap(h->arena.n, new_arena.n);
-    std::swap(h->host_arena.p, new_host.p);
-    std::swap(h->host_arena.n, new_host.n);
-    h->resident = mask;
-    h->res_row0 = new_res;
-    h->host_row0 = new_host_row;
-    h->n_resident = n_res;
-    h->host_used = n_off;
-    h->budgeted = p->hbm_budget_bytes != 0;
+    h->set_staging(0, 0);  // the ring is rebuilt for the new offloaded set
+    // a format change converts the store in place on the side where it is smaller: fp32 rows
+    // (4 B per element) before the relayout when leaving split3, after it when entering
+    if (!fmt3 && h->split3) h->convert_store(false);
+    relayout(h, mask, nullptr);
+    if (fmt3 && !h->split3) h->convert_store(true);  // stays fp32 if the split does not round-trip
+    compact_host(h);
+    h->budgeted = budget0 != 0;
     h->upload_residency();
     h->build_presplit();
     h->set_staging(slots, slot_rows);
@@ -588,7 +729,6 @@ int rd_index_migrate(rd_index* h, const int32_t* promote, int32_t n_promote, con
     CK(cudaSetDevice(h->device));
     const auto t0 = std::chrono::steady_clock::now();
     const int nl = h->nlist, d = h->d;
-    const size_t row_bytes = (size_t)d * sizeof(float);
     auto len_of = [&](int l) { return h->list_off[l + 1] - h->list_off[l]; };
     std::vector<uint8_t> seen(nl, 0);
     for (int i = 0; i < n_promote + n_demote; ++i) {
@@ -616,93 +756,33 @@ int rd_index_migrate(rd_index* h, const int32_t* promote, int32_t n_promote, con
       else
         max_off = std::max(max_off, len_of(l));
     }
-    const long long slot_rows = max_off >= 0 ? (std::max<long long>(max_off, 16384) + 255) / 256 * 256 : 0;
+    // the ring after the move: slots of >= the largest offloaded list; with a budget, as many slots
+    // as it leaves room for (at least two), otherwise the current depth (at least two)
+    const long long slot_rows = max_off >= 0 ? ring_slot_rows(max_off) : 0;
+    const uint64_t slot_bytes = (uint64_t)slot_rows * d * 4;
+    const uint64_t res_bytes = (uint64_t)res_rows * h->res_row_bytes();
+    int slots = max_off >= 0 ? std::max(2, h->slots) : 0;
     if (hbm_budget_bytes) {
-      const uint64_t need = (uint64_t)res_rows * row_bytes + (max_off >= 0 ? 2ull * slot_rows * row_bytes : 0);
+      const uint64_t need = res_bytes + (max_off >= 0 ? 2ull * slot_bytes : 0);
       if (need > hbm_budget_bytes)
         throw_rd(RD_ERR_INFEASIBLE, "migration infeasible: %llu bytes needed > budget %llu",
                  (unsigned long long)need, (unsigned long long)hbm_budget_bytes);
+      if (max_off >= 0)
+        slots = (int)std::max<uint64_t>(2, std::min<uint64_t>(slots, (hbm_budget_bytes - res_bytes) / slot_bytes));
     }
+    CK(cudaDeviceSynchronize());  // searches enqueued with rd_search_device read the store
     rd_migration_stats ms;
     std::memset(&ms, 0, sizeof ms);
-    cudaStream_t cs = h->copy_stream;
-    // 1. demote: lists without a host copy go to pinned host memory (write-once copies)
-    long long need_host = h->host_used;
-    for (int i = 0; i < n_demote; ++i)
-      if (h->host_row0[demote[i]] < 0) need_host += len_of(demote[i]);
-    if ((size_t)need_host * d > h->host_arena.n) {  // grow the host arena, keeping its contents
-      HBuf<float> grown;
-      grown.alloc((size_t)std::max<long long>(need_host, h->host_used + h->host_used / 2) * d);
-      if (h->host_used) std::memcpy(grown.p, h->host_arena.p, (size_t)h->host_used * row_bytes);
-      std::swap(h->host_arena.p, grown.p);
-      std::swap(h->host_arena.n, grown.n);
-    }
-    for (int i = 0; i < n_demote; ++i) {
-      const int l = demote[i];
-      if (h->host_row0[l] >= 0) continue;
-      const size_t bytes = (size_t)len_of(l) * row_bytes;
-      CK(cudaMemcpyAsync(h->host_arena.p + (size_t)h->host_used * d, h->arena.p + (size_t)h->res_row0[l] * d, bytes,
-                         cudaMemcpyDeviceToHost, cs));
-      h->host_row0[l] = h->host_used;
-      h->host_used += len_of(l);
-      ms.d2h_bytes += bytes;
-    }
-    CK(cudaStreamSynchronize(cs));
-    // 2. compact the lists that stay resident, in arena order, toward row 0 (forward chunked copies
-    //    never overlap: a chunk is at most the shift)
-    std::vector<int> keep;
-    for (int l = 0; l < nl; ++l)
-      if (h->resident[l] && after[l]) keep.push_back(l);
-    std::sort(keep.begin(), keep.end(), [&](int a, int b) { return h->res_row0[a] < h->res_row0[b]; });
-    long long tail = 0;
-    for (int l : keep) {
-      const long long old = h->res_row0[l], len = len_of(l);
-      if (old != tail && len > 0) {
-        const long long chunk = std::min(len, old - tail);
-        for (long long r = 0; r < len; r += chunk) {
-          const long long c = std::min(chunk, len - r);
-          CK(cudaMemcpyAsync(h->arena.p + (size_t)(tail + r) * d, h->arena.p + (size_t)(old + r) * d, (size_t)c * row_bytes,
-                             cudaMemcpyDeviceToDevice, cs));
-        }
-        ms.d2d_bytes += (size_t)len * row_bytes;
-      }
-      h->res_row0[l] = tail;
-      tail += len;
-    }
-    for (int i = 0; i < n_demote; ++i) h->res_row0[demote[i]] = -1;
-    // 3. promote into the freed space (the arena grows only if the resident set outgrows it)
-    if ((size_t)res_rows * d > h->arena.n) {
-      DBuf<float> grown;
-      grown.alloc((size_t)res_rows * d);
-      if (tail) CK(cudaMemcpyAsync(grown.p, h->arena.p, (size_t)tail * row_bytes, cudaMemcpyDeviceToDevice, cs));
-      CK(cudaStreamSynchronize(cs));
-      std::swap(h->arena.p, grown.p);
-      std::swap(h->arena.n, grown.n);
-    }
-    for (int i = 0; i < n_promote; ++i) {
-      const int l = promote[i];
-      const size_t bytes = (size_t)len_of(l) * row_bytes;
-      if (bytes)
-        CK(cudaMemcpyAsync(h->arena.p + (size_t)tail * d, h->host_arena.p + (size_t)h->host_row0[l] * d, bytes,
-                           cudaMemcpyHostToDevice, cs));
-      h->res_row0[l] = tail;
-      tail += len_of(l);
-      ms.h2d_bytes += bytes;
-    }
-    CK(cudaStreamSynchronize(cs));
-    h->resident = after;
-    h->n_resident = tail;
+    const bool ring_changes = slots != h->slots || (slots && slot_rows != h->slot_rows);
+    if (ring_changes) h->set_staging(0, 0);  // shrink before grow: the old ring goes first
+    relayout(h, after, &ms);
     if (hbm_budget_bytes) h->budgeted = true;
-    // 4. staging ring for the new offloaded set (slot >= its largest list)
-    if (max_off < 0)
-      h->set_staging(0, 0);
-    else if (h->slots == 0 || h->slot_rows < slot_rows)
-      h->set_staging(std::max(2, h->slots), slot_rows);
+    if (ring_changes) h->set_staging(slots, slot_rows);
     h->upload_residency();
     h->build_presplit();
     ms.lists_promoted = n_promote;
     ms.lists_demoted = n_demote;
-    ms.resident_bytes = (uint64_t)tail * row_bytes;
+    ms.resident_bytes = (uint64_t)h->n_resident * d * 4;
     ms.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (st) *st = ms;
   });

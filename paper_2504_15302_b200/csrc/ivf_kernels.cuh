@@ -1,6 +1,7 @@
 // ivf_kernels.cuh — launch interface of the IVF-Flat search kernels (sm_100a).
 #pragma once
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -174,6 +175,9 @@ struct SelectParams {
   int seed_rows = 32;
   float gamma_coarse = 0.f;  // dot-product bound of the coarse path that filled Dc (gamma_* above)
   float gamma_scan = 0.f;    // dot-product bound of the scans the seed threshold prunes
+  // split3 resident store (host.cuh; arena == nullptr then): seeding rows are rebuilt from it
+  const __nv_bfloat16* x12 = nullptr;
+  const __nv_bfloat16* x3 = nullptr;
 };
 // stage: q and candidate rows go through shared memory (latency-bound small batches)
 // num_sms: batches beyond one resident wave of 256-thread CTAs (4 per SM) use 128-thread CTAs
@@ -248,6 +252,10 @@ struct MergeParams {
   int m_rerank = 32;
   unsigned long long* dbg = nullptr;  // RD_DEBUG_TS: globaltimer checkpoints of CTA 0
   float gamma = 0.f;               // dot-product bound of the scans that produced the candidates
+  // split3 resident store: a list whose list_base is nullptr has its rows at res_row0 in x12 / x3
+  const long long* res_row0 = nullptr;
+  const __nv_bfloat16* x12 = nullptr;
+  const __nv_bfloat16* x3 = nullptr;
 };
 // stage: the 32 rerank rows go through shared memory (latency-bound small batches)
 cudaError_t launch_merge(const MergeParams& p, bool stage, cudaStream_t s);
@@ -270,6 +278,9 @@ struct FallbackParams {
   long long* out_ids;
   float* out_dists;
   unsigned* done_ctr;              // device scalar, 0 between launches (the kernel re-arms it)
+  const long long* res_row0 = nullptr;  // split3 store, as MergeParams
+  const __nv_bfloat16* x12 = nullptr;
+  const __nv_bfloat16* x3 = nullptr;
 };
 cudaError_t launch_fallback(const FallbackParams& p, int num_sms, cudaStream_t s);
 
@@ -288,6 +299,11 @@ cudaError_t launch_gen_vectors(float* X, const long long* ids, long long n, int 
                                const float* C, uint64_t sa, uint64_t sx, float sigma, cudaStream_t s);
 cudaError_t launch_row_norms(const float* X, long long n, int d, float* out, cudaStream_t s);
 cudaError_t launch_max_f32(const float* v, long long n, float* out, cudaStream_t s);
+// split3 resident store (host.cuh): x12 [rows][2][d] bf16 (x1, x2), x3 [rows][d] bf16, (x1 + x2) + x3 == x
+// bit for bit; elements that do not round-trip are added to *inexact (device counter)
+cudaError_t launch_split3(const float* X, long long rows, int d, void* x12, void* x3, unsigned* inexact,
+                          cudaStream_t s);
+cudaError_t launch_join3(const void* x12, const void* x3, long long rows, int d, float* X, cudaStream_t s);
 // IVF training (train.cu)
 cudaError_t launch_iota(int* v, long long n, cudaStream_t s);
 cudaError_t launch_histogram(const int* keys, long long n, unsigned* counts, int nbins, cudaStream_t s);

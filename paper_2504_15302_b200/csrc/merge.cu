@@ -15,6 +15,10 @@ namespace rd {
 namespace {
 
 constexpr float kInf = __builtin_huge_valf();
+// floats per staged candidate row: fp32 rows (d) or a split3 row's x12 + x3 (1.5 d)
+__host__ __device__ __forceinline__ int stage_stride(int d, bool split3) {
+  return (split3 ? d + d / 2 : d) + kStagePad;
+}
 constexpr long long kNoKey = 0x7fffffffffffffffll;
 
 // One CTA per query. kStage (small batches): the 32 candidate rows are staged in shared memory with
@@ -24,12 +28,13 @@ template <bool kStage>
 __global__ void __launch_bounds__(256, kStage ? 1 : 8) merge_rerank_kernel(const MergeParams p) {
   RD_TS(13);  // entry, before the wait on the previous kernel
   RD_PDL_PROLOGUE();
-  extern __shared__ __align__(16) float dyn[];  // kStage: q[d], rows[32][d + kStagePad]
+  extern __shared__ __align__(16) float dyn[];  // kStage: q[d], rows[32][ds] (ds: stage_stride)
   __shared__ float sd[8][kTopK];
   __shared__ long long sk[8][kTopK];
   __shared__ float ex_d[kTopK];
   __shared__ long long ex_id[kTopK];
-  __shared__ const float* rowp[kTopK];
+  __shared__ const float* rowp[kTopK];   // fp32 row (offloaded list / fp32 store), or nullptr
+  __shared__ long long srow[kTopK];      // split3 store row, or -1
   __shared__ float tau_s;
   __shared__ unsigned host_rows;  // kStage: candidate rows outside the device arena
   __shared__ __align__(8) uint64_t bar;
@@ -98,24 +103,37 @@ __global__ void __launch_bounds__(256, kStage ? 1 : 8) merge_rerank_kernel(const
     // the rerank's HBM reads (k = 10, margin 8: 18 of 32).
     const int m = p.m_rerank;
     const float* xp = nullptr;
+    long long sr = -1;
     long long id = kNoKey;
     if (lk != kNoKey && lane < m) {  // candidate rows: list of the row (row_list), address, user id
       const int l = __ldg(p.row_list + lk);
-      xp = p.list_base[l] + (size_t)(lk - __ldg(p.list_off + l)) * p.d;
+      const float* base = p.list_base[l];
+      const long long i = lk - __ldg(p.list_off + l);
+      if (base)
+        xp = base + (size_t)i * p.d;
+      else
+        sr = __ldg(p.res_row0 + l) + i;
       id = __ldg(p.ids + lk);
     }
     rowp[lane] = xp;
+    srow[lane] = sr;
     ex_id[lane] = id;
     if (lane == min(m, kTopK - 1)) tau_s = ld;
-    if constexpr (kStage) {  // device rows: one bulk (TMA) copy each, all in flight at once
+    if constexpr (kStage) {  // device rows: bulk (TMA) copies, all in flight at once
       float* st = dyn + p.d;
+      const int ds = stage_stride(p.d, p.x12 != nullptr);
       const bool dev = xp && xp >= p.arena_lo && xp < p.arena_hi;
-      const unsigned dm = __ballot_sync(0xffffffffu, dev);
-      if (lane == 0) mbar_arrive_expect_tx(&bar, (uint32_t)__popc(dm) * (uint32_t)p.d * 4u);
+      const unsigned dm = __ballot_sync(0xffffffffu, dev), sm3 = __ballot_sync(0xffffffffu, sr >= 0);
+      if (lane == 0)
+        mbar_arrive_expect_tx(&bar, ((uint32_t)__popc(dm) * 4u + (uint32_t)__popc(sm3) * 6u) * (uint32_t)p.d);
       const unsigned hm = __ballot_sync(0xffffffffu, xp && !dev);
       if (lane == 0) host_rows = hm;
       __syncwarp();
-      if (dev) bulk_g2s(st + lane * (p.d + kStagePad), xp, (uint32_t)p.d * 4u, &bar);
+      if (dev) bulk_g2s(st + lane * ds, xp, (uint32_t)p.d * 4u, &bar);
+      if (sr >= 0) {  // split3 row: x12 (4d bytes) then x3 (2d bytes) in one slot
+        bulk_g2s(st + lane * ds, p.x12 + (size_t)sr * 2 * p.d, (uint32_t)p.d * 4u, &bar);
+        bulk_g2s(st + lane * ds + p.d, p.x3 + (size_t)sr * p.d, (uint32_t)p.d * 2u, &bar);
+      }
     }
   }
   __syncthreads();
@@ -124,12 +142,15 @@ __global__ void __launch_bounds__(256, kStage ? 1 : 8) merge_rerank_kernel(const
   // exact rerank: thread (c = tid/8, j = tid%8)
   const int c = tid >> 3, j8 = tid & 7;
   const float* xp = rowp[c];
+  const long long sr = srow[c];
+  const bool have = xp || sr >= 0;
   float e;
   if constexpr (kStage) {
     float* st = dyn + p.d;
+    const int ds = stage_stride(p.d, p.x12 != nullptr);
     const unsigned hm = host_rows;
     if (hm) {  // rows of offloaded lists (mapped host memory): ordinary loads by every thread
-      const int v4 = p.d >> 2, ds = p.d + kStagePad;
+      const int v4 = p.d >> 2;
       for (int i = tid; i < kTopK * v4; i += 256) {
         const int r = i / v4, cc = i - r * v4;
         if ((hm >> r) & 1u)
@@ -139,12 +160,18 @@ __global__ void __launch_bounds__(256, kStage ? 1 : 8) merge_rerank_kernel(const
     mbar_wait(&bar, 0);
     __syncthreads();
     RD_TS(3);
-    e = exact_l2_group8_impl<false>(dyn, st + c * (p.d + kStagePad), xp ? p.d : 0, j8);
+    const float* slot = st + c * ds;
+    const RowRef x = sr >= 0 ? RowRef{nullptr, reinterpret_cast<const __nv_bfloat16*>(slot),
+                                      reinterpret_cast<const __nv_bfloat16*>(slot + p.d)}
+                             : row_f32(slot);
+    e = exact_l2_group8_row(dyn, x, p.d, j8, have ? p.d : 0);
   } else {
-    // a padded slot runs zero terms so the warp stays converged for the shuffles
-    e = exact_l2_group8_impl<false, 16>(q, xp ? xp : q, xp ? p.d : 0, j8);  // rows from HBM: 16 loads deep (32 registers: one wave of 8 CTAs per SM)
+    // a padded slot runs zero terms so the warp stays converged for the shuffles; rows from HBM:
+    // 16 loads deep (32 registers: one wave of 8 CTAs per SM)
+    const RowRef x = sr >= 0 ? row_split3(p.x12, p.x3, sr, p.d) : row_f32(xp ? xp : q);
+    e = exact_l2_group8_row<16>(q, x, p.d, j8, have ? p.d : 0);
   }
-  if (!xp) e = kInf;
+  if (!have) e = kInf;
   if (j8 == 0) ex_d[c] = e;
   __syncthreads();
   RD_TS(4);
@@ -277,7 +304,8 @@ __global__ void __launch_bounds__(256) fallback_kernel(const FallbackParams p) {
     long long lk = kNoKey;
     if (l >= 0) {
       const long long r0 = p.list_off[l], r1 = p.list_off[l + 1];
-      const float* base = p.list_base[l];
+      const float* base = p.list_base[l];  // nullptr: the list's rows are in the split3 store
+      const long long s0 = base ? 0 : p.res_row0[l];
       const float* qv = p.queries + (size_t)q * p.d;
       for (long long c = r0 + 32LL * warp; c < r1; c += 32LL * 8) {
         float mine = kInf;
@@ -285,7 +313,10 @@ __global__ void __launch_bounds__(256) fallback_kernel(const FallbackParams p) {
         for (int pass = 0; pass < 8; ++pass) {
           const long long row = c + pass * 4 + (lane >> 3);
           const bool ok = row < r1;
-          const float e = exact_l2_group8_any(qv, ok ? base + (size_t)(row - r0) * p.d : qv, ok ? p.d : 0, lane & 7);
+          const RowRef x = !ok ? row_f32(qv)
+                           : base ? row_f32(base + (size_t)(row - r0) * p.d)
+                                  : row_split3(p.x12, p.x3, s0 + (row - r0), p.d);
+          const float e = exact_l2_group8_row(qv, x, p.d, lane & 7, ok ? p.d : 0);
           const float v = __shfl_sync(0xffffffffu, e, (lane & 3) * 8);
           if ((lane >> 2) == pass && c + lane < r1) {
             mine = v;
@@ -339,7 +370,7 @@ cudaError_t launch_fallback(const FallbackParams& p, int num_sms, cudaStream_t s
 cudaError_t launch_merge(const MergeParams& p, bool stage, cudaStream_t s) {
   if (p.B == 0) return cudaSuccess;
   if (stage) {
-    const size_t smem = sizeof(float) * ((size_t)p.d + kTopK * (size_t)(p.d + kStagePad));
+    const size_t smem = sizeof(float) * ((size_t)p.d + kTopK * (size_t)stage_stride(p.d, p.x12 != nullptr));
     return launch_k(merge_rerank_kernel<true>, dim3(p.B), dim3(256), smem, s, p);
   }
   return launch_k(merge_rerank_kernel<false>, dim3(p.B), dim3(256), 0, s, p);

@@ -4,6 +4,7 @@
 // bitonic top-k on (distance, row) pairs.
 #pragma once
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -96,6 +97,53 @@ __device__ __forceinline__ float exact_l2_group8_any(const float* __restrict__ q
   return exact_l2_group8_impl<false>(q, x, d, j);
 }
 
+// ---------------------------------------------------------------- rows of the resident store
+// A row is fp32 (f != nullptr: offloaded lists in mapped host memory, or an fp32 arena) or the
+// exact bf16 triple split of the split3 arena (host.cuh): x = (x1 + x2) + x3 bit for bit, x1 / x2 at
+// x12[t] / x12[d + t] (the scan's [rows][2][d] operand), x3 at x3[t]. at() returns the fp32 value.
+struct RowRef {
+  const float* f;
+  const __nv_bfloat16* x12;
+  const __nv_bfloat16* x3;
+  __device__ __forceinline__ float at(int t, int d) const {
+    if (f) return f[t];
+    return __fadd_rn(__fadd_rn(__bfloat162float(x12[t]), __bfloat162float(x12[d + t])), __bfloat162float(x3[t]));
+  }
+};
+__device__ __forceinline__ RowRef row_f32(const float* f) { return RowRef{f, nullptr, nullptr}; }
+// row r of a split3 store (x12: [rows][2][d], x3: [rows][d])
+__device__ __forceinline__ RowRef row_split3(const __nv_bfloat16* x12, const __nv_bfloat16* x3, long long r, int d) {
+  return RowRef{nullptr, x12 + (size_t)r * 2 * d, x3 + (size_t)r * d};
+}
+// the canonical exact distance (exact_l2_group8_impl's order and value) to a RowRef row
+// (cnt < d terms: a padded slot passes 0 and the group stays converged for the shuffles)
+template <int kDepth = 8>
+__device__ __forceinline__ float exact_l2_group8_row(const float* q, const RowRef& x, int d, int j, int cnt) {
+  double s = 0.0;
+  int t = j;
+  for (; t + 8 * (kDepth - 1) < cnt; t += 8 * kDepth) {
+    float qv[kDepth], xv[kDepth];
+#pragma unroll
+    for (int i = 0; i < kDepth; ++i) {
+      qv[i] = q[t + 8 * i];
+      xv[i] = x.at(t + 8 * i, d);
+    }
+#pragma unroll
+    for (int i = 0; i < kDepth; ++i) {
+      const double df = __dsub_rn((double)qv[i], (double)xv[i]);
+      s = __dadd_rn(s, __dmul_rn(df, df));
+    }
+  }
+  for (; t < cnt; t += 8) {
+    const double df = __dsub_rn((double)q[t], (double)x.at(t, d));
+    s = __dadd_rn(s, __dmul_rn(df, df));
+  }
+  s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
+  s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+  s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
+  return __double2float_rn(s);
+}
+
 // ---------------------------------------------------------------- programmatic dependent launch
 // Every kernel of the search chain starts with RD_PDL_PROLOGUE: it lets the next kernel in the
 // stream begin launching (griddepcontrol.launch_dependents), then waits until every kernel it
@@ -181,6 +229,33 @@ __device__ __forceinline__ float l2_group8_f32(const float* q, const float* x, i
   return s;
 }
 __host__ __device__ __forceinline__ float l2_f32_rel_bound(int d) { return 2.f * (d / 8 + 8) * 5.9604645e-8f; }
+// l2_group8_f32 of a RowRef row (same order, same bound)
+template <int kDepth = 1>
+__device__ __forceinline__ float l2_group8_f32_row(const float* q, const RowRef& x, int d, int j) {
+  float s = 0.f;
+  int t = j;
+  for (; t + 8 * (kDepth - 1) < d; t += 8 * kDepth) {
+    float qv[kDepth], xv[kDepth];
+#pragma unroll
+    for (int i = 0; i < kDepth; ++i) {
+      qv[i] = q[t + 8 * i];
+      xv[i] = x.at(t + 8 * i, d);
+    }
+#pragma unroll
+    for (int i = 0; i < kDepth; ++i) {
+      const float df = qv[i] - xv[i];
+      s = fmaf(df, df, s);
+    }
+  }
+  for (; t < d; t += 8) {
+    const float df = q[t] - x.at(t, d);
+    s = fmaf(df, df, s);
+  }
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  s += __shfl_xor_sync(0xffffffffu, s, 4);
+  return s;
+}
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }

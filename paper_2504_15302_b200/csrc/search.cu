@@ -151,6 +151,8 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
                       h->d_list_off.p, h->d_res_row0.p, h->arena.p, h->xmax, seed ? w.qthr.p : nullptr, 0};
   sp.gamma_coarse = coarse_gamma(B, d);
   sp.gamma_scan = h->scan_gamma();
+  sp.x12 = h->x12_dev();
+  sp.x3 = h->x3_dev();
   unsigned long long* chain = nullptr;  // profiling only (RD_DEBUG_CHAIN): [select 32][plan 32][merge 32][scan 4/CTA]
   if (h->dbg_chain) {
     const size_t n = 96 + 4 * (size_t)h->num_sms;
@@ -203,7 +205,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
                       w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p, h->debug_skip};
   sc.thr_rank = thr_rank;
   tc.thr_rank = thr_rank;
-  if (!h->tc_scan() || h->tc_min_q > 1) {  // FFMA tiles exist only in these cases
+  if (!h->split3 && (!h->tc_scan() || h->tc_min_q > 1)) {  // FFMA tiles exist only in these cases (fp32 store)
     CK(rd::launch_scan(h->map256, h->map32, sc, h->num_sms, s));
     launches += 1;
   }
@@ -407,14 +409,20 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   w.fb_id.ensure((size_t)B * nprobe * rd::kTopK);
   rd::MergeParams mp{w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d_q, w.qnorm.p, h->d_list_off.p,
                      h->d_list_base.p, h->d_ids.p, h->d_row_list.p, h->arena.p,
-                     h->arena.p + (size_t)h->n_resident * d, nl, d, k, h->xmax, d_ids, d_dists,
+                     h->arena.p ? h->arena.p + (size_t)h->n_resident * d : nullptr, nl, d, k, h->xmax, d_ids, d_dists,
                      w.fails() + 1, w.fail_list.p, (int)B};
   mp.m_rerank = m_rerank;
   mp.gamma = h->scan_gamma();
+  mp.res_row0 = h->d_res_row0.p;
+  mp.x12 = h->x12_dev();
+  mp.x3 = h->x3_dev();
   if (chain) mp.dbg = chain + 64;
   h->traced("merge", s, mp.dbg, [&] { CK(rd::launch_merge(mp, h->stage_rows(B), s)); });
   rd::FallbackParams fp{w.fail_list.p, w.fails() + 1, w.probes.p, nprobe, d_q, h->d_list_off.p, h->d_list_base.p,
                         h->d_ids.p, nl, d, k, w.fb_dist.p, w.fb_id.p, d_ids, d_dists, w.fb_ctr.p};
+  fp.res_row0 = h->d_res_row0.p;
+  fp.x12 = h->x12_dev();
+  fp.x3 = h->x3_dev();
   CK(rd::launch_fallback(fp, h->num_sms, s));
   launches += 2;
   CK(cudaEventRecord(te[3], s));

@@ -76,7 +76,7 @@ class IndexInfo(C.Structure):
     _fields_ = [("n", C.c_int64), ("d", C.c_int32), ("nlist", C.c_int32), ("n_resident", C.c_int64),
                 ("hbm_bytes", C.c_uint64), ("host_pinned_bytes", C.c_uint64),
                 ("lists_resident", C.c_int32), ("staging_slots", C.c_int32), ("max_norm", C.c_float),
-                ("device", C.c_int32)]
+                ("device", C.c_int32), ("store", C.c_int32), ("reserved", C.c_int32)]
 
 
 class Timing(C.Structure):
