@@ -50,8 +50,12 @@ CONFIGS = {
     # of one rank of the 8-GPU job.
     "c4": dict(n=100_000_000, d=768, nlist=16384, nprobe=64, k=10, batch=1024, offload=0.0, total=True,
                workload="ivf-flat 100M x 768 fp32 sharded over the box's GPUs, nlist 16384, nprobe 64, k 10, batch 1024"),
-    "c5": dict(n=10_000_000, d=768, nlist=4096, nprobe=128, k=20, batch=64, offload=None,
+    "c5": dict(n=10_000_000, d=768, nlist=4096, nprobe=128, k=20, batch=64, offload=None, llm="70b",
                workload="ivf-flat 10M x 768 fp32, nlist 4096, nprobe 128, k 20, batch 64, under a 70B LLM-decode HBM reservation"),
+    # C2's search under the reference's default 8B model (configs/default_8b.json:11-19) resident
+    # beside it: the budget leaves room for the whole index in the fast (split3) store
+    "c2r8b": dict(n=10_000_000, d=768, nlist=4096, nprobe=64, k=10, batch=1024, offload=None, llm="8b",
+                  workload="ivf-flat 10M x 768 fp32, nlist 4096, nprobe 64, k 10, batch 1024, under an 8B LLM-decode HBM reservation"),
 }
 METRIC = "IVF top-k queries/sec at 10M×768 nprobe=64 k=10; achieved HBM GB/s vs peak"
 
@@ -136,14 +140,19 @@ def dist_env():
     return world, rank, local
 
 
-def c5_reservation(lib):
-    """RAGDoll placement for C5: ref_70b model (configs/ref_70b.json:11-19) fully on the GPU
-    in decode at gen batch 64; reservation = w_gpu*W + c_gpu*C(B) + H(B)*0.25
-    (memory_planner.cpp:20, prefetch_timeline.cpp:85-86)."""
+def llm_reservation(lib, model="70b"):
+    """RAGDoll placement: the LLM fully on the GPU in decode at gen batch 64; reservation =
+    w_gpu*W + c_gpu*C(B) + H(B)*0.25 (memory_planner.cpp:20, prefetch_timeline.cpp:85-86).
+    70b: configs/ref_70b.json:11-19 (C5); 8b: configs/default_8b.json:11-19."""
     GiB, MiB = 1 << 30, 1 << 20
-    return lib.llm_reservation_bytes(weight_total=140 * GiB, kv_bytes_per_request=256 * MiB,
-                                     workspace_bytes_per_request=128 * MiB, w_gpu=1.0, c_gpu=1.0,
-                                     gen_batch_size=64, decode_phase=1, workspace_fraction=0.25)
+    W, kv, ws = (140 * GiB, 256 * MiB, 128 * MiB) if model == "70b" else (16 * GiB, 128 * MiB, 64 * MiB)
+    return lib.llm_reservation_bytes(weight_total=W, kv_bytes_per_request=kv, workspace_bytes_per_request=ws,
+                                     w_gpu=1.0, c_gpu=1.0, gen_batch_size=64, decode_phase=1,
+                                     workspace_fraction=0.25)
+
+
+def c5_reservation(lib):
+    return llm_reservation(lib, "70b")
 
 
 def oracle_lib():
@@ -304,9 +313,9 @@ def run_ours(args, cfg):
         cal, _ = lib.synth_queries(desc, 50_000_000, 4096)
         pr = stripe.probe(cal, nprobe)
         heat = np.bincount(pr[pr >= 0].ravel(), minlength=cfg["nlist"]).astype(np.uint32)
-    if cfg["offload"] is None:  # C5: budget = device memory - LLM reservation - engine workspace
+    if cfg["offload"] is None:  # C5 / C2r8b: budget = device memory - LLM reservation - engine workspace
         free, total = torch.cuda.mem_get_info()
-        reservation = c5_reservation(lib)
+        reservation = llm_reservation(lib, cfg["llm"])
         budget = int(total - reservation - (4 << 30))
         searcher.place(hbm_budget_bytes=budget, list_heat=heat)
     elif cfg["offload"] > 0:
@@ -459,6 +468,8 @@ def run_ours(args, cfg):
         "certified": {"margin_failures": st["margin_failures"], "probe_failures": st["probe_failures"]},
         "h2d_link": h2d_link,
         "index": {"build_s": build_s, "lists_resident": info["lists_resident"], "hbm_bytes": info["hbm_bytes"],
+                  "store": {0: "fp32", 1: "fp32 + pre-split copy", 2: "split3 (exact bf16 triple)"}.get(info["store"]),
+                  "fp32_bytes": info["n"] * d * 4,
                   "host_pinned_bytes": info["host_pinned_bytes"], "h2d_list_bytes_per_step": st1["h2d_list_bytes"],
                   "llm_reservation_bytes": reservation},
     }
