@@ -492,6 +492,9 @@ struct rd_index {
     DBuf<long long> fb_id;
     DBuf<int> fail_list, qthr;
     DBuf<float> fb_dist;
+    DBuf<char> sel_scratch;          // the all-centroid selection (large nprobe)
+    DBuf<float> wide_d;              // the large-k pass: S x B x 32R per-split survivors
+    DBuf<long long> wide_id;
     HBuf<int> h_nq, h_qoff, h_meta;
     // per-search counters in one block so a synced search reads them back with one copy:
     // [0, 24) counters (u64 x 3), [24, 32) fails (u32 x 2), [32, 56) meta (i32 x 6); the host path
@@ -902,6 +905,8 @@ std::unique_ptr<rd_index> new_index(int device) {
 namespace rdh {
 enum SearchMode { kAsync = 0, kSync = 1, kStatsAsync = 2 };
 void validate_search(const rd_index* h, int nprobe, int k);
+bool select_all_needed(const rd_index* h, int nprobe);
+void* select_all_scratch(rd_index* h, long long B, size_t* bytes);
 // Enqueues one search of B device queries on stream s. kAsync: nothing is read back; kSync: the
 // counters are copied back and `st` filled before returning; kStatsAsync: the counter copy is
 // enqueued, the caller synchronizes s and then calls finish_stats. result_bytes: bytes after the

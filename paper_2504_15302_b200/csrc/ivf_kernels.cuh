@@ -284,14 +284,42 @@ struct FallbackParams {
 };
 cudaError_t launch_fallback(const FallbackParams& p, int num_sms, cudaStream_t s);
 
+// Beyond the fast path (wide.cu): nprobe + 32 > 512 takes the probe set from the exact distance to
+// every centroid (sorted by (distance, list id)); k > kMaxK an exact query-major pass over the probed
+// lists whose per-query S x 32R survivors [S][B][32R] the shard merge reduces to the top-k.
+size_t select_all_scratch_bytes(long long Bsub, int nlist);
+long long select_all_batch(int nlist);
+cudaError_t launch_select_all(const float* Q, const float* C, long long B, int nlist, int d, int nprobe, int* probes,
+                              unsigned* bitmap, int W, void* scratch, size_t scratch_bytes, cudaStream_t s);
+struct WideParams {
+  const float* queries;
+  const int* probes;  // B x nprobe
+  int nprobe;
+  const long long* list_off;
+  const float* const* list_base;
+  const long long* res_row0;
+  const __nv_bfloat16* x12;
+  const __nv_bfloat16* x3;
+  const long long* ids;
+  int d, k;
+  long long B;
+  float* out_d;       // S x B x 32R
+  long long* out_id;
+  int* qthr;          // B: running per-query threshold (f2ord), huge on entry
+};
+int wide_lists(int k);
+int wide_splits(long long B, int nprobe, int k, int num_sms);
+cudaError_t launch_wide(const WideParams& p, int S, cudaStream_t s);
+
 // [G][B][k] shard results -> [B][k] (device), any k with G * k <= shard_merge_max_candidates()
 cudaError_t launch_shard_merge(int G, long long B, int k, const long long* ids, const float* dists,
                                long long* out_ids, float* out_dists, cudaStream_t s);
 int shard_merge_max_candidates();
 // the same with shard g's B x k ids at ids + g * ids_stride bytes and distances at dists + g * d_stride
+// (kout: results per query written, <= G * k; 0 = k)
 cudaError_t launch_shard_merge_strided(int G, long long B, int k, const char* ids, size_t ids_stride,
                                        const char* dists, size_t d_stride, long long* out_ids, float* out_dists,
-                                       cudaStream_t s);
+                                       cudaStream_t s, int kout = 0);
 
 // Index build helpers
 cudaError_t launch_gen_centroids(float* C, int nlist, int d, uint64_t sc, cudaStream_t s);

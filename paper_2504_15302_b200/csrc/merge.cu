@@ -239,7 +239,8 @@ __global__ void shard_merge_kernel(int G, long long B, int k, const long long* _
 __global__ void __launch_bounds__(256) shard_merge_sort_kernel(int G, long long B, int k, int P,
                                                                const char* __restrict__ ids, size_t ids_stride,
                                                                const char* __restrict__ dists, size_t d_stride,
-                                                               long long* __restrict__ oid, float* __restrict__ od) {
+                                                               long long* __restrict__ oid, float* __restrict__ od,
+                                                               int kout) {
   RD_PDL_PROLOGUE();
   extern __shared__ __align__(16) unsigned char sm_raw[];
   long long* sk = reinterpret_cast<long long*>(sm_raw);
@@ -277,10 +278,10 @@ __global__ void __launch_bounds__(256) shard_merge_sort_kernel(int G, long long 
       }
       __syncthreads();
     }
-  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+  for (int i = threadIdx.x; i < kout; i += blockDim.x) {
     const bool ok = i < P && sk[i] != kNoKey;
-    oid[q * k + i] = ok ? sk[i] : -1;
-    od[q * k + i] = ok ? sv[i] : kInf;
+    oid[q * kout + i] = ok ? sk[i] : -1;
+    od[q * kout + i] = ok ? sv[i] : kInf;
   }
 }
 
@@ -393,15 +394,16 @@ int shard_merge_max_candidates() { return 8192; }
 
 cudaError_t launch_shard_merge_strided(int G, long long B, int k, const char* ids, size_t ids_stride,
                                        const char* dists, size_t d_stride, long long* out_ids, float* out_dists,
-                                       cudaStream_t s) {
+                                       cudaStream_t s, int kout) {
   if (B == 0) return cudaSuccess;
+  if (kout <= 0) kout = k;
   const long long tot = (long long)G * k;
   if (G < 1 || k < 1 || tot > shard_merge_max_candidates()) return cudaErrorInvalidValue;
   int P = 1;
   while (P < tot) P <<= 1;
   const size_t smem = (size_t)P * (sizeof(long long) + sizeof(float));
   return launch_k(shard_merge_sort_kernel, dim3((unsigned)B), dim3(256), smem, s, G, B, k, P, ids, ids_stride, dists,
-                  d_stride, out_ids, out_dists);
+                  d_stride, out_ids, out_dists, kout);
 }
 
 }  // namespace rd

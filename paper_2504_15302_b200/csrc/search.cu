@@ -56,10 +56,22 @@ float coarse_gamma(long long B, int d) {
   return !rd::coarse_small((int)B) && d % 64 == 0 ? rd::gamma_bf16x3(d) : rd::gamma_ffma_coarse(d);
 }
 
+constexpr int kMaxWideK = 256;  // the exact large-k pass keeps up to 8 x 32 rows per warp (wide.cu)
+
 void validate_search(const rd_index* h, int nprobe, int k) {
+  (void)h;
   if (nprobe < 1 || k < 1) throw_rd(RD_ERR_INVALID, "search: nprobe >= 1 and k >= 1 required");
-  if (k > rd::kMaxK) throw_rd(RD_ERR_INVALID, "search: k <= %d supported, got %d", rd::kMaxK, k);
-  if (std::min(nprobe, h->nlist) + rd::kCoarseExtra > 512) throw_rd(RD_ERR_INVALID, "search: nprobe <= 480 supported");
+  if (k > kMaxWideK) throw_rd(RD_ERR_INVALID, "search: k <= %d supported, got %d", kMaxWideK, k);
+}
+
+// nprobe beyond the certified selection's candidate buffer: the all-centroid exact selection
+bool select_all_needed(const rd_index* h, int nprobe) { return std::min(nprobe, h->nlist) + rd::kCoarseExtra > 512; }
+
+// the all-centroid selection's scratch (sort keys, values, offsets, CUB temp) for a batch of B
+void* select_all_scratch(rd_index* h, long long B, size_t* bytes) {
+  *bytes = rd::select_all_scratch_bytes(std::min<long long>(B, rd::select_all_batch(h->nlist)), h->nlist);
+  h->ws.sel_scratch.ensure(*bytes);
+  return h->ws.sel_scratch.p;
 }
 
 // Counters of the search whose stat block copy do_search enqueued (mode kSync / kStatsAsync), read
@@ -134,7 +146,11 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   // ||q||^2 and the query split (the tensor-core scan's operand) in one pass; at small batches it
   // rides in a trailing CTA of the GEMV coarse kernel
   const rd::QprepArgs qa{d_q, B, d, w.qnorm.p, d % 64 == 0 ? w.qsplit.p : nullptr, w.fails(), w.part_count.p};
-  if (rd::coarse_small((int)B)) {
+  const bool sel_all = select_all_needed(h, nprobe);  // probes from exact distances to every centroid
+  const bool wide = k > rd::kMaxK;                      // the exact large-k pass instead of scan + rerank
+  if (sel_all) {
+    CK(rd::launch_qprep(qa, s));
+  } else if (rd::coarse_small((int)B)) {
     CK(rd::launch_coarse_small(d_q, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, qa, s));
   } else if (d % 64 == 0) {
     CK(rd::launch_qprep(qa, s));
@@ -145,7 +161,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     CK(rd::launch_coarse(d_q, h->centroids.p, h->cnorm.p, w.Dc.p, (int)B, nl, d, s));
   }
   w.qthr.ensure(B);
-  const bool seed = B <= h->seed_max_b;
+  const bool seed = B <= h->seed_max_b && !sel_all && !wide;
   if (!seed) CK(cudaMemsetAsync(w.qthr.p, 0x7f, sizeof(int) * B, s));  // no threshold: huge
   rd::SelectParams sp{w.Dc.p, d_q, w.qnorm.p, h->centroids.p, w.probes.p, w.fails(), (int)B, nl, nprobe, d, h->cmax,
                       h->d_list_off.p, h->d_res_row0.p, h->arena.p, h->xmax, seed ? w.qthr.p : nullptr, 0};
@@ -161,7 +177,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     CK(cudaMemsetAsync(chain, 0, 8 * n, s));
     sp.dbg = chain;
   }
-  const bool use_bm = rd::plan_uses_bitmap((int)B, nprobe, nl);
+  const bool use_bm = !wide && rd::plan_uses_bitmap((int)B, nprobe, nl);
   if (use_bm) {  // zeroed on (re)allocation or after a search that stopped before its plan
     if (w.bitmap.n < (size_t)nl * W || !w.bitmap_clean) {
       w.bitmap.ensure((size_t)nl * W);
@@ -176,8 +192,47 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   const int m_rerank = std::min(rd::kTopK, k + h->rerank_margin);
   const int thr_rank = std::min(rd::kTopK - 1, m_rerank);
   sp.seed_rows = thr_rank + 1;
-  h->traced("select", s, sp.dbg, [&] { CK(rd::launch_select(sp, h->stage_rows(B), s, h->num_sms)); });
-  launches += rd::coarse_small((int)B) ? 2 : 3;  // (query prep +) coarse + select
+  if (sel_all) {
+    size_t sb = 0;
+    void* scratch = select_all_scratch(h, B, &sb);
+    CK(rd::launch_select_all(d_q, h->centroids.p, B, nl, d, nprobe, w.probes.p, use_bm ? w.bitmap.p : nullptr, W,
+                             scratch, sb, s));
+    launches += 1 + 4 * ((B + rd::select_all_batch(nl) - 1) / rd::select_all_batch(nl));
+  } else {
+    h->traced("select", s, sp.dbg, [&] { CK(rd::launch_select(sp, h->stage_rows(B), s, h->num_sms)); });
+    launches += rd::coarse_small((int)B) ? 2 : 3;  // (query prep +) coarse + select
+  }
+  if (wide) {  // exact query-major pass over the probed lists, then the per-query merge of its splits
+    const int R = rd::wide_lists(k), S = rd::wide_splits(B, nprobe, k, h->num_sms);
+    w.wide_d.ensure((size_t)S * B * 32 * R);
+    w.wide_id.ensure((size_t)S * B * 32 * R);
+    const rd::WideParams wp{d_q, w.probes.p, nprobe, h->d_list_off.p, h->d_list_base.p, h->d_res_row0.p,
+                            h->x12_dev(), h->x3_dev(), h->d_ids.p, d, k, B, w.wide_d.p, w.wide_id.p, w.qthr.p};
+    CK(rd::launch_wide(wp, S, s));
+    const int K = 32 * R;
+    CK(rd::launch_shard_merge_strided(S, B, K, reinterpret_cast<const char*>(w.wide_id.p), (size_t)B * K * 8,
+                                      reinterpret_cast<const char*>(w.wide_d.p), (size_t)B * K * 4, d_ids, d_dists, s,
+                                      k));
+    launches += 2;
+    if (h->stage_events) {
+      CK(cudaEventRecord(e1, s));
+      CK(cudaEventRecord(e2, s));
+    }
+    CK(cudaEventRecord(te[3], s));
+    if (before_sync) before_sync();
+    if (mode != kAsync) {
+      CK(cudaMemcpyAsync(w.h_blk.p, w.blk.p, kStatBytes + result_bytes, cudaMemcpyDeviceToHost, s));
+      h->pend = rd_index::Pending{B, k, 0, launches, h->stage_events, false, e0, e1, e2};
+      if (mode == kSync) {
+        CK(cudaStreamSynchronize(s));
+        if (st) finish_stats(h, st);
+      }
+    } else if (st) {
+      std::memset(st, 0, sizeof *st);
+      st->kernel_launches = launches;
+    }
+    return;
+  }
   rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
                     w.list_ntile.p, w.list_toff.p, w.list_q.p, {w.tiles16.p, w.tiles.p, w.ff_tiles.p}, w.meta(),
                     w.counters(), (int)B, nl, nprobe, pl.R, h->tc_scan() ? h->tc_min_q : 1 << 30, tc_mode,
@@ -571,8 +626,7 @@ int rd_search(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int3
 int rd_probe(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32_t* out_lists) {
   return guarded([&] {
     if (!h || B < 0 || (B > 0 && (!queries || !out_lists))) throw_rd(RD_ERR_INVALID, "probe: invalid arguments");
-    if (nprobe < 1 || std::min(nprobe, h->nlist) + rd::kCoarseExtra > 512)
-      throw_rd(RD_ERR_INVALID, "probe: 1 <= nprobe <= 480 required");
+    if (nprobe < 1) throw_rd(RD_ERR_INVALID, "probe: nprobe >= 1 required");
     if (B == 0) return;
     CK(cudaSetDevice(h->device));
     auto& w = h->ws;
@@ -584,6 +638,13 @@ int rd_probe(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32
     w.ensure_blk(kStatBytes);
     CK(cudaMemcpy(w.q.p, queries, sizeof(float) * B * d, cudaMemcpyHostToDevice));
     CK(cudaMemset(w.fails(), 0, 2 * sizeof(unsigned)));
+    if (rdh::select_all_needed(h, nprobe)) {  // large nprobe: already in exact order
+      size_t sb = 0;
+      void* scratch = rdh::select_all_scratch(h, B, &sb);
+      CK(rd::launch_select_all(w.q.p, h->centroids.p, B, nl, d, nprobe, w.probes.p, nullptr, 0, scratch, sb, 0));
+      CK(cudaMemcpy(out_lists, w.probes.p, sizeof(int) * B * nprobe, cudaMemcpyDeviceToHost));
+      return;
+    }
     w.qsplit.ensure((size_t)B * d);
     const rd::QprepArgs qa{w.q.p, B, d, w.qnorm.p, d % 64 == 0 ? w.qsplit.p : nullptr, nullptr, nullptr};
     if (rd::coarse_small((int)B)) {
