@@ -33,6 +33,9 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <condition_variable>
+#include <exception>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -307,6 +310,91 @@ struct VArena {
   }
 };
 
+// ------------------------------------------------------------------ stream memory operations
+// cuStreamWaitValue32 / cuStreamWriteValue32 (driver API, bound at run time): an asynchronous search
+// with offloaded lists gates the caller's stream on a device word that a host worker releases once
+// it has enqueued the offloaded part (search.cu).
+struct StreamMemApi {
+  CUresult (*wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+  CUresult (*write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+};
+const StreamMemApi& stream_mem() {
+  static StreamMemApi api = [] {
+    StreamMemApi a;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      a.wait32 = reinterpret_cast<decltype(a.wait32)>(p);
+    p = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      a.write32 = reinterpret_cast<decltype(a.write32)>(p);
+    return a;
+  }();
+  return api;
+}
+
+// One host thread that runs posted jobs one at a time (an asynchronous search's offloaded part).
+// wait() blocks until the last job finished and rethrows its error.
+class TailWorker {
+ public:
+  TailWorker() : th_([this] { loop(); }) {}
+  ~TailWorker() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      quit_ = true;
+    }
+    cv_.notify_all();
+    th_.join();
+  }
+  void post(std::function<void()> f) {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return !busy_; });
+    job_ = std::move(f);
+    busy_ = true;
+    cv_.notify_all();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return !busy_; });
+    if (err_) {
+      std::exception_ptr e = err_;
+      err_ = nullptr;
+      std::rethrow_exception(e);
+    }
+  }
+
+ private:
+  void loop() {
+    std::unique_lock<std::mutex> lk(mu_);
+    for (;;) {
+      cv_.wait(lk, [&] { return quit_ || (busy_ && job_); });
+      if (quit_ && !busy_) return;
+      auto f = std::move(job_);
+      job_ = nullptr;
+      lk.unlock();
+      std::exception_ptr e;
+      try {
+        f();
+      } catch (...) {
+        e = std::current_exception();
+      }
+      lk.lock();
+      if (e && !err_) err_ = e;
+      busy_ = false;
+      cv_.notify_all();
+      if (quit_) return;
+    }
+  }
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::function<void()> job_;
+  bool busy_ = false, quit_ = false;
+  std::exception_ptr err_;
+  std::thread th_;
+};
+
 // ------------------------------------------------------------------ tensor maps
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -556,7 +644,24 @@ struct rd_index {
   }
   std::vector<cudaEvent_t> slot_ready, slot_done;
 
+  // asynchronous searches with offloaded lists (search.cu): the caller's stream waits on gate >= seq
+  // until the tail worker has enqueued the offloaded part and the merge
+  DBuf<unsigned> gate;
+  unsigned gate_seq = 0;
+  std::unique_ptr<TailWorker> tailw;
+  // every entry point that touches the index first lets a pending tail finish enqueueing
+  void tail_wait() {
+    if (tailw) tailw->wait();
+  }
+
   ~rd_index() {
+    if (tailw) {
+      try {
+        tailw->wait();
+      } catch (...) {
+      }
+      tailw.reset();
+    }
     cudaSetDevice(device);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (off_stream) cudaStreamDestroy(off_stream);

@@ -313,6 +313,8 @@ int rd_index_save(const rd_index* h, const char* path) {
   return guarded([&] {
     if (!h || !path) throw_rd(RD_ERR_INVALID, "save: null argument");
     CK(cudaSetDevice(h->device));
+    const_cast<rd_index*>(h)->tail_wait();
+    CK(cudaDeviceSynchronize());
     rd_file_header hd;
     rd_fmt_layout(&hd, h->n, h->d, h->nlist);
     hd.check = rd_fmt_check(&hd, reinterpret_cast<const int64_t*>(h->list_off.data()));
@@ -605,6 +607,7 @@ int rd_index_place(rd_index* h, const rd_placement* p) {
   return guarded([&] {
     if (!h || !p) throw_rd(RD_ERR_INVALID, "null argument");
     CK(cudaSetDevice(h->device));
+    h->tail_wait();
     CK(cudaDeviceSynchronize());  // searches enqueued with rd_search_device read the store
     const int nl = h->nlist;
     const uint64_t budget0 = p->hbm_budget_bytes;
@@ -770,6 +773,7 @@ int rd_index_migrate(rd_index* h, const int32_t* promote, int32_t n_promote, con
       if (max_off >= 0)
         slots = (int)std::max<uint64_t>(2, std::min<uint64_t>(slots, (hbm_budget_bytes - res_bytes) / slot_bytes));
     }
+    h->tail_wait();
     CK(cudaDeviceSynchronize());  // searches enqueued with rd_search_device read the store
     rd_migration_stats ms;
     std::memset(&ms, 0, sizeof ms);

@@ -112,6 +112,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
                const std::function<void()>& before_sync) {
   validate_search(h, nprobe, k);
   CK(cudaSetDevice(h->device));
+  h->tail_wait();  // the previous asynchronous search's tail is enqueued (it shares the workspace)
   auto& w = h->ws;
   const int nl = h->nlist, d = h->d;
   const Plan pl = make_plan(h, B, nprobe);
@@ -328,187 +329,227 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   }
   if (staged) CK(cudaEventRecord(e2, s));
 
-  unsigned long long h2d = 0;
-  if (has_off) {
-    CK(cudaEventSynchronize(e_plan));
-    // offloaded, probed lists in ascending id, packed into staging slots
-    std::vector<std::vector<int>> batches;
-    long long fill = 0;
-    for (int l = 0; l < nl; ++l) {
-      if (h->resident[l] || w.h_nq.p[l] == 0) continue;
-      const long long len = h->list_off[l + 1] - h->list_off[l];
-      if (len == 0) continue;
-      if (batches.empty() || fill + len > h->slot_rows) {
-        batches.emplace_back();
-        fill = 0;
-      }
-      batches.back().push_back(l);
-      fill += len;
-    }
-    // host-planned tiles of every batch (tensor-core and FFMA groups), uploaded once
-    const size_t nb = batches.size();
-    std::vector<rd::ScanTile> tv;  // per batch: [tc tiles][ff tiles]
-    std::vector<int> tstart(nb + 1, 0), ntc(nb, 0);
-    for (size_t bi = 0; bi < nb; ++bi) {
-      tstart[bi] = (int)tv.size();
-      std::vector<rd::ScanTile> ff;
-      long long srow = (long long)(bi % h->slots) * h->slot_rows;
-      for (int l : batches[bi]) {
+  // The tail: offloaded lists (host-planned staging copies and scans on the side streams), then the
+  // merge + exact rerank and the fallback on stream ms. ms = s runs it inline; an asynchronous search
+  // with offloaded lists runs it on a host worker with ms = off_stream, while s waits on the gate.
+  cudaEvent_t te3 = te[3], e_res = h->ev[6];
+  auto tail = [=, &w](cudaStream_t ms, unsigned long long& launches) -> unsigned long long {
+    unsigned long long h2d = 0;
+    if (has_off) {
+      CK(cudaEventSynchronize(e_plan));
+      // offloaded, probed lists in ascending id, packed into staging slots
+      std::vector<std::vector<int>> batches;
+      long long fill = 0;
+      for (int l = 0; l < nl; ++l) {
+        if (h->resident[l] || w.h_nq.p[l] == 0) continue;
         const long long len = h->list_off[l + 1] - h->list_off[l];
-        const int nq = w.h_nq.p[l];
-        const bool tcl = nq >= h->tc_min_q && h->tc_scan();
-        const int ngr = tcl ? (nq + tc_g - 1) / tc_g : (nq + rd::kScanG - 1) / rd::kScanG;
-        const int rl = rd::chunk_rows(len, pl.R);
-        for (long long c = 0; c * rl < len; ++c)
-          for (int g = 0; g < ngr; ++g) {
-            rd::ScanTile T;
-            T.src_row = srow + c * rl;
-            T.grow0 = h->list_off[l] + c * rl;
-            T.list = l;
-            T.nrows = (int)std::min<long long>(rl, len - c * rl);
-            if (tcl) {
-              const int q0 = (int)((long long)g * nq / ngr), q1 = (int)((long long)(g + 1) * nq / ngr);
-              T.qoff = w.h_qoff.p[l] + q0;
-              T.nq = q1 - q0;
-              tv.push_back(T);
-            } else {
-              T.qoff = w.h_qoff.p[l] + g * rd::kScanG;
-              T.nq = std::min(rd::kScanG, nq - g * rd::kScanG);
-              ff.push_back(T);
-            }
-          }
-        srow += len;
+        if (len == 0) continue;
+        if (batches.empty() || fill + len > h->slot_rows) {
+          batches.emplace_back();
+          fill = 0;
+        }
+        batches.back().push_back(l);
+        fill += len;
       }
-      ntc[bi] = (int)tv.size() - tstart[bi];
-      tv.insert(tv.end(), ff.begin(), ff.end());
-    }
-    tstart[nb] = (int)tv.size();
-    if (nb) {
-      w.h_tiles.ensure(tv.size());
-      std::memcpy(w.h_tiles.p, tv.data(), sizeof(rd::ScanTile) * tv.size());
-      w.off_tiles.ensure(tv.size());
-      w.h_meta.ensure(4 * nb);
+      // host-planned tiles of every batch (tensor-core and FFMA groups), uploaded once
+      const size_t nb = batches.size();
+      std::vector<rd::ScanTile> tv;  // per batch: [tc tiles][ff tiles]
+      std::vector<int> tstart(nb + 1, 0), ntc(nb, 0);
       for (size_t bi = 0; bi < nb; ++bi) {
-        w.h_meta.p[4 * bi + 0] = ntc[bi];
-        w.h_meta.p[4 * bi + 1] = 0;
-        w.h_meta.p[4 * bi + 2] = tstart[bi + 1] - tstart[bi] - ntc[bi];
-        w.h_meta.p[4 * bi + 3] = 0;
-      }
-      DBuf<int>& dmeta = w.off_meta;
-      dmeta.ensure(4 * nb);
-      CK(cudaStreamWaitEvent(h->off_stream, e_plan, 0));
-      CK(cudaMemcpyAsync(w.off_tiles.p, w.h_tiles.p, sizeof(rd::ScanTile) * tv.size(), cudaMemcpyHostToDevice,
-                         h->off_stream));
-      CK(cudaMemcpyAsync(dmeta.p, w.h_meta.p, sizeof(int) * 4 * nb, cudaMemcpyHostToDevice, h->off_stream));
-      CK(cudaEventRecord(e3, h->off_stream));
-      CK(cudaStreamWaitEvent(h->copy_stream, e_plan, 0));
-      for (size_t bi = 0; bi < nb; ++bi) {
-        const int slot = (int)(bi % h->slots);
-        if (bi >= (size_t)h->slots) CK(cudaStreamWaitEvent(h->copy_stream, h->slot_done[slot], 0));
-        long long srow = (long long)slot * h->slot_rows;
-        // lists adjacent in the host arena (and so in the slot) go out as one copy: fewer, larger
-        // DMAs keep the host link closer to its peak than one copy per list
-        long long run_src = -1, run_dst = 0, run_rows = 0;
-        auto flush = [&] {
-          if (run_rows == 0) return;
-          const size_t bytes = (size_t)run_rows * d * sizeof(float);
-          CK(cudaMemcpyAsync(h->staging.p + (size_t)run_dst * d, h->host_arena.p + (size_t)run_src * d, bytes,
-                             cudaMemcpyHostToDevice, h->copy_stream));
-          h2d += bytes;
-          run_rows = 0;
-        };
+        tstart[bi] = (int)tv.size();
+        std::vector<rd::ScanTile> ff;
+        long long srow = (long long)(bi % h->slots) * h->slot_rows;
         for (int l : batches[bi]) {
           const long long len = h->list_off[l + 1] - h->list_off[l];
-          if (run_rows && h->host_row0[l] != run_src + run_rows) flush();
-          if (run_rows == 0) {
-            run_src = h->host_row0[l];
-            run_dst = srow;
-          }
-          run_rows += len;
+          const int nq = w.h_nq.p[l];
+          const bool tcl = nq >= h->tc_min_q && h->tc_scan();
+          const int ngr = tcl ? (nq + tc_g - 1) / tc_g : (nq + rd::kScanG - 1) / rd::kScanG;
+          const int rl = rd::chunk_rows(len, pl.R);
+          for (long long c = 0; c * rl < len; ++c)
+            for (int g = 0; g < ngr; ++g) {
+              rd::ScanTile T;
+              T.src_row = srow + c * rl;
+              T.grow0 = h->list_off[l] + c * rl;
+              T.list = l;
+              T.nrows = (int)std::min<long long>(rl, len - c * rl);
+              if (tcl) {
+                const int q0 = (int)((long long)g * nq / ngr), q1 = (int)((long long)(g + 1) * nq / ngr);
+                T.qoff = w.h_qoff.p[l] + q0;
+                T.nq = q1 - q0;
+                tv.push_back(T);
+              } else {
+                T.qoff = w.h_qoff.p[l] + g * rd::kScanG;
+                T.nq = std::min(rd::kScanG, nq - g * rd::kScanG);
+                ff.push_back(T);
+              }
+            }
           srow += len;
         }
-        flush();
-        CK(cudaEventRecord(h->slot_ready[slot], h->copy_stream));
-        CK(cudaStreamWaitEvent(h->off_stream, h->slot_ready[slot], 0));
-        const int nt_tc = ntc[bi], nt_ff = tstart[bi + 1] - tstart[bi] - ntc[bi];
-        if (nt_ff) {
-          rd::ScanParams so = sc;
-          so.tiles = w.off_tiles.p + tstart[bi] + nt_tc;
-          so.ntiles = dmeta.p + 4 * bi + 2;
-          so.tile_counter = dmeta.p + 4 * bi + 3;
-          CK(rd::launch_scan(h->smap256, h->smap32, so, std::min(h->num_sms, nt_ff), h->off_stream));
-          launches += 1;
-        }
-        if (nt_tc) {
-          rd::TcScanParams to = tc;
-          to.tiles = w.off_tiles.p + tstart[bi];
-          to.ntiles = dmeta.p + 4 * bi + 0;
-          to.tile_counter = dmeta.p + 4 * bi + 1;
-          CK(rd::launch_scan_tc(h->smap128, h->smap32, gmap, to, std::min(h->num_sms, nt_tc), h->off_stream, false,
-                                tc_g));
-          launches += 1;
-        }
-        CK(cudaEventRecord(h->slot_done[slot], h->off_stream));
+        ntc[bi] = (int)tv.size() - tstart[bi];
+        tv.insert(tv.end(), ff.begin(), ff.end());
       }
+      tstart[nb] = (int)tv.size();
+      if (nb) {
+        w.h_tiles.ensure(tv.size());
+        std::memcpy(w.h_tiles.p, tv.data(), sizeof(rd::ScanTile) * tv.size());
+        w.off_tiles.ensure(tv.size());
+        w.h_meta.ensure(4 * nb);
+        for (size_t bi = 0; bi < nb; ++bi) {
+          w.h_meta.p[4 * bi + 0] = ntc[bi];
+          w.h_meta.p[4 * bi + 1] = 0;
+          w.h_meta.p[4 * bi + 2] = tstart[bi + 1] - tstart[bi] - ntc[bi];
+          w.h_meta.p[4 * bi + 3] = 0;
+        }
+        DBuf<int>& dmeta = w.off_meta;
+        dmeta.ensure(4 * nb);
+        CK(cudaStreamWaitEvent(h->off_stream, e_plan, 0));
+        CK(cudaMemcpyAsync(w.off_tiles.p, w.h_tiles.p, sizeof(rd::ScanTile) * tv.size(), cudaMemcpyHostToDevice,
+                           h->off_stream));
+        CK(cudaMemcpyAsync(dmeta.p, w.h_meta.p, sizeof(int) * 4 * nb, cudaMemcpyHostToDevice, h->off_stream));
+        CK(cudaEventRecord(e3, h->off_stream));
+        CK(cudaStreamWaitEvent(h->copy_stream, e_plan, 0));
+        for (size_t bi = 0; bi < nb; ++bi) {
+          const int slot = (int)(bi % h->slots);
+          if (bi >= (size_t)h->slots) CK(cudaStreamWaitEvent(h->copy_stream, h->slot_done[slot], 0));
+          long long srow = (long long)slot * h->slot_rows;
+          // lists adjacent in the host arena (and so in the slot) go out as one copy: fewer, larger
+          // DMAs keep the host link closer to its peak than one copy per list
+          long long run_src = -1, run_dst = 0, run_rows = 0;
+          auto flush = [&] {
+            if (run_rows == 0) return;
+            const size_t bytes = (size_t)run_rows * d * sizeof(float);
+            CK(cudaMemcpyAsync(h->staging.p + (size_t)run_dst * d, h->host_arena.p + (size_t)run_src * d, bytes,
+                               cudaMemcpyHostToDevice, h->copy_stream));
+            h2d += bytes;
+            run_rows = 0;
+          };
+          for (int l : batches[bi]) {
+            const long long len = h->list_off[l + 1] - h->list_off[l];
+            if (run_rows && h->host_row0[l] != run_src + run_rows) flush();
+            if (run_rows == 0) {
+              run_src = h->host_row0[l];
+              run_dst = srow;
+            }
+            run_rows += len;
+            srow += len;
+          }
+          flush();
+          CK(cudaEventRecord(h->slot_ready[slot], h->copy_stream));
+          CK(cudaStreamWaitEvent(h->off_stream, h->slot_ready[slot], 0));
+          const int nt_tc = ntc[bi], nt_ff = tstart[bi + 1] - tstart[bi] - ntc[bi];
+          if (nt_ff) {
+            rd::ScanParams so = sc;
+            so.tiles = w.off_tiles.p + tstart[bi] + nt_tc;
+            so.ntiles = dmeta.p + 4 * bi + 2;
+            so.tile_counter = dmeta.p + 4 * bi + 3;
+            CK(rd::launch_scan(h->smap256, h->smap32, so, std::min(h->num_sms, nt_ff), h->off_stream));
+            launches += 1;
+          }
+          if (nt_tc) {
+            rd::TcScanParams to = tc;
+            to.tiles = w.off_tiles.p + tstart[bi];
+            to.ntiles = dmeta.p + 4 * bi + 0;
+            to.tile_counter = dmeta.p + 4 * bi + 1;
+            CK(rd::launch_scan_tc(h->smap128, h->smap32, gmap, to, std::min(h->num_sms, nt_tc), h->off_stream, false,
+                                  tc_g));
+            launches += 1;
+          }
+          CK(cudaEventRecord(h->slot_done[slot], h->off_stream));
+        }
+      }
+      CK(cudaEventRecord(e_off, h->off_stream));
+      CK(cudaStreamWaitEvent(ms, e_off, 0));
     }
-    CK(cudaEventRecord(e_off, h->off_stream));
-    CK(cudaStreamWaitEvent(s, e_off, 0));
-  }
+    if (ms != s) CK(cudaStreamWaitEvent(ms, e_res, 0));  // the resident scan, on the caller's stream
 
-  if (!w.fb_ctr.p) {  // the fallback kernel's completion counter: zeroed once, re-armed by the kernel
-    w.fb_ctr.alloc(1);
-    CK(cudaMemset(w.fb_ctr.p, 0, sizeof(unsigned)));
-  }
-  w.fail_list.ensure(B);
-  w.fb_dist.ensure((size_t)B * nprobe * rd::kTopK);
-  w.fb_id.ensure((size_t)B * nprobe * rd::kTopK);
-  rd::MergeParams mp{w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d_q, w.qnorm.p, h->d_list_off.p,
-                     h->d_list_base.p, h->d_ids.p, h->d_row_list.p, h->arena.p,
-                     h->arena.p ? h->arena.p + (size_t)h->n_resident * d : nullptr, nl, d, k, h->xmax, d_ids, d_dists,
-                     w.fails() + 1, w.fail_list.p, (int)B};
-  mp.m_rerank = m_rerank;
-  mp.gamma = h->scan_gamma();
-  mp.res_row0 = h->d_res_row0.p;
-  mp.x12 = h->x12_dev();
-  mp.x3 = h->x3_dev();
-  if (chain) mp.dbg = chain + 64;
-  h->traced("merge", s, mp.dbg, [&] { CK(rd::launch_merge(mp, h->stage_rows(B), s)); });
-  rd::FallbackParams fp{w.fail_list.p, w.fails() + 1, w.probes.p, nprobe, d_q, h->d_list_off.p, h->d_list_base.p,
-                        h->d_ids.p, nl, d, k, w.fb_dist.p, w.fb_id.p, d_ids, d_dists, w.fb_ctr.p};
-  fp.res_row0 = h->d_res_row0.p;
-  fp.x12 = h->x12_dev();
-  fp.x3 = h->x3_dev();
-  CK(rd::launch_fallback(fp, h->num_sms, s));
-  launches += 2;
-  CK(cudaEventRecord(te[3], s));
-  if (chain) {  // ns from select's entry: [13] = entry (before the PDL wait), [0] = past the wait
-    std::vector<unsigned long long> t(96 + 4 * (size_t)h->num_sms);
-    CK(cudaMemcpyAsync(t.data(), chain, 8 * t.size(), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    const long long t0 = (long long)t[13];
-    const char* nm[3] = {"select", "plan", "merge"};
-    for (int kk = 0; kk < 3; ++kk) {
-      fprintf(stderr, "%s:", nm[kk]);
-      if (t[32 * kk + 13]) fprintf(stderr, " entry=%lld", (long long)t[32 * kk + 13] - t0);
-      for (int i = 0; i < 13; ++i)
-        if (t[32 * kk + i]) fprintf(stderr, " %d=%lld", i, (long long)t[32 * kk + i] - t0);
-      fprintf(stderr, "\n");
+    if (!w.fb_ctr.p) {  // the fallback kernel's completion counter: zeroed once, re-armed by the kernel
+      w.fb_ctr.alloc(1);
+      CK(cudaMemset(w.fb_ctr.p, 0, sizeof(unsigned)));
     }
-    long long mn[4], mx[4];
-    double mean[4];
-    for (int j = 0; j < 4; ++j) {
-      mn[j] = 1LL << 62, mx[j] = -(1LL << 62), mean[j] = 0;
-      int cnt = 0;
-      for (int c = 0; c < h->num_sms; ++c) {
-        const unsigned long long v = t[96 + 4 * c + j];
-        if (!v) continue;
-        const long long r = (long long)v - t0;
-        mn[j] = std::min(mn[j], r), mx[j] = std::max(mx[j], r), mean[j] += r, ++cnt;
+    w.fail_list.ensure(B);
+    w.fb_dist.ensure((size_t)B * nprobe * rd::kTopK);
+    w.fb_id.ensure((size_t)B * nprobe * rd::kTopK);
+    rd::MergeParams mp{w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d_q, w.qnorm.p, h->d_list_off.p,
+                       h->d_list_base.p, h->d_ids.p, h->d_row_list.p, h->arena.p,
+                       h->arena.p ? h->arena.p + (size_t)h->n_resident * d : nullptr, nl, d, k, h->xmax, d_ids, d_dists,
+                       w.fails() + 1, w.fail_list.p, (int)B};
+    mp.m_rerank = m_rerank;
+    mp.gamma = h->scan_gamma();
+    mp.res_row0 = h->d_res_row0.p;
+    mp.x12 = h->x12_dev();
+    mp.x3 = h->x3_dev();
+    if (chain) mp.dbg = chain + 64;
+    h->traced("merge", ms, mp.dbg, [&] { CK(rd::launch_merge(mp, h->stage_rows(B), ms)); });
+    rd::FallbackParams fp{w.fail_list.p, w.fails() + 1, w.probes.p, nprobe, d_q, h->d_list_off.p, h->d_list_base.p,
+                          h->d_ids.p, nl, d, k, w.fb_dist.p, w.fb_id.p, d_ids, d_dists, w.fb_ctr.p};
+    fp.res_row0 = h->d_res_row0.p;
+    fp.x12 = h->x12_dev();
+    fp.x3 = h->x3_dev();
+    CK(rd::launch_fallback(fp, h->num_sms, ms));
+    launches += 2;
+    CK(cudaEventRecord(te3, ms));
+    if (chain) {  // ns from select's entry: [13] = entry (before the PDL wait), [0] = past the wait
+      std::vector<unsigned long long> t(96 + 4 * (size_t)h->num_sms);
+      CK(cudaMemcpyAsync(t.data(), chain, 8 * t.size(), cudaMemcpyDeviceToHost, ms));
+      CK(cudaStreamSynchronize(ms));
+      const long long t0 = (long long)t[13];
+      const char* nm[3] = {"select", "plan", "merge"};
+      for (int kk = 0; kk < 3; ++kk) {
+        fprintf(stderr, "%s:", nm[kk]);
+        if (t[32 * kk + 13]) fprintf(stderr, " entry=%lld", (long long)t[32 * kk + 13] - t0);
+        for (int i = 0; i < 13; ++i)
+          if (t[32 * kk + i]) fprintf(stderr, " %d=%lld", i, (long long)t[32 * kk + i] - t0);
+        fprintf(stderr, "\n");
       }
-      if (cnt) mean[j] /= cnt;
+      long long mn[4], mx[4];
+      double mean[4];
+      for (int j = 0; j < 4; ++j) {
+        mn[j] = 1LL << 62, mx[j] = -(1LL << 62), mean[j] = 0;
+        int cnt = 0;
+        for (int c = 0; c < h->num_sms; ++c) {
+          const unsigned long long v = t[96 + 4 * c + j];
+          if (!v) continue;
+          const long long r = (long long)v - t0;
+          mn[j] = std::min(mn[j], r), mx[j] = std::max(mx[j], r), mean[j] += r, ++cnt;
+        }
+        if (cnt) mean[j] /= cnt;
+      }
+      fprintf(stderr, "scan: entry %lld/%.0f/%lld ready %lld/%.0f/%lld first %lld/%.0f/%lld end %lld/%.0f/%lld (min/mean/max)\n",
+              mn[0], mean[0], mx[0], mn[1], mean[1], mx[1], mn[2], mean[2], mx[2], mn[3], mean[3], mx[3]);
     }
-    fprintf(stderr, "scan: entry %lld/%.0f/%lld ready %lld/%.0f/%lld first %lld/%.0f/%lld end %lld/%.0f/%lld (min/mean/max)\n",
-            mn[0], mean[0], mx[0], mn[1], mean[1], mx[1], mn[2], mean[2], mx[2], mn[3], mean[3], mx[3]);
+    return h2d;
+  };
+  unsigned long long h2d = 0;
+  const bool async_tail = has_off && mode == kAsync && !chain && stream_mem().wait32 && stream_mem().write32;
+  if (!async_tail) {
+    h2d = tail(s, launches);
+  } else {
+    // rd_search_device's contract: return once enqueued. The caller's stream s waits on gate >= seq;
+    // the worker waits for the plan, enqueues the offloaded part, the merge and the fallback on the
+    // side streams, then releases the gate from off_stream.
+    CK(cudaEventRecord(e_res, s));
+    if (!h->gate.p) {
+      h->gate.alloc(1);
+      CK(cudaMemset(h->gate.p, 0, sizeof(unsigned)));
+    }
+    if (!h->tailw) h->tailw = std::make_unique<TailWorker>();
+    const unsigned seq = ++h->gate_seq;
+    const CUdeviceptr gate = reinterpret_cast<CUdeviceptr>(h->gate.p);
+    const CUresult r = stream_mem().wait32((CUstream)s, gate, seq, CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) throw_rd(RD_ERR_RUNTIME, "cuStreamWaitValue32 failed (%d)", (int)r);
+    h->tailw->post([=]() mutable {
+      unsigned long long n = 0;
+      std::exception_ptr err;
+      try {
+        CK(cudaSetDevice(h->device));
+        tail(h->off_stream, n);
+      } catch (...) {
+        err = std::current_exception();
+      }
+      // released even after a failure, so the caller's stream never waits forever
+      stream_mem().write32((CUstream)h->off_stream, gate, seq, 0);
+      if (err) std::rethrow_exception(err);
+    });
   }
   if (before_sync) before_sync();  // e.g. the host path's result copies, ordered before the one sync
   if (mode != kAsync) {
@@ -629,6 +670,7 @@ int rd_probe(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32
     if (nprobe < 1) throw_rd(RD_ERR_INVALID, "probe: nprobe >= 1 required");
     if (B == 0) return;
     CK(cudaSetDevice(h->device));
+    h->tail_wait();
     auto& w = h->ws;
     const int nl = h->nlist, d = h->d;
     w.q.ensure((size_t)B * d);
@@ -676,6 +718,7 @@ int rd_timing_reset(rd_index* h) {
   return guarded([&] {
     if (!h) throw_rd(RD_ERR_INVALID, "null index");
     CK(cudaSetDevice(h->device));
+    h->tail_wait();
     while (h->t_accounted < h->t_recorded) {  // drain so the ring's events are free again
       CK(cudaEventSynchronize(h->tev[h->t_accounted % rd_index::kRing][3]));
       ++h->t_accounted;
@@ -688,6 +731,7 @@ int rd_timing_read(rd_index* h, rd_timing* out) {
   return guarded([&] {
     if (!h || !out) throw_rd(RD_ERR_INVALID, "null argument");
     CK(cudaSetDevice(h->device));
+    h->tail_wait();
     while (h->t_accounted < h->t_recorded) h->account(h->t_accounted++);
     *out = h->t_acc;
   });

@@ -65,7 +65,7 @@ def test_empty_batch_and_scaled_data(engine, oracle):
 def test_engine_argument_validation(engine):
     idx = engine.synthetic_index(engine.desc(2000, 64, 8))
     q = np.zeros((2, 64), np.float32)
-    for nprobe, k in [(0, 10), (4, 0), (4, 25)]:  # k <= 24 keeps >= 8 candidates of certification margin
+    for nprobe, k in [(0, 10), (4, 0), (4, 257)]:  # k <= 256: the exact large-k pass's widest lists
         with pytest.raises(ParseError):
             idx.search(q, nprobe, k)
     with pytest.raises(ParseError):
@@ -99,3 +99,40 @@ def test_probe_set_boundary_ties(engine, oracle, nprobe):
     o = oracle.index_from_host(X, offs, C)
     np.testing.assert_array_equal(e.probe(Q, nprobe), o.probe(Q, nprobe))
     _same(e.search(Q, nprobe, 10), o.search(Q, nprobe, 10))
+
+
+def test_async_search_with_offloaded_lists(engine, oracle):
+    """rd_search_device stays asynchronous with offloaded lists (rd.h): it returns once the search is
+    enqueued — the offloaded part is planned and enqueued by the index's worker thread while the
+    caller's stream waits on a device gate — and the results are the oracle's."""
+    import time
+    import torch
+    desc = engine.desc(600000, 768, 256)
+    q, _ = engine.synth_queries(desc, 12, 64)
+    want = oracle.synthetic_index(desc).search(q, 32, 10)
+    e = engine.synthetic_index(desc)
+    e.place(offload_fraction=0.5)
+    dq = torch.from_numpy(q).cuda()
+    stream = torch.cuda.current_stream()
+    outs = []
+    for rep in range(3):  # back to back on one stream: each tail waits for the previous one
+        di = torch.full((64, 10), -7, dtype=torch.int64, device="cuda")
+        dd = torch.empty((64, 10), dtype=torch.float32, device="cuda")
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        t0 = time.perf_counter()
+        e.search_device(dq.data_ptr(), 64, 32, 10, di.data_ptr(), dd.data_ptr(), stream=stream.cuda_stream)
+        host_ms = (time.perf_counter() - t0) * 1e3
+        ev1.record(stream)
+        pending = not ev1.query()
+        torch.cuda.synchronize()
+        dev_ms = ev0.elapsed_time(ev1)
+        outs.append((di.cpu().numpy(), dd.cpu().numpy(), host_ms, dev_ms, pending))
+    for ids, dists, host_ms, dev_ms, pending in outs:
+        np.testing.assert_array_equal(ids, want.ids)
+        np.testing.assert_array_equal(dists, want.dists)
+    # the call returned before the search completed (device work still pending, host time a fraction)
+    assert any(p for *_, p in outs)
+    assert min(h / dv for _, _, h, dv, _ in outs) < 0.5, [(h, dv) for _, _, h, dv, _ in outs]
+    assert e.search(q, 32, 10).stats["h2d_list_bytes"] > 0

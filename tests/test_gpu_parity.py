@@ -132,13 +132,14 @@ def test_device_shard_merge(engine):
     np.testing.assert_array_equal(od.cpu().numpy(), want_d)
 
 
-def test_k_above_limit_rejected(engine):
-    from paper_2504_15302_b200.retriever import ParseError
+def test_k_above_fast_path_is_exact(engine, oracle):
+    # k > 24 leaves the certified fast path for the exact large-k pass (wide.cu): same results
     desc = engine.desc(2000, 64, 8)
-    idx = engine.synthetic_index(desc)
     q, _ = engine.synth_queries(desc, 0, 2)
-    with pytest.raises(ParseError):
-        idx.search(q, 4, 25)
+    e = engine.synthetic_index(desc).search(q, 4, 25)
+    o = oracle.synthetic_index(desc).search(q, 4, 25)
+    np.testing.assert_array_equal(e.ids, o.ids)
+    np.testing.assert_array_equal(e.dists, o.dists)
 
 
 def test_search_device_matches_host_path(engine):
