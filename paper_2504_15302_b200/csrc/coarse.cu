@@ -426,7 +426,12 @@ __global__ void __launch_bounds__(NT) coarse_select_kernel(const SelectParams p)
     }
   if constexpr (kStage) {  // approximate nearest centroid: warm L2 with its list's first 32 rows (the likely seed)
     __syncthreads();
-    if (vmin < __builtin_huge_valf()) atomicMin(&amin, ((unsigned long long)f2key(vmin) << 32) | (unsigned)jmin);
+    // one shared atomic per warp (a 64-bit atomicMin from every thread serialises for microseconds)
+    unsigned long long key = vmin < __builtin_huge_valf() ? ((unsigned long long)f2key(vmin) << 32) | (unsigned)jmin
+                                                          : ~0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, o));
+    if (lane == 0 && key != ~0ull) atomicMin(&amin, key);
   }
   vmin = block_reduce_min<NT>(vmin, fsh);
   vmax = block_reduce_max<NT>(vmax, fsh);
@@ -513,8 +518,15 @@ __global__ void __launch_bounds__(NT) coarse_select_kernel(const SelectParams p)
   if (ncand >= 0) {
     if (tid == 0) ncand_s = 0;
     __syncthreads();
-    for (int j = tid; j < nlist; j += NT)
-      if (vals[j] < hi_edge) cand[atomicAdd(&ncand_s, 1)] = j;
+    for (int j0 = 0; j0 < nlist; j0 += NT) {  // warp-aggregated appends (order is irrelevant: ranked below)
+      const int j = j0 + tid;
+      const bool in = j < nlist && vals[j] < hi_edge;
+      const unsigned m = __ballot_sync(0xffffffffu, in);
+      int base = 0;
+      if (lane == 0 && m) base = atomicAdd(&ncand_s, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (in) cand[base + __popc(m & ((1u << lane) - 1u))] = j;
+    }
     __syncthreads();
   }
   RD_TS(3);
@@ -524,11 +536,13 @@ __global__ void __launch_bounds__(NT) coarse_select_kernel(const SelectParams p)
     if (seed_l >= 0) {
       mbar_wait(&bar, bphase);
       bphase ^= 1;
-      const float e = l2_group8_f32_row(qf, staged_ref(grp), d, j8);  // rows >= seed_rows: stale, masked
+      const float e = d % 64 == 0 ? l2_group8_f32_chunks(qf, staged_ref(grp), d, j8)  // rows >= seed_rows: stale, masked
+                                    : l2_group8_f32_row(qf, staged_ref(grp), d, j8);
       seed_pre = block_reduce_max<NT>(grp < p.seed_rows ? e : 0.f, fsh);
       __syncthreads();  // the staging area is free again
     }
   }
+  RD_TS(4);
 
   const float u = kUnit;
   // |approx - exact| of a coarse distance: the GEMM's dot bound (doubled: d = ... - 2 q.c) plus the
@@ -552,6 +566,7 @@ __global__ void __launch_bounds__(NT) coarse_select_kernel(const SelectParams p)
     }
     if (tid == 0) below_s = 0;
     __syncthreads();
+    RD_TS(10);
     // rank and window counts: one group of 8 lanes per candidate, lane j8 scans k = j8 (mod 8)
     int below = 0;
     for (int i0 = 0; i0 < C; i0 += NT / 8) {
@@ -579,7 +594,9 @@ __global__ void __launch_bounds__(NT) coarse_select_kernel(const SelectParams p)
         below += vi < hi_edge - e2;
       }
     }
-    if (below) atomicAdd(&below_s, below);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
+    if (lane == 0 && below) atomicAdd(&below_s, below);
     __syncthreads();
     RD_TS(7);
     if (warp == 0) {  // ambiguous list in rank order; sure-in count
@@ -763,7 +780,7 @@ __global__ void __launch_bounds__(NT) coarse_select_kernel(const SelectParams p)
           }
           mbar_wait(&bar, bphase);
           bphase ^= 1;
-          e = l2_group8_f32_row(qf, staged_ref(grp), d, j8);
+          e = d % 64 == 0 ? l2_group8_f32_chunks(qf, staged_ref(grp), d, j8) : l2_group8_f32_row(qf, staged_ref(grp), d, j8);
           if (grp >= p.seed_rows) e = 0.f;  // only the first seed_rows rows bound the threshold
         } else {  // NT / 8 rows per pass (a uniform trip count keeps the group shuffles converged)
           for (int rb = 0; rb < p.seed_rows; rb += NT / 8) {

@@ -149,6 +149,32 @@ inline float gamma_ffma_scan(int d) { return 2.f * (d / 2 + 8) * kUnit; }
 inline float gamma_ffma_coarse(int d) { return 2.f * (d + 4) * kUnit; }
 inline float gamma_bf16x3(int d) { return (524.f + 0.7f * d) * kUnit; }
 
+// Scan tile categories (plan.cu): tensor-core tiles of <= 16 queries (16-wide scan), of <= 32
+// queries (32-wide scan), and FFMA tiles.
+constexpr int kTileCats = 3;
+constexpr int kCatNarrow = 0, kCatWide = 1, kCatFfma = 2;
+
+struct PlanParams {
+  const int* probes;          // B x nprobe
+  unsigned* bitmap;           // nlist x W
+  int W;                      // words per list = ceil(B / 32)
+  const long long* list_off;  // nlist + 1 (global rows)
+  const long long* res_row0;  // nlist: row in the resident arena, -1 = offloaded
+  int* list_nq;               // nlist
+  int* list_qoff;             // nlist
+  int* list_ntile;            // kTileCats x nlist: resident tiles per category
+  int* list_toff;             // kTileCats x nlist
+  int* list_q;                // B x nprobe
+  ScanTile* tiles[kTileCats]; // tile arrays per category
+  int* meta;                  // per category c: [2c] #tiles, [2c + 1] the scan's tile counter
+  unsigned long long* counters;  // [0] unique lists, [1] resident rows probed, [2] offloaded rows probed
+  int B, nlist, nprobe, R, tc_min_q;
+  int tc_mode;                // 0: lists of <= 16 queries narrow, others wide; 16 / 32: one width
+  // lists j >= tail_from are cut at Rt (<= R) rows: the scan's dynamic queue hands out tiles in
+  // list order, so its last tiles are the short ones and the CTAs finish closer together
+  int Rt, tail_from;
+  unsigned long long* dbg = nullptr;  // RD_DEBUG_TS: globaltimer checkpoints of CTA 0
+};
 struct SelectParams {
   const float* Dc;         // B x nlist
   const float* queries;    // B x d
@@ -183,10 +209,6 @@ struct SelectParams {
 // num_sms: batches beyond one resident wave of 256-thread CTAs (4 per SM) use 128-thread CTAs
 cudaError_t launch_select(const SelectParams& p, bool stage, cudaStream_t s, int num_sms = 148);
 
-// Scan tile categories (plan.cu): tensor-core tiles of <= 16 queries (16-wide scan), of <= 32
-// queries (32-wide scan), and FFMA tiles.
-constexpr int kTileCats = 3;
-constexpr int kCatNarrow = 0, kCatWide = 1, kCatFfma = 2;
 
 // Rows per scan chunk of a list of `len` rows under the plan's cap R (a multiple of kTcRows): the
 // fewest chunks of <= R rows, balanced and rounded up to the tensor-core tile, so a list is not cut
@@ -200,27 +222,6 @@ __host__ __device__ __forceinline__ int chunk_rows(long long len, int R) {
   return (int)(rr < R ? rr : R);
 }
 
-struct PlanParams {
-  const int* probes;          // B x nprobe
-  unsigned* bitmap;           // nlist x W
-  int W;                      // words per list = ceil(B / 32)
-  const long long* list_off;  // nlist + 1 (global rows)
-  const long long* res_row0;  // nlist: row in the resident arena, -1 = offloaded
-  int* list_nq;               // nlist
-  int* list_qoff;             // nlist
-  int* list_ntile;            // kTileCats x nlist: resident tiles per category
-  int* list_toff;             // kTileCats x nlist
-  int* list_q;                // B x nprobe
-  ScanTile* tiles[kTileCats]; // tile arrays per category
-  int* meta;                  // per category c: [2c] #tiles, [2c + 1] the scan's tile counter
-  unsigned long long* counters;  // [0] unique lists, [1] resident rows probed, [2] offloaded rows probed
-  int B, nlist, nprobe, R, tc_min_q;
-  int tc_mode;                // 0: lists of <= 16 queries narrow, others wide; 16 / 32: one width
-  // lists j >= tail_from are cut at Rt (<= R) rows: the scan's dynamic queue hands out tiles in
-  // list order, so its last tiles are the short ones and the CTAs finish closer together
-  int Rt, tail_from;
-  unsigned long long* dbg = nullptr;  // RD_DEBUG_TS: globaltimer checkpoints of CTA 0
-};
 cudaError_t launch_plan(const PlanParams& p, cudaStream_t s);
 bool plan_fused_ok(int B, int nlist);  // the single-CTA bitmap plan applies
 bool plan_small_ok(int B, int nprobe);  // the single-CTA sorted-pairs plan applies (B * nprobe <= 512)

@@ -15,20 +15,19 @@ namespace rd {
 namespace {
 
 constexpr float kInf = __builtin_huge_valf();
-// floats per staged candidate row: fp32 rows (d) or a split3 row's x12 + x3 (1.5 d)
-__host__ __device__ __forceinline__ int stage_stride(int d, bool split3) {
-  return (split3 ? d + d / 2 : d) + kStagePad;
-}
 constexpr long long kNoKey = 0x7fffffffffffffffll;
+constexpr int kDecodeBatch = 8;  // 8-element row chunks per thread per round trip (staged rerank)
 
-// One CTA per query. kStage (small batches): the 32 candidate rows are staged in shared memory with
-// every load in flight before the canonical sums run; otherwise each group of 8 lanes streams its
-// row from global memory (enough CTAs are resident to hide the latency).
+// One CTA per query. kStage (small batches, one latency chain per query): the candidate rows are
+// decoded into fp32 rows in shared memory (128-bit loads, every load of a round in flight, split3
+// triples summed once per element) and the canonical sums read them with q already widened to fp64;
+// otherwise each group of 8 lanes streams its row from global memory (enough CTAs are resident to
+// hide the latency).
 template <bool kStage>
 __global__ void __launch_bounds__(256, kStage ? 1 : 8) merge_rerank_kernel(const MergeParams p) {
   RD_TS(13);  // entry, before the wait on the previous kernel
   RD_PDL_PROLOGUE();
-  extern __shared__ __align__(16) float dyn[];  // kStage: q[d], rows[32][ds] (ds: stage_stride)
+  extern __shared__ __align__(16) float dyn[];  // kStage: qd[d] (fp64), rows[32][d + kStagePad] (fp32)
   __shared__ float sd[8][kTopK];
   __shared__ long long sk[8][kTopK];
   __shared__ float ex_d[kTopK];
@@ -36,19 +35,17 @@ __global__ void __launch_bounds__(256, kStage ? 1 : 8) merge_rerank_kernel(const
   __shared__ const float* rowp[kTopK];   // fp32 row (offloaded list / fp32 store), or nullptr
   __shared__ long long srow[kTopK];      // split3 store row, or -1
   __shared__ float tau_s;
-  __shared__ unsigned host_rows;  // kStage: candidate rows outside the device arena
-  __shared__ __align__(8) uint64_t bar;
   RD_TS(0);
-  if (kStage && threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    fence_mbar_init();
-  }
   const int b = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cnt = min(p.part_count[b], p.part_cap);
   if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0) p.dbg[15] = (unsigned long long)cnt;
   const float* q = p.queries + (size_t)b * p.d;
+  double* qd = reinterpret_cast<double*>(dyn);
   if constexpr (kStage) {
-    for (int i = tid; i < (p.d >> 2); i += 256) reinterpret_cast<float4*>(dyn)[i] = reinterpret_cast<const float4*>(q)[i];
+    for (int i = tid; i < (p.d >> 2); i += 256) {
+      const float4 v = reinterpret_cast<const float4*>(q)[i];
+      qd[4 * i] = v.x, qd[4 * i + 1] = v.y, qd[4 * i + 2] = v.z, qd[4 * i + 3] = v.w;
+    }
   }
 
   // partial lists are ascending; read reversed to get a descending batch. Four partials per warp
@@ -81,21 +78,27 @@ __global__ void __launch_bounds__(256, kStage ? 1 : 8) merge_rerank_kernel(const
       for (int j = 16; j > 0; j >>= 1) bitonic_step(ld, lk, lane, j, true);
     }
   }
+  // the eight warps' lists: a merge tree (4, 2, 1 warps) into warp 0
   sd[warp][lane] = ld;
   sk[warp][lane] = lk;
   __syncthreads();
-  RD_TS(1);
-  if (warp == 0) {
-    for (int w = 1; w < 8; ++w) {
-      const float v = sd[w][kTopK - 1 - lane];
-      const long long key = sk[w][kTopK - 1 - lane];
+  for (int st = 1; st < 8; st <<= 1) {
+    if ((warp & (2 * st - 1)) == 0) {
+      const float v = sd[warp + st][kTopK - 1 - lane];
+      const long long key = sk[warp + st][kTopK - 1 - lane];
       if (pair_less(v, key, ld, lk)) {
         ld = v;
         lk = key;
       }
 #pragma unroll
       for (int j = 16; j > 0; j >>= 1) bitonic_step(ld, lk, lane, j, true);
+      sd[warp][lane] = ld;
+      sk[warp][lane] = lk;
     }
+    __syncthreads();
+  }
+  RD_TS(1);
+  if (warp == 0) {
     // The best m = min(32, k + margin) candidates are reranked: the (m+1)-th approximate distance
     // bounds every row not reranked (the rest of the list and everything the scan dropped), so
     // certification reads tau = that distance; the spare candidates keep it holding unless the data
@@ -107,34 +110,18 @@ __global__ void __launch_bounds__(256, kStage ? 1 : 8) merge_rerank_kernel(const
     long long id = kNoKey;
     if (lk != kNoKey && lane < m) {  // candidate rows: list of the row (row_list), address, user id
       const int l = __ldg(p.row_list + lk);
+      id = __ldg(p.ids + lk);
       const float* base = p.list_base[l];
       const long long i = lk - __ldg(p.list_off + l);
       if (base)
         xp = base + (size_t)i * p.d;
       else
         sr = __ldg(p.res_row0 + l) + i;
-      id = __ldg(p.ids + lk);
     }
     rowp[lane] = xp;
     srow[lane] = sr;
     ex_id[lane] = id;
     if (lane == min(m, kTopK - 1)) tau_s = ld;
-    if constexpr (kStage) {  // device rows: bulk (TMA) copies, all in flight at once
-      float* st = dyn + p.d;
-      const int ds = stage_stride(p.d, p.x12 != nullptr);
-      const bool dev = xp && xp >= p.arena_lo && xp < p.arena_hi;
-      const unsigned dm = __ballot_sync(0xffffffffu, dev), sm3 = __ballot_sync(0xffffffffu, sr >= 0);
-      if (lane == 0)
-        mbar_arrive_expect_tx(&bar, ((uint32_t)__popc(dm) * 4u + (uint32_t)__popc(sm3) * 6u) * (uint32_t)p.d);
-      const unsigned hm = __ballot_sync(0xffffffffu, xp && !dev);
-      if (lane == 0) host_rows = hm;
-      __syncwarp();
-      if (dev) bulk_g2s(st + lane * ds, xp, (uint32_t)p.d * 4u, &bar);
-      if (sr >= 0) {  // split3 row: x12 (4d bytes) then x3 (2d bytes) in one slot
-        bulk_g2s(st + lane * ds, p.x12 + (size_t)sr * 2 * p.d, (uint32_t)p.d * 4u, &bar);
-        bulk_g2s(st + lane * ds + p.d, p.x3 + (size_t)sr * p.d, (uint32_t)p.d * 2u, &bar);
-      }
-    }
   }
   __syncthreads();
 
@@ -146,25 +133,55 @@ __global__ void __launch_bounds__(256, kStage ? 1 : 8) merge_rerank_kernel(const
   const bool have = xp || sr >= 0;
   float e;
   if constexpr (kStage) {
-    float* st = dyn + p.d;
-    const int ds = stage_stride(p.d, p.x12 != nullptr);
-    const unsigned hm = host_rows;
-    if (hm) {  // rows of offloaded lists (mapped host memory): ordinary loads by every thread
-      const int v4 = p.d >> 2;
-      for (int i = tid; i < kTopK * v4; i += 256) {
-        const int r = i / v4, cc = i - r * v4;
-        if ((hm >> r) & 1u)
-          *reinterpret_cast<float4*>(st + r * ds + 4 * cc) = *reinterpret_cast<const float4*>(rowp[r] + 4 * cc);
+    // decode: task = (row r, 8-element chunk cc) over the m candidate rows; kDecodeBatch tasks per
+    // thread per round, all loads in flight (split3: x1, x2, x3 chunks; fp32: two float4 — rows of
+    // offloaded lists are mapped host memory, so plain loads throughout)
+    float* st = dyn + 2 * p.d;
+    const int ds = p.d + kStagePad, nc = p.d >> 3;
+    const int ntask = min(p.m_rerank, kTopK) * nc;
+    for (int t0 = tid; t0 < ntask; t0 += 256 * kDecodeBatch) {
+      uint4 a[kDecodeBatch], bb[kDecodeBatch], cc3[kDecodeBatch];
+#pragma unroll
+      for (int u = 0; u < kDecodeBatch; ++u) {
+        const int t = t0 + u * 256;
+        if (t >= ntask) break;
+        const int r = t / nc, ch = t - r * nc;
+        const long long rs = srow[r];
+        const float* rp = rowp[r];
+        if (rs >= 0) {
+          a[u] = reinterpret_cast<const uint4*>(p.x12 + (size_t)rs * 2 * p.d)[ch];
+          bb[u] = reinterpret_cast<const uint4*>(p.x12 + (size_t)rs * 2 * p.d + p.d)[ch];
+          cc3[u] = reinterpret_cast<const uint4*>(p.x3 + (size_t)rs * p.d)[ch];
+        } else if (rp) {
+          a[u] = reinterpret_cast<const uint4*>(rp)[2 * ch];
+          bb[u] = reinterpret_cast<const uint4*>(rp)[2 * ch + 1];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kDecodeBatch; ++u) {
+        const int t = t0 + u * 256;
+        if (t >= ntask) break;
+        const int r = t / nc, ch = t - r * nc;
+        float4* o = reinterpret_cast<float4*>(st + r * ds + 8 * ch);
+        if (srow[r] >= 0) {
+          const __nv_bfloat16* h1 = reinterpret_cast<const __nv_bfloat16*>(&a[u]);
+          const __nv_bfloat16* h2 = reinterpret_cast<const __nv_bfloat16*>(&bb[u]);
+          const __nv_bfloat16* h3 = reinterpret_cast<const __nv_bfloat16*>(&cc3[u]);
+          float xv[8];
+#pragma unroll
+          for (int e8 = 0; e8 < 8; ++e8)
+            xv[e8] = __fadd_rn(__fadd_rn(__bfloat162float(h1[e8]), __bfloat162float(h2[e8])), __bfloat162float(h3[e8]));
+          o[0] = make_float4(xv[0], xv[1], xv[2], xv[3]);
+          o[1] = make_float4(xv[4], xv[5], xv[6], xv[7]);
+        } else if (rowp[r]) {
+          o[0] = *reinterpret_cast<const float4*>(&a[u]);
+          o[1] = *reinterpret_cast<const float4*>(&bb[u]);
+        }
       }
     }
-    mbar_wait(&bar, 0);
     __syncthreads();
     RD_TS(3);
-    const float* slot = st + c * ds;
-    const RowRef x = sr >= 0 ? RowRef{nullptr, reinterpret_cast<const __nv_bfloat16*>(slot),
-                                      reinterpret_cast<const __nv_bfloat16*>(slot + p.d)}
-                             : row_f32(slot);
-    e = exact_l2_group8_row(dyn, x, p.d, j8, have ? p.d : 0);
+    e = exact_l2_group8_qd_cnt(qd, st + c * ds, have ? p.d : 0, j8);
   } else {
     // a padded slot runs zero terms so the warp stays converged for the shuffles; rows from HBM:
     // 16 loads deep (32 registers: one wave of 8 CTAs per SM)
@@ -370,8 +387,8 @@ cudaError_t launch_fallback(const FallbackParams& p, int num_sms, cudaStream_t s
 
 cudaError_t launch_merge(const MergeParams& p, bool stage, cudaStream_t s) {
   if (p.B == 0) return cudaSuccess;
-  if (stage) {
-    const size_t smem = sizeof(float) * ((size_t)p.d + kTopK * (size_t)stage_stride(p.d, p.x12 != nullptr));
+  if (stage && p.d % 8 == 0) {  // qd (fp64) + 32 decoded fp32 rows (8-element chunks)
+    const size_t smem = sizeof(float) * (2 * (size_t)p.d + kTopK * ((size_t)p.d + kStagePad));
     return launch_k(merge_rerank_kernel<true>, dim3(p.B), dim3(256), smem, s, p);
   }
   return launch_k(merge_rerank_kernel<false>, dim3(p.B), dim3(256), 0, s, p);

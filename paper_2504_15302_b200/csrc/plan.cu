@@ -9,67 +9,12 @@
 // Tiles of one list are adjacent so the query groups of a chunk hit L2 for each other. Offloaded
 // lists get no device tiles here; the host plans them as their bytes are staged (search.cu).
 #include "ivf_kernels.cuh"
+#include "plan_device.cuh"
 #include "rd_device.cuh"
 
 namespace rd {
 
 namespace {
-
-// Query groups per chunk of one list, by category. A list probed by >= tc_min_q queries goes to
-// the tensor cores: in mixed mode (tc_mode 0) a list of <= 16 queries is one narrow group and a
-// larger one balanced wide groups of <= 32 (usually one, so the list's bytes are read once);
-// tc_mode 16 / 32 forces one width. Sparser lists form FFMA groups of <= kScanG.
-struct Groups {
-  int g[kTileCats];
-};
-__device__ __forceinline__ Groups group_split(int nq, const PlanParams& p) {
-  Groups G = {{0, 0, 0}};
-  if (nq >= p.tc_min_q) {
-    if (p.tc_mode == 16 || (p.tc_mode == 0 && nq <= 16))
-      G.g[kCatNarrow] = (nq + 15) / 16;
-    else
-      G.g[kCatWide] = (nq + 31) / 32;
-  } else {
-    G.g[kCatFfma] = (nq + kScanG - 1) / kScanG;
-  }
-  return G;
-}
-
-// The tiles of one list: per category, chunk-major and group-minor in that category's array;
-// groups outer so each group's query split is computed once; chunks c = c0, c0 + cstep, ...
-// (lanes of a warp, or one thread). toff: the list's first tile in each category's array.
-__device__ __forceinline__ void emit_tiles(const PlanParams& p, int j, int nq, int qoff, int len, long long src0,
-                                           long long g0, const int (&toff)[kTileCats], const Groups& G, int chunks,
-                                           int rl, int c0, int cstep) {
-#pragma unroll
-  for (int cat = 0; cat < kTileCats; ++cat) {
-    const int ng = G.g[cat];
-    for (int g = 0; g < ng; ++g) {
-      int tq0, tnq;
-      if (cat != kCatFfma) {  // balanced tensor-core groups
-        const bool s32 = nq < 46341;  // g * nq < 2^31 for g <= nq / 16 + 1
-        const int q0 = s32 ? g * nq / ng : (int)((long long)g * nq / ng);
-        const int q1 = s32 ? (g + 1) * nq / ng : (int)((long long)(g + 1) * nq / ng);
-        tq0 = qoff + q0;
-        tnq = q1 - q0;
-      } else {
-        tq0 = qoff + g * kScanG;
-        tnq = min(kScanG, nq - g * kScanG);
-      }
-      ScanTile* dst = p.tiles[cat] + toff[cat] + g;
-      for (int c = c0; c < chunks; c += cstep) {
-        ScanTile T;
-        T.src_row = src0 + (long long)c * rl;
-        T.grow0 = g0 + (long long)c * rl;
-        T.list = j;
-        T.nrows = min(rl, len - c * rl);
-        T.qoff = tq0;
-        T.nq = tnq;
-        dst[c * ng] = T;
-      }
-    }
-  }
-}
 
 // warp per list: query count and resident tile counts per category (the bitmap was filled by the
 // selection kernel, coarse.cu)
@@ -94,78 +39,6 @@ __global__ void list_count_kernel(const PlanParams p) {
     }
 #pragma unroll
     for (int cat = 0; cat < kTileCats; ++cat) p.list_ntile[cat * p.nlist + warp] = G.g[cat] * chunks;
-  }
-}
-
-// Block exclusive scan of kV ints per thread (kNT threads), offset by carry[] (running totals of
-// earlier rounds, updated here); wsum is [kV][32] scratch.
-template <int kNT, int kV>
-__device__ __forceinline__ void block_scan_round(const int (&v)[kV], int (&ex)[kV], int (*wsum)[32], int* carry) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int inc[kV];
-#pragma unroll
-  for (int i = 0; i < kV; ++i) inc[i] = v[i];
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1)
-#pragma unroll
-    for (int i = 0; i < kV; ++i) {
-      const int y = __shfl_up_sync(0xffffffffu, inc[i], o);
-      if (lane >= o) inc[i] += y;
-    }
-  if (lane == 31)
-#pragma unroll
-    for (int i = 0; i < kV; ++i) wsum[i][w] = inc[i];
-  __syncthreads();
-  if (w == 0) {
-#pragma unroll
-    for (int i = 0; i < kV; ++i) {
-      int a = lane < kNT / 32 ? wsum[i][lane] : 0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, a, o);
-        if (lane >= o) a += y;
-      }
-      wsum[i][lane] = a;
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < kV; ++i) ex[i] = carry[i] + (w ? wsum[i][w - 1] : 0) + inc[i] - v[i];
-  __syncthreads();  // everyone has read carry
-  if (threadIdx.x == 0)
-#pragma unroll
-    for (int i = 0; i < kV; ++i) carry[i] += wsum[i][kNT / 32 - 1];
-  __syncthreads();
-}
-
-// block reduction of the byte counters; cat_total[cat] = tiles of each category -> counters / meta
-template <int kNT>
-__device__ __forceinline__ void finish_counters(const PlanParams& p, unsigned long long (&cc)[3],
-                                                unsigned long long (*wcnt)[32], const int* cat_total) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int i = 0; i < 3; ++i) cc[i] += __shfl_xor_sync(0xffffffffu, cc[i], o);
-  if (lane == 0)
-#pragma unroll
-    for (int i = 0; i < 3; ++i) wcnt[i][w] = cc[i];
-  __syncthreads();
-  if (w == 0) {
-    unsigned long long c[3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) c[i] = lane < kNT / 32 ? wcnt[i][lane] : 0ull;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int i = 0; i < 3; ++i) c[i] += __shfl_xor_sync(0xffffffffu, c[i], o);
-    if (lane == 0) {
-      for (int i = 0; i < 3; ++i) p.counters[i] = c[i];
-      for (int cat = 0; cat < kTileCats; ++cat) {
-        p.meta[2 * cat] = cat_total[cat];
-        p.meta[2 * cat + 1] = 0;
-      }
-    }
   }
 }
 
@@ -379,76 +252,13 @@ __global__ void __launch_bounds__(kPlanThreads) plan_fused_kernel(const PlanPara
   RD_TS(4);
 }
 
-// Tiny batches (B * nprobe <= 512 pairs): plan from the probe pairs alone. The (list, query) pairs
-// are rank-sorted in one CTA; a list's segment in sorted order IS its query CSR (list_q = the sorted
-// query ids, ascending within a list), so the only passes are O(pairs) plus one coalesced zeroing of
-// list_nq. Same outputs as the bitmap planners for every list.
 constexpr int kSmallPlanThreads = 1024;
 __global__ void __launch_bounds__(kSmallPlanThreads) plan_small_kernel(const PlanParams p) {
   RD_TS(13);  // entry, before the wait on the previous kernel
   RD_PDL_PROLOGUE();
-  __shared__ unsigned long long key[kSmallPlanThreads];
-  __shared__ int wsum[kTileCats][32];
-  __shared__ int carry[kTileCats];
-  __shared__ unsigned long long wcnt[3][32];
-  const int tid = threadIdx.x;
-  const int P = p.B * p.nprobe;
+  __shared__ SmallPlanSmem sm;
   RD_TS(0);
-  // (list, query) keys; padding / invalid probes sort last
-  unsigned long long kv = ~0ull;
-  if (tid < P) {
-    const int l = p.probes[tid];
-    if (l >= 0) kv = ((unsigned long long)(unsigned)l << 32) | (unsigned)(tid / p.nprobe);
-  }
-  key[tid] = kv;
-  if (tid < kTileCats) carry[tid] = 0;
-  for (int j = tid; j < p.nlist; j += kSmallPlanThreads) p.list_nq[j] = 0;  // coalesced
-  __syncthreads();
-  int r = 0;  // rank of this thread's key (keys are distinct)
-  if (kv != ~0ull)
-    for (int i = 0; i < P; ++i) r += key[i] < kv;
-  __syncthreads();
-  if (kv != ~0ull) key[r] = kv;
-  const int valid = __syncthreads_count(kv != ~0ull);
-  RD_TS(1);
-  // segment starts in sorted order: thread t owns sorted position t
-  const unsigned long long mine = tid < valid ? key[tid] : ~0ull;
-  const int l = (int)(mine >> 32);
-  const bool start = tid < valid && (tid == 0 || (key[tid - 1] >> 32) != (mine >> 32));
-  int nq = 0, chunks = 0, len = 0, rl = p.R;
-  Groups G = {{0, 0, 0}};
-  long long src0 = -1, g0 = 0;
-  if (start) {
-    int e = tid + 1;
-    while (e < valid && (key[e] >> 32) == (mine >> 32)) ++e;
-    nq = e - tid;
-    g0 = p.list_off[l];
-    len = (int)(p.list_off[l + 1] - g0);
-    src0 = p.res_row0[l];
-    if (src0 >= 0 && len > 0) {
-      rl = chunk_rows(len, l >= p.tail_from ? p.Rt : p.R);
-      chunks = (len + rl - 1) / rl;
-      G = group_split(nq, p);
-    }
-  }
-  if (tid < valid) p.list_q[tid] = (int)(mine & 0xffffffffu);
-  unsigned long long cc[3] = {start ? 1ull : 0ull, start && src0 >= 0 ? (unsigned long long)len : 0ull,
-                              start && src0 < 0 ? (unsigned long long)len : 0ull};
-  // block scan of the segment starts' tile counts (the query offset is the sorted position itself)
-  int v[kTileCats], ex[kTileCats];
-#pragma unroll
-  for (int cat = 0; cat < kTileCats; ++cat) v[cat] = G.g[cat] * chunks;
-  block_scan_round<kSmallPlanThreads, kTileCats>(v, ex, wsum, carry);
-  RD_TS(2);
-  if (start) {
-    p.list_nq[l] = nq;
-    p.list_qoff[l] = tid;
-    int any = 0;
-#pragma unroll
-    for (int cat = 0; cat < kTileCats; ++cat) any += G.g[cat];
-    if (any > 0) emit_tiles(p, l, nq, tid, len, src0, g0, ex, G, chunks, rl, 0, 1);
-  }
-  finish_counters<kSmallPlanThreads>(p, cc, wcnt, carry);
+  plan_small_body<kSmallPlanThreads>(p, sm);
   RD_TS(3);
 }
 

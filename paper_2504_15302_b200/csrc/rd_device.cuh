@@ -88,6 +88,35 @@ __device__ __forceinline__ float exact_l2_group8_qd(const double* qd, const floa
   s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
   return __double2float_rn(s);
 }
+// exact_l2_group8_qd over the first cnt elements (cnt < d: a padded slot passes 0 and its group
+// stays converged for the shuffles); x in shared memory
+__device__ __forceinline__ float exact_l2_group8_qd_cnt(const double* qd, const float* x, int cnt, int j) {
+  constexpr int kDepth = 8;
+  double s = 0.0;
+  int t = j;
+  for (; t + 8 * (kDepth - 1) < cnt; t += 8 * kDepth) {
+    float xv[kDepth];
+    double qv[kDepth];
+#pragma unroll
+    for (int i = 0; i < kDepth; ++i) {
+      xv[i] = x[t + 8 * i];
+      qv[i] = qd[t + 8 * i];
+    }
+#pragma unroll
+    for (int i = 0; i < kDepth; ++i) {
+      const double df = __dsub_rn(qv[i], (double)xv[i]);
+      s = __dadd_rn(s, __dmul_rn(df, df));
+    }
+  }
+  for (; t < cnt; t += 8) {
+    const double df = __dsub_rn(qd[t], (double)x[t]);
+    s = __dadd_rn(s, __dmul_rn(df, df));
+  }
+  s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
+  s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+  s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
+  return __double2float_rn(s);
+}
 __device__ __forceinline__ float exact_l2_group8(const float* __restrict__ q, const float* __restrict__ x, int d,
                                                  int j) {
   return exact_l2_group8_impl<true>(q, x, d, j);
@@ -250,6 +279,40 @@ __device__ __forceinline__ float l2_group8_f32_row(const float* q, const RowRef&
   for (; t < d; t += 8) {
     const float df = q[t] - x.at(t, d);
     s = fmaf(df, df, s);
+  }
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  s += __shfl_xor_sync(0xffffffffu, s, 4);
+  return s;
+}
+// Same bound as l2_group8_f32_row (each lane's chain is d/8 fp32 FMAs, then the 3-level tree), with
+// lane j summing the 8-element chunks c = j (mod 8) instead of residue classes: 128-bit shared-memory
+// loads (one per 8 elements and operand) instead of one load per element. q and the row are in
+// shared memory, 16-byte aligned, d % 64 == 0.
+__device__ __forceinline__ float l2_group8_f32_chunks(const float* q, const RowRef& x, int d, int j) {
+  float s = 0.f;
+  for (int c = j; c < d / 8; c += 8) {
+    const float4 q0 = reinterpret_cast<const float4*>(q)[2 * c], q1 = reinterpret_cast<const float4*>(q)[2 * c + 1];
+    float xv[8];
+    if (x.f) {
+      const float4 a = reinterpret_cast<const float4*>(x.f)[2 * c], b = reinterpret_cast<const float4*>(x.f)[2 * c + 1];
+      xv[0] = a.x, xv[1] = a.y, xv[2] = a.z, xv[3] = a.w, xv[4] = b.x, xv[5] = b.y, xv[6] = b.z, xv[7] = b.w;
+    } else {
+      const uint4 u1 = reinterpret_cast<const uint4*>(x.x12)[c], u2 = reinterpret_cast<const uint4*>(x.x12 + d)[c],
+                  u3 = reinterpret_cast<const uint4*>(x.x3)[c];
+      const __nv_bfloat16* h1 = reinterpret_cast<const __nv_bfloat16*>(&u1);
+      const __nv_bfloat16* h2 = reinterpret_cast<const __nv_bfloat16*>(&u2);
+      const __nv_bfloat16* h3 = reinterpret_cast<const __nv_bfloat16*>(&u3);
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        xv[e] = __fadd_rn(__fadd_rn(__bfloat162float(h1[e]), __bfloat162float(h2[e])), __bfloat162float(h3[e]));
+    }
+    const float qv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float df = qv[e] - xv[e];
+      s = fmaf(df, df, s);
+    }
   }
   s += __shfl_xor_sync(0xffffffffu, s, 1);
   s += __shfl_xor_sync(0xffffffffu, s, 2);

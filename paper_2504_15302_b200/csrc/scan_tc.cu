@@ -190,18 +190,31 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     uint32_t u = 0;
     const int nslices = d / 64;
+    // The queue is read one tile ahead: the next tile's index (atomic) and descriptor are fetched
+    // while the current tile's first stages go out, so a tile switch exposes no global round trip
+    // (they cost ~1 us each; at small batches, with a few tiles per CTA, that showed as CTAs with
+    // one more tile ending several us later).
+    int tn = 0;
+    ScanTile Tn{};
+    if (lane == 0) tn = atomicAdd(p.tile_counter, 1);
+    tn = __shfl_sync(0xffffffffu, tn, 0);
+    if (tn < ntiles) Tn = p.tiles[tn];
+    auto fetch_next = [&]() {  // after the current tile's first stages are issued
+      tn = __shfl_sync(0xffffffffu, tn, 0);
+      if (tn < ntiles) Tn = p.tiles[tn];
+    };
     for (uint32_t ti = 0;; ++ti) {
-      int t = 0;
+      const int t = tn;
       const int slot = ti & 1;
       if (lane == 0) {
-        t = atomicAdd(p.tile_counter, 1);
         RD_TWAIT(&sm.tempty[slot], ((ti >> 1) & 1) ^ 1, 0);
         sm.tring[slot] = t < ntiles ? t : -1;
         mbar_arrive(&sm.tfull[slot]);
       }
-      t = __shfl_sync(0xffffffffu, t, 0);
+      __syncwarp();
       if (t >= ntiles) break;
-      const ScanTile T = p.tiles[t];
+      const ScanTile T = Tn;
+      if (lane == 0) tn = atomicAdd(p.tile_counter, 1);  // consumed by fetch_next
       // x stage i of this tile: row tile i / nks, 64- (or 32-) dim slice i % nks; lane 0 issues
       const int nst = ((T.nrows + kRows - 1) / kRows) * nks;
       if constexpr (kStream) {
@@ -241,6 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           }
+          if (i == 0) fetch_next();
         }
         continue;
       }
@@ -294,6 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0)
         for (int i = 0; i < npre; ++i) issue_x(i);
       __syncwarp();
+      fetch_next();
       RD_TWAIT(sm.bempty, (ti & 1) ^ 1, 2);
       // one barrier for the whole gather (per-slice barriers let the first MMAs start earlier but
       // cost more than they saved: A/B on B200, 1024 queries, 206.4k vs 207.2k q/s)
@@ -315,14 +330,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     const unsigned char* bs_ptr = reinterpret_cast<unsigned char*>(smem_raw) + (sm.bs - smem_u32(smem_raw));
     const uint64_t bdesc0 = umma_desc_sw128(bs_ptr);
     uint32_t u = 0, rtc = 0;
+    long long dbg_rows = 0;
     for (uint32_t ti = 0;; ++ti) {
       const int slot = ti & 1;
       RD_TWAIT(&sm.tfull[slot], (ti >> 1) & 1, 3);
       const int t = sm.tring[slot];
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.tempty[slot]);
-      if (t < 0) break;
+      if (t < 0) {
+        if (p.dbg && lane == 0) {  // profiling only: tiles and rows this CTA scanned
+          p.dbg[4 * gridDim.x + blockIdx.x] = ti;
+          p.dbg[5 * gridDim.x + blockIdx.x] = dbg_rows;
+        }
+        break;
+      }
       const ScanTile T = p.tiles[t];
+      dbg_rows += T.nrows;
       if (p.dbg && ti == 0 && lane == 0) p.dbg[blockIdx.x * 4 + 2] = gtimer();
       for (int rt = 0; rt * kRows < T.nrows; ++rt, ++rtc) {
         const int a = rtc & 1;

@@ -34,11 +34,20 @@ Plan make_plan(const rd_index* h, long long B, int nprobe) {
   const long long gran = rd::kTcRows;
   const int tps = h->tiles_per_sm > 0 ? h->tiles_per_sm : (B >= 512 ? 8 : 32);
   long long R = (long long)std::ceil(est_rows / ((double)h->num_sms * tps));
-  R = std::max<long long>(rd::kScanRows, std::min<long long>(4096, (R + gran - 1) / gran * gran));
+  static const long long floor_r = std::getenv("RD_MIN_ROWS") ? std::atoll(std::getenv("RD_MIN_ROWS")) : rd::kScanRows;
+  // tail chunks: one tensor-core row tile (128) when every tile is a tensor-core tile (B200, B = 1:
+  // 150 -> 146 us), else one FFMA box; smaller tail tiles measured slower (each tile's fixed latency)
+  static const char* tail_env = std::getenv("RD_TAIL_ROWS");
+  const bool all_tc = h->split3 || (h->tc_scan() && h->tc_min_q <= 1);
+  const long long floor_t = tail_env ? std::atoll(tail_env) : all_tc ? rd::kTcRows : rd::kScanRows;
+  R = std::max<long long>(floor_r, std::min<long long>(4096, (R + gran - 1) / gran * gran));
   pl.R = (int)R;
   // the last eighth of the lists (in id order, the order the scan's queue hands tiles out) in
   // quarter-size chunks: a shorter tail at one more tile per list there
-  pl.Rt = (int)std::max<long long>(rd::kScanRows, (R / 4 + gran - 1) / gran * gran);
+  {
+    const long long tg = floor_t < gran ? 32 : gran;
+    pl.Rt = (int)std::max<long long>(floor_t, (R / 4 + tg - 1) / tg * tg);
+  }
   pl.tail_from = h->nlist - h->nlist / 8;
   if (const char* v = std::getenv("RD_TAIL_FRAC")) pl.tail_from = h->nlist - (int)(h->nlist * std::atof(v));
   pl.max_chunks = (int)std::max<long long>(1, (h->max_len + pl.Rt - 1) / pl.Rt);
@@ -193,6 +202,10 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   const int m_rerank = std::min(rd::kTopK, k + h->rerank_margin);
   const int thr_rank = std::min(rd::kTopK - 1, m_rerank);
   sp.seed_rows = thr_rank + 1;
+  rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
+                    w.list_ntile.p, w.list_toff.p, w.list_q.p, {w.tiles16.p, w.tiles.p, w.ff_tiles.p}, w.meta(),
+                    w.counters(), (int)B, nl, nprobe, pl.R, h->tc_scan() ? h->tc_min_q : 1 << 30, tc_mode,
+                    pl.Rt, pl.tail_from};
   if (sel_all) {
     size_t sb = 0;
     void* scratch = select_all_scratch(h, B, &sb);
@@ -234,10 +247,6 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     }
     return;
   }
-  rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
-                    w.list_ntile.p, w.list_toff.p, w.list_q.p, {w.tiles16.p, w.tiles.p, w.ff_tiles.p}, w.meta(),
-                    w.counters(), (int)B, nl, nprobe, pl.R, h->tc_scan() ? h->tc_min_q : 1 << 30, tc_mode,
-                    pl.Rt, pl.tail_from};
   if (chain) pp.dbg = chain + 32;
   h->traced("plan", s, pp.dbg, [&] { CK(rd::launch_plan(pp, s)); });
   if (use_bm) w.bitmap_clean = true;  // list_fill, now enqueued, clears every bit the selection sets
@@ -268,8 +277,8 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   if (h->tc_scan()) {  // otherwise every tile is FFMA
     if (chain) tc.dbg = chain + 96;
     if (h->dbg_ts) {  // profiling only: per-CTA entry / ready / first tile / end times
-      if (h->dbg_scan.n < 4 * (size_t)h->num_sms) h->dbg_scan.alloc(4 * (size_t)h->num_sms);
-      CK(cudaMemsetAsync(h->dbg_scan.p, 0, 8 * 4 * (size_t)h->num_sms, s));
+      if (h->dbg_scan.n < 6 * (size_t)h->num_sms) h->dbg_scan.alloc(6 * (size_t)h->num_sms);
+      CK(cudaMemsetAsync(h->dbg_scan.p, 0, 8 * 6 * (size_t)h->num_sms, s));
       tc.dbg = h->dbg_scan.p;
     }
     const bool stall = std::getenv("RD_DEBUG_STALL") != nullptr;  // profiling only (scan_tc.cu built with -DRD_STALL_PROF)
@@ -288,6 +297,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
       // streamed query operand for about one query per probed list or fewer (scan_tc.cu)
       const bool stream =
           h->stream_force >= 0 ? h->stream_force != 0 : (long long)B * std::min(nprobe, nl) <= nl;
+
       CK(rd::launch_scan_tc(xm128, xm32, gmap, tn, h->num_sms, s, h->presplit, 16, stream));
       launches += 1;
     }
@@ -310,9 +320,22 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
       fprintf(stderr, "\n");
     }
     if (h->dbg_ts) {
-      std::vector<unsigned long long> t(4 * (size_t)h->num_sms);
+      std::vector<unsigned long long> t(6 * (size_t)h->num_sms);
       CK(cudaMemcpyAsync(t.data(), h->dbg_scan.p, 8 * t.size(), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
+      {  // CTAs by end time: (end ns from the first entry, tiles, rows), earliest and latest five
+        const int G = h->num_sms;
+        unsigned long long e0 = ~0ull;
+        for (int c = 0; c < G; ++c) e0 = std::min(e0, t[4 * c]);
+        std::vector<int> ord(G);
+        for (int c = 0; c < G; ++c) ord[c] = c;
+        std::sort(ord.begin(), ord.end(), [&](int a, int b) { return t[4 * a + 3] < t[4 * b + 3]; });
+        fprintf(stderr, "scan CTA ends (ns, tiles, rows):");
+        for (int i = 0; i < G; ++i)
+          if (i < 5 || i >= G - 5)
+            fprintf(stderr, " [%lld %llu %llu]", (long long)(t[4 * ord[i] + 3] - e0), t[4 * G + ord[i]], t[5 * G + ord[i]]);
+        fprintf(stderr, "\n");
+      }
       unsigned long long t0 = ~0ull, mx[4] = {0, 0, 0, 0};
       for (int c = 0; c < h->num_sms; ++c) t0 = std::min(t0, t[4 * c]);
       double mean[4] = {0, 0, 0, 0};
