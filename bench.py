@@ -13,9 +13,12 @@ e2e         : same metric through the public C-ABI rd_search with host
               buffers: H2D of the queries and D2H of ids+distances every step.
 roofline    : the dominant kernel (N4 list scan): algorithmic bytes of the
               probed lists' vectors per launch / its CUDA-event duration.
-cpu_baseline: the CPU oracle (oracle/librd_cpu.so — the only CPU IVF path;
-              the reference has none) on a bounded query sample, rank 0, N=1.
---impl reference: that same CPU path as the timed arm.
+cpu_baseline: the exact CPU oracle (oracle/librd_cpu.so; the reference has no
+              search) on a bounded query sample, rank 0, N=1;
+cpu_baseline_batched: the batched list-major CPU search (oracle/rd_cpu_batched.c,
+              identical results) over whole batches, and the GPU's ratio to it.
+--impl reference: the batched CPU search over the whole configured batch every
+              step (the exact oracle's sample rate beside it).
 Inputs are larger than L2 (30.7 GB index), so no explicit flush is needed.
 N>1: the config's knowledge base is split into N row stripes of every list
 (strong scaling: 10M rows split N ways), one per GPU, searched as one shard group
@@ -170,7 +173,7 @@ def cpu_desc_args(cfg, shards):
     return dict(n=cfg["n"], d=cfg["d"], nlist=cfg["nlist"])
 
 
-def cpu_baseline(cfg, desc_args, sample, steps=1, batch_of=None):
+def cpu_baseline(cfg, desc_args, sample, steps=1, batch_of=None, batched_of=None):
     """Times the CPU oracle on `sample` queries of the same workload per step (rank 0, N=1).
     batch_of(s) gives step s's full query batch (the GPU arm's); its first `sample` queries are
     timed. Returns the per-step rates and the last step's queries and results (the parity check)."""
@@ -187,13 +190,32 @@ def cpu_baseline(cfg, desc_args, sample, steps=1, batch_of=None):
         t0 = time.perf_counter()
         res = idx.search(q, cfg["nprobe"], cfg["k"])
         vals.append(sample / (time.perf_counter() - t0))
+    batched = None
+    if batched_of is not None:  # the batched CPU search over whole batches, same index
+        bv, bout = cpu_batched(idx, oracle, batched_of, cfg["nprobe"], cfg["k"])
+        batched = {"per_step": bv, "ids": bout[0], "dists": bout[1], "fallbacks": bout[2]}
     idx.close()
     cpu = cpu_model()
     return {"value": statistics.median(vals), "unit": "queries/s", "cores": cores, "kind": "port",
             "cpu_model": cpu,
             "sample": f"first {sample} queries of each step's batch, exact IVF-Flat (fp64 canonical distances, "
                       f"query-at-a-time), {cores} threads on {cpu} (index build {build_s:.1f}s untimed)",
-            "per_step": vals, "queries": q, "result": res}
+            "per_step": vals, "queries": q, "result": res, "batched": batched}
+
+
+def cpu_batched(oracle_idx, oracle, batches, nprobe, k):
+    """The batched list-major CPU search (oracle/rd_cpu_batched.c: the tuned-CPU-retriever
+    baseline, results identical to the exact oracle) over whole batches: one untimed warm-up (the
+    row norms), then each batch timed. Returns (per-batch q/s, last result ids/dists, fallbacks)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_ext import batched_search
+    batched_search(oracle, oracle_idx, batches[0][: min(8, len(batches[0]))], nprobe, k)  # prepare
+    vals, out = [], None
+    for q in batches:
+        t0 = time.perf_counter()
+        out = batched_search(oracle, oracle_idx, q, nprobe, k)
+        vals.append(len(q) / (time.perf_counter() - t0))
+    return vals, out
 
 
 def cpu_model():
@@ -226,9 +248,11 @@ def shards_for(cfg, n_gpus, stripe_of):
 
 
 def run_reference(args, cfg):
-    """The reference's CPU path on the box's host cores: the exact oracle (the reference has no
-    search of its own), all host threads, on this arm's config; each step times the
-    first --cpu-sample queries of the batch the GPU arm searches in that step."""
+    """The reference's CPU path on the box's host cores. The reference has no search of its own
+    (SPEC.md:9), so its CPU path is the oracle library's: the batched list-major IVF-Flat search
+    (oracle/rd_cpu_batched.c; results identical to the exact oracle) over the whole configured batch
+    every step, all host threads, this arm's config. The exact query-at-a-time oracle is timed on a
+    sample beside it (cpu_exact)."""
     world, rank, _ = dist_env()
     n_gpus = world if world > 1 else args.gpus
     shards = shards_for(cfg, n_gpus, args.stripe_of)
@@ -241,19 +265,22 @@ def run_reference(args, cfg):
         return
     oracle = oracle_lib()
     desc_full = oracle.desc(cfg["n"], cfg["d"], cfg["nlist"])
+    nb = args.warmup + args.steps
+    batches = [oracle.synth_queries(desc_full, s * B, B)[0] for s in range(nb)]
     sample = min(args.cpu_sample, B)
-    if args.cpu_sample_auto:  # the whole batch when the run fits ~150 s of CPU time, else a sample
-        probe = cpu_baseline(cfg, cpu_desc_args(cfg, shards), min(32, B), steps=1,
-                             batch_of=lambda s: oracle.synth_queries(desc_full, 0, min(32, B))[0])
-        sample = int(min(B, max(32, 150.0 * probe["value"] / (args.steps + args.warmup))))
-    res = cpu_baseline(cfg, cpu_desc_args(cfg, shards), sample, steps=args.warmup + args.steps,
-                       batch_of=lambda s: oracle.synth_queries(desc_full, s * B, sample)[0])
-    vals = res["per_step"][args.warmup:]
+    res = cpu_baseline(cfg, cpu_desc_args(cfg, shards), sample, steps=1, batch_of=lambda s: batches[-1],
+                       batched_of=batches)
+    vals = res["batched"]["per_step"][args.warmup:]
     v = statistics.median(vals)
     line.update({"value": v, "ms_per_step": 1000.0 * B / v, "scaling": "replicas only",
                  "vs_baseline": None,
                  "cpu_baseline": {"value": v, "unit": "queries/s", "cores": res["cores"], "kind": "port",
-                                  "cpu_model": res["cpu_model"], "sample": res["sample"]},
+                                  "variant": "batched list-major IVF-Flat (oracle/rd_cpu_batched.c)",
+                                  "cpu_model": res["cpu_model"],
+                                  "sample": f"the whole batch of {B} queries every step, {res['cores']} threads on "
+                                            f"{res['cpu_model']}; exact fallbacks "
+                                            f"{res['batched']['fallbacks']} in the last step"},
+                 "cpu_exact": {"value": res["value"], "unit": "queries/s", "sample": res["sample"]},
                  "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
     print(json.dumps(line), flush=True)
 
@@ -482,7 +509,8 @@ def run_ours(args, cfg):
         # the CPU path on the first queries of the last timed batch, then the engine on those same
         # queries (outside every timed region): the parity check of this run
         sample = min(args.cpu_sample, B)
-        cb = cpu_baseline(cfg, cpu_desc_args(cfg, shards), sample, batch_of=lambda s: qs[nb - 1])
+        cb = cpu_baseline(cfg, cpu_desc_args(cfg, shards), sample, batch_of=lambda s: qs[nb - 1],
+                          batched_of=[qs[nb - 2], qs[nb - 1]] if nb >= 2 else [qs[nb - 1]])
         mine = idx0.search(cb["queries"], nprobe, k)
         want = cb["result"]
         line["parity"] = {"checked": int(sample),
@@ -490,9 +518,25 @@ def run_ours(args, cfg):
                           "dists_equal": int((mine.dists == want.dists).all(axis=1).sum()),
                           "oracle": "oracle/librd_cpu.so (exact IVF-Flat, canonical fp64 distances)",
                           "data": "the whole knowledge base" if shards == 1 else f"stripe 0 of {shards}"}
+        bt = cb.pop("batched")
+        full = idx0.search(qs[nb - 1], nprobe, k)  # the whole last timed batch vs the batched CPU search
+        line["parity_full_batch"] = {"checked": int(B),
+                                     "ids_equal": int((full.ids == bt["ids"]).all(axis=1).sum()),
+                                     "dists_equal": int((full.dists == bt["dists"]).all(axis=1).sum()),
+                                     "oracle": "oracle/rd_cpu_batched.c (bit-identical to the exact oracle: "
+                                               "tests/test_cpu_batched.py)"}
         for key in ("per_step", "queries", "result"):
             cb.pop(key, None)
         line["cpu_baseline"] = cb
+        bval = statistics.median(bt["per_step"])
+        line["cpu_baseline_batched"] = {
+            "value": bval, "unit": "queries/s", "cores": cb["cores"], "kind": "batched",
+            "cpu_model": cb["cpu_model"],
+            "sample": f"the whole batch ({B} queries), list-major: probes inverted per list, each list read "
+                      f"once per batch against its query group (fp32 AVX2/FMA dots), certified, exact canonical "
+                      f"rerank (oracle/rd_cpu_batched.c), {cb['cores']} threads; median of "
+                      f"{len(bt['per_step'])} batches; exact fallbacks {bt['fallbacks']}",
+            "gpu_over_cpu": value / bval, "gpu_e2e_over_cpu": e2e["value"] / bval}
     print(json.dumps(line), flush=True)
     if grp is not None:
         grp.close()
@@ -509,10 +553,7 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--cpu-sample", type=int, default=128,
-                    help="CPU-path queries per step (our arm's cpu_baseline; --impl reference: see --cpu-sample-auto)")
-    ap.add_argument("--cpu-sample-fixed", dest="cpu_sample_auto", action="store_false",
-                    help="--impl reference: time exactly --cpu-sample queries per step instead of the whole "
-                         "batch when ~150 s of CPU time allows")
+                    help="exact-oracle queries timed per step (the batched CPU search takes whole batches)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--stripe-of", type=int, default=0,

@@ -38,6 +38,7 @@
 
 #include "../include/rd.h"
 #include "../include/rd_format.h"
+#include "rd_oracle_internal.h"
 
 /* ------------------------------------------------------------------ errors */
 static __thread char g_err[512];
@@ -108,14 +109,13 @@ float rd_exact_l2(const float* a, const float* b, int32_t d) {
 }
 
 /* ------------------------------------------------------------------ threads */
-static int n_threads(void) {
+int rdo_threads(void) {
   const char* e = getenv("RD_CPU_THREADS");
   if (e && atoi(e) > 0) return atoi(e);
   long n = sysconf(_SC_NPROCESSORS_ONLN);
   return n > 0 ? (int)n : 1;
 }
 
-typedef void (*work_fn)(void* ctx, int64_t begin, int64_t end);
 typedef struct {
   work_fn fn;
   void* ctx;
@@ -138,9 +138,9 @@ static void* pool_worker(void* p) {
   return NULL;
 }
 
-static void parallel_for(int64_t n, int64_t chunk, work_fn fn, void* ctx) {
+void rdo_parallel_for(int64_t n, int64_t chunk, work_fn fn, void* ctx) {
   if (n <= 0) return;
-  int T = n_threads();
+  int T = rdo_threads();
   if (chunk < 1) chunk = 1;
   pool_job job = {fn, ctx, n, chunk, 0, PTHREAD_MUTEX_INITIALIZER};
   if (T == 1 || n <= chunk) {
@@ -153,18 +153,7 @@ static void parallel_for(int64_t n, int64_t chunk, work_fn fn, void* ctx) {
   free(th);
 }
 
-/* ------------------------------------------------------------------ index */
-struct rd_index {
-  int64_t n;
-  int32_t d, nlist;
-  float* vectors;   /* n x d, list order */
-  int64_t* offsets; /* nlist + 1 */
-  int64_t* ids;     /* n */
-  float* centroids; /* nlist x d */
-  uint8_t* resident;
-  uint8_t* hostcopy; /* list has a (write-once) pinned host copy: offloaded at some point */
-  float max_norm;
-};
+/* ------------------------------------------------------------------ index (struct: rd_oracle_internal.h) */
 
 static int check_desc(const rd_synth_desc* s) {
   if (!s) return fail(RD_ERR_INVALID, "null synth descriptor");
@@ -231,7 +220,7 @@ int rd_index_create_synthetic(const rd_synth_desc* s, int32_t device, rd_index**
   h->centroids = (float*)malloc(sizeof(float) * (size_t)nl * d);
   gen_ctx gc = {s, rd_derive_seed(s->seed, RD_STREAM_CENTROIDS),
                 rd_derive_seed(s->seed, RD_STREAM_VECTOR_NOISE), NULL, NULL, h->centroids, NULL};
-  parallel_for(nl, 16, gen_centroids, &gc);
+  rdo_parallel_for(nl, 16, gen_centroids, &gc);
 
   /* list membership: a(i) = u(s_a, i) mod nlist, members ascending by id */
   int32_t* assign = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
@@ -274,7 +263,7 @@ int rd_index_create_synthetic(const rd_synth_desc* s, int32_t device, rd_index**
   gc.lists_of_rows = row_list;
   gc.out = h->vectors;
   gc.centroids = h->centroids;
-  parallel_for(h->n, 4096, gen_rows, &gc);
+  rdo_parallel_for(h->n, 4096, gen_rows, &gc);
   free(row_list);
   h->resident = (uint8_t*)malloc((size_t)nl);
   h->hostcopy = (uint8_t*)calloc((size_t)nl, 1);
@@ -330,7 +319,7 @@ int rd_index_build(int64_t n, int32_t d, int32_t nlist, const float* vectors, co
   double* sum = (double*)malloc(sizeof(double) * (size_t)nlist * d);
   int64_t* cnt = (int64_t*)malloc(sizeof(int64_t) * (size_t)nlist);
   for (int32_t it = 0; it <= iters; ++it) {
-    parallel_for(n, 256, assign_rows, &ac);
+    rdo_parallel_for(n, 256, assign_rows, &ac);
     if (it == iters) break;
     memset(sum, 0, sizeof(double) * (size_t)nlist * d);
     memset(cnt, 0, sizeof(int64_t) * (size_t)nlist);
@@ -487,6 +476,8 @@ void rd_index_destroy(rd_index* h) {
   free(h->centroids);
   free(h->resident);
   free(h->hostcopy);
+  free(h->xnorm);
+  free(h->cnorm);
   free(h);
 }
 
@@ -732,7 +723,7 @@ int rd_search(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int3
     return fail(RD_ERR_INVALID, "search: null argument");
   if (B < 0 || nprobe < 1 || k < 1) return fail(RD_ERR_INVALID, "search: B >= 0, nprobe >= 1, k >= 1 required");
   search_ctx c = {h, queries, nprobe, k, out_ids, out_dists, NULL};
-  parallel_for(B, 1, search_range, &c);
+  rdo_parallel_for(B, 1, search_range, &c);
   if (stats) memset(stats, 0, sizeof *stats);
   return RD_OK;
 }
@@ -741,7 +732,7 @@ int rd_probe(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int32
   if (!h || (B > 0 && (!queries || !out_lists))) return fail(RD_ERR_INVALID, "probe: null argument");
   if (B < 0 || nprobe < 1) return fail(RD_ERR_INVALID, "probe: nprobe >= 1 required");
   search_ctx c = {h, queries, nprobe, 1, NULL, NULL, out_lists};
-  parallel_for(B, 1, search_range, &c);
+  rdo_parallel_for(B, 1, search_range, &c);
   return RD_OK;
 }
 
@@ -944,11 +935,11 @@ int rd_oracle_synth_search(const rd_synth_desc* s, uint64_t shard_mask, const fl
   c.k = k;
   float* cen = (float*)malloc(sizeof(float) * (size_t)nl * d);
   gen_ctx gc = {s, c.sc, c.sx, NULL, NULL, cen, NULL};
-  parallel_for(nl, 16, gen_centroids, &gc);
+  rdo_parallel_for(nl, 16, gen_centroids, &gc);
   c.centroids = cen;
   int32_t* lists = (int32_t*)malloc(sizeof(int32_t) * (size_t)B * np);
   c.lists = lists;
-  parallel_for(B, 1, synth_probe_range, &c);
+  rdo_parallel_for(B, 1, synth_probe_range, &c);
   /* marked lists and their (query, probe) pairs */
   int32_t* mark = (int32_t*)malloc(sizeof(int32_t) * (size_t)nl);
   for (int32_t l = 0; l < nl; ++l) mark[l] = -1;
@@ -970,7 +961,7 @@ int rd_oracle_synth_search(const rd_synth_desc* s, uint64_t shard_mask, const fl
   int32_t* assign = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
   if (!assign) return fail(RD_ERR_RUNTIME, "synth_search: out of host memory");
   assign_gen_ctx ac = {rd_derive_seed(s->seed, RD_STREAM_ASSIGN), nl, assign};
-  parallel_for(n, 1 << 20, synth_assign_range, &ac);
+  rdo_parallel_for(n, 1 << 20, synth_assign_range, &ac);
   int64_t* full_len = (int64_t*)calloc((size_t)nl, sizeof(int64_t));
   for (int64_t i = 0; i < n; ++i) full_len[assign[i]]++;
   int64_t* mem_off = (int64_t*)calloc((size_t)nm + 1, sizeof(int64_t));
@@ -1008,7 +999,7 @@ int rd_oracle_synth_search(const rd_synth_desc* s, uint64_t shard_mask, const fl
   c.pair_q = pair_q;
   c.part = (cand*)malloc(sizeof(cand) * (size_t)B * np * k);
   c.part_cnt = (int32_t*)calloc((size_t)B * np, sizeof(int32_t));
-  parallel_for(nm, 1, synth_scan_range, &c);
+  rdo_parallel_for(nm, 1, synth_scan_range, &c);
   cand* top = (cand*)malloc(sizeof(cand) * (size_t)k);
   for (int64_t qi = 0; qi < B; ++qi) {
     int32_t cnt = 0;
