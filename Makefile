@@ -39,6 +39,9 @@ tests/cpp/ragsim_adapter_cpu: tests/cpp/ragsim_adapter_test.cpp include/rd_ragsi
 tests/cpp/ragsim_adapter_b200: tests/cpp/ragsim_adapter_test.cpp include/rd_ragsim.hpp include/rd.h $(LIB)
 	g++ -std=c++17 -O2 -Wall -Wextra -Iinclude -o $@ $< -L$(PKG)/lib -l:librd_b200.so -Wl,-rpath,'$$ORIGIN/../../$(PKG)/lib'
 all: tests/cpp/ragsim_adapter_cpu tests/cpp/ragsim_adapter_b200
+tests/cpp/fit_pin: tests/cpp/fit_pin.cpp include/rd_ragsim.hpp include/rd.h oracle
+	g++ -std=c++17 -O2 -Wall -Wextra -Iinclude -o $@ $< -Loracle -l:librd_cpu.so -Wl,-rpath,'$$ORIGIN/../../oracle'
+all: tests/cpp/fit_pin
 
 # C++ end-to-end latency of rd_search through the C ABI (tools/e2e_latency.cpp)
 tools/e2e_latency: tools/e2e_latency.cpp include/rd.h $(LIB)

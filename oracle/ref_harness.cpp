@@ -6,6 +6,7 @@
 //   - ragsim::check_feasible gpu_used   (core/src/memory_planner.cpp:12-35)
 //   - ragsim::queue_capacity            (core/src/prefetch_timeline.cpp:79-90)
 //   - ragsim::retrieval_time            (core/src/cost_model.cpp:15-21)
+//   - ragsim::fit_power_law / predict   (core/src/cost_model.cpp:97-136)
 // The JSON it prints is committed as tests/golden/ref_golden.json.
 #include <cinttypes>
 #include <cstdio>
@@ -81,6 +82,24 @@ int main() {
   std::printf("\n  ],\n  \"retrieval_time\": [");
   for (int p = 0; p <= 32; p += 8)
     std::printf("%s{\"resident\": %d, \"seconds\": %.17g}", p ? ", " : "", p, retrieval_time(p, db));
-  std::printf("]\n}\n");
+  // fit_power_law (cost_model.cpp:97-136) on sample sets: B200 measured T_ret rows
+  // (profiles/round2_measured_tret.json, resident fractions 1.0 and 0.0), a decreasing set (exponent
+  // clamped to 0), repeated batch sizes, two points
+  const std::vector<std::vector<BatchTimeSample>> sets = {
+      {{1, 0.000181}, {2, 0.000241}, {4, 0.000362}, {8, 0.000588}, {16, 0.000968}, {32, 0.001521}, {64, 0.002264}},
+      {{1, 0.009134}, {2, 0.017783}, {4, 0.034356}, {8, 0.064310}, {16, 0.114713}, {32, 0.186829}, {64, 0.284393}},
+      {{1, 4.0}, {2, 2.0}, {4, 1.0}},
+      {{8, 0.1}, {8, 0.12}, {16, 0.2}, {64, 0.5}},
+      {{1, 1e-3}, {1000, 2.0}}};
+  std::printf("],\n  \"fit_power_law\": [");
+  for (size_t i = 0; i < sets.size(); ++i) {
+    const CostModelFit f = fit_power_law(sets[i]);
+    std::printf("%s\n    {\"samples\": [", i ? "," : "");
+    for (size_t j = 0; j < sets[i].size(); ++j)
+      std::printf("%s[%.17g, %.17g]", j ? ", " : "", sets[i][j].batch_size, sets[i][j].seconds);
+    std::printf("], \"a\": %.17g, \"c\": %.17g, \"residual\": %.17g, \"clamped\": %s, \"predict_256\": %.17g}",
+                f.a, f.c, f.residual, f.exponent_clamped ? "true" : "false", predict(f, 256));
+  }
+  std::printf("\n  ]\n}\n");
   return 0;
 }

@@ -86,6 +86,12 @@ int main(int argc, char** argv) {
     correct += !r.ids.empty() && r.ids[0] == src[r.query];
   }
   EXPECT(correct == nreq);  // each query's source vector is its nearest neighbour
+  // digest of every request's top-k ids (FNV-1a): the results do not depend on how the worker
+  // batched them, so the engine-linked and oracle-linked drivers must print the same digest
+  uint64_t digest = 1469598103934665603ull;
+  for (const auto& r : reqs)
+    for (int64_t id : r.ids)
+      for (int byte = 0; byte < 8; ++byte) digest = (digest ^ ((uint64_t)id >> (8 * byte) & 0xffu)) * 1099511628211ull;
   for (int b : rep.batch_sizes) EXPECT(b >= 1 && b <= 64);
   EXPECT(rep.reconfig_seconds > 0.0 && idx.info().lists_resident == nlist - 2);
 
@@ -95,8 +101,8 @@ int main(int argc, char** argv) {
   EXPECT(f.a > 0.0 && f.samples == 4);
   std::printf("{\"backend\": \"%s\", \"requests\": %d, \"batches\": %d, \"makespan_s\": %.6g, "
               "\"busy_s\": %.6g, \"reconfig_s\": %.6g, \"t_ret_fit\": {\"a\": %.6g, \"c\": %.4f, \"residual\": %.4f}, "
-              "\"t_ret_64_s\": %.6g, \"failures\": %d}\n",
+              "\"t_ret_64_s\": %.6g, \"results_digest\": \"%016llx\", \"failures\": %d}\n",
               rd_backend(), nreq, rep.batches, rep.makespan, rep.busy_seconds, rep.reconfig_seconds, f.a, f.c,
-              f.residual, cost.seconds(64), failures);
+              f.residual, cost.seconds(64), (unsigned long long)digest, failures);
   return failures ? 1 : 0;
 }

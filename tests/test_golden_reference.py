@@ -73,3 +73,19 @@ def test_reference_test_vectors(lib):
     got = lib.llm_reservation_bytes(weight_total=16 * GiB, kv_bytes_per_request=128 << 20,
                                     workspace_bytes_per_request=64 << 20, w_gpu=0.75, c_gpu=1.0, gen_batch_size=32)
     assert got == 18 * GiB
+
+
+@pytest.mark.parametrize("i", range(len(GOLD["fit_power_law"])))
+def test_fit_power_law_matches_reference(i):
+    """include/rd_ragsim.hpp's fit_power_law / predict against the reference's own (cost_model.cpp:97-136,
+    compiled by oracle/build_ref.sh) on the golden sample sets, including measured B200 T_ret rows."""
+    import subprocess
+    g = GOLD["fit_power_law"][i]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.check_call(["make", "-C", root, "-s", "tests/cpp/fit_pin"])
+    out = subprocess.run([os.path.join(root, "tests/cpp/fit_pin")] + [f"{b!r},{t!r}" for b, t in g["samples"]],
+                         capture_output=True, text=True, check=True)
+    f = json.loads(out.stdout)
+    assert f["clamped"] == g["clamped"]
+    for key in ("a", "c", "residual", "predict_256"):
+        assert f[key] == pytest.approx(g[key], rel=1e-12, abs=1e-15), key

@@ -27,5 +27,11 @@ def test_adapter_on_oracle():
 
 @pytest.mark.gpu
 def test_adapter_on_engine():
-    r = _run("tests/cpp/ragsim_adapter_b200", 200000, 768, 1024, 400)
+    """The same driver over the engine and over the oracle: identical top-k for every request
+    (digest of all ids), whatever batches the worker formed on each."""
+    args = (200000, 768, 1024, 400)
+    r = _run("tests/cpp/ragsim_adapter_b200", *args)
     assert r["backend"] == "b200-sm100a" and r["failures"] == 0
+    o = _run("tests/cpp/ragsim_adapter_cpu", *args)
+    assert o["backend"] == "cpu-oracle" and o["failures"] == 0
+    assert r["results_digest"] == o["results_digest"]
