@@ -96,6 +96,11 @@ struct TcScanParams {
 
 size_t scan_smem_bytes(int d);
 size_t scan_tc_smem_bytes(int d, int tc_g, bool presplit, bool stream = false);
+// 32-query tiles over the x1 | x2 plane on CTA pairs (scan_pair.cu, cta_group::2): ring depth for
+// this d (0: unsupported), and the launch (grid = the SMs rounded down to pairs)
+int scan_pair_stages(int d);
+cudaError_t launch_scan_pair(const CUtensorMap& map128, const CUtensorMap& map32, const CUtensorMap& qmap,
+                             const TcScanParams& p, int num_sms, cudaStream_t s);
 // qmap: 2D bf16 map over the qsplit buffer as [2B rows x d], box {64, 1} (gather4 source)
 // presplit: map128 / map32 are 3D bf16 maps over the pre-split [rows][2][d] arena, box {64, 1, 128|32}
 // tc_g: queries per tile, 16 or 32 (the planner grouped the tiles with the same width)

@@ -20,7 +20,7 @@ struct Plan {
   long long max_tiles;
 };
 
-Plan make_plan(const rd_index* h, long long B, int nprobe) {
+Plan make_plan(const rd_index* h, long long B, int nprobe, bool pair) {
   Plan pl;
   const int np = std::min(nprobe, h->nlist);
   const double avg = h->nlist ? (double)h->n / h->nlist : 0.0;
@@ -51,7 +51,8 @@ Plan make_plan(const rd_index* h, long long B, int nprobe) {
   pl.tail_from = h->nlist - h->nlist / 8;
   if (const char* v = std::getenv("RD_TAIL_FRAC")) pl.tail_from = h->nlist - (int)(h->nlist * std::atof(v));
   pl.max_chunks = (int)std::max<long long>(1, (h->max_len + pl.Rt - 1) / pl.Rt);
-  pl.cap = np * pl.max_chunks * rd::kPartsPerTile;
+  // a CTA pair (scan_pair.cu) emits one partial list per CTA and query of a tile
+  pl.cap = np * pl.max_chunks * rd::kPartsPerTile * (pair ? 2 : 1);
   pl.max_tiles = std::min<long long>(B * np, B * np / rd::kScanG + h->nlist) * pl.max_chunks + 1;
   return pl;
 }
@@ -124,10 +125,12 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   h->tail_wait();  // the previous asynchronous search's tail is enqueued (it shares the workspace)
   auto& w = h->ws;
   const int nl = h->nlist, d = h->d;
-  const Plan pl = make_plan(h, B, nprobe);
   // tensor-core tile widths: mixed (<= 16-query lists narrow, others wide) or one width; the
   // offloaded lists' host-planned tiles use one width
   const int tc_mode = h->tc_mode_for(B, nprobe);
+  // wide tiles over the x1 | x2 plane on CTA pairs (cta_group::2): RD_PAIR=1 only (slower)
+  const bool pair = tc_mode != 16 && h->tc_scan() && h->presplit && h->pair_scan && rd::scan_pair_stages(h->d) > 0;
+  const Plan pl = make_plan(h, B, nprobe, pair);
   const int tc_g = tc_mode == 16 ? 16 : 32;
   const int W = (int)((B + 31) / 32);
   w.qnorm.ensure(B);
@@ -302,7 +305,10 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
       launches += 1;
     }
     if (tc_mode != 16) {  // wide tiles: the 32-wide scan
-      CK(rd::launch_scan_tc(xm128, xm32, gmap, tc, h->num_sms, s, h->presplit, 32));
+      if (pair)
+        CK(rd::launch_scan_pair(xm128, xm32, gmap, tc, h->num_sms, s));
+      else
+        CK(rd::launch_scan_tc(xm128, xm32, gmap, tc, h->num_sms, s, h->presplit, 32));
       launches += 1;
     }
     if (stall) {
