@@ -255,6 +255,12 @@ int rd_merge_topk_device(int32_t G, int64_t B, int32_t k, const int64_t* d_shard
                          const float* d_shard_dists, int64_t* d_out_ids, float* d_out_dists,
                          void* stream);
 
+/* HBM read-stream peak of a device (GB/s), measured with the scan's load pattern (persistent
+ * CTAs, 32 KiB bulk-copy stages, released on arrival) over `bytes` of device memory, best of 5 after
+ * a warm-up: the denominator for a read-only kernel's roofline beside the copy bandwidth.
+ * CPU oracle: RD_ERR_INVALID. */
+int rd_device_read_bandwidth(int32_t device, uint64_t bytes, double* out_gbs);
+
 /* ---- multi-GPU shard groups ----
  * north_star: "the lists shard across the GPUs of one 8xB200 box, each shard returns a local
  * top-k, and the results are merged with an NCCL gather over NVLink". A group holds G row stripes

@@ -748,6 +748,11 @@ int rd_merge_topk_device(int32_t G, int64_t B, int32_t k, const int64_t* a, cons
   return fail(RD_ERR_INVALID, "cpu oracle has no device merge");
 }
 
+int rd_device_read_bandwidth(int32_t device, uint64_t bytes, double* out_gbs) {
+  (void)device; (void)bytes; (void)out_gbs;
+  return fail(RD_ERR_INVALID, "cpu oracle has no device");
+}
+
 int rd_timing_stages(rd_index* h, int32_t on) {
   (void)on;
   if (!h) return fail(RD_ERR_INVALID, "null index");

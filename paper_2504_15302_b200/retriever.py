@@ -149,6 +149,7 @@ _SIGS = {
     "rd_exact_l2": (C.c_float, [_FP, _FP, C.c_int32]),
     "rd_llm_reservation_bytes": (C.c_int, [C.POINTER(LlmReservation), C.POINTER(C.c_double)]),
     "rd_staging_depth": (C.c_int32, [C.c_double, C.c_double]),
+    "rd_device_read_bandwidth": (C.c_int, [C.c_int32, C.c_uint64, C.POINTER(C.c_double)]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGS)
 
@@ -307,6 +308,12 @@ class Library:
 
     def staging_depth(self, free_bytes: float, item_bytes: float) -> int:
         return int(self.lib.rd_staging_depth(free_bytes, item_bytes))
+
+    def device_read_bandwidth(self, device: int = 0, nbytes: int = 8 << 30) -> float:
+        """HBM read-stream peak (GB/s) measured with the scan's load pattern (rd_device_read_bandwidth)."""
+        out = C.c_double()
+        self.check(self.lib.rd_device_read_bandwidth(device, nbytes, C.byref(out)), "device_read_bandwidth")
+        return out.value
 
 
 def _check_queries(queries: np.ndarray, d: int) -> np.ndarray:

@@ -136,3 +136,11 @@ def test_async_search_with_offloaded_lists(engine, oracle):
     assert any(p for *_, p in outs)
     assert min(h / dv for _, _, h, dv, _ in outs) < 0.5, [(h, dv) for _, _, h, dv, _ in outs]
     assert e.search(q, 32, 10).stats["h2d_list_bytes"] > 0
+
+
+def test_device_read_bandwidth(engine):
+    """The read-stream peak probe the bench's roofline reports against: plausible for HBM3e."""
+    gbs = engine.device_read_bandwidth(0, 2 << 30)
+    assert 3000.0 < gbs < 9000.0
+    with pytest.raises(ParseError):
+        engine.device_read_bandwidth(0, 1024)
