@@ -787,7 +787,7 @@ __global__ void __launch_bounds__(NT) coarse_select_kernel(const SelectParams p)
             const int r = rb + grp;
             const long long sr = sr0 + min(r, p.seed_rows - 1);
             const RowRef x = p.x12 ? row_split3(p.x12, p.x3, sr, d) : row_f32(p.arena + (size_t)sr * d);
-            const float v = l2_group8_f32_row<16>(q, x, d, j8);
+            const float v = d % 64 == 0 ? l2_group8_f32_chunks(q, x, d, j8) : l2_group8_f32_row<16>(q, x, d, j8);
             if (r < p.seed_rows) e = fmaxf(e, v);
           }
         }

@@ -183,10 +183,20 @@ __global__ void __launch_bounds__(256, kStage ? 1 : 8) merge_rerank_kernel(const
     RD_TS(3);
     e = exact_l2_group8_qd_cnt(qd, st + c * ds, have ? p.d : 0, j8);
   } else {
-    // a padded slot runs zero terms so the warp stays converged for the shuffles; rows from HBM:
-    // 16 loads deep (32 registers: one wave of 8 CTAs per SM)
-    const RowRef x = sr >= 0 ? row_split3(p.x12, p.x3, sr, p.d) : row_f32(xp ? xp : q);
-    e = exact_l2_group8_row<16>(q, x, p.d, j8, have ? p.d : 0);
+    // a padded slot runs zero terms so the warp stays converged for the shuffles; fp32 rows from HBM:
+    // 16 loads deep (32 registers: one wave of 8 CTAs per SM); split3 rows: 128-bit loads and a
+    // transpose through a per-group scratch (exact_l2_group8_split3), warp-uniform calls
+    __shared__ __align__(16) float scr[8][4][72];  // [warp][group]: 64 floats + 8 of bank padding
+    if (p.x12 && p.d % 64 == 0) {
+      const __nv_bfloat16* x12 = p.x12 + (size_t)(sr >= 0 ? sr : 0) * 2 * p.d;
+      const __nv_bfloat16* x3 = p.x3 + (size_t)(sr >= 0 ? sr : 0) * p.d;
+      const float e3 = exact_l2_group8_split3(q, x12, x3, p.d, j8, sr >= 0, scr[warp][(tid >> 3) & 3]);
+      const float ef = exact_l2_group8_row<16>(q, row_f32(xp ? xp : q), p.d, j8, xp ? p.d : 0);
+      e = sr >= 0 ? e3 : ef;
+    } else {
+      const RowRef x = sr >= 0 ? row_split3(p.x12, p.x3, sr, p.d) : row_f32(xp ? xp : q);
+      e = exact_l2_group8_row<16>(q, x, p.d, j8, have ? p.d : 0);
+    }
   }
   if (!have) e = kInf;
   if (j8 == 0) ex_d[c] = e;

@@ -88,6 +88,52 @@ __device__ __forceinline__ float exact_l2_group8_qd(const double* qd, const floa
   s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
   return __double2float_rn(s);
 }
+// The canonical exact distance to a split3 row read from global memory, with 128-bit loads: per
+// 64-element block, lane j of the group loads and decodes chunk 8i + j (x1, x2, x3: one uint4 each),
+// the group transposes the block through its 64-float shared scratch (lane j then holds t = 64i + 8k
+// + j, k = 0..7, the canonical class order) and sums exactly as exact_l2_group8_impl. Every lane of
+// the warp must call it (it syncs the warp); have == false contributes nothing. d % 64 == 0.
+__device__ __forceinline__ float exact_l2_group8_split3(const float* q, const __nv_bfloat16* x12,
+                                                        const __nv_bfloat16* x3, int d, int j, bool have,
+                                                        float* scr) {
+  double s = 0.0;
+  for (int i = 0; i < d / 64; ++i) {
+    if (have) {
+      const int c = 8 * i + j;
+      const uint4 u1 = __ldg(reinterpret_cast<const uint4*>(x12) + c);
+      const uint4 u2 = __ldg(reinterpret_cast<const uint4*>(x12 + d) + c);
+      const uint4 u3 = __ldg(reinterpret_cast<const uint4*>(x3) + c);
+      const __nv_bfloat16* h1 = reinterpret_cast<const __nv_bfloat16*>(&u1);
+      const __nv_bfloat16* h2 = reinterpret_cast<const __nv_bfloat16*>(&u2);
+      const __nv_bfloat16* h3 = reinterpret_cast<const __nv_bfloat16*>(&u3);
+      float xv[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        xv[e] = __fadd_rn(__fadd_rn(__bfloat162float(h1[e]), __bfloat162float(h2[e])), __bfloat162float(h3[e]));
+      reinterpret_cast<float4*>(scr + 8 * j)[0] = make_float4(xv[0], xv[1], xv[2], xv[3]);
+      reinterpret_cast<float4*>(scr + 8 * j)[1] = make_float4(xv[4], xv[5], xv[6], xv[7]);
+    }
+    __syncwarp();
+    if (have) {
+      float xv[8], qv[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        xv[k] = scr[8 * k + j];
+        qv[k] = __ldg(q + 64 * i + 8 * k + j);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double df = __dsub_rn((double)qv[k], (double)xv[k]);
+        s = __dadd_rn(s, __dmul_rn(df, df));
+      }
+    }
+    __syncwarp();
+  }
+  s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
+  s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+  s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 4));
+  return __double2float_rn(s);
+}
 // exact_l2_group8_qd over the first cnt elements (cnt < d: a padded slot passes 0 and its group
 // stays converged for the shuffles); x in shared memory
 __device__ __forceinline__ float exact_l2_group8_qd_cnt(const double* qd, const float* x, int cnt, int j) {
