@@ -11,6 +11,7 @@
 #include <float.h>
 
 #include "ivf_kernels.cuh"
+#include "plan_device.cuh"
 #include "rd_device.cuh"
 
 namespace rd {
@@ -331,12 +332,76 @@ __device__ __forceinline__ float block_reduce_max(float v, float* sh) {
 // exact top-nprobe set is then the sure-in candidates plus the best ambiguous ones by (canonical
 // exact distance, list id) — only those few need the fp64 sum. Exact-order mode (rd_probe) and
 // uncertified queries recompute every candidate (or every centroid) exactly.
+// The B = 1 plan inside the selection CTA (SelectParams::fp_tiles): the probes this CTA just wrote,
+// each probed resident list cut into chunk_rows chunks (the planner's R / Rt rule), one narrow
+// tensor-core tile per chunk at the block-scanned offset; list_q = query 0; counters and tile count
+// as finish_counters writes them.
+template <int NT>
+__device__ __forceinline__ void fused_plan_b1(const SelectParams& p, int np, SmallPlanSmem& sm) {
+  constexpr int PPT = (kSelMaxCand + NT - 1) / NT;
+  const int tid = threadIdx.x;
+  int l[PPT], len[PPT], rl[PPT], ch[PPT];
+  long long g0[PPT], r0[PPT];
+  int v[kTileCats] = {0, 0, 0};
+  unsigned long long cc[3] = {0ull, 0ull, 0ull};
+  if (tid < kTileCats) sm.carry[tid] = 0;
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {  // thread t owns probe positions [t * PPT, (t + 1) * PPT)
+    const int i = tid * PPT + k;
+    l[k] = i < np ? p.probes[i] : -1;
+  }
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    ch[k] = 0, len[k] = 0, rl[k] = p.fp_R, g0[k] = 0, r0[k] = -1;
+    if (l[k] < 0) continue;
+    g0[k] = p.list_off[l[k]];
+    len[k] = (int)(p.list_off[l[k] + 1] - g0[k]);
+    r0[k] = p.res_row0[l[k]];
+  }
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    const int i = tid * PPT + k;
+    if (l[k] < 0) continue;
+    p.fp_list_q[i] = 0;
+    cc[0] += 1;
+    cc[r0[k] >= 0 ? 1 : 2] += (unsigned long long)len[k];
+    if (r0[k] >= 0 && len[k] > 0) {
+      // tiles go out in probe order, so the queue's tail is the last eighth of the probes (the
+      // planner's list-id rule, tail_from, would scatter the short chunks through the queue)
+      rl[k] = chunk_rows(len[k], i >= np - np / 8 ? p.fp_Rt : p.fp_R);
+      ch[k] = (len[k] + rl[k] - 1) / rl[k];
+      v[kCatNarrow] += ch[k];
+    }
+  }
+  int ex[kTileCats];
+  block_scan_round<NT, kTileCats>(v, ex, sm.wsum, sm.carry);
+  int off = ex[kCatNarrow];
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    for (int c = 0; c < ch[k]; ++c) {
+      ScanTile T;
+      T.src_row = r0[k] + (long long)c * rl[k];
+      T.grow0 = g0[k] + (long long)c * rl[k];
+      T.list = l[k];
+      T.nrows = min(rl[k], len[k] - c * rl[k]);
+      T.qoff = tid * PPT + k;
+      T.nq = 1;
+      p.fp_tiles[off + c] = T;
+    }
+    off += ch[k];
+  }
+  PlanParams fp{};
+  fp.counters = p.fp_counters;
+  fp.meta = p.fp_meta;
+  finish_counters<NT>(fp, cc, sm.wcnt, sm.carry);
+}
+
 template <bool kStage, int NT>
 __global__ void __launch_bounds__(NT) coarse_select_kernel(const SelectParams p) {
   RD_TS(13);  // entry, before the wait on the previous kernel
   RD_PDL_PROLOGUE();
   extern __shared__ __align__(16) uint32_t keys[];
-  __shared__ int hist[2048];
+  __shared__ __align__(16) int hist[2048];  // (and the B = 1 fused plan's scratch)
   __shared__ int scan_sh[8];
   __shared__ float fsh[8];
   __shared__ int cand[kSelMaxCand];
@@ -758,6 +823,12 @@ __global__ void __launch_bounds__(NT) coarse_select_kernel(const SelectParams p)
     __syncthreads();
   }
   RD_TS(5);
+  if (kStage && p.fp_tiles) {  // B = 1: plan the scan here (the probes are written)
+    static_assert(sizeof(SmallPlanSmem) <= sizeof(hist), "fused plan scratch");
+    __syncthreads();
+    fused_plan_b1<NT>(p, np, *reinterpret_cast<SmallPlanSmem*>(hist));
+    __syncthreads();
+  }
 
   // fused seed: fp32 distances to the first 32 rows of the seeding list; threshold = max * (1 + rel
   // bound) + 2 eps_scan, a valid upper bound on the final 32nd-best approximate distance, so the
@@ -835,13 +906,23 @@ cudaError_t launch_qprep(const QprepArgs& a, cudaStream_t s) {
   return launch_k(qprep_kernel, dim3((unsigned)(blocks < 148 * 8 ? blocks : 148 * 8)), dim3(256), 0, s, a);
 }
 
-cudaError_t launch_select(const SelectParams& p, bool stage, cudaStream_t s, int num_sms) {
-  if (p.nprobe + kCoarseExtra > kSelMaxCand) return cudaErrorInvalidValue;
+namespace {
+size_t select_staged_bytes(const SelectParams& p) {
   const size_t keys = sizeof(uint32_t) * (size_t)((p.nlist + 3) & ~3);
   const size_t qd = sizeof(double) * (size_t)p.d;
   const size_t ds = (size_t)p.d + (p.x12 ? p.d / 2 : 0) + kStagePad;  // the kernel's staged row stride
-  const size_t staged = keys + qd + sizeof(float) * ((size_t)p.d + 32 * ds);
-  if (stage && staged <= 200 * 1024)
+  return keys + qd + sizeof(float) * ((size_t)p.d + 32 * ds);
+}
+}  // namespace
+
+bool select_staged(const SelectParams& p, bool stage) { return stage && select_staged_bytes(p) <= 200 * 1024; }
+
+cudaError_t launch_select(const SelectParams& p, bool stage, cudaStream_t s, int num_sms) {
+  if (p.nprobe + kCoarseExtra > kSelMaxCand) return cudaErrorInvalidValue;
+  const size_t keys = sizeof(uint32_t) * (size_t)((p.nlist + 3) & ~3);
+  const size_t staged = select_staged_bytes(p);
+  if (p.fp_tiles && !select_staged(p, stage)) return cudaErrorInvalidValue;  // the fused plan is staged-only
+  if (select_staged(p, stage))
     return launch_k(coarse_select_kernel<true, kSelThreads>, dim3(p.B), dim3(kSelThreads), staged, s, p);
   // large batches (enough CTAs to hide latency) or very large nlist: the direct-load variant. Past
   // one resident wave of 256-thread CTAs (64 registers and ~35 KiB each: 4 per SM), 128 threads

@@ -495,6 +495,7 @@ struct rd_index {
   bool dbg_chain = std::getenv("RD_DEBUG_CHAIN") != nullptr;
   int stage_max_b = -1;  // batches up to this size stage exact-distance rows in smem (-1: 2 x SMs)
   int tiles_per_sm = 0;  // scan tiles per SM the planner aims for (RD_TILES_PER_SM; 0 = by batch, make_plan)
+  bool fuse_plan = !(std::getenv("RD_FUSE_PLAN") && std::atoi(std::getenv("RD_FUSE_PLAN")) == 0);  // B = 1 plan in the selection
   // scan_pair.cu for wide tiles: opt-in (RD_PAIR=1) — measured 6 % slower at B = 1024
   bool pair_scan = std::getenv("RD_PAIR") && std::atoi(std::getenv("RD_PAIR")) == 1;
   long long seed_max_b = 1LL << 40;  // batches up to this size seed the scan's pruning threshold (RD_SEED_MAX_B)

@@ -209,10 +209,19 @@ struct SelectParams {
   // split3 resident store (host.cuh; arena == nullptr then): seeding rows are rebuilt from it
   const __nv_bfloat16* x12 = nullptr;
   const __nv_bfloat16* x3 = nullptr;
+  // B = 1 without offloaded lists, every list a tensor-core list: the selection CTA also plans the
+  // scan (fp_tiles != nullptr: the narrow tile array; no plan launch): one tile per chunk of each
+  // probed list, list_q, the byte counters and the tile count (the sorted-pairs plan's outputs)
+  ScanTile* fp_tiles = nullptr;
+  int* fp_list_q = nullptr;
+  int* fp_meta = nullptr;
+  unsigned long long* fp_counters = nullptr;
+  int fp_R = 0, fp_Rt = 0;
 };
 // stage: q and candidate rows go through shared memory (latency-bound small batches)
 // num_sms: batches beyond one resident wave of 256-thread CTAs (4 per SM) use 128-thread CTAs
 cudaError_t launch_select(const SelectParams& p, bool stage, cudaStream_t s, int num_sms = 148);
+bool select_staged(const SelectParams& p, bool stage);  // the staged (small-batch) variant will run
 
 
 // Rows per scan chunk of a list of `len` rows under the plan's cap R (a multiple of kTcRows): the

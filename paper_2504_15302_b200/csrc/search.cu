@@ -209,6 +209,18 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
                     w.list_ntile.p, w.list_toff.p, w.list_q.p, {w.tiles16.p, w.tiles.p, w.ff_tiles.p}, w.meta(),
                     w.counters(), (int)B, nl, nprobe, pl.R, h->tc_scan() ? h->tc_min_q : 1 << 30, tc_mode,
                     pl.Rt, pl.tail_from};
+  // B = 1, every list resident and a tensor-core list: the selection CTA plans the scan itself
+  // (one launch and one kernel boundary fewer; RD_FUSE_PLAN=0 for A/B)
+  const bool fuse_plan = B == 1 && !wide && !sel_all && h->slots == 0 && h->tc_scan() && h->tc_min_q <= 1 &&
+                         tc_mode != 32 && h->fuse_plan && rd::select_staged(sp, h->stage_rows(B));
+  if (fuse_plan) {
+    sp.fp_tiles = w.tiles16.p;
+    sp.fp_list_q = w.list_q.p;
+    sp.fp_meta = w.meta();
+    sp.fp_counters = w.counters();
+    sp.fp_R = pl.R;
+    sp.fp_Rt = pl.Rt;
+  }
   if (sel_all) {
     size_t sb = 0;
     void* scratch = select_all_scratch(h, B, &sb);
@@ -250,10 +262,12 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     }
     return;
   }
-  if (chain) pp.dbg = chain + 32;
-  h->traced("plan", s, pp.dbg, [&] { CK(rd::launch_plan(pp, s)); });
-  if (use_bm) w.bitmap_clean = true;  // list_fill, now enqueued, clears every bit the selection sets
-  launches += use_bm ? 3 : 1;
+  if (!fuse_plan) {
+    if (chain) pp.dbg = chain + 32;
+    h->traced("plan", s, pp.dbg, [&] { CK(rd::launch_plan(pp, s)); });
+    if (use_bm) w.bitmap_clean = true;  // list_fill, now enqueued, clears every bit the selection sets
+    launches += use_bm ? 3 : 1;
+  }
   const bool staged = h->stage_events;
   if (staged) CK(cudaEventRecord(e1, s));
 
