@@ -477,29 +477,75 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* sd = sm.stage_d + ew * 32;                 // per-warp compaction batch
     long long* sk = sm.stage_k + ew * 32;
     uint32_t rtc = 0;
+    // Per owned slot j: the query whose running top-32 the slot holds (cq, -1: none) and that list.
+    // A list is written out (one partial list) only when the slot's query changes or the CTA runs
+    // out of tiles: consecutive tiles of one query — the chunks of a list, and every tile at B = 1 —
+    // keep one list, so the merge reads far fewer partials (B = 1: ~5 per CTA -> 1).
+    float ld[kOwn];
+    long long lk[kOwn];
+    int cq[kOwn];
+#pragma unroll
+    for (int j = 0; j < kOwn; ++j) {
+      ld[j] = kInf;
+      lk[j] = kNoKey;
+      cq[j] = -1;
+    }
+    // writes out the lists of the slots in fmask (slot reservations issued together, one lane per
+    // slot: one atomic round trip per flush) and empties them
+    auto flush = [&](unsigned fmask) {
+      int myqid = 0, myps = 0;
+      bool myhas = false;
+#pragma unroll
+      for (int j = 0; j < kOwn; ++j) {
+        const bool has = ((fmask >> j) & 1u) && cq[j] >= 0 && __shfl_sync(0xffffffffu, ld[j], 0) != kInf;
+        if (lane == j) {
+          myhas = has;
+          myqid = cq[j];
+        }
+      }
+      if (myhas) myps = atomicAdd(p.part_count + myqid, 1);
+#pragma unroll
+      for (int j = 0; j < kOwn; ++j) {
+        const int ps = __shfl_sync(0xffffffffu, myps, j);
+        const bool has = __shfl_sync(0xffffffffu, myhas ? 1 : 0, j) != 0;
+        if (has && ps < p.part_cap) {
+          const size_t o = ((size_t)cq[j] * p.part_cap + ps) * kTopK + lane;
+          p.part_dist[o] = ld[j];
+          p.part_row[o] = lk[j] == kNoKey ? -1 : (int)lk[j];
+        }
+        if ((fmask >> j) & 1u) {
+          ld[j] = kInf;
+          lk[j] = kNoKey;
+        }
+      }
+    };
     for (uint32_t ti = 0;; ++ti) {
       const int slot = ti & 1;
       RD_TWAIT(&sm.tfull[slot], (ti >> 1) & 1, 7);
       const int t = sm.tring[slot];
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.tempty[slot]);
-      if (t < 0) break;
+      if (t < 0) {
+        flush((1u << kOwn) - 1u);
+        break;
+      }
       const ScanTile T = p.tiles[t];
       const int nq = T.nq;
-      float qn[kOwn];  // ||q||^2 of the owned queries (added by the owner, not per row)
+      int nqid[kOwn];
+      unsigned fmask = 0;
 #pragma unroll
       for (int j = 0; j < kOwn; ++j) {
         const int g = ew + 4 * j;
-        qn[j] = g < nq ? __ldg(p.qnorm + __ldg(p.list_q + T.qoff + g)) : 0.f;
+        nqid[j] = g < nq ? __ldg(p.list_q + T.qoff + g) : -1;
+        if (nqid[j] != cq[j]) fmask |= 1u << j;
       }
-      float ld[kOwn], qt[kOwn];
-      long long lk[kOwn];
+      if (fmask) flush(fmask);
+      float qn[kOwn], qt[kOwn];  // ||q||^2 of the owned queries (added by the owner, not per row)
 #pragma unroll
       for (int j = 0; j < kOwn; ++j) {
-        const int g = ew + 4 * j;
-        ld[j] = kInf;
-        lk[j] = kNoKey;
-        qt[j] = g < nq ? ord2f(*(volatile int*)(p.qthr + __ldg(p.list_q + T.qoff + g))) : kInf;
+        cq[j] = nqid[j];
+        qn[j] = cq[j] >= 0 ? __ldg(p.qnorm + cq[j]) : 0.f;
+        qt[j] = cq[j] >= 0 ? ord2f(*(volatile int*)(p.qthr + cq[j])) : kInf;
       }
       for (int rt = 0; rt * kRows < T.nrows; ++rt, ++rtc) {
         const int a = rtc & 1;
@@ -575,38 +621,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      // per-query top-32 of this tile -> one partial list per query. The slot reservations
-      // (atomicAdd on the query's partial count) and threshold updates of the warp's queries are
-      // issued together, one lane per query, so a tile end costs one atomic round trip rather than
-      // one per query (short tiles made that the scan's per-tile overhead).
-      int myqid = 0, myps = 0;
-      bool myhas = false;
+      // the global pruning threshold: every tile end, fire-and-forget (the list itself waits for
+      // its query to change)
       float myl31 = kInf;
 #pragma unroll
       for (int j = 0; j < kOwn; ++j) {
-        const int g = ew + 4 * j;
         const float l31 = __shfl_sync(0xffffffffu, ld[j], p.thr_rank);  // the bound the merge needs
-        const bool has = g < nq && __shfl_sync(0xffffffffu, ld[j], 0) != kInf;  // something survived
-        if (lane == j) {
-          myhas = has;
-          myl31 = l31;
-          if (g < nq) myqid = __ldg(p.list_q + T.qoff + g);
-        }
+        if (lane == j) myl31 = l31;
       }
-      if (myhas) {
-        myps = atomicAdd(p.part_count + myqid, 1);
-        if (myl31 != kInf) atomicMin(p.qthr + myqid, f2ord(myl31));
-      }
+      if (lane < kOwn && myl31 != kInf) {
+        int myq = 0;
 #pragma unroll
-      for (int j = 0; j < kOwn; ++j) {
-        const int ps = __shfl_sync(0xffffffffu, myps, j);
-        const int qid = __shfl_sync(0xffffffffu, myqid, j);
-        const bool has = __shfl_sync(0xffffffffu, myhas ? 1 : 0, j) != 0;
-        if (has && ps < p.part_cap) {
-          const size_t o = ((size_t)qid * p.part_cap + ps) * kTopK + lane;
-          p.part_dist[o] = ld[j];
-          p.part_row[o] = lk[j] == kNoKey ? -1 : (int)lk[j];
-        }
+        for (int j = 0; j < kOwn; ++j)
+          if (lane == j) myq = cq[j];
+        if (myq >= 0) atomicMin(p.qthr + myq, f2ord(myl31));
       }
     }
   }
