@@ -224,7 +224,10 @@ __device__ int block_excl_scan(int v, int* sh, int* total) {
   return base + x - v;
 }
 
-constexpr int kSelThreads = 256;    // small batches (staged rows): more threads per query
+// small batches (staged rows, one CTA per SM): 256 threads — 1024 measured 1-2 % slower at B = 1-8
+// (more threads per barrier; the phases are latency chains, not throughput)
+constexpr int kSelThreadsStaged = 256;
+constexpr int kSelThreads = 256;
 constexpr int kSelThreadsLarge = 128;  // large batches: 7 CTAs per SM, one resident wave at B = 1024
 constexpr int kSelMaxCand = 512;
 
@@ -402,8 +405,8 @@ __global__ void __launch_bounds__(NT) coarse_select_kernel(const SelectParams p)
   RD_PDL_PROLOGUE();
   extern __shared__ __align__(16) uint32_t keys[];
   __shared__ __align__(16) int hist[2048];  // (and the B = 1 fused plan's scratch)
-  __shared__ int scan_sh[8];
-  __shared__ float fsh[8];
+  __shared__ int scan_sh[32];
+  __shared__ float fsh[32];
   __shared__ int cand[kSelMaxCand];
   __shared__ float cdist[kSelMaxCand];
   __shared__ uint32_t sel_prefix, sel_k;
@@ -452,9 +455,9 @@ __global__ void __launch_bounds__(NT) coarse_select_kernel(const SelectParams p)
       bulk_g2s(st + i * ds, p.arena + (size_t)sr * d, (uint32_t)(d * 4), &bar);
     }
   };
-  // a staged seeding row as a RowRef
+  // a staged seeding row as a RowRef (32 staging slots: groups beyond them read slot 31, masked)
   auto staged_ref = [&](int i) {
-    const float* slot = st + i * ds;
+    const float* slot = st + min(i, 31) * ds;
     return p.x12 ? RowRef{nullptr, reinterpret_cast<const __nv_bfloat16*>(slot),
                           reinterpret_cast<const __nv_bfloat16*>(slot + d)}
                  : row_f32(slot);
@@ -685,18 +688,19 @@ __global__ void __launch_bounds__(NT) coarse_select_kernel(const SelectParams p)
     if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0) p.dbg[14] = (unsigned long long)na;
     if (below_s >= np && need >= 0 && need <= na) {
       if (need > 0 && need < na) {  // the best `need` ambiguous candidates by exact (distance, list id)
-        for (int a0 = 0; a0 < na; a0 += NT / 8) {
-          const int rows = min(NT / 8, na - a0);
+        constexpr int kAmb = kStage ? (NT / 8 < 32 ? NT / 8 : 32) : NT / 8;  // (32 staging slots)
+        for (int a0 = 0; a0 < na; a0 += kAmb) {
+          const int rows = min(kAmb, na - a0);
           const int a = a0 + grp;
           float e;
           if constexpr (kStage) {
             stage_bulk(rows, [&](int r) { return p.centroids + (size_t)cand[ambl[a0 + r]] * d; });
-            e = exact_l2_group8_qd(qd, st + grp * ds, a < na ? d : 0, j8);
+            e = exact_l2_group8_qd(qd, st + min(grp, 31) * ds, grp < rows ? d : 0, j8);
             __syncthreads();  // the staging area is reused by the next chunk
           } else {
             e = exact_l2_group8_impl<true, 16>(q, p.centroids + (size_t)cand[ambl[a < na ? a : na - 1]] * d, d, j8);
           }
-          if (a < na && j8 == 0) adist[a] = e;
+          if (grp < rows && j8 == 0) adist[a] = e;
         }
         __syncthreads();
         for (int a = tid; a < na; a += NT) {
@@ -923,7 +927,7 @@ cudaError_t launch_select(const SelectParams& p, bool stage, cudaStream_t s, int
   const size_t staged = select_staged_bytes(p);
   if (p.fp_tiles && !select_staged(p, stage)) return cudaErrorInvalidValue;  // the fused plan is staged-only
   if (select_staged(p, stage))
-    return launch_k(coarse_select_kernel<true, kSelThreads>, dim3(p.B), dim3(kSelThreads), staged, s, p);
+    return launch_k(coarse_select_kernel<true, kSelThreadsStaged>, dim3(p.B), dim3(kSelThreadsStaged), staged, s, p);
   // large batches (enough CTAs to hide latency) or very large nlist: the direct-load variant. Past
   // one resident wave of 256-thread CTAs (64 registers and ~35 KiB each: 4 per SM), 128 threads
   // and no smem copy of q fit 7 per SM (1024 queries in one wave: 65 -> 55 us on B200)
