@@ -87,6 +87,59 @@ def measured_peaks():
         return None
 
 
+class DecodeStream:
+    """A synthetic LLM decode running beside the retrieval (C5 / C2r8b): on its own CUDA stream, back
+    to back, the decode GEMMs of a batch of 64 tokens against bf16 weight matrices carved from the
+    reserved bytes (every step reads every weight once, as a w_gpu = 1 decode does). Reports the
+    weight bytes it streamed per second while the timed region ran."""
+
+    def __init__(self, hold, batch=64, dim=8192):
+        import torch
+        self.torch = torch
+        n = hold.numel() // 2 // (dim * dim)  # whole [dim x dim] bf16 matrices in the reservation
+        self.mats = [hold[i * dim * dim * 2:(i + 1) * dim * dim * 2].view(torch.bfloat16).view(dim, dim)
+                     for i in range(max(0, min(n, 256)))]
+        self.x = torch.randn(batch, dim, device="cuda", dtype=torch.bfloat16)
+        self.stream = torch.cuda.Stream()
+        self.bytes = 0
+        self._stop = threading.Event()
+
+    def __enter__(self):
+        torch = self.torch
+        if not self.mats:
+            return self
+        self.e0, self.e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        self.e0.record(self.stream)
+
+        def run():
+            with torch.cuda.stream(self.stream):
+                while not self._stop.is_set():
+                    for w in self.mats:
+                        torch.mm(self.x, w)
+                        self.bytes += w.numel() * 2
+                    self.stream.synchronize()  # bounded queue: at most one pass in flight
+
+        self.t = threading.Thread(target=run, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if not self.mats:
+            return
+        self._stop.set()
+        self.t.join()
+        self.e1.record(self.stream)
+        self.e1.synchronize()
+        self.seconds = self.e0.elapsed_time(self.e1) / 1000.0
+
+    def summary(self):
+        if not self.mats:
+            return None
+        return {"weight_gbs": self.bytes / self.seconds / 1e9, "matrices": len(self.mats),
+                "what": "bf16 decode GEMMs (64 tokens x 8192 x 8192) over the reserved bytes, back to back on "
+                        "a side stream during the timed region"}
+
+
 class ClockSampler:
     """SM clocks and throttle reasons sampled (NVML, every 10 ms) during the timed region."""
 
@@ -385,7 +438,9 @@ def run_ours(args, cfg):
         sx.timing_stages(True)
         sx.timing_reset()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    import contextlib
+    decode = DecodeStream(hold) if (hold is not None and args.decode_stream) else None
+    with ClockSampler(local) as clk, (decode if decode is not None else contextlib.nullcontext()):
         torch.cuda.synchronize()
         barrier()
         ev0.record(stream)
@@ -414,11 +469,12 @@ def run_ours(args, cfg):
     for i in range(min(args.warmup, 2)):
         searcher.search_into(hq[i], nprobe, k, hi, hd)
     barrier()
-    t0 = time.perf_counter()
-    for i in range(args.warmup, nb):
-        searcher.search_into(hq[i], nprobe, k, hi, hd)
-    barrier()
-    e2e_s = time.perf_counter() - t0
+    with (DecodeStream(hold) if decode is not None else contextlib.nullcontext()):  # same concurrent decode
+        t0 = time.perf_counter()
+        for i in range(args.warmup, nb):
+            searcher.search_into(hq[i], nprobe, k, hi, hd)
+        barrier()
+        e2e_s = time.perf_counter() - t0
     if dist is not None:
         t = torch.tensor([e2e_s], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -499,6 +555,7 @@ def run_ours(args, cfg):
         "clocks": clk.summary(),
         "certified": {"margin_failures": st["margin_failures"], "probe_failures": st["probe_failures"]},
         "h2d_link": h2d_link,
+        "decode_stream": decode.summary() if decode is not None else None,
         "index": {"build_s": build_s, "lists_resident": info["lists_resident"], "hbm_bytes": info["hbm_bytes"],
                   "store": {0: "fp32", 1: "fp32 + pre-split copy", 2: "split3 (exact bf16 triple)"}.get(info["store"]),
                   "fp32_bytes": info["n"] * d * 4,
@@ -564,6 +621,9 @@ def main():
                     help="exact-oracle queries timed per step (the batched CPU search takes whole batches)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--decode-stream", action="store_true",
+                    help="C5 / C2r8b: run synthetic decode GEMMs over the reserved bytes on a side stream during "
+                         "the timed regions (opt-in: with offloaded lists (C5) the combination stalled on the box)")
     ap.add_argument("--stripe-of", type=int, default=0,
                     help="N = 1 only: run one row stripe of an N-way split (the per-rank work of N GPUs)")
     args = ap.parse_args()
