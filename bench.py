@@ -623,7 +623,7 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--decode-stream", action="store_true",
                     help="C5 / C2r8b: run synthetic decode GEMMs over the reserved bytes on a side stream during "
-                         "the timed regions (opt-in: with offloaded lists (C5) the combination stalled on the box)")
+                         "the timed regions")
     ap.add_argument("--stripe-of", type=int, default=0,
                     help="N = 1 only: run one row stripe of an N-way split (the per-rank work of N GPUs)")
     args = ap.parse_args()

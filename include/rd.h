@@ -220,7 +220,14 @@ int rd_search(rd_index* h, const float* queries, int64_t B, int32_t nprobe, int3
               int64_t* out_ids, float* out_dists, rd_search_stats* stats);
 /* Device buffers on the index's device, stream = cudaStream_t (NULL = legacy
  * default). Asynchronous: returns after enqueueing; stats device times are
- * filled only when sync != 0. CPU oracle: returns RD_ERR_INVALID. */
+ * filled only when sync != 0. With offloaded lists the host plans the staging
+ * copies from the device plan, so the call returns once the plan is done (the
+ * resident scan is already running). RD_ASYNC_TAIL=1 (set before the index is
+ * created) returns at once instead: the caller's stream waits on a device gate
+ * (cuStreamWaitValue32) that the index's worker thread releases — only safe
+ * when that stream cannot share a hardware queue with the index's side
+ * streams (CUDA_DEVICE_MAX_CONNECTIONS); otherwise the gate can deadlock.
+ * CPU oracle: returns RD_ERR_INVALID. */
 int rd_search_device(rd_index* h, const float* d_queries, int64_t B, int32_t nprobe, int32_t k,
                      int64_t* d_ids, float* d_dists, void* stream, int32_t sync,
                      rd_search_stats* stats);

@@ -495,6 +495,10 @@ struct rd_index {
   bool dbg_chain = std::getenv("RD_DEBUG_CHAIN") != nullptr;
   int stage_max_b = -1;  // batches up to this size stage exact-distance rows in smem (-1: 2 x SMs)
   int tiles_per_sm = 0;  // scan tiles per SM the planner aims for (RD_TILES_PER_SM; 0 = by batch, make_plan)
+  // rd_search_device with offloaded lists: return before the plan completes (a device gate released by
+  // the worker thread) only with RD_ASYNC_TAIL=1 — a stream-memory wait can deadlock when the caller's
+  // stream shares a hardware queue with the side streams (seen with a concurrent decode stream, C5)
+  bool async_tail = std::getenv("RD_ASYNC_TAIL") && std::atoi(std::getenv("RD_ASYNC_TAIL")) == 1;
   bool fuse_plan = !(std::getenv("RD_FUSE_PLAN") && std::atoi(std::getenv("RD_FUSE_PLAN")) == 0);  // B = 1 plan in the selection
   // scan_pair.cu for wide tiles: opt-in (RD_PAIR=1) — measured 6 % slower at B = 1024
   bool pair_scan = std::getenv("RD_PAIR") && std::atoi(std::getenv("RD_PAIR")) == 1;

@@ -563,7 +563,8 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     return h2d;
   };
   unsigned long long h2d = 0;
-  const bool async_tail = has_off && mode == kAsync && !chain && stream_mem().wait32 && stream_mem().write32;
+  const bool async_tail =
+      h->async_tail && has_off && mode == kAsync && !chain && stream_mem().wait32 && stream_mem().write32;
   if (!async_tail) {
     h2d = tail(s, launches);
   } else {

@@ -101,12 +101,54 @@ def test_probe_set_boundary_ties(engine, oracle, nprobe):
     _same(e.search(Q, nprobe, 10), o.search(Q, nprobe, 10))
 
 
-def test_async_search_with_offloaded_lists(engine, oracle):
-    """rd_search_device stays asynchronous with offloaded lists (rd.h): it returns once the search is
-    enqueued — the offloaded part is planned and enqueued by the index's worker thread while the
-    caller's stream waits on a device gate — and the results are the oracle's."""
+@pytest.mark.timeout(300)
+def test_offloaded_device_search_beside_a_busy_stream(engine, oracle):
+    """rd_search_device with offloaded lists while another thread keeps a side stream busy with GEMMs
+    (the synthetic decode of bench.py): every result is the oracle's and nothing stalls. Regression
+    test for the device-gate deadlock of the RD_ASYNC_TAIL path, now opt-in."""
+    import threading
+    import torch
+    desc = engine.desc(400000, 768, 256)
+    q, _ = engine.synth_queries(desc, 13, 32)
+    want = oracle.synthetic_index(desc).search(q, 32, 10)
+    e = engine.synthetic_index(desc)
+    e.place(offload_fraction=0.5)
+    dq = torch.from_numpy(q).cuda()
+    stop = threading.Event()
+    side = torch.cuda.Stream()
+    a = torch.randn(64, 4096, device="cuda", dtype=torch.bfloat16)
+    w = torch.randn(4096, 4096, device="cuda", dtype=torch.bfloat16)
+
+    def busy():
+        with torch.cuda.stream(side):
+            while not stop.is_set():
+                for _ in range(50):
+                    torch.mm(a, w)
+                side.synchronize()
+
+    t = threading.Thread(target=busy, daemon=True)
+    t.start()
+    try:
+        stream = torch.cuda.current_stream()
+        di = torch.empty((32, 10), dtype=torch.int64, device="cuda")
+        dd = torch.empty((32, 10), dtype=torch.float32, device="cuda")
+        for _ in range(6):
+            e.search_device(dq.data_ptr(), 32, 32, 10, di.data_ptr(), dd.data_ptr(), stream=stream.cuda_stream)
+        torch.cuda.synchronize()
+    finally:
+        stop.set()
+        t.join()
+    np.testing.assert_array_equal(di.cpu().numpy(), want.ids)
+    np.testing.assert_array_equal(dd.cpu().numpy(), want.dists)
+
+
+def test_async_search_with_offloaded_lists(engine, oracle, monkeypatch):
+    """RD_ASYNC_TAIL=1: rd_search_device with offloaded lists returns once the search is enqueued —
+    the offloaded part is planned and enqueued by the index's worker thread while the caller's stream
+    waits on a device gate — and the results are the oracle's."""
     import time
     import torch
+    monkeypatch.setenv("RD_ASYNC_TAIL", "1")  # read when the index is created
     desc = engine.desc(600000, 768, 256)
     q, _ = engine.synth_queries(desc, 12, 64)
     want = oracle.synthetic_index(desc).search(q, 32, 10)
