@@ -7,7 +7,7 @@ for path in sys.argv[1:]:
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     h, data = rows[hi], rows[hi + 1:]
     kn, mv = h.index("Kernel Name"), h.index("Metric Value")
-    ks = [(r[kn], float(r[mv].replace(",", ""))) for r in data if len(r) > mv]
+    ks = [(r[kn], float(r[mv].replace(",", ""))) for r in data if len(r) > mv and "read_stream" not in r[kn]]
     # the last search starts at the last qsplit/row_norms launch pair
     starts = [i for i, (n, _) in enumerate(ks) if "row_norms" in n or "qprep" in n]
     last = ks[starts[-1]:] if starts else ks
