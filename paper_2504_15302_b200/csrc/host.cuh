@@ -495,7 +495,6 @@ struct rd_index {
   bool dbg_chain = std::getenv("RD_DEBUG_CHAIN") != nullptr;
   int stage_max_b = -1;  // batches up to this size stage exact-distance rows in smem (-1: 2 x SMs)
   int tiles_per_sm = 0;  // scan tiles per SM the planner aims for (RD_TILES_PER_SM; 0 = by batch, make_plan)
-  long long prefetch_max_b = std::getenv("RD_PREFETCH_MAX_B") ? std::atoll(std::getenv("RD_PREFETCH_MAX_B")) : 8;
   // rd_search_device with offloaded lists: return before the plan completes (a device gate released by
   // the worker thread) only with RD_ASYNC_TAIL=1 — a stream-memory wait can deadlock when the caller's
   // stream shares a hardware queue with the side streams (seen with a concurrent decode stream, C5)

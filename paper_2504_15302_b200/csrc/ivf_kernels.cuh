@@ -92,15 +92,6 @@ struct TcScanParams {
   unsigned long long* stall = nullptr;  // profiling only (RD_DEBUG_STALL): per CTA x 12 barrier-wait cycles
   unsigned long long* dbg = nullptr;  // profiling only (RD_DEBUG_TS): per CTA [entry, ready, first tile, end] globaltimer
   int thr_rank = 31;       // as ScanParams::thr_rank
-  // small batches: each written partial list's best prefetch_m rows are prefetched into L2 from the
-  // resident store (split3 x12 + x3, or fp32 rows), so the merge's exact rerank reads hit L2
-  int prefetch_m = 0;
-  const int* row_list = nullptr;
-  const long long* list_off = nullptr;
-  const long long* res_row0 = nullptr;
-  const void* x12 = nullptr;
-  const void* x3 = nullptr;
-  const float* arena = nullptr;
 };
 
 size_t scan_smem_bytes(int d);

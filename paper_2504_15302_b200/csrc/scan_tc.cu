@@ -513,21 +513,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           p.part_dist[o] = ld[j];
           p.part_row[o] = lk[j] == kNoKey ? -1 : (int)lk[j];
         }
-        // small batches: pull the list's best rows into L2 for the merge's exact rerank
-        if (p.prefetch_m && has && lane < p.prefetch_m && lk[j] != kNoKey) {
-          const long long row = lk[j];
-          const int l = __ldg(p.row_list + row);
-          const long long r0 = __ldg(p.res_row0 + l);
-          if (r0 >= 0) {
-            const long long sr = r0 + (row - __ldg(p.list_off + l));
-            if (p.x12) {
-              bulk_prefetch_l2(reinterpret_cast<const char*>(p.x12) + (size_t)sr * 4 * p.d, (uint32_t)(4 * p.d));
-              bulk_prefetch_l2(reinterpret_cast<const char*>(p.x3) + (size_t)sr * 2 * p.d, (uint32_t)(2 * p.d));
-            } else if (p.arena) {
-              bulk_prefetch_l2(p.arena + (size_t)sr * p.d, (uint32_t)(4 * p.d));
-            }
-          }
-        }
         if ((fmask >> j) & 1u) {
           ld[j] = kInf;
           lk[j] = kNoKey;

@@ -287,15 +287,6 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
                       w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p, h->debug_skip};
   sc.thr_rank = thr_rank;
   tc.thr_rank = thr_rank;
-  if (B <= h->prefetch_max_b) {  // small batches: the scan prefetches the rerank's rows (scan_tc.cu)
-    tc.prefetch_m = m_rerank;
-    tc.row_list = h->d_row_list.p;
-    tc.list_off = h->d_list_off.p;
-    tc.res_row0 = h->d_res_row0.p;
-    tc.x12 = h->x12_dev();
-    tc.x3 = h->x3_dev();
-    tc.arena = h->arena.p;
-  }
   if (!h->split3 && (!h->tc_scan() || h->tc_min_q > 1)) {  // FFMA tiles exist only in these cases (fp32 store)
     CK(rd::launch_scan(h->map256, h->map32, sc, h->num_sms, s));
     launches += 1;
