@@ -234,8 +234,10 @@ struct VArena {
     p = nullptr;
     n = cap = 0;
   }
-  // reserves room for `capacity` elements on the current device (contents dropped)
-  void reserve(size_t capacity) {
+  // reserves room for `capacity` elements on the current device (contents dropped); chunks hold whole
+  // rows of row_elems elements, so no row (one TMA box row, one bulk copy) spans two physical
+  // allocations
+  void reserve(size_t capacity, size_t row_elems = 1) {
     reset();
     const auto& v = vmm();
     CK(cudaGetDevice(&device));
@@ -249,8 +251,16 @@ struct VArena {
     const size_t bytes = std::max<size_t>(1, capacity) * sizeof(T);
     // chunks of at most 64 MiB (the most a store holds beyond its rows), at least one granule,
     // ~1/512 of the range for large arenas
-    chunk = std::min<size_t>(size_t(64) << 20, std::max(gran, (bytes / 512 + gran - 1) / gran * gran));
-    chunk = (chunk + gran - 1) / gran * gran;
+    const size_t rb = std::max<size_t>(1, row_elems) * sizeof(T);
+    size_t g = gran, r = rb;  // unit = lcm(granule, row bytes)
+    while (r) {
+      const size_t t = g % r;
+      g = r;
+      r = t;
+    }
+    const size_t unit = gran / g * rb;
+    chunk = std::min<size_t>(std::max<size_t>(size_t(64) << 20, unit), std::max(unit, bytes / 512));
+    chunk = (chunk + unit - 1) / unit * unit;
     const size_t nchunks = (bytes + chunk - 1) / chunk;
     CUdeviceptr base = 0;
     CUK(v.reserve(&base, nchunks * chunk, 0, 0, 0));  // default alignment (chunk need not be a power of two)
@@ -709,12 +719,12 @@ struct rd_index {
   void store_reserve(long long rows_cap) {  // capacity for rows_cap rows, contents dropped
     if (split3) {
       arena.reset();
-      xsplit.reserve((size_t)std::max(1LL, rows_cap) * d);
-      x3.reserve((size_t)std::max(1LL, rows_cap) * d);
+      xsplit.reserve((size_t)std::max(1LL, rows_cap) * d, d);
+      x3.reserve((size_t)std::max(1LL, rows_cap) * d, d);
     } else {
       xsplit.reset();
       x3.reset();
-      arena.reserve((size_t)std::max(1LL, rows_cap) * d);
+      arena.reserve((size_t)std::max(1LL, rows_cap) * d, d);
     }
   }
   void store_resize(long long rows) {
@@ -779,8 +789,8 @@ struct rd_index {
       unsigned bad = 0;
       CK(cudaMemcpy(&bad, inexact_ctr.p, sizeof bad, cudaMemcpyDeviceToHost));
       if (bad) return false;
-      xsplit.reserve((size_t)std::max(1LL, n) * d);
-      x3.reserve((size_t)std::max(1LL, n) * d);
+      xsplit.reserve((size_t)std::max(1LL, n) * d, d);
+      x3.reserve((size_t)std::max(1LL, n) * d, d);
       for (long long hi = rows; hi > 0;) {
         const long long lo = std::max(0LL, hi - cr);
         xsplit.map_range((size_t)lo * d, (size_t)hi * d);
@@ -794,7 +804,7 @@ struct rd_index {
       arena.reset();
       xsplit.n = x3.n = (size_t)rows * d;
     } else {
-      arena.reserve((size_t)std::max(1LL, n) * d);
+      arena.reserve((size_t)std::max(1LL, n) * d, d);
       for (long long hi = rows; hi > 0;) {
         const long long lo = std::max(0LL, hi - cr);
         arena.map_range((size_t)lo * d, (size_t)hi * d);

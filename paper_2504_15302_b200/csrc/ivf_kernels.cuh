@@ -14,6 +14,7 @@ namespace rd {
 // results. RD_PDL=0 in the environment launches them plainly (A/B).
 bool pdl_enabled();
 cudaError_t ensure_smem(const void* kern, size_t smem);  // per (device, kernel) dynamic smem limit
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
   const cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), smem);

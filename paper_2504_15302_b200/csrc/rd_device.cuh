@@ -365,10 +365,6 @@ __device__ __forceinline__ float l2_group8_f32_chunks(const float* q, const RowR
   s += __shfl_xor_sync(0xffffffffu, s, 4);
   return s;
 }
-// bulk prefetch of [p, p + bytes) into L2 (bytes % 16 == 0, p 16-byte aligned); no completion to wait on
-__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
