@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kTcG = kG, kStages = Ring<kPre, kG, kSB>::S, kBRows = TcGeom<kG>::BRows,
                 kBSlice = TcGeom<kG>::BSlice;
   constexpr bool kStream = kSB;  // the query operand travels with the stages
+  constexpr bool kHalfN = kPre && !kSB && kG == 32;  // half-N MMAs for tiles of <= 16 queries
   RD_PDL_PROLOGUE();
   if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 4 + 0] = gtimer();
   extern __shared__ unsigned char smem_raw[];
@@ -315,7 +316,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive_expect_tx(sm.bfull, (uint32_t)(nslices * 2 * qq * 512));
       __syncwarp();
       if (grp < ngrp) {
-        const uint32_t dst = sm.bs + (part * (kTcG / 4) + g0 / 4) * 512;
+        // half tiles (<= 16 queries of a 32-wide tile): q2 right after q1 (rows 16-31), so the MMAs run
+        // at half N (see the MMA issuer)
+        const bool half = kHalfN && T.nq <= kTcG / 2;
+        const uint32_t dst = sm.bs + (part * (half ? kTcG / 8 : kTcG / 4) + g0 / 4) * 512;
         for (int slice = grp; slice < nslices; slice += ngrp)
           tma_gather4_u32(dst + slice * kBSlice, &qmap, slice * 64, r[0], r[1], r[2], r[3], sm.bfull);
       }
@@ -326,7 +330,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   // ---------------------------------------------------------------- warp 1: MMA issuer
   else if (warp == 1) {
-    const uint32_t ida = idesc_bf16(kRows, kBRows), idb = idesc_bf16(kRows, kTcG);
+    // per tile: full N (x1.[q1;q2] N = 64, x2.q1 N = 32) or, for tiles of <= 16 queries in the
+    // 32-wide scan, half N (32, 16) over the compacted operand — half the tensor work (and power)
+    const uint32_t ida_full = idesc_bf16(kRows, kBRows), idb_full = idesc_bf16(kRows, kTcG);
+    const uint32_t ida_half = idesc_bf16(kRows, kBRows / 2), idb_half = idesc_bf16(kRows, kTcG / 2);
     const unsigned char* bs_ptr = reinterpret_cast<unsigned char*>(smem_raw) + (sm.bs - smem_u32(smem_raw));
     const uint64_t bdesc0 = umma_desc_sw128(bs_ptr);
     uint32_t u = 0, rtc = 0;
@@ -346,6 +353,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const ScanTile T = p.tiles[t];
       dbg_rows += T.nrows;
+      const bool half = kHalfN && T.nq <= kTcG / 2;
+      const uint32_t ida = half ? ida_half : ida_full, idb = half ? idb_half : idb_full;
       if (p.dbg && ti == 0 && lane == 0) p.dbg[blockIdx.x * 4 + 2] = gtimer();
       for (int rt = 0; rt * kRows < T.nrows; ++rt, ++rtc) {
         const int a = rtc & 1;
@@ -552,12 +561,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         RD_TWAIT(&sm.afull[a], (rtc >> 1) & 1, 8);
         tc_fence_after();
         const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + a * kAccCols;
-        // D_a = [x1.q1 | x1.q2] in columns [0, 2 kTcG), D_b = x2.q1 in [2 kTcG, 3 kTcG)
+        // D_a = [x1.q1 | x1.q2] in columns [0, 2 kTcG) (half tiles: [0, kTcG) with x1.q2 from kTcG / 2),
+        // D_b = x2.q1 in [2 kTcG, 3 kTcG)
         uint32_t d1[kTcG], d2[kTcG], d3[kTcG];
+        const uint32_t c2 = (kHalfN && nq <= kTcG / 2) ? kTcG / 2 : kTcG;
 #pragma unroll
         for (int c = 0; c < kTcG; c += 16) {
           RD_TMEM_LD16(ta + c, (d1 + c));
-          RD_TMEM_LD16(ta + kTcG + c, (d2 + c));
+          RD_TMEM_LD16(ta + c2 + c, (d2 + c));
           RD_TMEM_LD16(ta + 2 * kTcG + c, (d3 + c));
         }
         tmem_ld_wait();
