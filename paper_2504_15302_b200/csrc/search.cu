@@ -182,9 +182,9 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   sp.gamma_scan = h->scan_gamma();
   sp.x12 = h->x12_dev();
   sp.x3 = h->x3_dev();
-  unsigned long long* chain = nullptr;  // profiling only (RD_DEBUG_CHAIN): [select 32][plan 32][merge 32][scan 4/CTA]
+  unsigned long long* chain = nullptr;  // profiling only (RD_DEBUG_CHAIN): [select 32][plan 32][merge 32][scan 4/CTA + tiles, rows]
   if (h->dbg_chain) {
-    const size_t n = 96 + 4 * (size_t)h->num_sms;
+    const size_t n = 96 + 6 * (size_t)h->num_sms;
     if (h->dbg_chain_buf.n < n) h->dbg_chain_buf.alloc(n);
     chain = h->dbg_chain_buf.p;
     CK(cudaMemsetAsync(chain, 0, 8 * n, s));
@@ -532,7 +532,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     launches += 2;
     CK(cudaEventRecord(te3, ms));
     if (chain) {  // ns from select's entry: [13] = entry (before the PDL wait), [0] = past the wait
-      std::vector<unsigned long long> t(96 + 4 * (size_t)h->num_sms);
+      std::vector<unsigned long long> t(96 + 6 * (size_t)h->num_sms);
       CK(cudaMemcpyAsync(t.data(), chain, 8 * t.size(), cudaMemcpyDeviceToHost, ms));
       CK(cudaStreamSynchronize(ms));
       const long long t0 = (long long)t[13];
