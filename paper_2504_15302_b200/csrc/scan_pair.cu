@@ -327,7 +327,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
   // ---------------------------------------------------------------- warp 1: MMA issuer (leader)
   else if (warp == 1) {
     if (leader) {
-      const uint32_t idesc = idesc_bf16(kPBlock, 2 * kPG);
+      // tiles of <= 16 queries: half N (each CTA's B half holds its part's queries in rows 0..nq-1, so
+      // N = 32 reads 16 rows from each CTA: x1.[q1;q2] in columns 0-31, x2.[q1;q2] from 64)
+      const uint32_t idesc_full = idesc_bf16(kPBlock, 2 * kPG), idesc_half = idesc_bf16(kPBlock, kPG);
       const unsigned char* bs_ptr = reinterpret_cast<unsigned char*>(smem_raw) + (sm.bs - smem_u32(smem_raw));
       const uint64_t bdesc0 = umma_desc_sw128(bs_ptr);
       uint32_t u = 0, rtc = 0;
@@ -336,6 +338,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
         RD_PWAIT(mbar_wait(&sm.tfull[slot], (ti >> 1) & 1), 3);
         const int t = sm.tring[slot];
         const int nrows = sm.tinfo[slot].nrows;
+        const uint32_t idesc = sm.tinfo[slot].nq <= kPG / 2 ? idesc_half : idesc_full;
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.tempty[slot]);
         if (t < 0) break;
@@ -414,10 +417,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
         tc_fence_after();
         const uint32_t ta = tmem + ((uint32_t)(quarter * 32) << 16) + a * kPAccCols;
         uint32_t d1[kPG], d2[kPG], d3[kPG];
+        const uint32_t c2 = nq <= kPG / 2 ? kPG / 2 : kPG;  // half tiles: x1.q2 from column 16
 #pragma unroll
         for (int c = 0; c < kPG; c += 16) {
           RD_TMEM_LD16(ta + c, (d1 + c));
-          RD_TMEM_LD16(ta + kPG + c, (d2 + c));
+          RD_TMEM_LD16(ta + c2 + c, (d2 + c));
           RD_TMEM_LD16(ta + 2 * kPG + c, (d3 + c));
         }
         tmem_ld_wait();
