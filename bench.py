@@ -512,7 +512,14 @@ def run_ours(args, cfg):
     peaks = measured_peaks()
     peak = peaks["hbm_gbs"] if peaks else 6650.0
     scan_ms = tm["scan_ms"] / max(1, tm["stage_searches"])
-    scan_bytes = st1["bytes_lists_resident"]
+    scan_bytes = st1["bytes_lists_resident"]  # probed resident rows x d x 4 (SURVEY §8d's per-row unit)
+    fp32_equiv = None
+    if info["store"] == 3:  # residual store: the scan reads r1 (d x 2 B) and ||x - c||^2 (4 B) per row
+        rows = scan_bytes // (d * 4)
+        fp32_equiv = {"bytes_per_launch": scan_bytes,
+                      "gbs": scan_bytes / (scan_ms * 1e-3) / 1e9 if scan_ms > 0 else 0.0,
+                      "note": "the same rows at fp32 (3072 B per row): the rate an fp32 scan would need"}
+        scan_bytes = rows * (d * 2 + 4)
     achieved = scan_bytes / (scan_ms * 1e-3) / 1e9 if scan_ms > 0 else 0.0
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "scan_traffic.json")
@@ -544,11 +551,12 @@ def run_ours(args, cfg):
         "e2e": e2e,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "ivf_scan_tc_kernel (N5; FFMA ivf_scan_kernel N4 when d % 64 != 0)",
+                     "kernel": ("ivf_scan_tc_kernel (N5 over the residual store: r1 = bf16(x - c) tiles)" if info["store"] == 3
+                                else "ivf_scan_tc_kernel (N5; FFMA ivf_scan_kernel N4 when d % 64 != 0)"),
                      "peak_source": ("MEASURED_PEAKS.json hbm_gbs (a torch copy: read + write bytes); a read-only "
                                      "stream of the scan's TMA pattern reaches ~7.46 TB/s (tools/micro/bw.cu)")
                      if peaks else "fallback",
-                     "bytes_per_launch": scan_bytes, "avg_launch_ms": scan_ms,
+                     "bytes_per_launch": scan_bytes, "avg_launch_ms": scan_ms, "fp32_equivalent": fp32_equiv,
                      "stripe": "per GPU (this process's slowest stripe)" if n_gpus > 1 else "the index"},
         "step_breakdown_ms": {k2: tm[k2] / max(1, tm["stage_searches"]) for k2 in ("coarse_ms", "scan_ms", "tail_ms", "total_ms")},
         "step_gbps_algorithmic": st["bytes_algorithmic"] / (ms_step * 1e-3) / 1e9,
@@ -559,7 +567,8 @@ def run_ours(args, cfg):
         "h2d_link": h2d_link,
         "decode_stream": decode.summary() if decode is not None else None,
         "index": {"build_s": build_s, "lists_resident": info["lists_resident"], "hbm_bytes": info["hbm_bytes"],
-                  "store": {0: "fp32", 1: "fp32 + pre-split copy", 2: "split3 (exact bf16 triple)"}.get(info["store"]),
+                  "store": {0: "fp32", 1: "fp32 + pre-split copy", 2: "split3 (exact bf16 triple)",
+                            3: "fp32 + bf16 residual plane (scan reads 2 B/element)"}.get(info["store"]),
                   "fp32_bytes": info["n"] * d * 4,
                   "host_pinned_bytes": info["host_pinned_bytes"], "h2d_list_bytes_per_step": st1["h2d_list_bytes"],
                   "llm_reservation_bytes": reservation},

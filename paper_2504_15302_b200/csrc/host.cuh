@@ -454,6 +454,23 @@ CUtensorMap make_gather_map(const void* base, long long rows, int d) {
   return m;
 }
 
+// 2D bf16 map over a [rows][d] plane (the residual store's r1), box {64 dims, box_rows}, 128B swizzle:
+// the same smem tile as one part of the split map's box.
+CUtensorMap make_bf16_row_map(const void* base, long long rows, int d, int box_rows) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof m);
+  if (rows < 1) rows = 1;
+  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw_rd(RD_ERR_RUNTIME, "cuTensorMapEncodeTiled (bf16 rows) failed (%d)", (int)r);
+  return m;
+}
+
 // 2D fp32 map over rows x d, box [32 dims x box_rows], 128B swizzle.
 CUtensorMap make_row_map(const float* base, long long rows, int d, int box_rows) {
   CUtensorMap m;
@@ -521,6 +538,7 @@ struct rd_index {
   // dot-product error bound of the scans whose candidates the merge certifies (ivf_kernels.cuh): the
   // tensor-core and FFMA scans may both run in one search (offloaded or sparse lists)
   float scan_gamma() const {
+    if (resid) return 0.f;  // the residual scan's keys are lower bounds already (resid.cu)
     return tc_scan() ? std::max(rd::gamma_bf16x3(d), rd::gamma_ffma_scan(d)) : rd::gamma_ffma_scan(d);
   }
   // Tensor-core tile width for a batch: 16-query tiles (the 16-wide scan's deeper ring) when the
@@ -539,9 +557,12 @@ struct rd_index {
   // spare candidates reranked beyond k (RD_RERANK_MARGIN, 8..32): more tolerate more duplicate
   // vectors around rank k before a query needs the exact fallback, at more rerank reads and a
   // looser scan pruning rank
-  int rerank_margin = std::getenv("RD_RERANK_MARGIN")
-                          ? std::max(8, std::min(32, std::atoi(std::getenv("RD_RERANK_MARGIN"))))
-                          : 8;
+  // (-1: by store — 14 over the residual store, whose keys sit up to eps_pair below the exact
+  // distances, so rank k + 15 clears rank k's near-ties; 8 otherwise)
+  int rerank_margin_env = std::getenv("RD_RERANK_MARGIN")
+                              ? std::max(8, std::min(32, std::atoi(std::getenv("RD_RERANK_MARGIN"))))
+                              : -1;
+  int rerank_margin() const { return rerank_margin_env >= 0 ? rerank_margin_env : resid ? 14 : 8; }
   bool stage_rows(long long B) const { return B <= (stage_max_b >= 0 ? stage_max_b : 2LL * num_sms); }
   long long n = 0;
   int d = 0, nlist = 0;
@@ -567,6 +588,43 @@ struct rd_index {
   VArena<uint16_t> x3;
   CUtensorMap xmap128{}, xmap32{};
   bool presplit = false;
+  // Residual store (RD_STORE=resid, resid.cu): the fp32 arena plus r1 = bf16(x - c_list) [rows][d]
+  // (2 B per element: the scan's only operand), ||x - c||^2 per row and max ||x - c|| per list. Built
+  // while every list is resident and no byte budget applies; any relayout drops it (build_presplit
+  // rebuilds it).
+  bool resid = false;
+  DBuf<uint16_t> rplane;
+  DBuf<float> rnorm, rmax;
+  CUtensorMap rmap128{}, rmap32{};
+  // RD_STORE=split3 keeps the round-2 stores (split3 / fp32 by budget) for fully resident indexes too
+  static bool resid_wanted() {
+    const char* v = std::getenv("RD_STORE");
+    return !(v && std::strcmp(v, "split3") == 0);
+  }
+  bool resid_ok = true;  // the last placement chose the residual store (materialize: always)
+  // the residual store applies: wanted, the tensor-core scan for every list, 128-dim pair-operand blocks
+  bool resid_fmt() const { return resid_wanted() && tc_scan() && tc_min_q == 1 && d % 128 == 0; }
+  void drop_resid() {
+    resid = false;
+    rplane.reset();
+    rnorm.reset();
+    rmax.reset();
+  }
+  bool build_resid() {
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    const size_t need = (size_t)n * d * 2 + (size_t)n * 4 + (size_t)nlist * 4;
+    if (need + (size_t(1) << 30) > fr) return false;
+    rplane.alloc((size_t)n * d);
+    rnorm.alloc(n);
+    rmax.alloc(nlist);
+    CK(rd::launch_resid_build(arena.p, d_res_row0.p, d_list_off.p, centroids.p, nlist, d, rplane.p, rnorm.p, rmax.p, 0));
+    CK(cudaDeviceSynchronize());
+    rmap128 = make_bf16_row_map(rplane.p, n_resident, d, rd::kTcRows);
+    rmap32 = make_bf16_row_map(rplane.p, n_resident, d, 32);
+    resid = true;
+    return true;
+  }
   DBuf<unsigned> inexact_ctr;  // split3_kernel's count of elements that did not round-trip
   bool budgeted = false;  // last placement had an HBM byte budget
   DBuf<long long> d_list_off, d_ids, d_res_row0;
@@ -589,6 +647,7 @@ struct rd_index {
   // per-search workspace
   struct Ws {
     DBuf<float> qnorm, Dc, q, qsplit;
+    DBuf<float> pairs, pqn;  // residual store: per (query, list) pair operands and ||q - c||^2 - eps
     DBuf<int> probes, list_nq, list_qoff, list_ntile, list_toff, list_q, part_count, part_row, off_meta;
     DBuf<unsigned> bitmap, fb_ctr;
     bool bitmap_clean = false;  // the bitmap is all-zero (the plan's list_fill re-zeroes it)
@@ -835,7 +894,8 @@ struct rd_index {
     const long long cr = std::min<long long>(std::max(1LL, n), conv_rows());
     tmp.alloc((size_t)cr * d);
     for (int attempt = 0; attempt < 2; ++attempt) {
-      split3 = attempt == 0 && split3_eligible();
+      split3 = attempt == 0 && split3_eligible() && !resid_fmt();
+      resid_ok = true;
       if (attempt == 1 && !std::getenv("RD_SPLIT3_QUIET"))
         fprintf(stderr, "rd: split3 store inexact for this data (%s); using fp32 rows\n", "residual out of bf16 range");
       store_reserve(n);
@@ -902,16 +962,36 @@ struct rd_index {
     cmax = std::sqrt(m2) * (1.f + 1e-6f);
   }
 
+  // After every (re)layout: the scan's operand for the resident store. Default (RD_STORE unset):
+  // every list resident and the last placement chose it -> the residual store (fp32 rows + r1 plane;
+  // a split3 store is converted back to fp32 rows in place first); otherwise split3 unless a byte
+  // budget already chose fp32 rows. RD_STORE=split3: the round-2 rule (split3 by placement, a
+  // pre-split copy beside fp32 rows only without a budget).
   void build_presplit() {
+    drop_resid();
+    const char* env = std::getenv("RD_PRESPLIT");
+    const bool pre_off = env && std::atoi(env) == 0;
+    if (resid_fmt() && !pre_off && n_resident > 0) {
+      if (resid_ok && n_resident == n) {
+        if (split3 && convert_store(false)) upload_residency();
+        if (!split3) {
+          presplit = false;
+          xsplit.reset();
+          if (build_resid()) return;
+        }
+      }
+      // not every list resident, or no room for the residual plane: split3 in place (1.5 x the fp32
+      // rows) unless a budget chose fp32 rows
+      if (!split3 && !budgeted && split3_eligible() && convert_store(true)) upload_residency();
+    }
     if (split3) {  // the store is the scan's operand
       presplit = n_resident > 0;
       return;
     }
     presplit = false;
     xsplit.reset();
-    const char* env = std::getenv("RD_PRESPLIT");
     // a byte budget (e.g. the LLM reservation, C5) must not be exceeded by a second copy
-    if (!tc_scan() || (env && std::atoi(env) == 0) || n_resident == 0 || budgeted) return;
+    if (!tc_scan() || pre_off || n_resident == 0 || budgeted) return;
     size_t fr = 0, tot = 0;
     CK(cudaMemGetInfo(&fr, &tot));
     const size_t need = (size_t)n_resident * d * 4;
@@ -983,6 +1063,7 @@ struct rd_index {
     if (!split3) {
       xsplit.reset();  // any relayout invalidates the pre-split copy (rebuilt by build_presplit)
       presplit = false;
+      drop_resid();
     }
     std::vector<const float*> base(nlist);
     for (int l = 0; l < nlist; ++l)

@@ -453,13 +453,13 @@ int rd_index_info_get(const rd_index* h, rd_index_info* o) {
     for (int l = 0; l < h->nlist; ++l) o->lists_resident += h->resident[l];
     // what the index holds on the device: the resident store as mapped (rows rounded up to its
     // arena chunks), the staging ring, per-row norms / ids / list map and the coarse-stage state
-    o->hbm_bytes = h->store_bytes() + (uint64_t)h->staging.n * 4 + (uint64_t)h->n * (4 + 8 + 4) +
+    o->hbm_bytes = h->store_bytes() + (uint64_t)h->rplane.n * 2 + (uint64_t)h->rnorm.n * 4 + (uint64_t)h->staging.n * 4 + (uint64_t)h->n * (4 + 8 + 4) +
                    (uint64_t)h->nlist * ((uint64_t)h->d * 8 + 4 + 8 + 8 + 8);
     o->host_pinned_bytes = (uint64_t)h->host_arena.n * 4;
     o->staging_slots = h->slots;
     o->max_norm = h->xmax;
     o->device = h->device;
-    o->store = h->split3 ? RD_STORE_SPLIT3 : h->presplit ? RD_STORE_F32_PRESPLIT : RD_STORE_F32;
+    o->store = h->split3 ? RD_STORE_SPLIT3 : h->resid ? RD_STORE_F32_RESID : h->presplit ? RD_STORE_F32_PRESPLIT : RD_STORE_F32;
   });
 }
 
@@ -662,12 +662,20 @@ int rd_index_place(rd_index* h, const rd_placement* p) {
     // speed, since every list left out streams over the host link on every search.
     std::vector<uint8_t> mask;
     uint64_t res_bytes = 0;
-    bool cut = false, fmt3 = false;
-    if (h->split3_eligible()) {
+    bool cut = false, fmt3 = false, fmt_res = false;
+    // the residual store (fp32 rows + bf16 residual plane + ||x - c||^2: 6 B + 4 B per row) when every
+    // list stays resident in it — the fastest scan (2 B per element read)
+    if (h->resid_fmt()) {
+      choose((uint64_t)h->d * 6 + 4, mask, res_bytes, cut);
+      bool all = !cut;
+      for (int l = 0; l < nl && all; ++l) all = mask[l] != 0;
+      fmt_res = all && !(budget0 && res_bytes > budget0);
+    }
+    if (!fmt_res && h->split3_eligible()) {
       choose((uint64_t)h->d * 6, mask, res_bytes, cut);
       fmt3 = !cut && !(p->resident_mask && budget0 && res_bytes > budget0);
     }
-    if (!fmt3) choose((uint64_t)h->d * 4, mask, res_bytes, cut);
+    if (!fmt3 && !fmt_res) choose((uint64_t)h->d * 4, mask, res_bytes, cut);
     if (p->resident_mask && budget0 && res_bytes > budget0)
       throw_rd(RD_ERR_INFEASIBLE, "placement infeasible: resident lists need %llu bytes > budget %llu",
                (unsigned long long)res_bytes, (unsigned long long)budget0);
@@ -683,7 +691,7 @@ int rd_index_place(rd_index* h, const rd_placement* p) {
     }
     long long slot_rows = 0;
     int slots = 0;
-    const uint64_t row_bytes = (uint64_t)h->d * (fmt3 ? 6 : 4);
+    const uint64_t row_bytes = (uint64_t)h->d * (fmt3 || fmt_res ? 6 : 4);
     if (n_off > 0) {
       slot_rows = ring_slot_rows(max_off);
       const double slot_bytes = (double)slot_rows * h->d * 4;
@@ -717,6 +725,7 @@ int rd_index_place(rd_index* h, const rd_placement* p) {
     if (fmt3 && !h->split3) h->convert_store(true);  // stays fp32 if the split does not round-trip
     compact_host(h);
     h->budgeted = budget0 != 0;
+    h->resid_ok = fmt_res;
     h->upload_residency();
     h->build_presplit();
     h->set_staging(slots, slot_rows);
@@ -780,7 +789,10 @@ int rd_index_migrate(rd_index* h, const int32_t* promote, int32_t n_promote, con
     const bool ring_changes = slots != h->slots || (slots && slot_rows != h->slot_rows);
     if (ring_changes) h->set_staging(0, 0);  // shrink before grow: the old ring goes first
     relayout(h, after, &ms);
-    if (hbm_budget_bytes) h->budgeted = true;
+    if (hbm_budget_bytes) {
+      h->budgeted = true;
+      h->resid_ok = false;  // the budget rule counted the store's own row bytes only
+    }
     if (ring_changes) h->set_staging(slots, slot_rows);
     h->upload_residency();
     h->build_presplit();

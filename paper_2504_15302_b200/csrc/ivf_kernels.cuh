@@ -96,7 +96,7 @@ struct TcScanParams {
 };
 
 size_t scan_smem_bytes(int d);
-size_t scan_tc_smem_bytes(int d, int tc_g, bool presplit, bool stream = false);
+size_t scan_tc_smem_bytes(int d, int tc_g, bool presplit, bool stream = false, bool resid = false);
 // 32-query tiles over the x1 | x2 plane on CTA pairs (scan_pair.cu, cta_group::2): ring depth for
 // this d (0: unsupported), and the launch (grid = the SMs rounded down to pairs)
 int scan_pair_stages(int d);
@@ -107,7 +107,35 @@ cudaError_t launch_scan_pair(const CUtensorMap& map128, const CUtensorMap& map32
 // tc_g: queries per tile, 16 or 32 (the planner grouped the tiles with the same width)
 cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, const CUtensorMap& qmap,
                            const TcScanParams& p, int grid, cudaStream_t s, bool presplit, int tc_g,
-                           bool stream = false);
+                           bool stream = false, bool resid = false);
+
+// Residual store (resid.cu). r1 = bf16(x - c_list) per resident row ([rows][d], the scan's A
+// operand), rnorm[global row] = ||x - c_list||^2 (fp64 sum, RN), rmax[list] = max ||x - c_list||
+// rounded up. One CTA per list.
+cudaError_t launch_resid_build(const float* arena, const long long* res_row0, const long long* list_off,
+                               const float* centroids, int nlist, int d, void* r1, float* rnorm, float* rmax,
+                               cudaStream_t s);
+// Per (query, list) pair of the scan's tiles, by CSR position pos (tile qoff + g): the operand rows
+// 2 pos / 2 pos + 1 = (p1, p2), the bf16 split of p = fl32(q - c_list), and pqn[pos] = ||q - c||^2
+// less the pair's error bound eps (rounded down): the residual scan's keys are then lower bounds on
+// the exact distances. Tiles of two arrays (either may be null); only each (list, query group)'s
+// first chunk computes (its grow0 is the list's first row).
+struct PairParams {
+  const ScanTile* t16;
+  const int* n16;
+  const ScanTile* t32;
+  const int* n32;
+  const int* list_q;
+  const long long* list_off;
+  const float* queries;
+  const float* centroids;
+  const float* rmax;
+  int d;
+  float gamma;  // dot-product error bound of the residual scan (gamma_resid)
+  void* pairs;  // [2 * positions][d] bf16
+  float* pqn;   // [positions]
+};
+cudaError_t launch_pair_operand(const PairParams& p, int grid, cudaStream_t s);
 cudaError_t launch_qsplit(const float* Q, void* out, long long B, int d, cudaStream_t s);
 cudaError_t launch_scan(const CUtensorMap& map256, const CUtensorMap& map32, const ScanParams& p,
                         int grid, cudaStream_t s);
@@ -154,6 +182,9 @@ constexpr float kUnit = 5.9604645e-8f;
 inline float gamma_ffma_scan(int d) { return 2.f * (d / 2 + 8) * kUnit; }
 inline float gamma_ffma_coarse(int d) { return 2.f * (d + 4) * kUnit; }
 inline float gamma_bf16x3(int d) { return (524.f + 0.7f * d) * kUnit; }
+// residual scan (r1 = bf16(x - c), p = fl32(q - c) split in two bf16): 2^-9 (1 + 2^-7) for r1's
+// rounding, 2^-17 + 2u for p's, the measured fp32 accumulation term of the bf16x3 model
+inline float gamma_resid(int d) { return (33100.f + 14.f + 0.7f * d) * kUnit; }
 
 // Scan tile categories (plan.cu): tensor-core tiles of <= 16 queries (16-wide scan), of <= 32
 // queries (32-wide scan), and FFMA tiles.

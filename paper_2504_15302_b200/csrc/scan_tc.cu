@@ -48,11 +48,16 @@ struct TcGeom {
   static constexpr int BSlice = BRows * 128;
 };
 // ring depth / stage bytes of a (path, width, streamed operand) variant
-template <bool kPre, int kG, bool kSB>
+// kRes (residual plane, implies kPre): one 16 KiB r1 tile per stage instead of x1 | x2, so twice the
+// stages in the same bytes
+template <bool kPre, int kG, bool kSB, bool kRes = false>
 struct Ring {
   static_assert(!kSB || (kPre && kG == 16), "streamed operand: pre-split 16-query tiles only");
-  static constexpr int S = kPre ? (kSB ? 6 : TcGeom<kG>::Stages / 2) : TcGeom<kG>::Stages;
-  static constexpr int B = kPre ? 2 * kRows * 128 + (kSB ? TcGeom<kG>::BSlice : 0) : kRows * 128;
+  static_assert(!kRes || kPre, "the residual plane is read straight into smem");
+  static constexpr int S = kRes ? (kSB ? 10 : (kG == 16 ? 10 : 6))
+                                : kPre ? (kSB ? 6 : TcGeom<kG>::Stages / 2) : TcGeom<kG>::Stages;
+  static constexpr int B = kRes ? kRows * 128 + (kSB ? TcGeom<kG>::BSlice : 0)
+                                : kPre ? 2 * kRows * 128 + (kSB ? TcGeom<kG>::BSlice : 0) : kRows * 128;
   // converter group g owns stages / TMEM buffers with u % 2 == g; an odd ring depth would let one
   // group wait on a phase two ahead of the other group's and alias its mbarrier parity
   static_assert(TcGeom<kG>::Stages % 2 == 0, "x ring depth must be even");
@@ -78,11 +83,11 @@ struct Smem {
   long long* stage_k; // [4][32]
 };
 
-template <bool kPre, int kG, bool kSB>
+template <bool kPre, int kG, bool kSB, bool kRes>
 __device__ __forceinline__ Smem carve(unsigned char* raw, int d) {
-  constexpr int kStages = Ring<kPre, kG, kSB>::S, kBSlice = TcGeom<kG>::BSlice;
+  constexpr int kStages = Ring<kPre, kG, kSB, kRes>::S, kBSlice = TcGeom<kG>::BSlice;
   // ring bytes (+ the resident operand unless the stages carry it)
-  const size_t xring = (size_t)kStages * Ring<kPre, kG, kSB>::B;
+  const size_t xring = (size_t)kStages * Ring<kPre, kG, kSB, kRes>::B;
   const size_t ring = xring + (kSB ? 0 : (size_t)(d / 64) * kBSlice);
   Smem s;
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
@@ -133,11 +138,15 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 // kPre = true : pre-split bf16 (x1, x2) arena ([rows][2][d], built with the index); the producer TMA-loads
 //               both 64-dim tiles of a stage straight into 128B-swizzled smem and the MMAs read A from
 //               smem (SS) — no conversion on the scan path; converter warps are idle.
-template <bool kPre, int kG, bool kSB>
+// kRes: the residual store (resid.cu): A = r1 = bf16(x - c_list) [rows][d], B = the tile's (query, list)
+//       pair operands (p1, p2) = split(q - c_list) gathered by CSR position, one MMA per K step
+//       (r1.[p1;p2]); qnorm is per position (||q - c||^2 less the pair's error bound) and xnorm is
+//       ||x - c||^2, so every key is a lower bound on the exact distance.
+template <bool kPre, int kG, bool kSB, bool kRes>
 __global__ void __launch_bounds__(kThreads, 1)
     ivf_scan_tc_kernel(const __grid_constant__ CUtensorMap map128, const __grid_constant__ CUtensorMap map32,
                        const __grid_constant__ CUtensorMap qmap, const TcScanParams p) {
-  constexpr int kTcG = kG, kStages = Ring<kPre, kG, kSB>::S, kBRows = TcGeom<kG>::BRows,
+  constexpr int kTcG = kG, kStages = Ring<kPre, kG, kSB, kRes>::S, kBRows = TcGeom<kG>::BRows,
                 kBSlice = TcGeom<kG>::BSlice;
   constexpr bool kStream = kSB;  // the query operand travels with the stages
   constexpr bool kHalfN = kPre && !kSB && kG == 32;  // half-N MMAs for tiles of <= 16 queries
@@ -145,10 +154,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 4 + 0] = gtimer();
   extern __shared__ unsigned char smem_raw[];
   const int d = p.d, nks = kPre ? d / 64 : d / 32;
-  const Smem sm = carve<kPre, kG, kSB>(smem_raw, d);
+  const Smem sm = carve<kPre, kG, kSB, kRes>(smem_raw, d);
   // ring geometry: kStages stages of RB bytes (pre-split: x1 | x2 [| B slice]; converter: fp32 x)
   constexpr int RS = kStages;
-  constexpr int RB = Ring<kPre, kG, kSB>::B;
+  constexpr int RB = Ring<kPre, kG, kSB, kRes>::B;
+  constexpr int kXTiles = kRes ? 1 : 2;  // A tiles per stage (r1; or x1, x2)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -226,11 +236,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int qq = (T.nq + 3) >> 2, per = 2 * qq;
         const int part = lane >= qq ? 1 : 0;
         const int g0 = (lane - part * qq) * 4;
-        const uint32_t boff = 2 * kRows * 128 + (part * (kTcG / 4) + g0 / 4) * 512;
+        const uint32_t boff = kXTiles * kRows * 128 + (part * (kTcG / 4) + g0 / 4) * 512;
         int r[4] = {0, 0, 0, 0};
         if (lane < per)
 #pragma unroll
-          for (int i = 0; i < 4; ++i) r[i] = 2 * __ldg(p.list_q + T.qoff + min(g0 + i, T.nq - 1)) + part;
+          for (int i = 0; i < 4; ++i)
+            r[i] = 2 * (kRes ? T.qoff + min(g0 + i, T.nq - 1) : __ldg(p.list_q + T.qoff + min(g0 + i, T.nq - 1))) + part;
         for (int i = 0; i < nst; ++i, ++u) {
           const int rt = i / nks, ks = i - rt * nks;
           const int rows = min(kRows, T.nrows - rt * kRows);
@@ -240,11 +251,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t dst = sm.xs + s * RB;
           if (lane == 0) {
             RD_TWAIT(&sm.empty[s], ((u / RS) & 1) ^ 1, 1);
-            mbar_arrive_expect_tx(&sm.full[s], (uint32_t)(2 * nb * 4096 + per * 512));
+            mbar_arrive_expect_tx(&sm.full[s], (uint32_t)(kXTiles * nb * 4096 + per * 512));
           }
           __syncwarp();
           if (lane < per) tma_gather4_u32(dst + boff, &qmap, ks * 64, r[0], r[1], r[2], r[3], &sm.full[s]);
-          if (lane == 0) {
+          if (kRes && lane == 0) {
+            if (nb == 4) {
+              tma_load_2d_u32(dst, &map128, ks * 64, row, &sm.full[s]);
+            } else {
+              for (int b = 0; b < nb; ++b) tma_load_2d_u32(dst + b * 4096, &map32, ks * 64, row + b * 32, &sm.full[s]);
+            }
+          } else if (lane == 0) {
             if (nb == 4) {
               tma_load_3d_u32(dst, &map128, ks * 64, 0, row, &sm.full[s]);
               tma_load_3d_u32(dst + kRows * 128, &map128, ks * 64, 1, row, &sm.full[s]);
@@ -267,7 +284,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = u % RS;
         RD_TWAIT(&sm.empty[s], ((u / RS) & 1) ^ 1, 1);
         const uint32_t dst = sm.xs + s * RB;
-        if constexpr (kPre) {  // x1 and x2 tiles of a 64-dim slice: 2 x 16 KiB
+        if constexpr (kRes) {  // the r1 tile of a 64-dim slice: 16 KiB
+          if (nb == 4) {
+            mbar_arrive_expect_tx(&sm.full[s], kRows * 128);
+            tma_load_2d_u32(dst, &map128, ks * 64, row, &sm.full[s]);
+          } else {
+            mbar_arrive_expect_tx(&sm.full[s], nb * 4096);
+            for (int b = 0; b < nb; ++b) tma_load_2d_u32(dst + b * 4096, &map32, ks * 64, row + b * 32, &sm.full[s]);
+          }
+        } else if constexpr (kPre) {  // x1 and x2 tiles of a 64-dim slice: 2 x 16 KiB
           if (nb == 4) {
             mbar_arrive_expect_tx(&sm.full[s], 2 * kRows * 128);
             tma_load_3d_u32(dst, &map128, ks * 64, 0, row, &sm.full[s]);
@@ -301,7 +326,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int r[4];
       if (grp < ngrp)  // the ids load while the ring is refilled below
 #pragma unroll
-        for (int i = 0; i < 4; ++i) r[i] = 2 * __ldg(p.list_q + T.qoff + min(g0 + i, T.nq - 1)) + part;
+        for (int i = 0; i < 4; ++i)
+          r[i] = 2 * (kRes ? T.qoff + min(g0 + i, T.nq - 1) : __ldg(p.list_q + T.qoff + min(g0 + i, T.nq - 1))) + part;
       // the first ring's worth of this tile's x stages go out before the wait for the B operand
       // buffer (free once the previous tile's MMAs are done), so HBM keeps streaming across the
       // tile boundary and only the gather's latency is exposed
@@ -371,13 +397,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               const unsigned char* st = reinterpret_cast<unsigned char*>(smem_raw) + (sm.xs - smem_u32(smem_raw)) +
                                         s * RB;
               const uint64_t a1 = umma_desc_sw128(st), a2 = umma_desc_sw128(st + kRows * 128);
-              const uint64_t bd = kStream ? umma_desc_sw128(st + 2 * kRows * 128)
+              const uint64_t bd = kStream ? umma_desc_sw128(st + kXTiles * kRows * 128)
                                           : bdesc0 + (uint64_t)(ks * (kBSlice >> 4));
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk) {
                 const uint32_t acc = (ks | kk) != 0;
                 mma_bf16_ss(dacc, a1 + kk * 2, bd + (uint64_t)(kk * 2), ida, acc);
-                mma_bf16_ss(dacc + kBRows, a2 + kk * 2, bd + (uint64_t)(kk * 2), idb, acc);
+                if constexpr (!kRes) mma_bf16_ss(dacc + kBRows, a2 + kk * 2, bd + (uint64_t)(kk * 2), idb, acc);
               }
               tc_commit(&sm.empty[s]);
             }
@@ -553,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int j = 0; j < kOwn; ++j) {
         cq[j] = nqid[j];
-        qn[j] = cq[j] >= 0 ? __ldg(p.qnorm + cq[j]) : 0.f;
+        qn[j] = cq[j] >= 0 ? __ldg(p.qnorm + (kRes ? T.qoff + ew + 4 * j : cq[j])) : 0.f;
         qt[j] = cq[j] >= 0 ? ord2f(*(volatile int*)(p.qthr + cq[j])) : kInf;
       }
       for (int rt = 0; rt * kRows < T.nrows; ++rt, ++rtc) {
@@ -569,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < kTcG; c += 16) {
           RD_TMEM_LD16(ta + c, (d1 + c));
           RD_TMEM_LD16(ta + c2 + c, (d2 + c));
-          RD_TMEM_LD16(ta + 2 * kTcG + c, (d3 + c));
+          if constexpr (!kRes) RD_TMEM_LD16(ta + 2 * kTcG + c, (d3 + c));
         }
         tmem_ld_wait();
         tc_fence_before();
@@ -583,7 +609,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         named_bar_sync(2, 128);  // every owner finished reading the previous row tile
 #pragma unroll
         for (int g = 0; g < kTcG; ++g) {
-          const float dot = (__uint_as_float(d1[g]) + __uint_as_float(d2[g])) + __uint_as_float(d3[g]);
+          const float dot = kRes ? __uint_as_float(d1[g]) + __uint_as_float(d2[g])
+                                 : (__uint_as_float(d1[g]) + __uint_as_float(d2[g])) + __uint_as_float(d3[g]);
           eb[g * kRows + r] = (valid && g < nq) ? xn - 2.f * dot : kInf;
         }
         named_bar_sync(2, 128);
@@ -696,12 +723,19 @@ __global__ void qsplit_kernel(const float* __restrict__ Q, __nv_bfloat16* __rest
 
 }  // namespace
 
-size_t scan_tc_smem_bytes(int d, int tc_g, bool presplit, bool stream) {
+size_t scan_tc_smem_bytes(int d, int tc_g, bool presplit, bool stream, bool resid) {
   stream = stream && presplit && tc_g == 16;
-  const size_t stages = stream ? Ring<true, 16, true>::S
-                        : presplit ? (tc_g == 16 ? Ring<true, 16, false>::S : Ring<true, 32, false>::S)
-                                   : (tc_g == 16 ? Ring<false, 16, false>::S : Ring<false, 32, false>::S);
-  const size_t sbytes = stream ? Ring<true, 16, true>::B : presplit ? Ring<true, 16, false>::B : Ring<false, 16, false>::B;
+  resid = resid && presplit;
+  size_t stages, sbytes;
+  if (resid) {
+    stages = stream ? Ring<true, 16, true, true>::S : tc_g == 16 ? Ring<true, 16, false, true>::S : Ring<true, 32, false, true>::S;
+    sbytes = stream ? Ring<true, 16, true, true>::B : Ring<true, 16, false, true>::B;
+  } else {
+    stages = stream ? Ring<true, 16, true>::S
+             : presplit ? (tc_g == 16 ? Ring<true, 16, false>::S : Ring<true, 32, false>::S)
+                        : (tc_g == 16 ? Ring<false, 16, false>::S : Ring<false, 32, false>::S);
+    sbytes = stream ? Ring<true, 16, true>::B : presplit ? Ring<true, 16, false>::B : Ring<false, 16, false>::B;
+  }
   const size_t bslice = tc_g == 16 ? TcGeom<16>::BSlice : TcGeom<32>::BSlice;
   const size_t xring = stages * sbytes;
   const size_t ring = xring + (stream ? 0 : (size_t)(d / 64) * bslice);
@@ -711,21 +745,31 @@ size_t scan_tc_smem_bytes(int d, int tc_g, bool presplit, bool stream) {
 }
 
 cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, const CUtensorMap& qmap,
-                           const TcScanParams& p, int grid, cudaStream_t s, bool presplit, int tc_g, bool stream) {
+                           const TcScanParams& p, int grid, cudaStream_t s, bool presplit, int tc_g, bool stream,
+                           bool resid) {
   if (p.d % 64 != 0 || (tc_g != 16 && tc_g != 32)) return cudaErrorInvalidValue;
   stream = stream && presplit && tc_g == 16;
-  const size_t smem = scan_tc_smem_bytes(p.d, tc_g, presplit, stream);
+  resid = resid && presplit;
+  const size_t smem = scan_tc_smem_bytes(p.d, tc_g, presplit, stream, resid);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  if (resid) {
+    if (tc_g == 16) {
+      if (stream)
+        return launch_k(ivf_scan_tc_kernel<true, 16, true, true>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+      return launch_k(ivf_scan_tc_kernel<true, 16, false, true>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+    }
+    return launch_k(ivf_scan_tc_kernel<true, 32, false, true>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+  }
   if (tc_g == 16) {
     if (stream)
-      return launch_k(ivf_scan_tc_kernel<true, 16, true>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+      return launch_k(ivf_scan_tc_kernel<true, 16, true, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
     if (presplit)
-      return launch_k(ivf_scan_tc_kernel<true, 16, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
-    return launch_k(ivf_scan_tc_kernel<false, 16, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+      return launch_k(ivf_scan_tc_kernel<true, 16, false, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+    return launch_k(ivf_scan_tc_kernel<false, 16, false, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
   }
   if (presplit)
-    return launch_k(ivf_scan_tc_kernel<true, 32, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
-  return launch_k(ivf_scan_tc_kernel<false, 32, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+    return launch_k(ivf_scan_tc_kernel<true, 32, false, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+  return launch_k(ivf_scan_tc_kernel<false, 32, false, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
 }
 
 cudaError_t launch_qsplit(const float* Q, void* out, long long B, int d, cudaStream_t s) {

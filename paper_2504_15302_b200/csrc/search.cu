@@ -202,7 +202,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   }
   // the merge reranks m = min(32, k + margin) candidates and certifies against the next: scans
   // prune with, and the seed bounds, that rank's distance
-  const int m_rerank = std::min(rd::kTopK, k + h->rerank_margin);
+  const int m_rerank = std::min(rd::kTopK, k + h->rerank_margin());
   const int thr_rank = std::min(rd::kTopK - 1, m_rerank);
   sp.seed_rows = thr_rank + 1;
   rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
@@ -268,6 +268,17 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     if (use_bm) w.bitmap_clean = true;  // list_fill, now enqueued, clears every bit the selection sets
     launches += use_bm ? 3 : 1;
   }
+  // residual store: the scan's B operand is per (query, list) pair, by CSR position (resid.cu)
+  const bool res = h->resid && h->tc_scan() && h->slots == 0;
+  if (res) {
+    w.pairs.ensure((size_t)B * nprobe * d);  // 2 bf16 per element
+    w.pqn.ensure((size_t)B * nprobe);
+    rd::PairParams pr{tc_mode != 32 ? w.tiles16.p : nullptr, w.meta() + 2 * rd::kCatNarrow,
+                      tc_mode != 16 ? w.tiles.p : nullptr, w.meta() + 2 * rd::kCatWide, w.list_q.p,
+                      h->d_list_off.p, d_q, h->centroids.p, h->rmax.p, d, rd::gamma_resid(d), w.pairs.p, w.pqn.p};
+    CK(rd::launch_pair_operand(pr, 4 * h->num_sms, s));
+    launches += 1;
+  }
   const bool staged = h->stage_events;
   if (staged) CK(cudaEventRecord(e1, s));
 
@@ -279,7 +290,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     CK(cudaMemcpyAsync(w.h_qoff.p, w.list_qoff.p, sizeof(int) * nl, cudaMemcpyDeviceToHost, s));
   }
   if (has_off) CK(cudaEventRecord(e_plan, s));  // an event between two kernels costs their PDL overlap
-  const CUtensorMap gmap = make_gather_map(w.qsplit.p, B, d);
+  const CUtensorMap gmap = res ? make_gather_map(w.pairs.p, B * nprobe, d) : make_gather_map(w.qsplit.p, B, d);
   rd::ScanParams sc{w.ff_tiles.p, w.meta() + 2 * rd::kCatFfma, w.meta() + 2 * rd::kCatFfma + 1, d_q, w.qnorm.p,
                     w.list_q.p, h->xnorm.p, w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p};
   rd::TcScanParams tc{w.tiles.p, w.meta() + 2 * rd::kCatWide, w.meta() + 2 * rd::kCatWide + 1, w.qsplit.p, w.qnorm.p,
@@ -287,6 +298,10 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
                       w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p, h->debug_skip};
   sc.thr_rank = thr_rank;
   tc.thr_rank = thr_rank;
+  if (res) {
+    tc.qnorm = w.pqn.p;
+    tc.xnorm = h->rnorm.p;
+  }
   if (!h->split3 && (!h->tc_scan() || h->tc_min_q > 1)) {  // FFMA tiles exist only in these cases (fp32 store)
     CK(rd::launch_scan(h->map256, h->map32, sc, h->num_sms, s));
     launches += 1;
@@ -304,8 +319,8 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
       CK(cudaMemsetAsync(h->dbg_stall.p, 0, 8 * 12 * (size_t)h->num_sms, s));
       tc.stall = h->dbg_stall.p;
     }
-    const CUtensorMap& xm128 = h->presplit ? h->xmap128 : h->map128;
-    const CUtensorMap& xm32 = h->presplit ? h->xmap32 : h->map32;
+    const CUtensorMap& xm128 = res ? h->rmap128 : h->presplit ? h->xmap128 : h->map128;
+    const CUtensorMap& xm32 = res ? h->rmap32 : h->presplit ? h->xmap32 : h->map32;
     if (tc_mode != 32) {  // narrow tiles: the 16-wide scan (deeper ring)
       rd::TcScanParams tn = tc;
       tn.tiles = w.tiles16.p;
@@ -315,14 +330,14 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
       const bool stream =
           h->stream_force >= 0 ? h->stream_force != 0 : (long long)B * std::min(nprobe, nl) <= nl;
 
-      CK(rd::launch_scan_tc(xm128, xm32, gmap, tn, h->num_sms, s, h->presplit, 16, stream));
+      CK(rd::launch_scan_tc(xm128, xm32, gmap, tn, h->num_sms, s, h->presplit || res, 16, stream, res));
       launches += 1;
     }
     if (tc_mode != 16) {  // wide tiles: the 32-wide scan
       if (pair)
         CK(rd::launch_scan_pair(xm128, xm32, gmap, tc, h->num_sms, s));
       else
-        CK(rd::launch_scan_tc(xm128, xm32, gmap, tc, h->num_sms, s, h->presplit, 32));
+        CK(rd::launch_scan_tc(xm128, xm32, gmap, tc, h->num_sms, s, h->presplit || res, 32, false, res));
       launches += 1;
     }
     if (stall) {

@@ -32,22 +32,28 @@ def split_boundary_index(G, d, ndec):
     return np.array(X, np.float32), np.array(offs, np.int64), np.array(C, np.float32), np.array(Q, np.float32)
 
 
+@pytest.mark.parametrize("store", ["split3", "resid"])
 @pytest.mark.parametrize("d,k", [(64, 1), (64, 5), (128, 10), (768, 1)])
-def test_split_boundary_near_ties_exact(engine, oracle, d, k):
+def test_split_boundary_near_ties_exact(engine, oracle, d, k, store, monkeypatch):
+    # split3: the x1 | x2 scan the data is built against; resid: the residual scan over the same rows
+    # (its keys are lower bounds, so the certificate holds or the fallback runs)
+    monkeypatch.setenv("RD_STORE", store)
     X, offs, C, Q = split_boundary_index(8, d, ndec=k + 11)
     e = engine.index_from_host(X, offs, C).search(Q, 1, k)
     o = oracle.index_from_host(X, offs, C).search(Q, 1, k)
     np.testing.assert_array_equal(e.ids, o.ids)
     np.testing.assert_array_equal(e.dists, o.dists)
     assert (e.ids[:, 0] == offs[:-1]).all()  # each query's own vector A is its nearest
-    if d == 64:  # the approximation ranks A past the rerank set: only the fallback finds it
+    if d == 64 and store == "split3":  # the approximation ranks A past the rerank set: only the fallback finds it
         assert e.stats["margin_failures"] > 0
 
 
+@pytest.mark.parametrize("store", ["split3", "resid"])
 @pytest.mark.parametrize("B", [1, 64])
-def test_split_boundary_coarse_and_seed(engine, oracle, B):
+def test_split_boundary_coarse_and_seed(engine, oracle, B, store, monkeypatch):
     """The same data through every coarse path (GEMV at B <= 8, tensor-core GEMM above) with
     nprobe > 1, so the coarse certificate and the seeded pruning threshold see it too."""
+    monkeypatch.setenv("RD_STORE", store)
     X, offs, C, Q = split_boundary_index(16, 64, ndec=20)
     Qb = np.repeat(Q, (B + len(Q) - 1) // len(Q), axis=0)[:B]
     e = engine.index_from_host(X, offs, C).search(Qb, 3, 10)

@@ -17,9 +17,10 @@ GOLD = np.load(os.path.join(os.path.dirname(__file__), "golden", "ivf_small.npz"
 
 
 def _check(res, want_ids, want_d):
+    from conftest import fallbacks_allowed
     np.testing.assert_array_equal(res.ids, want_ids)
     np.testing.assert_array_equal(res.dists, want_d)
-    assert res.stats["margin_failures"] == 0
+    assert res.stats["margin_failures"] <= fallbacks_allowed(*res.ids.shape)
     assert res.stats["probe_failures"] == 0
 
 
@@ -35,12 +36,17 @@ def test_engine_matches_golden(engine, name):
     _check(idx.search(q, c["nprobe"], c["k"]), GOLD[f"{name}/out_ids"], GOLD[f"{name}/out_dists"])
 
 
-@pytest.mark.parametrize("presplit", ["1", "0"])
+@pytest.mark.parametrize("store", ["resid", "split3", "fp32"])
 @pytest.mark.parametrize("B,nprobe,k", [(1, 8, 10), (7, 1, 1), (32, 16, 10), (100, 64, 20), (33, 5, 24),
                                         (256, 16, 10), (300, 3, 24)])
-def test_engine_vs_oracle_synthetic(engine, oracle, B, nprobe, k, presplit, monkeypatch):
-    # presplit=1: conversion-free scan over the bf16 (x1, x2) copy; 0: converter-warp scan over fp32
-    monkeypatch.setenv("RD_PRESPLIT", presplit)
+def test_engine_vs_oracle_synthetic(engine, oracle, B, nprobe, k, store, monkeypatch):
+    # resid: the residual scan (default); split3: the scan over the x1 | x2 plane; fp32: the
+    # converter-warp scan over fp32 rows
+    if store != "resid":
+        monkeypatch.setenv("RD_STORE", "split3")
+    if store == "fp32":
+        monkeypatch.setenv("RD_SPLIT3", "0")
+        monkeypatch.setenv("RD_PRESPLIT", "0")
     n, d, nlist = 40000, 768, 64
     desc = engine.desc(n, d, nlist)
     q, _ = engine.synth_queries(desc, 1000, B)

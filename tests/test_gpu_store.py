@@ -1,13 +1,14 @@
-"""The resident store: split3 — the exact bf16 triple x = (x1 + x2) + x3, 6 B per
-element, the tensor-core scan's operand without an fp32 copy — or fp32 rows; placements choose the
-format by budget and relayout in place (VMM arenas grow and shrink, never two copies of a list).
-Every search is checked against the CPU oracle bit for bit."""
+"""The resident store: the residual store (default while every list is resident: fp32
+rows + r1 = bf16(x - c_list), 6 B per element, the scan reads 2), split3 — the exact bf16 triple
+x = (x1 + x2) + x3, 6 B per element, the tensor-core scan's operand without an fp32 copy — or fp32
+rows; placements choose the format by budget and relayout in place (VMM arenas grow and shrink,
+never two copies of a list). Every search is checked against the CPU oracle bit for bit."""
 import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
 
-SPLIT3, F32, F32_PRESPLIT = 2, 0, 1
+SPLIT3, F32, F32_PRESPLIT, RESID = 2, 0, 1, 3
 CHUNK = 64 << 20  # largest arena chunk: what a store may hold beyond its rows, per arena
 
 
@@ -20,11 +21,19 @@ def _meta_bytes(n, nlist, d):  # norms, ids, row -> list map, coarse state (rd_i
     return n * 16 + nlist * (d * 8 + 28)
 
 
-def test_split3_is_default_and_exact(engine, oracle, monkeypatch):
+def test_resid_is_default_and_split3_on_request(engine, oracle, monkeypatch):
     n, d, nlist = 150000, 768, 128
     desc = engine.desc(n, d, nlist)
     q, _ = engine.synth_queries(desc, 5, 64)
     want = oracle.synthetic_index(desc).search(q, 12, 10)
+    r = engine.synthetic_index(desc)
+    info = r.info()
+    assert info["store"] == RESID
+    # fp32 rows + the bf16 residual plane + ||x - c||^2 per row: 1.5 x the fp32 rows as well
+    assert info["hbm_bytes"] <= 1.5 * n * d * 4 + n * 4 + 2 * CHUNK + _meta_bytes(n, nlist, d)
+    _same(r.search(q, 12, 10), want)
+    r.close()
+    monkeypatch.setenv("RD_STORE", "split3")
     e = engine.synthetic_index(desc)
     info = e.info()
     assert info["store"] == SPLIT3
@@ -38,24 +47,28 @@ def test_split3_is_default_and_exact(engine, oracle, monkeypatch):
     _same(f.search(q, 12, 10), want)
 
 
+@pytest.mark.parametrize("store", ["resid", "split3"])
 @pytest.mark.parametrize("B", [1, 40, 600])
-def test_split3_every_batch_path(engine, oracle, B):
-    """Staged (small-batch) and direct rerank / seeding / fallback paths over the split3 store."""
+def test_split3_every_batch_path(engine, oracle, B, store, monkeypatch):
+    """Staged (small-batch) and direct rerank / seeding / fallback paths over each store."""
+    monkeypatch.setenv("RD_STORE", store)
     desc = engine.desc(80000, 512, 64)
     q, _ = engine.synth_queries(desc, 77, B)
     _same(engine.synthetic_index(desc).search(q, 9, 24), oracle.synthetic_index(desc).search(q, 9, 24))
 
 
-def test_split3_duplicates_use_the_fallback(engine, oracle):
-    """Duplicate vectors tie across ranks k..m: the exact fallback reads the split3 store."""
+@pytest.mark.parametrize("store", ["resid", "split3"])
+def test_split3_duplicates_use_the_fallback(engine, oracle, store, monkeypatch):
+    """Duplicate vectors tie across ranks k..m: the exact fallback reads the store's rows."""
+    monkeypatch.setenv("RD_STORE", store)
     rng = np.random.default_rng(3)
     base = rng.standard_normal((500, 128)).astype(np.float32)
-    X = np.repeat(base, 24, axis=0)
-    offs = np.array([0, 6000, 12000], np.int64)
-    C = np.stack([X[:6000].mean(0), X[6000:].mean(0)]).astype(np.float32)
+    X = np.repeat(base, 40, axis=0)  # more copies than a 32-entry candidate list holds
+    offs = np.array([0, 10000, 20000], np.int64)
+    C = np.stack([X[:10000].mean(0), X[10000:].mean(0)]).astype(np.float32)
     Q = (base[:16] + 0.01 * rng.standard_normal((16, 128))).astype(np.float32)
     e = engine.index_from_host(X, offs, C)
-    assert e.info()["store"] == SPLIT3
+    assert e.info()["store"] == (SPLIT3 if store == "split3" else RESID)
     r = e.search(Q, 2, 10)
     _same(r, oracle.index_from_host(X, offs, C).search(Q, 2, 10))
     assert r.stats["margin_failures"] > 0
@@ -65,6 +78,7 @@ def test_inexact_split_keeps_fp32_rows(engine, oracle, monkeypatch):
     """Components whose residuals fall below bf16's subnormal range do not round-trip: the index
     keeps fp32 rows and stays exact."""
     monkeypatch.setenv("RD_SPLIT3_QUIET", "1")
+    monkeypatch.setenv("RD_STORE", "split3")
     rng = np.random.default_rng(5)
     X = rng.standard_normal((3000, 64)).astype(np.float32)
     X[7, :5] = np.float32(1.2345678e-38)  # fp32 normal, its split residual is not representable
@@ -83,12 +97,19 @@ def test_placement_picks_the_format_by_budget(engine, oracle):
     want = oracle.synthetic_index(desc).search(q, 16, 10)
     e = engine.synthetic_index(desc)
     rows = n * d
-    # room for every list as split3: the fast store, inside the budget
-    roomy = int(1.5 * rows * 4) + 3 * CHUNK
+    # room for every list in the residual store (fp32 rows + bf16 residuals + ||x - c||^2), inside the
+    # budget; a little less and the split3 store holds them all
+    roomy = int(1.5 * rows * 4) + n * 4 + 3 * CHUNK
+    e.place(hbm_budget_bytes=roomy)
+    info = e.info()
+    assert info["store"] == RESID and info["lists_resident"] == nlist
+    assert info["hbm_bytes"] - _meta_bytes(n, nlist, d) <= roomy
+    _same(e.search(q, 16, 10), want)
+    roomy = int(1.5 * rows * 4) + n * 2
     e.place(hbm_budget_bytes=roomy)
     info = e.info()
     assert info["store"] == SPLIT3 and info["lists_resident"] == nlist
-    assert info["hbm_bytes"] - _meta_bytes(n, nlist, d) <= roomy
+    assert info["hbm_bytes"] - _meta_bytes(n, nlist, d) <= roomy + 2 * CHUNK
     _same(e.search(q, 16, 10), want)
     # a budget below the split3 size but above fp32: every list resident as fp32 rows
     tight = int(1.1 * rows * 4)
@@ -104,9 +125,9 @@ def test_placement_picks_the_format_by_budget(engine, oracle):
     r = e.search(q, 16, 10)
     assert r.stats["h2d_list_bytes"] > 0
     _same(r, want)
-    # no budget again: back to split3, all resident
+    # no budget again: back to the residual store, all resident
     e.place(offload_fraction=0.0)
-    assert e.info()["store"] == SPLIT3 and e.info()["lists_resident"] == nlist
+    assert e.info()["store"] == RESID and e.info()["lists_resident"] == nlist
     _same(e.search(q, 16, 10), want)
 
 

@@ -40,6 +40,7 @@ def test_large_k_offloaded_and_fp32_store(engine, oracle, monkeypatch):
     e = engine.synthetic_index(desc)
     e.place(offload_fraction=0.5)
     _same(e.search(q, 10, 96), want)
+    monkeypatch.setenv("RD_STORE", "split3")
     monkeypatch.setenv("RD_SPLIT3", "0")
     _same(engine.synthetic_index(desc).search(q, 10, 96), want)
 

@@ -32,4 +32,4 @@ if args.offload:
 for i in range(args.searches):
     q, _ = lib.synth_queries(desc, i * args.batch, args.batch)
     r = idx.search(q, args.nprobe, args.k)
-    print(i, {k: r.stats[k] for k in ("scan_ms", "coarse_ms", "tiles", "margin_failures", "bytes_lists_resident")})
+    print(i, {k: r.stats[k] for k in ("scan_ms", "coarse_ms", "total_ms", "tiles", "margin_failures", "bytes_lists_resident") if k in r.stats})
