@@ -537,8 +537,8 @@ struct rd_index {
   bool tc_scan() const { return d % 64 == 0 && rd::scan_tc_smem_bytes(d, 32, false) <= 227 * 1024; }
   // dot-product error bound of the scans whose candidates the merge certifies (ivf_kernels.cuh): the
   // tensor-core and FFMA scans may both run in one search (offloaded or sparse lists)
-  float scan_gamma() const {
-    if (resid) return 0.f;  // the residual scan's keys are lower bounds already (resid.cu)
+  // (a search over the residual store passes 0 instead: its keys are lower bounds already, resid.cu)
+  float scan_gamma_base() const {
     return tc_scan() ? std::max(rd::gamma_bf16x3(d), rd::gamma_ffma_scan(d)) : rd::gamma_ffma_scan(d);
   }
   // Tensor-core tile width for a batch: 16-query tiles (the 16-wide scan's deeper ring) when the
@@ -562,7 +562,7 @@ struct rd_index {
   int rerank_margin_env = std::getenv("RD_RERANK_MARGIN")
                               ? std::max(8, std::min(32, std::atoi(std::getenv("RD_RERANK_MARGIN"))))
                               : -1;
-  int rerank_margin() const { return rerank_margin_env >= 0 ? rerank_margin_env : resid ? 14 : 8; }
+  int rerank_margin(bool res) const { return rerank_margin_env >= 0 ? rerank_margin_env : res ? 14 : 8; }
   bool stage_rows(long long B) const { return B <= (stage_max_b >= 0 ? stage_max_b : 2LL * num_sms); }
   long long n = 0;
   int d = 0, nlist = 0;
@@ -647,7 +647,6 @@ struct rd_index {
   // per-search workspace
   struct Ws {
     DBuf<float> qnorm, Dc, q, qsplit;
-    DBuf<float> pairs, pqn;  // residual store: per (query, list) pair operands and ||q - c||^2 - eps
     DBuf<int> probes, list_nq, list_qoff, list_ntile, list_toff, list_q, part_count, part_row, off_meta;
     DBuf<unsigned> bitmap, fb_ctr;
     bool bitmap_clean = false;  // the bitmap is all-zero (the plan's list_fill re-zeroes it)

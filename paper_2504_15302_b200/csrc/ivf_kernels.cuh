@@ -93,6 +93,13 @@ struct TcScanParams {
   unsigned long long* stall = nullptr;  // profiling only (RD_DEBUG_STALL): per CTA x 12 barrier-wait cycles
   unsigned long long* dbg = nullptr;  // profiling only (RD_DEBUG_TS): per CTA [entry, ready, first tile, end] globaltimer
   int thr_rank = 31;       // as ScanParams::thr_rank
+  // residual store only (scan_tc.cu resid_pair_term): the coarse distances and their bound, ||c||^2
+  // and max ||x - c|| per list, the scan's error factors (gamma_resid_r, gamma_resid_q)
+  const float* Dc = nullptr;
+  int nlist = 0;
+  const float* cnorm = nullptr;
+  const float* rmax = nullptr;
+  float gamma_coarse = 0.f, cmax = 0.f, gamma_res = 0.f, gamma_q = 0.f;
 };
 
 size_t scan_smem_bytes(int d);
@@ -110,32 +117,12 @@ cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, 
                            bool stream = false, bool resid = false);
 
 // Residual store (resid.cu). r1 = bf16(x - c_list) per resident row ([rows][d], the scan's A
-// operand), rnorm[global row] = ||x - c_list||^2 (fp64 sum, RN), rmax[list] = max ||x - c_list||
-// rounded up. One CTA per list.
+// operand), rnorm[global row] = ||x - c_list||^2 + 2 c_list . r1 (fp64 sums, RN), rmax[list] =
+// max ||x - c_list|| rounded up. One CTA per list.
 cudaError_t launch_resid_build(const float* arena, const long long* res_row0, const long long* list_off,
                                const float* centroids, int nlist, int d, void* r1, float* rnorm, float* rmax,
                                cudaStream_t s);
-// Per (query, list) pair of the scan's tiles, by CSR position pos (tile qoff + g): the operand rows
-// 2 pos / 2 pos + 1 = (p1, p2), the bf16 split of p = fl32(q - c_list), and pqn[pos] = ||q - c||^2
-// less the pair's error bound eps (rounded down): the residual scan's keys are then lower bounds on
-// the exact distances. Tiles of two arrays (either may be null); only each (list, query group)'s
-// first chunk computes (its grow0 is the list's first row).
-struct PairParams {
-  const ScanTile* t16;
-  const int* n16;
-  const ScanTile* t32;
-  const int* n32;
-  const int* list_q;
-  const long long* list_off;
-  const float* queries;
-  const float* centroids;
-  const float* rmax;
-  int d;
-  float gamma;  // dot-product error bound of the residual scan (gamma_resid)
-  void* pairs;  // [2 * positions][d] bf16
-  float* pqn;   // [positions]
-};
-cudaError_t launch_pair_operand(const PairParams& p, int grid, cudaStream_t s);
+
 cudaError_t launch_qsplit(const float* Q, void* out, long long B, int d, cudaStream_t s);
 cudaError_t launch_scan(const CUtensorMap& map256, const CUtensorMap& map32, const ScanParams& p,
                         int grid, cudaStream_t s);
@@ -182,9 +169,11 @@ constexpr float kUnit = 5.9604645e-8f;
 inline float gamma_ffma_scan(int d) { return 2.f * (d / 2 + 8) * kUnit; }
 inline float gamma_ffma_coarse(int d) { return 2.f * (d + 4) * kUnit; }
 inline float gamma_bf16x3(int d) { return (524.f + 0.7f * d) * kUnit; }
-// residual scan (r1 = bf16(x - c), p = fl32(q - c) split in two bf16): 2^-9 (1 + 2^-7) for r1's
-// rounding, 2^-17 + 2u for p's, the measured fp32 accumulation term of the bf16x3 model
-inline float gamma_resid(int d) { return (33100.f + 14.f + 0.7f * d) * kUnit; }
+// residual scan (scan_tc.cu resid_pair_term): r1 = bf16(x - c) is within 2^-9 |x - c| (against
+// ||q - c||); D = r1 . (q1 + q2) carries q's split (2^-17) and the measured fp32 accumulation term of
+// the bf16x3 model (against ||q|| max ||r1||, r1 <= (1 + 2^-9) r)
+inline float gamma_resid_r(int) { return 2.f * 16384.f * kUnit * (1.f + 1.f / 128.f); }
+inline float gamma_resid_q(int d) { return (128.f + 16.f + 0.7f * d) * kUnit * (1.f + 1.f / 256.f); }
 
 // Scan tile categories (plan.cu): tensor-core tiles of <= 16 queries (16-wide scan), of <= 32
 // queries (32-wide scan), and FFMA tiles.

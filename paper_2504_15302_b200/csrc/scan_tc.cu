@@ -48,13 +48,22 @@ struct TcGeom {
   static constexpr int BSlice = BRows * 128;
 };
 // ring depth / stage bytes of a (path, width, streamed operand) variant
+#ifndef RD_RES_S32  // residual-store ring depths (16 KiB stages; A/B builds override)
+#define RD_RES_S32 6
+#endif
+#ifndef RD_RES_S16
+#define RD_RES_S16 10
+#endif
+#ifndef RD_RES_SSB
+#define RD_RES_SSB 10
+#endif
 // kRes (residual plane, implies kPre): one 16 KiB r1 tile per stage instead of x1 | x2, so twice the
 // stages in the same bytes
 template <bool kPre, int kG, bool kSB, bool kRes = false>
 struct Ring {
   static_assert(!kSB || (kPre && kG == 16), "streamed operand: pre-split 16-query tiles only");
   static_assert(!kRes || kPre, "the residual plane is read straight into smem");
-  static constexpr int S = kRes ? (kSB ? 10 : (kG == 16 ? 10 : 6))
+  static constexpr int S = kRes ? (kSB ? RD_RES_SSB : (kG == 16 ? RD_RES_S16 : RD_RES_S32))
                                 : kPre ? (kSB ? 6 : TcGeom<kG>::Stages / 2) : TcGeom<kG>::Stages;
   static constexpr int B = kRes ? kRows * 128 + (kSB ? TcGeom<kG>::BSlice : 0)
                                 : kPre ? 2 * kRows * 128 + (kSB ? TcGeom<kG>::BSlice : 0) : kRows * 128;
@@ -129,6 +138,21 @@ __device__ __forceinline__ Smem carve(unsigned char* raw, int d) {
 #define RD_TWAIT(bar, parity, slot) mbar_wait(bar, parity)
 #endif
 
+// Residual store: ||q - c_l||^2 - eps for query b and list l, from ||q||^2 (qq) and the coarse
+// distance Dc = ||c||^2 - 2 q.c (error <= ec, the selection's bound). eps bounds |key - exact| with
+// key = that + rnorm_row - 2 D, D = r1 . (q1 + q2) in fp32 (resid.cu): the coarse error, the bf16
+// rounding of r (2^-9 |r|, against ||q - c||), D's split and accumulation error (against ||q||) and
+// the fp32 roundings of the terms; every bound inflated by 1 %.
+__device__ __forceinline__ float resid_pair_term(const TcScanParams& p, float qq, int b, int l) {
+  const float Q = qq + __ldg(p.Dc + (size_t)b * p.nlist + l);
+  const float nq = sqrtf(qq), rm = __ldg(p.rmax + l), cn = sqrtf(__ldg(p.cnorm + l)) * 1.0001f;
+  const float ec = 2.f * p.gamma_coarse * nq * p.cmax + 16.f * kUnit * (qq + p.cmax * p.cmax);
+  const float na = sqrtf(fmaxf(Q + ec, 0.f)) * 1.0001f;
+  const float eps = 1.01f * (ec + 2.f * p.gamma_res * na * rm + 2.f * p.gamma_q * rm * nq) +
+                    8.f * kUnit * (fabsf(Q) + rm * rm + 2.f * cn * rm + 2.f * rm * nq + qq) + 1e-30f;
+  return Q - eps;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // .x = lo -> low 16 bits
   return *reinterpret_cast<const uint32_t*>(&v);
@@ -138,10 +162,11 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 // kPre = true : pre-split bf16 (x1, x2) arena ([rows][2][d], built with the index); the producer TMA-loads
 //               both 64-dim tiles of a stage straight into 128B-swizzled smem and the MMAs read A from
 //               smem (SS) — no conversion on the scan path; converter warps are idle.
-// kRes: the residual store (resid.cu): A = r1 = bf16(x - c_list) [rows][d], B = the tile's (query, list)
-//       pair operands (p1, p2) = split(q - c_list) gathered by CSR position, one MMA per K step
-//       (r1.[p1;p2]); qnorm is per position (||q - c||^2 less the pair's error bound) and xnorm is
-//       ||x - c||^2, so every key is a lower bound on the exact distance.
+// kRes: the residual store (resid.cu): A = r1 = bf16(x - c_list) [rows][d], B = the queries' split
+//       [q1; q2] as for the split3 store, one MMA per K step (D = r1 . q); xnorm is the row constant
+//       ||x - c||^2 + 2 c . r1 and the per-(query, list) term ||q - c||^2 - eps comes from the coarse
+//       stage's distance (resid_pair_term), so every key is a lower bound on the exact distance:
+//       key = ||q - c||^2 - eps + ||r||^2 + 2 c . r1 - 2 r1 . q.
 template <bool kPre, int kG, bool kSB, bool kRes>
 __global__ void __launch_bounds__(kThreads, 1)
     ivf_scan_tc_kernel(const __grid_constant__ CUtensorMap map128, const __grid_constant__ CUtensorMap map32,
@@ -241,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane < per)
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            r[i] = 2 * (kRes ? T.qoff + min(g0 + i, T.nq - 1) : __ldg(p.list_q + T.qoff + min(g0 + i, T.nq - 1))) + part;
+            r[i] = 2 * __ldg(p.list_q + T.qoff + min(g0 + i, T.nq - 1)) + part;
         for (int i = 0; i < nst; ++i, ++u) {
           const int rt = i / nks, ks = i - rt * nks;
           const int rows = min(kRows, T.nrows - rt * kRows);
@@ -327,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (grp < ngrp)  // the ids load while the ring is refilled below
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          r[i] = 2 * (kRes ? T.qoff + min(g0 + i, T.nq - 1) : __ldg(p.list_q + T.qoff + min(g0 + i, T.nq - 1))) + part;
+          r[i] = 2 * __ldg(p.list_q + T.qoff + min(g0 + i, T.nq - 1)) + part;
       // the first ring's worth of this tile's x stages go out before the wait for the B operand
       // buffer (free once the previous tile's MMAs are done), so HBM keeps streaming across the
       // tile boundary and only the gather's latency is exposed
@@ -579,7 +604,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int j = 0; j < kOwn; ++j) {
         cq[j] = nqid[j];
-        qn[j] = cq[j] >= 0 ? __ldg(p.qnorm + (kRes ? T.qoff + ew + 4 * j : cq[j])) : 0.f;
+        qn[j] = cq[j] >= 0 ? __ldg(p.qnorm + cq[j]) : 0.f;
+        if (kRes && cq[j] >= 0) qn[j] = resid_pair_term(p, qn[j], cq[j], T.list);
         qt[j] = cq[j] >= 0 ? ord2f(*(volatile int*)(p.qthr + cq[j])) : kInf;
       }
       for (int rt = 0; rt * kRows < T.nrows; ++rt, ++rtc) {

@@ -160,6 +160,12 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   // rides in a trailing CTA of the GEMV coarse kernel
   const rd::QprepArgs qa{d_q, B, d, w.qnorm.p, d % 64 == 0 ? w.qsplit.p : nullptr, w.fails(), w.part_count.p};
   const bool sel_all = select_all_needed(h, nprobe);  // probes from exact distances to every centroid
+  // residual store: the scan's keys need the coarse distances (not computed by the all-centroid
+  // selection: those searches take the converter scan over the fp32 rows, with its error bound);
+  // k > 18 as well: its rerank margin (32 - k) no longer clears the residual keys' bound, so a few
+  // percent of queries would take the exact fallback (measured 4 % at k = 24)
+  const bool res = h->resid && h->tc_scan() && h->slots == 0 && !sel_all && k + 14 <= rd::kTopK;
+  const float scan_gamma = res ? 0.f : h->scan_gamma_base();
   const bool wide = k > rd::kMaxK;                      // the exact large-k pass instead of scan + rerank
   if (sel_all) {
     CK(rd::launch_qprep(qa, s));
@@ -179,7 +185,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   rd::SelectParams sp{w.Dc.p, d_q, w.qnorm.p, h->centroids.p, w.probes.p, w.fails(), (int)B, nl, nprobe, d, h->cmax,
                       h->d_list_off.p, h->d_res_row0.p, h->arena.p, h->xmax, seed ? w.qthr.p : nullptr, 0};
   sp.gamma_coarse = coarse_gamma(B, d);
-  sp.gamma_scan = h->scan_gamma();
+  sp.gamma_scan = scan_gamma;
   sp.x12 = h->x12_dev();
   sp.x3 = h->x3_dev();
   unsigned long long* chain = nullptr;  // profiling only (RD_DEBUG_CHAIN): [select 32][plan 32][merge 32][scan 4/CTA + tiles, rows]
@@ -202,7 +208,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   }
   // the merge reranks m = min(32, k + margin) candidates and certifies against the next: scans
   // prune with, and the seed bounds, that rank's distance
-  const int m_rerank = std::min(rd::kTopK, k + h->rerank_margin());
+  const int m_rerank = std::min(rd::kTopK, k + h->rerank_margin(res));
   const int thr_rank = std::min(rd::kTopK - 1, m_rerank);
   sp.seed_rows = thr_rank + 1;
   rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
@@ -268,17 +274,6 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     if (use_bm) w.bitmap_clean = true;  // list_fill, now enqueued, clears every bit the selection sets
     launches += use_bm ? 3 : 1;
   }
-  // residual store: the scan's B operand is per (query, list) pair, by CSR position (resid.cu)
-  const bool res = h->resid && h->tc_scan() && h->slots == 0;
-  if (res) {
-    w.pairs.ensure((size_t)B * nprobe * d);  // 2 bf16 per element
-    w.pqn.ensure((size_t)B * nprobe);
-    rd::PairParams pr{tc_mode != 32 ? w.tiles16.p : nullptr, w.meta() + 2 * rd::kCatNarrow,
-                      tc_mode != 16 ? w.tiles.p : nullptr, w.meta() + 2 * rd::kCatWide, w.list_q.p,
-                      h->d_list_off.p, d_q, h->centroids.p, h->rmax.p, d, rd::gamma_resid(d), w.pairs.p, w.pqn.p};
-    CK(rd::launch_pair_operand(pr, 4 * h->num_sms, s));
-    launches += 1;
-  }
   const bool staged = h->stage_events;
   if (staged) CK(cudaEventRecord(e1, s));
 
@@ -290,7 +285,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     CK(cudaMemcpyAsync(w.h_qoff.p, w.list_qoff.p, sizeof(int) * nl, cudaMemcpyDeviceToHost, s));
   }
   if (has_off) CK(cudaEventRecord(e_plan, s));  // an event between two kernels costs their PDL overlap
-  const CUtensorMap gmap = res ? make_gather_map(w.pairs.p, B * nprobe, d) : make_gather_map(w.qsplit.p, B, d);
+  const CUtensorMap gmap = make_gather_map(w.qsplit.p, B, d);
   rd::ScanParams sc{w.ff_tiles.p, w.meta() + 2 * rd::kCatFfma, w.meta() + 2 * rd::kCatFfma + 1, d_q, w.qnorm.p,
                     w.list_q.p, h->xnorm.p, w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p};
   rd::TcScanParams tc{w.tiles.p, w.meta() + 2 * rd::kCatWide, w.meta() + 2 * rd::kCatWide + 1, w.qsplit.p, w.qnorm.p,
@@ -298,9 +293,16 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
                       w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p, h->debug_skip};
   sc.thr_rank = thr_rank;
   tc.thr_rank = thr_rank;
-  if (res) {
-    tc.qnorm = w.pqn.p;
+  if (res) {  // residual store: lower-bound keys from the coarse distances (scan_tc.cu resid_pair_term)
     tc.xnorm = h->rnorm.p;
+    tc.Dc = w.Dc.p;
+    tc.nlist = nl;
+    tc.cnorm = h->cnorm.p;
+    tc.rmax = h->rmax.p;
+    tc.gamma_coarse = coarse_gamma(B, d);
+    tc.cmax = h->cmax;
+    tc.gamma_res = rd::gamma_resid_r(d);
+    tc.gamma_q = rd::gamma_resid_q(d);
   }
   if (!h->split3 && (!h->tc_scan() || h->tc_min_q > 1)) {  // FFMA tiles exist only in these cases (fp32 store)
     CK(rd::launch_scan(h->map256, h->map32, sc, h->num_sms, s));
@@ -532,7 +534,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
                        h->arena.p ? h->arena.p + (size_t)h->n_resident * d : nullptr, nl, d, k, h->xmax, d_ids, d_dists,
                        w.fails() + 1, w.fail_list.p, (int)B};
     mp.m_rerank = m_rerank;
-    mp.gamma = h->scan_gamma();
+    mp.gamma = scan_gamma;
     mp.res_row0 = h->d_res_row0.p;
     mp.x12 = h->x12_dev();
     mp.x3 = h->x3_dev();
