@@ -106,9 +106,9 @@ size_t scan_smem_bytes(int d);
 size_t scan_tc_smem_bytes(int d, int tc_g, bool presplit, bool stream = false, bool resid = false);
 // 32-query tiles over the x1 | x2 plane on CTA pairs (scan_pair.cu, cta_group::2): ring depth for
 // this d (0: unsupported), and the launch (grid = the SMs rounded down to pairs)
-int scan_pair_stages(int d);
+int scan_pair_stages(int d, bool resid = false);
 cudaError_t launch_scan_pair(const CUtensorMap& map128, const CUtensorMap& map32, const CUtensorMap& qmap,
-                             const TcScanParams& p, int num_sms, cudaStream_t s);
+                             const TcScanParams& p, int num_sms, cudaStream_t s, bool resid = false);
 // qmap: 2D bf16 map over the qsplit buffer as [2B rows x d], box {64, 1} (gather4 source)
 // presplit: map128 / map32 are 3D bf16 maps over the pre-split [rows][2][d] arena, box {64, 1, 128|32}
 // tc_g: queries per tile, 16 or 32 (the planner grouped the tiles with the same width)
@@ -174,6 +174,25 @@ inline float gamma_bf16x3(int d) { return (524.f + 0.7f * d) * kUnit; }
 // the bf16x3 model (against ||q|| max ||r1||, r1 <= (1 + 2^-9) r)
 inline float gamma_resid_r(int) { return 2.f * 16384.f * kUnit * (1.f + 1.f / 128.f); }
 inline float gamma_resid_q(int d) { return (128.f + 16.f + 0.7f * d) * kUnit * (1.f + 1.f / 256.f); }
+
+#ifdef __CUDACC__
+// Residual store: ||q - c_l||^2 - eps for query b and list l, from ||q||^2 (qq) and the coarse
+// distance Dc = ||c||^2 - 2 q.c (error <= ec, the selection's bound). eps bounds |key - exact| with
+// key = that + rnorm_row - 2 D, D = r1 . (q1 + q2) in fp32 (resid.cu): the coarse error, the bf16
+// rounding of r (2^-9 |r|, against ||q - c||), D's split and accumulation error (against ||q||) and
+// the fp32 roundings of the terms; every bound inflated by 1 %.
+__device__ __forceinline__ float resid_pair_term(const TcScanParams& p, float qq, int b, int l) {
+  const float Q = qq + __ldg(p.Dc + (size_t)b * p.nlist + l);
+  const float nq = sqrtf(qq), rm = __ldg(p.rmax + l), cn = sqrtf(__ldg(p.cnorm + l)) * 1.0001f;
+  const float ec = 2.f * p.gamma_coarse * nq * p.cmax + 16.f * kUnit * (qq + p.cmax * p.cmax);
+  const float na = sqrtf(fmaxf(Q + ec, 0.f)) * 1.0001f;
+  const float eps = 1.01f * (ec + 2.f * p.gamma_res * na * rm + 2.f * p.gamma_q * rm * nq) +
+                    8.f * kUnit * (fabsf(Q) + rm * rm + 2.f * cn * rm + 2.f * rm * nq + qq) + 1e-30f;
+  return Q - eps;
+}
+
+#endif
+
 
 // Scan tile categories (plan.cu): tensor-core tiles of <= 16 queries (16-wide scan), of <= 32
 // queries (32-wide scan), and FFMA tiles.

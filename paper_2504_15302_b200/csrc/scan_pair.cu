@@ -88,6 +88,13 @@ __device__ __forceinline__ void tma3_pair(uint32_t dst, const CUtensorMap* map, 
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(cl_bar)
       : "memory");
 }
+__device__ __forceinline__ void tma2_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t cl_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(cl_bar)
+      : "memory");
+}
 __device__ __forceinline__ void gather4_pair(uint32_t dst, const CUtensorMap* map, int col, int r0, int r1, int r2, int r3,
                                              uint32_t cl_bar) {
   asm volatile(
@@ -133,8 +140,13 @@ struct PSmem {
   float* edist;
 };
 
-template <int kS>
+// x stage bytes per CTA: x1 | x2 (split3), or the residual store's r1 (one 16 KiB tile)
+template <bool kRes>
+constexpr int pstage_bytes() { return kRes ? kPRows * 128 : kPStageBytes; }
+
+template <int kS, bool kRes>
 __device__ __forceinline__ PSmem pcarve(unsigned char* raw, int d) {
+  constexpr int kPStageBytes = pstage_bytes<kRes>();
   PSmem s;
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
   s.xs = smem_u32(base);
@@ -156,16 +168,18 @@ __device__ __forceinline__ PSmem pcarve(unsigned char* raw, int d) {
   s.edist = s.stage_d + 4 * 32;
   return s;
 }
-template <int kS>
+template <int kS, bool kRes = false>
 constexpr size_t pair_smem_bytes_for(int d) {
+  constexpr int kPStageBytes = pstage_bytes<kRes>();
   return 1024 + (size_t)kS * kPStageBytes + (size_t)(d / 64) * kPHalfSlice + (2 * kS + 10) * 8 + 16 +
          2 * sizeof(ScanTile) + 8 + 4 * 32 * 12 + (size_t)kPG * kPRows * 4 + 64;
 }
 
 // bytes one CTA's TMA brings for its half of row block rt (rows in 32-row boxes, x1 and x2)
+template <bool kRes>
 __device__ __forceinline__ uint32_t half_bytes(int nrows, int rt, int rank) {
   const int rows = min(kPRows, max(0, nrows - rt * kPBlock - rank * kPRows));
-  return (uint32_t)(2 * ((rows + 31) >> 5) * 4096);
+  return (uint32_t)((kRes ? 1 : 2) * ((rows + 31) >> 5) * 4096);
 }
 
 // profiling only (built with -DRD_STALL_PROF, run with RD_DEBUG_STALL): cycles a role spends blocked
@@ -185,14 +199,17 @@ __device__ __forceinline__ uint32_t half_bytes(int nrows, int rt, int rank) {
 #define RD_PWAIT(expr, slot) expr
 #endif
 
-template <int kS>
+// kRes: the residual store (resid.cu, scan_tc.cu): A = r1 tiles, one M = 256 MMA per K step
+// (r1.[q1;q2]), lower-bound keys from resid_pair_term.
+template <int kS, bool kRes>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
     ivf_scan_pair_kernel(const __grid_constant__ CUtensorMap map128, const __grid_constant__ CUtensorMap map32,
                          const __grid_constant__ CUtensorMap qmap, const TcScanParams p) {
   RD_PDL_PROLOGUE();
   extern __shared__ unsigned char smem_raw[];
   const int d = p.d, nks = d / 64;
-  const PSmem sm = pcarve<kS>(smem_raw, d);
+  const PSmem sm = pcarve<kS, kRes>(smem_raw, d);
+  constexpr int kPStageBytes = pstage_bytes<kRes>();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
@@ -279,12 +296,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
         const int s = u % kS;
         RD_PWAIT(mbar_wait(&sm.empty[s], ((u / kS) & 1) ^ 1), 1);
         const uint32_t lb = L_full0 + 8 * s;
-        if (leader) mbar_arrive_expect_tx(&sm.full[s], half_bytes(T.nrows, rt, 0) + half_bytes(T.nrows, rt, 1));
+        if (leader)
+          mbar_arrive_expect_tx(&sm.full[s], half_bytes<kRes>(T.nrows, rt, 0) + half_bytes<kRes>(T.nrows, rt, 1));
         const int rows = min(kPRows, T.nrows - rt * kPBlock - (int)rank * kPRows);
         if (rows > 0) {
           const uint32_t dst = sm.xs + s * kPStageBytes;
           const int row = (int)(T.src_row + rt * kPBlock + (int)rank * kPRows);
-          if (rows == kPRows) {
+          if (kRes) {
+            if (rows == kPRows)
+              tma2_pair(dst, &map128, ks * 64, row, lb);
+            else
+              for (int b = 0; b < (rows + 31) >> 5; ++b) tma2_pair(dst + b * 4096, &map32, ks * 64, row + b * 32, lb);
+          } else if (rows == kPRows) {
             tma3_pair(dst, &map128, ks * 64, 0, row, lb);
             tma3_pair(dst + kPRows * 128, &map128, ks * 64, 1, row, lb);
           } else {
@@ -361,7 +384,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
               for (int kk = 0; kk < 4; ++kk) {
                 const uint32_t acc = (ks | kk) != 0;
                 mma2_bf16_ss(dacc, a1 + kk * 2, bd + (uint64_t)(kk * 2), idesc, acc);
-                mma2_bf16_ss(dacc + 2 * kPG, a2 + kk * 2, bd + (uint64_t)(kk * 2), idesc, acc);
+                if constexpr (!kRes) mma2_bf16_ss(dacc + 2 * kPG, a2 + kk * 2, bd + (uint64_t)(kk * 2), idesc, acc);
               }
               tc_commit_mc(&sm.empty[s]);
             }
@@ -407,6 +430,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
         const int g = ew + 4 * j;
         const int qid = g < nq ? __ldg(p.list_q + T.qoff + g) : 0;
         qn[j] = g < nq ? __ldg(p.qnorm + qid) : 0.f;
+        if (kRes && g < nq) qn[j] = resid_pair_term(p, qn[j], qid, T.list);
         qt[j] = g < nq ? ord2f(*(volatile int*)(p.qthr + qid)) : kPInf;
         ld[j] = kPInf;
         lk[j] = kPNoKey;
@@ -422,7 +446,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
         for (int c = 0; c < kPG; c += 16) {
           RD_TMEM_LD16(ta + c, (d1 + c));
           RD_TMEM_LD16(ta + c2 + c, (d2 + c));
-          RD_TMEM_LD16(ta + 2 * kPG + c, (d3 + c));
+          if constexpr (!kRes) RD_TMEM_LD16(ta + 2 * kPG + c, (d3 + c));
         }
         tmem_ld_wait();
         tc_fence_before();
@@ -440,7 +464,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
         named_bar_sync(2, 128);  // every owner finished reading the previous row tile
 #pragma unroll
         for (int g = 0; g < kPG; ++g) {
-          const float dot = (__uint_as_float(d1[g]) + __uint_as_float(d2[g])) + __uint_as_float(d3[g]);
+          const float dot = kRes ? __uint_as_float(d1[g]) + __uint_as_float(d2[g])
+                                 : (__uint_as_float(d1[g]) + __uint_as_float(d2[g])) + __uint_as_float(d3[g]);
           edist[g * kPRows + r] = (valid && g < nq) ? xn - 2.f * dot : kPInf;
         }
         named_bar_sync(2, 128);
@@ -544,8 +569,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
 
 }  // namespace
 
-int scan_pair_stages(int d) {
+int scan_pair_stages(int d, bool resid) {
   if (d % 64 != 0) return 0;
+  if (resid) return pair_smem_bytes_for<10, true>(d) <= 227 * 1024 ? 10 : pair_smem_bytes_for<8, true>(d) <= 227 * 1024 ? 8 : 0;
   if (pair_smem_bytes_for<5>(d) <= 227 * 1024) return 5;
   if (pair_smem_bytes_for<4>(d) <= 227 * 1024) return 4;
   if (pair_smem_bytes_for<3>(d) <= 227 * 1024) return 3;
@@ -553,19 +579,28 @@ int scan_pair_stages(int d) {
 }
 
 cudaError_t launch_scan_pair(const CUtensorMap& map128, const CUtensorMap& map32, const CUtensorMap& qmap,
-                             const TcScanParams& p, int num_sms, cudaStream_t s) {
-  const int S = scan_pair_stages(p.d);
+                             const TcScanParams& p, int num_sms, cudaStream_t s, bool resid) {
+  const int S = scan_pair_stages(p.d, resid);
   const dim3 grid((unsigned)(num_sms / 2 * 2));
+  if (resid) {
+    if (S == 10)
+      return launch_k(ivf_scan_pair_kernel<10, true>, grid, dim3(kPThreads), pair_smem_bytes_for<10, true>(p.d), s,
+                      map128, map32, qmap, p);
+    if (S == 8)
+      return launch_k(ivf_scan_pair_kernel<8, true>, grid, dim3(kPThreads), pair_smem_bytes_for<8, true>(p.d), s,
+                      map128, map32, qmap, p);
+    return cudaErrorInvalidValue;
+  }
   switch (S) {
     case 5:
-      return launch_k(ivf_scan_pair_kernel<5>, grid, dim3(kPThreads), pair_smem_bytes_for<5>(p.d), s, map128, map32,
-                      qmap, p);
+      return launch_k(ivf_scan_pair_kernel<5, false>, grid, dim3(kPThreads), pair_smem_bytes_for<5>(p.d), s, map128,
+                      map32, qmap, p);
     case 4:
-      return launch_k(ivf_scan_pair_kernel<4>, grid, dim3(kPThreads), pair_smem_bytes_for<4>(p.d), s, map128, map32,
-                      qmap, p);
+      return launch_k(ivf_scan_pair_kernel<4, false>, grid, dim3(kPThreads), pair_smem_bytes_for<4>(p.d), s, map128,
+                      map32, qmap, p);
     case 3:
-      return launch_k(ivf_scan_pair_kernel<3>, grid, dim3(kPThreads), pair_smem_bytes_for<3>(p.d), s, map128, map32,
-                      qmap, p);
+      return launch_k(ivf_scan_pair_kernel<3, false>, grid, dim3(kPThreads), pair_smem_bytes_for<3>(p.d), s, map128,
+                      map32, qmap, p);
     default:
       return cudaErrorInvalidValue;
   }

@@ -138,21 +138,6 @@ __device__ __forceinline__ Smem carve(unsigned char* raw, int d) {
 #define RD_TWAIT(bar, parity, slot) mbar_wait(bar, parity)
 #endif
 
-// Residual store: ||q - c_l||^2 - eps for query b and list l, from ||q||^2 (qq) and the coarse
-// distance Dc = ||c||^2 - 2 q.c (error <= ec, the selection's bound). eps bounds |key - exact| with
-// key = that + rnorm_row - 2 D, D = r1 . (q1 + q2) in fp32 (resid.cu): the coarse error, the bf16
-// rounding of r (2^-9 |r|, against ||q - c||), D's split and accumulation error (against ||q||) and
-// the fp32 roundings of the terms; every bound inflated by 1 %.
-__device__ __forceinline__ float resid_pair_term(const TcScanParams& p, float qq, int b, int l) {
-  const float Q = qq + __ldg(p.Dc + (size_t)b * p.nlist + l);
-  const float nq = sqrtf(qq), rm = __ldg(p.rmax + l), cn = sqrtf(__ldg(p.cnorm + l)) * 1.0001f;
-  const float ec = 2.f * p.gamma_coarse * nq * p.cmax + 16.f * kUnit * (qq + p.cmax * p.cmax);
-  const float na = sqrtf(fmaxf(Q + ec, 0.f)) * 1.0001f;
-  const float eps = 1.01f * (ec + 2.f * p.gamma_res * na * rm + 2.f * p.gamma_q * rm * nq) +
-                    8.f * kUnit * (fabsf(Q) + rm * rm + 2.f * cn * rm + 2.f * rm * nq + qq) + 1e-30f;
-  return Q - eps;
-}
-
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // .x = lo -> low 16 bits
   return *reinterpret_cast<const uint32_t*>(&v);

@@ -129,7 +129,14 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   // offloaded lists' host-planned tiles use one width
   const int tc_mode = h->tc_mode_for(B, nprobe);
   // wide tiles over the x1 | x2 plane on CTA pairs (cta_group::2): RD_PAIR=1 only (slower)
-  const bool pair = tc_mode != 16 && h->tc_scan() && h->presplit && h->pair_scan && rd::scan_pair_stages(h->d) > 0;
+  const bool sel_all = select_all_needed(h, nprobe);  // probes from exact distances to every centroid
+  // residual store: the scan's keys need the coarse distances (not computed by the all-centroid
+  // selection: those searches take the converter scan over the fp32 rows, with its error bound);
+  // k > 18 as well: its rerank margin (32 - k) no longer clears the residual keys' bound, so a few
+  // percent of queries would take the exact fallback (measured 4 % at k = 24)
+  const bool res = h->resid && h->tc_scan() && h->slots == 0 && !sel_all && k + 14 <= rd::kTopK;
+  const bool pair = tc_mode != 16 && h->tc_scan() && (h->presplit || res) && h->pair_scan &&
+                    rd::scan_pair_stages(h->d, res) > 0;
   const Plan pl = make_plan(h, B, nprobe, pair);
   const int tc_g = tc_mode == 16 ? 16 : 32;
   const int W = (int)((B + 31) / 32);
@@ -159,12 +166,6 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   // ||q||^2 and the query split (the tensor-core scan's operand) in one pass; at small batches it
   // rides in a trailing CTA of the GEMV coarse kernel
   const rd::QprepArgs qa{d_q, B, d, w.qnorm.p, d % 64 == 0 ? w.qsplit.p : nullptr, w.fails(), w.part_count.p};
-  const bool sel_all = select_all_needed(h, nprobe);  // probes from exact distances to every centroid
-  // residual store: the scan's keys need the coarse distances (not computed by the all-centroid
-  // selection: those searches take the converter scan over the fp32 rows, with its error bound);
-  // k > 18 as well: its rerank margin (32 - k) no longer clears the residual keys' bound, so a few
-  // percent of queries would take the exact fallback (measured 4 % at k = 24)
-  const bool res = h->resid && h->tc_scan() && h->slots == 0 && !sel_all && k + 14 <= rd::kTopK;
   const float scan_gamma = res ? 0.f : h->scan_gamma_base();
   const bool wide = k > rd::kMaxK;                      // the exact large-k pass instead of scan + rerank
   if (sel_all) {
@@ -337,7 +338,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     }
     if (tc_mode != 16) {  // wide tiles: the 32-wide scan
       if (pair)
-        CK(rd::launch_scan_pair(xm128, xm32, gmap, tc, h->num_sms, s));
+        CK(rd::launch_scan_pair(xm128, xm32, gmap, tc, h->num_sms, s, res));
       else
         CK(rd::launch_scan_tc(xm128, xm32, gmap, tc, h->num_sms, s, h->presplit || res, 32, false, res));
       launches += 1;

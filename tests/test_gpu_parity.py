@@ -245,12 +245,14 @@ def test_duplicate_heavy_data(engine, oracle, margin, monkeypatch):
         assert e.stats["margin_failures"] == 0
 
 
+@pytest.mark.parametrize("store", ["resid", "split3"])
 @pytest.mark.parametrize("n,nlist,B,nprobe", [(200000, 64, 300, 16), (60000, 32, 97, 8), (300000, 128, 1024, 24)])
-def test_pair_scan_matches_oracle(engine, oracle, monkeypatch, n, nlist, B, nprobe):
-    """The paired-CTA wide scan (scan_pair.cu, tcgen05 cta_group::2; opt-in RD_PAIR=1): lists probed
-    by > 8 queries on average take 32-query tiles on CTA pairs, including lists whose last 256-row
-    block leaves the peer CTA no rows; bit-exact against the oracle."""
+def test_pair_scan_matches_oracle(engine, oracle, monkeypatch, n, nlist, B, nprobe, store):
+    """The paired-CTA wide scan (scan_pair.cu, tcgen05 cta_group::2; opt-in RD_PAIR=1) over either
+    store: lists probed by > 8 queries on average take 32-query tiles on CTA pairs, including lists
+    whose last 256-row block leaves the peer CTA no rows; bit-exact against the oracle."""
     monkeypatch.setenv("RD_PAIR", "1")  # read when the index is created
+    monkeypatch.setenv("RD_STORE", store)
     desc = engine.desc(n, 768, nlist)
     q, _ = engine.synth_queries(desc, 11, B)
     r = engine.synthetic_index(desc).search(q, nprobe, 10)
