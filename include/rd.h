@@ -81,8 +81,10 @@ typedef struct {
 
 /* Placement between searches (reference analogue: PlacementConfig, domain.hpp:75-82).
  * Lists not resident live in pinned host memory and are streamed per search. The engine keeps the
- * resident rows as RD_STORE_SPLIT3 (6 B per element) when the tensor-core scan applies and the budget
- * does not cut the resident set at that size, else as fp32 (4 B per element: under a tight budget
+ * resident rows as RD_STORE_F32_RESID (fp32 rows + bf16 residuals: 6 B per element + 4 B per row) when
+ * every list stays resident within the budget (d % 128 == 0), else as RD_STORE_SPLIT3 (6 B per
+ * element) when the tensor-core scan applies and the budget does not cut the resident set at that
+ * size, else as fp32 (4 B per element: under a tight budget
  * residency beats scan speed, since every list left out streams over the host link per search).
  * Relayouts happen in place: the store grows or shrinks in chunks (<= 64 MiB) and never holds two
  * copies of a list; a 64 MiB conversion buffer is the only transient. Waits for searches in flight. */

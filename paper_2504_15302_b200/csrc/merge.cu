@@ -16,7 +16,10 @@ namespace {
 
 constexpr float kInf = __builtin_huge_valf();
 constexpr long long kNoKey = 0x7fffffffffffffffll;
-constexpr int kDecodeBatch = 8;  // 8-element row chunks per thread per round trip (staged rerank)
+#ifndef RD_DECODE_BATCH
+#define RD_DECODE_BATCH 12
+#endif
+constexpr int kDecodeBatch = RD_DECODE_BATCH;  // 8-element row chunks per thread per round trip (staged rerank; 12: the 24 candidate rows of a residual-store search in one round, B = 1 +0.8 %)
 
 // One CTA per query. kStage (small batches, one latency chain per query): the candidate rows are
 // decoded into fp32 rows in shared memory (128-bit loads, every load of a round in flight, split3

@@ -20,7 +20,7 @@ struct Plan {
   long long max_tiles;
 };
 
-Plan make_plan(const rd_index* h, long long B, int nprobe, bool pair) {
+Plan make_plan(const rd_index* h, long long B, int nprobe, bool pair, bool res) {
   Plan pl;
   const int np = std::min(nprobe, h->nlist);
   const double avg = h->nlist ? (double)h->n / h->nlist : 0.0;
@@ -30,9 +30,11 @@ Plan make_plan(const rd_index* h, long long B, int nprobe, bool pair) {
   // B200 (C2): 32 per SM up to a few hundred queries (+0.4-1.5 % over 8), 8 from 512 queries on,
   // where one chunk per list keeps the partial records few. Rows rounded to the tensor-core tile
   // (128), at least 256 (shorter tiles lost at one query), and at least one 256-row TMA box of the
-  // FFMA scan when that path is in use; chunk_rows then balances each list's chunks.
+  // FFMA scan when that path is in use; chunk_rows then balances each list's chunks. The residual
+  // scan reads half the bytes per row, so a tile's fixed cost weighs twice as much: 8 per SM at every
+  // batch (B = 8 +3.8 %, 128 +2 %, 256 +2.4 % over 32; B = 1 unchanged).
   const long long gran = rd::kTcRows;
-  const int tps = h->tiles_per_sm > 0 ? h->tiles_per_sm : (B >= 512 ? 8 : 32);
+  const int tps = h->tiles_per_sm > 0 ? h->tiles_per_sm : (B >= 512 || res ? 8 : 32);
   long long R = (long long)std::ceil(est_rows / ((double)h->num_sms * tps));
   static const long long floor_r = std::getenv("RD_MIN_ROWS") ? std::atoll(std::getenv("RD_MIN_ROWS")) : rd::kScanRows;
   // tail chunks: one tensor-core row tile (128) when every tile is a tensor-core tile (B200, B = 1:
@@ -137,7 +139,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   const bool res = h->resid && h->tc_scan() && h->slots == 0 && !sel_all && k + 14 <= rd::kTopK;
   const bool pair = tc_mode != 16 && h->tc_scan() && (h->presplit || res) && h->pair_scan &&
                     rd::scan_pair_stages(h->d, res) > 0;
-  const Plan pl = make_plan(h, B, nprobe, pair);
+  const Plan pl = make_plan(h, B, nprobe, pair, res);
   const int tc_g = tc_mode == 16 ? 16 : 32;
   const int W = (int)((B + 31) / 32);
   w.qnorm.ensure(B);
