@@ -412,6 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk) {
                 const uint32_t acc = (ks | kk) != 0;
+                if (p.debug_skip & 4) continue;  // profiling only: no MMAs (RD_DEBUG_SKIP)
                 mma_bf16_ss(dacc, a1 + kk * 2, bd + (uint64_t)(kk * 2), ida, acc);
                 if constexpr (!kRes) mma_bf16_ss(dacc + kBRows, a2 + kk * 2, bd + (uint64_t)(kk * 2), idb, acc);
               }
