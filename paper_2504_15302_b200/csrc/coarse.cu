@@ -8,6 +8,7 @@
 //     is certified when every non-candidate's approximate distance, less the
 //     GEMM's error bound, exceeds the nprobe-th exact distance.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <float.h>
 
 #include "ivf_kernels.cuh"
@@ -132,6 +133,11 @@ __device__ __forceinline__ void qprep_rows(const QprepArgs& a, long long r0, lon
         uint2* q2 = reinterpret_cast<uint2*>(qs + (size_t)(r * 2 + 1) * a.d);
         q1[i] = make_uint2(hi[0], hi[1]);
         q2[i] = make_uint2(lo[0], lo[1]);
+      }
+      if (a.qhalf) {  // fp16 residual scan's operand (RN; overflow to inf is caught by the scan)
+        const __half2 h01 = __floats2half2_rn(q[0], q[1]), h23 = __floats2half2_rn(q[2], q[3]);
+        reinterpret_cast<uint2*>(a.qhalf)[(size_t)r * (a.d / 4) + i] =
+            make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
       }
     }
 #pragma unroll

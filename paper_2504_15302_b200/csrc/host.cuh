@@ -456,7 +456,7 @@ CUtensorMap make_gather_map(const void* base, long long rows, int d) {
 
 // 2D bf16 map over a [rows][d] plane (the residual store's r1), box {64 dims, box_rows}, 128B swizzle:
 // the same smem tile as one part of the split map's box.
-CUtensorMap make_bf16_row_map(const void* base, long long rows, int d, int box_rows) {
+CUtensorMap make_bf16_row_map(const void* base, long long rows, int d, int box_rows, bool fp16 = false) {
   CUtensorMap m;
   std::memset(&m, 0, sizeof m);
   if (rows < 1) rows = 1;
@@ -464,10 +464,11 @@ CUtensorMap make_bf16_row_map(const void* base, long long rows, int d, int box_r
   cuuint64_t strides[1] = {(cuuint64_t)d * 2};
   cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw_rd(RD_ERR_RUNTIME, "cuTensorMapEncodeTiled (bf16 rows) failed (%d)", (int)r);
+  CUresult r = encode_fn()(&m, fp16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                           const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw_rd(RD_ERR_RUNTIME, "cuTensorMapEncodeTiled (16-bit rows) failed (%d)", (int)r);
   return m;
 }
 
@@ -562,7 +563,12 @@ struct rd_index {
   int rerank_margin_env = std::getenv("RD_RERANK_MARGIN")
                               ? std::max(8, std::min(32, std::atoi(std::getenv("RD_RERANK_MARGIN"))))
                               : -1;
-  int rerank_margin(bool res) const { return rerank_margin_env >= 0 ? rerank_margin_env : res ? 14 : 8; }
+  // (fp16 residual scan from 512 queries: 21 — its slightly wider bound sent ~1 query in a few
+  // thousand to the exact fallback at margin 14, which at B = 1024 costs more than the wider rerank:
+  // +3-4 % measured; below 512 queries 14 is as fast or faster)
+  int rerank_margin(bool res, bool res16, long long B) const {
+    return rerank_margin_env >= 0 ? rerank_margin_env : res ? (res16 && B >= 512 ? 21 : 14) : 8;
+  }
   bool stage_rows(long long B) const { return B <= (stage_max_b >= 0 ? stage_max_b : 2LL * num_sms); }
   long long n = 0;
   int d = 0, nlist = 0;
@@ -610,6 +616,13 @@ struct rd_index {
     rnorm.reset();
     rmax.reset();
   }
+  // fp16 residual plane and fp16(q) operand (default; RD_RES16=0: bf16 plane with the (q1; q2) split)
+  // unless a component leaves fp16's range
+  bool res16 = false;
+  static bool res16_wanted() {
+    const char* v = std::getenv("RD_RES16");
+    return !(v && std::atoi(v) == 0);
+  }
   bool build_resid() {
     size_t fr = 0, tot = 0;
     CK(cudaMemGetInfo(&fr, &tot));
@@ -618,10 +631,22 @@ struct rd_index {
     rplane.alloc((size_t)n * d);
     rnorm.alloc(n);
     rmax.alloc(nlist);
-    CK(rd::launch_resid_build(arena.p, d_res_row0.p, d_list_off.p, centroids.p, nlist, d, rplane.p, rnorm.p, rmax.p, 0));
+    res16 = res16_wanted();
+    if (res16) {
+      DBuf<unsigned> ovf;
+      ovf.alloc(1);
+      CK(cudaMemset(ovf.p, 0, sizeof(unsigned)));
+      CK(rd::launch_resid_build(arena.p, d_res_row0.p, d_list_off.p, centroids.p, nlist, d, rplane.p, rnorm.p,
+                                rmax.p, 0, true, ovf.p));
+      unsigned bad = 0;
+      CK(cudaMemcpy(&bad, ovf.p, sizeof bad, cudaMemcpyDeviceToHost));
+      res16 = bad == 0;
+    }
+    if (!res16)
+      CK(rd::launch_resid_build(arena.p, d_res_row0.p, d_list_off.p, centroids.p, nlist, d, rplane.p, rnorm.p, rmax.p, 0));
     CK(cudaDeviceSynchronize());
-    rmap128 = make_bf16_row_map(rplane.p, n_resident, d, rd::kTcRows);
-    rmap32 = make_bf16_row_map(rplane.p, n_resident, d, 32);
+    rmap128 = make_bf16_row_map(rplane.p, n_resident, d, rd::kTcRows, res16);
+    rmap32 = make_bf16_row_map(rplane.p, n_resident, d, 32, res16);
     resid = true;
     return true;
   }
@@ -647,6 +672,7 @@ struct rd_index {
   // per-search workspace
   struct Ws {
     DBuf<float> qnorm, Dc, q, qsplit;
+    DBuf<uint16_t> qhalf;  // fp16 residual scan: q as fp16 [B][d]
     DBuf<int> probes, list_nq, list_qoff, list_ntile, list_toff, list_q, part_count, part_row, off_meta;
     DBuf<unsigned> bitmap, fb_ctr;
     bool bitmap_clean = false;  // the bitmap is all-zero (the plan's list_fill re-zeroes it)

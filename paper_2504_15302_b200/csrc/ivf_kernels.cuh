@@ -99,11 +99,11 @@ struct TcScanParams {
   int nlist = 0;
   const float* cnorm = nullptr;
   const float* rmax = nullptr;
-  float gamma_coarse = 0.f, cmax = 0.f, gamma_res = 0.f, gamma_q = 0.f;
+  float gamma_coarse = 0.f, cmax = 0.f, gamma_res = 0.f, gamma_q = 0.f, abs_res = 0.f;
 };
 
 size_t scan_smem_bytes(int d);
-size_t scan_tc_smem_bytes(int d, int tc_g, bool presplit, bool stream = false, bool resid = false);
+size_t scan_tc_smem_bytes(int d, int tc_g, bool presplit, bool stream = false, bool resid = false, bool half = false);
 // 32-query tiles over the x1 | x2 plane on CTA pairs (scan_pair.cu, cta_group::2): ring depth for
 // this d (0: unsupported), and the launch (grid = the SMs rounded down to pairs)
 int scan_pair_stages(int d, bool resid = false);
@@ -114,14 +114,15 @@ cudaError_t launch_scan_pair(const CUtensorMap& map128, const CUtensorMap& map32
 // tc_g: queries per tile, 16 or 32 (the planner grouped the tiles with the same width)
 cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, const CUtensorMap& qmap,
                            const TcScanParams& p, int grid, cudaStream_t s, bool presplit, int tc_g,
-                           bool stream = false, bool resid = false);
+                           bool stream = false, bool resid = false, bool half = false);
 
 // Residual store (resid.cu). r1 = bf16(x - c_list) per resident row ([rows][d], the scan's A
 // operand), rnorm[global row] = ||x - c_list||^2 + 2 c_list . r1 (fp64 sums, RN), rmax[list] =
 // max ||x - c_list|| rounded up. One CTA per list.
+// half: r1 as fp16 (the fp16 residual scan); *ovf counts components beyond fp16's range
 cudaError_t launch_resid_build(const float* arena, const long long* res_row0, const long long* list_off,
                                const float* centroids, int nlist, int d, void* r1, float* rnorm, float* rmax,
-                               cudaStream_t s);
+                               cudaStream_t s, bool half = false, unsigned* ovf = nullptr);
 
 cudaError_t launch_qsplit(const float* Q, void* out, long long B, int d, cudaStream_t s);
 cudaError_t launch_scan(const CUtensorMap& map256, const CUtensorMap& map32, const ScanParams& p,
@@ -141,6 +142,7 @@ struct QprepArgs {
   void* qsplit;
   unsigned* zero2;
   int* zeroB;
+  void* qhalf = nullptr;  // fp16 residual scan: q as fp16 rows [B][d]
 };
 cudaError_t launch_qprep(const QprepArgs& a, cudaStream_t s);
 // small batches: FFMA GEMV over the centroids (memory-bound; see coarse_small for the cut-over), with
@@ -174,6 +176,13 @@ inline float gamma_bf16x3(int d) { return (524.f + 0.7f * d) * kUnit; }
 // the bf16x3 model (against ||q|| max ||r1||, r1 <= (1 + 2^-9) r)
 inline float gamma_resid_r(int) { return 2.f * 16384.f * kUnit * (1.f + 1.f / 128.f); }
 inline float gamma_resid_q(int d) { return (128.f + 16.f + 0.7f * d) * kUnit * (1.f + 1.f / 256.f); }
+// fp16 residual scan (r1 = fp16(x - c), B = fp16(q), no split): 2^-11 for each rounding (r1 against
+// ||q - c||; q1 against ||q|| max ||r1||, with the accumulation term); subnormals: abs_resid16
+inline float gamma_resid16_r(int) { return 8192.f * kUnit * (1.f + 1.f / 512.f); }
+inline float gamma_resid16_q(int d) { return (8192.f + 16.f + 0.7f * d) * kUnit * (1.f + 1.f / 256.f); }
+// fp16 subnormals (|v| < 2^-14) round with an absolute error <= 2^-25 per element: with Cauchy-Schwarz
+// <= 2^-25 sqrt(d) (||q - c|| + max ||r1||) on the dot, doubled in the distance
+inline float abs_resid16(int d) { return 2.f * 2.9802322e-8f * sqrtf((float)d) * 1.01f; }
 
 #ifdef __CUDACC__
 // Residual store: ||q - c_l||^2 - eps for query b and list l, from ||q||^2 (qq) and the coarse
@@ -186,7 +195,7 @@ __device__ __forceinline__ float resid_pair_term(const TcScanParams& p, float qq
   const float nq = sqrtf(qq), rm = __ldg(p.rmax + l), cn = sqrtf(__ldg(p.cnorm + l)) * 1.0001f;
   const float ec = 2.f * p.gamma_coarse * nq * p.cmax + 16.f * kUnit * (qq + p.cmax * p.cmax);
   const float na = sqrtf(fmaxf(Q + ec, 0.f)) * 1.0001f;
-  const float eps = 1.01f * (ec + 2.f * p.gamma_res * na * rm + 2.f * p.gamma_q * rm * nq) +
+  const float eps = 1.01f * (ec + 2.f * p.gamma_res * na * rm + 2.f * p.gamma_q * rm * nq + p.abs_res * (na + rm)) +
                     8.f * kUnit * (fabsf(Q) + rm * rm + 2.f * cn * rm + 2.f * rm * nq + qq) + 1e-30f;
   return Q - eps;
 }

@@ -13,6 +13,7 @@
 // seeding threshold need no error term of their own. Exactness is every store's: exact rerank of
 // the candidates from the fp32 rows, certification, exact fallback.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "ivf_kernels.cuh"
 #include "rd_device.cuh"
@@ -34,8 +35,8 @@ __global__ void __launch_bounds__(256) resid_build_kernel(const float* __restric
                                                           const long long* __restrict__ res_row0,
                                                           const long long* __restrict__ list_off,
                                                           const float* __restrict__ centroids, int d,
-                                                          __nv_bfloat16* __restrict__ r1, float* __restrict__ rnorm,
-                                                          float* __restrict__ rmax) {
+                                                          uint16_t* __restrict__ r1, float* __restrict__ rnorm,
+                                                          float* __restrict__ rmax, bool half, unsigned* ovf) {
   __shared__ double wmax[8];
   const int l = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long g0 = list_off[l], len = list_off[l + 1] - g0, sr0 = res_row0[l];
@@ -47,20 +48,31 @@ __global__ void __launch_bounds__(256) resid_build_kernel(const float* __restric
   if (sr0 >= 0)
     for (long long i = warp; i < len; i += 8) {
       const float* x = arena + (size_t)(sr0 + i) * d;
-      __nv_bfloat16* o = r1 + (size_t)(sr0 + i) * d;
+      uint16_t* o = r1 + (size_t)(sr0 + i) * d;
       double s = 0.0, t = 0.0;  // ||r||^2, c . r1
+      unsigned bad = 0;
 #pragma unroll
       for (int j = 0; j < kMaxPerLane; ++j) {
         if (j >= per) break;
         const double r = (double)x[j * 32 + lane] - c[j];
-        const __nv_bfloat16 h = __double2bfloat16(r);
-        o[j * 32 + lane] = h;
+        double rv;
+        if (half) {
+          const __half h = __double2half(r);
+          rv = (double)__half2float(h);
+          bad += fabs(r) >= 65504.0;
+          o[j * 32 + lane] = __half_as_ushort(h);
+        } else {
+          const __nv_bfloat16 h = __double2bfloat16(r);
+          rv = (double)__bfloat162float(h);
+          o[j * 32 + lane] = __bfloat16_as_ushort(h);
+        }
         s = fma(r, r, s);
-        t = fma(c[j], (double)__bfloat162float(h), t);
+        t = fma(c[j], rv, t);
       }
       s = warp_sum_f64(s);
       t = warp_sum_f64(t);
       if (lane == 0) rnorm[g0 + i] = (float)(s + 2.0 * t);
+      if (bad && ovf) atomicAdd(ovf, bad);
       mx = fmax(mx, s);
     }
   if (lane == 0) wmax[warp] = mx;
@@ -76,10 +88,10 @@ __global__ void __launch_bounds__(256) resid_build_kernel(const float* __restric
 
 cudaError_t launch_resid_build(const float* arena, const long long* res_row0, const long long* list_off,
                                const float* centroids, int nlist, int d, void* r1, float* rnorm, float* rmax,
-                               cudaStream_t s) {
+                               cudaStream_t s, bool half, unsigned* ovf) {
   if (d % 32 != 0 || d > 32 * kMaxPerLane || nlist <= 0) return cudaErrorInvalidValue;
-  resid_build_kernel<<<nlist, 256, 0, s>>>(arena, res_row0, list_off, centroids, d,
-                                           reinterpret_cast<__nv_bfloat16*>(r1), rnorm, rmax);
+  resid_build_kernel<<<nlist, 256, 0, s>>>(arena, res_row0, list_off, centroids, d, reinterpret_cast<uint16_t*>(r1),
+                                           rnorm, rmax, half, ovf);
   return cudaGetLastError();
 }
 

@@ -48,6 +48,15 @@ struct TcGeom {
   static constexpr int BSlice = BRows * 128;
 };
 // ring depth / stage bytes of a (path, width, streamed operand) variant
+#ifndef RD_RESH_S32  // fp16 residual scan: half the resident operand, deeper rings
+#define RD_RESH_S32 10
+#endif
+#ifndef RD_RESH_S16
+#define RD_RESH_S16 11
+#endif
+#ifndef RD_RESH_SSB
+#define RD_RESH_SSB 11
+#endif
 #ifndef RD_RES_S32  // residual-store ring depths (16 KiB stages; A/B builds override)
 #define RD_RES_S32 6
 #endif
@@ -59,13 +68,20 @@ struct TcGeom {
 #endif
 // kRes (residual plane, implies kPre): one 16 KiB r1 tile per stage instead of x1 | x2, so twice the
 // stages in the same bytes
-template <bool kPre, int kG, bool kSB, bool kRes = false>
+// query-operand rows per tile: [q1; q2] (bf16 split), or q1 alone for the fp16 residual scan (kH)
+template <int kG, bool kH>
+struct BGeom {
+  static constexpr int Rows = kH ? kG : 2 * kG;
+  static constexpr int Slice = Rows * 128;
+};
+template <bool kPre, int kG, bool kSB, bool kRes = false, bool kH = false>
 struct Ring {
   static_assert(!kSB || (kPre && kG == 16), "streamed operand: pre-split 16-query tiles only");
   static_assert(!kRes || kPre, "the residual plane is read straight into smem");
-  static constexpr int S = kRes ? (kSB ? RD_RES_SSB : (kG == 16 ? RD_RES_S16 : RD_RES_S32))
+  static constexpr int S = kH ? (kSB ? RD_RESH_SSB : (kG == 16 ? RD_RESH_S16 : RD_RESH_S32))
+                         : kRes ? (kSB ? RD_RES_SSB : (kG == 16 ? RD_RES_S16 : RD_RES_S32))
                                 : kPre ? (kSB ? 6 : TcGeom<kG>::Stages / 2) : TcGeom<kG>::Stages;
-  static constexpr int B = kRes ? kRows * 128 + (kSB ? TcGeom<kG>::BSlice : 0)
+  static constexpr int B = kRes ? kRows * 128 + (kSB ? BGeom<kG, kH>::Slice : 0)
                                 : kPre ? 2 * kRows * 128 + (kSB ? TcGeom<kG>::BSlice : 0) : kRows * 128;
   // converter group g owns stages / TMEM buffers with u % 2 == g; an odd ring depth would let one
   // group wait on a phase two ahead of the other group's and alias its mbarrier parity
@@ -92,11 +108,11 @@ struct Smem {
   long long* stage_k; // [4][32]
 };
 
-template <bool kPre, int kG, bool kSB, bool kRes>
+template <bool kPre, int kG, bool kSB, bool kRes, bool kH>
 __device__ __forceinline__ Smem carve(unsigned char* raw, int d) {
-  constexpr int kStages = Ring<kPre, kG, kSB, kRes>::S, kBSlice = TcGeom<kG>::BSlice;
+  constexpr int kStages = Ring<kPre, kG, kSB, kRes, kH>::S, kBSlice = BGeom<kG, kH>::Slice;
   // ring bytes (+ the resident operand unless the stages carry it)
-  const size_t xring = (size_t)kStages * Ring<kPre, kG, kSB, kRes>::B;
+  const size_t xring = (size_t)kStages * Ring<kPre, kG, kSB, kRes, kH>::B;
   const size_t ring = xring + (kSB ? 0 : (size_t)(d / 64) * kBSlice);
   Smem s;
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
@@ -152,22 +168,25 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 //       ||x - c||^2 + 2 c . r1 and the per-(query, list) term ||q - c||^2 - eps comes from the coarse
 //       stage's distance (resid_pair_term), so every key is a lower bound on the exact distance:
 //       key = ||q - c||^2 - eps + ||r||^2 + 2 c . r1 - 2 r1 . q.
-template <bool kPre, int kG, bool kSB, bool kRes>
+// kH (implies kRes): the fp16 residual scan — r1 = fp16(x - c) and B = fp16(q) alone (N = G): 2^-11
+//       roundings instead of bf16's 2^-9 leave q's split out; half the operand, twice the ring.
+template <bool kPre, int kG, bool kSB, bool kRes, bool kH>
 __global__ void __launch_bounds__(kThreads, 1)
     ivf_scan_tc_kernel(const __grid_constant__ CUtensorMap map128, const __grid_constant__ CUtensorMap map32,
                        const __grid_constant__ CUtensorMap qmap, const TcScanParams p) {
-  constexpr int kTcG = kG, kStages = Ring<kPre, kG, kSB, kRes>::S, kBRows = TcGeom<kG>::BRows,
-                kBSlice = TcGeom<kG>::BSlice;
+  constexpr int kTcG = kG, kStages = Ring<kPre, kG, kSB, kRes, kH>::S, kBRows = BGeom<kG, kH>::Rows,
+                kBSlice = BGeom<kG, kH>::Slice;
+  static_assert(!kH || kRes, "fp16 operands: residual store only");
   constexpr bool kStream = kSB;  // the query operand travels with the stages
   constexpr bool kHalfN = kPre && !kSB && kG == 32;  // half-N MMAs for tiles of <= 16 queries
   RD_PDL_PROLOGUE();
   if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 4 + 0] = gtimer();
   extern __shared__ unsigned char smem_raw[];
   const int d = p.d, nks = kPre ? d / 64 : d / 32;
-  const Smem sm = carve<kPre, kG, kSB, kRes>(smem_raw, d);
+  const Smem sm = carve<kPre, kG, kSB, kRes, kH>(smem_raw, d);
   // ring geometry: kStages stages of RB bytes (pre-split: x1 | x2 [| B slice]; converter: fp32 x)
   constexpr int RS = kStages;
-  constexpr int RB = Ring<kPre, kG, kSB, kRes>::B;
+  constexpr int RB = Ring<kPre, kG, kSB, kRes, kH>::B;
   constexpr int kXTiles = kRes ? 1 : 2;  // A tiles per stage (r1; or x1, x2)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -243,15 +262,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         // (TMA gather4 from the L2-resident split queries: rows 0..kG-1 q1, kG..2kG-1 q2; lane qi
         // < 2 qq loads quad qi; padding rows repeat the tile's last query; quads beyond the tile's
         // queries keep stale rows whose D columns the epilogue never reads).
-        const int qq = (T.nq + 3) >> 2, per = 2 * qq;
-        const int part = lane >= qq ? 1 : 0;
+        const int qq = (T.nq + 3) >> 2, per = kH ? qq : 2 * qq;
+        const int part = !kH && lane >= qq ? 1 : 0;
         const int g0 = (lane - part * qq) * 4;
         const uint32_t boff = kXTiles * kRows * 128 + (part * (kTcG / 4) + g0 / 4) * 512;
         int r[4] = {0, 0, 0, 0};
         if (lane < per)
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            r[i] = 2 * __ldg(p.list_q + T.qoff + min(g0 + i, T.nq - 1)) + part;
+            r[i] = (kH ? 1 : 2) * __ldg(p.list_q + T.qoff + min(g0 + i, T.nq - 1)) + part;
         for (int i = 0; i < nst; ++i, ++u) {
           const int rt = i / nks, ks = i - rt * nks;
           const int rows = min(kRows, T.nrows - rt * kRows);
@@ -330,14 +349,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       // quads holding real queries are loaded; the others keep stale rows whose D columns the
       // epilogue never reads. Lane (grp, qi) owns quad qi of part qi / qq for slices grp, grp + ngrp..
       const int qq = (T.nq + 3) >> 2;  // quads per part
-      const int per = 2 * qq, ngrp = 32 / per, grp = lane / per, qi = lane - grp * per;
-      const int part = qi >= qq ? 1 : 0;
+      const int per = kH ? qq : 2 * qq, ngrp = 32 / per, grp = lane / per, qi = lane - grp * per;
+      const int part = !kH && qi >= qq ? 1 : 0;
       const int g0 = (qi - part * qq) * 4;
       int r[4];
       if (grp < ngrp)  // the ids load while the ring is refilled below
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          r[i] = 2 * __ldg(p.list_q + T.qoff + min(g0 + i, T.nq - 1)) + part;
+          r[i] = (kH ? 1 : 2) * __ldg(p.list_q + T.qoff + min(g0 + i, T.nq - 1)) + part;
       // the first ring's worth of this tile's x stages go out before the wait for the B operand
       // buffer (free once the previous tile's MMAs are done), so HBM keeps streaming across the
       // tile boundary and only the gather's latency is exposed
@@ -349,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       RD_TWAIT(sm.bempty, (ti & 1) ^ 1, 2);
       // one barrier for the whole gather (per-slice barriers let the first MMAs start earlier but
       // cost more than they saved: A/B on B200, 1024 queries, 206.4k vs 207.2k q/s)
-      if (lane == 0) mbar_arrive_expect_tx(sm.bfull, (uint32_t)(nslices * 2 * qq * 512));
+      if (lane == 0) mbar_arrive_expect_tx(sm.bfull, (uint32_t)(nslices * per * 512));
       __syncwarp();
       if (grp < ngrp) {
         // half tiles (<= 16 queries of a 32-wide tile): q2 right after q1 (rows 16-31), so the MMAs run
@@ -368,8 +387,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   else if (warp == 1) {
     // per tile: full N (x1.[q1;q2] N = 64, x2.q1 N = 32) or, for tiles of <= 16 queries in the
     // 32-wide scan, half N (32, 16) over the compacted operand — half the tensor work (and power)
-    const uint32_t ida_full = idesc_bf16(kRows, kBRows), idb_full = idesc_bf16(kRows, kTcG);
-    const uint32_t ida_half = idesc_bf16(kRows, kBRows / 2), idb_half = idesc_bf16(kRows, kTcG / 2);
+    const uint32_t ida_full = kH ? idesc_f16(kRows, kBRows) : idesc_bf16(kRows, kBRows), idb_full = idesc_bf16(kRows, kTcG);
+    const uint32_t ida_half = kH ? idesc_f16(kRows, kBRows / 2) : idesc_bf16(kRows, kBRows / 2),
+                   idb_half = idesc_bf16(kRows, kTcG / 2);
     const unsigned char* bs_ptr = reinterpret_cast<unsigned char*>(smem_raw) + (sm.bs - smem_u32(smem_raw));
     const uint64_t bdesc0 = umma_desc_sw128(bs_ptr);
     uint32_t u = 0, rtc = 0;
@@ -606,7 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c = 0; c < kTcG; c += 16) {
           RD_TMEM_LD16(ta + c, (d1 + c));
-          RD_TMEM_LD16(ta + c2 + c, (d2 + c));
+          if constexpr (!kH) RD_TMEM_LD16(ta + c2 + c, (d2 + c));
           if constexpr (!kRes) RD_TMEM_LD16(ta + 2 * kTcG + c, (d3 + c));
         }
         tmem_ld_wait();
@@ -621,8 +641,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         named_bar_sync(2, 128);  // every owner finished reading the previous row tile
 #pragma unroll
         for (int g = 0; g < kTcG; ++g) {
-          const float dot = kRes ? __uint_as_float(d1[g]) + __uint_as_float(d2[g])
-                                 : (__uint_as_float(d1[g]) + __uint_as_float(d2[g])) + __uint_as_float(d3[g]);
+          float dot = kH     ? __uint_as_float(d1[g])
+                      : kRes ? __uint_as_float(d1[g]) + __uint_as_float(d2[g])
+                             : (__uint_as_float(d1[g]) + __uint_as_float(d2[g])) + __uint_as_float(d3[g]);
+          // fp16 operands can overflow (|q| or |x - c| >= 65520): a non-finite dot gives the key -inf,
+          // still a lower bound, so the certificate fails and the exact fallback answers the query
+          if (kH && !(fabsf(dot) <= 3.0e38f)) dot = __builtin_huge_valf();
           eb[g * kRows + r] = (valid && g < nq) ? xn - 2.f * dot : kInf;
         }
         named_bar_sync(2, 128);
@@ -735,11 +759,16 @@ __global__ void qsplit_kernel(const float* __restrict__ Q, __nv_bfloat16* __rest
 
 }  // namespace
 
-size_t scan_tc_smem_bytes(int d, int tc_g, bool presplit, bool stream, bool resid) {
+size_t scan_tc_smem_bytes(int d, int tc_g, bool presplit, bool stream, bool resid, bool half) {
   stream = stream && presplit && tc_g == 16;
   resid = resid && presplit;
+  half = half && resid;
   size_t stages, sbytes;
-  if (resid) {
+  if (half) {
+    stages = stream ? Ring<true, 16, true, true, true>::S
+                    : tc_g == 16 ? Ring<true, 16, false, true, true>::S : Ring<true, 32, false, true, true>::S;
+    sbytes = stream ? Ring<true, 16, true, true, true>::B : Ring<true, 16, false, true, true>::B;
+  } else if (resid) {
     stages = stream ? Ring<true, 16, true, true>::S : tc_g == 16 ? Ring<true, 16, false, true>::S : Ring<true, 32, false, true>::S;
     sbytes = stream ? Ring<true, 16, true, true>::B : Ring<true, 16, false, true>::B;
   } else {
@@ -748,7 +777,8 @@ size_t scan_tc_smem_bytes(int d, int tc_g, bool presplit, bool stream, bool resi
                         : (tc_g == 16 ? Ring<false, 16, false>::S : Ring<false, 32, false>::S);
     sbytes = stream ? Ring<true, 16, true>::B : presplit ? Ring<true, 16, false>::B : Ring<false, 16, false>::B;
   }
-  const size_t bslice = tc_g == 16 ? TcGeom<16>::BSlice : TcGeom<32>::BSlice;
+  const size_t bslice = half ? (tc_g == 16 ? BGeom<16, true>::Slice : BGeom<32, true>::Slice)
+                             : (tc_g == 16 ? TcGeom<16>::BSlice : TcGeom<32>::BSlice);
   const size_t xring = stages * sbytes;
   const size_t ring = xring + (stream ? 0 : (size_t)(d / 64) * bslice);
   return 1024 + ring +
@@ -758,30 +788,39 @@ size_t scan_tc_smem_bytes(int d, int tc_g, bool presplit, bool stream, bool resi
 
 cudaError_t launch_scan_tc(const CUtensorMap& map128, const CUtensorMap& map32, const CUtensorMap& qmap,
                            const TcScanParams& p, int grid, cudaStream_t s, bool presplit, int tc_g, bool stream,
-                           bool resid) {
+                           bool resid, bool half) {
   if (p.d % 64 != 0 || (tc_g != 16 && tc_g != 32)) return cudaErrorInvalidValue;
   stream = stream && presplit && tc_g == 16;
   resid = resid && presplit;
-  const size_t smem = scan_tc_smem_bytes(p.d, tc_g, presplit, stream, resid);
+  half = half && resid;
+  const size_t smem = scan_tc_smem_bytes(p.d, tc_g, presplit, stream, resid, half);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  if (half) {
+    if (tc_g == 16) {
+      if (stream)
+        return launch_k(ivf_scan_tc_kernel<true, 16, true, true, true>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+      return launch_k(ivf_scan_tc_kernel<true, 16, false, true, true>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+    }
+    return launch_k(ivf_scan_tc_kernel<true, 32, false, true, true>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+  }
   if (resid) {
     if (tc_g == 16) {
       if (stream)
-        return launch_k(ivf_scan_tc_kernel<true, 16, true, true>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
-      return launch_k(ivf_scan_tc_kernel<true, 16, false, true>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+        return launch_k(ivf_scan_tc_kernel<true, 16, true, true, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+      return launch_k(ivf_scan_tc_kernel<true, 16, false, true, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
     }
-    return launch_k(ivf_scan_tc_kernel<true, 32, false, true>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+    return launch_k(ivf_scan_tc_kernel<true, 32, false, true, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
   }
   if (tc_g == 16) {
     if (stream)
-      return launch_k(ivf_scan_tc_kernel<true, 16, true, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+      return launch_k(ivf_scan_tc_kernel<true, 16, true, false, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
     if (presplit)
-      return launch_k(ivf_scan_tc_kernel<true, 16, false, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
-    return launch_k(ivf_scan_tc_kernel<false, 16, false, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+      return launch_k(ivf_scan_tc_kernel<true, 16, false, false, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+    return launch_k(ivf_scan_tc_kernel<false, 16, false, false, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
   }
   if (presplit)
-    return launch_k(ivf_scan_tc_kernel<true, 32, false, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
-  return launch_k(ivf_scan_tc_kernel<false, 32, false, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+    return launch_k(ivf_scan_tc_kernel<true, 32, false, false, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
+  return launch_k(ivf_scan_tc_kernel<false, 32, false, false, false>, dim3(grid), dim3(kThreads), smem, s, map128, map32, qmap, p);
 }
 
 cudaError_t launch_qsplit(const float* Q, void* out, long long B, int d, cudaStream_t s) {

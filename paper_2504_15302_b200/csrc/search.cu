@@ -137,7 +137,8 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   // k > 18 as well: its rerank margin (32 - k) no longer clears the residual keys' bound, so a few
   // percent of queries would take the exact fallback (measured 4 % at k = 24)
   const bool res = h->resid && h->tc_scan() && h->slots == 0 && !sel_all && k + 14 <= rd::kTopK;
-  const bool pair = tc_mode != 16 && h->tc_scan() && (h->presplit || res) && h->pair_scan &&
+  const bool res16 = res && h->res16;  // fp16 residual scan (B = fp16(q) alone)
+  const bool pair = tc_mode != 16 && h->tc_scan() && (h->presplit || res) && !res16 && h->pair_scan &&
                     rd::scan_pair_stages(h->d, res) > 0;
   const Plan pl = make_plan(h, B, nprobe, pair, res);
   const int tc_g = tc_mode == 16 ? 16 : 32;
@@ -167,7 +168,11 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   CK(cudaEventRecord(e0, s));
   // ||q||^2 and the query split (the tensor-core scan's operand) in one pass; at small batches it
   // rides in a trailing CTA of the GEMV coarse kernel
-  const rd::QprepArgs qa{d_q, B, d, w.qnorm.p, d % 64 == 0 ? w.qsplit.p : nullptr, w.fails(), w.part_count.p};
+  rd::QprepArgs qa{d_q, B, d, w.qnorm.p, d % 64 == 0 ? w.qsplit.p : nullptr, w.fails(), w.part_count.p};
+  if (res16) {
+    w.qhalf.ensure((size_t)B * d);
+    qa.qhalf = w.qhalf.p;
+  }
   const float scan_gamma = res ? 0.f : h->scan_gamma_base();
   const bool wide = k > rd::kMaxK;                      // the exact large-k pass instead of scan + rerank
   if (sel_all) {
@@ -211,7 +216,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
   }
   // the merge reranks m = min(32, k + margin) candidates and certifies against the next: scans
   // prune with, and the seed bounds, that rank's distance
-  const int m_rerank = std::min(rd::kTopK, k + h->rerank_margin(res));
+  const int m_rerank = std::min(rd::kTopK, k + h->rerank_margin(res, res16, B));
   const int thr_rank = std::min(rd::kTopK - 1, m_rerank);
   sp.seed_rows = thr_rank + 1;
   rd::PlanParams pp{w.probes.p, w.bitmap.p, W, h->d_list_off.p, h->d_res_row0.p, w.list_nq.p, w.list_qoff.p,
@@ -288,7 +293,7 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     CK(cudaMemcpyAsync(w.h_qoff.p, w.list_qoff.p, sizeof(int) * nl, cudaMemcpyDeviceToHost, s));
   }
   if (has_off) CK(cudaEventRecord(e_plan, s));  // an event between two kernels costs their PDL overlap
-  const CUtensorMap gmap = make_gather_map(w.qsplit.p, B, d);
+  const CUtensorMap gmap = res16 ? make_bf16_row_map(w.qhalf.p, B, d, 1, true) : make_gather_map(w.qsplit.p, B, d);
   rd::ScanParams sc{w.ff_tiles.p, w.meta() + 2 * rd::kCatFfma, w.meta() + 2 * rd::kCatFfma + 1, d_q, w.qnorm.p,
                     w.list_q.p, h->xnorm.p, w.part_dist.p, w.part_row.p, w.part_count.p, pl.cap, d, w.qthr.p};
   rd::TcScanParams tc{w.tiles.p, w.meta() + 2 * rd::kCatWide, w.meta() + 2 * rd::kCatWide + 1, w.qsplit.p, w.qnorm.p,
@@ -304,8 +309,9 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
     tc.rmax = h->rmax.p;
     tc.gamma_coarse = coarse_gamma(B, d);
     tc.cmax = h->cmax;
-    tc.gamma_res = rd::gamma_resid_r(d);
-    tc.gamma_q = rd::gamma_resid_q(d);
+    tc.gamma_res = res16 ? rd::gamma_resid16_r(d) : rd::gamma_resid_r(d);
+    tc.gamma_q = res16 ? rd::gamma_resid16_q(d) : rd::gamma_resid_q(d);
+    tc.abs_res = res16 ? rd::abs_resid16(d) : 0.f;
   }
   if (!h->split3 && (!h->tc_scan() || h->tc_min_q > 1)) {  // FFMA tiles exist only in these cases (fp32 store)
     CK(rd::launch_scan(h->map256, h->map32, sc, h->num_sms, s));
@@ -335,14 +341,14 @@ void do_search(rd_index* h, const float* d_q, long long B, int nprobe, int k, lo
       const bool stream =
           h->stream_force >= 0 ? h->stream_force != 0 : (long long)B * std::min(nprobe, nl) <= nl;
 
-      CK(rd::launch_scan_tc(xm128, xm32, gmap, tn, h->num_sms, s, h->presplit || res, 16, stream, res));
+      CK(rd::launch_scan_tc(xm128, xm32, gmap, tn, h->num_sms, s, h->presplit || res, 16, stream, res, res16));
       launches += 1;
     }
     if (tc_mode != 16) {  // wide tiles: the 32-wide scan
       if (pair)
         CK(rd::launch_scan_pair(xm128, xm32, gmap, tc, h->num_sms, s, res));
       else
-        CK(rd::launch_scan_tc(xm128, xm32, gmap, tc, h->num_sms, s, h->presplit || res, 32, false, res));
+        CK(rd::launch_scan_tc(xm128, xm32, gmap, tc, h->num_sms, s, h->presplit || res, 32, false, res, res16));
       launches += 1;
     }
     if (stall) {
