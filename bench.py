@@ -514,7 +514,7 @@ def run_ours(args, cfg):
     scan_ms = tm["scan_ms"] / max(1, tm["stage_searches"])
     scan_bytes = st1["bytes_lists_resident"]  # probed resident rows x d x 4 (SURVEY §8d's per-row unit)
     fp32_equiv = None
-    if info["store"] == 3:  # residual store: the scan reads r1 (d x 2 B) and ||x - c||^2 (4 B) per row
+    if info["store"] in (3, 4):  # residual store: the scan reads r1 (d x 2 B) and ||x - c||^2 (4 B) per row
         rows = scan_bytes // (d * 4)
         fp32_equiv = {"bytes_per_launch": scan_bytes,
                       "gbs": scan_bytes / (scan_ms * 1e-3) / 1e9 if scan_ms > 0 else 0.0,
@@ -551,7 +551,7 @@ def run_ours(args, cfg):
         "e2e": e2e,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": ("ivf_scan_tc_kernel (N5 over the residual store: r1 = bf16(x - c) tiles)" if info["store"] == 3
+                     "kernel": ("ivf_scan_tc_kernel (N5 over the residual store: 16-bit r1 = x - c tiles)" if info["store"] in (3, 4)
                                 else "ivf_scan_tc_kernel (N5; FFMA ivf_scan_kernel N4 when d % 64 != 0)"),
                      "peak_source": ("MEASURED_PEAKS.json hbm_gbs (a torch copy: read + write bytes); a read-only "
                                      "stream of the scan's TMA pattern reaches ~7.46 TB/s (tools/micro/bw.cu)")
@@ -568,7 +568,8 @@ def run_ours(args, cfg):
         "decode_stream": decode.summary() if decode is not None else None,
         "index": {"build_s": build_s, "lists_resident": info["lists_resident"], "hbm_bytes": info["hbm_bytes"],
                   "store": {0: "fp32", 1: "fp32 + pre-split copy", 2: "split3 (exact bf16 triple)",
-                            3: "fp32 + bf16 residual plane (scan reads 2 B/element)"}.get(info["store"]),
+                            3: "fp32 + bf16 residual plane (scan reads 2 B/element)",
+                            4: "fp32 + fp16 residual plane (scan reads 2 B/element)"}.get(info["store"]),
                   "fp32_bytes": info["n"] * d * 4,
                   "host_pinned_bytes": info["host_pinned_bytes"], "h2d_list_bytes_per_step": st1["h2d_list_bytes"],
                   "llm_reservation_bytes": reservation},

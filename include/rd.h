@@ -133,7 +133,8 @@ typedef struct {
 #define RD_STORE_F32_PRESPLIT 1 /* fp32 rows plus a bf16 (x1, x2) copy for the scan: 8 B per element */
 #define RD_STORE_SPLIT3 2       /* the exact bf16 triple x = (x1 + x2) + x3 only: 6 B per element */
 #define RD_STORE_F32_RESID 3    /* fp32 rows plus a bf16 residual plane r1 = bf16(x - c_list) for the scan
-                                   (RD_STORE=resid; every list resident): 6 B per element, scan reads 2 */
+                                   (every list resident): 6 B per element, scan reads 2 */
+#define RD_STORE_F32_RESID16 4  /* the same with an fp16 residual plane (default; RD_RES16=0 for bf16) */
 
 /* LLM-side memory reservation for the retrieval GPU (C5). Mirrors
  * ragsim::ModelProfile (domain.hpp:37-55) and the PlacementConfig weight/KV

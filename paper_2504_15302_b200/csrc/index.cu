@@ -459,7 +459,7 @@ int rd_index_info_get(const rd_index* h, rd_index_info* o) {
     o->staging_slots = h->slots;
     o->max_norm = h->xmax;
     o->device = h->device;
-    o->store = h->split3 ? RD_STORE_SPLIT3 : h->resid ? RD_STORE_F32_RESID : h->presplit ? RD_STORE_F32_PRESPLIT : RD_STORE_F32;
+    o->store = h->split3 ? RD_STORE_SPLIT3 : h->resid ? (h->res16 ? RD_STORE_F32_RESID16 : RD_STORE_F32_RESID) : h->presplit ? RD_STORE_F32_PRESPLIT : RD_STORE_F32;
   });
 }
 

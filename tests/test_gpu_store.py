@@ -8,7 +8,8 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-SPLIT3, F32, F32_PRESPLIT, RESID = 2, 0, 1, 3
+SPLIT3, F32, F32_PRESPLIT = 2, 0, 1
+RESID = 4  # the residual store with its default fp16 plane (3: bf16 plane)
 CHUNK = 64 << 20  # largest arena chunk: what a store may hold beyond its rows, per arena
 
 
