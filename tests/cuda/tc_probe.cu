@@ -321,7 +321,7 @@ extern "C" int tc_gather4(const float* hX, int R, int Ccols, int c0, const int* 
 // initial accumulator (stored to TMEM with tcgen05.st; has_c = 0 starts from the first product).
 // The test uses it to measure the accumulator's rounding error on adversarial operands.
 __global__ void __launch_bounds__(128, 1) tc_bf16_acc_kernel(const uint16_t* A, const uint16_t* B, const float* C,
-                                                             int has_c, int K, float* D) {
+                                                             int has_c, int K, float* D, int fp16) {
   extern __shared__ unsigned char dyn[];
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(dyn) + 1023) & ~uintptr_t(1023));
   unsigned char* sa = base;                       // [K/64][128 rows x 128 B]
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(128, 1) tc_bf16_acc_kernel(const uint16_t* A, 
   __syncthreads();
   tc_fence_after();
   if (tid == 0) {
-    const uint32_t id = idesc_bf16(128, 32);
+    const uint32_t id = fp16 ? idesc_f16(128, 32) : idesc_bf16(128, 32);  // fp16: the residual scan's operands
     for (int ks = 0; ks < K / 64; ++ks) {
       const uint64_t ad = umma_desc_sw128(sa + ks * 128 * 128), bd = umma_desc_sw128(sb + ks * 32 * 128);
       for (int kk = 0; kk < 4; ++kk) mma_bf16_ss(tm, ad + kk * 2, bd + kk * 2, id, (has_c | ks | kk) != 0);
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(128, 1) tc_bf16_acc_kernel(const uint16_t* A, 
   }
 }
 
-extern "C" int tc_bf16_acc(const uint16_t* hA, const uint16_t* hB, const float* hC, int has_c, int K, float* hD) {
+static int tc_acc_impl(const uint16_t* hA, const uint16_t* hB, const float* hC, int has_c, int K, float* hD, int fp16) {
   if (K % 64 != 0 || K <= 0 || K > 512) return -1;
   uint16_t *A, *B;
   float *C, *D;
@@ -402,7 +402,7 @@ extern "C" int tc_bf16_acc(const uint16_t* hA, const uint16_t* hB, const float* 
   if (has_c) cudaMemcpy(C, hC, 128 * 32 * 4, cudaMemcpyHostToDevice);
   const int smem = 1024 + (K / 64) * (128 + 32) * 128;
   cudaFuncSetAttribute(tc_bf16_acc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  tc_bf16_acc_kernel<<<1, 128, smem>>>(A, B, C, has_c, K, D);
+  tc_bf16_acc_kernel<<<1, 128, smem>>>(A, B, C, has_c, K, D, fp16);
   cudaError_t e = cudaDeviceSynchronize();
   cudaMemcpy(hD, D, 128 * 32 * 4, cudaMemcpyDeviceToHost);
   cudaFree(A);
@@ -410,4 +410,12 @@ extern "C" int tc_bf16_acc(const uint16_t* hA, const uint16_t* hB, const float* 
   cudaFree(C);
   cudaFree(D);
   return (int)e;
+}
+
+extern "C" int tc_bf16_acc(const uint16_t* hA, const uint16_t* hB, const float* hC, int has_c, int K, float* hD) {
+  return tc_acc_impl(hA, hB, hC, has_c, K, hD, 0);
+}
+// the same probe with fp16 operands (kind::f16, a/b format F16)
+extern "C" int tc_f16_acc(const uint16_t* hA, const uint16_t* hB, const float* hC, int has_c, int K, float* hD) {
+  return tc_acc_impl(hA, hB, hC, has_c, K, hD, 1);
 }

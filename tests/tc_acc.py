@@ -21,22 +21,34 @@ def bf16_val(a):
     return (bf16_bits(a).astype(np.uint32) << 16).view(np.float32)
 
 
-def run_acc(A, B, Cinit=None):
-    """D[128 x 32] = Cinit + A . B^T on the tensor core (A: 128 x K, B: 32 x K, values bf16-exact)."""
+def f16_val(a):
+    """float32 rounded to the nearest fp16 (round to nearest even), as float32."""
+    return np.ascontiguousarray(a, np.float32).astype(np.float16).astype(np.float32)
+
+
+def run_acc(A, B, Cinit=None, fp16=False):
+    """D[128 x 32] = Cinit + A . B^T on the tensor core (A: 128 x K, B: 32 x K, values bf16-exact,
+    or fp16-exact with fp16=True)."""
     global _lib
     if _lib is None:
         _lib = C.CDLL(SO)
     A = np.ascontiguousarray(A, np.float32)
     B = np.ascontiguousarray(B, np.float32)
     assert A.shape[0] == 128 and B.shape[0] == 32 and A.shape[1] == B.shape[1]
-    ab, bb = bf16_bits(A), bf16_bits(B)
-    assert np.array_equal(bf16_val(A), A) and np.array_equal(bf16_val(B), B), "operands must be bf16 values"
+    if fp16:
+        assert np.array_equal(f16_val(A), A) and np.array_equal(f16_val(B), B), "operands must be fp16 values"
+        ab, bb = A.astype(np.float16).view(np.uint16), B.astype(np.float16).view(np.uint16)
+    else:
+        ab, bb = bf16_bits(A), bf16_bits(B)
+        assert np.array_equal(bf16_val(A), A) and np.array_equal(bf16_val(B), B), "operands must be bf16 values"
     D = np.zeros((128, 32), np.float32)
     has_c = Cinit is not None
     Cm = np.ascontiguousarray(Cinit if has_c else np.zeros((128, 32)), np.float32)
     u16 = C.POINTER(C.c_uint16)
     fp = C.POINTER(C.c_float)
-    rc = _lib.tc_bf16_acc(ab.ctypes.data_as(u16), bb.ctypes.data_as(u16), Cm.ctypes.data_as(fp), int(has_c),
+    fn = _lib.tc_f16_acc if fp16 else _lib.tc_bf16_acc
+    ab, bb = np.ascontiguousarray(ab), np.ascontiguousarray(bb)
+    rc = fn(ab.ctypes.data_as(u16), bb.ctypes.data_as(u16), Cm.ctypes.data_as(fp), int(has_c),
                           A.shape[1], D.ctypes.data_as(fp))
     assert rc == 0, rc
     return D

@@ -162,3 +162,51 @@ def test_bf16x3_dot_within_certification_bound(engine, d):
         worst = max(worst, r)
         assert r <= gamma, (d, t, r / U)
     print(f"d={d}: worst |dot error| / sum|xq| = {worst / U:.1f} u (bound {gamma / U:.0f} u)")
+
+
+@pytest.mark.parametrize("K", [64, 512])
+def test_f16_accumulator_error_within_model(engine, K):
+    """The residual scan's fp16 operands on the same kind::f16 datapath: the accumulator model the
+    bounds use (10 u of each K = 16 step's magnitude) holds for fp16 inputs too (magnitudes kept in
+    fp16's normal range, so the products are exact)."""
+    from tc_acc import f16_val, run_acc
+    rng = np.random.default_rng(100 + K)
+    for t in range(6):
+        A = 2.0 ** rng.uniform(-7, 4, (128, K)) * rng.choice([-1.0, 1.0], (128, K))
+        B = 2.0 ** rng.uniform(-7, 4, (32, K))
+        if t % 2:
+            A[:, rng.integers(0, K)] = 2.0 ** 8  # one dominant product
+        A, B = f16_val(A.astype(np.float32)), f16_val(B.astype(np.float32))
+        D = run_acc(A, B, fp16=True).astype(np.float64)
+        P = A.astype(np.float64)[:, None, :] * B.astype(np.float64)[None, :, :]
+        steps = P.reshape(128, 32, K // 16, 16)
+        partial = np.cumsum(steps.sum(3), axis=2)
+        acc_before = np.concatenate([np.zeros((128, 32, 1)), partial[:, :, :-1]], axis=2)
+        model = 10 * U * (np.abs(acc_before) + np.abs(steps).sum(3)).sum(2)
+        err = np.abs(D - partial[:, :, -1])
+        assert (err <= model * 1.0001 + 1e-45).all(), (err / model).max()
+
+
+@pytest.mark.parametrize("d", [128, 512])  # (the probe's K <= 512)
+def test_fp16_residual_dot_within_certification_bound(engine, d):
+    """The fp16 residual scan's dot as it computes it — fp16(r) . fp16(q) in one fp32 accumulator —
+    against the exact r . q, on rounding-boundary operands (components just under half an fp16 ulp
+    past a representable value, aligned signs): within (2^-11 (1 + 2^-9) + 2^-11 + 16 u + 0.7 d u)
+    * sum |r_t q_t| (1 + 2^-9), the terms gamma_resid16_r / _q bound with Cauchy-Schwarz."""
+    from tc_acc import f16_val, run_acc
+    rng = np.random.default_rng(d)
+    gamma = (8192 * (1 + 2.0 ** -9) + 8192 + 16 + 0.7 * d) * U * (1 + 2.0 ** -9)
+    worst = 0.0
+    for t in range(4):
+        r = (2.0 ** rng.uniform(-6, 2, (128, d)) * rng.choice([-1, 1], (128, d))).astype(np.float32)
+        q = (2.0 ** rng.uniform(-6, 2, (32, d))).astype(np.float32)
+        if t % 2:
+            r = np.abs(r)
+            r = (f16_val(r) * (1 + 2.0 ** -11 - 2.0 ** -20)).astype(np.float32)
+            q = (f16_val(q) * (1 + 2.0 ** -11 - 2.0 ** -20)).astype(np.float32)
+        D = run_acc(f16_val(r), f16_val(q), fp16=True).astype(np.float64)
+        exact = r.astype(np.float64) @ q.T.astype(np.float64)
+        mag = np.abs(r).astype(np.float64) @ np.abs(q).T.astype(np.float64)
+        ratio = np.abs(D - exact) / (gamma * mag)
+        worst = max(worst, ratio.max())
+    assert worst <= 1.0, worst
